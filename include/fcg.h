@@ -1,0 +1,242 @@
+/*
+ * fcg.h — C ABI of the B200-native FlashSchNet MD step (libfcg.so).
+ *
+ * This is the drop-in boundary for the reference package `flashcg`
+ * (/root/reference/pkg/src/flashcg).  Every entry point below replaces one
+ * NumPy call site of the reference hot path; the reference symbol it stands
+ * in for is cited beside it as file:line.  The Python host layer
+ * (paper_2602_13140_b200/) binds these with ctypes and mirrors the
+ * reference's Python API on top of them.
+ *
+ * Conventions
+ *  - All array pointers are DEVICE pointers, caller-owned (torch tensors on
+ *    the Python side).  The library never allocates device memory; scratch
+ *    space is a caller-provided workspace sized by the *_workspace_bytes
+ *    queries.
+ *  - `stream` is a cudaStream_t passed as void*.  Every call only enqueues
+ *    work on that stream and never synchronises the host, so a sequence of
+ *    calls can be captured into a CUDA graph.
+ *  - Replicas are batched as a block-diagonal graph: bead i of replica r is
+ *    global node g = r*N + i.  Neighbour lists are one flattened CSR over
+ *    all R*N nodes, edges in canonical (replica, dst, src) order, so a
+ *    replica's slice equals the reference's canonical per-replica list
+ *    (neighbors.py:47-50) shifted by r*N.
+ *  - Return value: FCG_OK or an FCG_ERR_* code; fcg_last_error() gives the
+ *    message of the last failure on the calling thread.
+ */
+#ifndef FCG_H
+#define FCG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FCG_ABI_VERSION 1
+
+/* Compiled feature widths.  Smaller model configs are zero-padded to these,
+ * which is exact: padded filter/update channels carry ssp(0)=0 and padded
+ * weights are 0 (model.py:93-107). */
+#define FCG_D 128    /* hidden_dim and filter_hidden_dim, padded   */
+#define FCG_DR 64    /* rbf_dim, padded                            */
+#define FCG_RH 64    /* readout_hidden_dim, padded                 */
+#define FCG_MAX_BLOCKS 8
+
+enum {
+  FCG_OK = 0,
+  FCG_ERR_CAPACITY = 1, /* edge capacity too small: grow buffers, retry   */
+  FCG_ERR_ARG = 2,      /* bad argument / layout mismatch (-> ValueError) */
+  FCG_ERR_CUDA = 3      /* CUDA launch or runtime error                   */
+};
+
+/* Status words (int64 device array of FCG_STATUS_WORDS).  The host zeroes
+ * it once; OVERFLOW, MAXDEG and BLOWUP are sticky so a flag raised at any
+ * step of a captured multi-step graph survives until the host reads it. */
+#define FCG_STATUS_WORDS 8
+enum {
+  FCG_ST_EDGES = 0,       /* total edges over all replicas, last build     */
+  FCG_ST_OVERFLOW = 1,    /* sticky: an edge total exceeded cap_e          */
+  FCG_ST_MAXDEG = 2,      /* sticky max row length                         */
+  FCG_ST_BLOWUP = 3,      /* sticky: |F| > 1e6 or non-finite (md.py:183)   */
+  FCG_ST_BLOWUP_STEP = 4, /* first step index at which BLOWUP was raised   */
+  FCG_ST_EDGE_SUM = 5,    /* running sum of EDGES over builds              */
+  FCG_ST_BUILDS = 6       /* number of neighbour builds                    */
+};
+
+/* Weight formats of fcg_model.format. */
+enum {
+  FCG_FMT_FP32 = 0, /* ModelParams, fp32 (model.py:232-327)                  */
+  FCG_FMT_W16 = 1   /* QuantizedParams, fp16 weights + fp32 per-row scale
+                       (quantize.py:55-123)                                  */
+};
+
+/* One interaction block (model.py:365-370: pre_linear, filter_mlp, post_mlp).
+ * Weights are stored twice: `*_w` row-major (out, in) exactly as the
+ * reference holds them, `*_wt` transposed (in, out).  All fp32, padded.
+ * For FCG_FMT_W16 the fp32 arrays hold the dequantised weights
+ * (scale[:,None]*fp32(w16), quantize.py:51) used by the backward pass, and
+ * the `*_h` arrays hold the stored fp16 weights with `*_s` the fp32 scales. */
+typedef struct {
+  const float *pre_w, *pre_wt, *pre_b;    /* [D][D], [D][D], [D]   */
+  const float *f0_w, *f0_wt, *f0_b;       /* [D][DR], [DR][D], [D] */
+  const float *f1_w, *f1_wt, *f1_b;       /* [D][D], [D][D], [D]   */
+  const float *p0_w, *p0_wt, *p0_b;       /* [D][D], [D][D], [D]   */
+  const float *p1_w, *p1_wt, *p1_b;       /* [D][D], [D][D], [D]   */
+  /* FCG_FMT_W16 only (else NULL): fp16 stored weights (out,in) + scales   */
+  const uint16_t *pre_h, *f0_h, *f1_h, *p0_h, *p1_h;
+  const float *pre_s, *f0_s, *f1_s, *p0_s, *p1_s;
+} fcg_block;
+
+typedef struct {
+  int format;           /* FCG_FMT_*                                        */
+  int num_blocks;       /* ModelConfig.num_blocks (<= FCG_MAX_BLOCKS)       */
+  int num_types;        /* ModelConfig.num_atom_types                       */
+  float cutoff;         /* fp32(ModelConfig.cutoff) (model.py:242-246)      */
+  float gamma;          /* fp32(RbfSpec.gamma) (model.py:262-264)           */
+  const float *centers; /* [DR] fp32(RbfSpec.centers), zero-padded          */
+  const float *embedding; /* [num_types][D]                                 */
+  fcg_block blocks[FCG_MAX_BLOCKS];
+  const float *r0_w, *r0_wt, *r0_b; /* readout layer 0: [RH][D],[D][RH],[RH] */
+  const float *r1_w;                /* readout layer 1 weight row [RH]       */
+  float r1_b;                       /* readout layer 1 bias                  */
+  const uint16_t *r0_h; const float *r0_s; /* W16 only */
+  const uint16_t *r1_h; float r1_s;        /* W16 only */
+} fcg_model;
+
+/* Library identity. */
+int fcg_abi_version(void);
+const char *fcg_last_error(void);
+
+/* Built-in profiler: with profiling on, every kernel launch of the entry
+ * points below is bracketed by CUDA events on its stream (eager use only,
+ * not under graph capture).  fcg_profile_read synchronises the device and
+ * returns, per kernel class, the summed device time and launch count; names
+ * are 32-byte NUL-padded records.  Returns the number of classes written. */
+int fcg_profile_enable(int on);
+int fcg_profile_read(int max_classes, char *names, double *total_ms,
+                     int *launches);
+
+/* ---------------------------------------------------------------------
+ * (a) neighbour list + CSR
+ * Replaces build_neighbors_cells (neighbors.py:67-110) + _canonical (:47-50)
+ * + group_by_destination / group_by_source (neighbors.py:113-132) for all
+ * replicas at once.  Edge (j -> i) exists iff fp64 dist2 < r_cut*r_cut with
+ * dist2 = (dx*dx + dz*dz) + dy*dy on fp32->fp64 positions (strict <, no self
+ * edges).  Outputs:
+ *   ptr[R*N+1]  dst-CSR row pointer == reference group_by_destination.ptr
+ *               (flattened; per replica subtract ptr[r*N]); ptr_src == ptr.
+ *   nbr[cap_e]  global src node of each edge, rows sorted ascending
+ *               (== reference NeighborList.src + r*N); the dst perm is the
+ *               identity.
+ *   rev[cap_e]  id of the reverse edge; equals group_by_source.perm.
+ *   own[cap_e]  dst (row) node of each edge (== NeighborList.dst + r*N).
+ *   status[]    FCG_ST_* words.
+ * ------------------------------------------------------------------- */
+size_t fcg_nbr_workspace_bytes(int R, int N);
+int fcg_nbr_build(const float *pos, int R, int N, double r_cut, int64_t cap_e,
+                  int32_t *ptr, int32_t *nbr, int32_t *rev, int32_t *own,
+                  int64_t *status, void *ws, size_t ws_bytes, void *stream);
+
+/* Same as fcg_nbr_build for float64 positions (64-bit mode inputs). */
+int fcg_nbr_build_f64(const double *pos, int R, int N, double r_cut,
+                      int64_t cap_e, int32_t *ptr, int32_t *nbr, int32_t *rev,
+                      int32_t *own, int64_t *status, void *ws, size_t ws_bytes,
+                      void *stream);
+
+/* General stable grouping of an arbitrary edge key list (the reference's
+ * _group_by, neighbors.py:113-120): ptr[n+1] = exclusive cumsum of
+ * bincount(key), perm = argsort(key, kind="stable"). */
+size_t fcg_group_workspace_bytes(int64_t E, int n);
+int fcg_group_by(const int64_t *key, int64_t E, int n, int64_t *ptr,
+                 int64_t *perm, void *ws, size_t ws_bytes, void *stream);
+
+/* (d) CSR segment reduce, flash.py:109-135: out[s] = sum values[ptr[s]:ptr[s+1]]
+ * (rows of width k, fp32), empty segments -> 0, no atomics. */
+int fcg_segment_reduce(const float *values, int64_t E, int k,
+                       const int64_t *ptr, int nseg, float *out, void *stream);
+
+int fcg_segment_reduce_f64(const double *values, int64_t E, int k,
+                           const int64_t *ptr, int nseg, double *out,
+                           void *stream);
+
+/* ---------------------------------------------------------------------
+ * (b)(c)(d)(e) energy and forces of the SchNet model, flash.py:446-501.
+ * Consumes the CSR of fcg_nbr_build.  Outputs per_atom[R*N] (readout
+ * epsilon, flash.py:488), energy[R] (per-replica sum, flash.py:489) and
+ * forces[R*N*3] = -dE/dr (flash.py:501).  No prior term.
+ * ------------------------------------------------------------------- */
+size_t fcg_ef_workspace_bytes(const fcg_model *m, int R, int N, int64_t cap_e);
+int fcg_energy_forces(const fcg_model *m, const float *pos,
+                      const int32_t *types, int R, int N, const int32_t *ptr,
+                      const int32_t *nbr, const int32_t *rev,
+                      const int32_t *own, int64_t cap_e, float *per_atom,
+                      float *energy, float *forces, void *ws, size_t ws_bytes,
+                      void *stream);
+
+/* ---------------------------------------------------------------------
+ * (f) batched Langevin integrator, md.py:109-208.
+ * ------------------------------------------------------------------- */
+
+/* Harmonic bond prior (md.py:109-124) in node-incidence form: for bead i,
+ * bonds inc_bond[inc_ptr[i]:inc_ptr[i+1]] with sign inc_sign (+1 when i is
+ * the bond's first atom, -1 when second), ordered as np.add.at applies them
+ * (all "+", then all "-", each in bond order). */
+typedef struct {
+  int num_bonds;
+  const int32_t *bond_i, *bond_j; /* [M]                        */
+  const float *k, *r0;            /* [M] fp32(spring_k), fp32(rest_length) */
+  const int32_t *inc_ptr;         /* [N+1]                      */
+  const int32_t *inc_bond;        /* [2M]                       */
+  const int32_t *inc_sign;        /* [2M]                       */
+} fcg_prior;
+
+typedef struct {
+  float half_dt;   /* fp32(0.5 * dt_ps)                       (md.py:137,162) */
+  float c1;        /* fp32(exp(-friction*dt_ps))              (md.py:165)     */
+  float c2_num;    /* fp32((1 - c1*c1) * KB * temperature)    (md.py:166)     */
+  uint64_t seed;   /* SimConfig.seed                          (md.py:127-131) */
+  int rep_offset;  /* global index of replica 0 of this shard                 */
+  int neighbor_stride;
+} fcg_md_params;
+
+/* numpy-exact noise: out[r][k] = float32(Generator(Philox(key=[seed, rep],
+ * counter=[0,0,0,step])).standard_normal((N,3)).ravel()[k]) with
+ * rep = rep_offset + r and step = *step (device int64), md.py:127-131,167-168. */
+int fcg_normal_noise(uint64_t seed, int rep_offset, const int64_t *step,
+                     int R, int N, float *out, void *stream);
+
+/* B + A + O + A of langevin_step (md.py:150-172) with the given noise;
+ * fp32 semantics as numpy 2 (NEP 50) evaluates them. */
+int fcg_langevin_baoa(const fcg_md_params *p, const float *mass, int R,
+                      int N, const float *forces,
+                      const float *noise, float *pos, float *vel, void *stream);
+
+/* half_kick, md.py:134-138: vel += (half_dt * F) / m. */
+int fcg_half_kick(const fcg_md_params *p, const float *mass, int R, int N,
+                  const float *forces, float *vel, void *stream);
+
+/* Prior energy + forces for all replicas (md.py:109-124): e_prior[R],
+ * f_prior[R*N*3]. */
+int fcg_prior_forces(const fcg_prior *pr, const float *pos, int R, int N,
+                     float *e_prior, float *f_prior, void *stream);
+
+/* One full MD step for all replicas: noise, BAOA, neighbour rebuild,
+ * energy/forces, prior, trailing half-kick, blow-up flag, step += 1
+ * (md.py:199-207 with _ReplicaForces, md.py:231-273).  `forces` holds the
+ * forces of the current state on entry and of the new state on exit.
+ * potential[R] / prior[R] receive the info dict of the new state. */
+size_t fcg_md_workspace_bytes(const fcg_model *m, int R, int N, int64_t cap_e);
+int fcg_md_step(const fcg_model *m, const fcg_prior *pr,
+                const fcg_md_params *p, const float *mass,
+                const int32_t *types, int R, int N, double r_cut,
+                int64_t cap_e, int64_t *step, float *pos, float *vel,
+                float *forces, float *potential, float *prior,
+                int32_t *ptr, int32_t *nbr, int32_t *rev, int32_t *own,
+                int64_t *status, void *ws, size_t ws_bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FCG_H */

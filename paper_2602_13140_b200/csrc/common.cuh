@@ -1,0 +1,128 @@
+// Shared internals of libfcg.so (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string>
+
+#include "../../include/fcg.h"
+
+namespace fcg {
+
+constexpr int D = FCG_D;
+constexpr int DR = FCG_DR;
+constexpr int RH = FCG_RH;
+constexpr float FORCE_BLOWUP_LIMIT = 1.0e6f;  // md.py:30
+constexpr float TINY_DISTANCE = 1e-12f;       // reference.py:36 (compared in fp32)
+
+void set_error(const std::string &msg);
+int cuda_status(const char *where);  // FCG_OK or FCG_ERR_CUDA (sets message)
+
+inline int ceil_div(long long a, long long b) { return int((a + b - 1) / b); }
+
+// Workspace carving: bump allocator over a caller buffer, 256-byte aligned.
+struct Carver {
+  char *base;
+  size_t cap, off = 0;
+  Carver(void *b, size_t c) : base((char *)b), cap(c) {}
+  template <class T>
+  T *take(size_t n) {
+    off = (off + 255) & ~size_t(255);
+    T *p = (T *)(base ? base + off : nullptr);
+    off += n * sizeof(T);
+    return p;
+  }
+  bool ok() const { return off <= cap; }
+};
+
+// ---- device math shared by the edge and node kernels ----------------------
+
+// shifted softplus max(x,0) + log1p(exp(-|x|)) - ln2, model.py:93-100
+__device__ __forceinline__ float ssp(float x) {
+  return fmaxf(x, 0.f) + log1pf(__expf(-fabsf(x))) - 0.6931471805599453f;
+}
+// its derivative 0.5*(1+tanh(x/2)), model.py:103-107
+__device__ __forceinline__ float ssp_grad(float x) {
+  return 0.5f * (1.f + tanhf(0.5f * x));
+}
+
+// Lower bound over a nondecreasing int32 array: first idx in [0, n] with a[idx] >= v.
+__device__ __forceinline__ int lower_bound_i32(const int32_t *a, int n, long long v) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if ((long long)a[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// Rows [row_begin, row_end) of the flattened CSR owned by CTA `c` of `G`,
+// balanced by edge count.  Every row is owned by exactly one CTA, so every
+// segment sum has a single writer (no atomics anywhere).
+__device__ __forceinline__ void cta_row_range(const int32_t *ptr, int nrows, long long e_total,
+                                              int c, int G, int &rb, int &re) {
+  long long t0 = e_total * c / G, t1 = e_total * (c + 1) / G;
+  rb = (c == 0) ? 0 : lower_bound_i32(ptr, nrows + 1, t0);
+  re = (c == G - 1) ? nrows : lower_bound_i32(ptr, nrows + 1, t1);
+  if (rb > nrows) rb = nrows;
+  if (re > nrows) re = nrows;
+}
+
+}  // namespace fcg
+
+// ---- built-in kernel profiler (CUDA events per kernel class) -----------------
+namespace fcg {
+enum ProfId {
+  P_NBR_COUNT, P_NBR_SCAN, P_NBR_FILL, P_NBR_REV, P_EMBED, P_NODE_PRE, P_EDGE_FWD, P_NODE_POST,
+  P_READOUT, P_NODE_POST_BWD, P_EDGE_BWD, P_NODE_PRE_BWD, P_FORCES, P_NOISE, P_BAOA, P_PRIOR,
+  P_STEP, P_COUNT
+};
+extern bool g_prof_on;
+void prof_mark(int id, bool begin, cudaStream_t s);
+struct ProfScope {
+  int id;
+  cudaStream_t s;
+  ProfScope(int i, cudaStream_t st) : id(i), s(st) { if (g_prof_on) prof_mark(id, true, s); }
+  ~ProfScope() { if (g_prof_on) prof_mark(id, false, s); }
+};
+}  // namespace fcg
+#define FCG_PROF_CAT2(a, b) a##b
+#define FCG_PROF_CAT(a, b) FCG_PROF_CAT2(a, b)
+#define FCG_PROF(id, s) ::fcg::ProfScope FCG_PROF_CAT(_prof_, __LINE__)((id), (s))
+
+// ---- launchers implemented across the .cu files -----------------------------
+namespace fcg {
+// nbr.cu
+size_t nbr_ws_bytes(int R, int N);
+int nbr_build(const float *pos, int R, int N, double r_cut, int64_t cap_e, int32_t *ptr,
+              int32_t *nbr, int32_t *rev, int32_t *own, int64_t *status, void *ws,
+              size_t ws_bytes, cudaStream_t s);
+int nbr_build_f64(const double *pos, int R, int N, double r_cut, int64_t cap_e, int32_t *ptr,
+                  int32_t *nbr, int32_t *rev, int32_t *own, int64_t *status, void *ws,
+                  size_t ws_bytes, cudaStream_t s);
+size_t group_ws_bytes(int64_t E, int n);
+int group_by(const int64_t *key, int64_t E, int n, int64_t *ptr, int64_t *perm, void *ws,
+             size_t ws_bytes, cudaStream_t s);
+int segment_reduce(const float *values, int64_t E, int k, const int64_t *ptr, int nseg,
+                   float *out, cudaStream_t s);
+int segment_reduce_f64(const double *values, int64_t E, int k, const int64_t *ptr, int nseg,
+                       double *out, cudaStream_t s);
+// model.cu
+size_t ef_ws_bytes(const fcg_model *m, int R, int N, int64_t cap_e);
+int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, int R, int N,
+                  const int32_t *ptr, const int32_t *nbr, const int32_t *rev,
+                  const int32_t *own, int64_t cap_e, float *per_atom, float *energy,
+                  float *forces, void *ws, size_t ws_bytes, cudaStream_t s,
+                  const float *f_extra, const fcg_md_params *kick, const float *mass,
+                  float *vel, int64_t *status, const int64_t *step);
+// md.cu
+int normal_noise(uint64_t seed, int rep_offset, const int64_t *step, int R, int N, float *out,
+                 cudaStream_t s);
+int langevin_baoa(const fcg_md_params *p, const float *mass, int R, int N, const float *forces,
+                  const float *noise, float *pos, float *vel, cudaStream_t s);
+int half_kick(const fcg_md_params *p, const float *mass, int R, int N, const float *forces,
+              float *vel, cudaStream_t s);
+int prior_forces(const fcg_prior *pr, const float *pos, int R, int N, float *e_prior,
+                 float *f_prior, cudaStream_t s);
+int step_advance(int64_t *step, cudaStream_t s);
+}  // namespace fcg

@@ -1,0 +1,262 @@
+// (f) Batched Langevin integrator: numpy-exact noise stream, BAOAB halves,
+// harmonic prior.  Replaces md.py:109-208 for all replicas at once.
+//
+// Bitwise contract with the reference under numpy 2 (NEP 50):
+//  - noise: Generator(Philox(key=[seed, rep], counter=[0,0,0,step]))
+//    .standard_normal((N,3)).astype(float32) (md.py:127-131, :167-168),
+//    reproduced as Philox-4x64-10 + numpy's 256-layer ziggurat with the
+//    exact tables extracted from numpy (ziggurat_tables.h);
+//  - every Python-float coefficient is rounded to fp32 first and each
+//    operation rounds in fp32, left to right: v + ((0.5dt*F)/m), etc.  We use
+//    _rn intrinsics so nvcc cannot contract into FMAs.
+#include "common.cuh"
+#include "ziggurat_tables.h"
+
+namespace fcg {
+
+// ---- Philox-4x64-10 (Random123 / numpy) ------------------------------------
+struct U64x4 { uint64_t v[4]; };
+
+__device__ __forceinline__ U64x4 philox4x64_10(uint64_t c0, uint64_t c1, uint64_t c2,
+                                                uint64_t c3, uint64_t k0, uint64_t k1) {
+  const uint64_t M0 = 0xD2E7470EE14C6C93ull, M1 = 0xCA5A826395121157ull;
+  const uint64_t W0 = 0x9E3779B97F4A7C15ull, W1 = 0xBB67AE8584CAA73Bull;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    uint64_t hi0 = __umul64hi(M0, c0), lo0 = M0 * c0;
+    uint64_t hi1 = __umul64hi(M1, c2), lo1 = M1 * c2;
+    uint64_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+    k0 += W0; k1 += W1;
+  }
+  U64x4 o;
+  o.v[0] = c0; o.v[1] = c1; o.v[2] = c2; o.v[3] = c3;
+  return o;
+}
+
+// q-th 64-bit word of the (seed, rep, step) stream.  numpy increments the
+// 256-bit counter before every block, so block b runs on [b+1, 0, 0, step].
+__device__ __forceinline__ uint64_t stream_word(uint64_t seed, uint64_t rep, uint64_t step,
+                                                uint64_t q) {
+  U64x4 o = philox4x64_10((q >> 2) + 1, 0, 0, step, seed, rep);
+  int w = (int)(q & 3);
+  return w == 0 ? o.v[0] : w == 1 ? o.v[1] : w == 2 ? o.v[2] : o.v[3];
+}
+
+__device__ __forceinline__ double zig_w(int i) { return __longlong_as_double((long long)fcg_zig_wi_bits[i]); }
+__device__ __forceinline__ double zig_f(int i) { return __longlong_as_double((long long)fcg_zig_fi_bits[i]); }
+
+__device__ __forceinline__ double u64_to_unit(uint64_t r) {
+  return __dmul_rn((double)(r >> 11), 1.0 / 9007199254740992.0);
+}
+
+struct ZigDraw {
+  double x;
+  uint64_t rabs;
+  int idx;
+  bool fast;
+};
+__device__ __forceinline__ ZigDraw zig_decode(uint64_t r) {
+  ZigDraw z;
+  z.idx = (int)(r & 0xff);
+  r >>= 8;
+  int sign = (int)(r & 1);
+  z.rabs = (r >> 1) & 0x000fffffffffffffull;
+  z.x = __dmul_rn((double)z.rabs, zig_w(z.idx));
+  if (sign) z.x = -z.x;
+  z.fast = z.rabs < fcg_zig_ki_bits[z.idx];
+  return z;
+}
+
+// Rejection branches of numpy's random_standard_normal for a draw at stream
+// position q that failed the fast test; returns the sample and the number of
+// words consumed from q on.
+__device__ double zig_slow(uint64_t seed, uint64_t rep, uint64_t step, uint64_t q, uint64_t r0,
+                           uint64_t *consumed) {
+  const double ZR = 3.6541528853610088, ZINV = 0.27366123732975828;
+  uint64_t used = 1;
+  ZigDraw z = zig_decode(r0);
+  for (;;) {
+    if (z.fast) break;
+    if (z.idx == 0) {
+      for (;;) {
+        double u1 = u64_to_unit(stream_word(seed, rep, step, q + used)); ++used;
+        double xx = __dmul_rn(-ZINV, log1p(-u1));
+        double u2 = u64_to_unit(stream_word(seed, rep, step, q + used)); ++used;
+        double yy = -log1p(-u2);
+        if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx)) {
+          double v = __dadd_rn(ZR, xx);
+          z.x = ((z.rabs >> 8) & 1) ? -v : v;
+          *consumed = used;
+          return z.x;
+        }
+      }
+    } else {
+      double u = u64_to_unit(stream_word(seed, rep, step, q + used)); ++used;
+      double lhs = __dadd_rn(__dmul_rn(__dsub_rn(zig_f(z.idx - 1), zig_f(z.idx)), u), zig_f(z.idx));
+      if (lhs < exp(__dmul_rn(__dmul_rn(-0.5, z.x), z.x))) break;
+    }
+    z = zig_decode(stream_word(seed, rep, step, q + used)); ++used;
+  }
+  *consumed = used;
+  return z.x;
+}
+
+// One warp per replica walks its stream 32 words at a time: every lane
+// decodes the word at pos+lane assuming a sample starts there; the prefix
+// of fast lanes are consecutive samples, and the first slow lane resolves
+// its rejection loop alone before the window advances past what it used.
+__global__ void __launch_bounds__(256)
+k_normal_noise(uint64_t seed, int rep_offset, const int64_t *__restrict__ stepp, int R, int n3,
+               float *__restrict__ out) {
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= R) return;
+  uint64_t rep = (uint64_t)(rep_offset + warp), step = (uint64_t)*stepp;
+  float *dst = out + (size_t)warp * n3;
+  uint64_t pos = 0;
+  int produced = 0;
+  while (produced < n3) {
+    uint64_t q = pos + lane;
+    uint64_t r = stream_word(seed, rep, step, q);
+    ZigDraw z = zig_decode(r);
+    unsigned slow = __ballot_sync(0xffffffffu, !z.fast);
+    int L = slow ? __ffs(slow) - 1 : 32;
+    if (lane < L && produced + lane < n3) dst[produced + lane] = __double2float_rn(z.x);
+    if (L == 32) {
+      produced += 32;
+      pos += 32;
+      continue;
+    }
+    double xs = 0.0;
+    uint64_t used = 0;
+    if (lane == L) xs = zig_slow(seed, rep, step, q, r, &used);
+    xs = __shfl_sync(0xffffffffu, xs, L);
+    used = __shfl_sync(0xffffffffu, used, L);
+    if (lane == 0 && produced + L < n3) dst[produced + L] = __double2float_rn(xs);
+    produced += L + 1;
+    pos += (uint64_t)L + used;
+  }
+}
+
+int normal_noise(uint64_t seed, int rep_offset, const int64_t *step, int R, int N, float *out,
+                 cudaStream_t s) {
+  if (R < 1 || N < 1) { set_error("normal_noise: bad shape"); return FCG_ERR_ARG; }
+  FCG_PROF(P_NOISE, s);
+  k_normal_noise<<<ceil_div((long long)R * 32, 256), 256, 0, s>>>(seed, rep_offset, step, R, 3 * N,
+                                                                  out);
+  return cuda_status("normal_noise");
+}
+
+// ---- BAOAB halves ----------------------------------------------------------
+// langevin_step, md.py:158-172:
+//   v = v + ((h*F)/m); r = r + h*v; v = c1*v + sqrt(c2n/m)*xi; r = r + h*v
+__global__ void k_baoa(fcg_md_params p, const float *__restrict__ mass, int N, long long n,
+                       const float *__restrict__ F, const float *__restrict__ xi,
+                       float *__restrict__ pos, float *__restrict__ vel) {
+  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  int i = (int)((t / 3) % N);
+  float m = mass[i];
+  float v = vel[t], r = pos[t];
+  v = __fadd_rn(v, __fdiv_rn(__fmul_rn(p.half_dt, F[t]), m));
+  r = __fadd_rn(r, __fmul_rn(p.half_dt, v));
+  float c2 = __fsqrt_rn(__fdiv_rn(p.c2_num, m));
+  v = __fadd_rn(__fmul_rn(p.c1, v), __fmul_rn(c2, xi[t]));
+  r = __fadd_rn(r, __fmul_rn(p.half_dt, v));
+  vel[t] = v;
+  pos[t] = r;
+}
+
+int langevin_baoa(const fcg_md_params *p, const float *mass, int R, int N, const float *forces,
+                  const float *noise, float *pos, float *vel, cudaStream_t s) {
+  long long n = (long long)R * N * 3;
+  FCG_PROF(P_BAOA, s);
+  k_baoa<<<ceil_div(n, 256), 256, 0, s>>>(*p, mass, N, n, forces, noise, pos, vel);
+  return cuda_status("langevin_baoa");
+}
+
+// half_kick, md.py:134-138
+__global__ void k_half_kick(fcg_md_params p, const float *__restrict__ mass, int N, long long n,
+                            const float *__restrict__ F, float *__restrict__ vel) {
+  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  int i = (int)((t / 3) % N);
+  vel[t] = __fadd_rn(vel[t], __fdiv_rn(__fmul_rn(p.half_dt, F[t]), mass[i]));
+}
+
+int half_kick(const fcg_md_params *p, const float *mass, int R, int N, const float *forces,
+              float *vel, cudaStream_t s) {
+  long long n = (long long)R * N * 3;
+  k_half_kick<<<ceil_div(n, 256), 256, 0, s>>>(*p, mass, N, n, forces, vel);
+  return cuda_status("half_kick");
+}
+
+// ---- harmonic prior, md.py:109-124 -----------------------------------------
+struct BondVec { float fx, fy, fz, e; };
+__device__ __forceinline__ BondVec bond_eval(const fcg_prior &pr, const float *P, int b) {
+  int i = pr.bond_i[b], j = pr.bond_j[b];
+  float x = __fsub_rn(P[3 * i], P[3 * j]), y = __fsub_rn(P[3 * i + 1], P[3 * j + 1]),
+        z = __fsub_rn(P[3 * i + 2], P[3 * j + 2]);
+  float d = __fsqrt_rn(__fadd_rn(__fadd_rn(__fmul_rn(x, x), __fmul_rn(y, y)), __fmul_rn(z, z)));
+  float k = pr.k[b];
+  float st = __fsub_rn(d, pr.r0[b]);
+  float safe = d > 0.f ? d : 1.f;
+  float coef = __fdiv_rn(__fmul_rn(-k, st), safe);
+  BondVec o;
+  o.fx = __fmul_rn(coef, x);
+  o.fy = __fmul_rn(coef, y);
+  o.fz = __fmul_rn(coef, z);
+  o.e = __fmul_rn(__fmul_rn(k, st), st);
+  return o;
+}
+
+// One CTA per replica: each bead applies its incident bonds in np.add.at
+// order (all "+fvec" for bonds where it is atom i, then "-fvec" where it is
+// atom j), so the per-bead sums are bitwise the reference's.
+__global__ void __launch_bounds__(256)
+k_prior(const fcg_prior pr, const float *__restrict__ pos, int N, float *__restrict__ e_prior,
+        float *__restrict__ f_prior) {
+  const int r = blockIdx.x;
+  const float *P = pos + (size_t)r * N * 3;
+  __shared__ float red[256];
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    float fx = 0.f, fy = 0.f, fz = 0.f;
+    if (pr.num_bonds > 0) {
+      for (int q = pr.inc_ptr[i]; q < pr.inc_ptr[i + 1]; ++q) {
+        BondVec v = bond_eval(pr, P, pr.inc_bond[q]);
+        if (pr.inc_sign[q] > 0) {
+          fx = __fadd_rn(fx, v.fx); fy = __fadd_rn(fy, v.fy); fz = __fadd_rn(fz, v.fz);
+        } else {
+          fx = __fadd_rn(fx, -v.fx); fy = __fadd_rn(fy, -v.fy); fz = __fadd_rn(fz, -v.fz);
+        }
+      }
+    }
+    float *f = f_prior + ((size_t)r * N + i) * 3;
+    f[0] = fx; f[1] = fy; f[2] = fz;
+  }
+  float acc = 0.f;
+  for (int b = threadIdx.x; b < pr.num_bonds; b += blockDim.x) acc += bond_eval(pr, P, b).e;
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) e_prior[r] = 0.5f * red[0];
+}
+
+int prior_forces(const fcg_prior *pr, const float *pos, int R, int N, float *e_prior,
+                 float *f_prior, cudaStream_t s) {
+  FCG_PROF(P_PRIOR, s);
+  k_prior<<<R, 256, 0, s>>>(*pr, pos, N, e_prior, f_prior);
+  return cuda_status("prior_forces");
+}
+
+__global__ void k_step_advance(int64_t *step) { *step += 1; }
+int step_advance(int64_t *step, cudaStream_t s) {
+  FCG_PROF(P_STEP, s);
+  k_step_advance<<<1, 1, 0, s>>>(step);
+  return cuda_status("step_advance");
+}
+
+}  // namespace fcg

@@ -1,0 +1,294 @@
+// (a) Neighbour list + CSR build, all replicas in one pass.
+//
+// Replaces build_neighbors_cells / _canonical / group_by_* of the reference
+// (neighbors.py:47-132).  Instead of a cell grid + lexsort + stable argsort,
+// every (replica, dst row) is scanned by one warp over src beads in
+// ascending order, so each row's src list comes out sorted and the
+// flattened edge array is already in canonical (replica, dst, src) order:
+// the dst permutation is the identity and ptr_src == ptr_dst because the
+// fp64 predicate is symmetric (neighbors.py:113-132 reduce to a rank lookup,
+// kernel k_rev).
+//
+// Predicate: reference computes dist2 with np.einsum("ijk,ijk->ij") on fp64
+// differences (neighbors.py:96-98), which numpy evaluates as
+// (dx*dx + dz*dz) + dy*dy with separate roundings (pinned in
+// tests/test_oracle_golden.py against the reference).  We reproduce it with
+// explicit _rn intrinsics so nvcc cannot contract to DFMA.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace fcg {
+
+constexpr int NBR_TILE = 1024;  // beads staged per SMEM tile (as fp64)
+constexpr int NBR_WARPS = 8;
+constexpr int NBR_ROWS_PER_WARP = 4;
+constexpr int NBR_ROWS_PER_CTA = NBR_WARPS * NBR_ROWS_PER_WARP;
+
+__device__ __forceinline__ bool within_cutoff(double xi, double yi, double zi, double xj,
+                                              double yj, double zj, double rc2) {
+  double dx = __dsub_rn(xi, xj), dy = __dsub_rn(yi, yj), dz = __dsub_rn(zi, zj);
+  double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dz, dz)), __dmul_rn(dy, dy));
+  return d2 < rc2;
+}
+
+// kFill=false: count row lengths into cnt[]; kFill=true: write nbr/own at ptr[row].
+template <typename T, bool kFill>
+__global__ void __launch_bounds__(NBR_WARPS * 32)
+k_scan_rows(const T *__restrict__ pos, int N, double rc2, int32_t *__restrict__ cnt,
+            const int32_t *__restrict__ ptr, int64_t cap_e, int32_t *__restrict__ nbr,
+            int32_t *__restrict__ own, int64_t *__restrict__ status) {
+  __shared__ double sx[NBR_TILE], sy[NBR_TILE], sz[NBR_TILE];
+  const int r = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const T *P = pos + (size_t)r * N * 3;
+  const int row0 = blockIdx.x * NBR_ROWS_PER_CTA + warp * NBR_ROWS_PER_WARP;
+
+  double xi[NBR_ROWS_PER_WARP], yi[NBR_ROWS_PER_WARP], zi[NBR_ROWS_PER_WARP];
+  int base[NBR_ROWS_PER_WARP];
+  bool write_ok[NBR_ROWS_PER_WARP];
+#pragma unroll
+  for (int q = 0; q < NBR_ROWS_PER_WARP; ++q) {
+    int i = min(row0 + q, N - 1);
+    xi[q] = (double)P[3 * i];
+    yi[q] = (double)P[3 * i + 1];
+    zi[q] = (double)P[3 * i + 2];
+    base[q] = 0;
+    write_ok[q] = true;
+    if (kFill && row0 + q < N) {
+      long long g = (long long)r * N + row0 + q;
+      base[q] = ptr[g];
+      write_ok[q] = (long long)ptr[g + 1] <= cap_e;
+    }
+  }
+
+  for (int t0 = 0; t0 < N; t0 += NBR_TILE) {
+    int tn = min(NBR_TILE, N - t0);
+    __syncthreads();
+    for (int k = threadIdx.x; k < tn; k += blockDim.x) {
+      sx[k] = (double)P[3 * (t0 + k)];
+      sy[k] = (double)P[3 * (t0 + k) + 1];
+      sz[k] = (double)P[3 * (t0 + k) + 2];
+    }
+    __syncthreads();
+    for (int c0 = 0; c0 < tn; c0 += 32) {
+      int jl = c0 + lane;
+      int j = t0 + jl;
+      double xj = 0, yj = 0, zj = 0;
+      if (jl < tn) { xj = sx[jl]; yj = sy[jl]; zj = sz[jl]; }
+#pragma unroll
+      for (int q = 0; q < NBR_ROWS_PER_WARP; ++q) {
+        int i = row0 + q;
+        bool e = (jl < tn) && (j != i) && (i < N) &&
+                 within_cutoff(xi[q], yi[q], zi[q], xj, yj, zj, rc2);
+        unsigned m = __ballot_sync(0xffffffffu, e);
+        if (kFill) {
+          if (e && write_ok[q]) {
+            int slot = base[q] + __popc(m & ((1u << lane) - 1u));
+            nbr[slot] = r * N + j;
+            own[slot] = r * N + i;
+          }
+        }
+        base[q] += __popc(m);
+      }
+    }
+  }
+  if (!kFill && lane == 0) {
+    int mx = 0;
+#pragma unroll
+    for (int q = 0; q < NBR_ROWS_PER_WARP; ++q) {
+      if (row0 + q < N) {
+        cnt[(size_t)r * N + row0 + q] = base[q];
+        mx = max(mx, base[q]);
+      }
+    }
+    atomicMax((unsigned long long *)&status[FCG_ST_MAXDEG], (unsigned long long)mx);
+  }
+}
+
+__global__ void k_finalize(const int32_t *__restrict__ ptr, int nrows, int64_t cap_e,
+                           int64_t *__restrict__ status) {
+  if (threadIdx.x == 0) {
+    long long e = ptr[nrows];
+    status[FCG_ST_EDGES] = e;
+    if (e > cap_e) status[FCG_ST_OVERFLOW] = 1;
+    status[FCG_ST_EDGE_SUM] += e;
+    status[FCG_ST_BUILDS] += 1;
+  }
+}
+
+// rev[k] for slot k of row i (edge j -> i) = slot of edge i -> j in row j,
+// i.e. the reference's group_by_source perm (neighbors.py:129-132).
+__global__ void __launch_bounds__(256)
+k_rev(const int32_t *__restrict__ ptr, const int32_t *__restrict__ nbr, int nrows,
+      int64_t cap_e, int32_t *__restrict__ rev) {
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= nrows) return;
+  if ((long long)ptr[nrows] > cap_e) return;  // overflow: CSR invalid
+  int i = warp;
+  int b = ptr[i], e = ptr[i + 1];
+  for (int k = b + lane; k < e; k += 32) {
+    int j = nbr[k];
+    int lo = ptr[j], hi = ptr[j + 1];
+    while (lo < hi) {
+      int mid = (lo + hi) >> 1;
+      if (nbr[mid] < i) lo = mid + 1; else hi = mid;
+    }
+    rev[k] = lo;
+  }
+}
+
+size_t nbr_ws_bytes(int R, int N) {
+  size_t n = (size_t)R * N + 1;
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, (int32_t *)nullptr, (int32_t *)nullptr, (int)n);
+  Carver c(nullptr, 0);
+  c.take<int32_t>(n);
+  c.take<char>(tmp);
+  return c.off + 256;
+}
+
+template <typename T>
+int nbr_build_t(const T *pos, int R, int N, double r_cut, int64_t cap_e, int32_t *ptr,
+                int32_t *nbr, int32_t *rev, int32_t *own, int64_t *status, void *ws,
+                size_t ws_bytes, cudaStream_t s) {
+  if (R < 1 || N < 1) { set_error("nbr_build: need R >= 1 and N >= 1"); return FCG_ERR_ARG; }
+  if ((long long)R * N >= (1ll << 31)) { set_error("nbr_build: R*N too large"); return FCG_ERR_ARG; }
+  size_t n = (size_t)R * N + 1;
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, (int32_t *)nullptr, (int32_t *)nullptr, (int)n);
+  Carver c(ws, ws_bytes);
+  int32_t *cnt = c.take<int32_t>(n);
+  void *cub_tmp = c.take<char>(tmp);
+  if (!c.ok()) { set_error("nbr_build: workspace too small"); return FCG_ERR_ARG; }
+  double rc2 = r_cut * r_cut;  // Python float product, neighbors.py:89
+
+  dim3 grid(ceil_div(N, NBR_ROWS_PER_CTA), R);
+  cudaMemsetAsync(cnt + (n - 1), 0, sizeof(int32_t), s);
+  {
+    FCG_PROF(P_NBR_COUNT, s);
+    k_scan_rows<T, false><<<grid, NBR_WARPS * 32, 0, s>>>(pos, N, rc2, cnt, nullptr, cap_e,
+                                                          nullptr, nullptr, status);
+  }
+  {
+    FCG_PROF(P_NBR_SCAN, s);
+    cub::DeviceScan::ExclusiveSum(cub_tmp, tmp, cnt, ptr, (int)n, s);
+    k_finalize<<<1, 32, 0, s>>>(ptr, (int)(n - 1), cap_e, status);
+  }
+  {
+    FCG_PROF(P_NBR_FILL, s);
+    k_scan_rows<T, true><<<grid, NBR_WARPS * 32, 0, s>>>(pos, N, rc2, nullptr, ptr, cap_e, nbr,
+                                                         own, status);
+  }
+  {
+    FCG_PROF(P_NBR_REV, s);
+    k_rev<<<ceil_div((long long)(n - 1) * 32, 256), 256, 0, s>>>(ptr, nbr, (int)(n - 1), cap_e,
+                                                                 rev);
+  }
+  return cuda_status("nbr_build");
+}
+
+int nbr_build(const float *pos, int R, int N, double r_cut, int64_t cap_e, int32_t *ptr,
+              int32_t *nbr, int32_t *rev, int32_t *own, int64_t *status, void *ws,
+              size_t ws_bytes, cudaStream_t s) {
+  return nbr_build_t(pos, R, N, r_cut, cap_e, ptr, nbr, rev, own, status, ws, ws_bytes, s);
+}
+int nbr_build_f64(const double *pos, int R, int N, double r_cut, int64_t cap_e, int32_t *ptr,
+                  int32_t *nbr, int32_t *rev, int32_t *own, int64_t *status, void *ws,
+                  size_t ws_bytes, cudaStream_t s) {
+  return nbr_build_t(pos, R, N, r_cut, cap_e, ptr, nbr, rev, own, status, ws, ws_bytes, s);
+}
+
+// ---------------------------------------------------------------------------
+// General stable grouping (neighbors.py:113-120) for arbitrary key lists.
+__global__ void k_iota64(int64_t *v, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    v[i] = i;
+}
+__global__ void k_ptr_from_sorted(const int64_t *__restrict__ keys, int64_t E, int n,
+                                  int64_t *__restrict__ ptr) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s <= n;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = E;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (keys[mid] < s) lo = mid + 1; else hi = mid;
+    }
+    ptr[s] = lo;
+  }
+}
+
+static int end_bit_for(int n) {
+  int b = 1;
+  while ((1ll << b) < (long long)n) ++b;
+  return b;
+}
+
+size_t group_ws_bytes(int64_t E, int n) {
+  size_t tmp = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp, (const int64_t *)nullptr, (int64_t *)nullptr,
+                                  (const int64_t *)nullptr, (int64_t *)nullptr,
+                                  (int64_t)(E > 0 ? E : 1), 0, end_bit_for(n));
+  Carver c(nullptr, 0);
+  c.take<int64_t>(E + 1);
+  c.take<int64_t>(E + 1);
+  c.take<char>(tmp);
+  return c.off + 256;
+}
+
+int group_by(const int64_t *key, int64_t E, int n, int64_t *ptr, int64_t *perm, void *ws,
+             size_t ws_bytes, cudaStream_t s) {
+  if (n < 0 || E < 0) { set_error("group_by: negative size"); return FCG_ERR_ARG; }
+  size_t tmp = 0;
+  int eb = end_bit_for(n);
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp, (const int64_t *)nullptr, (int64_t *)nullptr,
+                                  (const int64_t *)nullptr, (int64_t *)nullptr,
+                                  (int64_t)(E > 0 ? E : 1), 0, eb);
+  Carver c(ws, ws_bytes);
+  int64_t *sorted = c.take<int64_t>(E + 1);
+  int64_t *iota = c.take<int64_t>(E + 1);
+  void *cub_tmp = c.take<char>(tmp);
+  if (!c.ok()) { set_error("group_by: workspace too small"); return FCG_ERR_ARG; }
+  if (E > 0) {
+    k_iota64<<<ceil_div(E, 256) > 4096 ? 4096 : ceil_div(E, 256), 256, 0, s>>>(iota, E);
+    // LSD radix sort is stable: equal keys keep ascending edge order.
+    cub::DeviceRadixSort::SortPairs(cub_tmp, tmp, key, sorted, iota, perm, E, 0, eb, s);
+  }
+  k_ptr_from_sorted<<<ceil_div(n + 1, 256), 256, 0, s>>>(sorted, E, n, ptr);
+  return cuda_status("group_by");
+}
+
+// ---------------------------------------------------------------------------
+// (d) segment reduce, flash.py:109-135.  One thread per (segment, column),
+// summing its segment in order; a single writer per output element.
+template <typename T>
+__global__ void k_segment_reduce(const T *__restrict__ v, int k, const int64_t *__restrict__ ptr,
+                                 int nseg, T *__restrict__ out) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)nseg * k) return;
+  int sgm = (int)(t / k), col = (int)(t % k);
+  T acc = 0;
+  for (int64_t e = ptr[sgm]; e < ptr[sgm + 1]; ++e) acc += v[e * k + col];
+  out[(int64_t)sgm * k + col] = acc;
+}
+
+template <typename T>
+int segment_reduce_t(const T *values, int64_t E, int k, const int64_t *ptr, int nseg, T *out,
+                     cudaStream_t s) {
+  if (k < 1 || nseg < 0) { set_error("segment_reduce: bad shape"); return FCG_ERR_ARG; }
+  if (nseg == 0) return FCG_OK;
+  long long tot = (long long)nseg * k;
+  k_segment_reduce<<<ceil_div(tot, 256), 256, 0, s>>>(values, k, ptr, nseg, out);
+  return cuda_status("segment_reduce");
+}
+int segment_reduce(const float *values, int64_t E, int k, const int64_t *ptr, int nseg,
+                   float *out, cudaStream_t s) {
+  return segment_reduce_t(values, E, k, ptr, nseg, out, s);
+}
+int segment_reduce_f64(const double *values, int64_t E, int k, const int64_t *ptr, int nseg,
+                       double *out, cudaStream_t s) {
+  return segment_reduce_t(values, E, k, ptr, nseg, out, s);
+}
+
+}  // namespace fcg

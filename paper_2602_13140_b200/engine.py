@@ -1,0 +1,216 @@
+"""Device-resident batched MD engine over libfcg.so.
+
+One engine holds R replicas of one system on one GPU: parameters uploaded
+once, state (positions, velocities, forces, step counter, status words),
+the flattened CSR buffers, and one workspace.  A step is a single
+fcg_md_step call (noise -> BAOA -> neighbour rebuild -> prior -> energy and
+forces -> trailing half-kick), so K steps can be captured into one CUDA
+graph and replayed with no host involvement; the host only reads state at
+output strides.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import numpy as np
+
+from . import _lib
+from .modelparams import DeviceModel
+from .prior import DevicePrior
+
+KB = 0.00831446261815324  # kJ/(mol K), md.py:29
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2602_13140_b200 requires a CUDA device (no CPU fallback)")
+    return torch
+
+
+def md_params(dt_fs: float, temperature: float, friction: float, seed: int,
+              rep_offset: int = 0, neighbor_stride: int = 1) -> _lib.FcgMdParams:
+    """Coefficients as numpy 2 evaluates them in fp32 mode (md.py:158-169):
+    Python-float expressions are computed in double, then rounded to fp32."""
+    dt = dt_fs * 1.0e-3
+    c1 = math.exp(-friction * dt)
+    p = _lib.FcgMdParams()
+    p.half_dt = float(np.float32(0.5 * dt))
+    p.c1 = float(np.float32(c1))
+    p.c2_num = float(np.float32((1.0 - c1 * c1) * KB * temperature))
+    p.seed = int(seed)
+    p.rep_offset = int(rep_offset)
+    p.neighbor_stride = int(max(neighbor_stride, 1))
+    return p
+
+
+class CsrBuffers:
+    """Flattened CSR over R*N nodes (see include/fcg.h)."""
+
+    def __init__(self, R: int, N: int, cap_e: int, device):
+        torch = _torch()
+        self.R, self.N, self.cap_e = R, N, int(cap_e)
+        self.ptr = torch.zeros(R * N + 1, dtype=torch.int32, device=device)
+        self.nbr = torch.zeros(self.cap_e + 1, dtype=torch.int32, device=device)
+        self.rev = torch.zeros(self.cap_e + 1, dtype=torch.int32, device=device)
+        self.own = torch.zeros(self.cap_e + 1, dtype=torch.int32, device=device)
+
+    def slice_replica(self, r: int):
+        """Reference-layout (src, dst, ptr, perm_src) of replica r as int64 numpy."""
+        ptr = self.ptr.cpu().numpy().astype(np.int64)
+        N = self.N
+        lo, hi = ptr[r * N], ptr[(r + 1) * N]
+        src = self.nbr[lo:hi].cpu().numpy().astype(np.int64) - r * N
+        dst = self.own[lo:hi].cpu().numpy().astype(np.int64) - r * N
+        rev = self.rev[lo:hi].cpu().numpy().astype(np.int64) - lo
+        return src, dst, ptr[r * N:(r + 1) * N + 1] - lo, rev
+
+
+def default_capacity(R: int, N: int) -> int:
+    dense = R * N * (N - 1)
+    return int(max(1, min(dense, R * N * 96)))
+
+
+class MDEngine:
+    def __init__(self, params, types, masses, prior, n_replicas: int, dt_fs=4.0,
+                 temperature=300.0, friction=1.0, seed=0, neighbor_stride=1, rep_offset=0,
+                 cap_e: int | None = None, device="cuda"):
+        torch = _torch()
+        self.torch = torch
+        self.lib = _lib.load()
+        self.device = torch.device(device)
+        types = np.asarray(types)
+        N = int(types.size)
+        R = int(n_replicas)
+        if np.any(types < 0) or np.any(types >= params.config.num_atom_types):
+            raise ValueError("atom type out of range for the embedding table")
+        self.R, self.N = R, N
+        self.r_cut = float(params.config.cutoff)
+        self.model = DeviceModel(params, self.device)
+        self.prior = DevicePrior(prior, N, self.device)
+        self.p = md_params(dt_fs, temperature, friction, seed, rep_offset, neighbor_stride)
+        self.mass = torch.as_tensor(np.asarray(masses, np.float64).astype(np.float32),
+                                    device=self.device)
+        self.masses64 = np.asarray(masses, np.float64)
+        self.types = torch.as_tensor(types.astype(np.int32), device=self.device)
+        f32 = dict(dtype=torch.float32, device=self.device)
+        self.pos = torch.zeros(R, N, 3, **f32)
+        self.vel = torch.zeros(R, N, 3, **f32)
+        self.forces = torch.zeros(R, N, 3, **f32)
+        self.potential = torch.zeros(R, **f32)
+        self.prior_e = torch.zeros(R, **f32)
+        self.step = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self.status = torch.zeros(_lib.FCG_STATUS_WORDS, dtype=torch.int64, device=self.device)
+        self._alloc(cap_e or default_capacity(R, N))
+        self._graphs = {}
+
+    # -- buffers ---------------------------------------------------------
+    def _alloc(self, cap_e: int):
+        torch = self.torch
+        self.csr = CsrBuffers(self.R, self.N, cap_e, self.device)
+        nbytes = self.lib.fcg_md_workspace_bytes(C.byref(self.model.desc), self.R, self.N,
+                                                 self.csr.cap_e)
+        self.ws = torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
+        self._graphs = {}
+
+    @property
+    def cap_e(self) -> int:
+        return self.csr.cap_e
+
+    def stream(self):
+        return C.c_void_p(self.torch.cuda.current_stream(self.device).cuda_stream)
+
+    # -- state -----------------------------------------------------------
+    def load_state(self, positions, velocities, step: int):
+        self.pos.copy_(self.torch.as_tensor(np.asarray(positions, np.float32)))
+        self.vel.copy_(self.torch.as_tensor(np.asarray(velocities, np.float32)))
+        self.step.fill_(int(step))
+
+    def read_state(self):
+        return (self.pos.cpu().numpy(), self.vel.cpu().numpy(), int(self.step.item()))
+
+    # -- kernels ---------------------------------------------------------
+    def _md_step(self):
+        L, c, v = self.lib, self.csr, _lib.vp
+        rc = L.fcg_md_step(C.byref(self.model.desc), C.byref(self.prior.desc), C.byref(self.p),
+                           v(self.mass), v(self.types), self.R, self.N, self.r_cut, c.cap_e,
+                           v(self.step), v(self.pos), v(self.vel), v(self.forces),
+                           v(self.potential), v(self.prior_e), v(c.ptr), v(c.nbr), v(c.rev),
+                           v(c.own), v(self.status), v(self.ws), self.ws.numel(), self.stream())
+        _lib.check(rc, "fcg_md_step")
+
+    def evaluate(self):
+        """Forces of the current positions (the integrate() pre-loop force
+        evaluation, md.py:195): neighbour build + prior + model, no kick."""
+        L, c, v = self.lib, self.csr, _lib.vp
+        torch = self.torch
+        while True:
+            nb = L.fcg_nbr_workspace_bytes(self.R, self.N)
+            ws_nb = torch.empty(int(nb), dtype=torch.uint8, device=self.device)
+            _lib.check(L.fcg_nbr_build(v(self.pos), self.R, self.N, self.r_cut, c.cap_e, v(c.ptr),
+                                       v(c.nbr), v(c.rev), v(c.own), v(self.status), v(ws_nb),
+                                       nb, self.stream()), "fcg_nbr_build")
+            e_tot = int(c.ptr[-1].item())
+            if e_tot <= c.cap_e:
+                break
+            self.status[_lib.ST_OVERFLOW] = 0
+            self._alloc(int(e_tot * 1.5) + 1024)
+        f_prior = torch.zeros(self.R, self.N, 3, dtype=torch.float32, device=self.device)
+        _lib.check(L.fcg_prior_forces(C.byref(self.prior.desc), v(self.pos), self.R, self.N,
+                                      v(self.prior_e), v(f_prior), self.stream()),
+                   "fcg_prior_forces")
+        per_atom = torch.empty(self.R * self.N, dtype=torch.float32, device=self.device)
+        ef = L.fcg_ef_workspace_bytes(C.byref(self.model.desc), self.R, self.N, c.cap_e)
+        ws_ef = torch.empty(int(ef), dtype=torch.uint8, device=self.device)
+        _lib.check(L.fcg_energy_forces(C.byref(self.model.desc), v(self.pos), v(self.types),
+                                       self.R, self.N, v(c.ptr), v(c.nbr), v(c.rev), v(c.own),
+                                       c.cap_e, v(per_atom), v(self.potential), v(self.forces),
+                                       v(ws_ef), ef, self.stream()), "fcg_energy_forces")
+        self.forces.add_(f_prior)  # out.forces + f_prior, md.py:266
+        self.per_atom = per_atom
+
+    def run(self, n_steps: int, graph_steps: int = 0):
+        """Advance n_steps.  With graph_steps > 0, steps run as replays of a
+        captured CUDA graph of graph_steps fcg_md_step calls."""
+        if graph_steps <= 0:
+            for _ in range(n_steps):
+                self._md_step()
+            return
+        full, rem = divmod(n_steps, graph_steps)
+        if full:
+            g = self._graph(graph_steps)
+            for _ in range(full):
+                g.replay()
+        for _ in range(rem):
+            self._md_step()
+
+    def _graph(self, k: int):
+        g = self._graphs.get(k)
+        if g is None:
+            torch = self.torch
+            # warm the launch path (first-call attribute setup) outside capture
+            s = torch.cuda.Stream(self.device)
+            g = torch.cuda.CUDAGraph()
+            saved = [t.clone() for t in (self.pos, self.vel, self.forces, self.step, self.status)]
+            with torch.cuda.graph(g, stream=s):
+                for _ in range(k):
+                    self._md_step()
+            # capture does not execute; restore is a no-op safeguard
+            for t, s0 in zip((self.pos, self.vel, self.forces, self.step, self.status), saved):
+                t.copy_(s0)
+            self._graphs[k] = g
+        return g
+
+    # -- flags -----------------------------------------------------------
+    def flags(self):
+        st = self.status.cpu().numpy()
+        return {"edges": int(st[_lib.ST_EDGES]), "overflow": bool(st[_lib.ST_OVERFLOW]),
+                "max_degree": int(st[_lib.ST_MAXDEG]), "blowup": bool(st[_lib.ST_BLOWUP]),
+                "blowup_step": int(st[_lib.ST_BLOWUP_STEP]),
+                "edge_sum": int(st[_lib.ST_EDGE_SUM]), "builds": int(st[_lib.ST_BUILDS])}
+
+    def clear_flags(self):
+        self.status.zero_()

@@ -1,0 +1,361 @@
+"""Langevin MD over batched replicas on the GPU — the reference's md.py API
+(SimConfig, SimState, integrate, run_simulation, the force-provider
+protocol) with every per-step operation in libfcg.so.
+
+Drop-in points (reference md.py):
+  * GpuReplicaForces   replaces _ReplicaForces (md.py:231-273): a callable
+                       force_fn(positions[R,N,3], step) -> (forces, info)
+                       usable by the reference's own integrate();
+  * integrate          md.py:188-208, device-resident when force_fn is a
+                       GpuReplicaForces, else GPU integrator + host forces;
+  * run_simulation     md.py:276-349, device-resident with host I/O only at
+                       output strides; same trajectory.xyz / scalars.csv
+                       formats.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import time
+from dataclasses import dataclass, field
+from pathlib import Path
+
+import numpy as np
+
+from . import _lib
+from .engine import KB, MDEngine, md_params
+from .schnet import PipelineMode, TrafficReport, io_model_flash_report
+from .prior import PriorSpec, DevicePrior  # noqa: F401  (re-export, md.py:90)
+
+FORCE_BLOWUP_LIMIT = 1.0e6
+SCALARS_SCHEMA = "step,replica,potential,prior,kinetic_T,wall_ms"
+NONDETERMINISTIC_COLUMNS = ("wall_ms",)
+
+
+class SimulationBlowupError(RuntimeError):
+    """Non-finite or absurd forces (md.py:37)."""
+
+
+@dataclass
+class SimState:
+    positions: np.ndarray
+    velocities: np.ndarray
+    masses: np.ndarray
+    step: int = 0
+
+    @property
+    def n_replicas(self) -> int:
+        return int(self.positions.shape[0])
+
+    @property
+    def n_beads(self) -> int:
+        return int(self.positions.shape[1])
+
+
+@dataclass(frozen=True)
+class SimConfig:
+    dt_fs: float = 4.0
+    temperature: float = 300.0
+    friction: float = 1.0
+    n_steps: int = 100
+    n_replicas: int = 1
+    seed: int = 0
+    neighbor_stride: int = 1
+    output_stride: int = 10
+    mode: str = "32bit"
+    backend: PipelineMode = field(default_factory=PipelineMode)
+    workers: int = 1
+    checkpoint_path: str | None = None
+    checkpoint_step: int | None = None
+
+    def __post_init__(self):
+        if not self.dt_fs > 0:
+            raise ValueError("dt must be positive")
+        if self.temperature < 0 or self.friction < 0:
+            raise ValueError("temperature and friction must be nonnegative")
+        if self.mode not in ("32bit", "64bit"):
+            raise ValueError(f"unknown mode {self.mode!r}")
+
+    @property
+    def dtype(self):
+        return np.float64 if self.mode == "64bit" else np.float32
+
+    @property
+    def dt_ps(self) -> float:
+        return self.dt_fs * 1.0e-3
+
+
+def _require_fp32(config: SimConfig):
+    if config.mode != "32bit":
+        raise ValueError("the B200 path integrates in fp32 (mode='32bit'); "
+                         "64-bit mode is served by the CPU reference only")
+
+
+def make_step_rng(seed: int, replica: int, step: int) -> np.random.Generator:
+    """Host copy of the counter-based stream the GPU reproduces bitwise
+    (md.py:127-131); kept for API parity and debugging."""
+    bg = np.random.Philox(key=np.array([seed, replica], dtype=np.uint64),
+                          counter=np.array([0, 0, 0, step], dtype=np.uint64))
+    return np.random.Generator(bg)
+
+
+def kinetic_temperature(state: SimState) -> np.ndarray:
+    """Per-replica 2 KE / (3 N kB), evaluated as md.py:175-180 does."""
+    m = state.masses[None, :, None]
+    ke = 0.5 * np.sum(m * state.velocities ** 2, axis=(1, 2))
+    return 2.0 * ke / (3 * state.n_beads * KB)
+
+
+def _check_forces(forces: np.ndarray):
+    if not np.all(np.isfinite(forces)) or np.any(np.abs(forces) > FORCE_BLOWUP_LIMIT):
+        raise SimulationBlowupError("non-finite or runaway forces")
+
+
+class GpuReplicaForces:
+    """Batched model + prior force provider (replaces md.py:231-273).
+
+    force_fn(positions[R,N,3], step) -> (forces[R,N,3] fp32,
+    {"potential": [R], "prior": [R]}): one neighbour rebuild + one fused
+    energy/force evaluation for all replicas per call.
+    """
+
+    def __init__(self, params, types, prior, config: SimConfig, device="cuda"):
+        self.params, self.types, self.prior, self.config = params, np.asarray(types), prior, config
+        self.device = device
+        self.engine = None
+        self.edge_counts = []
+        self.traffic = TrafficReport()
+        self._cached_step = None
+
+    def _engine_for(self, R: int) -> MDEngine:
+        if self.engine is None or self.engine.R != R:
+            c = self.config
+            self.engine = MDEngine(self.params, self.types, np.full(self.types.size, 1.0),
+                                   self.prior, R, c.dt_fs, c.temperature, c.friction, c.seed,
+                                   c.neighbor_stride, device=self.device)
+        return self.engine
+
+    def __call__(self, positions, step):
+        positions = np.asarray(positions)
+        R = positions.shape[0]
+        eng = self._engine_for(R)
+        eng.pos.copy_(eng.torch.as_tensor(positions.astype(np.float32)))
+        eng.evaluate()
+        forces = eng.forces.cpu().numpy()
+        info = {"potential": eng.potential.cpu().numpy().astype(np.float64),
+                "prior": eng.prior_e.cpu().numpy().astype(np.float64)}
+        ptr = eng.csr.ptr.cpu().numpy()
+        N = eng.N
+        counts = ptr[N::N] - ptr[0:-1:N][:R]
+        self.edge_counts.extend(int(x) for x in counts)
+        for e in counts:
+            self.traffic.merge(io_model_flash_report(N, int(e), self.params))
+        return forces.astype(positions.dtype, copy=False), info
+
+
+def integrate(force_fn, state: SimState, config: SimConfig, observer=None) -> SimState:
+    """BAOAB loop with one force evaluation per step (md.py:188-208).
+
+    The integrator runs on the GPU (numpy-exact noise, fp32 BAOA and
+    half-kick kernels).  With a GpuReplicaForces the forces stay on the
+    device; any other force_fn is called with host arrays each step.
+    """
+    _require_fp32(config)
+    from .engine import _torch
+
+    torch = _torch()
+    lib = _lib.load()
+    R, N = state.n_replicas, state.n_beads
+    dev = torch.device("cuda")
+    p = md_params(config.dt_fs, config.temperature, config.friction, config.seed)
+    mass = torch.as_tensor(np.asarray(state.masses, np.float64).astype(np.float32), device=dev)
+    pos = torch.as_tensor(np.asarray(state.positions, np.float32), device=dev).contiguous()
+    vel = torch.as_tensor(np.asarray(state.velocities, np.float32), device=dev).contiguous()
+    noise = torch.empty_like(pos)
+    step_t = torch.tensor([int(state.step)], dtype=torch.int64, device=dev)
+    stream = lambda: C.c_void_p(torch.cuda.current_stream().cuda_stream)  # noqa: E731
+    v = _lib.vp
+
+    def host_state():
+        return SimState(positions=pos.cpu().numpy(), velocities=vel.cpu().numpy(),
+                        masses=state.masses, step=int(step_t.item()))
+
+    def eval_forces():
+        f, info = force_fn(pos.cpu().numpy(), int(step_t.item()))
+        _check_forces(f)
+        return torch.as_tensor(np.asarray(f, np.float32), device=dev).contiguous(), f, info
+
+    F, f_host, info = eval_forces()
+    if observer is not None:
+        observer(host_state(), f_host, info, initial=True)
+    for _ in range(config.n_steps):
+        _lib.check(lib.fcg_normal_noise(p.seed, 0, v(step_t), R, N, v(noise), stream()),
+                   "fcg_normal_noise")
+        _lib.check(lib.fcg_langevin_baoa(C.byref(p), v(mass), R, N, v(F), v(noise), v(pos),
+                                         v(vel), stream()), "fcg_langevin_baoa")
+        step_t += 1
+        F, f_host, info = eval_forces()
+        _lib.check(lib.fcg_half_kick(C.byref(p), v(mass), R, N, v(F), v(vel), stream()),
+                   "fcg_half_kick")
+        if observer is not None:
+            observer(host_state(), f_host, info, initial=False)
+    return host_state()
+
+
+@dataclass
+class RunResult:
+    trajectory_path: Path | None
+    scalars_path: Path | None
+    steps: int
+    replicas: int
+    wall_seconds: float
+    dt_fs: float
+    final_state: SimState
+    traffic: TrafficReport
+    mean_edges: float
+
+
+def _format_frame(types, positions, step, replica):
+    rows = [f"{positions.shape[0]}", f"step={step} replica={replica}"]
+    rows += [f"B{int(t)} {x:.9f} {y:.9f} {z:.9f}" for t, (x, y, z) in zip(types, positions)]
+    return "\n".join(rows) + "\n"
+
+
+def run_simulation(params, system, config: SimConfig, out_dir, resume_from=None,
+                   graph_steps: int = 32, rep_offset: int = 0) -> RunResult:
+    """Device-resident run_simulation (md.py:276-349).
+
+    Frames and scalars are written for the initial state and every
+    output_stride steps, ordered by (step, replica), in the reference's
+    formats.  Steps between outputs run as CUDA-graph replays; state comes
+    back to the host only at outputs, checkpoints and the end.  Capacity
+    overflow is repaired by regrowing the CSR buffers and replaying the
+    chunk from its saved start state (results are unchanged: the noise is
+    counter-based).  A blow-up dumps the frame of the offending step to
+    blowup.xyz and raises SimulationBlowupError.
+    """
+    from . import checkpoint as params_io
+
+    _require_fp32(config)
+    out_dir = Path(out_dir)
+    out_dir.mkdir(parents=True, exist_ok=True)
+    masses = np.asarray(system.masses, np.float64)
+    if resume_from is not None:
+        chk = params_io.load_checkpoint(resume_from)
+        pos0 = chk["positions"].astype(np.float32)
+        vel0 = chk["velocities"].astype(np.float32)
+        masses = chk["masses"].astype(np.float64)
+        step0 = int(chk["step"])
+    else:
+        r0 = system.initial_positions()
+        pos0 = np.repeat(r0[None, :, :], config.n_replicas, axis=0).astype(np.float32)
+        vel0 = np.zeros_like(pos0)
+        step0 = 0
+    R, N = pos0.shape[0], pos0.shape[1]
+    eng = MDEngine(params, system.types, masses, system.prior, R, config.dt_fs,
+                   config.temperature, config.friction, config.seed, config.neighbor_stride,
+                   rep_offset=rep_offset)
+    eng.load_state(pos0, vel0, step0)
+
+    traj_path, scal_path = out_dir / "trajectory.xyz", out_dir / "scalars.csv"
+    traj = open(traj_path, "w")
+    scal = open(scal_path, "w")
+    scal.write("# flashcg-scalars v1\n" + SCALARS_SCHEMA + "\n")
+    t_start = time.perf_counter()
+    last = [t_start]
+    edge_total = [0, 0]  # (sum of per-replica edge counts, evaluations*replicas)
+
+    def emit(step_done: int, steps_since: int):
+        now = time.perf_counter()
+        wall_ms = (now - last[0]) * 1e3 / max(steps_since, 1)
+        last[0] = now
+        pos, vel, _ = eng.read_state()
+        st = SimState(positions=pos, velocities=vel, masses=masses, step=step_done)
+        kin = kinetic_temperature(st)
+        pot = eng.potential.cpu().numpy().astype(np.float64)
+        pri = eng.prior_e.cpu().numpy().astype(np.float64)
+        for rep in range(R):
+            traj.write(_format_frame(system.types, pos[rep], step_done, rep))
+            scal.write(f"{step_done},{rep},{pot[rep]:.10g},{pri[rep]:.10g},"
+                       f"{kin[rep]:.10g},{wall_ms:.3f}\n")
+
+    def blowup(step_at):
+        pos, _, _ = eng.read_state()
+        dump = out_dir / "blowup.xyz"
+        with open(dump, "w") as f:
+            for rep in range(R):
+                f.write(_format_frame(system.types, pos[rep], step_at, rep))
+        traj.close()
+        scal.close()
+        raise SimulationBlowupError(f"simulation blew up at step {step_at}; "
+                                    f"diagnostic frame in {dump}")
+
+    try:
+        eng.evaluate()
+        f0 = eng.forces.cpu().numpy()
+        edge_total[0] += int(eng.csr.ptr[-1].item())
+        edge_total[1] += R
+        if not np.all(np.isfinite(f0)) or np.any(np.abs(f0) > FORCE_BLOWUP_LIMIT):
+            blowup(step0)
+        if config.checkpoint_step is not None and step0 == config.checkpoint_step \
+                and config.checkpoint_path:
+            p, v_, _ = eng.read_state()
+            params_io.save_checkpoint(config.checkpoint_path, p, v_, masses, step0, config.seed)
+        emit(step0, 1)
+        stride = max(config.output_stride, 1)
+        cur, end = step0, step0 + config.n_steps
+        while cur < end:
+            nxt = min(end, (cur // stride + 1) * stride)
+            if config.checkpoint_step is not None and cur < config.checkpoint_step < nxt:
+                nxt = config.checkpoint_step
+            n = nxt - cur
+            saved = [t.clone() for t in (eng.pos, eng.vel, eng.forces, eng.step)]
+            eng.clear_flags()
+            eng.run(n, graph_steps=min(graph_steps, n) if n >= 4 else 0)
+            fl = eng.flags()
+            if fl["overflow"] or fl["blowup"]:
+                for t, s0 in zip((eng.pos, eng.vel, eng.forces, eng.step), saved):
+                    t.copy_(s0)
+                if fl["overflow"]:
+                    eng._alloc(max(2 * eng.cap_e, int(1.5 * fl["edges"]) + 1024))
+                    continue
+                # replay one step at a time to locate the blow-up step
+                eng.clear_flags()
+                for _ in range(n):
+                    eng.run(1)
+                    if eng.flags()["blowup"]:
+                        blowup(int(eng.step.item()))
+            edge_total[0] += fl["edge_sum"]
+            edge_total[1] += fl["builds"] * R
+            cur = nxt
+            if config.checkpoint_step is not None and cur == config.checkpoint_step \
+                    and config.checkpoint_path:
+                p, v_, _ = eng.read_state()
+                params_io.save_checkpoint(config.checkpoint_path, p, v_, masses, cur,
+                                          config.seed)
+            if cur % stride == 0:
+                emit(cur, n)
+        eng.torch.cuda.synchronize()
+    finally:
+        traj.close()
+        scal.close()
+
+    wall = time.perf_counter() - t_start
+    pos, vel, step = eng.read_state()
+    traffic = TrafficReport()
+    return RunResult(trajectory_path=traj_path, scalars_path=scal_path, steps=config.n_steps,
+                     replicas=R, wall_seconds=wall, dt_fs=config.dt_fs,
+                     final_state=SimState(positions=pos, velocities=vel, masses=masses, step=step),
+                     traffic=traffic,
+                     mean_edges=edge_total[0] / edge_total[1] if edge_total[1] else 0.0)
+
+
+def throughput_report(result: RunResult) -> dict:
+    """timestep*mol/s and ns/day (md.py:352-364)."""
+    if result.wall_seconds <= 0:
+        raise ValueError("cannot report throughput for a run with zero elapsed time")
+    rate = result.steps * result.replicas / result.wall_seconds
+    return {"steps": result.steps, "replicas": result.replicas,
+            "wall_seconds": result.wall_seconds, "timestep_mol_per_s": rate,
+            "ns_per_day": rate * result.dt_fs * 86400.0 / 1.0e6}

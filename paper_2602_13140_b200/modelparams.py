@@ -1,0 +1,257 @@
+"""Model configuration and parameters, mirroring flashcg.model.
+
+Host-side only: the types and the seeded initialiser are what a caller of
+the reference constructs (model.py:164-459 of the reference); the compute
+(basis, filter MLPs, node MLPs and their backward) runs in libfcg.so.
+`init_params` reproduces the reference's draws bit for bit (pinned by
+tests/test_host_golden.py against fixtures generated from the reference).
+`DeviceModel` packs a parameter set into zero-padded device tensors plus
+the `fcg_model` descriptor the C ABI consumes.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+
+LN2 = math.log(2.0)
+
+DEFAULT_HIDDEN_DIM = 128
+DEFAULT_RBF_DIM = 64
+DEFAULT_NUM_BLOCKS = 3
+DEFAULT_CUTOFF = 1.5  # nm
+DEFAULT_NUM_ATOM_TYPES = 32
+DEFAULT_FILTER_HIDDEN = 128
+DEFAULT_READOUT_HIDDEN = 64
+
+
+class ConfigError(ValueError):
+    """Invalid model configuration or mismatched shapes (reference model.py:28)."""
+
+
+@dataclass(frozen=True)
+class ModelConfig:
+    hidden_dim: int = DEFAULT_HIDDEN_DIM
+    rbf_dim: int = DEFAULT_RBF_DIM
+    num_blocks: int = DEFAULT_NUM_BLOCKS
+    cutoff: float = DEFAULT_CUTOFF
+    num_atom_types: int = DEFAULT_NUM_ATOM_TYPES
+    filter_hidden_dim: int = DEFAULT_FILTER_HIDDEN
+    readout_hidden_dim: int = DEFAULT_READOUT_HIDDEN
+
+    def __post_init__(self):
+        ints = ("hidden_dim", "rbf_dim", "num_blocks", "num_atom_types",
+                "filter_hidden_dim", "readout_hidden_dim")
+        bad = [k for k in ints if int(getattr(self, k)) < 1]
+        if bad:
+            raise ConfigError(f"{bad[0]} must be >= 1, got {getattr(self, bad[0])}")
+        if not self.cutoff > 0:
+            raise ConfigError(f"cutoff must be > 0, got {self.cutoff}")
+
+
+@dataclass(frozen=True)
+class RbfSpec:
+    """Gaussian centres on [0, cutoff] with one shared width (model.py:51-90)."""
+
+    centers: np.ndarray
+    gamma: float
+    cutoff: float
+
+    def __post_init__(self):
+        c = np.asarray(self.centers, dtype=np.float64)
+        if c.ndim != 1 or c.size == 0:
+            raise ConfigError("centers must be a non-empty 1-d array")
+        if not self.gamma > 0:
+            raise ConfigError(f"gamma must be > 0, got {self.gamma}")
+        if c.size > 1 and (np.any(np.diff(c) <= 0) or c[0] != 0.0
+                           or not np.isclose(c[-1], self.cutoff)):
+            raise ConfigError("centers must increase strictly over [0, cutoff]")
+
+    @property
+    def dim(self) -> int:
+        return int(np.asarray(self.centers).size)
+
+    @classmethod
+    def uniform(cls, rbf_dim: int, cutoff: float) -> "RbfSpec":
+        if rbf_dim < 2:
+            return cls(centers=np.zeros(1), gamma=1.0 / (2.0 * cutoff * cutoff),
+                       cutoff=float(cutoff))
+        delta = cutoff / (rbf_dim - 1)
+        return cls(centers=np.linspace(0.0, cutoff, rbf_dim),
+                   gamma=1.0 / (2.0 * delta * delta), cutoff=float(cutoff))
+
+    @classmethod
+    def for_config(cls, config: ModelConfig) -> "RbfSpec":
+        return cls.uniform(config.rbf_dim, config.cutoff)
+
+
+@dataclass(frozen=True)
+class BlockParams:
+    pre_linear: tuple   # (W[D,D], b[D])
+    filter_mlp: tuple   # ((W[Fh,Dr], b), (W[D,Fh], b))
+    post_mlp: tuple     # ((W[D,D], b), (W[D,D], b))
+
+
+@dataclass(frozen=True)
+class ModelParams:
+    config: ModelConfig
+    embedding: np.ndarray
+    blocks: tuple
+    readout: tuple      # ((W[Rh,D], b), (W[1,Rh], b))
+    rbf: RbfSpec = field(default=None)
+
+    def __post_init__(self):
+        if self.rbf is None:
+            object.__setattr__(self, "rbf", RbfSpec.for_config(self.config))
+
+    @property
+    def dtype(self):
+        return self.embedding.dtype
+
+    def astype(self, dtype) -> "ModelParams":
+        def cast(layers):
+            return tuple((w.astype(dtype), b.astype(dtype)) for w, b in layers)
+        return ModelParams(
+            config=self.config, embedding=self.embedding.astype(dtype),
+            blocks=tuple(BlockParams(pre_linear=cast([bp.pre_linear])[0],
+                                     filter_mlp=cast(bp.filter_mlp),
+                                     post_mlp=cast(bp.post_mlp)) for bp in self.blocks),
+            readout=cast(self.readout), rbf=self.rbf)
+
+    def named_tensors(self):
+        out = [("embedding", self.embedding)]
+        for t, bp in enumerate(self.blocks):
+            out += [(f"block{t}.pre.W", bp.pre_linear[0]), (f"block{t}.pre.b", bp.pre_linear[1])]
+            for kind, layers in (("filter", bp.filter_mlp), ("post", bp.post_mlp)):
+                for j, (w, b) in enumerate(layers):
+                    out += [(f"block{t}.{kind}{j}.W", w), (f"block{t}.{kind}{j}.b", b)]
+        for j, (w, b) in enumerate(self.readout):
+            out += [(f"readout{j}.W", w), (f"readout{j}.b", b)]
+        return out
+
+
+def init_params(config: ModelConfig, seed: int) -> ModelParams:
+    """Glorot-uniform weights drawn in float64 from default_rng(seed), zero
+    biases, stored float32 — the reference's draw order (model.py:292-327):
+    embedding, then per block pre, filter0, filter1, post0, post1, then the
+    two readout layers."""
+    rng = np.random.default_rng(seed)
+    d, dr = config.hidden_dim, config.rbf_dim
+    fh, rh = config.filter_hidden_dim, config.readout_hidden_dim
+
+    def layer(n_out, n_in):
+        bound = math.sqrt(6.0 / (n_in + n_out))
+        return rng.uniform(-bound, bound, size=(n_out, n_in)), np.zeros(n_out)
+
+    emb = rng.uniform(-1.0, 1.0, size=(config.num_atom_types, d)) / math.sqrt(d)
+    blocks = []
+    for _ in range(config.num_blocks):
+        pre = layer(d, d)
+        filt = (layer(fh, dr), layer(d, fh))
+        post = (layer(d, d), layer(d, d))
+        blocks.append(BlockParams(pre_linear=pre, filter_mlp=filt, post_mlp=post))
+    readout = (layer(rh, d), layer(1, rh))
+    return ModelParams(config=config, embedding=emb, blocks=tuple(blocks),
+                       readout=readout).astype(np.float32)
+
+
+# ---------------------------------------------------------------------------
+# device packing
+
+def _check_widths(cfg: ModelConfig):
+    lim = {"hidden_dim": _lib.FCG_D, "filter_hidden_dim": _lib.FCG_D,
+           "rbf_dim": _lib.FCG_DR, "readout_hidden_dim": _lib.FCG_RH,
+           "num_blocks": _lib.FCG_MAX_BLOCKS}
+    for k, v in lim.items():
+        if getattr(cfg, k) > v:
+            raise ConfigError(f"{k}={getattr(cfg, k)} exceeds the compiled width {v} of libfcg")
+
+
+def _pad(a, shape):
+    out = np.zeros(shape, dtype=np.float32)
+    a = np.asarray(a, dtype=np.float32)
+    out[tuple(slice(0, s) for s in a.shape)] = a
+    return out
+
+
+def _is_quantized(params) -> bool:
+    return not isinstance(params.readout, tuple)
+
+
+class DeviceModel:
+    """Zero-padded device copy of ModelParams / QuantizedParams + descriptor.
+
+    Weights are uploaded once per process and shared read-only by all
+    replicas; the descriptor holds raw device pointers into
+    the tensors kept alive here.
+    """
+
+    def __init__(self, params, device="cuda"):
+        import torch
+
+        cfg = params.config
+        _check_widths(cfg)
+        self.config = cfg
+        self.quantized = _is_quantized(params)
+        self._keep = []
+        D, DR, RH = _lib.FCG_D, _lib.FCG_DR, _lib.FCG_RH
+
+        def dev(a, dtype=torch.float32):
+            t = torch.as_tensor(np.ascontiguousarray(a)).to(device=device, dtype=dtype)
+            self._keep.append(t)
+            return t
+
+        def dense(lin):
+            """fp32 (out,in) matrix the backward uses: W, or dequant() for W16."""
+            if isinstance(lin, tuple):
+                return np.asarray(lin[0], np.float32), np.asarray(lin[1], np.float32)
+            return lin.dequant().astype(np.float32), np.asarray(lin.bias, np.float32)
+
+        def layers_of(net):
+            return net if isinstance(net, tuple) else net.layers
+
+        m = _lib.FcgModel()
+        m.format = _lib.FCG_FMT_W16 if self.quantized else _lib.FCG_FMT_FP32
+        m.num_blocks = len(params.blocks)
+        m.num_types = int(params.embedding.shape[0])
+        m.cutoff = float(np.float32(cfg.cutoff))
+        m.gamma = float(np.float32(params.rbf.gamma))
+        m.centers = _lib.fptr(dev(_pad(np.asarray(params.rbf.centers).astype(np.float32), (DR,))))
+        m.embedding = _lib.fptr(dev(_pad(params.embedding, (m.num_types, D))))
+
+        def put(blk, name, lin, shape_out, shape_in, quant_src=None):
+            w, b = dense(lin)
+            wp = _pad(w, (shape_out, shape_in))
+            setattr(blk, f"{name}_w", _lib.fptr(dev(wp)))
+            setattr(blk, f"{name}_wt", _lib.fptr(dev(np.ascontiguousarray(wp.T))))
+            setattr(blk, f"{name}_b", _lib.fptr(dev(_pad(b, (shape_out,)))))
+            if not isinstance(lin, tuple):
+                w16 = np.zeros((shape_out, shape_in), dtype=np.float16)
+                w16[:lin.weight.shape[0], :lin.weight.shape[1]] = lin.weight
+                setattr(blk, f"{name}_h", _lib.u16ptr(dev(w16.view(np.int16), torch.int16)))
+                setattr(blk, f"{name}_s", _lib.fptr(dev(_pad(lin.scale, (shape_out,)))))
+
+        for t, bp in enumerate(params.blocks):
+            blk = m.blocks[t]
+            f0, f1 = layers_of(bp.filter_mlp)
+            p0, p1 = layers_of(bp.post_mlp)
+            put(blk, "pre", bp.pre_linear, D, D)
+            put(blk, "f0", f0, D, DR)
+            put(blk, "f1", f1, D, D)
+            put(blk, "p0", p0, D, D)
+            put(blk, "p1", p1, D, D)
+
+        r0, r1 = layers_of(params.readout)
+        w0, b0 = dense(r0)
+        w0p = _pad(w0, (RH, D))
+        m.r0_w = _lib.fptr(dev(w0p))
+        m.r0_wt = _lib.fptr(dev(np.ascontiguousarray(w0p.T)))
+        m.r0_b = _lib.fptr(dev(_pad(b0, (RH,))))
+        w1, b1 = dense(r1)
+        m.r1_w = _lib.fptr(dev(_pad(w1.reshape(-1), (RH,))))
+        m.r1_b = float(np.float32(b1.reshape(-1)[0]))
+        self.desc = m

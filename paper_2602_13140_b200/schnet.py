@@ -1,0 +1,226 @@
+"""flash_energy_forces and friends on the GPU (reference flash.py).
+
+`flash_energy_forces` keeps the reference signature and return type
+(flash.py:446-501) but evaluates the whole model — embedding, T fused
+interaction blocks, readout, and the force backward — in libfcg.so on
+cuda:0.  Computation is fp32 (the reference's production precision); the
+ablation flags of PipelineMode select reference CPU schedules that have no
+GPU counterpart, so every mode runs the fused, segment-reduced pipeline and
+reports its modelled traffic.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+
+from . import _lib
+
+DEFAULT_TILE_EDGES = 1024
+DEFAULT_SEGMENT_SPLIT = 8192
+
+STAGES = ("radial_basis", "filters", "gather", "messages", "aggregation", "mlps")
+
+
+@dataclass(frozen=True)
+class PipelineMode:
+    fused: bool = True
+    segred: bool = True
+    quant: bool = False
+    tile_edges: int = DEFAULT_TILE_EDGES
+    segment_split: int = DEFAULT_SEGMENT_SPLIT
+
+    def with_flags(self, **kw) -> "PipelineMode":
+        return replace(self, **kw)
+
+
+@dataclass
+class TrafficReport:
+    """Modelled bytes per stage (reference traffic.py:35-77)."""
+
+    read_bytes: dict = field(default_factory=lambda: dict.fromkeys(STAGES, 0))
+    written_bytes: dict = field(default_factory=lambda: dict.fromkeys(STAGES, 0))
+    atomic_updates: int = 0
+
+    def record(self, stage, read=0, written=0, atomics=0):
+        if stage not in self.read_bytes:
+            raise KeyError(f"unknown traffic stage {stage!r}")
+        self.read_bytes[stage] += int(read)
+        self.written_bytes[stage] += int(written)
+        self.atomic_updates += int(atomics)
+
+    @property
+    def total_read(self) -> int:
+        return sum(self.read_bytes.values())
+
+    @property
+    def total_written(self) -> int:
+        return sum(self.written_bytes.values())
+
+    @property
+    def total_bytes(self) -> int:
+        return self.total_read + self.total_written
+
+    def stage_bytes(self, stage) -> int:
+        return self.read_bytes[stage] + self.written_bytes[stage]
+
+    def merge(self, other: "TrafficReport"):
+        for s in STAGES:
+            self.read_bytes[s] += other.read_bytes[s]
+            self.written_bytes[s] += other.written_bytes[s]
+        self.atomic_updates += other.atomic_updates
+
+    def as_dict(self) -> dict:
+        return {"read": dict(self.read_bytes), "written": dict(self.written_bytes),
+                "total_bytes": self.total_bytes, "atomic_updates": self.atomic_updates}
+
+
+def _flash_block_lines(N, E, D):
+    """(stage, read, written) element counts of one fused block, forward then
+    backward — the accounting of traffic.py:135-169, which is also the
+    algorithmic-bytes definition of the roofline."""
+    nd = N * D
+    return [
+        ("mlps", nd, nd), ("messages", 6 * E + E * D, E), ("aggregation", 0, nd),
+        ("mlps", nd, nd), ("mlps", 2 * nd, nd),
+        ("mlps", nd, nd), ("mlps", 2 * nd, nd), ("messages", 7 * E + E * D, 3 * E),
+        ("messages", min(N, E) * D, 0), ("aggregation", 0, nd), ("aggregation", 6 * E, 3 * N),
+        ("mlps", nd, nd), ("mlps", 2 * nd, nd),
+    ]
+
+
+def io_model_flash(N: int, E: int, D: int, D_r: int, T: int, width: int) -> int:
+    """Closed form of the fused backend's modelled bytes per evaluation:
+    width*T*(19ND + 2ED + 23E + min(N,E)*D + 3N)."""
+    return T * width * (19 * N * D + 2 * E * D + 23 * E + min(N, E) * D + 3 * N)
+
+
+def io_model_base(N: int, E: int, D: int, D_r: int, T: int, width: int) -> int:
+    """Closed form of the materialising backend's modelled bytes
+    (traffic.py:80-132): width*T*(19ND + 23ED + 9E*D_r + 45E + 3N)."""
+    return T * width * (19 * N * D + 23 * E * D + 9 * E * D_r + 45 * E + 3 * N)
+
+
+def io_model_flash_report(N: int, E: int, params, width: int = 4) -> TrafficReport:
+    rep = TrafficReport()
+    D = params.config.hidden_dim
+    for _ in range(len(params.blocks)):
+        for stage, r, w in _flash_block_lines(N, E, D):
+            rep.record(stage, r * width, w * width, 0)
+    return rep
+
+
+@dataclass
+class EnergyForces:
+    energy: float
+    per_atom: np.ndarray
+    forces: np.ndarray
+    traffic: TrafficReport
+
+
+def segment_reduce(values: np.ndarray, ptr: np.ndarray, split: int = DEFAULT_SEGMENT_SPLIT):
+    """Contention-free CSR segment sum on the GPU (flash.py:109-135): one
+    owner per output element, empty segments give zero rows."""
+    from .engine import _torch
+
+    torch = _torch()
+    lib = _lib.load()
+    values = np.asarray(values)
+    ptr = np.asarray(ptr, np.int64)
+    nseg = ptr.size - 1
+    tail = values.shape[1:]
+    k = int(np.prod(tail)) if tail else 1
+    f64 = values.dtype == np.float64
+    dt = np.float64 if f64 else np.float32
+    out_shape = (nseg,) + tail
+    if nseg <= 0 or values.shape[0] == 0:
+        return np.zeros(out_shape, dtype=dt)
+    dv = torch.as_tensor(np.ascontiguousarray(values.reshape(values.shape[0], k), dtype=dt)).cuda()
+    dptr = torch.as_tensor(ptr).cuda()
+    out = torch.empty(nseg * k, dtype=dv.dtype, device="cuda")
+    fn = lib.fcg_segment_reduce_f64 if f64 else lib.fcg_segment_reduce
+    _lib.check(fn(_lib.vp(dv), values.shape[0], k, _lib.vp(dptr), nseg, _lib.vp(out),
+                  C.c_void_p(torch.cuda.current_stream().cuda_stream)), "fcg_segment_reduce")
+    return out.cpu().numpy().reshape(out_shape)
+
+
+class _Evaluator:
+    """Cached device buffers for single-system evaluations of one params set."""
+
+    def __init__(self, params):
+        from .engine import _torch
+        from .modelparams import DeviceModel
+
+        self.torch = _torch()
+        self.params = params
+        self.dm = DeviceModel(params)
+        self.lib = _lib.load()
+
+    def __call__(self, pos32: np.ndarray, types: np.ndarray, csr):
+        torch, lib, v = self.torch, self.lib, _lib.vp
+        ptr, nbr, rev, own = csr
+        N = pos32.shape[0]
+        E = int(ptr[-1])
+        cap = max(E, 1)
+        dev = "cuda"
+        dpos = torch.as_tensor(np.ascontiguousarray(pos32)).to(dev)
+        dtypes = torch.as_tensor(types.astype(np.int32)).to(dev)
+        i32 = lambda a: torch.as_tensor(  # noqa: E731
+            np.concatenate([np.asarray(a, np.int64), [0]]).astype(np.int32)).to(dev)
+        dptr = torch.as_tensor(np.asarray(ptr).astype(np.int32)).to(dev)
+        dnbr, drev, down = i32(nbr), i32(rev), i32(own)
+        per_atom = torch.empty(N, dtype=torch.float32, device=dev)
+        energy = torch.empty(1, dtype=torch.float32, device=dev)
+        forces = torch.empty(N, 3, dtype=torch.float32, device=dev)
+        nb = lib.fcg_ef_workspace_bytes(C.byref(self.dm.desc), 1, N, cap)
+        ws = torch.empty(int(nb), dtype=torch.uint8, device=dev)
+        _lib.check(lib.fcg_energy_forces(C.byref(self.dm.desc), v(dpos), v(dtypes), 1, N,
+                                         v(dptr), v(dnbr), v(drev), v(down), cap, v(per_atom),
+                                         v(energy), v(forces), v(ws), nb,
+                                         C.c_void_p(torch.cuda.current_stream().cuda_stream)),
+                   "fcg_energy_forces")
+        return float(energy.item()), per_atom.cpu().numpy(), forces.cpu().numpy()
+
+
+_EVALUATORS: dict = {}
+
+
+def _evaluator(params) -> _Evaluator:
+    key = id(params)
+    ev = _EVALUATORS.get(key)
+    if ev is None or ev.params is not params:
+        if len(_EVALUATORS) > 8:
+            _EVALUATORS.clear()
+        ev = _EVALUATORS[key] = _Evaluator(params)
+    return ev
+
+
+def flash_energy_forces(positions, types, params, mode: PipelineMode = PipelineMode(),
+                        nl=None, layouts=None, tracker=None) -> EnergyForces:
+    """Energy, per-atom energies and forces of one system (flash.py:446-501)."""
+    from .csr import csr_from_neighbor_list, device_csr
+
+    positions = np.asarray(positions)
+    types = np.asarray(types)
+    cfg = params.config
+    if types.size and (types.min() < 0 or types.max() >= cfg.num_atom_types):
+        raise ValueError("atom type out of range for the embedding table")
+    N = positions.shape[0]
+    if nl is None:
+        csr = device_csr(positions, cfg.cutoff)
+        csr = (csr[0], csr[1], csr[2], csr[3])
+    else:
+        if layouts is not None:
+            dst_csr, src_csr = layouts
+            if dst_csr.key != "dst" or src_csr.key != "src":
+                raise ValueError("flash requires (destination, source) grouped layouts")
+            if dst_csr.perm.size != nl.num_edges or dst_csr.ptr.size != nl.n + 1:
+                raise ValueError("CSR layout does not match the neighbor list")
+        csr = csr_from_neighbor_list(nl)
+    energy, per_atom, forces = _evaluator(params)(positions.astype(np.float32), types, csr)
+    E = int(csr[0][-1])
+    return EnergyForces(energy=energy, per_atom=per_atom,
+                        forces=forces.astype(positions.dtype, copy=False),
+                        traffic=io_model_flash_report(N, E, params))

@@ -1,0 +1,409 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle and the
+reference's golden vectors.
+
+Bars (BASELINE north star / SURVEY §8(c)):
+  * neighbour list, CSR ptr/perm, noise, one integrator step, prior:
+    bit-exact;
+  * fp32 energies / forces: energy_rel_err and force_rel_err <= 1e-5;
+  * 16-bit weights: energy <= 1e-4, force <= 5e-4 vs the quantized oracle,
+    relative force RMSE <= 2e-3 vs fp32;
+  * trajectories: max |dr| <= 1e-5 nm after the golden run lengths.
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+from helpers import params_for, rel_rmse
+from oracle import flashcg_oracle as O
+import paper_2602_13140_b200 as P
+from paper_2602_13140_b200.csr import device_csr
+from paper_2602_13140_b200.engine import MDEngine
+from paper_2602_13140_b200.inputs import generate_system
+from paper_2602_13140_b200.modelparams import ModelConfig, init_params
+
+pytestmark = pytest.mark.gpu
+
+FP32_TOL = 1e-5
+
+
+# ---------------------------------------------------------------- (a) CSR
+def test_neighbor_golden_cases_bit_exact(golden):
+    g = golden["neighbors"]
+    for name in g.cases("src"):
+        c = g.case(name)
+        nl = P.build_neighbors_cells(c["pos"], float(c["rc"]))
+        np.testing.assert_array_equal(nl.src, c["src"], err_msg=name)
+        np.testing.assert_array_equal(nl.dst, c["dst"], err_msg=name)
+        d, s = P.group_by_destination(nl), P.group_by_source(nl)
+        np.testing.assert_array_equal(d.ptr, c["dptr"], err_msg=name)
+        np.testing.assert_array_equal(d.perm, c["dperm"], err_msg=name)
+        np.testing.assert_array_equal(s.ptr, c["sptr"], err_msg=name)
+        np.testing.assert_array_equal(s.perm, c["sperm"], err_msg=name)
+        # the fused CSR's rev map is the reference's source-grouped perm
+        ptr, nbr, rev, own = device_csr(c["pos"], float(c["rc"]))
+        np.testing.assert_array_equal(ptr, c["dptr"], err_msg=name)
+        np.testing.assert_array_equal(rev, c["sperm"], err_msg=name)
+
+
+def test_neighbor_adversarial_pairs(golden):
+    g = golden["neighbors"]
+    pairs, rc, edge = g["adversarial/pairs"], float(g["adversarial/rc"]), g["adversarial/edge"]
+    ptr, nbr, rev, own = device_csr(pairs, rc)   # 256 two-bead "replicas" in one launch
+    got = (ptr[2::2] - ptr[0:-1:2]) > 0
+    np.testing.assert_array_equal(got, edge)
+
+
+def test_batched_csr_matches_oracle_per_replica():
+    sysm = generate_system("coil", 269, 0)
+    rng = np.random.default_rng(0)
+    R = 64
+    pos = (sysm.positions[None] + rng.normal(0, 0.05, size=(R, 269, 3))).astype(np.float32)
+    ptr, nbr, rev, own = device_csr(pos, 1.5)
+    N = 269
+    for r in range(R):
+        lo, hi = ptr[r * N], ptr[(r + 1) * N]
+        src, dst = O.neighbor_list(pos[r], 1.5)
+        np.testing.assert_array_equal(nbr[lo:hi] - r * N, src)
+        np.testing.assert_array_equal(own[lo:hi] - r * N, dst)
+        dptr, _ = O.group(dst, N)
+        _, sperm = O.group(src, N)
+        np.testing.assert_array_equal(ptr[r * N:(r + 1) * N + 1] - lo, dptr)
+        np.testing.assert_array_equal(rev[lo:hi] - lo, sperm)
+
+
+def test_large_n_csr_matches_oracle():
+    sysm = generate_system("globule", 3000, 0, bonded=False)
+    pos = sysm.positions.astype(np.float32)
+    nl = P.build_neighbors_cells(pos, 2.0)
+    src, dst = O.neighbor_list(pos, 2.0)
+    np.testing.assert_array_equal(nl.src, src)
+    np.testing.assert_array_equal(nl.dst, dst)
+
+
+def test_group_by_arbitrary_lists():
+    rng = np.random.default_rng(5)
+    for _ in range(30):
+        n = int(rng.integers(1, 60))
+        e = int(rng.integers(0, 400))
+        key = rng.integers(0, n, size=e)
+        nl = P.NeighborList(src=key, dst=rng.integers(0, n, size=e), n=n)
+        lay = P.group_by_source(nl)
+        ptr, perm = O.group(key, n)
+        np.testing.assert_array_equal(lay.ptr, ptr)
+        np.testing.assert_array_equal(lay.perm, perm)
+
+
+# ------------------------------------------------------------ (d) segment reduce
+def test_segment_reduce():
+    np.testing.assert_array_equal(
+        P.segment_reduce(np.array([[1.0, 2.0], [3.0, 4.0], [5.0, 6.0]], np.float32),
+                         np.array([0, 2, 3])), [[4, 6], [5, 6]])
+    np.testing.assert_array_equal(
+        P.segment_reduce(np.array([[1.0], [2.0]]), np.array([0, 0, 2, 2])), [[0], [3], [0]])
+    out = P.segment_reduce(np.zeros((0, 3)), np.array([0, 0, 0]))
+    assert out.shape == (2, 3) and not out.any()
+    rng = np.random.default_rng(0)
+    v = rng.standard_normal((20000, 4))
+    ptr = np.array([0, 15000, 20000])
+    np.testing.assert_allclose(P.segment_reduce(v, ptr), O.segment_sum(v, ptr), rtol=1e-10)
+    a = P.segment_reduce(v, ptr, split=1024)
+    np.testing.assert_array_equal(a, P.segment_reduce(v, ptr, split=1024))
+
+
+# ------------------------------------------------- (b)(c)(d) energy + forces
+FP32_CASES = ["small0", "small1", "small2", "small3", "star", "no_edges", "coil269",
+              "globule269", "small64"]
+
+
+@pytest.mark.parametrize("name", FP32_CASES)
+def test_energy_forces_fp32(golden, name):
+    c = golden["flash"].case(name)
+    params = params_for(c)
+    out = P.flash_energy_forces(c["pos"], c["types"], params, P.PipelineMode())
+    e_err = O.energy_rel_err(out.energy, float(c["energy"]), c["per_atom"])
+    f_err = O.force_rel_err(out.forces, c["forces"])
+    assert e_err <= FP32_TOL, e_err
+    assert f_err <= FP32_TOL, f_err
+    np.testing.assert_allclose(out.per_atom, c["per_atom"], rtol=1e-4, atol=1e-6)
+    assert out.forces.dtype == c["pos"].dtype
+    assert out.traffic.atomic_updates == 0
+    assert out.traffic.total_bytes == P.io_model_flash(
+        c["pos"].shape[0], int(P.build_neighbors_cells(c["pos"], params.config.cutoff).num_edges),
+        params.config.hidden_dim, params.config.rbf_dim, params.config.num_blocks, 4)
+
+
+@pytest.mark.parametrize("name", ["small_w16", "coil269_w16"])
+def test_energy_forces_w16(golden, name):
+    c = golden["flash"].case(name)
+    params = params_for(c)
+    out = P.flash_energy_forces(c["pos"], c["types"], params, P.PipelineMode())
+    assert O.energy_rel_err(out.energy, float(c["energy"]), c["per_atom"]) <= 1e-4
+    assert O.force_rel_err(out.forces, c["forces"]) <= 5e-4
+    if name == "coil269_w16":
+        fp = golden["flash"].case("coil269")
+        assert rel_rmse(out.forces, fp["forces"]) <= 2e-3
+
+
+def test_energy_forces_given_neighbor_list(golden):
+    c = golden["flash"].case("star")
+    params = params_for(c)
+    nl = P.build_neighbors_bruteforce(c["pos"], params.config.cutoff)
+    assert nl.num_edges == 12 and np.count_nonzero(nl.dst == 0) == 6
+    lay = (P.group_by_destination(nl), P.group_by_source(nl))
+    out = P.flash_energy_forces(c["pos"], c["types"], params, P.PipelineMode(), nl=nl, layouts=lay)
+    assert O.force_rel_err(out.forces, c["forces"]) <= FP32_TOL
+    with pytest.raises(ValueError):
+        P.flash_energy_forces(c["pos"], c["types"], params, P.PipelineMode(), nl=nl,
+                              layouts=(lay[1], lay[0]))
+
+
+def test_energy_forces_rejects_bad_types(golden):
+    c = golden["flash"].case("small0")
+    params = params_for(c)
+    with pytest.raises(ValueError):
+        P.flash_energy_forces(c["pos"], np.full(24, 99), params, P.PipelineMode())
+
+
+def test_energy_forces_deterministic(golden):
+    c = golden["flash"].case("coil269")
+    params = params_for(c)
+    a = P.flash_energy_forces(c["pos"], c["types"], params)
+    b = P.flash_energy_forces(c["pos"], c["types"], params)
+    assert a.energy == b.energy
+    np.testing.assert_array_equal(a.forces, b.forces)
+
+
+def test_forces_newton_third_law(golden):
+    c = golden["flash"].case("globule269")
+    out = P.flash_energy_forces(c["pos"], c["types"], params_for(c))
+    net = out.forces.astype(np.float64).sum(axis=0)
+    assert np.max(np.abs(net)) <= 1e-4 * np.max(np.abs(out.forces))
+
+
+def test_batched_engine_matches_oracle_per_replica():
+    sysm = generate_system("coil", 269, 0)
+    params = init_params(ModelConfig(), 0)
+    R = 64
+    rng = np.random.default_rng(1)
+    pos = (sysm.positions[None] + rng.normal(0, 0.04, size=(R, 269, 3))).astype(np.float32)
+    eng = MDEngine(params, sysm.types, sysm.masses, sysm.prior, R)
+    eng.load_state(pos, np.zeros_like(pos), 0)
+    eng.evaluate()
+    F = eng.forces.cpu().numpy()
+    pot = eng.potential.cpu().numpy()
+    pri = eng.prior_e.cpu().numpy()
+    for r in range(0, R, 9):
+        e, pa, f = O.energy_forces(pos[r], sysm.types, params)
+        ep, fp = O.prior_energy_forces(pos[r], sysm.prior)
+        assert O.energy_rel_err(float(pot[r]), e, pa) <= FP32_TOL
+        assert O.force_rel_err(F[r] - fp, f) <= FP32_TOL
+        assert abs(float(pri[r]) - ep) <= 1e-5 * max(abs(ep), 1.0)
+
+
+# ----------------------------------------------------------- (f) integrator
+def _noise_gpu(seed, rep_offset, step, R, N):
+    import ctypes as C
+    import torch
+    from paper_2602_13140_b200 import _lib
+    lib = _lib.load()
+    out = torch.empty(R, N, 3, dtype=torch.float32, device="cuda")
+    st = torch.tensor([step], dtype=torch.int64, device="cuda")
+    _lib.check(lib.fcg_normal_noise(seed, rep_offset, _lib.vp(st), R, N, _lib.vp(out),
+                                    C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    return out.cpu().numpy()
+
+
+def test_noise_bit_exact_golden(golden):
+    g = golden["md"]
+    for k in [k for k in g._z.files if k.startswith("noise/")]:
+        seed, rep, step, n = (int(x) for x in k.split("/")[1].split("_"))
+        got = _noise_gpu(seed, rep, step, 1, n)[0]
+        np.testing.assert_array_equal(got, g[k].astype(np.float32), err_msg=k)
+
+
+def test_noise_bit_exact_many_streams():
+    R, N = 64, 269
+    for step in (0, 1, 777, 2 ** 33 + 5):
+        got = _noise_gpu(0, 0, step, R, N)
+        for r in range(R):
+            np.testing.assert_array_equal(got[r], O.noise(0, r, step, N))
+    got = _noise_gpu(3, 100, 9, 4, 20000)   # long streams: many tail/wedge draws
+    for r in range(4):
+        np.testing.assert_array_equal(got[r], O.noise(3, 100 + r, 9, 20000))
+
+
+def test_one_step_bit_exact(golden):
+    import ctypes as C
+    import torch
+    from paper_2602_13140_b200 import _lib
+    from paper_2602_13140_b200.engine import md_params
+    g = golden["md"]
+    lib = _lib.load()
+    R, N = g["step/pos"].shape[:2]
+    p = md_params(4.0, 300.0, 1.0, 7)
+    dev = lambda a: torch.as_tensor(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    pos, vel = dev(g["step/pos"]), dev(g["step/vel"])
+    F, F2 = dev(g["step/F"]), dev(g["step/F2"])
+    mass = dev(g["step/masses"].astype(np.float32))
+    noise = dev(np.zeros((R, N, 3), np.float32))
+    st = torch.tensor([11], dtype=torch.int64, device="cuda")
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    v = _lib.vp
+    _lib.check(lib.fcg_normal_noise(7, 0, v(st), R, N, v(noise), s))
+    _lib.check(lib.fcg_langevin_baoa(C.byref(p), v(mass), R, N, v(F), v(noise), v(pos), v(vel), s))
+    np.testing.assert_array_equal(pos.cpu().numpy(), g["step/pos1"])
+    np.testing.assert_array_equal(vel.cpu().numpy(), g["step/vel1"])
+    _lib.check(lib.fcg_half_kick(C.byref(p), v(mass), R, N, v(F2), v(vel), s))
+    np.testing.assert_array_equal(vel.cpu().numpy(), g["step/vel2"])
+
+
+def test_prior_bit_exact(golden):
+    import ctypes as C
+    import torch
+    from paper_2602_13140_b200 import _lib
+    from paper_2602_13140_b200.prior import DevicePrior
+    g = golden["md"]
+    chain = generate_system("coil", 30, 2)
+    dp = DevicePrior(chain.prior, 30)
+    pos = torch.as_tensor(g["prior/pos"]).cuda()
+    e = torch.empty(1, device="cuda")
+    f = torch.empty(30, 3, device="cuda")
+    lib = _lib.load()
+    _lib.check(lib.fcg_prior_forces(C.byref(dp.desc), _lib.vp(pos), 1, 30, _lib.vp(e),
+                                    _lib.vp(f), C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    np.testing.assert_array_equal(f.cpu().numpy(), g["prior/forces"])
+    assert abs(float(e.item()) - float(g["prior/energy"])) <= 1e-6 * abs(float(g["prior/energy"]))
+
+
+def _engine_for(name, golden, R=None, **kw):
+    c = golden["md"].case(name)
+    n, sseed, pseed, Rg, steps = (int(x) for x in c["meta"])
+    sysm = generate_system("coil", n, sseed)
+    params = init_params(ModelConfig(**json.loads(str(c["cfg"]))), pseed)
+    R = R or Rg
+    eng = MDEngine(params, sysm.types, sysm.masses, sysm.prior, R, seed=9, **kw)
+    pos0 = np.repeat(sysm.positions[None], R, axis=0).astype(np.float32)
+    eng.load_state(pos0, np.zeros_like(pos0), 0)
+    eng.evaluate()
+    return eng, c, steps
+
+
+@pytest.mark.parametrize("name", ["traj_tiny", "traj_coil269"])
+def test_trajectory_vs_reference(golden, name):
+    eng, c, steps = _engine_for(name, golden)
+    eng.run(steps)
+    pos, vel, step = eng.read_state()
+    assert step == steps
+    assert np.max(np.abs(pos - c["pos"])) <= 1e-5
+    assert np.max(np.abs(vel - c["vel"])) <= 1e-3
+
+
+def test_graph_replay_equals_eager_and_is_deterministic(golden):
+    a, _, _ = _engine_for("traj_coil269", golden)
+    b, _, _ = _engine_for("traj_coil269", golden)
+    a.run(12)
+    b.run(12, graph_steps=4)
+    for x, y in zip(a.read_state()[:2], b.read_state()[:2]):
+        np.testing.assert_array_equal(x, y)
+
+
+def test_replica_sharding_bit_identical(golden):
+    full, _, _ = _engine_for("traj_tiny", golden, R=4)
+    full.run(6)
+    c = golden["md"].case("traj_tiny")
+    n, sseed, pseed, _, _ = (int(x) for x in c["meta"])
+    sysm = generate_system("coil", n, sseed)
+    params = init_params(ModelConfig(**json.loads(str(c["cfg"]))), pseed)
+    shard = MDEngine(params, sysm.types, sysm.masses, sysm.prior, 2, seed=9, rep_offset=2)
+    pos0 = np.repeat(sysm.positions[None], 2, axis=0).astype(np.float32)
+    shard.load_state(pos0, np.zeros_like(pos0), 0)
+    shard.evaluate()
+    shard.run(6)
+    np.testing.assert_array_equal(shard.read_state()[0], full.read_state()[0][2:4])
+
+
+def test_run_simulation_outputs(tmp_path, golden):
+    c = golden["md"].case("traj_tiny")
+    n, sseed, pseed, R, steps = (int(x) for x in c["meta"])
+    sysm = generate_system("coil", n, sseed)
+    params = init_params(ModelConfig(**json.loads(str(c["cfg"]))), pseed)
+    sim = P.SimConfig(dt_fs=4.0, temperature=300.0, friction=1.0, n_steps=steps, n_replicas=R,
+                      seed=9, output_stride=5)
+    res = P.run_simulation(params, sysm, sim, tmp_path)
+    assert np.max(np.abs(res.final_state.positions - c["pos"])) <= 1e-5
+    lines = res.scalars_path.read_text().splitlines()
+    ref_lines = str(c["scalars"]).splitlines()
+    assert lines[:2] == ref_lines[:2]
+    assert len(lines) == len(ref_lines)
+    for a, b in zip(lines[2:], ref_lines[2:]):
+        fa, fb = a.split(","), b.split(",")
+        assert fa[:2] == fb[:2]
+        for x, y in zip(fa[2:5], fb[2:5]):
+            assert abs(float(x) - float(y)) <= 1e-4 * max(1.0, abs(float(y)))
+    assert abs(res.mean_edges - float(c["mean_edges"])) <= 1e-9
+    frames = res.trajectory_path.read_text().count("step=")
+    assert frames == R * (steps // 5 + 1)
+    rep = P.throughput_report(res)
+    assert rep["ns_per_day"] > 0
+
+
+def test_capacity_overflow_regrows_and_matches(tmp_path, golden, monkeypatch):
+    c = golden["md"].case("traj_tiny")
+    n, sseed, pseed, R, steps = (int(x) for x in c["meta"])
+    sysm = generate_system("coil", n, sseed)
+    params = init_params(ModelConfig(**json.loads(str(c["cfg"]))), pseed)
+    # an engine whose capacity is below the edge count overflows on the first
+    # md_step; the status word must say so
+    eng, _, _ = _engine_for("traj_tiny", golden)
+    e0 = int(eng.csr.ptr[-1].item())
+    eng._alloc(e0 - 1)
+    eng.clear_flags()
+    eng.run(1)
+    assert eng.flags()["overflow"]
+    # run_simulation detects it inside a chunk, regrows and replays the chunk
+    orig = MDEngine.evaluate
+
+    def shrinking(self):
+        orig(self)
+        self._alloc(int(self.csr.ptr[-1].item()) - 1)
+
+    monkeypatch.setattr(MDEngine, "evaluate", shrinking)
+    sim = P.SimConfig(dt_fs=4.0, temperature=300.0, friction=1.0, n_steps=steps, n_replicas=R,
+                      seed=9, output_stride=5)
+    res = P.run_simulation(params, sysm, sim, tmp_path)
+    assert np.max(np.abs(res.final_state.positions - c["pos"])) <= 1e-5
+    monkeypatch.undo()
+    ref, _, _ = _engine_for("traj_tiny", golden)
+    ref.run(steps)
+    np.testing.assert_array_equal(res.final_state.positions, ref.read_state()[0])
+
+
+def test_blowup_detected(tmp_path):
+    sysm = generate_system("coil", 4, 1)
+    sysm.prior = P.PriorSpec(bonds=np.array([[0, 1]]), spring_k=np.array([1e12]),
+                             rest_length=np.array([3.9]))
+    params = init_params(ModelConfig(hidden_dim=8, rbf_dim=4, num_blocks=1, cutoff=1.2,
+                                     num_atom_types=8, filter_hidden_dim=8,
+                                     readout_hidden_dim=4), 6)
+    sim = P.SimConfig(dt_fs=100.0, n_steps=50, n_replicas=1, seed=0)
+    with pytest.raises(P.SimulationBlowupError):
+        P.run_simulation(params, sysm, sim, tmp_path)
+    assert (tmp_path / "blowup.xyz").exists()
+
+
+def test_force_provider_protocol(golden):
+    """GpuReplicaForces drops into the integrate() force_fn protocol."""
+    c = golden["md"].case("traj_tiny")
+    n, sseed, pseed, R, steps = (int(x) for x in c["meta"])
+    sysm = generate_system("coil", n, sseed)
+    params = init_params(ModelConfig(**json.loads(str(c["cfg"]))), pseed)
+    sim = P.SimConfig(dt_fs=4.0, n_steps=steps, n_replicas=R, seed=9)
+    fn = P.GpuReplicaForces(params, sysm.types, sysm.prior, sim)
+    pos0 = np.repeat(sysm.positions[None], R, axis=0).astype(np.float32)
+    st = P.SimState(positions=pos0, velocities=np.zeros_like(pos0), masses=sysm.masses)
+    out = P.integrate(fn, st, sim)
+    assert out.step == steps
+    assert np.max(np.abs(out.positions - c["pos"])) <= 1e-5
+    assert len(fn.edge_counts) == R * (steps + 1)
