@@ -169,6 +169,7 @@ class MDEngine:
                                        self.R, self.N, v(c.ptr), v(c.nbr), v(c.rev), v(c.own),
                                        c.cap_e, v(per_atom), v(self.potential), v(self.forces),
                                        v(ws_ef), ef, self.stream()), "fcg_energy_forces")
+        self.model_forces = self.forces.clone()
         self.forces.add_(f_prior)  # out.forces + f_prior, md.py:266
         self.per_atom = per_atom
 
