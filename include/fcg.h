@@ -87,6 +87,14 @@ typedef struct {
   /* FCG_FMT_W16 only (else NULL): fp16 stored weights (out,in) + scales   */
   const uint16_t *pre_h, *f0_h, *f1_h, *p0_h, *p1_h;
   const float *pre_s, *f0_s, *f1_s, *p0_s, *p1_s;
+  /* tcgen05 operand images of the filter MLP for the fused edge kernels:
+   * fp16, canonical no-swizzle core-matrix layout of the (out, in) matrix
+   * (element (r,c) at ((r/8)*(in/8) + c/8)*64 + (r%8)*8 + c%8), the "hi"
+   * image followed by the "lo" image.  FCG_FMT_FP32: hi+lo = W * 2^exp
+   * to ~22 bits; FCG_FMT_W16: hi = stored fp16 weights, lo = 0, exp = 0
+   * (the per-row scales *_s are applied in the epilogue). */
+  const uint16_t *f0_img, *f1_img; /* [2][D][DR], [2][D][D] */
+  int f0_exp, f1_exp;
 } fcg_block;
 
 typedef struct {
@@ -235,6 +243,14 @@ int fcg_md_step(const fcg_model *m, const fcg_prior *pr,
                 float *forces, float *potential, float *prior,
                 int32_t *ptr, int32_t *nbr, int32_t *rev, int32_t *own,
                 int64_t *status, void *ws, size_t ws_bytes, void *stream);
+
+/* Diagnostics: tcgen05 (kind::f16) GEMM self-test.  dump[128][N] receives
+ * the raw TMEM accumulator lanes of D = A * B^T for A[M][K], B[N][K] fp16
+ * staged in the canonical no-swizzle core-matrix layout (K-major or
+ * MN-major, two core orders, LBO/SBO assignment optionally swapped). */
+int fcg_selftest_mma(const uint16_t *A, const uint16_t *B, float *dump, int M,
+                     int N, int K, int a_mn, int a_order, int a_swap, int b_mn,
+                     int b_order, int b_swap, void *stream);
 
 #ifdef __cplusplus
 }

@@ -29,7 +29,8 @@ class FcgBlock(C.Structure):
         "pre_w", "pre_wt", "pre_b", "f0_w", "f0_wt", "f0_b", "f1_w", "f1_wt", "f1_b",
         "p0_w", "p0_wt", "p0_b", "p1_w", "p1_wt", "p1_b")] + \
         [(n, _u16) for n in ("pre_h", "f0_h", "f1_h", "p0_h", "p1_h")] + \
-        [(n, _f) for n in ("pre_s", "f0_s", "f1_s", "p0_s", "p1_s")]
+        [(n, _f) for n in ("pre_s", "f0_s", "f1_s", "p0_s", "p1_s")] + \
+        [("f0_img", _u16), ("f1_img", _u16), ("f0_exp", C.c_int), ("f1_exp", C.c_int)]
 
 
 class FcgModel(C.Structure):
@@ -78,6 +79,8 @@ _SIGS = {
                                     _VP, _VP, _VP]),
     "fcg_half_kick": (C.c_int, [C.POINTER(FcgMdParams), _VP, C.c_int, C.c_int, _VP, _VP, _VP]),
     "fcg_prior_forces": (C.c_int, [C.POINTER(FcgPrior), _VP, C.c_int, C.c_int, _VP, _VP, _VP]),
+    "fcg_selftest_mma": (C.c_int, [_VP, _VP, _VP, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                   C.c_int, C.c_int, C.c_int, C.c_int, _VP]),
     "fcg_md_workspace_bytes": (C.c_size_t, [C.POINTER(FcgModel), C.c_int, C.c_int, C.c_int64]),
     "fcg_md_step": (C.c_int, [C.POINTER(FcgModel), C.POINTER(FcgPrior), C.POINTER(FcgMdParams),
                               _VP, _VP, C.c_int, C.c_int, C.c_double, C.c_int64, _VP, _VP, _VP,

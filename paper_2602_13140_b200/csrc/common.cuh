@@ -68,6 +68,18 @@ __device__ __forceinline__ void cta_row_range(const int32_t *ptr, int nrows, lon
   if (re > nrows) re = nrows;
 }
 
+// Arguments shared by the fused edge kernels (SIMT and tcgen05).
+struct EdgeArgs {
+  const float *pos;
+  const int32_t *ptr, *nbr, *own;
+  int nrows;
+  int64_t cap_e;
+  float cutoff, gamma;
+  const float *centers;
+  fcg_block blk;
+  int quant;
+};
+
 }  // namespace fcg
 
 // ---- built-in kernel profiler (CUDA events per kernel class) -----------------
@@ -125,4 +137,9 @@ int half_kick(const fcg_md_params *p, const float *mass, int R, int N, const flo
 int prior_forces(const fcg_prior *pr, const float *pos, int R, int N, float *e_prior,
                  float *f_prior, cudaStream_t s);
 int step_advance(int64_t *step, cudaStream_t s);
+// edge_tc.cu
+void edge_tc_configure();
+void launch_edge_fwd_tc(const EdgeArgs &a, const float *P, float *H, int grid, cudaStream_t s);
+void launch_edge_bwd_tc(const EdgeArgs &a, const float *P, const float *GH, float *GP,
+                        float4 *gsum, int accumulate, int grid, cudaStream_t s);
 }  // namespace fcg

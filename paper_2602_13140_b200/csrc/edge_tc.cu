@@ -1,0 +1,585 @@
+// (b)(c)(d) Fused edge passes on the 5th-generation tensor cores.
+//
+// Same contract as the fused edge loop of the reference (flash.py:215-236
+// forward, :272-295 backward) — edge tensors never reach HBM — but the four
+// per-edge filter-MLP GEMMs run as tcgen05.mma (kind::f16, fp32 accumulate
+// in TMEM) over 128-edge tiles.
+//
+// Formulation ("transposed"): D[channel][edge] = W[channel][k] * X[k][edge].
+//   A = weights, resident in SMEM for the whole kernel (K-major in the
+//       forward; the SAME bytes read MN-major give W^T for the backward);
+//   B = per-tile edge activations written by the epilogue threads
+//       (MN-major: row = channel, 128 contiguous edges);
+//   D = TMEM, lane = channel, column = edge.
+// Every epilogue thread therefore owns one channel across consecutive edges,
+// so the destination (forward) / source (backward) segment reduction is a
+// running sum in one thread with a single store per CSR row — no atomics.
+//
+// fp32 parity (SURVEY §7 hard part 2): plain fp16/TF32 operands lose ~1e-3;
+// we split both operands as x*2^s = hi + lo (fp16 each, ~22 significant
+// bits) and accumulate hi*hi + hi*lo + lo*hi.  Weights carry a host-chosen
+// power-of-two prescale; activations get a per-tile power-of-two scale from
+// a block max, removed exactly in the epilogue.  W16 weights (quantize.py)
+// use the stored fp16 weights directly: one MMA in the forward (inputs
+// rounded to fp16 as the reference does), two in the backward.
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+#include "tc.cuh"
+
+namespace fcg {
+
+constexpr int TT = 128;          // edges per tile (MMA N)
+constexpr int TC_THREADS = 256;  // 8 warps: two per TMEM lane quarter
+constexpr uint32_t SM_W0 = 0;          // W0 hi|lo: 2 x 128x64 fp16
+constexpr uint32_t SM_W1 = 32768;      // W1 hi|lo: 2 x 128x128 fp16
+constexpr uint32_t SM_ACT = 98304;     // B operand hi|lo (<= 2 x 128x128 fp16) / scratch
+constexpr uint32_t SM_META = 163840;
+constexpr uint32_t W0_BYTES = 128 * 64 * 2, W1_BYTES = 128 * 128 * 2;
+constexpr uint32_t TM_D0 = 0, TM_D1 = 128, TM_D2 = 256, TM_D3 = 384;
+constexpr int RED_LD = 65;       // padded stride of the [edge][k] fp32 scratch
+
+struct TcMeta {
+  int own[TT], nbr[TT];
+  float d[TT], env[TT], denv[TT];
+  float4 u[TT];
+  unsigned int amax[4];
+  uint64_t bar;
+  uint32_t tmem;
+};
+constexpr uint32_t SM_TOTAL = SM_META + sizeof(TcMeta);
+
+__device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }
+
+// Power-of-two scale s with max*2^s in [2^14, 2^15); 1 for an all-zero tile.
+__device__ __forceinline__ int scale_exp(float m) {
+  if (!(m > 0.f) || !isfinite(m)) return 0;
+  int e;
+  frexpf(m, &e);  // m = f * 2^e, f in [0.5, 1)
+  return 15 - e;
+}
+
+// Block-wide max of non-negative values (all TC_THREADS threads call it).
+__device__ __forceinline__ float block_amax(float v, unsigned int *slot) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(slot, __float_as_uint(v));
+  __syncthreads();
+  return __uint_as_float(*slot);
+}
+
+// Store 8 consecutive edges e0..e0+7 of K-row r of an MN-major B operand
+// (hi image at act, lo image at act + K*256 bytes), values pre-scaled.
+__device__ __forceinline__ void put_b8(uint8_t *act, int K, int r, int e0, const float *v,
+                                       float scale, bool with_lo) {
+  uint32_t off = (uint32_t)(r >> 3) * 2048u + (uint32_t)(e0 >> 3) * 128u + (uint32_t)(r & 7) * 16u;
+  __half2 hi[4], lo[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float a = v[2 * i] * scale, b = v[2 * i + 1] * scale;
+    hi[i] = __floats2half2_rn(a, b);
+    float2 hf = __half22float2(hi[i]);
+    lo[i] = __floats2half2_rn(a - hf.x, b - hf.y);
+  }
+  *(uint4 *)(act + off) = *(uint4 *)hi;
+  if (with_lo) *(uint4 *)(act + (uint32_t)K * 256u + off) = *(uint4 *)lo;
+}
+
+// Descriptors (SWIZZLE_NONE, LBO = core stride along K, SBO = along M/N).
+__device__ __forceinline__ uint64_t desc_w_kmajor(uint32_t base, int in_dim, int k0) {
+  return tc::smem_desc(base + (uint32_t)(k0 >> 3) * 128u, 128u, (uint32_t)(in_dim >> 3) * 128u);
+}
+__device__ __forceinline__ uint64_t desc_w_mnmajor(uint32_t base, int in_dim, int k0) {
+  uint32_t rowstride = (uint32_t)(in_dim >> 3) * 128u;
+  return tc::smem_desc(base + (uint32_t)(k0 >> 3) * rowstride, rowstride, 128u);
+}
+__device__ __forceinline__ uint64_t desc_act(uint32_t base, int k0) {
+  return tc::smem_desc(base + (uint32_t)(k0 >> 3) * 2048u, 2048u, 128u);
+}
+
+// Issue one GEMM D(tmem) = A(weights) x B(act) over K, with the product set
+// {hi*hi, hi*lo, lo*hi} (nprod=3), {hi*hi, hi*lo} (2) or {hi*hi} (1).
+__device__ __forceinline__ void issue_gemm(uint32_t d, uint32_t w_base, uint32_t w_lo_off,
+                                           int in_dim, bool w_mn, uint32_t act_base, int K,
+                                           uint32_t idesc, int nprod) {
+  uint32_t act_lo = act_base + (uint32_t)K * 256u;
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    uint64_t ah = w_mn ? desc_w_mnmajor(w_base, in_dim, k0) : desc_w_kmajor(w_base, in_dim, k0);
+    uint64_t bh = desc_act(act_base, k0);
+    tc::mma_f16_ss(d, ah, bh, idesc, k0 > 0);
+    if (nprod >= 2) tc::mma_f16_ss(d, ah, desc_act(act_lo, k0), idesc, 1);
+    if (nprod >= 3) {
+      uint64_t al = w_mn ? desc_w_mnmajor(w_base + w_lo_off, in_dim, k0)
+                         : desc_w_kmajor(w_base + w_lo_off, in_dim, k0);
+      tc::mma_f16_ss(d, al, bh, idesc, 1);
+    }
+  }
+}
+
+struct Reducer {  // running CSR segment sum of one channel (single writer per row)
+  int cur;
+  float acc;
+  __device__ __forceinline__ void add(int row, float v, int c, float *__restrict__ out) {
+    if (row != cur) {
+      out[(size_t)cur * D + c] = acc;
+      for (int z = cur + 1; z < row; ++z) out[(size_t)z * D + c] = 0.f;
+      cur = row;
+      acc = 0.f;
+    }
+    acc += v;
+  }
+  __device__ __forceinline__ void finish(int re, int c, float *__restrict__ out) {
+    if (cur < re) {
+      out[(size_t)cur * D + c] = acc;
+      for (int z = cur + 1; z < re; ++z) out[(size_t)z * D + c] = 0.f;
+    }
+  }
+};
+
+__device__ __forceinline__ void envelope2(float d, float cutoff, float &c, float &dc) {
+  if (d < cutoff) {
+    float sn, cs;
+    sincosf((3.14159265358979f * d) / cutoff, &sn, &cs);
+    c = 0.5f * (cs + 1.f);
+    dc = (float)(-0.5 * 3.141592653589793 / (double)cutoff) * sn;
+  } else {
+    c = 0.f;
+    dc = 0.f;
+  }
+}
+
+// ---- shared prologue pieces ----------------------------------------------
+__device__ __forceinline__ void stage_weights(uint8_t *sm, const fcg_block &b) {
+  const uint4 *s0 = (const uint4 *)b.f0_img, *s1 = (const uint4 *)b.f1_img;
+  uint4 *d0 = (uint4 *)(sm + SM_W0), *d1 = (uint4 *)(sm + SM_W1);
+  for (int q = threadIdx.x; q < (int)(2 * W0_BYTES / 16); q += TC_THREADS) d0[q] = __ldg(s0 + q);
+  for (int q = threadIdx.x; q < (int)(2 * W1_BYTES / 16); q += TC_THREADS) d1[q] = __ldg(s1 + q);
+}
+
+__device__ __forceinline__ void tile_meta(const EdgeArgs &a, TcMeta *m, int t0, int n_e,
+                                          bool src_owned) {
+  int t = threadIdx.x;
+  if (t < TT) {
+    int o = -1, n = 0;
+    float d = 0.f, c = 0.f, dc = 0.f;
+    float4 u = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (t < n_e) {
+      o = a.own[t0 + t];
+      n = a.nbr[t0 + t];
+      const float *po = a.pos + (size_t)o * 3, *pn = a.pos + (size_t)n * 3;
+      float ux = __fsub_rn(po[0], pn[0]), uy = __fsub_rn(po[1], pn[1]), uz = __fsub_rn(po[2], pn[2]);
+      if (src_owned) { ux = -ux; uy = -uy; uz = -uz; }
+      d = __fsqrt_rn(__fadd_rn(__fadd_rn(__fmul_rn(ux, ux), __fmul_rn(uy, uy)), __fmul_rn(uz, uz)));
+      u = make_float4(ux, uy, uz, 0.f);
+      envelope2(d, a.cutoff, c, dc);
+    }
+    m->own[t] = o;
+    m->nbr[t] = n;
+    m->d[t] = d;
+    m->env[t] = c;
+    m->denv[t] = dc;
+    m->u[t] = u;
+  }
+  if (t < 4) m->amax[t] = 0u;
+}
+
+// Basis b[k][e] (model.py:255-265) as the K=64 B operand: fp32 path scaled by
+// 2^14 and split; W16 path rounded to fp16 unscaled (quantize.py:68-71).
+__device__ __forceinline__ void tile_basis_tc(const EdgeArgs &a, const TcMeta *m, int n_e,
+                                              uint8_t *act, bool quant) {
+  for (int q = threadIdx.x; q < DR * (TT / 8); q += TC_THREADS) {
+    int k = q % DR, e0 = (q / DR) * 8;
+    float mu = __ldg(&a.centers[k]);
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      int e = e0 + i;
+      float dl = m->d[e] - mu;
+      v[i] = e < n_e ? __expf((-a.gamma * dl) * dl) * m->env[e] : 0.f;
+    }
+    put_b8(act, DR, k, e0, v, quant ? 1.f : 16384.f, !quant);
+  }
+}
+
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, float (&v)[64]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    float t[16];
+    tc::tmem_ld16(taddr + 16 * c, t);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[16 * c + i] = t[i];
+  }
+  tc::tmem_ld_wait();
+}
+
+// ---------------------------------------------------------------------------
+// Forward: per 128-edge tile of dst rows
+//   b -> [GEMM1] z0 -> h=ssp(z0) -> [GEMM2] w -> m = P[src]*w -> H rows.
+__global__ void __launch_bounds__(TC_THREADS, 1)
+k_edge_fwd_tc(const EdgeArgs a, const float *__restrict__ P, float *__restrict__ H) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  TcMeta *meta = (TcMeta *)(sm + SM_META);
+  uint8_t *act = sm + SM_ACT;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int quarter = warp & 3, half = warp >> 2;
+  const int ch = 32 * quarter + lane;
+  const bool quant = a.quant != 0;
+  const fcg_block &B = a.blk;
+
+  stage_weights(sm, B);
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&meta->bar, 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc<512>(&meta->tmem);
+  tc::fence_async_smem();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tm = meta->tmem;
+  const uint32_t lane_off = (uint32_t)(32 * quarter) << 16;
+  const uint32_t sbase = tc::smem_u32(sm);
+  const uint32_t idesc = tc::idesc_f16(128, TT, 0, 1);
+  const int nprod = quant ? 1 : 3;
+  uint32_t phase = 0;
+
+  const int e_tot = a.ptr[a.nrows];
+  const long long eff = e_tot > a.cap_e ? a.cap_e : e_tot;
+  int rbeg, rend;
+  cta_row_range(a.ptr, a.nrows, eff, blockIdx.x, gridDim.x, rbeg, rend);
+  int eb = a.ptr[rbeg], ee = a.ptr[rend];
+  if (ee > eff) ee = (int)eff;
+  if (eb > ee) eb = ee;
+  Reducer red{rbeg, 0.f};
+
+  // per-channel epilogue constants
+  const float b0c = __ldg(&B.f0_b[ch]), b1c = __ldg(&B.f1_b[ch]);
+  const float rs0 = quant ? __ldg(&B.f0_s[ch]) : pow2f(-(B.f0_exp + 14));
+  const float rs1 = quant ? __ldg(&B.f1_s[ch]) : 1.f;
+
+  for (int t0 = eb; t0 < ee; t0 += TT) {
+    const int n_e = min(TT, ee - t0);
+    tile_meta(a, meta, t0, n_e, false);
+    __syncthreads();
+    tile_basis_tc(a, meta, n_e, act, quant);
+    tc::fence_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tc::fence_after_sync();
+      issue_gemm(tm + TM_D0, sbase + SM_W0, W0_BYTES, DR, false, sbase + SM_ACT, DR, idesc,
+                 nprod);
+      tc::mma_commit(&meta->bar);
+    }
+    tc::mbar_wait(&meta->bar, phase);
+    phase ^= 1;
+    tc::fence_after_sync();
+
+    // epilogue 1: h = ssp(W0 b + b0) -> B operand of GEMM2
+    float v[64];
+    tmem_ld64(tm + TM_D0 + lane_off + 64 * half, v);
+    float mx = 0.f;
+#pragma unroll
+    for (int i = 0; i < 64; ++i) {
+      int e = 64 * half + i;
+      float h = ssp(v[i] * rs0 + b0c);
+      if (quant) h = __half2float(__float2half_rn(h));
+      v[i] = e < n_e ? h : 0.f;
+      mx = fmaxf(mx, fabsf(v[i]));
+    }
+    int sh = 0;
+    if (!quant) sh = scale_exp(block_amax(mx, &meta->amax[0]));
+    const float scale_h = pow2f(sh);
+#pragma unroll
+    for (int g = 0; g < 8; ++g) put_b8(act, D, ch, 64 * half + 8 * g, &v[8 * g], scale_h, !quant);
+    tc::fence_async_smem();
+    tc::fence_before_sync();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tc::fence_after_sync();
+      issue_gemm(tm + TM_D1, sbase + SM_W1, W1_BYTES, D, false, sbase + SM_ACT, D, idesc, nprod);
+      tc::mma_commit(&meta->bar);
+    }
+    tc::mbar_wait(&meta->bar, phase);
+    phase ^= 1;
+    tc::fence_after_sync();
+
+    // epilogue 2 (one warp per lane quarter, all 128 edges): m = w * P[src],
+    // running segment sums into H (flash.py:229-234)
+    if (warp < 4) {
+      const float s1 = quant ? rs1 : pow2f(-(B.f1_exp + sh));
+#pragma unroll 1
+      for (int c0 = 0; c0 < TT; c0 += 16) {
+        float w[16], pv[16];
+        tc::tmem_ld16(tm + TM_D1 + lane_off + c0, w);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) pv[i] = __ldg(&P[(size_t)meta->nbr[c0 + i] * D + ch]);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          int e = c0 + i;
+          if (e < n_e) red.add(meta->own[e], (w[i] * s1 + b1c) * pv[i], ch, H);
+        }
+      }
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+  }
+  if (warp < 4) red.finish(rend, ch, H);
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<512>(tm);
+}
+
+// ---------------------------------------------------------------------------
+// Backward over src-owned rows (flash_block_backward, flash.py:272-295):
+//   b -> [G1] z0 -> h -> [G2] w;  gH = GH[dst], grad_w = gH*P[src] ->
+//   [G3] grad_h = grad_w W1 -> gz = grad_h*ssp'(z0) -> [G4] grad_b = gz W0
+//   -> grad_d = sum_k grad_b*db -> g_e = grad_d/d * u  (gsum, owner slot);
+//   grad_P rows = src-segment sums of gH*w.
+__global__ void __launch_bounds__(TC_THREADS, 1)
+k_edge_bwd_tc(const EdgeArgs a, const float *__restrict__ P, const float *__restrict__ GH,
+              float *__restrict__ GP, float4 *__restrict__ gsum, int accumulate) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  TcMeta *meta = (TcMeta *)(sm + SM_META);
+  uint8_t *act = sm + SM_ACT;
+  float *red_s = (float *)(sm + SM_ACT);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int quarter = warp & 3, half = warp >> 2;
+  const int ch = 32 * quarter + lane;
+  const bool quant = a.quant != 0;
+  const fcg_block &B = a.blk;
+
+  stage_weights(sm, B);
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&meta->bar, 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc<512>(&meta->tmem);
+  tc::fence_async_smem();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tm = meta->tmem;
+  const uint32_t lane_off = (uint32_t)(32 * quarter) << 16;
+  const uint32_t sbase = tc::smem_u32(sm);
+  const uint32_t idesc_fwd = tc::idesc_f16(128, TT, 0, 1);
+  const uint32_t idesc_g3 = tc::idesc_f16(128, TT, 1, 1);
+  const uint32_t idesc_g4 = tc::idesc_f16(64, TT, 1, 1);
+  const int nprod_f = quant ? 1 : 3, nprod_b = quant ? 2 : 3;
+  uint32_t phase = 0;
+
+  const int e_tot = a.ptr[a.nrows];
+  const long long eff = e_tot > a.cap_e ? a.cap_e : e_tot;
+  int rbeg, rend;
+  cta_row_range(a.ptr, a.nrows, eff, blockIdx.x, gridDim.x, rbeg, rend);
+  int eb = a.ptr[rbeg], ee = a.ptr[rend];
+  if (ee > eff) ee = (int)eff;
+  if (eb > ee) eb = ee;
+  Reducer red{rbeg, 0.f};
+
+  const float b0c = __ldg(&B.f0_b[ch]), b1c = __ldg(&B.f1_b[ch]);
+  const float rs0 = quant ? __ldg(&B.f0_s[ch]) : pow2f(-(B.f0_exp + 14));
+  const float rs1 = quant ? __ldg(&B.f1_s[ch]) : 1.f;
+  // backward GEMMs against the stored fp16 weights fold the W16 dequant
+  // scale into the operand: g @ (s*w16) == (g*s) @ w16
+  const float q1 = quant ? __ldg(&B.f1_s[ch]) : 1.f;
+  const float q0 = quant ? __ldg(&B.f0_s[ch]) : 1.f;
+  const int ew0 = quant ? 0 : B.f0_exp, ew1 = quant ? 0 : B.f1_exp;
+
+  for (int t0 = eb; t0 < ee; t0 += TT) {
+    const int n_e = min(TT, ee - t0);
+    tile_meta(a, meta, t0, n_e, true);
+    __syncthreads();
+    tile_basis_tc(a, meta, n_e, act, quant);
+    tc::fence_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tc::fence_after_sync();
+      issue_gemm(tm + TM_D0, sbase + SM_W0, W0_BYTES, DR, false, sbase + SM_ACT, DR, idesc_fwd,
+                 nprod_f);
+      tc::mma_commit(&meta->bar);
+    }
+    tc::mbar_wait(&meta->bar, phase);
+    phase ^= 1;
+    tc::fence_after_sync();
+
+    // recompute h = ssp(z0); z0 stays in TMEM (D0) for ssp'(z0) later
+    float v[64];
+    tmem_ld64(tm + TM_D0 + lane_off + 64 * half, v);
+    float mx = 0.f;
+#pragma unroll
+    for (int i = 0; i < 64; ++i) {
+      int e = 64 * half + i;
+      float h = ssp(v[i] * rs0 + b0c);
+      if (quant) h = __half2float(__float2half_rn(h));
+      v[i] = e < n_e ? h : 0.f;
+      mx = fmaxf(mx, fabsf(v[i]));
+    }
+    int sh = 0;
+    if (!quant) sh = scale_exp(block_amax(mx, &meta->amax[0]));
+    float sc = pow2f(sh);
+#pragma unroll
+    for (int g = 0; g < 8; ++g) put_b8(act, D, ch, 64 * half + 8 * g, &v[8 * g], sc, !quant);
+    tc::fence_async_smem();
+    tc::fence_before_sync();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tc::fence_after_sync();
+      issue_gemm(tm + TM_D1, sbase + SM_W1, W1_BYTES, D, false, sbase + SM_ACT, D, idesc_fwd,
+                 nprod_f);
+      tc::mma_commit(&meta->bar);
+    }
+    tc::mbar_wait(&meta->bar, phase);
+    phase ^= 1;
+    tc::fence_after_sync();
+
+    // grad_w[c][e] = gH[e][c] * P[src][c] (flash.py:291) -> B operand of G3
+    const float s1 = quant ? rs1 : pow2f(-(B.f1_exp + sh));
+    {
+      float gw[64];
+      mx = 0.f;
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        int e = 64 * half + i;
+        float g = 0.f;
+        if (e < n_e)
+          g = __ldg(&GH[(size_t)meta->nbr[e] * D + ch]) * __ldg(&P[(size_t)meta->own[e] * D + ch]);
+        gw[i] = g * q1;
+        mx = fmaxf(mx, fabsf(gw[i]));
+      }
+      int sg = scale_exp(block_amax(mx, &meta->amax[1]));
+      sc = pow2f(sg);
+#pragma unroll
+      for (int g = 0; g < 8; ++g) put_b8(act, D, ch, 64 * half + 8 * g, &gw[8 * g], sc, true);
+      tc::fence_async_smem();
+      tc::fence_before_sync();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        tc::fence_after_sync();
+        issue_gemm(tm + TM_D2, sbase + SM_W1, W1_BYTES, D, true, sbase + SM_ACT, D, idesc_g3,
+                   nprod_b);
+        tc::mma_commit(&meta->bar);
+      }
+      sh = sg;  // remember for unscaling D2
+    }
+    // while G3 runs: grad_P rows = src-segment sums of gH * w (flash.py:283-288)
+    if (warp < 4) {
+#pragma unroll 1
+      for (int c0 = 0; c0 < TT; c0 += 16) {
+        float w[16], gv[16];
+        tc::tmem_ld16(tm + TM_D1 + lane_off + c0, w);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) gv[i] = __ldg(&GH[(size_t)meta->nbr[c0 + i] * D + ch]);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          int e = c0 + i;
+          if (e < n_e) red.add(meta->own[e], gv[i] * (w[i] * s1 + b1c), ch, GP);
+        }
+      }
+    }
+    tc::mbar_wait(&meta->bar, phase);
+    phase ^= 1;
+    tc::fence_after_sync();
+
+    // gz = grad_h * ssp'(z0) (mlp_backward_input, model.py:326-331) -> B of G4
+    {
+      float gh[64];
+      tmem_ld64(tm + TM_D2 + lane_off + 64 * half, gh);
+      tmem_ld64(tm + TM_D0 + lane_off + 64 * half, v);
+      const float sg3 = pow2f(-(ew1 + sh));
+      mx = 0.f;
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        int e = 64 * half + i;
+        float z0 = v[i] * rs0 + b0c;
+        float g = e < n_e ? gh[i] * sg3 * ssp_grad(z0) * q0 : 0.f;
+        gh[i] = g;
+        mx = fmaxf(mx, fabsf(g));
+      }
+      int sz = scale_exp(block_amax(mx, &meta->amax[2]));
+      sc = pow2f(sz);
+#pragma unroll
+      for (int g = 0; g < 8; ++g) put_b8(act, D, ch, 64 * half + 8 * g, &gh[8 * g], sc, true);
+      tc::fence_async_smem();
+      tc::fence_before_sync();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        tc::fence_after_sync();
+        issue_gemm(tm + TM_D3, sbase + SM_W0, W0_BYTES, DR, true, sbase + SM_ACT, D, idesc_g4,
+                   nprod_b);
+        tc::mma_commit(&meta->bar);
+      }
+      sh = sz;
+    }
+    tc::mbar_wait(&meta->bar, phase);
+    phase ^= 1;
+    tc::fence_after_sync();
+
+    // grad_d[e] = sum_k grad_b[k][e] * db[k][e] (flash.py:293).  M=64 D lives
+    // in lanes 32q + (0..15) of each quarter: row k = 16q + lane.
+    {
+      float gb[64];
+      tmem_ld64(tm + TM_D3 + lane_off + 64 * half, gb);
+      if (lane < 16) {
+        const int k = 16 * quarter + lane;
+        const float mu = __ldg(&a.centers[k]);
+        const float s4 = pow2f(-(ew0 + sh));
+        const float g2 = -2.f * a.gamma;
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+          int e = 64 * half + i;
+          float dl = meta->d[e] - mu;
+          float gs = __expf((-a.gamma * dl) * dl);
+          float db = gs * (g2 * dl * meta->env[e] + meta->denv[e]);
+          red_s[e * RED_LD + k] = gb[i] * s4 * db;
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < TT && threadIdx.x < n_e) {
+      const int e = threadIdx.x;
+      float gd = 0.f;
+#pragma unroll 8
+      for (int k = 0; k < DR; ++k) gd += red_s[e * RED_LD + k];
+      float d = meta->d[e];
+      float inv = d > TINY_DISTANCE ? 1.f / d : 0.f;  // _safe_inv, flash.py:176-178
+      float s = gd * inv;
+      float4 u = meta->u[e];
+      float4 g = make_float4(s * u.x, s * u.y, s * u.z, 0.f);
+      float4 *dst = &gsum[t0 + e];
+      if (accumulate) {
+        float4 o = *dst;
+        g.x += o.x; g.y += o.y; g.z += o.z;
+      }
+      *dst = g;
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+  }
+  if (warp < 4) red.finish(rend, ch, GP);
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<512>(tm);
+}
+
+void edge_tc_configure() {
+  static bool done = false;
+  if (done) return;
+  cudaFuncSetAttribute(k_edge_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(SM_TOTAL + 1024));
+  cudaFuncSetAttribute(k_edge_bwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(SM_TOTAL + 1024));
+  done = true;
+}
+
+void launch_edge_fwd_tc(const EdgeArgs &a, const float *P, float *H, int grid, cudaStream_t s) {
+  k_edge_fwd_tc<<<grid, TC_THREADS, SM_TOTAL + 1024, s>>>(a, P, H);
+}
+
+void launch_edge_bwd_tc(const EdgeArgs &a, const float *P, const float *GH, float *GP,
+                        float4 *gsum, int accumulate, int grid, cudaStream_t s) {
+  k_edge_bwd_tc<<<grid, TC_THREADS, SM_TOTAL + 1024, s>>>(a, P, GH, GP, gsum, accumulate);
+}
+
+}  // namespace fcg

@@ -22,6 +22,7 @@
 // src segments (grad_P rows) — identical because the graph is symmetric and
 // the reference's src-grouped perm is the rev[] map.  No atomics.
 #include <cuda_fp16.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -262,17 +263,6 @@ k_readout(const float *__restrict__ X, const fcg_model m, float *__restrict__ pe
 
 // ---------------------------------------------------------------------------
 // edge kernels
-struct EdgeArgs {
-  const float *pos;
-  const int32_t *ptr, *nbr, *own;
-  int nrows;
-  int64_t cap_e;
-  float cutoff, gamma;
-  const float *centers;
-  fcg_block blk;
-  int quant;
-};
-
 // Envelope C(d) and C'(d) (model.py:242-252), fp32 as numpy evaluates them.
 __device__ __forceinline__ void envelope(float d, float cutoff, float &c, float &dc) {
   const float pi = 3.14159265358979f;
@@ -581,15 +571,27 @@ k_forces_finish(const int32_t *__restrict__ ptr, const int32_t *__restrict__ rev
 }
 
 // ---------------------------------------------------------------------------
-static int edge_grid() {
-  static int g = 0;
-  if (!g) {
-    int dev = 0, sms = 148;
+static int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    n = 148;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    g = sms * 2;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
   }
-  return g;
+  return n;
+}
+
+// Edge-kernel implementation: the tcgen05 kernels (edge_tc.cu) are the
+// product path; FCG_EDGE_IMPL=simt selects the fp32 FFMA kernels above as a
+// diagnostic A/B reference (same results within fp32 round-off).
+static bool use_simt_edges() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("FCG_EDGE_IMPL");
+    v = (e && e[0] == 's') ? 1 : 0;
+  }
+  return v == 1;
 }
 
 struct EfBuffers {
@@ -674,7 +676,9 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
   ea.cutoff = m->cutoff; ea.gamma = m->gamma; ea.centers = m->centers;
   const int quant = m->format == FCG_FMT_W16;
   ea.quant = quant;
-  const int eg = edge_grid();
+  const bool simt = use_simt_edges();
+  const int eg = simt ? 2 * sm_count() : sm_count();
+  if (!simt) edge_tc_configure();
 
   for (int t = 0; t < T; ++t) {
     const fcg_block &blk = m->blocks[t];
@@ -686,7 +690,10 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
     }
     {
       FCG_PROF(P_EDGE_FWD, s);
-      k_edge_fwd<<<eg, NT, (TE * LDR + TE * LDH) * sizeof(float), s>>>(ea, b.P[t], b.H);
+      if (simt)
+        k_edge_fwd<<<eg, NT, (TE * LDR + TE * LDH) * sizeof(float), s>>>(ea, b.P[t], b.H);
+      else
+        launch_edge_fwd_tc(ea, b.P[t], b.H, eg, s);
     }
     {
       FCG_PROF(P_NODE_POST, s);
@@ -707,8 +714,11 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
     }
     {
       FCG_PROF(P_EDGE_BWD, s);
-      k_edge_bwd<<<eg, NT, 3 * TE * LDH * sizeof(float), s>>>(ea, b.P[t], b.GH, b.GP, b.gsum,
-                                                             t != T - 1);
+      if (simt)
+        k_edge_bwd<<<eg, NT, 3 * TE * LDH * sizeof(float), s>>>(ea, b.P[t], b.GH, b.GP, b.gsum,
+                                                               t != T - 1);
+      else
+        launch_edge_bwd_tc(ea, b.P[t], b.GH, b.GP, b.gsum, t != T - 1, eg, s);
     }
     {
       FCG_PROF(P_NODE_PRE_BWD, s);

@@ -178,6 +178,30 @@ def _pad(a, shape):
     return out
 
 
+def core_matrix_image(w: np.ndarray) -> np.ndarray:
+    """(out, in) matrix -> flat canonical no-swizzle core-matrix order used by
+    the tcgen05 descriptors: 8x8 blocks of 128 bytes, row-block major."""
+    R, Cc = w.shape
+    assert R % 8 == 0 and Cc % 8 == 0
+    return np.ascontiguousarray(w.reshape(R // 8, 8, Cc // 8, 8).transpose(0, 2, 1, 3)).reshape(-1)
+
+
+def tc_image(w: np.ndarray, quantized_f16: np.ndarray | None = None):
+    """fp16 (hi, lo) operand image of a padded (out, in) weight matrix and its
+    power-of-two prescale exponent.  fp32 weights: W*2^e = hi + lo (~22-bit
+    split, max|W*2^e| <= 2^15).  W16 weights: hi = stored fp16, lo = 0."""
+    if quantized_f16 is not None:
+        hi = quantized_f16.astype(np.float16)
+        return np.concatenate([core_matrix_image(hi), np.zeros(hi.size, np.float16)]), 0
+    w = np.asarray(w, np.float32)
+    amax = float(np.max(np.abs(w))) if w.size else 0.0
+    e = 14 - int(np.floor(np.log2(amax))) if amax > 0 else 0
+    ws = (w.astype(np.float64) * 2.0 ** e).astype(np.float32)
+    hi = ws.astype(np.float16)
+    lo = (ws - hi.astype(np.float32)).astype(np.float16)
+    return np.concatenate([core_matrix_image(hi), core_matrix_image(lo)]), e
+
+
 def _is_quantized(params) -> bool:
     return not isinstance(params.readout, tuple)
 
@@ -233,7 +257,9 @@ class DeviceModel:
                 w16 = np.zeros((shape_out, shape_in), dtype=np.float16)
                 w16[:lin.weight.shape[0], :lin.weight.shape[1]] = lin.weight
                 setattr(blk, f"{name}_h", _lib.u16ptr(dev(w16.view(np.int16), torch.int16)))
-                setattr(blk, f"{name}_s", _lib.fptr(dev(_pad(lin.scale, (shape_out,)))))
+                sc = np.ones(shape_out, np.float32)
+                sc[:lin.scale.shape[0]] = lin.scale
+                setattr(blk, f"{name}_s", _lib.fptr(dev(sc)))
 
         for t, bp in enumerate(params.blocks):
             blk = m.blocks[t]
@@ -244,6 +270,15 @@ class DeviceModel:
             put(blk, "f1", f1, D, D)
             put(blk, "p0", p0, D, D)
             put(blk, "p1", p1, D, D)
+            for name, lin, shape in (("f0", f0, (D, DR)), ("f1", f1, (D, D))):
+                if isinstance(lin, tuple):
+                    img, e = tc_image(_pad(lin[0], shape))
+                else:
+                    q = np.zeros(shape, np.float16)
+                    q[:lin.weight.shape[0], :lin.weight.shape[1]] = lin.weight
+                    img, e = tc_image(None, q)
+                setattr(blk, f"{name}_img", _lib.u16ptr(dev(img.view(np.int16), torch.int16)))
+                setattr(blk, f"{name}_exp", e)
 
         r0, r1 = layers_of(params.readout)
         w0, b0 = dense(r0)
