@@ -44,6 +44,7 @@ struct TcMeta {
   float d[TT], env[TT], denv[TT];
   float4 u[TT];
   unsigned int amax[4];
+  float xch[3 * 128];  // half-1 -> half-0 segment boundary partials
   uint64_t bar;
   uint32_t tmem;
 };
@@ -103,6 +104,7 @@ __device__ __forceinline__ void issue_gemm(uint32_t d, uint32_t w_base, uint32_t
                                            int in_dim, bool w_mn, uint32_t act_base, int K,
                                            uint32_t idesc, int nprod) {
   uint32_t act_lo = act_base + (uint32_t)K * 256u;
+#pragma unroll 1
   for (int k0 = 0; k0 < K; k0 += 16) {
     uint64_t ah = w_mn ? desc_w_mnmajor(w_base, in_dim, k0) : desc_w_kmajor(w_base, in_dim, k0);
     uint64_t bh = desc_act(act_base, k0);
@@ -116,25 +118,75 @@ __device__ __forceinline__ void issue_gemm(uint32_t d, uint32_t w_base, uint32_t
   }
 }
 
-struct Reducer {  // running CSR segment sum of one channel (single writer per row)
-  int cur;
-  float acc;
-  __device__ __forceinline__ void add(int row, float v, int c, float *__restrict__ out) {
-    if (row != cur) {
-      out[(size_t)cur * D + c] = acc;
-      for (int z = cur + 1; z < row; ++z) out[(size_t)z * D + c] = 0.f;
-      cur = row;
+
+// ---- CSR segment sums across the two edge halves of a tile ------------------
+// Each (channel, half) thread feeds its 64 edges in order: runs that start
+// and end inside the half are complete and written directly (one store per
+// row, empty rows between them zeroed); the first and last run of the half
+// are handed to an ordered merge done by the half-0 thread.
+struct Runs {
+  int row, nruns;
+  float acc, head;
+  __device__ __forceinline__ void init() { row = -1; nruns = 0; acc = 0.f; head = 0.f; }
+  __device__ __forceinline__ void feed(int o, float v, int c, float *__restrict__ out) {
+    if (o != row) {
+      if (row >= 0) {
+        if (nruns == 0) head = acc; else out[(size_t)row * D + c] = acc;
+#pragma unroll 1
+        for (int z = row + 1; z < o; ++z) out[(size_t)z * D + c] = 0.f;
+        ++nruns;
+      }
+      row = o;
       acc = 0.f;
     }
     acc += v;
   }
-  __device__ __forceinline__ void finish(int re, int c, float *__restrict__ out) {
-    if (cur < re) {
-      out[(size_t)cur * D + c] = acc;
-      for (int z = cur + 1; z < re; ++z) out[(size_t)z * D + c] = 0.f;
+  // close: nruns = #runs, head = first run's partial, acc = last run's partial
+  __device__ __forceinline__ void close() {
+    if (row >= 0) {
+      if (nruns == 0) head = acc;
+      ++nruns;
     }
   }
 };
+
+// Ordered merge of one half's boundary runs into the open carry segment.
+__device__ __forceinline__ void merge_half(int &crow, float &cacc, int nruns, float head,
+                                           float tail, int head_row, int tail_row, int c,
+                                           float *__restrict__ out) {
+  if (nruns == 0) return;
+  if (head_row == crow) {
+    cacc += head;
+  } else {
+    out[(size_t)crow * D + c] = cacc;
+#pragma unroll 1
+    for (int z = crow + 1; z < head_row; ++z) out[(size_t)z * D + c] = 0.f;
+    crow = head_row;
+    cacc = head;
+  }
+  if (nruns > 1) {  // head run complete; rows up to the tail were written by the half
+    out[(size_t)crow * D + c] = cacc;
+    crow = tail_row;
+    cacc = tail;
+  }
+}
+
+__device__ __forceinline__ void finish_rows(int crow, float cacc, int rend, int c,
+                                            float *__restrict__ out) {
+  if (crow < rend) {
+    out[(size_t)crow * D + c] = cacc;
+#pragma unroll 1
+    for (int z = crow + 1; z < rend; ++z) out[(size_t)z * D + c] = 0.f;
+  }
+}
+
+// shifted softplus and its derivative with MUFU ex2/lg2/rcp (abs. error ~1e-7)
+__device__ __forceinline__ float ssp_fast(float x) {
+  return fmaxf(x, 0.f) + __logf(1.f + __expf(-fabsf(x))) - 0.6931471805599453f;
+}
+__device__ __forceinline__ float sigmoid_fast(float x) {
+  return __fdividef(1.f, 1.f + __expf(-x));
+}
 
 __device__ __forceinline__ void envelope2(float d, float cutoff, float &c, float &dc) {
   if (d < cutoff) {
@@ -201,20 +253,63 @@ __device__ __forceinline__ void tile_basis_tc(const EdgeArgs &a, const TcMeta *m
   }
 }
 
-__device__ __forceinline__ void tmem_ld64(uint32_t taddr, float (&v)[64]) {
+
+__device__ __forceinline__ uint32_t lane_base(int quarter) { return (uint32_t)(32 * quarter) << 16; }
+
+// The segment reduction of a [128 ch][128 e] tile held in TMEM columns
+// [col, col+128): both halves scan, half 1 publishes boundary partials,
+// half 0 merges them into the carry.  Called by all 256 threads.
+__device__ __forceinline__ void reduce_tile(uint32_t tcol, const TcMeta *meta, int n_e, int half,
+                                            int ch, float *xch, int &crow, float &cacc,
+                                            float *__restrict__ out) {
+  const int lo = 64 * half, hi = min(lo + 64, n_e);
+  Runs r;
+  r.init();
+#pragma unroll 1
+  for (int c0 = 0; c0 < 64; c0 += 16) {
+    float m[16];
+    tc::tmem_ld16(tcol + 64 * half + c0, m);
+    tc::tmem_ld_wait();
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    float t[16];
-    tc::tmem_ld16(taddr + 16 * c, t);
-#pragma unroll
-    for (int i = 0; i < 16; ++i) v[16 * c + i] = t[i];
+    for (int i = 0; i < 16; ++i) {
+      int e = lo + c0 + i;
+      if (e < hi) r.feed(meta->own[e], m[i], ch, out);
+    }
   }
-  tc::tmem_ld_wait();
+  r.close();
+  if (half == 1) {
+    xch[ch] = r.head;
+    xch[128 + ch] = r.acc;
+    xch[256 + ch] = __int_as_float(r.nruns);
+  }
+  __syncthreads();
+  if (half == 0) {
+    merge_half(crow, cacc, r.nruns, r.head, r.acc, meta->own[0], meta->own[max(hi - 1, 0)], ch,
+               out);
+    merge_half(crow, cacc, __float_as_int(xch[256 + ch]), xch[ch], xch[128 + ch], meta->own[64],
+               meta->own[max(n_e - 1, 64)], ch, out);
+  }
 }
 
-// ---------------------------------------------------------------------------
+// Write a [128 ch][64 e-half] fp32 TMEM block as the hi/lo fp16 B operand of
+// the next GEMM with scale 2^sexp (chunks of 16 edges).
+__device__ __forceinline__ void tmem_to_act(uint32_t tcol, uint8_t *act, int half, int ch,
+                                            float scale, bool with_lo) {
+#pragma unroll 1
+  for (int c0 = 0; c0 < 64; c0 += 16) {
+    float v[16];
+    tc::tmem_ld16(tcol + 64 * half + c0, v);
+    tc::tmem_ld_wait();
+    put_b8(act, D, ch, 64 * half + c0, &v[0], scale, with_lo);
+    put_b8(act, D, ch, 64 * half + c0 + 8, &v[8], scale, with_lo);
+  }
+}
+
 // Forward: per 128-edge tile of dst rows
 //   b -> [GEMM1] z0 -> h=ssp(z0) -> [GEMM2] w -> m = P[src]*w -> H rows.
+// The P[src] gather is issued right after GEMM1 so its latency hides under
+// the tensor-core work; h and m are staged back into TMEM so every epilogue
+// pass streams 16 columns at a time.
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_edge_fwd_tc(const EdgeArgs a, const float *__restrict__ P, float *__restrict__ H) {
   extern __shared__ __align__(1024) uint8_t sm[];
@@ -237,7 +332,7 @@ k_edge_fwd_tc(const EdgeArgs a, const float *__restrict__ P, float *__restrict__
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tm = meta->tmem;
-  const uint32_t lane_off = (uint32_t)(32 * quarter) << 16;
+  const uint32_t tl = tm + lane_base(quarter);
   const uint32_t sbase = tc::smem_u32(sm);
   const uint32_t idesc = tc::idesc_f16(128, TT, 0, 1);
   const int nprod = quant ? 1 : 3;
@@ -250,9 +345,9 @@ k_edge_fwd_tc(const EdgeArgs a, const float *__restrict__ P, float *__restrict__
   int eb = a.ptr[rbeg], ee = a.ptr[rend];
   if (ee > eff) ee = (int)eff;
   if (eb > ee) eb = ee;
-  Reducer red{rbeg, 0.f};
+  int crow = rbeg;
+  float cacc = 0.f;
 
-  // per-channel epilogue constants
   const float b0c = __ldg(&B.f0_b[ch]), b1c = __ldg(&B.f1_b[ch]);
   const float rs0 = quant ? __ldg(&B.f0_s[ch]) : pow2f(-(B.f0_exp + 14));
   const float rs1 = quant ? __ldg(&B.f1_s[ch]) : 1.f;
@@ -270,27 +365,33 @@ k_edge_fwd_tc(const EdgeArgs a, const float *__restrict__ P, float *__restrict__
                  nprod);
       tc::mma_commit(&meta->bar);
     }
+    float pv[64];  // P[src][ch] of this half's edges, in flight during the MMAs
+#pragma unroll
+    for (int i = 0; i < 64; ++i) pv[i] = __ldg(&P[(size_t)meta->nbr[64 * half + i] * D + ch]);
     tc::mbar_wait(&meta->bar, phase);
     phase ^= 1;
     tc::fence_after_sync();
 
-    // epilogue 1: h = ssp(W0 b + b0) -> B operand of GEMM2
-    float v[64];
-    tmem_ld64(tm + TM_D0 + lane_off + 64 * half, v);
+    // epilogue 1: h = ssp(W0 b + b0), staged in place in D0, then -> B of GEMM2
     float mx = 0.f;
+#pragma unroll 1
+    for (int c0 = 0; c0 < 64; c0 += 16) {
+      float v[16];
+      tc::tmem_ld16(tl + TM_D0 + 64 * half + c0, v);
+      tc::tmem_ld_wait();
 #pragma unroll
-    for (int i = 0; i < 64; ++i) {
-      int e = 64 * half + i;
-      float h = ssp(v[i] * rs0 + b0c);
-      if (quant) h = __half2float(__float2half_rn(h));
-      v[i] = e < n_e ? h : 0.f;
-      mx = fmaxf(mx, fabsf(v[i]));
+      for (int i = 0; i < 16; ++i) {
+        float h = ssp_fast(v[i] * rs0 + b0c);
+        if (quant) h = __half2float(__float2half_rn(h));
+        v[i] = (64 * half + c0 + i) < n_e ? h : 0.f;
+        mx = fmaxf(mx, fabsf(v[i]));
+      }
+      tc::tmem_st16(tl + TM_D0 + 64 * half + c0, v);
     }
+    tc::tmem_st_wait();
     int sh = 0;
     if (!quant) sh = scale_exp(block_amax(mx, &meta->amax[0]));
-    const float scale_h = pow2f(sh);
-#pragma unroll
-    for (int g = 0; g < 8; ++g) put_b8(act, D, ch, 64 * half + 8 * g, &v[8 * g], scale_h, !quant);
+    tmem_to_act(tl + TM_D0, act, half, ch, pow2f(sh), !quant);
     tc::fence_async_smem();
     tc::fence_before_sync();
     __syncthreads();
@@ -303,28 +404,24 @@ k_edge_fwd_tc(const EdgeArgs a, const float *__restrict__ P, float *__restrict__
     phase ^= 1;
     tc::fence_after_sync();
 
-    // epilogue 2 (one warp per lane quarter, all 128 edges): m = w * P[src],
-    // running segment sums into H (flash.py:229-234)
-    if (warp < 4) {
-      const float s1 = quant ? rs1 : pow2f(-(B.f1_exp + sh));
-#pragma unroll 1
-      for (int c0 = 0; c0 < TT; c0 += 16) {
-        float w[16], pv[16];
-        tc::tmem_ld16(tm + TM_D1 + lane_off + c0, w);
+    // epilogue 2: m = (W1 h + b1) * P[src] (flash.py:229), in place in D1,
+    // then dst segment sums (flash.py:232-234)
+    const float s1 = quant ? rs1 : pow2f(-(B.f1_exp + sh));
 #pragma unroll
-        for (int i = 0; i < 16; ++i) pv[i] = __ldg(&P[(size_t)meta->nbr[c0 + i] * D + ch]);
-        tc::tmem_ld_wait();
+    for (int c = 0; c < 4; ++c) {
+      float v[16];
+      tc::tmem_ld16(tl + TM_D1 + 64 * half + 16 * c, v);
+      tc::tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          int e = c0 + i;
-          if (e < n_e) red.add(meta->own[e], (w[i] * s1 + b1c) * pv[i], ch, H);
-        }
-      }
+      for (int i = 0; i < 16; ++i) v[i] = (v[i] * s1 + b1c) * pv[16 * c + i];
+      tc::tmem_st16(tl + TM_D1 + 64 * half + 16 * c, v);
     }
+    tc::tmem_st_wait();
+    reduce_tile(tl + TM_D1, meta, n_e, half, ch, meta->xch, crow, cacc, H);
     tc::fence_before_sync();
     __syncthreads();
   }
-  if (warp < 4) red.finish(rend, ch, H);
+  if (half == 0) finish_rows(crow, cacc, rend, ch, H);
   tc::fence_before_sync();
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc<512>(tm);
@@ -335,7 +432,9 @@ k_edge_fwd_tc(const EdgeArgs a, const float *__restrict__ P, float *__restrict__
 //   b -> [G1] z0 -> h -> [G2] w;  gH = GH[dst], grad_w = gH*P[src] ->
 //   [G3] grad_h = grad_w W1 -> gz = grad_h*ssp'(z0) -> [G4] grad_b = gz W0
 //   -> grad_d = sum_k grad_b*db -> g_e = grad_d/d * u  (gsum, owner slot);
-//   grad_P rows = src-segment sums of gH*w.
+//   grad_P rows = src-segment sums of gH*w (computed while G3 runs).
+// TMEM: D0 z0 (then gz), D1 w (then gH*w), D2 grad_h, D3 grad_w stash
+// (then grad_b from G4).
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_edge_bwd_tc(const EdgeArgs a, const float *__restrict__ P, const float *__restrict__ GH,
               float *__restrict__ GP, float4 *__restrict__ gsum, int accumulate) {
@@ -360,7 +459,7 @@ k_edge_bwd_tc(const EdgeArgs a, const float *__restrict__ P, const float *__rest
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tm = meta->tmem;
-  const uint32_t lane_off = (uint32_t)(32 * quarter) << 16;
+  const uint32_t tl = tm + lane_base(quarter);
   const uint32_t sbase = tc::smem_u32(sm);
   const uint32_t idesc_fwd = tc::idesc_f16(128, TT, 0, 1);
   const uint32_t idesc_g3 = tc::idesc_f16(128, TT, 1, 1);
@@ -375,7 +474,8 @@ k_edge_bwd_tc(const EdgeArgs a, const float *__restrict__ P, const float *__rest
   int eb = a.ptr[rbeg], ee = a.ptr[rend];
   if (ee > eff) ee = (int)eff;
   if (eb > ee) eb = ee;
-  Reducer red{rbeg, 0.f};
+  int crow = rbeg;
+  float cacc = 0.f;
 
   const float b0c = __ldg(&B.f0_b[ch]), b1c = __ldg(&B.f1_b[ch]);
   const float rs0 = quant ? __ldg(&B.f0_s[ch]) : pow2f(-(B.f0_exp + 14));
@@ -399,27 +499,50 @@ k_edge_bwd_tc(const EdgeArgs a, const float *__restrict__ P, const float *__rest
                  nprod_f);
       tc::mma_commit(&meta->bar);
     }
+    // while G1 runs: grad_w[c][e] = gH * P[src][c] (flash.py:291) into the
+    // D3 stash (G4 overwrites D3 only after grad_w is consumed) + tile max
+    float mx = 0.f;
+#pragma unroll 2
+    for (int c0 = 0; c0 < 64; c0 += 16) {
+      float v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        int e = 64 * half + c0 + i;
+        float g = 0.f;
+        if (e < n_e)
+          g = __ldg(&GH[(size_t)meta->nbr[e] * D + ch]) * __ldg(&P[(size_t)meta->own[e] * D + ch]);
+        v[i] = g * q1;
+        mx = fmaxf(mx, fabsf(v[i]));
+      }
+      tc::tmem_st16(tl + TM_D3 + 64 * half + c0, v);
+    }
+    tc::tmem_st_wait();
+    const int sg = scale_exp(block_amax(mx, &meta->amax[1]));
     tc::mbar_wait(&meta->bar, phase);
     phase ^= 1;
     tc::fence_after_sync();
 
-    // recompute h = ssp(z0); z0 stays in TMEM (D0) for ssp'(z0) later
-    float v[64];
-    tmem_ld64(tm + TM_D0 + lane_off + 64 * half, v);
-    float mx = 0.f;
+    // recompute h = ssp(z0); z0 stays in D0 for ssp'(z0) later, h goes
+    // straight to the B operand (no max pass needed for the W16 path)
+    mx = 0.f;
+#pragma unroll 1
+    for (int c0 = 0; c0 < 64; c0 += 16) {
+      float v[16];
+      tc::tmem_ld16(tl + TM_D0 + 64 * half + c0, v);
+      tc::tmem_ld_wait();
 #pragma unroll
-    for (int i = 0; i < 64; ++i) {
-      int e = 64 * half + i;
-      float h = ssp(v[i] * rs0 + b0c);
-      if (quant) h = __half2float(__float2half_rn(h));
-      v[i] = e < n_e ? h : 0.f;
-      mx = fmaxf(mx, fabsf(v[i]));
+      for (int i = 0; i < 16; ++i) {
+        float h = ssp_fast(v[i] * rs0 + b0c);
+        if (quant) h = __half2float(__float2half_rn(h));
+        v[i] = (64 * half + c0 + i) < n_e ? h : 0.f;
+        mx = fmaxf(mx, fabsf(v[i]));
+      }
+      tc::tmem_st16(tl + TM_D2 + 64 * half + c0, v);  // D2 is free until G3
     }
+    tc::tmem_st_wait();
     int sh = 0;
     if (!quant) sh = scale_exp(block_amax(mx, &meta->amax[0]));
-    float sc = pow2f(sh);
-#pragma unroll
-    for (int g = 0; g < 8; ++g) put_b8(act, D, ch, 64 * half + 8 * g, &v[8 * g], sc, !quant);
+    tmem_to_act(tl + TM_D2, act, half, ch, pow2f(sh), !quant);
     tc::fence_async_smem();
     tc::fence_before_sync();
     __syncthreads();
@@ -433,74 +556,61 @@ k_edge_bwd_tc(const EdgeArgs a, const float *__restrict__ P, const float *__rest
     phase ^= 1;
     tc::fence_after_sync();
 
-    // grad_w[c][e] = gH[e][c] * P[src][c] (flash.py:291) -> B operand of G3
-    const float s1 = quant ? rs1 : pow2f(-(B.f1_exp + sh));
-    {
-      float gw[64];
-      mx = 0.f;
-#pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        int e = 64 * half + i;
-        float g = 0.f;
-        if (e < n_e)
-          g = __ldg(&GH[(size_t)meta->nbr[e] * D + ch]) * __ldg(&P[(size_t)meta->own[e] * D + ch]);
-        gw[i] = g * q1;
-        mx = fmaxf(mx, fabsf(gw[i]));
-      }
-      int sg = scale_exp(block_amax(mx, &meta->amax[1]));
-      sc = pow2f(sg);
-#pragma unroll
-      for (int g = 0; g < 8; ++g) put_b8(act, D, ch, 64 * half + 8 * g, &gw[8 * g], sc, true);
-      tc::fence_async_smem();
-      tc::fence_before_sync();
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        tc::fence_after_sync();
-        issue_gemm(tm + TM_D2, sbase + SM_W1, W1_BYTES, D, true, sbase + SM_ACT, D, idesc_g3,
-                   nprod_b);
-        tc::mma_commit(&meta->bar);
-      }
-      sh = sg;  // remember for unscaling D2
+    // grad_w (stashed in D3) -> B operand of G3
+    tmem_to_act(tl + TM_D3, act, half, ch, pow2f(sg), true);
+    tc::fence_async_smem();
+    tc::fence_before_sync();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tc::fence_after_sync();
+      issue_gemm(tm + TM_D2, sbase + SM_W1, W1_BYTES, D, true, sbase + SM_ACT, D, idesc_g3,
+                 nprod_b);
+      tc::mma_commit(&meta->bar);
     }
     // while G3 runs: grad_P rows = src-segment sums of gH * w (flash.py:283-288)
-    if (warp < 4) {
-#pragma unroll 1
-      for (int c0 = 0; c0 < TT; c0 += 16) {
-        float w[16], gv[16];
-        tc::tmem_ld16(tm + TM_D1 + lane_off + c0, w);
+    {
+      const float s1 = quant ? rs1 : pow2f(-(B.f1_exp + sh));
+#pragma unroll 2
+      for (int c0 = 0; c0 < 64; c0 += 16) {
+        float v[16];
+        tc::tmem_ld16(tl + TM_D1 + 64 * half + c0, v);
+        float g[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) gv[i] = __ldg(&GH[(size_t)meta->nbr[c0 + i] * D + ch]);
+        for (int i = 0; i < 16; ++i) g[i] = __ldg(&GH[(size_t)meta->nbr[64 * half + c0 + i] * D + ch]);
         tc::tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          int e = c0 + i;
-          if (e < n_e) red.add(meta->own[e], gv[i] * (w[i] * s1 + b1c), ch, GP);
-        }
+        for (int i = 0; i < 16; ++i) v[i] = g[i] * (v[i] * s1 + b1c);
+        tc::tmem_st16(tl + TM_D1 + 64 * half + c0, v);
       }
+      tc::tmem_st_wait();
+      reduce_tile(tl + TM_D1, meta, n_e, half, ch, meta->xch, crow, cacc, GP);
     }
     tc::mbar_wait(&meta->bar, phase);
     phase ^= 1;
     tc::fence_after_sync();
 
-    // gz = grad_h * ssp'(z0) (mlp_backward_input, model.py:326-331) -> B of G4
+    // gz = grad_h * ssp'(z0) (mlp_backward_input, model.py:326-331), in place in D0
     {
-      float gh[64];
-      tmem_ld64(tm + TM_D2 + lane_off + 64 * half, gh);
-      tmem_ld64(tm + TM_D0 + lane_off + 64 * half, v);
-      const float sg3 = pow2f(-(ew1 + sh));
+      const float sg3 = pow2f(-(ew1 + sg));
       mx = 0.f;
+#pragma unroll 1
+      for (int c0 = 0; c0 < 64; c0 += 16) {
+        float gh[16], z[16];
+        tc::tmem_ld16(tl + TM_D2 + 64 * half + c0, gh);
+        tc::tmem_ld16(tl + TM_D0 + 64 * half + c0, z);
+        tc::tmem_ld_wait();
 #pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        int e = 64 * half + i;
-        float z0 = v[i] * rs0 + b0c;
-        float g = e < n_e ? gh[i] * sg3 * ssp_grad(z0) * q0 : 0.f;
-        gh[i] = g;
-        mx = fmaxf(mx, fabsf(g));
+        for (int i = 0; i < 16; ++i) {
+          float z0 = z[i] * rs0 + b0c;
+          float g = (64 * half + c0 + i) < n_e ? gh[i] * sg3 * sigmoid_fast(z0) * q0 : 0.f;
+          z[i] = g;
+          mx = fmaxf(mx, fabsf(g));
+        }
+        tc::tmem_st16(tl + TM_D0 + 64 * half + c0, z);
       }
-      int sz = scale_exp(block_amax(mx, &meta->amax[2]));
-      sc = pow2f(sz);
-#pragma unroll
-      for (int g = 0; g < 8; ++g) put_b8(act, D, ch, 64 * half + 8 * g, &gh[8 * g], sc, true);
+      tc::tmem_st_wait();
+      const int sz = scale_exp(block_amax(mx, &meta->amax[2]));
+      tmem_to_act(tl + TM_D0, act, half, ch, pow2f(sz), true);
       tc::fence_async_smem();
       tc::fence_before_sync();
       __syncthreads();
@@ -519,20 +629,24 @@ k_edge_bwd_tc(const EdgeArgs a, const float *__restrict__ P, const float *__rest
     // grad_d[e] = sum_k grad_b[k][e] * db[k][e] (flash.py:293).  M=64 D lives
     // in lanes 32q + (0..15) of each quarter: row k = 16q + lane.
     {
-      float gb[64];
-      tmem_ld64(tm + TM_D3 + lane_off + 64 * half, gb);
-      if (lane < 16) {
-        const int k = 16 * quarter + lane;
-        const float mu = __ldg(&a.centers[k]);
-        const float s4 = pow2f(-(ew0 + sh));
-        const float g2 = -2.f * a.gamma;
+      const int k = 16 * quarter + (lane & 15);
+      const float mu = __ldg(&a.centers[k]);
+      const float s4 = pow2f(-(ew0 + sh));
+      const float g2 = -2.f * a.gamma;
+#pragma unroll 1
+      for (int c0 = 0; c0 < 64; c0 += 16) {
+        float gb[16];
+        tc::tmem_ld16(tl + TM_D3 + 64 * half + c0, gb);
+        tc::tmem_ld_wait();
+        if (lane < 16) {
 #pragma unroll
-        for (int i = 0; i < 64; ++i) {
-          int e = 64 * half + i;
-          float dl = meta->d[e] - mu;
-          float gs = __expf((-a.gamma * dl) * dl);
-          float db = gs * (g2 * dl * meta->env[e] + meta->denv[e]);
-          red_s[e * RED_LD + k] = gb[i] * s4 * db;
+          for (int i = 0; i < 16; ++i) {
+            int e = 64 * half + c0 + i;
+            float dl = meta->d[e] - mu;
+            float gs = __expf((-a.gamma * dl) * dl);
+            float db = gs * (g2 * dl * meta->env[e] + meta->denv[e]);
+            red_s[e * RED_LD + k] = gb[i] * s4 * db;
+          }
         }
       }
     }
@@ -557,7 +671,7 @@ k_edge_bwd_tc(const EdgeArgs a, const float *__restrict__ P, const float *__rest
     tc::fence_before_sync();
     __syncthreads();
   }
-  if (warp < 4) red.finish(rend, ch, GP);
+  if (half == 0) finish_rows(crow, cacc, rend, ch, GP);
   tc::fence_before_sync();
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc<512>(tm);
