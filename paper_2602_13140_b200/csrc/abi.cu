@@ -23,7 +23,7 @@ bool g_prof_on = false;
 static const char *kProfNames[P_COUNT] = {
     "nbr_count", "nbr_scan", "nbr_fill", "nbr_rev", "embed", "node_pre", "edge_fwd",
     "node_post", "readout", "node_post_bwd", "edge_bwd", "node_pre_bwd", "forces_finish",
-    "noise", "baoa", "prior", "step_advance"};
+    "noise", "baoa", "prior", "step_advance", "edge_geom"};
 constexpr int kProfMax = 8192;
 struct ProfClass {
   cudaEvent_t ev[2 * kProfMax];

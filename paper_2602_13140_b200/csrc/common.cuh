@@ -87,7 +87,7 @@ namespace fcg {
 enum ProfId {
   P_NBR_COUNT, P_NBR_SCAN, P_NBR_FILL, P_NBR_REV, P_EMBED, P_NODE_PRE, P_EDGE_FWD, P_NODE_POST,
   P_READOUT, P_NODE_POST_BWD, P_EDGE_BWD, P_NODE_PRE_BWD, P_FORCES, P_NOISE, P_BAOA, P_PRIOR,
-  P_STEP, P_COUNT
+  P_STEP, P_EDGE_GEOM, P_COUNT
 };
 extern bool g_prof_on;
 void prof_mark(int id, bool begin, cudaStream_t s);
@@ -139,7 +139,10 @@ int prior_forces(const fcg_prior *pr, const float *pos, int R, int N, float *e_p
 int step_advance(int64_t *step, cudaStream_t s);
 // edge_tc.cu
 void edge_tc_configure();
-void launch_edge_fwd_tc(const EdgeArgs &a, const float *P, float *H, int grid, cudaStream_t s);
-void launch_edge_bwd_tc(const EdgeArgs &a, const float *P, const float *GH, float *GP,
-                        float4 *gsum, int accumulate, int grid, cudaStream_t s);
+void launch_edge_geom(const EdgeArgs &a, float4 *geo, float2 *env, cudaStream_t s);
+void launch_edge_fwd_tc(const EdgeArgs &a, const float4 *geo, const float2 *env, const float *P,
+                        float *H, int grid, cudaStream_t s);
+void launch_edge_bwd_tc(const EdgeArgs &a, const float4 *geo, const float2 *env, const float *P,
+                        const float *GH, float *GP, float4 *gsum, int accumulate, int grid,
+                        cudaStream_t s);
 }  // namespace fcg

@@ -11,9 +11,10 @@
 //   B = per-tile edge activations written by the epilogue threads
 //       (MN-major: row = channel, 128 contiguous edges);
 //   D = TMEM, lane = channel, column = edge.
-// Every epilogue thread therefore owns one channel across consecutive edges,
-// so the destination (forward) / source (backward) segment reduction is a
-// running sum in one thread with a single store per CSR row — no atomics.
+// Every epilogue thread owns one channel across 32 consecutive edges (4
+// threads per channel), so the destination (forward) / source (backward)
+// segment reduction is a running sum per thread plus an ordered 4-way merge,
+// with a single store per CSR row — no atomics.
 //
 // fp32 parity (SURVEY §7 hard part 2): plain fp16/TF32 operands lose ~1e-3;
 // we split both operands as x*2^s = hi + lo (fp16 each, ~22 significant
@@ -30,7 +31,9 @@
 namespace fcg {
 
 constexpr int TT = 128;          // edges per tile (MMA N)
-constexpr int TC_THREADS = 256;  // 8 warps: two per TMEM lane quarter
+constexpr int TC_THREADS = 512;  // 16 warps: 4 per TMEM lane quarter
+constexpr int NPART = 4;         // edge parts per channel
+constexpr int EPT = TT / NPART;  // edges per thread
 constexpr uint32_t SM_W0 = 0;          // W0 hi|lo: 2 x 128x64 fp16
 constexpr uint32_t SM_W1 = 32768;      // W1 hi|lo: 2 x 128x128 fp16
 constexpr uint32_t SM_ACT = 98304;     // B operand hi|lo (<= 2 x 128x128 fp16) / scratch
@@ -44,7 +47,7 @@ struct TcMeta {
   float d[TT], env[TT], denv[TT];
   float4 u[TT];
   unsigned int amax[4];
-  float xch[3 * 128];  // half-1 -> half-0 segment boundary partials
+  float xch[NPART - 1][3][128];  // parts 1..3 -> part 0 segment boundary partials
   uint64_t bar;
   uint32_t tmem;
 };
@@ -86,7 +89,8 @@ __device__ __forceinline__ void put_b8(uint8_t *act, int K, int r, int e0, const
   if (with_lo) *(uint4 *)(act + (uint32_t)K * 256u + off) = *(uint4 *)lo;
 }
 
-// Descriptors (SWIZZLE_NONE, LBO = core stride along K, SBO = along M/N).
+// Descriptors (SWIZZLE_NONE, LBO = core stride along K, SBO = along M/N;
+// pinned on hardware by tests/test_gpu_tcgen05.py).
 __device__ __forceinline__ uint64_t desc_w_kmajor(uint32_t base, int in_dim, int k0) {
   return tc::smem_desc(base + (uint32_t)(k0 >> 3) * 128u, 128u, (uint32_t)(in_dim >> 3) * 128u);
 }
@@ -118,30 +122,48 @@ __device__ __forceinline__ void issue_gemm(uint32_t d, uint32_t w_base, uint32_t
   }
 }
 
-
-// ---- CSR segment sums across the two edge halves of a tile ------------------
-// Each (channel, half) thread feeds its 64 edges in order: runs that start
-// and end inside the half are complete and written directly (one store per
-// row, empty rows between them zeroed); the first and last run of the half
-// are handed to an ordered merge done by the half-0 thread.
+// ---- CSR segment sums across the 4 edge parts of a tile ----------------------
+// Each (channel, part) thread feeds its 32 edges in order: runs that start
+// and end inside the part are complete and written directly (one store per
+// row, empty rows between them zeroed); the first and last run of the part
+// go to an ordered merge done by the part-0 thread.
 struct Runs {
   int row, nruns;
   float acc, head;
   __device__ __forceinline__ void init() { row = -1; nruns = 0; acc = 0.f; head = 0.f; }
-  __device__ __forceinline__ void feed(int o, float v, int c, float *__restrict__ out) {
-    if (o != row) {
-      if (row >= 0) {
-        if (nruns == 0) head = acc; else out[(size_t)row * D + c] = acc;
+  __device__ __forceinline__ void begin(int o, int c, float *__restrict__ out) {
+    if (row >= 0) {
+      if (nruns == 0) head = acc; else out[(size_t)row * D + c] = acc;
 #pragma unroll 1
-        for (int z = row + 1; z < o; ++z) out[(size_t)z * D + c] = 0.f;
-        ++nruns;
-      }
-      row = o;
-      acc = 0.f;
+      for (int z = row + 1; z < o; ++z) out[(size_t)z * D + c] = 0.f;
+      ++nruns;
     }
-    acc += v;
+    row = o;
+    acc = 0.f;
   }
-  // close: nruns = #runs, head = first run's partial, acc = last run's partial
+  // 16 consecutive edges e0.. with values m (first `cnt` valid)
+  __device__ __forceinline__ void chunk(const int *own, int e0, int cnt, const float (&m)[16], int c,
+                                        float *__restrict__ out) {
+    if (cnt == 16 && own[e0] == own[e0 + 15]) {  // one row: branch-free tree sum
+      int o = own[e0];
+      if (o != row) begin(o, c, out);
+      float s[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s[i] = m[i] + m[i + 8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) s[i] += s[i + 4];
+      acc += (s[0] + s[2]) + (s[1] + s[3]);
+      return;
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      if (i < cnt) {
+        int o = own[e0 + i];
+        if (o != row) begin(o, c, out);
+        acc += m[i];
+      }
+    }
+  }
   __device__ __forceinline__ void close() {
     if (row >= 0) {
       if (nruns == 0) head = acc;
@@ -150,8 +172,8 @@ struct Runs {
   }
 };
 
-// Ordered merge of one half's boundary runs into the open carry segment.
-__device__ __forceinline__ void merge_half(int &crow, float &cacc, int nruns, float head,
+// Ordered merge of one part's boundary runs into the open carry segment.
+__device__ __forceinline__ void merge_part(int &crow, float &cacc, int nruns, float head,
                                            float tail, int head_row, int tail_row, int c,
                                            float *__restrict__ out) {
   if (nruns == 0) return;
@@ -164,7 +186,7 @@ __device__ __forceinline__ void merge_half(int &crow, float &cacc, int nruns, fl
     crow = head_row;
     cacc = head;
   }
-  if (nruns > 1) {  // head run complete; rows up to the tail were written by the half
+  if (nruns > 1) {  // head run complete; rows up to the tail were written by the part
     out[(size_t)crow * D + c] = cacc;
     crow = tail_row;
     cacc = tail;
@@ -188,15 +210,28 @@ __device__ __forceinline__ float sigmoid_fast(float x) {
   return __fdividef(1.f, 1.f + __expf(-x));
 }
 
-__device__ __forceinline__ void envelope2(float d, float cutoff, float &c, float &dc) {
-  if (d < cutoff) {
-    float sn, cs;
-    sincosf((3.14159265358979f * d) / cutoff, &sn, &cs);
-    c = 0.5f * (cs + 1.f);
-    dc = (float)(-0.5 * 3.141592653589793 / (double)cutoff) * sn;
-  } else {
-    c = 0.f;
-    dc = 0.f;
+// ---- per-step edge geometry (the reference's d cache, flash.py:221-223) ------
+// geo[k] = (u, d) with u = r[own] - r[nbr] for CSR slot k; env[k] = (C, C').
+__global__ void __launch_bounds__(256)
+k_edge_geom(const float *__restrict__ pos, const int32_t *__restrict__ ptr,
+            const int32_t *__restrict__ nbr, const int32_t *__restrict__ own, int nrows,
+            int64_t cap_e, float cutoff, float4 *__restrict__ geo, float2 *__restrict__ env) {
+  long long e_tot = ptr[nrows];
+  if (e_tot > cap_e) e_tot = cap_e;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < e_tot;
+       k += (long long)gridDim.x * blockDim.x) {
+    const float *po = pos + (size_t)own[k] * 3, *pn = pos + (size_t)nbr[k] * 3;
+    float ux = __fsub_rn(po[0], pn[0]), uy = __fsub_rn(po[1], pn[1]), uz = __fsub_rn(po[2], pn[2]);
+    float d = __fsqrt_rn(__fadd_rn(__fadd_rn(__fmul_rn(ux, ux), __fmul_rn(uy, uy)), __fmul_rn(uz, uz)));
+    float c = 0.f, dc = 0.f;
+    if (d < cutoff) {  // cutoff_envelope(_grad), model.py:242-252
+      float sn, cs;
+      sincosf((3.14159265358979f * d) / cutoff, &sn, &cs);
+      c = 0.5f * (cs + 1.f);
+      dc = (float)(-0.5 * 3.141592653589793 / (double)cutoff) * sn;
+    }
+    geo[k] = make_float4(ux, uy, uz, d);
+    env[k] = make_float2(c, dc);
   }
 }
 
@@ -208,29 +243,28 @@ __device__ __forceinline__ void stage_weights(uint8_t *sm, const fcg_block &b) {
   for (int q = threadIdx.x; q < (int)(2 * W1_BYTES / 16); q += TC_THREADS) d1[q] = __ldg(s1 + q);
 }
 
-__device__ __forceinline__ void tile_meta(const EdgeArgs &a, TcMeta *m, int t0, int n_e,
-                                          bool src_owned) {
+__device__ __forceinline__ void tile_meta(const EdgeArgs &a, const float4 *__restrict__ geo,
+                                          const float2 *__restrict__ env, TcMeta *m, int t0,
+                                          int n_e, bool src_owned) {
   int t = threadIdx.x;
   if (t < TT) {
     int o = -1, n = 0;
-    float d = 0.f, c = 0.f, dc = 0.f;
-    float4 u = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+    float2 c = make_float2(0.f, 0.f);
     if (t < n_e) {
       o = a.own[t0 + t];
       n = a.nbr[t0 + t];
-      const float *po = a.pos + (size_t)o * 3, *pn = a.pos + (size_t)n * 3;
-      float ux = __fsub_rn(po[0], pn[0]), uy = __fsub_rn(po[1], pn[1]), uz = __fsub_rn(po[2], pn[2]);
-      if (src_owned) { ux = -ux; uy = -uy; uz = -uz; }
-      d = __fsqrt_rn(__fadd_rn(__fadd_rn(__fmul_rn(ux, ux), __fmul_rn(uy, uy)), __fmul_rn(uz, uz)));
-      u = make_float4(ux, uy, uz, 0.f);
-      envelope2(d, a.cutoff, c, dc);
+      g = geo[t0 + t];
+      c = env[t0 + t];
     }
+    // backward edge (dst=nbr, src=own): u = r_nbr - r_own (flash.py:279)
+    if (src_owned) { g.x = -g.x; g.y = -g.y; g.z = -g.z; }
     m->own[t] = o;
     m->nbr[t] = n;
-    m->d[t] = d;
-    m->env[t] = c;
-    m->denv[t] = dc;
-    m->u[t] = u;
+    m->d[t] = g.w;
+    m->env[t] = c.x;
+    m->denv[t] = c.y;
+    m->u[t] = make_float4(g.x, g.y, g.z, 0.f);
   }
   if (t < 4) m->amax[t] = 0u;
 }
@@ -239,6 +273,7 @@ __device__ __forceinline__ void tile_meta(const EdgeArgs &a, TcMeta *m, int t0, 
 // 2^14 and split; W16 path rounded to fp16 unscaled (quantize.py:68-71).
 __device__ __forceinline__ void tile_basis_tc(const EdgeArgs &a, const TcMeta *m, int n_e,
                                               uint8_t *act, bool quant) {
+#pragma unroll 1
   for (int q = threadIdx.x; q < DR * (TT / 8); q += TC_THREADS) {
     int k = q % DR, e0 = (q / DR) * 8;
     float mu = __ldg(&a.centers[k]);
@@ -253,84 +288,126 @@ __device__ __forceinline__ void tile_basis_tc(const EdgeArgs &a, const TcMeta *m
   }
 }
 
-
 __device__ __forceinline__ uint32_t lane_base(int quarter) { return (uint32_t)(32 * quarter) << 16; }
 
-// The segment reduction of a [128 ch][128 e] tile held in TMEM columns
-// [col, col+128): both halves scan, half 1 publishes boundary partials,
-// half 0 merges them into the carry.  Called by all 256 threads.
-__device__ __forceinline__ void reduce_tile(uint32_t tcol, const TcMeta *meta, int n_e, int half,
-                                            int ch, float *xch, int &crow, float &cacc,
+// Segment reduction of a [128 ch][128 e] fp32 tile held in TMEM columns
+// starting at tcol: every part scans, parts 1..3 publish boundary partials,
+// part 0 merges them into the carry.  Called by all threads.
+__device__ __forceinline__ void reduce_tile(uint32_t tcol, TcMeta *meta, int n_e, int part,
+                                            int ch, int &crow, float &cacc,
                                             float *__restrict__ out) {
-  const int lo = 64 * half, hi = min(lo + 64, n_e);
+  const int lo = EPT * part, hi = min(lo + EPT, n_e);
   Runs r;
   r.init();
 #pragma unroll 1
-  for (int c0 = 0; c0 < 64; c0 += 16) {
+  for (int c0 = 0; c0 < EPT; c0 += 16) {
     float m[16];
-    tc::tmem_ld16(tcol + 64 * half + c0, m);
+    tc::tmem_ld16(tcol + lo + c0, m);
     tc::tmem_ld_wait();
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      int e = lo + c0 + i;
-      if (e < hi) r.feed(meta->own[e], m[i], ch, out);
-    }
+    r.chunk(meta->own, lo + c0, min(16, hi - lo - c0), m, ch, out);
   }
   r.close();
-  if (half == 1) {
-    xch[ch] = r.head;
-    xch[128 + ch] = r.acc;
-    xch[256 + ch] = __int_as_float(r.nruns);
+  if (part > 0) {
+    meta->xch[part - 1][0][ch] = r.head;
+    meta->xch[part - 1][1][ch] = r.acc;
+    meta->xch[part - 1][2][ch] = __int_as_float(r.nruns);
   }
   __syncthreads();
-  if (half == 0) {
-    merge_half(crow, cacc, r.nruns, r.head, r.acc, meta->own[0], meta->own[max(hi - 1, 0)], ch,
+  if (part == 0) {
+    merge_part(crow, cacc, r.nruns, r.head, r.acc, meta->own[0], meta->own[max(hi - 1, 0)], ch,
                out);
-    merge_half(crow, cacc, __float_as_int(xch[256 + ch]), xch[ch], xch[128 + ch], meta->own[64],
-               meta->own[max(n_e - 1, 64)], ch, out);
+#pragma unroll
+    for (int p = 1; p < NPART; ++p) {
+      const int plo = EPT * p, phi = min(plo + EPT, n_e);
+      merge_part(crow, cacc, __float_as_int(meta->xch[p - 1][2][ch]), meta->xch[p - 1][0][ch],
+                 meta->xch[p - 1][1][ch], meta->own[plo], meta->own[max(phi - 1, plo)], ch, out);
+    }
   }
 }
 
-// Write a [128 ch][64 e-half] fp32 TMEM block as the hi/lo fp16 B operand of
-// the next GEMM with scale 2^sexp (chunks of 16 edges).
-__device__ __forceinline__ void tmem_to_act(uint32_t tcol, uint8_t *act, int half, int ch,
+// Write this thread's [ch][32 edges] fp32 TMEM block as the hi/lo fp16 B
+// operand of the next GEMM with the given scale.
+__device__ __forceinline__ void tmem_to_act(uint32_t tcol, uint8_t *act, int part, int ch,
                                             float scale, bool with_lo) {
 #pragma unroll 1
-  for (int c0 = 0; c0 < 64; c0 += 16) {
+  for (int c0 = 0; c0 < EPT; c0 += 16) {
     float v[16];
-    tc::tmem_ld16(tcol + 64 * half + c0, v);
+    tc::tmem_ld16(tcol + EPT * part + c0, v);
     tc::tmem_ld_wait();
-    put_b8(act, D, ch, 64 * half + c0, &v[0], scale, with_lo);
-    put_b8(act, D, ch, 64 * half + c0 + 8, &v[8], scale, with_lo);
+    put_b8(act, D, ch, EPT * part + c0, &v[0], scale, with_lo);
+    put_b8(act, D, ch, EPT * part + c0 + 8, &v[8], scale, with_lo);
   }
 }
 
+struct TileRange {
+  int rbeg, rend, eb, ee;
+};
+__device__ __forceinline__ TileRange cta_tiles(const EdgeArgs &a) {
+  TileRange t;
+  const int e_tot = a.ptr[a.nrows];
+  const long long eff = e_tot > a.cap_e ? a.cap_e : e_tot;
+  cta_row_range(a.ptr, a.nrows, eff, blockIdx.x, gridDim.x, t.rbeg, t.rend);
+  t.eb = a.ptr[t.rbeg];
+  t.ee = a.ptr[t.rend];
+  if (t.ee > eff) t.ee = (int)eff;
+  if (t.eb > t.ee) t.eb = t.ee;
+  return t;
+}
+
+__device__ __forceinline__ void kernel_prologue(uint8_t *sm, TcMeta *meta, const fcg_block &B) {
+  stage_weights(sm, B);
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&meta->bar, 1);
+    tc::fence_mbar_init();
+  }
+  if (threadIdx.x < 32) tc::tmem_alloc<512>(&meta->tmem);
+  tc::fence_async_smem();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+}
+
+// all threads: make the act writes visible to the tensor core, then thread 0
+// issues the GEMM and commits it to the mbarrier
+#define FCG_ISSUE(...)                  \
+  do {                                  \
+    tc::fence_async_smem();             \
+    tc::fence_before_sync();            \
+    __syncthreads();                    \
+    if (threadIdx.x == 0) {             \
+      tc::fence_after_sync();           \
+      issue_gemm(__VA_ARGS__);          \
+      tc::mma_commit(&meta->bar);       \
+    }                                   \
+  } while (0)
+
+#define FCG_WAIT()                      \
+  do {                                  \
+    tc::mbar_wait(&meta->bar, phase);   \
+    phase ^= 1;                         \
+    tc::fence_after_sync();             \
+  } while (0)
+
+// ---------------------------------------------------------------------------
 // Forward: per 128-edge tile of dst rows
 //   b -> [GEMM1] z0 -> h=ssp(z0) -> [GEMM2] w -> m = P[src]*w -> H rows.
 // The P[src] gather is issued right after GEMM1 so its latency hides under
 // the tensor-core work; h and m are staged back into TMEM so every epilogue
 // pass streams 16 columns at a time.
 __global__ void __launch_bounds__(TC_THREADS, 1)
-k_edge_fwd_tc(const EdgeArgs a, const float *__restrict__ P, float *__restrict__ H) {
+k_edge_fwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__restrict__ env,
+              const float *__restrict__ P, float *__restrict__ H) {
   extern __shared__ __align__(1024) uint8_t sm[];
   TcMeta *meta = (TcMeta *)(sm + SM_META);
   uint8_t *act = sm + SM_ACT;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int quarter = warp & 3, half = warp >> 2;
+  const int quarter = warp & 3, part = warp >> 2;
   const int ch = 32 * quarter + lane;
+  const int ec = EPT * part;  // this thread's first edge column
   const bool quant = a.quant != 0;
   const fcg_block &B = a.blk;
 
-  stage_weights(sm, B);
-  if (threadIdx.x == 0) {
-    tc::mbar_init(&meta->bar, 1);
-    tc::fence_mbar_init();
-  }
-  if (warp == 0) tc::tmem_alloc<512>(&meta->tmem);
-  tc::fence_async_smem();
-  tc::fence_before_sync();
-  __syncthreads();
-  tc::fence_after_sync();
+  kernel_prologue(sm, meta, B);
   const uint32_t tm = meta->tmem;
   const uint32_t tl = tm + lane_base(quarter);
   const uint32_t sbase = tc::smem_u32(sm);
@@ -338,93 +415,69 @@ k_edge_fwd_tc(const EdgeArgs a, const float *__restrict__ P, float *__restrict__
   const int nprod = quant ? 1 : 3;
   uint32_t phase = 0;
 
-  const int e_tot = a.ptr[a.nrows];
-  const long long eff = e_tot > a.cap_e ? a.cap_e : e_tot;
-  int rbeg, rend;
-  cta_row_range(a.ptr, a.nrows, eff, blockIdx.x, gridDim.x, rbeg, rend);
-  int eb = a.ptr[rbeg], ee = a.ptr[rend];
-  if (ee > eff) ee = (int)eff;
-  if (eb > ee) eb = ee;
-  int crow = rbeg;
+  const TileRange tr = cta_tiles(a);
+  int crow = tr.rbeg;
   float cacc = 0.f;
 
   const float b0c = __ldg(&B.f0_b[ch]), b1c = __ldg(&B.f1_b[ch]);
   const float rs0 = quant ? __ldg(&B.f0_s[ch]) : pow2f(-(B.f0_exp + 14));
   const float rs1 = quant ? __ldg(&B.f1_s[ch]) : 1.f;
 
-  for (int t0 = eb; t0 < ee; t0 += TT) {
-    const int n_e = min(TT, ee - t0);
-    tile_meta(a, meta, t0, n_e, false);
+  for (int t0 = tr.eb; t0 < tr.ee; t0 += TT) {
+    const int n_e = min(TT, tr.ee - t0);
+    tile_meta(a, geo, env, meta, t0, n_e, false);
     __syncthreads();
     tile_basis_tc(a, meta, n_e, act, quant);
-    tc::fence_async_smem();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      tc::fence_after_sync();
-      issue_gemm(tm + TM_D0, sbase + SM_W0, W0_BYTES, DR, false, sbase + SM_ACT, DR, idesc,
-                 nprod);
-      tc::mma_commit(&meta->bar);
-    }
-    float pv[64];  // P[src][ch] of this half's edges, in flight during the MMAs
+    FCG_ISSUE(tm + TM_D0, sbase + SM_W0, W0_BYTES, DR, false, sbase + SM_ACT, DR, idesc, nprod);
+    float pv[EPT];  // P[src][ch] of this thread's edges, in flight during the MMAs
 #pragma unroll
-    for (int i = 0; i < 64; ++i) pv[i] = __ldg(&P[(size_t)meta->nbr[64 * half + i] * D + ch]);
-    tc::mbar_wait(&meta->bar, phase);
-    phase ^= 1;
-    tc::fence_after_sync();
+    for (int i = 0; i < EPT; ++i) pv[i] = __ldg(&P[(size_t)meta->nbr[ec + i] * D + ch]);
+    FCG_WAIT();
 
     // epilogue 1: h = ssp(W0 b + b0), staged in place in D0, then -> B of GEMM2
     float mx = 0.f;
-#pragma unroll 1
-    for (int c0 = 0; c0 < 64; c0 += 16) {
+#pragma unroll
+    for (int c0 = 0; c0 < EPT; c0 += 16) {
       float v[16];
-      tc::tmem_ld16(tl + TM_D0 + 64 * half + c0, v);
+      tc::tmem_ld16(tl + TM_D0 + ec + c0, v);
       tc::tmem_ld_wait();
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         float h = ssp_fast(v[i] * rs0 + b0c);
         if (quant) h = __half2float(__float2half_rn(h));
-        v[i] = (64 * half + c0 + i) < n_e ? h : 0.f;
+        v[i] = (ec + c0 + i) < n_e ? h : 0.f;
         mx = fmaxf(mx, fabsf(v[i]));
       }
-      tc::tmem_st16(tl + TM_D0 + 64 * half + c0, v);
+      tc::tmem_st16(tl + TM_D0 + ec + c0, v);
     }
     tc::tmem_st_wait();
     int sh = 0;
     if (!quant) sh = scale_exp(block_amax(mx, &meta->amax[0]));
-    tmem_to_act(tl + TM_D0, act, half, ch, pow2f(sh), !quant);
-    tc::fence_async_smem();
-    tc::fence_before_sync();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      tc::fence_after_sync();
-      issue_gemm(tm + TM_D1, sbase + SM_W1, W1_BYTES, D, false, sbase + SM_ACT, D, idesc, nprod);
-      tc::mma_commit(&meta->bar);
-    }
-    tc::mbar_wait(&meta->bar, phase);
-    phase ^= 1;
-    tc::fence_after_sync();
+    tmem_to_act(tl + TM_D0, act, part, ch, pow2f(sh), !quant);
+    FCG_ISSUE(tm + TM_D1, sbase + SM_W1, W1_BYTES, D, false, sbase + SM_ACT, D, idesc, nprod);
+    FCG_WAIT();
 
     // epilogue 2: m = (W1 h + b1) * P[src] (flash.py:229), in place in D1,
     // then dst segment sums (flash.py:232-234)
     const float s1 = quant ? rs1 : pow2f(-(B.f1_exp + sh));
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < EPT / 16; ++c) {
       float v[16];
-      tc::tmem_ld16(tl + TM_D1 + 64 * half + 16 * c, v);
+      tc::tmem_ld16(tl + TM_D1 + ec + 16 * c, v);
       tc::tmem_ld_wait();
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] = (v[i] * s1 + b1c) * pv[16 * c + i];
-      tc::tmem_st16(tl + TM_D1 + 64 * half + 16 * c, v);
+      tc::tmem_st16(tl + TM_D1 + ec + 16 * c, v);
     }
     tc::tmem_st_wait();
-    reduce_tile(tl + TM_D1, meta, n_e, half, ch, meta->xch, crow, cacc, H);
+    reduce_tile(tl + TM_D1, meta, n_e, part, ch, crow, cacc, H);
     tc::fence_before_sync();
     __syncthreads();
   }
-  if (half == 0) finish_rows(crow, cacc, rend, ch, H);
+  if (part == 0) finish_rows(crow, cacc, tr.rend, ch, H);
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == 0) tc::tmem_dealloc<512>(tm);
+  if (threadIdx.x < 32) tc::tmem_dealloc<512>(tm);
 }
 
 // ---------------------------------------------------------------------------
@@ -433,31 +486,24 @@ k_edge_fwd_tc(const EdgeArgs a, const float *__restrict__ P, float *__restrict__
 //   [G3] grad_h = grad_w W1 -> gz = grad_h*ssp'(z0) -> [G4] grad_b = gz W0
 //   -> grad_d = sum_k grad_b*db -> g_e = grad_d/d * u  (gsum, owner slot);
 //   grad_P rows = src-segment sums of gH*w (computed while G3 runs).
-// TMEM: D0 z0 (then gz), D1 w (then gH*w), D2 grad_h, D3 grad_w stash
-// (then grad_b from G4).
+// TMEM: D0 z0 (then gz), D1 w (then gH*w), D2 h (then grad_h), D3 grad_w
+// stash (then grad_b from G4).
 __global__ void __launch_bounds__(TC_THREADS, 1)
-k_edge_bwd_tc(const EdgeArgs a, const float *__restrict__ P, const float *__restrict__ GH,
-              float *__restrict__ GP, float4 *__restrict__ gsum, int accumulate) {
+k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__restrict__ env,
+              const float *__restrict__ P, const float *__restrict__ GH, float *__restrict__ GP,
+              float4 *__restrict__ gsum, int accumulate) {
   extern __shared__ __align__(1024) uint8_t sm[];
   TcMeta *meta = (TcMeta *)(sm + SM_META);
   uint8_t *act = sm + SM_ACT;
   float *red_s = (float *)(sm + SM_ACT);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int quarter = warp & 3, half = warp >> 2;
+  const int quarter = warp & 3, part = warp >> 2;
   const int ch = 32 * quarter + lane;
+  const int ec = EPT * part;
   const bool quant = a.quant != 0;
   const fcg_block &B = a.blk;
 
-  stage_weights(sm, B);
-  if (threadIdx.x == 0) {
-    tc::mbar_init(&meta->bar, 1);
-    tc::fence_mbar_init();
-  }
-  if (warp == 0) tc::tmem_alloc<512>(&meta->tmem);
-  tc::fence_async_smem();
-  tc::fence_before_sync();
-  __syncthreads();
-  tc::fence_after_sync();
+  kernel_prologue(sm, meta, B);
   const uint32_t tm = meta->tmem;
   const uint32_t tl = tm + lane_base(quarter);
   const uint32_t sbase = tc::smem_u32(sm);
@@ -467,14 +513,8 @@ k_edge_bwd_tc(const EdgeArgs a, const float *__restrict__ P, const float *__rest
   const int nprod_f = quant ? 1 : 3, nprod_b = quant ? 2 : 3;
   uint32_t phase = 0;
 
-  const int e_tot = a.ptr[a.nrows];
-  const long long eff = e_tot > a.cap_e ? a.cap_e : e_tot;
-  int rbeg, rend;
-  cta_row_range(a.ptr, a.nrows, eff, blockIdx.x, gridDim.x, rbeg, rend);
-  int eb = a.ptr[rbeg], ee = a.ptr[rend];
-  if (ee > eff) ee = (int)eff;
-  if (eb > ee) eb = ee;
-  int crow = rbeg;
+  const TileRange tr = cta_tiles(a);
+  int crow = tr.rbeg;
   float cacc = 0.f;
 
   const float b0c = __ldg(&B.f0_b[ch]), b1c = __ldg(&B.f1_b[ch]);
@@ -486,145 +526,106 @@ k_edge_bwd_tc(const EdgeArgs a, const float *__restrict__ P, const float *__rest
   const float q0 = quant ? __ldg(&B.f0_s[ch]) : 1.f;
   const int ew0 = quant ? 0 : B.f0_exp, ew1 = quant ? 0 : B.f1_exp;
 
-  for (int t0 = eb; t0 < ee; t0 += TT) {
-    const int n_e = min(TT, ee - t0);
-    tile_meta(a, meta, t0, n_e, true);
+  for (int t0 = tr.eb; t0 < tr.ee; t0 += TT) {
+    const int n_e = min(TT, tr.ee - t0);
+    tile_meta(a, geo, env, meta, t0, n_e, true);
     __syncthreads();
     tile_basis_tc(a, meta, n_e, act, quant);
-    tc::fence_async_smem();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      tc::fence_after_sync();
-      issue_gemm(tm + TM_D0, sbase + SM_W0, W0_BYTES, DR, false, sbase + SM_ACT, DR, idesc_fwd,
-                 nprod_f);
-      tc::mma_commit(&meta->bar);
-    }
+    FCG_ISSUE(tm + TM_D0, sbase + SM_W0, W0_BYTES, DR, false, sbase + SM_ACT, DR, idesc_fwd,
+              nprod_f);
     // while G1 runs: grad_w[c][e] = gH * P[src][c] (flash.py:291) into the
     // D3 stash (G4 overwrites D3 only after grad_w is consumed) + tile max
     float mx = 0.f;
-#pragma unroll 2
-    for (int c0 = 0; c0 < 64; c0 += 16) {
+#pragma unroll
+    for (int c0 = 0; c0 < EPT; c0 += 16) {
       float v[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
-        int e = 64 * half + c0 + i;
+        int e = ec + c0 + i;
         float g = 0.f;
         if (e < n_e)
           g = __ldg(&GH[(size_t)meta->nbr[e] * D + ch]) * __ldg(&P[(size_t)meta->own[e] * D + ch]);
         v[i] = g * q1;
         mx = fmaxf(mx, fabsf(v[i]));
       }
-      tc::tmem_st16(tl + TM_D3 + 64 * half + c0, v);
+      tc::tmem_st16(tl + TM_D3 + ec + c0, v);
     }
     tc::tmem_st_wait();
     const int sg = scale_exp(block_amax(mx, &meta->amax[1]));
-    tc::mbar_wait(&meta->bar, phase);
-    phase ^= 1;
-    tc::fence_after_sync();
+    FCG_WAIT();
 
-    // recompute h = ssp(z0); z0 stays in D0 for ssp'(z0) later, h goes
-    // straight to the B operand (no max pass needed for the W16 path)
+    // recompute h = ssp(z0) into D2 (free until G3); z0 stays in D0
     mx = 0.f;
-#pragma unroll 1
-    for (int c0 = 0; c0 < 64; c0 += 16) {
+#pragma unroll
+    for (int c0 = 0; c0 < EPT; c0 += 16) {
       float v[16];
-      tc::tmem_ld16(tl + TM_D0 + 64 * half + c0, v);
+      tc::tmem_ld16(tl + TM_D0 + ec + c0, v);
       tc::tmem_ld_wait();
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         float h = ssp_fast(v[i] * rs0 + b0c);
         if (quant) h = __half2float(__float2half_rn(h));
-        v[i] = (64 * half + c0 + i) < n_e ? h : 0.f;
+        v[i] = (ec + c0 + i) < n_e ? h : 0.f;
         mx = fmaxf(mx, fabsf(v[i]));
       }
-      tc::tmem_st16(tl + TM_D2 + 64 * half + c0, v);  // D2 is free until G3
+      tc::tmem_st16(tl + TM_D2 + ec + c0, v);
     }
     tc::tmem_st_wait();
     int sh = 0;
     if (!quant) sh = scale_exp(block_amax(mx, &meta->amax[0]));
-    tmem_to_act(tl + TM_D2, act, half, ch, pow2f(sh), !quant);
-    tc::fence_async_smem();
-    tc::fence_before_sync();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      tc::fence_after_sync();
-      issue_gemm(tm + TM_D1, sbase + SM_W1, W1_BYTES, D, false, sbase + SM_ACT, D, idesc_fwd,
-                 nprod_f);
-      tc::mma_commit(&meta->bar);
-    }
-    tc::mbar_wait(&meta->bar, phase);
-    phase ^= 1;
-    tc::fence_after_sync();
+    tmem_to_act(tl + TM_D2, act, part, ch, pow2f(sh), !quant);
+    FCG_ISSUE(tm + TM_D1, sbase + SM_W1, W1_BYTES, D, false, sbase + SM_ACT, D, idesc_fwd,
+              nprod_f);
+    FCG_WAIT();
 
     // grad_w (stashed in D3) -> B operand of G3
-    tmem_to_act(tl + TM_D3, act, half, ch, pow2f(sg), true);
-    tc::fence_async_smem();
-    tc::fence_before_sync();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      tc::fence_after_sync();
-      issue_gemm(tm + TM_D2, sbase + SM_W1, W1_BYTES, D, true, sbase + SM_ACT, D, idesc_g3,
-                 nprod_b);
-      tc::mma_commit(&meta->bar);
-    }
+    tmem_to_act(tl + TM_D3, act, part, ch, pow2f(sg), true);
+    FCG_ISSUE(tm + TM_D2, sbase + SM_W1, W1_BYTES, D, true, sbase + SM_ACT, D, idesc_g3, nprod_b);
     // while G3 runs: grad_P rows = src-segment sums of gH * w (flash.py:283-288)
     {
       const float s1 = quant ? rs1 : pow2f(-(B.f1_exp + sh));
-#pragma unroll 2
-      for (int c0 = 0; c0 < 64; c0 += 16) {
-        float v[16];
-        tc::tmem_ld16(tl + TM_D1 + 64 * half + c0, v);
-        float g[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) g[i] = __ldg(&GH[(size_t)meta->nbr[64 * half + c0 + i] * D + ch]);
+      for (int c0 = 0; c0 < EPT; c0 += 16) {
+        float v[16], g[16];
+        tc::tmem_ld16(tl + TM_D1 + ec + c0, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) g[i] = __ldg(&GH[(size_t)meta->nbr[ec + c0 + i] * D + ch]);
         tc::tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = g[i] * (v[i] * s1 + b1c);
-        tc::tmem_st16(tl + TM_D1 + 64 * half + c0, v);
+        tc::tmem_st16(tl + TM_D1 + ec + c0, v);
       }
       tc::tmem_st_wait();
-      reduce_tile(tl + TM_D1, meta, n_e, half, ch, meta->xch, crow, cacc, GP);
+      reduce_tile(tl + TM_D1, meta, n_e, part, ch, crow, cacc, GP);
     }
-    tc::mbar_wait(&meta->bar, phase);
-    phase ^= 1;
-    tc::fence_after_sync();
+    FCG_WAIT();
 
     // gz = grad_h * ssp'(z0) (mlp_backward_input, model.py:326-331), in place in D0
     {
       const float sg3 = pow2f(-(ew1 + sg));
       mx = 0.f;
-#pragma unroll 1
-      for (int c0 = 0; c0 < 64; c0 += 16) {
+#pragma unroll
+      for (int c0 = 0; c0 < EPT; c0 += 16) {
         float gh[16], z[16];
-        tc::tmem_ld16(tl + TM_D2 + 64 * half + c0, gh);
-        tc::tmem_ld16(tl + TM_D0 + 64 * half + c0, z);
+        tc::tmem_ld16(tl + TM_D2 + ec + c0, gh);
+        tc::tmem_ld16(tl + TM_D0 + ec + c0, z);
         tc::tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           float z0 = z[i] * rs0 + b0c;
-          float g = (64 * half + c0 + i) < n_e ? gh[i] * sg3 * sigmoid_fast(z0) * q0 : 0.f;
+          float g = (ec + c0 + i) < n_e ? gh[i] * sg3 * sigmoid_fast(z0) * q0 : 0.f;
           z[i] = g;
           mx = fmaxf(mx, fabsf(g));
         }
-        tc::tmem_st16(tl + TM_D0 + 64 * half + c0, z);
+        tc::tmem_st16(tl + TM_D0 + ec + c0, z);
       }
       tc::tmem_st_wait();
-      const int sz = scale_exp(block_amax(mx, &meta->amax[2]));
-      tmem_to_act(tl + TM_D0, act, half, ch, pow2f(sz), true);
-      tc::fence_async_smem();
-      tc::fence_before_sync();
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        tc::fence_after_sync();
-        issue_gemm(tm + TM_D3, sbase + SM_W0, W0_BYTES, DR, true, sbase + SM_ACT, D, idesc_g4,
-                   nprod_b);
-        tc::mma_commit(&meta->bar);
-      }
-      sh = sz;
+      sh = scale_exp(block_amax(mx, &meta->amax[2]));
+      tmem_to_act(tl + TM_D0, act, part, ch, pow2f(sh), true);
+      FCG_ISSUE(tm + TM_D3, sbase + SM_W0, W0_BYTES, DR, true, sbase + SM_ACT, D, idesc_g4,
+                nprod_b);
     }
-    tc::mbar_wait(&meta->bar, phase);
-    phase ^= 1;
-    tc::fence_after_sync();
+    FCG_WAIT();
 
     // grad_d[e] = sum_k grad_b[k][e] * db[k][e] (flash.py:293).  M=64 D lives
     // in lanes 32q + (0..15) of each quarter: row k = 16q + lane.
@@ -633,18 +634,18 @@ k_edge_bwd_tc(const EdgeArgs a, const float *__restrict__ P, const float *__rest
       const float mu = __ldg(&a.centers[k]);
       const float s4 = pow2f(-(ew0 + sh));
       const float g2 = -2.f * a.gamma;
-#pragma unroll 1
-      for (int c0 = 0; c0 < 64; c0 += 16) {
+#pragma unroll
+      for (int c0 = 0; c0 < EPT; c0 += 16) {
         float gb[16];
-        tc::tmem_ld16(tl + TM_D3 + 64 * half + c0, gb);
+        tc::tmem_ld16(tl + TM_D3 + ec + c0, gb);
         tc::tmem_ld_wait();
         if (lane < 16) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            int e = 64 * half + c0 + i;
+            int e = ec + c0 + i;
             float dl = meta->d[e] - mu;
             float gs = __expf((-a.gamma * dl) * dl);
-            float db = gs * (g2 * dl * meta->env[e] + meta->denv[e]);
+            float db = gs * (g2 * dl * meta->env[e] + meta->denv[e]);  // model.py:289
             red_s[e * RED_LD + k] = gb[i] * s4 * db;
           }
         }
@@ -671,10 +672,10 @@ k_edge_bwd_tc(const EdgeArgs a, const float *__restrict__ P, const float *__rest
     tc::fence_before_sync();
     __syncthreads();
   }
-  if (half == 0) finish_rows(crow, cacc, rend, ch, GP);
+  if (part == 0) finish_rows(crow, cacc, tr.rend, ch, GP);
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == 0) tc::tmem_dealloc<512>(tm);
+  if (threadIdx.x < 32) tc::tmem_dealloc<512>(tm);
 }
 
 void edge_tc_configure() {
@@ -687,13 +688,21 @@ void edge_tc_configure() {
   done = true;
 }
 
-void launch_edge_fwd_tc(const EdgeArgs &a, const float *P, float *H, int grid, cudaStream_t s) {
-  k_edge_fwd_tc<<<grid, TC_THREADS, SM_TOTAL + 1024, s>>>(a, P, H);
+void launch_edge_geom(const EdgeArgs &a, float4 *geo, float2 *env, cudaStream_t s) {
+  k_edge_geom<<<1184, 256, 0, s>>>(a.pos, a.ptr, a.nbr, a.own, a.nrows, a.cap_e, a.cutoff, geo,
+                                   env);
 }
 
-void launch_edge_bwd_tc(const EdgeArgs &a, const float *P, const float *GH, float *GP,
-                        float4 *gsum, int accumulate, int grid, cudaStream_t s) {
-  k_edge_bwd_tc<<<grid, TC_THREADS, SM_TOTAL + 1024, s>>>(a, P, GH, GP, gsum, accumulate);
+void launch_edge_fwd_tc(const EdgeArgs &a, const float4 *geo, const float2 *env, const float *P,
+                        float *H, int grid, cudaStream_t s) {
+  k_edge_fwd_tc<<<grid, TC_THREADS, SM_TOTAL + 1024, s>>>(a, geo, env, P, H);
+}
+
+void launch_edge_bwd_tc(const EdgeArgs &a, const float4 *geo, const float2 *env, const float *P,
+                        const float *GH, float *GP, float4 *gsum, int accumulate, int grid,
+                        cudaStream_t s) {
+  k_edge_bwd_tc<<<grid, TC_THREADS, SM_TOTAL + 1024, s>>>(a, geo, env, P, GH, GP, gsum,
+                                                         accumulate);
 }
 
 }  // namespace fcg

@@ -598,6 +598,8 @@ struct EfBuffers {
   float *X, *H, *G, *GH, *GP;
   float *P[FCG_MAX_BLOCKS], *Zp[FCG_MAX_BLOCKS];
   float4 *gsum;
+  float4 *geo;
+  float2 *env;
 };
 
 static EfBuffers carve_ef(Carver &c, int T, size_t RN, int64_t cap_e) {
@@ -613,6 +615,8 @@ static EfBuffers carve_ef(Carver &c, int T, size_t RN, int64_t cap_e) {
     b.Zp[t] = c.take<float>(rows * D);
   }
   b.gsum = c.take<float4>((size_t)cap_e + 1);
+  b.geo = c.take<float4>((size_t)cap_e + 1);
+  b.env = c.take<float2>((size_t)cap_e + 1);
   return b;
 }
 
@@ -678,7 +682,11 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
   ea.quant = quant;
   const bool simt = use_simt_edges();
   const int eg = simt ? 2 * sm_count() : sm_count();
-  if (!simt) edge_tc_configure();
+  if (!simt) {
+    edge_tc_configure();
+    FCG_PROF(P_EDGE_GEOM, s);
+    launch_edge_geom(ea, b.geo, b.env, s);
+  }
 
   for (int t = 0; t < T; ++t) {
     const fcg_block &blk = m->blocks[t];
@@ -693,7 +701,7 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
       if (simt)
         k_edge_fwd<<<eg, NT, (TE * LDR + TE * LDH) * sizeof(float), s>>>(ea, b.P[t], b.H);
       else
-        launch_edge_fwd_tc(ea, b.P[t], b.H, eg, s);
+        launch_edge_fwd_tc(ea, b.geo, b.env, b.P[t], b.H, eg, s);
     }
     {
       FCG_PROF(P_NODE_POST, s);
@@ -718,7 +726,7 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
         k_edge_bwd<<<eg, NT, 3 * TE * LDH * sizeof(float), s>>>(ea, b.P[t], b.GH, b.GP, b.gsum,
                                                                t != T - 1);
       else
-        launch_edge_bwd_tc(ea, b.P[t], b.GH, b.GP, b.gsum, t != T - 1, eg, s);
+        launch_edge_bwd_tc(ea, b.geo, b.env, b.P[t], b.GH, b.GP, b.gsum, t != T - 1, eg, s);
     }
     {
       FCG_PROF(P_NODE_PRE_BWD, s);
