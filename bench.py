@@ -329,9 +329,8 @@ def main():
     # ---- end-of-run gather of per-replica observables (NCCL) -------------
     energies = eng.potential.clone()
     if world > 1:
-        allg = [torch.empty_like(energies) for _ in range(world)]
-        dist.all_gather(allg, energies)
-        energies = torch.cat(allg)
+        from paper_2602_13140_b200.sharding import gather_replicas
+        energies = gather_replicas(energies, R * world)
 
     if rank == 0:
         sysline = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
