@@ -95,6 +95,9 @@ typedef struct {
    * (the per-row scales *_s are applied in the epilogue). */
   const uint16_t *f0_img, *f1_img; /* [2][D][DR], [2][D][D] */
   int f0_exp, f1_exp;
+  /* same images for the node MLPs (pre_linear, post0, post1), [2][D][D] */
+  const uint16_t *pre_img, *p0_img, *p1_img;
+  int pre_exp, p0_exp, p1_exp;
 } fcg_block;
 
 typedef struct {
@@ -111,6 +114,8 @@ typedef struct {
   float r1_b;                       /* readout layer 1 bias                  */
   const uint16_t *r0_h; const float *r0_s; /* W16 only */
   const uint16_t *r1_h; float r1_s;        /* W16 only */
+  const uint16_t *r0_img;                  /* readout layer 0 image, [2][RH][D] */
+  int r0_exp;
 } fcg_model;
 
 /* Library identity. */

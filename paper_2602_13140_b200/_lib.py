@@ -30,7 +30,9 @@ class FcgBlock(C.Structure):
         "p0_w", "p0_wt", "p0_b", "p1_w", "p1_wt", "p1_b")] + \
         [(n, _u16) for n in ("pre_h", "f0_h", "f1_h", "p0_h", "p1_h")] + \
         [(n, _f) for n in ("pre_s", "f0_s", "f1_s", "p0_s", "p1_s")] + \
-        [("f0_img", _u16), ("f1_img", _u16), ("f0_exp", C.c_int), ("f1_exp", C.c_int)]
+        [("f0_img", _u16), ("f1_img", _u16), ("f0_exp", C.c_int), ("f1_exp", C.c_int),
+         ("pre_img", _u16), ("p0_img", _u16), ("p1_img", _u16),
+         ("pre_exp", C.c_int), ("p0_exp", C.c_int), ("p1_exp", C.c_int)]
 
 
 class FcgModel(C.Structure):
@@ -41,6 +43,7 @@ class FcgModel(C.Structure):
         ("blocks", FcgBlock * FCG_MAX_BLOCKS),
         ("r0_w", _f), ("r0_wt", _f), ("r0_b", _f), ("r1_w", _f), ("r1_b", C.c_float),
         ("r0_h", _u16), ("r0_s", _f), ("r1_h", _u16), ("r1_s", C.c_float),
+        ("r0_img", _u16), ("r0_exp", C.c_int),
     ]
 
 

@@ -137,6 +137,18 @@ int half_kick(const fcg_md_params *p, const float *mass, int R, int N, const flo
 int prior_forces(const fcg_prior *pr, const float *pos, int R, int N, float *e_prior,
                  float *f_prior, cudaStream_t s);
 int step_advance(int64_t *step, cudaStream_t s);
+// node_tc.cu
+void node_tc_configure();
+void launch_node_pre_tc(const float *X, const fcg_block &b, int quant, float *P, int nrows,
+                        cudaStream_t s);
+void launch_node_pre_bwd_tc(const float *GP, const fcg_block &b, int quant, float *G, int nrows,
+                            cudaStream_t s);
+void launch_node_post_tc(const float *H, const fcg_block &b, int quant, float *Zp, float *X,
+                         int nrows, cudaStream_t s);
+void launch_node_post_bwd_tc(const float *G, const fcg_block &b, int quant, const float *Zp,
+                             float *GH, int nrows, cudaStream_t s);
+void launch_readout_tc(const float *X, const fcg_model &m, float *per_atom, float *G, int nrows,
+                       cudaStream_t s);
 // edge_tc.cu
 void edge_tc_configure();
 void launch_edge_geom(const EdgeArgs &a, float4 *geo, float2 *env, cudaStream_t s);

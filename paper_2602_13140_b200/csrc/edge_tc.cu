@@ -27,6 +27,7 @@
 
 #include "common.cuh"
 #include "tc.cuh"
+#include "tc_ops.cuh"
 
 namespace fcg {
 
@@ -52,75 +53,6 @@ struct TcMeta {
   uint32_t tmem;
 };
 constexpr uint32_t SM_TOTAL = SM_META + sizeof(TcMeta);
-
-__device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }
-
-// Power-of-two scale s with max*2^s in [2^14, 2^15); 1 for an all-zero tile.
-__device__ __forceinline__ int scale_exp(float m) {
-  if (!(m > 0.f) || !isfinite(m)) return 0;
-  int e;
-  frexpf(m, &e);  // m = f * 2^e, f in [0.5, 1)
-  return 15 - e;
-}
-
-// Block-wide max of non-negative values (all TC_THREADS threads call it).
-__device__ __forceinline__ float block_amax(float v, unsigned int *slot) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(slot, __float_as_uint(v));
-  __syncthreads();
-  return __uint_as_float(*slot);
-}
-
-// Store 8 consecutive edges e0..e0+7 of K-row r of an MN-major B operand
-// (hi image at act, lo image at act + K*256 bytes), values pre-scaled.
-__device__ __forceinline__ void put_b8(uint8_t *act, int K, int r, int e0, const float *v,
-                                       float scale, bool with_lo) {
-  uint32_t off = (uint32_t)(r >> 3) * 2048u + (uint32_t)(e0 >> 3) * 128u + (uint32_t)(r & 7) * 16u;
-  __half2 hi[4], lo[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    float a = v[2 * i] * scale, b = v[2 * i + 1] * scale;
-    hi[i] = __floats2half2_rn(a, b);
-    float2 hf = __half22float2(hi[i]);
-    lo[i] = __floats2half2_rn(a - hf.x, b - hf.y);
-  }
-  *(uint4 *)(act + off) = *(uint4 *)hi;
-  if (with_lo) *(uint4 *)(act + (uint32_t)K * 256u + off) = *(uint4 *)lo;
-}
-
-// Descriptors (SWIZZLE_NONE, LBO = core stride along K, SBO = along M/N;
-// pinned on hardware by tests/test_gpu_tcgen05.py).
-__device__ __forceinline__ uint64_t desc_w_kmajor(uint32_t base, int in_dim, int k0) {
-  return tc::smem_desc(base + (uint32_t)(k0 >> 3) * 128u, 128u, (uint32_t)(in_dim >> 3) * 128u);
-}
-__device__ __forceinline__ uint64_t desc_w_mnmajor(uint32_t base, int in_dim, int k0) {
-  uint32_t rowstride = (uint32_t)(in_dim >> 3) * 128u;
-  return tc::smem_desc(base + (uint32_t)(k0 >> 3) * rowstride, rowstride, 128u);
-}
-__device__ __forceinline__ uint64_t desc_act(uint32_t base, int k0) {
-  return tc::smem_desc(base + (uint32_t)(k0 >> 3) * 2048u, 2048u, 128u);
-}
-
-// Issue one GEMM D(tmem) = A(weights) x B(act) over K, with the product set
-// {hi*hi, hi*lo, lo*hi} (nprod=3), {hi*hi, hi*lo} (2) or {hi*hi} (1).
-__device__ __forceinline__ void issue_gemm(uint32_t d, uint32_t w_base, uint32_t w_lo_off,
-                                           int in_dim, bool w_mn, uint32_t act_base, int K,
-                                           uint32_t idesc, int nprod) {
-  uint32_t act_lo = act_base + (uint32_t)K * 256u;
-#pragma unroll 1
-  for (int k0 = 0; k0 < K; k0 += 16) {
-    uint64_t ah = w_mn ? desc_w_mnmajor(w_base, in_dim, k0) : desc_w_kmajor(w_base, in_dim, k0);
-    uint64_t bh = desc_act(act_base, k0);
-    tc::mma_f16_ss(d, ah, bh, idesc, k0 > 0);
-    if (nprod >= 2) tc::mma_f16_ss(d, ah, desc_act(act_lo, k0), idesc, 1);
-    if (nprod >= 3) {
-      uint64_t al = w_mn ? desc_w_mnmajor(w_base + w_lo_off, in_dim, k0)
-                         : desc_w_kmajor(w_base + w_lo_off, in_dim, k0);
-      tc::mma_f16_ss(d, al, bh, idesc, 1);
-    }
-  }
-}
 
 // ---- CSR segment sums across the 4 edge parts of a tile ----------------------
 // Each (channel, part) thread feeds its 32 edges in order: runs that start
@@ -200,14 +132,6 @@ __device__ __forceinline__ void finish_rows(int crow, float cacc, int rend, int 
 #pragma unroll 1
     for (int z = crow + 1; z < rend; ++z) out[(size_t)z * D + c] = 0.f;
   }
-}
-
-// shifted softplus and its derivative with MUFU ex2/lg2/rcp (abs. error ~1e-7)
-__device__ __forceinline__ float ssp_fast(float x) {
-  return fmaxf(x, 0.f) + __logf(1.f + __expf(-fabsf(x))) - 0.6931471805599453f;
-}
-__device__ __forceinline__ float sigmoid_fast(float x) {
-  return __fdividef(1.f, 1.f + __expf(-x));
 }
 
 // ---- per-step edge geometry (the reference's d cache, flash.py:221-223) ------

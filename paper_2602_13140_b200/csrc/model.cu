@@ -684,6 +684,7 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
   const int eg = simt ? 2 * sm_count() : sm_count();
   if (!simt) {
     edge_tc_configure();
+    node_tc_configure();
     FCG_PROF(P_EDGE_GEOM, s);
     launch_edge_geom(ea, b.geo, b.env, s);
   }
@@ -693,8 +694,11 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
     ea.blk = blk;
     {
       FCG_PROF(P_NODE_PRE, s);
-      k_node_linear<true, false><<<node_grid, NT, sm1, s>>>(b.X, blk.pre_wt, blk.pre_b, b.P[t],
-                                                           RN, quant);
+      if (simt)
+        k_node_linear<true, false><<<node_grid, NT, sm1, s>>>(b.X, blk.pre_wt, blk.pre_b, b.P[t],
+                                                             RN, quant);
+      else
+        launch_node_pre_tc(b.X, blk, quant, b.P[t], RN, s);
     }
     {
       FCG_PROF(P_EDGE_FWD, s);
@@ -705,20 +709,29 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
     }
     {
       FCG_PROF(P_NODE_POST, s);
-      k_node_post<<<node_grid, NT, sm2, s>>>(b.H, blk, b.Zp[t], b.X, RN, quant);
+      if (simt)
+        k_node_post<<<node_grid, NT, sm2, s>>>(b.H, blk, b.Zp[t], b.X, RN, quant);
+      else
+        launch_node_post_tc(b.H, blk, quant, b.Zp[t], b.X, RN, s);
     }
   }
   {
     FCG_PROF(P_READOUT, s);
-    k_readout<<<node_grid, NT, (TE * LDH + TE * LDR) * sizeof(float), s>>>(b.X, *m, per_atom,
-                                                                           b.G, RN);
+    if (simt)
+      k_readout<<<node_grid, NT, (TE * LDH + TE * LDR) * sizeof(float), s>>>(b.X, *m, per_atom,
+                                                                             b.G, RN);
+    else
+      launch_readout_tc(b.X, *m, per_atom, b.G, RN, s);
   }
   for (int t = T - 1; t >= 0; --t) {
     const fcg_block &blk = m->blocks[t];
     ea.blk = blk;
     {
       FCG_PROF(P_NODE_POST_BWD, s);
-      k_node_post_bwd<<<node_grid, NT, sm2, s>>>(b.G, blk, b.Zp[t], b.GH, RN);
+      if (simt)
+        k_node_post_bwd<<<node_grid, NT, sm2, s>>>(b.G, blk, b.Zp[t], b.GH, RN);
+      else
+        launch_node_post_bwd_tc(b.G, blk, quant, b.Zp[t], b.GH, RN, s);
     }
     {
       FCG_PROF(P_EDGE_BWD, s);
@@ -730,7 +743,10 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
     }
     {
       FCG_PROF(P_NODE_PRE_BWD, s);
-      k_node_linear<false, true><<<node_grid, NT, sm1, s>>>(b.GP, blk.pre_w, nullptr, b.G, RN, 0);
+      if (simt)
+        k_node_linear<false, true><<<node_grid, NT, sm1, s>>>(b.GP, blk.pre_w, nullptr, b.G, RN, 0);
+      else
+        launch_node_pre_bwd_tc(b.GP, blk, quant, b.G, RN, s);
     }
   }
   if (T == 0) cudaMemsetAsync(b.gsum, 0, sizeof(float4) * (size_t)(cap_e + 1), s);

@@ -238,6 +238,13 @@ class DeviceModel:
         def layers_of(net):
             return net if isinstance(net, tuple) else net.layers
 
+        def image_of(lin, shape):
+            if isinstance(lin, tuple):
+                return tc_image(_pad(lin[0], shape))
+            q = np.zeros(shape, np.float16)
+            q[:lin.weight.shape[0], :lin.weight.shape[1]] = lin.weight
+            return tc_image(None, q)
+
         m = _lib.FcgModel()
         m.format = _lib.FCG_FMT_W16 if self.quantized else _lib.FCG_FMT_FP32
         m.num_blocks = len(params.blocks)
@@ -270,17 +277,21 @@ class DeviceModel:
             put(blk, "f1", f1, D, D)
             put(blk, "p0", p0, D, D)
             put(blk, "p1", p1, D, D)
-            for name, lin, shape in (("f0", f0, (D, DR)), ("f1", f1, (D, D))):
-                if isinstance(lin, tuple):
-                    img, e = tc_image(_pad(lin[0], shape))
-                else:
-                    q = np.zeros(shape, np.float16)
-                    q[:lin.weight.shape[0], :lin.weight.shape[1]] = lin.weight
-                    img, e = tc_image(None, q)
+            for name, lin, shape in (("f0", f0, (D, DR)), ("f1", f1, (D, D)),
+                                     ("pre", bp.pre_linear, (D, D)), ("p0", p0, (D, D)),
+                                     ("p1", p1, (D, D))):
+                img, e = image_of(lin, shape)
                 setattr(blk, f"{name}_img", _lib.u16ptr(dev(img.view(np.int16), torch.int16)))
                 setattr(blk, f"{name}_exp", e)
 
         r0, r1 = layers_of(params.readout)
+        img, e = image_of(r0, (RH, D))
+        m.r0_img = _lib.u16ptr(dev(img.view(np.int16), torch.int16))
+        m.r0_exp = e
+        if not isinstance(r0, tuple):
+            sc = np.ones(RH, np.float32)
+            sc[:r0.scale.shape[0]] = r0.scale
+            m.r0_s = _lib.fptr(dev(sc))
         w0, b0 = dense(r0)
         w0p = _pad(w0, (RH, D))
         m.r0_w = _lib.fptr(dev(w0p))
