@@ -151,10 +151,13 @@ void launch_readout_tc(const float *X, const fcg_model &m, float *per_atom, floa
                        cudaStream_t s);
 // edge_tc.cu
 void edge_tc_configure();
-void launch_edge_geom(const EdgeArgs &a, float4 *geo, float2 *env, cudaStream_t s);
-void launch_edge_fwd_tc(const EdgeArgs &a, const float4 *geo, const float2 *env, const float *P,
-                        float *H, int grid, cudaStream_t s);
-void launch_edge_bwd_tc(const EdgeArgs &a, const float4 *geo, const float2 *env, const float *P,
-                        const float *GH, float *GP, float4 *gsum, int accumulate, int grid,
+int edge_tc_units(int grid);
+void launch_edge_geom(const EdgeArgs &a, float4 *geo, float2 *env, int32_t *unit_rows,
+                      int nunits, cudaStream_t s);
+void launch_edge_fwd_tc(const EdgeArgs &a, const float4 *geo, const float2 *env,
+                        const int32_t *unit_rows, const float *P, float *H, int grid,
                         cudaStream_t s);
+void launch_edge_bwd_tc(const EdgeArgs &a, const float4 *geo, const float2 *env,
+                        const int32_t *unit_rows, const float *P, const float *GH, float *GP,
+                        float4 *gsum, int accumulate, int grid, cudaStream_t s);
 }  // namespace fcg

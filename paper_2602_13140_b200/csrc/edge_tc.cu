@@ -3,24 +3,30 @@
 // Same contract as the fused edge loop of the reference (flash.py:215-236
 // forward, :272-295 backward) — edge tensors never reach HBM — but the four
 // per-edge filter-MLP GEMMs run as tcgen05.mma (kind::f16, fp32 accumulate
-// in TMEM) over 128-edge tiles.
+// in TMEM).
 //
 // Formulation ("transposed"): D[channel][edge] = W[channel][k] * X[k][edge].
 //   A = weights, resident in SMEM for the whole kernel (K-major in the
 //       forward; the SAME bytes read MN-major give W^T for the backward);
 //   B = per-tile edge activations written by the epilogue threads
-//       (MN-major: row = channel, 128 contiguous edges);
+//       (MN-major: row = channel, contiguous edges);
 //   D = TMEM, lane = channel, column = edge.
-// Every epilogue thread owns one channel across 32 consecutive edges (4
-// threads per channel), so the destination (forward) / source (backward)
-// segment reduction is a running sum per thread plus an ordered 4-way merge,
-// with a single store per CSR row — no atomics.
+//
+// Work decomposition: a CTA (one per SM, 16 warps) hosts two independent
+// groups of 8 warps.  Both groups read the same resident weights but own a
+// separate range of CSR rows, 64-edge tiles, B-operand buffer, TMEM columns,
+// mbarrier and named barrier, so one group's MMA and gather latency hides
+// under the other group's epilogue.  Inside a group every thread owns one
+// channel across 32 consecutive edges of the tile (2 threads per channel),
+// so the destination (forward) / source (backward) segment reduction is a
+// running sum per thread plus an ordered 2-way merge, with a single store
+// per CSR row — no atomics.
 //
 // fp32 parity (SURVEY §7 hard part 2): plain fp16/TF32 operands lose ~1e-3;
 // we split both operands as x*2^s = hi + lo (fp16 each, ~22 significant
 // bits) and accumulate hi*hi + hi*lo + lo*hi.  Weights carry a host-chosen
 // power-of-two prescale; activations get a per-tile power-of-two scale from
-// a block max, removed exactly in the epilogue.  W16 weights (quantize.py)
+// a group max, removed exactly in the epilogue.  W16 weights (quantize.py)
 // use the stored fp16 weights directly: one MMA in the forward (inputs
 // rounded to fp16 as the reference does), two in the backward.
 #include <cuda_fp16.h>
@@ -31,16 +37,20 @@
 
 namespace fcg {
 
-constexpr int TT = 128;          // edges per tile (MMA N)
-constexpr int TC_THREADS = 512;  // 16 warps: 4 per TMEM lane quarter
-constexpr int NPART = 4;         // edge parts per channel
-constexpr int EPT = TT / NPART;  // edges per thread
+constexpr int TT = 64;           // edges per tile (MMA N)
+constexpr int NGRP = 2;          // independent warp groups per CTA
+constexpr int GT = 256;          // threads per group (8 warps, 2 per lane quarter)
+constexpr int TC_THREADS = NGRP * GT;
+constexpr int NPART = 2;         // edge parts per channel within a group
+constexpr int EPT = TT / NPART;  // edges per thread (32)
+constexpr uint32_t KSTR = (TT / 8) * 128;  // B operand bytes per 8 K-rows
 constexpr uint32_t SM_W0 = 0;          // W0 hi|lo: 2 x 128x64 fp16
 constexpr uint32_t SM_W1 = 32768;      // W1 hi|lo: 2 x 128x128 fp16
-constexpr uint32_t SM_ACT = 98304;     // B operand hi|lo (<= 2 x 128x128 fp16) / scratch
-constexpr uint32_t SM_META = 163840;
+constexpr uint32_t SM_ACT = 98304;     // per group: B operand hi|lo (2 x 128x64 fp16) / scratch
+constexpr uint32_t ACT_BYTES = 32768;
+constexpr uint32_t SM_META = SM_ACT + NGRP * ACT_BYTES;
 constexpr uint32_t W0_BYTES = 128 * 64 * 2, W1_BYTES = 128 * 128 * 2;
-constexpr uint32_t TM_D0 = 0, TM_D1 = 128, TM_D2 = 256, TM_D3 = 384;
+constexpr uint32_t TM_D0 = 0, TM_D1 = 64, TM_D2 = 128, TM_D3 = 192;  // + 256*group
 constexpr int RED_LD = 65;       // padded stride of the [edge][k] fp32 scratch
 
 struct TcMeta {
@@ -48,13 +58,16 @@ struct TcMeta {
   float d[TT], env[TT], denv[TT];
   float4 u[TT];
   unsigned int amax[4];
-  float xch[NPART - 1][3][128];  // parts 1..3 -> part 0 segment boundary partials
+  float xch[NPART - 1][3][128];  // part 1 -> part 0 segment boundary partials
   uint64_t bar;
+};
+struct TcShared {
+  TcMeta g[NGRP];
   uint32_t tmem;
 };
-constexpr uint32_t SM_TOTAL = SM_META + sizeof(TcMeta);
+constexpr uint32_t SM_TOTAL = SM_META + sizeof(TcShared);
 
-// ---- CSR segment sums across the 4 edge parts of a tile ----------------------
+// ---- CSR segment sums across the edge parts of a tile -------------------------
 // Each (channel, part) thread feeds its 32 edges in order: runs that start
 // and end inside the part are complete and written directly (one store per
 // row, empty rows between them zeroed); the first and last run of the part
@@ -73,19 +86,41 @@ struct Runs {
     row = o;
     acc = 0.f;
   }
-  // 16 consecutive edges e0.. with values m (first `cnt` valid)
+  // 16 consecutive edges e0.. with values m (first `cnt` valid).  Rows are
+  // warp-uniform; a chunk with one row or one row change avoids per-edge
+  // branches.
   __device__ __forceinline__ void chunk(const int *own, int e0, int cnt, const float (&m)[16], int c,
                                         float *__restrict__ out) {
-    if (cnt == 16 && own[e0] == own[e0 + 15]) {  // one row: branch-free tree sum
-      int o = own[e0];
-      if (o != row) begin(o, c, out);
-      float s[8];
+    if (cnt == 16) {
+      const int o0 = own[e0], o15 = own[e0 + 15];
+      if (o0 == o15) {
+        if (o0 != row) begin(o0, c, out);
+        float s[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) s[i] = m[i] + m[i + 8];
+        for (int i = 0; i < 8; ++i) s[i] = m[i] + m[i + 8];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) s[i] += s[i + 4];
-      acc += (s[0] + s[2]) + (s[1] + s[3]);
-      return;
+        for (int i = 0; i < 4; ++i) s[i] += s[i + 4];
+        acc += (s[0] + s[2]) + (s[1] + s[3]);
+        return;
+      }
+      // first index whose row equals the chunk's last row
+      int b = 15;
+      while (b > 0 && own[e0 + b - 1] == o15) --b;
+      bool single_change = true;
+#pragma unroll 1
+      for (int i = 1; i < b; ++i) single_change &= own[e0 + i] == o0;
+      if (single_change) {
+        float lo = 0.f, hi = 0.f;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          if (i < b) lo += m[i]; else hi += m[i];
+        }
+        if (o0 != row) begin(o0, c, out);
+        acc += lo;
+        begin(o15, c, out);
+        acc += hi;
+        return;
+      }
     }
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
@@ -136,12 +171,22 @@ __device__ __forceinline__ void finish_rows(int crow, float cacc, int rend, int 
 
 // ---- per-step edge geometry (the reference's d cache, flash.py:221-223) ------
 // geo[k] = (u, d) with u = r[own] - r[nbr] for CSR slot k; env[k] = (C, C').
+// Block 0 also computes the row range of every work unit (balanced by edge
+// count) once per step for the six edge launches that follow.
 __global__ void __launch_bounds__(256)
 k_edge_geom(const float *__restrict__ pos, const int32_t *__restrict__ ptr,
             const int32_t *__restrict__ nbr, const int32_t *__restrict__ own, int nrows,
-            int64_t cap_e, float cutoff, float4 *__restrict__ geo, float2 *__restrict__ env) {
+            int64_t cap_e, float cutoff, float4 *__restrict__ geo, float2 *__restrict__ env,
+            int32_t *__restrict__ unit_rows, int nunits) {
   long long e_tot = ptr[nrows];
   if (e_tot > cap_e) e_tot = cap_e;
+  if (blockIdx.x == 0) {
+    for (int u = threadIdx.x; u <= nunits; u += blockDim.x) {
+      int rb, re;
+      cta_row_range(ptr, nrows, e_tot, u < nunits ? u : nunits - 1, nunits, rb, re);
+      unit_rows[u] = u < nunits ? rb : re;
+    }
+  }
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < e_tot;
        k += (long long)gridDim.x * blockDim.x) {
     const float *po = pos + (size_t)own[k] * 3, *pn = pos + (size_t)nbr[k] * 3;
@@ -159,7 +204,41 @@ k_edge_geom(const float *__restrict__ pos, const int32_t *__restrict__ ptr,
   }
 }
 
-// ---- shared prologue pieces ----------------------------------------------
+// ---- per-group context ---------------------------------------------------------
+struct Grp {
+  int g;              // group index
+  int gt;             // thread index within the group
+  int warp, lane, quarter, part, ch, ec;
+  int bar_id;         // named barrier of the group
+  uint32_t tl;        // TMEM address of this lane quarter + group column base
+  uint32_t sact;      // shared address of the group's B operand buffer
+  uint32_t tmem_g;    // TMEM base of the group (lane 0)
+  uint8_t *act;
+  TcMeta *meta;
+  uint32_t phase;
+  __device__ __forceinline__ void sync() const { named_sync(bar_id, GT); }
+};
+
+__device__ __forceinline__ Grp make_group(uint8_t *sm, TcShared *sh) {
+  Grp G;
+  G.g = threadIdx.x / GT;
+  G.gt = threadIdx.x % GT;
+  G.warp = G.gt >> 5;
+  G.lane = threadIdx.x & 31;
+  G.quarter = G.warp & 3;
+  G.part = G.warp >> 2;
+  G.ch = 32 * G.quarter + G.lane;
+  G.ec = EPT * G.part;
+  G.bar_id = 1 + G.g;
+  G.meta = &sh->g[G.g];
+  G.act = sm + SM_ACT + G.g * ACT_BYTES;
+  G.sact = tc::smem_u32(G.act);
+  G.tmem_g = sh->tmem + 256u * G.g;
+  G.tl = G.tmem_g + ((uint32_t)(32 * G.quarter) << 16);
+  G.phase = 0;
+  return G;
+}
+
 __device__ __forceinline__ void stage_weights(uint8_t *sm, const fcg_block &b) {
   const uint4 *s0 = (const uint4 *)b.f0_img, *s1 = (const uint4 *)b.f1_img;
   uint4 *d0 = (uint4 *)(sm + SM_W0), *d1 = (uint4 *)(sm + SM_W1);
@@ -167,10 +246,24 @@ __device__ __forceinline__ void stage_weights(uint8_t *sm, const fcg_block &b) {
   for (int q = threadIdx.x; q < (int)(2 * W1_BYTES / 16); q += TC_THREADS) d1[q] = __ldg(s1 + q);
 }
 
+__device__ __forceinline__ void kernel_prologue(uint8_t *sm, TcShared *sh, const fcg_block &B) {
+  stage_weights(sm, B);
+  if (threadIdx.x % GT == 0) {
+    tc::mbar_init(&sh->g[threadIdx.x / GT].bar, 1);
+    tc::fence_mbar_init();
+  }
+  if (threadIdx.x < 32) tc::tmem_alloc<512>(&sh->tmem);
+  tc::fence_async_smem();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+}
+
 __device__ __forceinline__ void tile_meta(const EdgeArgs &a, const float4 *__restrict__ geo,
-                                          const float2 *__restrict__ env, TcMeta *m, int t0,
+                                          const float2 *__restrict__ env, const Grp &G, int t0,
                                           int n_e, bool src_owned) {
-  int t = threadIdx.x;
+  TcMeta *m = G.meta;
+  int t = G.gt;
   if (t < TT) {
     int o = -1, n = 0;
     float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -195,32 +288,34 @@ __device__ __forceinline__ void tile_meta(const EdgeArgs &a, const float4 *__res
 
 // Basis b[k][e] (model.py:255-265) as the K=64 B operand: fp32 path scaled by
 // 2^14 and split; W16 path rounded to fp16 unscaled (quantize.py:68-71).
-__device__ __forceinline__ void tile_basis_tc(const EdgeArgs &a, const TcMeta *m, int n_e,
-                                              uint8_t *act, bool quant) {
-#pragma unroll 1
-  for (int q = threadIdx.x; q < DR * (TT / 8); q += TC_THREADS) {
+__device__ __forceinline__ void tile_basis_tc(const EdgeArgs &a, const Grp &G, int n_e,
+                                              bool quant) {
+  const TcMeta *m = G.meta;
+#pragma unroll 2
+  for (int q = G.gt; q < DR * (TT / 8); q += GT) {
     int k = q % DR, e0 = (q / DR) * 8;
     float mu = __ldg(&a.centers[k]);
+    float4 d0 = *(const float4 *)&m->d[e0], d1 = *(const float4 *)&m->d[e0 + 4];
+    float4 c0 = *(const float4 *)&m->env[e0], c1 = *(const float4 *)&m->env[e0 + 4];
+    float dd[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+    float cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
     float v[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      int e = e0 + i;
-      float dl = m->d[e] - mu;
-      v[i] = e < n_e ? __expf((-a.gamma * dl) * dl) * m->env[e] : 0.f;
+      float dl = dd[i] - mu;
+      v[i] = (e0 + i) < n_e ? __expf((-a.gamma * dl) * dl) * cc[i] : 0.f;
     }
-    put_b8(act, DR, k, e0, v, quant ? 1.f : 16384.f, !quant);
+    put_b8n(G.act, DR, KSTR, k, e0, v, quant ? 1.f : 16384.f, !quant);
   }
 }
 
-__device__ __forceinline__ uint32_t lane_base(int quarter) { return (uint32_t)(32 * quarter) << 16; }
-
-// Segment reduction of a [128 ch][128 e] fp32 tile held in TMEM columns
-// starting at tcol: every part scans, parts 1..3 publish boundary partials,
-// part 0 merges them into the carry.  Called by all threads.
-__device__ __forceinline__ void reduce_tile(uint32_t tcol, TcMeta *meta, int n_e, int part,
-                                            int ch, int &crow, float &cacc,
-                                            float *__restrict__ out) {
-  const int lo = EPT * part, hi = min(lo + EPT, n_e);
+// Segment reduction of a [128 ch][64 e] fp32 tile held in TMEM columns
+// starting at tcol: both parts scan, part 1 publishes boundary partials, part
+// 0 merges them into the carry.  Called by every thread of the group.
+__device__ __forceinline__ void reduce_tile(uint32_t tcol, const Grp &G, int n_e, int &crow,
+                                            float &cacc, float *__restrict__ out) {
+  TcMeta *meta = G.meta;
+  const int lo = EPT * G.part, hi = min(lo + EPT, n_e);
   Runs r;
   r.init();
 #pragma unroll 1
@@ -228,49 +323,68 @@ __device__ __forceinline__ void reduce_tile(uint32_t tcol, TcMeta *meta, int n_e
     float m[16];
     tc::tmem_ld16(tcol + lo + c0, m);
     tc::tmem_ld_wait();
-    r.chunk(meta->own, lo + c0, min(16, hi - lo - c0), m, ch, out);
+    r.chunk(meta->own, lo + c0, min(16, hi - lo - c0), m, G.ch, out);
   }
   r.close();
-  if (part > 0) {
-    meta->xch[part - 1][0][ch] = r.head;
-    meta->xch[part - 1][1][ch] = r.acc;
-    meta->xch[part - 1][2][ch] = __int_as_float(r.nruns);
+  if (G.part == 1) {
+    meta->xch[0][0][G.ch] = r.head;
+    meta->xch[0][1][G.ch] = r.acc;
+    meta->xch[0][2][G.ch] = __int_as_float(r.nruns);
   }
-  __syncthreads();
-  if (part == 0) {
-    merge_part(crow, cacc, r.nruns, r.head, r.acc, meta->own[0], meta->own[max(hi - 1, 0)], ch,
+  G.sync();
+  if (G.part == 0) {
+    merge_part(crow, cacc, r.nruns, r.head, r.acc, meta->own[0], meta->own[max(hi - 1, 0)], G.ch,
                out);
-#pragma unroll
-    for (int p = 1; p < NPART; ++p) {
-      const int plo = EPT * p, phi = min(plo + EPT, n_e);
-      merge_part(crow, cacc, __float_as_int(meta->xch[p - 1][2][ch]), meta->xch[p - 1][0][ch],
-                 meta->xch[p - 1][1][ch], meta->own[plo], meta->own[max(phi - 1, plo)], ch, out);
-    }
+    merge_part(crow, cacc, __float_as_int(meta->xch[0][2][G.ch]), meta->xch[0][0][G.ch],
+               meta->xch[0][1][G.ch], meta->own[EPT], meta->own[max(n_e - 1, EPT)], G.ch, out);
   }
 }
 
 // Write this thread's [ch][32 edges] fp32 TMEM block as the hi/lo fp16 B
-// operand of the next GEMM with the given scale.
-__device__ __forceinline__ void tmem_to_act(uint32_t tcol, uint8_t *act, int part, int ch,
-                                            float scale, bool with_lo) {
+// operand (K = 128 rows) of the next GEMM with the given scale.
+__device__ __forceinline__ void tmem_to_act(uint32_t tcol, const Grp &G, float scale,
+                                            bool with_lo) {
 #pragma unroll 1
   for (int c0 = 0; c0 < EPT; c0 += 16) {
     float v[16];
-    tc::tmem_ld16(tcol + EPT * part + c0, v);
+    tc::tmem_ld16(tcol + G.ec + c0, v);
     tc::tmem_ld_wait();
-    put_b8(act, D, ch, EPT * part + c0, &v[0], scale, with_lo);
-    put_b8(act, D, ch, EPT * part + c0 + 8, &v[8], scale, with_lo);
+    put_b8n(G.act, D, KSTR, G.ch, G.ec + c0, &v[0], scale, with_lo);
+    put_b8n(G.act, D, KSTR, G.ch, G.ec + c0 + 8, &v[8], scale, with_lo);
   }
 }
 
-struct TileRange {
+// all threads of the group: make the act writes visible to the tensor core,
+// then the group's first thread issues the GEMM and commits it
+#define GRP_ISSUE(...)                  \
+  do {                                  \
+    tc::fence_async_smem();             \
+    tc::fence_before_sync();            \
+    G.sync();                           \
+    if (G.gt == 0) {                    \
+      tc::fence_after_sync();           \
+      issue_gemm(__VA_ARGS__, KSTR);    \
+      tc::mma_commit(&G.meta->bar);     \
+    }                                   \
+  } while (0)
+
+#define GRP_WAIT()                          \
+  do {                                      \
+    tc::mbar_wait(&G.meta->bar, G.phase);   \
+    G.phase ^= 1;                           \
+    tc::fence_after_sync();                 \
+  } while (0)
+
+struct UnitRange {
   int rbeg, rend, eb, ee;
 };
-__device__ __forceinline__ TileRange cta_tiles(const EdgeArgs &a) {
-  TileRange t;
+__device__ __forceinline__ UnitRange unit_range(const EdgeArgs &a, const int32_t *unit_rows,
+                                                int unit) {
+  UnitRange t;
   const int e_tot = a.ptr[a.nrows];
   const long long eff = e_tot > a.cap_e ? a.cap_e : e_tot;
-  cta_row_range(a.ptr, a.nrows, eff, blockIdx.x, gridDim.x, t.rbeg, t.rend);
+  t.rbeg = unit_rows[unit];
+  t.rend = unit_rows[unit + 1];
   t.eb = a.ptr[t.rbeg];
   t.ee = a.ptr[t.rend];
   if (t.ee > eff) t.ee = (int)eff;
@@ -278,92 +392,52 @@ __device__ __forceinline__ TileRange cta_tiles(const EdgeArgs &a) {
   return t;
 }
 
-__device__ __forceinline__ void kernel_prologue(uint8_t *sm, TcMeta *meta, const fcg_block &B) {
-  stage_weights(sm, B);
-  if (threadIdx.x == 0) {
-    tc::mbar_init(&meta->bar, 1);
-    tc::fence_mbar_init();
-  }
-  if (threadIdx.x < 32) tc::tmem_alloc<512>(&meta->tmem);
-  tc::fence_async_smem();
-  tc::fence_before_sync();
-  __syncthreads();
-  tc::fence_after_sync();
-}
-
-// all threads: make the act writes visible to the tensor core, then thread 0
-// issues the GEMM and commits it to the mbarrier
-#define FCG_ISSUE(...)                  \
-  do {                                  \
-    tc::fence_async_smem();             \
-    tc::fence_before_sync();            \
-    __syncthreads();                    \
-    if (threadIdx.x == 0) {             \
-      tc::fence_after_sync();           \
-      issue_gemm(__VA_ARGS__);          \
-      tc::mma_commit(&meta->bar);       \
-    }                                   \
-  } while (0)
-
-#define FCG_WAIT()                      \
-  do {                                  \
-    tc::mbar_wait(&meta->bar, phase);   \
-    phase ^= 1;                         \
-    tc::fence_after_sync();             \
-  } while (0)
-
 // ---------------------------------------------------------------------------
-// Forward: per 128-edge tile of dst rows
+// Forward: per 64-edge tile of dst rows
 //   b -> [GEMM1] z0 -> h=ssp(z0) -> [GEMM2] w -> m = P[src]*w -> H rows.
 // The P[src] gather is issued right after GEMM1 so its latency hides under
 // the tensor-core work; h and m are staged back into TMEM so every epilogue
 // pass streams 16 columns at a time.
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_edge_fwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__restrict__ env,
-              const float *__restrict__ P, float *__restrict__ H) {
+              const int32_t *__restrict__ unit_rows, const float *__restrict__ P,
+              float *__restrict__ H) {
   extern __shared__ __align__(1024) uint8_t sm[];
-  TcMeta *meta = (TcMeta *)(sm + SM_META);
-  uint8_t *act = sm + SM_ACT;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int quarter = warp & 3, part = warp >> 2;
-  const int ch = 32 * quarter + lane;
-  const int ec = EPT * part;  // this thread's first edge column
+  TcShared *sh = (TcShared *)(sm + SM_META);
   const bool quant = a.quant != 0;
   const fcg_block &B = a.blk;
-
-  kernel_prologue(sm, meta, B);
-  const uint32_t tm = meta->tmem;
-  const uint32_t tl = tm + lane_base(quarter);
+  kernel_prologue(sm, sh, B);
+  Grp G = make_group(sm, sh);
   const uint32_t sbase = tc::smem_u32(sm);
   const uint32_t idesc = tc::idesc_f16(128, TT, 0, 1);
   const int nprod = quant ? 1 : 3;
-  uint32_t phase = 0;
 
-  const TileRange tr = cta_tiles(a);
+  const UnitRange tr = unit_range(a, unit_rows, NGRP * blockIdx.x + G.g);
   int crow = tr.rbeg;
   float cacc = 0.f;
 
+  const int ch = G.ch, ec = G.ec;
   const float b0c = __ldg(&B.f0_b[ch]), b1c = __ldg(&B.f1_b[ch]);
   const float rs0 = quant ? __ldg(&B.f0_s[ch]) : pow2f(-(B.f0_exp + 14));
   const float rs1 = quant ? __ldg(&B.f1_s[ch]) : 1.f;
 
   for (int t0 = tr.eb; t0 < tr.ee; t0 += TT) {
     const int n_e = min(TT, tr.ee - t0);
-    tile_meta(a, geo, env, meta, t0, n_e, false);
-    __syncthreads();
-    tile_basis_tc(a, meta, n_e, act, quant);
-    FCG_ISSUE(tm + TM_D0, sbase + SM_W0, W0_BYTES, DR, false, sbase + SM_ACT, DR, idesc, nprod);
+    tile_meta(a, geo, env, G, t0, n_e, false);
+    G.sync();
+    tile_basis_tc(a, G, n_e, quant);
+    GRP_ISSUE(G.tmem_g + TM_D0, sbase + SM_W0, W0_BYTES, DR, false, G.sact, DR, idesc, nprod);
     float pv[EPT];  // P[src][ch] of this thread's edges, in flight during the MMAs
 #pragma unroll
-    for (int i = 0; i < EPT; ++i) pv[i] = __ldg(&P[(size_t)meta->nbr[ec + i] * D + ch]);
-    FCG_WAIT();
+    for (int i = 0; i < EPT; ++i) pv[i] = __ldg(&P[(size_t)G.meta->nbr[ec + i] * D + ch]);
+    GRP_WAIT();
 
     // epilogue 1: h = ssp(W0 b + b0), staged in place in D0, then -> B of GEMM2
     float mx = 0.f;
 #pragma unroll
     for (int c0 = 0; c0 < EPT; c0 += 16) {
       float v[16];
-      tc::tmem_ld16(tl + TM_D0 + ec + c0, v);
+      tc::tmem_ld16(G.tl + TM_D0 + ec + c0, v);
       tc::tmem_ld_wait();
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
@@ -372,36 +446,36 @@ k_edge_fwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
         v[i] = (ec + c0 + i) < n_e ? h : 0.f;
         mx = fmaxf(mx, fabsf(v[i]));
       }
-      tc::tmem_st16(tl + TM_D0 + ec + c0, v);
+      tc::tmem_st16(G.tl + TM_D0 + ec + c0, v);
     }
     tc::tmem_st_wait();
-    int sh = 0;
-    if (!quant) sh = scale_exp(block_amax(mx, &meta->amax[0]));
-    tmem_to_act(tl + TM_D0, act, part, ch, pow2f(sh), !quant);
-    FCG_ISSUE(tm + TM_D1, sbase + SM_W1, W1_BYTES, D, false, sbase + SM_ACT, D, idesc, nprod);
-    FCG_WAIT();
+    int sh_ = 0;
+    if (!quant) sh_ = scale_exp(group_amax(mx, &G.meta->amax[0], G.bar_id, GT));
+    tmem_to_act(G.tl + TM_D0, G, pow2f(sh_), !quant);
+    GRP_ISSUE(G.tmem_g + TM_D1, sbase + SM_W1, W1_BYTES, D, false, G.sact, D, idesc, nprod);
+    GRP_WAIT();
 
     // epilogue 2: m = (W1 h + b1) * P[src] (flash.py:229), in place in D1,
     // then dst segment sums (flash.py:232-234)
-    const float s1 = quant ? rs1 : pow2f(-(B.f1_exp + sh));
+    const float s1 = quant ? rs1 : pow2f(-(B.f1_exp + sh_));
 #pragma unroll
     for (int c = 0; c < EPT / 16; ++c) {
       float v[16];
-      tc::tmem_ld16(tl + TM_D1 + ec + 16 * c, v);
+      tc::tmem_ld16(G.tl + TM_D1 + ec + 16 * c, v);
       tc::tmem_ld_wait();
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] = (v[i] * s1 + b1c) * pv[16 * c + i];
-      tc::tmem_st16(tl + TM_D1 + ec + 16 * c, v);
+      tc::tmem_st16(G.tl + TM_D1 + ec + 16 * c, v);
     }
     tc::tmem_st_wait();
-    reduce_tile(tl + TM_D1, meta, n_e, part, ch, crow, cacc, H);
+    reduce_tile(G.tl + TM_D1, G, n_e, crow, cacc, H);
     tc::fence_before_sync();
-    __syncthreads();
+    G.sync();
   }
-  if (part == 0) finish_rows(crow, cacc, tr.rend, ch, H);
+  if (G.part == 0) finish_rows(crow, cacc, tr.rend, ch, H);
   tc::fence_before_sync();
   __syncthreads();
-  if (threadIdx.x < 32) tc::tmem_dealloc<512>(tm);
+  if (threadIdx.x < 32) tc::tmem_dealloc<512>(sh->tmem);
 }
 
 // ---------------------------------------------------------------------------
@@ -410,37 +484,31 @@ k_edge_fwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
 //   [G3] grad_h = grad_w W1 -> gz = grad_h*ssp'(z0) -> [G4] grad_b = gz W0
 //   -> grad_d = sum_k grad_b*db -> g_e = grad_d/d * u  (gsum, owner slot);
 //   grad_P rows = src-segment sums of gH*w (computed while G3 runs).
-// TMEM: D0 z0 (then gz), D1 w (then gH*w), D2 h (then grad_h), D3 grad_w
-// stash (then grad_b from G4).
+// TMEM (per group): D0 z0 (then gz), D1 w (then gH*w), D2 h (then grad_h),
+// D3 grad_w stash (then grad_b from G4).
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__restrict__ env,
-              const float *__restrict__ P, const float *__restrict__ GH, float *__restrict__ GP,
-              float4 *__restrict__ gsum, int accumulate) {
+              const int32_t *__restrict__ unit_rows, const float *__restrict__ P,
+              const float *__restrict__ GH, float *__restrict__ GP, float4 *__restrict__ gsum,
+              int accumulate) {
   extern __shared__ __align__(1024) uint8_t sm[];
-  TcMeta *meta = (TcMeta *)(sm + SM_META);
-  uint8_t *act = sm + SM_ACT;
-  float *red_s = (float *)(sm + SM_ACT);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int quarter = warp & 3, part = warp >> 2;
-  const int ch = 32 * quarter + lane;
-  const int ec = EPT * part;
+  TcShared *sh = (TcShared *)(sm + SM_META);
   const bool quant = a.quant != 0;
   const fcg_block &B = a.blk;
-
-  kernel_prologue(sm, meta, B);
-  const uint32_t tm = meta->tmem;
-  const uint32_t tl = tm + lane_base(quarter);
+  kernel_prologue(sm, sh, B);
+  Grp G = make_group(sm, sh);
+  float *red_s = (float *)G.act;
   const uint32_t sbase = tc::smem_u32(sm);
   const uint32_t idesc_fwd = tc::idesc_f16(128, TT, 0, 1);
   const uint32_t idesc_g3 = tc::idesc_f16(128, TT, 1, 1);
   const uint32_t idesc_g4 = tc::idesc_f16(64, TT, 1, 1);
   const int nprod_f = quant ? 1 : 3, nprod_b = quant ? 2 : 3;
-  uint32_t phase = 0;
 
-  const TileRange tr = cta_tiles(a);
+  const UnitRange tr = unit_range(a, unit_rows, NGRP * blockIdx.x + G.g);
   int crow = tr.rbeg;
   float cacc = 0.f;
 
+  const int ch = G.ch, ec = G.ec;
   const float b0c = __ldg(&B.f0_b[ch]), b1c = __ldg(&B.f1_b[ch]);
   const float rs0 = quant ? __ldg(&B.f0_s[ch]) : pow2f(-(B.f0_exp + 14));
   const float rs1 = quant ? __ldg(&B.f1_s[ch]) : 1.f;
@@ -452,10 +520,10 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
 
   for (int t0 = tr.eb; t0 < tr.ee; t0 += TT) {
     const int n_e = min(TT, tr.ee - t0);
-    tile_meta(a, geo, env, meta, t0, n_e, true);
-    __syncthreads();
-    tile_basis_tc(a, meta, n_e, act, quant);
-    FCG_ISSUE(tm + TM_D0, sbase + SM_W0, W0_BYTES, DR, false, sbase + SM_ACT, DR, idesc_fwd,
+    tile_meta(a, geo, env, G, t0, n_e, true);
+    G.sync();
+    tile_basis_tc(a, G, n_e, quant);
+    GRP_ISSUE(G.tmem_g + TM_D0, sbase + SM_W0, W0_BYTES, DR, false, G.sact, DR, idesc_fwd,
               nprod_f);
     // while G1 runs: grad_w[c][e] = gH * P[src][c] (flash.py:291) into the
     // D3 stash (G4 overwrites D3 only after grad_w is consumed) + tile max
@@ -468,22 +536,23 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
         int e = ec + c0 + i;
         float g = 0.f;
         if (e < n_e)
-          g = __ldg(&GH[(size_t)meta->nbr[e] * D + ch]) * __ldg(&P[(size_t)meta->own[e] * D + ch]);
+          g = __ldg(&GH[(size_t)G.meta->nbr[e] * D + ch]) *
+              __ldg(&P[(size_t)G.meta->own[e] * D + ch]);
         v[i] = g * q1;
         mx = fmaxf(mx, fabsf(v[i]));
       }
-      tc::tmem_st16(tl + TM_D3 + ec + c0, v);
+      tc::tmem_st16(G.tl + TM_D3 + ec + c0, v);
     }
     tc::tmem_st_wait();
-    const int sg = scale_exp(block_amax(mx, &meta->amax[1]));
-    FCG_WAIT();
+    const int sg = scale_exp(group_amax(mx, &G.meta->amax[1], G.bar_id, GT));
+    GRP_WAIT();
 
     // recompute h = ssp(z0) into D2 (free until G3); z0 stays in D0
     mx = 0.f;
 #pragma unroll
     for (int c0 = 0; c0 < EPT; c0 += 16) {
       float v[16];
-      tc::tmem_ld16(tl + TM_D0 + ec + c0, v);
+      tc::tmem_ld16(G.tl + TM_D0 + ec + c0, v);
       tc::tmem_ld_wait();
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
@@ -492,37 +561,37 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
         v[i] = (ec + c0 + i) < n_e ? h : 0.f;
         mx = fmaxf(mx, fabsf(v[i]));
       }
-      tc::tmem_st16(tl + TM_D2 + ec + c0, v);
+      tc::tmem_st16(G.tl + TM_D2 + ec + c0, v);
     }
     tc::tmem_st_wait();
-    int sh = 0;
-    if (!quant) sh = scale_exp(block_amax(mx, &meta->amax[0]));
-    tmem_to_act(tl + TM_D2, act, part, ch, pow2f(sh), !quant);
-    FCG_ISSUE(tm + TM_D1, sbase + SM_W1, W1_BYTES, D, false, sbase + SM_ACT, D, idesc_fwd,
+    int sh_ = 0;
+    if (!quant) sh_ = scale_exp(group_amax(mx, &G.meta->amax[0], G.bar_id, GT));
+    tmem_to_act(G.tl + TM_D2, G, pow2f(sh_), !quant);
+    GRP_ISSUE(G.tmem_g + TM_D1, sbase + SM_W1, W1_BYTES, D, false, G.sact, D, idesc_fwd,
               nprod_f);
-    FCG_WAIT();
+    GRP_WAIT();
 
     // grad_w (stashed in D3) -> B operand of G3
-    tmem_to_act(tl + TM_D3, act, part, ch, pow2f(sg), true);
-    FCG_ISSUE(tm + TM_D2, sbase + SM_W1, W1_BYTES, D, true, sbase + SM_ACT, D, idesc_g3, nprod_b);
+    tmem_to_act(G.tl + TM_D3, G, pow2f(sg), true);
+    GRP_ISSUE(G.tmem_g + TM_D2, sbase + SM_W1, W1_BYTES, D, true, G.sact, D, idesc_g3, nprod_b);
     // while G3 runs: grad_P rows = src-segment sums of gH * w (flash.py:283-288)
     {
-      const float s1 = quant ? rs1 : pow2f(-(B.f1_exp + sh));
+      const float s1 = quant ? rs1 : pow2f(-(B.f1_exp + sh_));
 #pragma unroll
       for (int c0 = 0; c0 < EPT; c0 += 16) {
         float v[16], g[16];
-        tc::tmem_ld16(tl + TM_D1 + ec + c0, v);
+        tc::tmem_ld16(G.tl + TM_D1 + ec + c0, v);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) g[i] = __ldg(&GH[(size_t)meta->nbr[ec + c0 + i] * D + ch]);
+        for (int i = 0; i < 16; ++i) g[i] = __ldg(&GH[(size_t)G.meta->nbr[ec + c0 + i] * D + ch]);
         tc::tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = g[i] * (v[i] * s1 + b1c);
-        tc::tmem_st16(tl + TM_D1 + ec + c0, v);
+        tc::tmem_st16(G.tl + TM_D1 + ec + c0, v);
       }
       tc::tmem_st_wait();
-      reduce_tile(tl + TM_D1, meta, n_e, part, ch, crow, cacc, GP);
+      reduce_tile(G.tl + TM_D1, G, n_e, crow, cacc, GP);
     }
-    FCG_WAIT();
+    GRP_WAIT();
 
     // gz = grad_h * ssp'(z0) (mlp_backward_input, model.py:326-331), in place in D0
     {
@@ -531,8 +600,8 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
 #pragma unroll
       for (int c0 = 0; c0 < EPT; c0 += 16) {
         float gh[16], z[16];
-        tc::tmem_ld16(tl + TM_D2 + ec + c0, gh);
-        tc::tmem_ld16(tl + TM_D0 + ec + c0, z);
+        tc::tmem_ld16(G.tl + TM_D2 + ec + c0, gh);
+        tc::tmem_ld16(G.tl + TM_D0 + ec + c0, z);
         tc::tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
@@ -541,50 +610,50 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
           z[i] = g;
           mx = fmaxf(mx, fabsf(g));
         }
-        tc::tmem_st16(tl + TM_D0 + ec + c0, z);
+        tc::tmem_st16(G.tl + TM_D0 + ec + c0, z);
       }
       tc::tmem_st_wait();
-      sh = scale_exp(block_amax(mx, &meta->amax[2]));
-      tmem_to_act(tl + TM_D0, act, part, ch, pow2f(sh), true);
-      FCG_ISSUE(tm + TM_D3, sbase + SM_W0, W0_BYTES, DR, true, sbase + SM_ACT, D, idesc_g4,
+      sh_ = scale_exp(group_amax(mx, &G.meta->amax[2], G.bar_id, GT));
+      tmem_to_act(G.tl + TM_D0, G, pow2f(sh_), true);
+      GRP_ISSUE(G.tmem_g + TM_D3, sbase + SM_W0, W0_BYTES, DR, true, G.sact, D, idesc_g4,
                 nprod_b);
     }
-    FCG_WAIT();
+    GRP_WAIT();
 
     // grad_d[e] = sum_k grad_b[k][e] * db[k][e] (flash.py:293).  M=64 D lives
     // in lanes 32q + (0..15) of each quarter: row k = 16q + lane.
     {
-      const int k = 16 * quarter + (lane & 15);
+      const int k = 16 * G.quarter + (G.lane & 15);
       const float mu = __ldg(&a.centers[k]);
-      const float s4 = pow2f(-(ew0 + sh));
+      const float s4 = pow2f(-(ew0 + sh_));
       const float g2 = -2.f * a.gamma;
 #pragma unroll
       for (int c0 = 0; c0 < EPT; c0 += 16) {
         float gb[16];
-        tc::tmem_ld16(tl + TM_D3 + ec + c0, gb);
+        tc::tmem_ld16(G.tl + TM_D3 + ec + c0, gb);
         tc::tmem_ld_wait();
-        if (lane < 16) {
+        if (G.lane < 16) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             int e = ec + c0 + i;
-            float dl = meta->d[e] - mu;
+            float dl = G.meta->d[e] - mu;
             float gs = __expf((-a.gamma * dl) * dl);
-            float db = gs * (g2 * dl * meta->env[e] + meta->denv[e]);  // model.py:289
+            float db = gs * (g2 * dl * G.meta->env[e] + G.meta->denv[e]);  // model.py:289
             red_s[e * RED_LD + k] = gb[i] * s4 * db;
           }
         }
       }
     }
-    __syncthreads();
-    if (threadIdx.x < TT && threadIdx.x < n_e) {
-      const int e = threadIdx.x;
+    G.sync();
+    if (G.gt < TT && G.gt < n_e) {
+      const int e = G.gt;
       float gd = 0.f;
 #pragma unroll 8
       for (int k = 0; k < DR; ++k) gd += red_s[e * RED_LD + k];
-      float d = meta->d[e];
+      float d = G.meta->d[e];
       float inv = d > TINY_DISTANCE ? 1.f / d : 0.f;  // _safe_inv, flash.py:176-178
       float s = gd * inv;
-      float4 u = meta->u[e];
+      float4 u = G.meta->u[e];
       float4 g = make_float4(s * u.x, s * u.y, s * u.z, 0.f);
       float4 *dst = &gsum[t0 + e];
       if (accumulate) {
@@ -594,12 +663,12 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
       *dst = g;
     }
     tc::fence_before_sync();
-    __syncthreads();
+    G.sync();
   }
-  if (part == 0) finish_rows(crow, cacc, tr.rend, ch, GP);
+  if (G.part == 0) finish_rows(crow, cacc, tr.rend, ch, GP);
   tc::fence_before_sync();
   __syncthreads();
-  if (threadIdx.x < 32) tc::tmem_dealloc<512>(tm);
+  if (threadIdx.x < 32) tc::tmem_dealloc<512>(sh->tmem);
 }
 
 void edge_tc_configure() {
@@ -612,21 +681,25 @@ void edge_tc_configure() {
   done = true;
 }
 
-void launch_edge_geom(const EdgeArgs &a, float4 *geo, float2 *env, cudaStream_t s) {
+int edge_tc_units(int grid) { return NGRP * grid; }
+
+void launch_edge_geom(const EdgeArgs &a, float4 *geo, float2 *env, int32_t *unit_rows,
+                      int nunits, cudaStream_t s) {
   k_edge_geom<<<1184, 256, 0, s>>>(a.pos, a.ptr, a.nbr, a.own, a.nrows, a.cap_e, a.cutoff, geo,
-                                   env);
+                                   env, unit_rows, nunits);
 }
 
-void launch_edge_fwd_tc(const EdgeArgs &a, const float4 *geo, const float2 *env, const float *P,
-                        float *H, int grid, cudaStream_t s) {
-  k_edge_fwd_tc<<<grid, TC_THREADS, SM_TOTAL + 1024, s>>>(a, geo, env, P, H);
-}
-
-void launch_edge_bwd_tc(const EdgeArgs &a, const float4 *geo, const float2 *env, const float *P,
-                        const float *GH, float *GP, float4 *gsum, int accumulate, int grid,
+void launch_edge_fwd_tc(const EdgeArgs &a, const float4 *geo, const float2 *env,
+                        const int32_t *unit_rows, const float *P, float *H, int grid,
                         cudaStream_t s) {
-  k_edge_bwd_tc<<<grid, TC_THREADS, SM_TOTAL + 1024, s>>>(a, geo, env, P, GH, GP, gsum,
-                                                         accumulate);
+  k_edge_fwd_tc<<<grid, TC_THREADS, SM_TOTAL + 1024, s>>>(a, geo, env, unit_rows, P, H);
+}
+
+void launch_edge_bwd_tc(const EdgeArgs &a, const float4 *geo, const float2 *env,
+                        const int32_t *unit_rows, const float *P, const float *GH, float *GP,
+                        float4 *gsum, int accumulate, int grid, cudaStream_t s) {
+  k_edge_bwd_tc<<<grid, TC_THREADS, SM_TOTAL + 1024, s>>>(a, geo, env, unit_rows, P, GH, GP,
+                                                         gsum, accumulate);
 }
 
 }  // namespace fcg

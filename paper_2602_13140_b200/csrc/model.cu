@@ -600,6 +600,7 @@ struct EfBuffers {
   float4 *gsum;
   float4 *geo;
   float2 *env;
+  int32_t *unit_rows;
 };
 
 static EfBuffers carve_ef(Carver &c, int T, size_t RN, int64_t cap_e) {
@@ -617,6 +618,7 @@ static EfBuffers carve_ef(Carver &c, int T, size_t RN, int64_t cap_e) {
   b.gsum = c.take<float4>((size_t)cap_e + 1);
   b.geo = c.take<float4>((size_t)cap_e + 1);
   b.env = c.take<float2>((size_t)cap_e + 1);
+  b.unit_rows = c.take<int32_t>(4096);
   return b;
 }
 
@@ -686,7 +688,7 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
     edge_tc_configure();
     node_tc_configure();
     FCG_PROF(P_EDGE_GEOM, s);
-    launch_edge_geom(ea, b.geo, b.env, s);
+    launch_edge_geom(ea, b.geo, b.env, b.unit_rows, edge_tc_units(eg), s);
   }
 
   for (int t = 0; t < T; ++t) {
@@ -705,7 +707,7 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
       if (simt)
         k_edge_fwd<<<eg, NT, (TE * LDR + TE * LDH) * sizeof(float), s>>>(ea, b.P[t], b.H);
       else
-        launch_edge_fwd_tc(ea, b.geo, b.env, b.P[t], b.H, eg, s);
+        launch_edge_fwd_tc(ea, b.geo, b.env, b.unit_rows, b.P[t], b.H, eg, s);
     }
     {
       FCG_PROF(P_NODE_POST, s);
@@ -739,7 +741,8 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
         k_edge_bwd<<<eg, NT, 3 * TE * LDH * sizeof(float), s>>>(ea, b.P[t], b.GH, b.GP, b.gsum,
                                                                t != T - 1);
       else
-        launch_edge_bwd_tc(ea, b.geo, b.env, b.P[t], b.GH, b.GP, b.gsum, t != T - 1, eg, s);
+        launch_edge_bwd_tc(ea, b.geo, b.env, b.unit_rows, b.P[t], b.GH, b.GP, b.gsum, t != T - 1,
+                           eg, s);
     }
     {
       FCG_PROF(P_NODE_PRE_BWD, s);

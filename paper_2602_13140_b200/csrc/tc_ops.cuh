@@ -27,8 +27,39 @@ __device__ __forceinline__ float block_amax(float v, unsigned int *slot) {
   return __uint_as_float(*slot);
 }
 
-// Store 8 consecutive edges e0..e0+7 of K-row r of an MN-major B operand
-// (hi image at act, lo image at act + K*256 bytes), values pre-scaled.
+// Named barrier over a subset of the CTA (id 1.. ; id 0 is __syncthreads).
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Max over the threads of one named-barrier group.
+__device__ __forceinline__ float group_amax(float v, unsigned int *slot, int bar_id, int nthreads) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(slot, __float_as_uint(v));
+  named_sync(bar_id, nthreads);
+  return __uint_as_float(*slot);
+}
+
+// Store 8 consecutive columns e0..e0+7 of K-row r of an MN-major B operand
+// with N columns (kstride = bytes per 8 K-rows = 16*N; hi image at act, lo
+// image at act + K*kstride/8), values pre-scaled.
+__device__ __forceinline__ void put_b8n(uint8_t *act, int K, uint32_t kstride, int r, int e0,
+                                        const float *v, float scale, bool with_lo) {
+  uint32_t off = (uint32_t)(r >> 3) * kstride + (uint32_t)(e0 >> 3) * 128u + (uint32_t)(r & 7) * 16u;
+  __half2 hi[4], lo[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float a = v[2 * i] * scale, b = v[2 * i + 1] * scale;
+    hi[i] = __floats2half2_rn(a, b);
+    float2 hf = __half22float2(hi[i]);
+    lo[i] = __floats2half2_rn(a - hf.x, b - hf.y);
+  }
+  *(uint4 *)(act + off) = *(uint4 *)hi;
+  if (with_lo) *(uint4 *)(act + (uint32_t)K * (kstride >> 3) + off) = *(uint4 *)lo;
+}
+
+// N=128 variant (kstride 2048).
 __device__ __forceinline__ void put_b8(uint8_t *act, int K, int r, int e0, const float *v,
                                        float scale, bool with_lo) {
   uint32_t off = (uint32_t)(r >> 3) * 2048u + (uint32_t)(e0 >> 3) * 128u + (uint32_t)(r & 7) * 16u;
@@ -53,22 +84,23 @@ __device__ __forceinline__ uint64_t desc_w_mnmajor(uint32_t base, int in_dim, in
   uint32_t rowstride = (uint32_t)(in_dim >> 3) * 128u;
   return tc::smem_desc(base + (uint32_t)(k0 >> 3) * rowstride, rowstride, 128u);
 }
-__device__ __forceinline__ uint64_t desc_act(uint32_t base, int k0) {
-  return tc::smem_desc(base + (uint32_t)(k0 >> 3) * 2048u, 2048u, 128u);
+__device__ __forceinline__ uint64_t desc_act(uint32_t base, int k0, uint32_t kstride = 2048u) {
+  return tc::smem_desc(base + (uint32_t)(k0 >> 3) * kstride, kstride, 128u);
 }
 
 // Issue one GEMM D(tmem) = A(weights) x B(act) over K, with the product set
 // {hi*hi, hi*lo, lo*hi} (nprod=3), {hi*hi, hi*lo} (2) or {hi*hi} (1).
 __device__ __forceinline__ void issue_gemm(uint32_t d, uint32_t w_base, uint32_t w_lo_off,
                                            int in_dim, bool w_mn, uint32_t act_base, int K,
-                                           uint32_t idesc, int nprod) {
-  uint32_t act_lo = act_base + (uint32_t)K * 256u;
+                                           uint32_t idesc, int nprod,
+                                           uint32_t kstride = 2048u) {
+  uint32_t act_lo = act_base + (uint32_t)K * (kstride >> 3);
 #pragma unroll 1
   for (int k0 = 0; k0 < K; k0 += 16) {
     uint64_t ah = w_mn ? desc_w_mnmajor(w_base, in_dim, k0) : desc_w_kmajor(w_base, in_dim, k0);
-    uint64_t bh = desc_act(act_base, k0);
+    uint64_t bh = desc_act(act_base, k0, kstride);
     tc::mma_f16_ss(d, ah, bh, idesc, k0 > 0);
-    if (nprod >= 2) tc::mma_f16_ss(d, ah, desc_act(act_lo, k0), idesc, 1);
+    if (nprod >= 2) tc::mma_f16_ss(d, ah, desc_act(act_lo, k0, kstride), idesc, 1);
     if (nprod >= 3) {
       uint64_t al = w_mn ? desc_w_mnmajor(w_base + w_lo_off, in_dim, k0)
                          : desc_w_kmajor(w_base + w_lo_off, in_dim, k0);
