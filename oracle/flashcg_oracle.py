@@ -268,10 +268,12 @@ def kinetic_temperature(vel, masses):
     return 2.0 * ke / (3 * vel.shape[1] * KB)
 
 
-def replica_forces(params, types, prior, positions, workers=1):
-    """Per-replica model + prior forces (md.py:243-273)."""
+def replica_forces(params, types, prior, positions, workers=1, edges=None):
+    """Per-replica model + prior forces (md.py:243-273); `edges` optionally
+    gives a cached (src, dst) per replica (neighbor_stride > 1)."""
     def one(rep):
-        e, _, f = energy_forces(positions[rep], types, params)
+        e, _, f = energy_forces(positions[rep], types, params,
+                                edges=None if edges is None else edges[rep])
         ep, fp = prior_energy_forces(positions[rep], prior)
         return e, ep, f + fp
     reps = range(positions.shape[0])
@@ -286,20 +288,24 @@ def replica_forces(params, types, prior, positions, workers=1):
 
 def run_md(params, types, masses, prior, positions, velocities, n_steps, dt_fs=4.0,
            temperature=300.0, friction=1.0, seed=0, step0=0, rep_offset=0, workers=1,
-           record=False):
+           record=False, neighbor_stride=1):
     """BAOAB loop with one force evaluation per step (md.py:188-208).
     Returns (positions, velocities, forces, potential, prior, trace)."""
     pos = np.array(positions, dtype=np.float32)
     vel = np.array(velocities, dtype=np.float32)
     R, N = pos.shape[0], pos.shape[1]
-    F, pot, pri = replica_forces(params, types, prior, pos, workers)
+    cut = params.config.cutoff
+    cache = [neighbor_list(pos[r], cut) for r in range(R)]
+    F, pot, pri = replica_forces(params, types, prior, pos, workers, edges=cache)
     trace = [(step0, pot, pri)] if record else None
     step = step0
     for _ in range(n_steps):
         xi = np.stack([noise(seed, rep_offset + r, step, N) for r in range(R)])
         pos, vel = baoa(pos, vel, F, masses, xi, dt_fs, temperature, friction)
         step += 1
-        F, pot, pri = replica_forces(params, types, prior, pos, workers)
+        if step % max(neighbor_stride, 1) == 0:  # md.py:245-250
+            cache = [neighbor_list(pos[r], cut) for r in range(R)]
+        F, pot, pri = replica_forces(params, types, prior, pos, workers, edges=cache)
         vel = half_kick(vel, F, masses, dt_fs)
         if record:
             trace.append((step, pot, pri))

@@ -184,7 +184,8 @@ int fcg_md_step(const fcg_model *m, const fcg_prior *pr, const fcg_md_params *p,
   if ((rc = langevin_baoa(p, mass, R, N, forces, noise, pos, vel, s))) return rc;
   if ((rc = step_advance(step, s))) return rc;
   // force evaluation at the new positions (md.py:203, _ReplicaForces)
-  if ((rc = nbr_build(pos, R, N, r_cut, cap_e, ptr, nbr, rev, own, status, ws_nbr, nb, s)))
+  if ((rc = nbr_build(pos, R, N, r_cut, cap_e, ptr, nbr, rev, own, status, ws_nbr, nb, s, step,
+                      p->neighbor_stride)))
     return rc;
   if ((rc = prior_forces(pr, pos, R, N, prior, fprior, s))) return rc;
   // model forces + prior, blow-up check and the trailing half-kick (md.py:204-205)

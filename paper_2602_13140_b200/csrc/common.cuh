@@ -108,7 +108,7 @@ namespace fcg {
 size_t nbr_ws_bytes(int R, int N);
 int nbr_build(const float *pos, int R, int N, double r_cut, int64_t cap_e, int32_t *ptr,
               int32_t *nbr, int32_t *rev, int32_t *own, int64_t *status, void *ws,
-              size_t ws_bytes, cudaStream_t s);
+              size_t ws_bytes, cudaStream_t s, const int64_t *gate = nullptr, int stride = 1);
 int nbr_build_f64(const double *pos, int R, int N, double r_cut, int64_t cap_e, int32_t *ptr,
                   int32_t *nbr, int32_t *rev, int32_t *own, int64_t *status, void *ws,
                   size_t ws_bytes, cudaStream_t s);

@@ -102,10 +102,12 @@ __device__ double zig_slow(uint64_t seed, uint64_t rep, uint64_t step, uint64_t 
   return z.x;
 }
 
-// One warp per replica walks its stream 32 words at a time: every lane
-// decodes the word at pos+lane assuming a sample starts there; the prefix
-// of fast lanes are consecutive samples, and the first slow lane resolves
-// its rejection loop alone before the window advances past what it used.
+// One warp per replica walks its stream in windows of 128 words: lane L
+// computes Philox block (base + L), i.e. words 4L..4L+3 of the window, and
+// decodes a draw at each of them.  Draws from the current sample start up to
+// the first draw that misses the fast path are consecutive samples; that
+// draw's owner lane resolves numpy's rejection loop alone (reading further
+// words on demand) and the walk resumes after the words it consumed.
 __global__ void __launch_bounds__(256)
 k_normal_noise(uint64_t seed, int rep_offset, const int64_t *__restrict__ stepp, int R, int n3,
                float *__restrict__ out) {
@@ -113,28 +115,52 @@ k_normal_noise(uint64_t seed, int rep_offset, const int64_t *__restrict__ stepp,
   if (warp >= R) return;
   uint64_t rep = (uint64_t)(rep_offset + warp), step = (uint64_t)*stepp;
   float *dst = out + (size_t)warp * n3;
-  uint64_t pos = 0;
+  uint64_t pos = 0;  // stream position of the next sample start
   int produced = 0;
   while (produced < n3) {
-    uint64_t q = pos + lane;
-    uint64_t r = stream_word(seed, rep, step, q);
-    ZigDraw z = zig_decode(r);
-    unsigned slow = __ballot_sync(0xffffffffu, !z.fast);
-    int L = slow ? __ffs(slow) - 1 : 32;
-    if (lane < L && produced + lane < n3) dst[produced + lane] = __double2float_rn(z.x);
-    if (L == 32) {
-      produced += 32;
-      pos += 32;
-      continue;
+    const uint64_t wbase = (pos >> 2) << 2;  // window = words [wbase, wbase + 128)
+    U64x4 o = philox4x64_10(((wbase >> 2) + lane) + 1, 0, 0, step, seed, rep);
+    ZigDraw z[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) z[j] = zig_decode(o.v[j]);
+    const uint64_t wend = wbase + 128;
+    while (pos < wend && produced < n3) {
+      // first slow draw at or after pos (window-relative index, 128 = none)
+      int my = 128;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint64_t p = wbase + 4 * lane + j;
+        if (my == 128 && p >= pos && !z[j].fast) my = 4 * lane + j;
+      }
+      const int first = __reduce_min_sync(0xffffffffu, my);
+      const uint64_t stop = first == 128 ? wend : wbase + first;
+      // fast samples at positions [pos, stop)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint64_t p = wbase + 4 * lane + j;
+        if (p >= pos && p < stop) {
+          long long idx = produced + (long long)(p - pos);
+          if (idx < n3) dst[idx] = __double2float_rn(z[j].x);
+        }
+      }
+      produced += (int)(stop - pos);
+      if (first == 128) {
+        pos = wend;
+        break;
+      }
+      double xs = 0.0;
+      uint64_t used = 0;
+      const int owner = first >> 2, jj = first & 3;
+      if (lane == owner) {
+        uint64_t r = jj == 0 ? o.v[0] : jj == 1 ? o.v[1] : jj == 2 ? o.v[2] : o.v[3];
+        xs = zig_slow(seed, rep, step, stop, r, &used);
+      }
+      xs = __shfl_sync(0xffffffffu, xs, owner);
+      used = __shfl_sync(0xffffffffu, used, owner);
+      if (lane == 0 && produced < n3) dst[produced] = __double2float_rn(xs);
+      produced += 1;
+      pos = stop + used;
     }
-    double xs = 0.0;
-    uint64_t used = 0;
-    if (lane == L) xs = zig_slow(seed, rep, step, q, r, &used);
-    xs = __shfl_sync(0xffffffffu, xs, L);
-    used = __shfl_sync(0xffffffffu, used, L);
-    if (lane == 0 && produced + L < n3) dst[produced + L] = __double2float_rn(xs);
-    produced += L + 1;
-    pos += (uint64_t)L + used;
   }
 }
 

@@ -37,7 +37,10 @@ template <typename T, bool kFill>
 __global__ void __launch_bounds__(NBR_WARPS * 32)
 k_scan_rows(const T *__restrict__ pos, int N, double rc2, int32_t *__restrict__ cnt,
             const int32_t *__restrict__ ptr, int64_t cap_e, int32_t *__restrict__ nbr,
-            int32_t *__restrict__ own, int64_t *__restrict__ status) {
+            int32_t *__restrict__ own, int64_t *__restrict__ status, const int64_t *gate,
+            int stride) {
+  // neighbor_stride > 1 (md.py:245-250): keep the previous list between rebuilds
+  if (gate && stride > 1 && (*gate % stride) != 0) return;
   __shared__ double sx[NBR_TILE], sy[NBR_TILE], sz[NBR_TILE];
   const int r = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -121,7 +124,8 @@ __global__ void k_finalize(const int32_t *__restrict__ ptr, int nrows, int64_t c
 // i.e. the reference's group_by_source perm (neighbors.py:129-132).
 __global__ void __launch_bounds__(256)
 k_rev(const int32_t *__restrict__ ptr, const int32_t *__restrict__ nbr, int nrows,
-      int64_t cap_e, int32_t *__restrict__ rev) {
+      int64_t cap_e, int32_t *__restrict__ rev, const int64_t *gate, int stride) {
+  if (gate && stride > 1 && (*gate % stride) != 0) return;
   int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= nrows) return;
   if ((long long)ptr[nrows] > cap_e) return;  // overflow: CSR invalid
@@ -151,7 +155,8 @@ size_t nbr_ws_bytes(int R, int N) {
 template <typename T>
 int nbr_build_t(const T *pos, int R, int N, double r_cut, int64_t cap_e, int32_t *ptr,
                 int32_t *nbr, int32_t *rev, int32_t *own, int64_t *status, void *ws,
-                size_t ws_bytes, cudaStream_t s) {
+                size_t ws_bytes, cudaStream_t s, const int64_t *gate = nullptr,
+                int stride = 1) {
   if (R < 1 || N < 1) { set_error("nbr_build: need R >= 1 and N >= 1"); return FCG_ERR_ARG; }
   if ((long long)R * N >= (1ll << 31)) { set_error("nbr_build: R*N too large"); return FCG_ERR_ARG; }
   size_t n = (size_t)R * N + 1;
@@ -168,7 +173,7 @@ int nbr_build_t(const T *pos, int R, int N, double r_cut, int64_t cap_e, int32_t
   {
     FCG_PROF(P_NBR_COUNT, s);
     k_scan_rows<T, false><<<grid, NBR_WARPS * 32, 0, s>>>(pos, N, rc2, cnt, nullptr, cap_e,
-                                                          nullptr, nullptr, status);
+                                                          nullptr, nullptr, status, gate, stride);
   }
   {
     FCG_PROF(P_NBR_SCAN, s);
@@ -178,20 +183,21 @@ int nbr_build_t(const T *pos, int R, int N, double r_cut, int64_t cap_e, int32_t
   {
     FCG_PROF(P_NBR_FILL, s);
     k_scan_rows<T, true><<<grid, NBR_WARPS * 32, 0, s>>>(pos, N, rc2, nullptr, ptr, cap_e, nbr,
-                                                         own, status);
+                                                         own, status, gate, stride);
   }
   {
     FCG_PROF(P_NBR_REV, s);
     k_rev<<<ceil_div((long long)(n - 1) * 32, 256), 256, 0, s>>>(ptr, nbr, (int)(n - 1), cap_e,
-                                                                 rev);
+                                                                 rev, gate, stride);
   }
   return cuda_status("nbr_build");
 }
 
 int nbr_build(const float *pos, int R, int N, double r_cut, int64_t cap_e, int32_t *ptr,
               int32_t *nbr, int32_t *rev, int32_t *own, int64_t *status, void *ws,
-              size_t ws_bytes, cudaStream_t s) {
-  return nbr_build_t(pos, R, N, r_cut, cap_e, ptr, nbr, rev, own, status, ws, ws_bytes, s);
+              size_t ws_bytes, cudaStream_t s, const int64_t *gate, int stride) {
+  return nbr_build_t(pos, R, N, r_cut, cap_e, ptr, nbr, rev, own, status, ws, ws_bytes, s, gate,
+                     stride);
 }
 int nbr_build_f64(const double *pos, int R, int N, double r_cut, int64_t cap_e, int32_t *ptr,
                   int32_t *nbr, int32_t *rev, int32_t *own, int64_t *status, void *ws,

@@ -108,9 +108,14 @@ class MDEngine:
         self._graphs = {}
 
     # -- buffers ---------------------------------------------------------
-    def _alloc(self, cap_e: int):
+    def _alloc(self, cap_e: int, keep: dict | None = None):
         torch = self.torch
         self.csr = CsrBuffers(self.R, self.N, cap_e, self.device)
+        if keep is not None:  # restore a saved CSR (see save_csr) into the new buffers
+            self.csr.ptr.copy_(keep["ptr"])
+            for k in ("nbr", "rev", "own"):
+                src = keep[k]
+                getattr(self.csr, k)[:src.numel()].copy_(src)
         nbytes = self.lib.fcg_md_workspace_bytes(C.byref(self.model.desc), self.R, self.N,
                                                  self.csr.cap_e)
         self.ws = torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
@@ -119,6 +124,14 @@ class MDEngine:
     @property
     def cap_e(self) -> int:
         return self.csr.cap_e
+
+    def save_csr(self) -> dict:
+        """Copy of the live CSR (needed to replay a chunk exactly when the
+        neighbour list is only rebuilt every neighbor_stride steps)."""
+        e = int(self.csr.ptr[-1].item())
+        e = min(e, self.cap_e)
+        return {"ptr": self.csr.ptr.clone(), "nbr": self.csr.nbr[:e].clone(),
+                "rev": self.csr.rev[:e].clone(), "own": self.csr.own[:e].clone()}
 
     def stream(self):
         return C.c_void_p(self.torch.cuda.current_stream(self.device).cuda_stream)
@@ -142,12 +155,14 @@ class MDEngine:
                            v(c.own), v(self.status), v(self.ws), self.ws.numel(), self.stream())
         _lib.check(rc, "fcg_md_step")
 
-    def evaluate(self):
+    def evaluate(self, rebuild: bool = True):
         """Forces of the current positions (the integrate() pre-loop force
-        evaluation, md.py:195): neighbour build + prior + model, no kick."""
+        evaluation, md.py:195): neighbour build + prior + model, no kick.
+        rebuild=False reuses the current CSR (neighbor_stride > 1,
+        md.py:245-250)."""
         L, c, v = self.lib, self.csr, _lib.vp
         torch = self.torch
-        while True:
+        while rebuild:
             nb = L.fcg_nbr_workspace_bytes(self.R, self.N)
             ws_nb = torch.empty(int(nb), dtype=torch.uint8, device=self.device)
             _lib.check(L.fcg_nbr_build(v(self.pos), self.R, self.N, self.r_cut, c.cap_e, v(c.ptr),

@@ -139,9 +139,11 @@ class GpuReplicaForces:
     def __call__(self, positions, step):
         positions = np.asarray(positions)
         R = positions.shape[0]
+        fresh = self.engine is None or self.engine.R != R
         eng = self._engine_for(R)
         eng.pos.copy_(eng.torch.as_tensor(positions.astype(np.float32)))
-        eng.evaluate()
+        # md.py:245: rebuild on first use and every neighbor_stride steps
+        eng.evaluate(rebuild=fresh or step % max(self.config.neighbor_stride, 1) == 0)
         forces = eng.forces.cpu().numpy()
         info = {"potential": eng.potential.cpu().numpy().astype(np.float64),
                 "prior": eng.prior_e.cpu().numpy().astype(np.float64)}
@@ -311,6 +313,7 @@ def run_simulation(params, system, config: SimConfig, out_dir, resume_from=None,
                 nxt = config.checkpoint_step
             n = nxt - cur
             saved = [t.clone() for t in (eng.pos, eng.vel, eng.forces, eng.step)]
+            csr0 = eng.save_csr() if config.neighbor_stride > 1 else None
             eng.clear_flags()
             eng.run(n, graph_steps=min(graph_steps, n) if n >= 4 else 0)
             fl = eng.flags()
@@ -318,9 +321,11 @@ def run_simulation(params, system, config: SimConfig, out_dir, resume_from=None,
                 for t, s0 in zip((eng.pos, eng.vel, eng.forces, eng.step), saved):
                     t.copy_(s0)
                 if fl["overflow"]:
-                    eng._alloc(max(2 * eng.cap_e, int(1.5 * fl["edges"]) + 1024))
+                    eng._alloc(max(2 * eng.cap_e, int(1.5 * fl["edges"]) + 1024), keep=csr0)
                     continue
                 # replay one step at a time to locate the blow-up step
+                if csr0 is not None:
+                    eng._alloc(eng.cap_e, keep=csr0)
                 eng.clear_flags()
                 for _ in range(n):
                     eng.run(1)

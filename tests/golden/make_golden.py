@@ -187,13 +187,14 @@ def md_fixture():
     out.update({"prior/pos": p32, "prior/energy": e, "prior/forces": f})
     # short trajectories through run_simulation
     import tempfile
-    for name, kind, n, sseed, cfgd, pseed, R, steps in [
-            ("traj_tiny", "coil", 20, 3, TINY, 2, 3, 20),
-            ("traj_coil269", "coil", 269, 0, {}, 0, 2, 10)]:
+    for name, kind, n, sseed, cfgd, pseed, R, steps, stride in [
+            ("traj_tiny", "coil", 20, 3, TINY, 2, 3, 20, 1),
+            ("traj_tiny_stride3", "coil", 20, 3, TINY, 2, 2, 20, 3),
+            ("traj_coil269", "coil", 269, 0, {}, 0, 2, 10, 1)]:
         params = RM.init_params(RM.ModelConfig(**cfgd), pseed)
         sysm = RS.generate_system(kind, n, sseed)
         sim = RMD.SimConfig(dt_fs=4.0, temperature=300.0, friction=1.0, n_steps=steps,
-                            n_replicas=R, seed=9, output_stride=5)
+                            n_replicas=R, seed=9, output_stride=5, neighbor_stride=stride)
         with tempfile.TemporaryDirectory() as td:
             res = RMD.run_simulation(params, sysm, sim, td)
             scal = (Path(td) / "scalars.csv").read_text()
@@ -202,8 +203,8 @@ def md_fixture():
                     f"{name}/vel": res.final_state.velocities,
                     f"{name}/mean_edges": res.mean_edges, f"{name}/scalars": scal,
                     f"{name}/traj_sha": hashlib.sha256(traj.encode()).hexdigest(),
-                    f"{name}/cfg": json.dumps(cfgd), f"{name}/meta":
-                        np.array([n, sseed, pseed, R, steps])})
+                    f"{name}/cfg": json.dumps(cfgd), f"{name}/stride": stride,
+                    f"{name}/meta": np.array([n, sseed, pseed, R, steps])})
     np.savez_compressed(OUT / "md.npz", **out)
 
 

@@ -287,14 +287,15 @@ def _engine_for(name, golden, R=None, **kw):
     sysm = generate_system("coil", n, sseed)
     params = init_params(ModelConfig(**json.loads(str(c["cfg"]))), pseed)
     R = R or Rg
-    eng = MDEngine(params, sysm.types, sysm.masses, sysm.prior, R, seed=9, **kw)
+    eng = MDEngine(params, sysm.types, sysm.masses, sysm.prior, R, seed=9,
+                   neighbor_stride=int(c["stride"]), **kw)
     pos0 = np.repeat(sysm.positions[None], R, axis=0).astype(np.float32)
     eng.load_state(pos0, np.zeros_like(pos0), 0)
     eng.evaluate()
     return eng, c, steps
 
 
-@pytest.mark.parametrize("name", ["traj_tiny", "traj_coil269"])
+@pytest.mark.parametrize("name", ["traj_tiny", "traj_tiny_stride3", "traj_coil269"])
 def test_trajectory_vs_reference(golden, name):
     eng, c, steps = _engine_for(name, golden)
     eng.run(steps)
@@ -411,3 +412,43 @@ def test_force_provider_protocol(golden):
     assert out.step == steps
     assert np.max(np.abs(out.positions - c["pos"])) <= 1e-5
     assert len(fn.edge_counts) == R * (steps + 1)
+
+
+def test_run_simulation_neighbor_stride(tmp_path, golden):
+    c = golden["md"].case("traj_tiny_stride3")
+    n, sseed, pseed, R, steps = (int(x) for x in c["meta"])
+    sysm = generate_system("coil", n, sseed)
+    params = init_params(ModelConfig(**json.loads(str(c["cfg"]))), pseed)
+    sim = P.SimConfig(dt_fs=4.0, temperature=300.0, friction=1.0, n_steps=steps, n_replicas=R,
+                      seed=9, output_stride=5, neighbor_stride=3)
+    res = P.run_simulation(params, sysm, sim, tmp_path)
+    assert np.max(np.abs(res.final_state.positions - c["pos"])) <= 1e-5
+    assert abs(res.mean_edges - float(c["mean_edges"])) <= 1e-9
+    fn = P.GpuReplicaForces(params, sysm.types, sysm.prior, sim)
+    pos0 = np.repeat(sysm.positions[None], R, axis=0).astype(np.float32)
+    out = P.integrate(fn, P.SimState(positions=pos0, velocities=np.zeros_like(pos0),
+                                     masses=sysm.masses), sim)
+    assert np.max(np.abs(out.positions - c["pos"])) <= 1e-5
+
+
+@pytest.mark.parametrize("kind,n,rc,bonded", [("coil", 1000, 2.0, True),
+                                              ("globule", 1000, 1.5, False)])
+def test_large_system_sweep(kind, n, rc, bonded):
+    """BASELINE configs[4]: ~1k-bead systems at raised cutoff / high degree."""
+    sysm = generate_system(kind, n, 0, bonded=bonded)
+    params = init_params(ModelConfig(cutoff=rc), 0)
+    R = 3
+    rng = np.random.default_rng(2)
+    pos = (sysm.positions[None] + rng.normal(0, 0.02, size=(R, n, 3))).astype(np.float32)
+    eng = MDEngine(params, sysm.types, sysm.masses, sysm.prior, R)
+    eng.load_state(pos, np.zeros_like(pos), 0)
+    eng.evaluate()
+    Fm = eng.model_forces.cpu().numpy()
+    pot = eng.potential.cpu().numpy()
+    for r in range(R):
+        e, pa, f = O.energy_forces(pos[r], sysm.types, params)
+        assert O.energy_rel_err(float(pot[r]), e, pa) <= FP32_TOL
+        assert O.force_rel_err(Fm[r], f) <= FP32_TOL
+    assert eng.flags()["max_degree"] >= 40
+    eng.run(3, graph_steps=3)
+    assert not eng.flags()["blowup"]

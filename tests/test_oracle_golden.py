@@ -111,7 +111,7 @@ def test_prior_bit_exact(golden):
     np.testing.assert_array_equal(f, g["prior/forces"])
 
 
-@pytest.mark.parametrize("name", ["traj_tiny", "traj_coil269"])
+@pytest.mark.parametrize("name", ["traj_tiny", "traj_tiny_stride3", "traj_coil269"])
 def test_trajectory_matches_reference(golden, name):
     c = golden["md"].case(name)
     n, sseed, pseed, R, steps = (int(x) for x in c["meta"])
@@ -119,7 +119,8 @@ def test_trajectory_matches_reference(golden, name):
     params = init_params(ModelConfig(**json.loads(str(c["cfg"]))), pseed)
     pos0 = np.repeat(sysm.positions[None], R, axis=0).astype(np.float32)
     pos, vel, *_ = O.run_md(params, sysm.types, sysm.masses, sysm.prior, pos0,
-                            np.zeros_like(pos0), steps, seed=9)
+                            np.zeros_like(pos0), steps, seed=9,
+                            neighbor_stride=int(c["stride"]))
     # the oracle restates the same numpy ops: identical trajectories
     np.testing.assert_array_equal(pos, c["pos"])
     np.testing.assert_array_equal(vel, c["vel"])
