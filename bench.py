@@ -49,12 +49,13 @@ def ns_per_day(replica_steps: float, seconds: float) -> float:
     return replica_steps / seconds * DT_FS * 86400.0 / 1.0e6
 
 
-def workload(config: str):
+def workload(config: str, system: str = "coil", beads: int = 269, cutoff: float = 1.5):
     from paper_2602_13140_b200.inputs import generate_system
     from paper_2602_13140_b200.modelparams import ModelConfig, init_params
 
-    sysm = generate_system("coil", 269, 0)
-    params = init_params(ModelConfig(), 0)
+    # BASELINE configs[4] stress variant: unbonded globule
+    sysm = generate_system(system, beads, 0, bonded=(system != "globule"))
+    params = init_params(ModelConfig(cutoff=cutoff), 0)
     if config == "w16":
         from paper_2602_13140_b200.w16 import quantize_model
         params = quantize_model(params, seed=0)
@@ -157,7 +158,7 @@ def run_reference(args):
         return
     from threadpoolctl import threadpool_limits
 
-    sysm, params = workload(args.config)
+    sysm, params = workload(args.config, args.system, args.beads, args.cutoff)
     cores = os.cpu_count() or 1
     R = min(args.replicas, max(8, cores))
     with threadpool_limits(limits=1):
@@ -193,6 +194,9 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", choices=("fp32", "w16"), default="fp32")
     ap.add_argument("--replicas", type=int, default=64, help="replicas per GPU")
+    ap.add_argument("--system", choices=("coil", "globule"), default="coil")
+    ap.add_argument("--beads", type=int, default=269)
+    ap.add_argument("--cutoff", type=float, default=1.5)
     ap.add_argument("--e2e-steps", type=int, default=30)
     ap.add_argument("--profile-steps", type=int, default=3)
     ap.add_argument("--no-flush", action="store_true")
@@ -215,7 +219,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    sysm, params = workload(args.config)
+    sysm, params = workload(args.config, args.system, args.beads, args.cutoff)
     R, N = args.replicas, sysm.n_beads
     eng = MDEngine(params, sysm.types, sysm.masses, sysm.prior, R, dt_fs=DT_FS, seed=0,
                    rep_offset=rank * R, device=dev)
@@ -296,13 +300,14 @@ def main():
     prof = _lib.profile_read()
     lib.fcg_profile_enable(0)
     E_tot = eng.flags()["edges"]
+    flags = eng.flags()
     per_step_launch = sum(c for _, c in prof.values()) / args.profile_steps + 2  # +CUB scan kernels
     dom = max(prof.items(), key=lambda kv: kv[1][0])
     dom_name, (dom_ms, dom_n) = dom
     avg_ms = dom_ms / dom_n
     pk, pk_kind = peaks()
     if dom_name in ("edge_fwd", "edge_bwd"):
-        alg = E_tot * flops_per_edge_block()
+        alg = flags["edges"] * flops_per_edge_block()
         achieved = alg / (avg_ms / 1e3) / 1e12
         roof = {"kernel": dom_name, "bound": "tensor", "achieved": achieved,
                 "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
@@ -338,8 +343,11 @@ def main():
                    "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                    "dtype": "f32" if args.config == "fp32" else "f16-weights/f32-accum",
                    "data": "synthetic (generate_system coil-269 seed 0; random-init weights)",
-                   "config": {"workload": "1ENH stand-in coil-269, 64 replicas/GPU, T=3 D=128 "
-                                          "D_r=64 r_cut=1.5 nm, dt=4 fs, nbr rebuild every step",
+                   "config": {"workload": (f"1ENH stand-in coil-269, {R} replicas/GPU, T=3 D=128 "
+                                           f"D_r=64 r_cut={args.cutoff} nm, dt=4 fs, nbr rebuild "
+                                           "every step") if (args.system, args.beads) == ("coil", 269)
+                              else (f"{args.system}-{args.beads} (BASELINE configs[4] sweep), "
+                                    f"{R} replicas/GPU, r_cut={args.cutoff} nm, dt=4 fs"),
                               "replicas_per_gpu": R, "total_replicas": R * world,
                               "weights": args.config, "parallelism": f"replica-shard x{world}",
                               "l2": "flushed (256 MiB write) before every timed step"

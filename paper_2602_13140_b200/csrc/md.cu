@@ -236,30 +236,38 @@ __device__ __forceinline__ BondVec bond_eval(const fcg_prior &pr, const float *P
   return o;
 }
 
-// One CTA per replica: each bead applies its incident bonds in np.add.at
-// order (all "+fvec" for bonds where it is atom i, then "-fvec" where it is
-// atom j), so the per-bead sums are bitwise the reference's.
+// One thread per bead: it applies its incident bonds in np.add.at order (all
+// "+fvec" for bonds where it is atom i, then "-fvec" where it is atom j), so
+// the per-bead sums are bitwise the reference's.
 __global__ void __launch_bounds__(256)
-k_prior(const fcg_prior pr, const float *__restrict__ pos, int N, float *__restrict__ e_prior,
+k_prior(const fcg_prior pr, const float *__restrict__ pos, int N, int RN,
         float *__restrict__ f_prior) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= RN) return;
+  const int r = g / N, i = g % N;
+  const float *P = pos + (size_t)r * N * 3;
+  float fx = 0.f, fy = 0.f, fz = 0.f;
+  if (pr.num_bonds > 0) {
+    for (int q = pr.inc_ptr[i]; q < pr.inc_ptr[i + 1]; ++q) {
+      BondVec v = bond_eval(pr, P, pr.inc_bond[q]);
+      if (pr.inc_sign[q] > 0) {
+        fx = __fadd_rn(fx, v.fx); fy = __fadd_rn(fy, v.fy); fz = __fadd_rn(fz, v.fz);
+      } else {
+        fx = __fadd_rn(fx, -v.fx); fy = __fadd_rn(fy, -v.fy); fz = __fadd_rn(fz, -v.fz);
+      }
+    }
+  }
+  float *f = f_prior + (size_t)g * 3;
+  f[0] = fx; f[1] = fy; f[2] = fz;
+}
+
+// Prior energy 0.5 * sum k*s^2 per replica (md.py:118), one CTA per replica.
+__global__ void __launch_bounds__(256)
+k_prior_energy(const fcg_prior pr, const float *__restrict__ pos, int N,
+               float *__restrict__ e_prior) {
   const int r = blockIdx.x;
   const float *P = pos + (size_t)r * N * 3;
   __shared__ float red[256];
-  for (int i = threadIdx.x; i < N; i += blockDim.x) {
-    float fx = 0.f, fy = 0.f, fz = 0.f;
-    if (pr.num_bonds > 0) {
-      for (int q = pr.inc_ptr[i]; q < pr.inc_ptr[i + 1]; ++q) {
-        BondVec v = bond_eval(pr, P, pr.inc_bond[q]);
-        if (pr.inc_sign[q] > 0) {
-          fx = __fadd_rn(fx, v.fx); fy = __fadd_rn(fy, v.fy); fz = __fadd_rn(fz, v.fz);
-        } else {
-          fx = __fadd_rn(fx, -v.fx); fy = __fadd_rn(fy, -v.fy); fz = __fadd_rn(fz, -v.fz);
-        }
-      }
-    }
-    float *f = f_prior + ((size_t)r * N + i) * 3;
-    f[0] = fx; f[1] = fy; f[2] = fz;
-  }
   float acc = 0.f;
   for (int b = threadIdx.x; b < pr.num_bonds; b += blockDim.x) acc += bond_eval(pr, P, b).e;
   red[threadIdx.x] = acc;
@@ -274,7 +282,8 @@ k_prior(const fcg_prior pr, const float *__restrict__ pos, int N, float *__restr
 int prior_forces(const fcg_prior *pr, const float *pos, int R, int N, float *e_prior,
                  float *f_prior, cudaStream_t s) {
   FCG_PROF(P_PRIOR, s);
-  k_prior<<<R, 256, 0, s>>>(*pr, pos, N, e_prior, f_prior);
+  k_prior<<<ceil_div((long long)R * N, 256), 256, 0, s>>>(*pr, pos, N, R * N, f_prior);
+  k_prior_energy<<<R, 256, 0, s>>>(*pr, pos, N, e_prior);
   return cuda_status("prior_forces");
 }
 

@@ -519,55 +519,58 @@ k_edge_bwd(const EdgeArgs a, const float *__restrict__ P, const float *__restric
 // grad_r[x] = sum_{k in row x} (gsum[rev[k]] - gsum[k])  (flash.py:298-299,
 // dst-segment sum minus src-segment sum), forces = -grad_r (+ f_extra), then
 // optionally the trailing half-kick (md.py:134-138) and the blow-up check
-// (md.py:183-185).  One CTA per replica; also reduces per-replica energy.
+// (md.py:183-185).  One thread per node; single writer per output.
 __global__ void __launch_bounds__(256)
 k_forces_finish(const int32_t *__restrict__ ptr, const int32_t *__restrict__ rev,
-                const float4 *__restrict__ gsum, int N, int64_t cap_e,
-                const float *__restrict__ per_atom, float *__restrict__ energy,
+                const float4 *__restrict__ gsum, int N, int RN, int64_t cap_e,
                 const float *__restrict__ f_extra, float *__restrict__ forces,
                 fcg_md_params kick, int do_kick, const float *__restrict__ mass,
                 float *__restrict__ vel, int64_t *__restrict__ status, const int64_t *step) {
-  const int r = blockIdx.x;
-  __shared__ float red[256];
-  float esum = 0.f;
-  bool bad = false;
-  bool valid = (long long)ptr[(size_t)gridDim.x * N] <= cap_e;
-  for (int i = threadIdx.x; i < N; i += blockDim.x) {
-    int g = r * N + i;
-    float gx = 0.f, gy = 0.f, gz = 0.f;
-    if (valid) {
-      for (int k = ptr[g]; k < ptr[g + 1]; ++k) {
-        float4 a = gsum[rev[k]], b = gsum[k];
-        gx += a.x - b.x;
-        gy += a.y - b.y;
-        gz += a.z - b.z;
-      }
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= RN) return;
+  const bool valid = (long long)ptr[RN] <= cap_e;
+  float gx = 0.f, gy = 0.f, gz = 0.f;
+  if (valid) {
+    for (int k = ptr[g]; k < ptr[g + 1]; ++k) {
+      float4 a = gsum[rev[k]], b = gsum[k];
+      gx += a.x - b.x;
+      gy += a.y - b.y;
+      gz += a.z - b.z;
     }
-    float f[3] = {-gx, -gy, -gz};
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      if (f_extra) f[q] = __fadd_rn(f[q], f_extra[(size_t)g * 3 + q]);
-      forces[(size_t)g * 3 + q] = f[q];
-      bad |= !(fabsf(f[q]) <= FORCE_BLOWUP_LIMIT);  // catches NaN too
-      if (do_kick) {
-        float mi = mass[i];
-        float dv = __fdiv_rn(__fmul_rn(kick.half_dt, f[q]), mi);
-        vel[(size_t)g * 3 + q] = __fadd_rn(vel[(size_t)g * 3 + q], dv);
-      }
-    }
-    esum += per_atom[g];
   }
-  red[threadIdx.x] = esum;
+  float f[3] = {-gx, -gy, -gz};
+  bool bad = false;
+  const int i = g % N;
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    if (f_extra) f[q] = __fadd_rn(f[q], f_extra[(size_t)g * 3 + q]);  // out.forces + f_prior
+    forces[(size_t)g * 3 + q] = f[q];
+    bad |= !(fabsf(f[q]) <= FORCE_BLOWUP_LIMIT);  // catches NaN too
+    if (do_kick) {
+      float dv = __fdiv_rn(__fmul_rn(kick.half_dt, f[q]), mass[i]);
+      vel[(size_t)g * 3 + q] = __fadd_rn(vel[(size_t)g * 3 + q], dv);
+    }
+  }
+  if (bad && status) {
+    if (atomicCAS((unsigned long long *)&status[FCG_ST_BLOWUP], 0ull, 1ull) == 0ull)
+      status[FCG_ST_BLOWUP_STEP] = step ? *step : 0;
+  }
+}
+
+// energy[r] = sum_i per_atom[r*N + i] (flash.py:489), fixed tree order.
+__global__ void __launch_bounds__(256)
+k_replica_energy(const float *__restrict__ per_atom, int N, float *__restrict__ energy) {
+  __shared__ float red[256];
+  const int r = blockIdx.x;
+  float acc = 0.f;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) acc += per_atom[(size_t)r * N + i];
+  red[threadIdx.x] = acc;
   __syncthreads();
   for (int s = blockDim.x / 2; s > 0; s >>= 1) {
     if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
     __syncthreads();
   }
   if (threadIdx.x == 0) energy[r] = red[0];
-  if (bad && status) {
-    if (atomicCAS((unsigned long long *)&status[FCG_ST_BLOWUP], 0ull, 1ull) == 0ull)
-      status[FCG_ST_BLOWUP_STEP] = step ? *step : 0;
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -756,8 +759,10 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
   fcg_md_params kp{};
   if (kick) kp = *kick;
   FCG_PROF(P_FORCES, s);
-  k_forces_finish<<<R, 256, 0, s>>>(ptr, rev, b.gsum, N, cap_e, per_atom, energy, f_extra, forces,
-                                    kp, kick != nullptr, mass, vel, status, step);
+  k_forces_finish<<<ceil_div(RN, 256), 256, 0, s>>>(ptr, rev, b.gsum, N, RN, cap_e, f_extra,
+                                                    forces, kp, kick != nullptr, mass, vel, status,
+                                                    step);
+  k_replica_energy<<<R, 256, 0, s>>>(per_atom, N, energy);
   return cuda_status("energy_forces");
 }
 

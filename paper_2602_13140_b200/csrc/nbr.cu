@@ -39,11 +39,22 @@ k_scan_rows(const T *__restrict__ pos, int N, double rc2, int32_t *__restrict__ 
             const int32_t *__restrict__ ptr, int64_t cap_e, int32_t *__restrict__ nbr,
             int32_t *__restrict__ own, int64_t *__restrict__ status, const int64_t *gate,
             int stride) {
-  // neighbor_stride > 1 (md.py:245-250): keep the previous list between rebuilds
-  if (gate && stride > 1 && (*gate % stride) != 0) return;
   __shared__ double sx[NBR_TILE], sy[NBR_TILE], sz[NBR_TILE];
   const int r = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // neighbor_stride > 1 (md.py:245-250): keep the previous list between
+  // rebuilds; the count pass re-derives the row counts from the live ptr so
+  // the (unconditional) scan reproduces it exactly.
+  if (gate && stride > 1 && (*gate % stride) != 0) {
+    if (!kFill) {
+      int row0 = blockIdx.x * NBR_ROWS_PER_CTA + warp * NBR_ROWS_PER_WARP;
+      if (lane < NBR_ROWS_PER_WARP && row0 + lane < N) {
+        long long g = (long long)r * N + row0 + lane;
+        cnt[g] = ptr[g + 1] - ptr[g];
+      }
+    }
+    return;
+  }
   const T *P = pos + (size_t)r * N * 3;
   const int row0 = blockIdx.x * NBR_ROWS_PER_CTA + warp * NBR_ROWS_PER_WARP;
 
@@ -172,7 +183,7 @@ int nbr_build_t(const T *pos, int R, int N, double r_cut, int64_t cap_e, int32_t
   cudaMemsetAsync(cnt + (n - 1), 0, sizeof(int32_t), s);
   {
     FCG_PROF(P_NBR_COUNT, s);
-    k_scan_rows<T, false><<<grid, NBR_WARPS * 32, 0, s>>>(pos, N, rc2, cnt, nullptr, cap_e,
+    k_scan_rows<T, false><<<grid, NBR_WARPS * 32, 0, s>>>(pos, N, rc2, cnt, ptr, cap_e,
                                                           nullptr, nullptr, status, gate, stride);
   }
   {

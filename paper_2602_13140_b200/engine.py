@@ -160,9 +160,10 @@ class MDEngine:
         evaluation, md.py:195): neighbour build + prior + model, no kick.
         rebuild=False reuses the current CSR (neighbor_stride > 1,
         md.py:245-250)."""
-        L, c, v = self.lib, self.csr, _lib.vp
+        L, v = self.lib, _lib.vp
         torch = self.torch
         while rebuild:
+            c = self.csr  # re-read: a regrow below replaces the buffers
             nb = L.fcg_nbr_workspace_bytes(self.R, self.N)
             ws_nb = torch.empty(int(nb), dtype=torch.uint8, device=self.device)
             _lib.check(L.fcg_nbr_build(v(self.pos), self.R, self.N, self.r_cut, c.cap_e, v(c.ptr),
@@ -173,6 +174,7 @@ class MDEngine:
                 break
             self.status[_lib.ST_OVERFLOW] = 0
             self._alloc(int(e_tot * 1.5) + 1024)
+        c = self.csr
         f_prior = torch.zeros(self.R, self.N, 3, dtype=torch.float32, device=self.device)
         _lib.check(L.fcg_prior_forces(C.byref(self.prior.desc), v(self.pos), self.R, self.N,
                                       v(self.prior_e), v(f_prior), self.stream()),
