@@ -128,6 +128,10 @@ const char *fcg_last_error(void);
  * returns, per kernel class, the summed device time and launch count; names
  * are 32-byte NUL-padded records.  Returns the number of classes written. */
 int fcg_profile_enable(int on);
+/* Diagnostics: when set (device buffer of >= 2*64*16 uint64), the tcgen05
+ * edge kernels record clock64() at phase boundaries of CTA 0 / group 0 for
+ * the first 16 tiles ([kernel 0=fwd,1=bwd][tile][phase]); NULL disables. */
+int fcg_debug_phase_buffer(void *dev_ptr);
 int fcg_profile_read(int max_classes, char *names, double *total_ms,
                      int *launches);
 

@@ -63,6 +63,7 @@ _SIGS = {
     "fcg_abi_version": (C.c_int, []),
     "fcg_last_error": (C.c_char_p, []),
     "fcg_profile_enable": (C.c_int, [C.c_int]),
+    "fcg_debug_phase_buffer": (C.c_int, [_VP]),
     "fcg_profile_read": (C.c_int, [C.c_int, C.c_char_p, C.POINTER(C.c_double),
                                    C.POINTER(C.c_int)]),
     "fcg_nbr_workspace_bytes": (C.c_size_t, [C.c_int, C.c_int]),

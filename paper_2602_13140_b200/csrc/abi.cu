@@ -20,6 +20,7 @@ int cuda_status(const char *where) {
 
 // ---- profiler ----------------------------------------------------------
 bool g_prof_on = false;
+unsigned long long *g_dbg_phase = nullptr;
 static const char *kProfNames[P_COUNT] = {
     "nbr_count", "nbr_scan", "nbr_fill", "nbr_rev", "embed", "node_pre", "edge_fwd",
     "node_post", "readout", "node_post_bwd", "edge_bwd", "node_pre_bwd", "forces_finish",
@@ -86,6 +87,11 @@ int fcg_profile_read(int max_classes, char *names, double *total_ms, int *launch
     ++k;
   }
   return k;
+}
+
+int fcg_debug_phase_buffer(void *dev_ptr) {
+  g_dbg_phase = (unsigned long long *)dev_ptr;
+  return FCG_OK;
 }
 
 size_t fcg_nbr_workspace_bytes(int R, int N) { return nbr_ws_bytes(R, N); }

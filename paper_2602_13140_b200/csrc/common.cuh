@@ -78,7 +78,9 @@ struct EdgeArgs {
   const float *centers;
   fcg_block blk;
   int quant;
+  unsigned long long *dbg;  // optional phase timestamps (fcg_debug_phase_buffer)
 };
+extern unsigned long long *g_dbg_phase;
 
 }  // namespace fcg
 

@@ -46,23 +46,24 @@ constexpr int EPT = TT / NPART;  // edges per thread (32)
 constexpr uint32_t KSTR = (TT / 8) * 128;  // B operand bytes per 8 K-rows
 constexpr uint32_t SM_W0 = 0;          // W0 hi|lo: 2 x 128x64 fp16
 constexpr uint32_t SM_W1 = 32768;      // W1 hi|lo: 2 x 128x128 fp16
-constexpr uint32_t SM_ACT = 98304;     // per group: B operand hi|lo (2 x 128x64 fp16) / scratch
-constexpr uint32_t ACT_BYTES = 32768;
-constexpr uint32_t SM_META = SM_ACT + NGRP * ACT_BYTES;
+constexpr uint32_t SM_BUF = 98304;     // per group: basis buffer (K=64) + act buffer (K=128)
+constexpr uint32_t BB_BYTES = 2 * 64 * TT * 2;   // basis hi|lo: 16 KB
+constexpr uint32_t HB_BYTES = 2 * 128 * TT * 2;  // h / grad_w / gz hi|lo, or fp32 scratch: 32 KB
+constexpr uint32_t GBUF_BYTES = BB_BYTES + HB_BYTES;
+constexpr uint32_t SM_META = SM_BUF + NGRP * GBUF_BYTES;
 constexpr uint32_t W0_BYTES = 128 * 64 * 2, W1_BYTES = 128 * 128 * 2;
-constexpr uint32_t TM_D0 = 0, TM_D1 = 64, TM_D2 = 128, TM_D3 = 192;  // + 256*group
 constexpr int RED_LD = 65;       // padded stride of the [edge][k] fp32 scratch
 
-struct TcMeta {
+struct TcMeta {  // per tile (double-buffered per group)
   int own[TT], nbr[TT];
   float d[TT], env[TT], denv[TT];
   float4 u[TT];
   unsigned int amax[4];
   float xch[NPART - 1][3][128];  // part 1 -> part 0 segment boundary partials
-  uint64_t bar;
 };
 struct TcShared {
-  TcMeta g[NGRP];
+  TcMeta meta[NGRP][2];
+  uint64_t bar[NGRP][2];  // [0]: GEMM1 commits, [1]: other GEMM commits
   uint32_t tmem;
 };
 constexpr uint32_t SM_TOTAL = SM_META + sizeof(TcShared);
@@ -211,12 +212,18 @@ struct Grp {
   int warp, lane, quarter, part, ch, ec;
   int bar_id;         // named barrier of the group
   uint32_t tl;        // TMEM address of this lane quarter + group column base
-  uint32_t sact;      // shared address of the group's B operand buffer
   uint32_t tmem_g;    // TMEM base of the group (lane 0)
-  uint8_t *act;
-  TcMeta *meta;
-  uint32_t phase;
+  uint8_t *bb, *hb;   // basis buffer, act buffer
+  uint32_t sbb, shb;  // their shared addresses
+  TcShared *sh;
+  uint32_t ph[2];
   __device__ __forceinline__ void sync() const { named_sync(bar_id, GT); }
+  __device__ __forceinline__ TcMeta *meta(int i) const { return &sh->meta[g][i & 1]; }
+  __device__ __forceinline__ void wait(int which) {
+    tc::mbar_wait(&sh->bar[g][which], ph[which]);
+    ph[which] ^= 1;
+    tc::fence_after_sync();
+  }
 };
 
 __device__ __forceinline__ Grp make_group(uint8_t *sm, TcShared *sh) {
@@ -230,12 +237,14 @@ __device__ __forceinline__ Grp make_group(uint8_t *sm, TcShared *sh) {
   G.ch = 32 * G.quarter + G.lane;
   G.ec = EPT * G.part;
   G.bar_id = 1 + G.g;
-  G.meta = &sh->g[G.g];
-  G.act = sm + SM_ACT + G.g * ACT_BYTES;
-  G.sact = tc::smem_u32(G.act);
+  G.sh = sh;
+  G.bb = sm + SM_BUF + G.g * GBUF_BYTES;
+  G.hb = G.bb + BB_BYTES;
+  G.sbb = tc::smem_u32(G.bb);
+  G.shb = tc::smem_u32(G.hb);
   G.tmem_g = sh->tmem + 256u * G.g;
   G.tl = G.tmem_g + ((uint32_t)(32 * G.quarter) << 16);
-  G.phase = 0;
+  G.ph[0] = G.ph[1] = 0;
   return G;
 }
 
@@ -249,7 +258,8 @@ __device__ __forceinline__ void stage_weights(uint8_t *sm, const fcg_block &b) {
 __device__ __forceinline__ void kernel_prologue(uint8_t *sm, TcShared *sh, const fcg_block &B) {
   stage_weights(sm, B);
   if (threadIdx.x % GT == 0) {
-    tc::mbar_init(&sh->g[threadIdx.x / GT].bar, 1);
+    tc::mbar_init(&sh->bar[threadIdx.x / GT][0], 1);
+    tc::mbar_init(&sh->bar[threadIdx.x / GT][1], 1);
     tc::fence_mbar_init();
   }
   if (threadIdx.x < 32) tc::tmem_alloc<512>(&sh->tmem);
@@ -260,9 +270,8 @@ __device__ __forceinline__ void kernel_prologue(uint8_t *sm, TcShared *sh, const
 }
 
 __device__ __forceinline__ void tile_meta(const EdgeArgs &a, const float4 *__restrict__ geo,
-                                          const float2 *__restrict__ env, const Grp &G, int t0,
-                                          int n_e, bool src_owned) {
-  TcMeta *m = G.meta;
+                                          const float2 *__restrict__ env, const Grp &G,
+                                          TcMeta *m, int t0, int n_e, bool src_owned) {
   int t = G.gt;
   if (t < TT) {
     int o = -1, n = 0;
@@ -286,11 +295,11 @@ __device__ __forceinline__ void tile_meta(const EdgeArgs &a, const float4 *__res
   if (t < 4) m->amax[t] = 0u;
 }
 
-// Basis b[k][e] (model.py:255-265) as the K=64 B operand: fp32 path scaled by
-// 2^14 and split; W16 path rounded to fp16 unscaled (quantize.py:68-71).
-__device__ __forceinline__ void tile_basis_tc(const EdgeArgs &a, const Grp &G, int n_e,
-                                              bool quant) {
-  const TcMeta *m = G.meta;
+// Basis b[k][e] (model.py:255-265) as the K=64 B operand (basis buffer):
+// fp32 path scaled by 2^14 and split; W16 path rounded to fp16 unscaled
+// (quantize.py:68-71).
+__device__ __forceinline__ void tile_basis_tc(const EdgeArgs &a, const Grp &G, const TcMeta *m,
+                                              int n_e, bool quant) {
 #pragma unroll 2
   for (int q = G.gt; q < DR * (TT / 8); q += GT) {
     int k = q % DR, e0 = (q / DR) * 8;
@@ -305,16 +314,15 @@ __device__ __forceinline__ void tile_basis_tc(const EdgeArgs &a, const Grp &G, i
       float dl = dd[i] - mu;
       v[i] = (e0 + i) < n_e ? __expf((-a.gamma * dl) * dl) * cc[i] : 0.f;
     }
-    put_b8n(G.act, DR, KSTR, k, e0, v, quant ? 1.f : 16384.f, !quant);
+    put_b8n(G.bb, DR, KSTR, k, e0, v, quant ? 1.f : 16384.f, !quant);
   }
 }
 
 // Segment reduction of a [128 ch][64 e] fp32 tile held in TMEM columns
 // starting at tcol: both parts scan, part 1 publishes boundary partials, part
 // 0 merges them into the carry.  Called by every thread of the group.
-__device__ __forceinline__ void reduce_tile(uint32_t tcol, const Grp &G, int n_e, int &crow,
-                                            float &cacc, float *__restrict__ out) {
-  TcMeta *meta = G.meta;
+__device__ __forceinline__ void reduce_tile(uint32_t tcol, const Grp &G, TcMeta *meta, int n_e,
+                                            int &crow, float &cacc, float *__restrict__ out) {
   const int lo = EPT * G.part, hi = min(lo + EPT, n_e);
   Runs r;
   r.init();
@@ -341,7 +349,7 @@ __device__ __forceinline__ void reduce_tile(uint32_t tcol, const Grp &G, int n_e
 }
 
 // Write this thread's [ch][32 edges] fp32 TMEM block as the hi/lo fp16 B
-// operand (K = 128 rows) of the next GEMM with the given scale.
+// operand (K = 128 rows, act buffer) of the next GEMM with the given scale.
 __device__ __forceinline__ void tmem_to_act(uint32_t tcol, const Grp &G, float scale,
                                             bool with_lo) {
 #pragma unroll 1
@@ -349,14 +357,15 @@ __device__ __forceinline__ void tmem_to_act(uint32_t tcol, const Grp &G, float s
     float v[16];
     tc::tmem_ld16(tcol + G.ec + c0, v);
     tc::tmem_ld_wait();
-    put_b8n(G.act, D, KSTR, G.ch, G.ec + c0, &v[0], scale, with_lo);
-    put_b8n(G.act, D, KSTR, G.ch, G.ec + c0 + 8, &v[8], scale, with_lo);
+    put_b8n(G.hb, D, KSTR, G.ch, G.ec + c0, &v[0], scale, with_lo);
+    put_b8n(G.hb, D, KSTR, G.ch, G.ec + c0 + 8, &v[8], scale, with_lo);
   }
 }
 
-// all threads of the group: make the act writes visible to the tensor core,
-// then the group's first thread issues the GEMM and commits it
-#define GRP_ISSUE(...)                  \
+// all threads of the group: make the smem operand writes visible to the
+// tensor core, then the group's first thread issues the GEMM and commits it
+// to barrier `which`
+#define GRP_ISSUE(which, ...)           \
   do {                                  \
     tc::fence_async_smem();             \
     tc::fence_before_sync();            \
@@ -364,15 +373,15 @@ __device__ __forceinline__ void tmem_to_act(uint32_t tcol, const Grp &G, float s
     if (G.gt == 0) {                    \
       tc::fence_after_sync();           \
       issue_gemm(__VA_ARGS__, KSTR);    \
-      tc::mma_commit(&G.meta->bar);     \
+      tc::mma_commit(&G.sh->bar[G.g][which]); \
     }                                   \
   } while (0)
 
-#define GRP_WAIT()                          \
-  do {                                      \
-    tc::mbar_wait(&G.meta->bar, G.phase);   \
-    G.phase ^= 1;                           \
-    tc::fence_after_sync();                 \
+// phase timestamps for diagnosis: CTA 0, group 0, first 16 tiles
+#define PHASE(kind, it, ph)                                                          \
+  do {                                                                             \
+    if (a.dbg && blockIdx.x == 0 && threadIdx.x == 0 && (it) < 16)                 \
+      a.dbg[((kind) * 16 + (it)) * 64 + (ph)] = clock64();                         \
   } while (0)
 
 struct UnitRange {
@@ -394,10 +403,11 @@ __device__ __forceinline__ UnitRange unit_range(const EdgeArgs &a, const int32_t
 
 // ---------------------------------------------------------------------------
 // Forward: per 64-edge tile of dst rows
-//   b -> [GEMM1] z0 -> h=ssp(z0) -> [GEMM2] w -> m = P[src]*w -> H rows.
-// The P[src] gather is issued right after GEMM1 so its latency hides under
-// the tensor-core work; h and m are staged back into TMEM so every epilogue
-// pass streams 16 columns at a time.
+//   b -> [G1] z0 -> h=ssp(z0) -> [G2] w -> m = P[src]*w -> H rows.
+// Software-pipelined per group: while G2(i) runs the group builds the basis
+// of tile i+1 and issues G1(i+1); while G1(i+1) runs it finishes tile i
+// (messages + segment sums).  TMEM per group: D0[2] = cols 0/64 (z0, h),
+// D1[2] = 128/192 (w, m), by tile parity.
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_edge_fwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__restrict__ env,
               const int32_t *__restrict__ unit_rows, const float *__restrict__ P,
@@ -413,6 +423,7 @@ k_edge_fwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
   const int nprod = quant ? 1 : 3;
 
   const UnitRange tr = unit_range(a, unit_rows, NGRP * blockIdx.x + G.g);
+  const int ntiles = (tr.ee - tr.eb + TT - 1) / TT;
   int crow = tr.rbeg;
   float cacc = 0.f;
 
@@ -421,23 +432,31 @@ k_edge_fwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
   const float rs0 = quant ? __ldg(&B.f0_s[ch]) : pow2f(-(B.f0_exp + 14));
   const float rs1 = quant ? __ldg(&B.f1_s[ch]) : 1.f;
 
-  for (int t0 = tr.eb; t0 < tr.ee; t0 += TT) {
-    const int n_e = min(TT, tr.ee - t0);
-    tile_meta(a, geo, env, G, t0, n_e, false);
+  float pv[EPT];  // P[src][ch] of this thread's edges of the current tile
+  if (ntiles > 0) {
+    TcMeta *m0 = G.meta(0);
+    tile_meta(a, geo, env, G, m0, tr.eb, min(TT, tr.ee - tr.eb), false);
     G.sync();
-    tile_basis_tc(a, G, n_e, quant);
-    GRP_ISSUE(G.tmem_g + TM_D0, sbase + SM_W0, W0_BYTES, DR, false, G.sact, DR, idesc, nprod);
-    float pv[EPT];  // P[src][ch] of this thread's edges, in flight during the MMAs
+    tile_basis_tc(a, G, m0, min(TT, tr.ee - tr.eb), quant);
+    GRP_ISSUE(0, G.tmem_g + 0, sbase + SM_W0, W0_BYTES, DR, false, G.sbb, DR, idesc, nprod);
 #pragma unroll
-    for (int i = 0; i < EPT; ++i) pv[i] = __ldg(&P[(size_t)G.meta->nbr[ec + i] * D + ch]);
-    GRP_WAIT();
+    for (int i = 0; i < EPT; ++i) pv[i] = __ldg(&P[(size_t)m0->nbr[ec + i] * D + ch]);
+  }
+  for (int it = 0; it < ntiles; ++it) {
+    const int t0 = tr.eb + it * TT;
+    const int n_e = min(TT, tr.ee - t0);
+    TcMeta *M = G.meta(it);
+    const uint32_t d0 = 64u * (it & 1), d1 = 128u + 64u * (it & 1);
+    PHASE(0, it, 0);
+    G.wait(0);  // G1(it)
+    PHASE(0, it, 1);
 
-    // epilogue 1: h = ssp(W0 b + b0), staged in place in D0, then -> B of GEMM2
+    // epilogue 1: h = ssp(W0 b + b0), staged in place in D0, then -> act buffer
     float mx = 0.f;
 #pragma unroll
     for (int c0 = 0; c0 < EPT; c0 += 16) {
       float v[16];
-      tc::tmem_ld16(G.tl + TM_D0 + ec + c0, v);
+      tc::tmem_ld16(G.tl + d0 + ec + c0, v);
       tc::tmem_ld_wait();
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
@@ -446,14 +465,33 @@ k_edge_fwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
         v[i] = (ec + c0 + i) < n_e ? h : 0.f;
         mx = fmaxf(mx, fabsf(v[i]));
       }
-      tc::tmem_st16(G.tl + TM_D0 + ec + c0, v);
+      tc::tmem_st16(G.tl + d0 + ec + c0, v);
     }
     tc::tmem_st_wait();
+    PHASE(0, it, 2);
     int sh_ = 0;
-    if (!quant) sh_ = scale_exp(group_amax(mx, &G.meta->amax[0], G.bar_id, GT));
-    tmem_to_act(G.tl + TM_D0, G, pow2f(sh_), !quant);
-    GRP_ISSUE(G.tmem_g + TM_D1, sbase + SM_W1, W1_BYTES, D, false, G.sact, D, idesc, nprod);
-    GRP_WAIT();
+    if (!quant) sh_ = scale_exp(group_amax(mx, &M->amax[0], G.bar_id, GT));
+    PHASE(0, it, 3);
+    tmem_to_act(G.tl + d0, G, pow2f(sh_), !quant);
+    PHASE(0, it, 4);
+    GRP_ISSUE(1, G.tmem_g + d1, sbase + SM_W1, W1_BYTES, D, false, G.shb, D, idesc, nprod);
+    PHASE(0, it, 5);
+
+    // overlap with G2(it): basis of the next tile and its G1
+    if (it + 1 < ntiles) {
+      TcMeta *Mn = G.meta(it + 1);
+      const int n_n = min(TT, tr.ee - (t0 + TT));
+      tile_meta(a, geo, env, G, Mn, t0 + TT, n_n, false);
+      G.sync();
+      PHASE(0, it, 6);
+      tile_basis_tc(a, G, Mn, n_n, quant);
+      PHASE(0, it, 7);
+      GRP_ISSUE(0, G.tmem_g + (64u * ((it + 1) & 1)), sbase + SM_W0, W0_BYTES, DR, false, G.sbb,
+                DR, idesc, nprod);
+    }
+    PHASE(0, it, 8);
+    G.wait(1);  // G2(it)
+    PHASE(0, it, 9);
 
     // epilogue 2: m = (W1 h + b1) * P[src] (flash.py:229), in place in D1,
     // then dst segment sums (flash.py:232-234)
@@ -461,16 +499,24 @@ k_edge_fwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
 #pragma unroll
     for (int c = 0; c < EPT / 16; ++c) {
       float v[16];
-      tc::tmem_ld16(G.tl + TM_D1 + ec + 16 * c, v);
+      tc::tmem_ld16(G.tl + d1 + ec + 16 * c, v);
       tc::tmem_ld_wait();
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] = (v[i] * s1 + b1c) * pv[16 * c + i];
-      tc::tmem_st16(G.tl + TM_D1 + ec + 16 * c, v);
+      tc::tmem_st16(G.tl + d1 + ec + 16 * c, v);
     }
     tc::tmem_st_wait();
-    reduce_tile(G.tl + TM_D1, G, n_e, crow, cacc, H);
+    PHASE(0, it, 10);
+    reduce_tile(G.tl + d1, G, M, n_e, crow, cacc, H);
+    PHASE(0, it, 11);
+    if (it + 1 < ntiles) {
+      const TcMeta *Mn = G.meta(it + 1);
+#pragma unroll
+      for (int i = 0; i < EPT; ++i) pv[i] = __ldg(&P[(size_t)Mn->nbr[ec + i] * D + ch]);
+    }
     tc::fence_before_sync();
     G.sync();
+    PHASE(0, it, 12);
   }
   if (G.part == 0) finish_rows(crow, cacc, tr.rend, ch, H);
   tc::fence_before_sync();
@@ -483,9 +529,10 @@ k_edge_fwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
 //   b -> [G1] z0 -> h -> [G2] w;  gH = GH[dst], grad_w = gH*P[src] ->
 //   [G3] grad_h = grad_w W1 -> gz = grad_h*ssp'(z0) -> [G4] grad_b = gz W0
 //   -> grad_d = sum_k grad_b*db -> g_e = grad_d/d * u  (gsum, owner slot);
-//   grad_P rows = src-segment sums of gH*w (computed while G3 runs).
-// TMEM (per group): D0 z0 (then gz), D1 w (then gH*w), D2 h (then grad_h),
-// D3 grad_w stash (then grad_b from G4).
+//   grad_P rows = src-segment sums of gH*w (computed while G3 runs).  The
+//   basis and G1 of tile i+1 overlap G4 of tile i.
+// TMEM per group: D0 = 0 z0, D1 = 64 w (then gH*w), D2 = 128 h (then
+// grad_h, then gz), D3 = 192 grad_w stash (then grad_b from G4).
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__restrict__ env,
               const int32_t *__restrict__ unit_rows, const float *__restrict__ P,
@@ -497,14 +544,16 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
   const fcg_block &B = a.blk;
   kernel_prologue(sm, sh, B);
   Grp G = make_group(sm, sh);
-  float *red_s = (float *)G.act;
+  float *red_s = (float *)G.hb;
   const uint32_t sbase = tc::smem_u32(sm);
   const uint32_t idesc_fwd = tc::idesc_f16(128, TT, 0, 1);
   const uint32_t idesc_g3 = tc::idesc_f16(128, TT, 1, 1);
   const uint32_t idesc_g4 = tc::idesc_f16(64, TT, 1, 1);
   const int nprod_f = quant ? 1 : 3, nprod_b = quant ? 2 : 3;
+  constexpr uint32_t D0 = 0, D1 = 64, D2 = 128, D3 = 192;
 
   const UnitRange tr = unit_range(a, unit_rows, NGRP * blockIdx.x + G.g);
+  const int ntiles = (tr.ee - tr.eb + TT - 1) / TT;
   int crow = tr.rbeg;
   float cacc = 0.f;
 
@@ -518,15 +567,21 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
   const float q0 = quant ? __ldg(&B.f0_s[ch]) : 1.f;
   const int ew0 = quant ? 0 : B.f0_exp, ew1 = quant ? 0 : B.f1_exp;
 
-  for (int t0 = tr.eb; t0 < tr.ee; t0 += TT) {
-    const int n_e = min(TT, tr.ee - t0);
-    tile_meta(a, geo, env, G, t0, n_e, true);
+  if (ntiles > 0) {
+    TcMeta *m0 = G.meta(0);
+    tile_meta(a, geo, env, G, m0, tr.eb, min(TT, tr.ee - tr.eb), true);
     G.sync();
-    tile_basis_tc(a, G, n_e, quant);
-    GRP_ISSUE(G.tmem_g + TM_D0, sbase + SM_W0, W0_BYTES, DR, false, G.sact, DR, idesc_fwd,
+    tile_basis_tc(a, G, m0, min(TT, tr.ee - tr.eb), quant);
+    GRP_ISSUE(0, G.tmem_g + D0, sbase + SM_W0, W0_BYTES, DR, false, G.sbb, DR, idesc_fwd,
               nprod_f);
+  }
+  for (int it = 0; it < ntiles; ++it) {
+    const int t0 = tr.eb + it * TT;
+    const int n_e = min(TT, tr.ee - t0);
+    TcMeta *M = G.meta(it);
+    PHASE(1, it, 0);
     // while G1 runs: grad_w[c][e] = gH * P[src][c] (flash.py:291) into the
-    // D3 stash (G4 overwrites D3 only after grad_w is consumed) + tile max
+    // D3 stash + tile max
     float mx = 0.f;
 #pragma unroll
     for (int c0 = 0; c0 < EPT; c0 += 16) {
@@ -536,23 +591,25 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
         int e = ec + c0 + i;
         float g = 0.f;
         if (e < n_e)
-          g = __ldg(&GH[(size_t)G.meta->nbr[e] * D + ch]) *
-              __ldg(&P[(size_t)G.meta->own[e] * D + ch]);
+          g = __ldg(&GH[(size_t)M->nbr[e] * D + ch]) * __ldg(&P[(size_t)M->own[e] * D + ch]);
         v[i] = g * q1;
         mx = fmaxf(mx, fabsf(v[i]));
       }
-      tc::tmem_st16(G.tl + TM_D3 + ec + c0, v);
+      tc::tmem_st16(G.tl + D3 + ec + c0, v);
     }
     tc::tmem_st_wait();
-    const int sg = scale_exp(group_amax(mx, &G.meta->amax[1], G.bar_id, GT));
-    GRP_WAIT();
+    PHASE(1, it, 1);
+    const int sg = scale_exp(group_amax(mx, &M->amax[1], G.bar_id, GT));
+    PHASE(1, it, 2);
+    G.wait(0);  // G1(it)
+    PHASE(1, it, 3);
 
-    // recompute h = ssp(z0) into D2 (free until G3); z0 stays in D0
+    // recompute h = ssp(z0) into D2; z0 stays in D0
     mx = 0.f;
 #pragma unroll
     for (int c0 = 0; c0 < EPT; c0 += 16) {
       float v[16];
-      tc::tmem_ld16(G.tl + TM_D0 + ec + c0, v);
+      tc::tmem_ld16(G.tl + D0 + ec + c0, v);
       tc::tmem_ld_wait();
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
@@ -561,64 +618,84 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
         v[i] = (ec + c0 + i) < n_e ? h : 0.f;
         mx = fmaxf(mx, fabsf(v[i]));
       }
-      tc::tmem_st16(G.tl + TM_D2 + ec + c0, v);
+      tc::tmem_st16(G.tl + D2 + ec + c0, v);
     }
     tc::tmem_st_wait();
     int sh_ = 0;
-    if (!quant) sh_ = scale_exp(group_amax(mx, &G.meta->amax[0], G.bar_id, GT));
-    tmem_to_act(G.tl + TM_D2, G, pow2f(sh_), !quant);
-    GRP_ISSUE(G.tmem_g + TM_D1, sbase + SM_W1, W1_BYTES, D, false, G.sact, D, idesc_fwd,
-              nprod_f);
-    GRP_WAIT();
+    if (!quant) sh_ = scale_exp(group_amax(mx, &M->amax[0], G.bar_id, GT));
+    tmem_to_act(G.tl + D2, G, pow2f(sh_), !quant);
+    PHASE(1, it, 4);
+    GRP_ISSUE(1, G.tmem_g + D1, sbase + SM_W1, W1_BYTES, D, false, G.shb, D, idesc_fwd, nprod_f);
+    PHASE(1, it, 5);
+    G.wait(1);  // G2
+    PHASE(1, it, 6);
 
     // grad_w (stashed in D3) -> B operand of G3
-    tmem_to_act(G.tl + TM_D3, G, pow2f(sg), true);
-    GRP_ISSUE(G.tmem_g + TM_D2, sbase + SM_W1, W1_BYTES, D, true, G.sact, D, idesc_g3, nprod_b);
+    tmem_to_act(G.tl + D3, G, pow2f(sg), true);
+    GRP_ISSUE(1, G.tmem_g + D2, sbase + SM_W1, W1_BYTES, D, true, G.shb, D, idesc_g3, nprod_b);
+    PHASE(1, it, 7);
     // while G3 runs: grad_P rows = src-segment sums of gH * w (flash.py:283-288)
     {
       const float s1 = quant ? rs1 : pow2f(-(B.f1_exp + sh_));
 #pragma unroll
       for (int c0 = 0; c0 < EPT; c0 += 16) {
         float v[16], g[16];
-        tc::tmem_ld16(G.tl + TM_D1 + ec + c0, v);
+        tc::tmem_ld16(G.tl + D1 + ec + c0, v);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) g[i] = __ldg(&GH[(size_t)G.meta->nbr[ec + c0 + i] * D + ch]);
+        for (int i = 0; i < 16; ++i) g[i] = __ldg(&GH[(size_t)M->nbr[ec + c0 + i] * D + ch]);
         tc::tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = g[i] * (v[i] * s1 + b1c);
-        tc::tmem_st16(G.tl + TM_D1 + ec + c0, v);
+        tc::tmem_st16(G.tl + D1 + ec + c0, v);
       }
       tc::tmem_st_wait();
-      reduce_tile(G.tl + TM_D1, G, n_e, crow, cacc, GP);
+      PHASE(1, it, 8);
+      reduce_tile(G.tl + D1, G, M, n_e, crow, cacc, GP);
     }
-    GRP_WAIT();
+    PHASE(1, it, 9);
+    G.wait(1);  // G3
+    PHASE(1, it, 10);
 
-    // gz = grad_h * ssp'(z0) (mlp_backward_input, model.py:326-331), in place in D0
+    // gz = grad_h * ssp'(z0) (mlp_backward_input, model.py:326-331), in place in D2
     {
       const float sg3 = pow2f(-(ew1 + sg));
       mx = 0.f;
 #pragma unroll
       for (int c0 = 0; c0 < EPT; c0 += 16) {
         float gh[16], z[16];
-        tc::tmem_ld16(G.tl + TM_D2 + ec + c0, gh);
-        tc::tmem_ld16(G.tl + TM_D0 + ec + c0, z);
+        tc::tmem_ld16(G.tl + D2 + ec + c0, gh);
+        tc::tmem_ld16(G.tl + D0 + ec + c0, z);
         tc::tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           float z0 = z[i] * rs0 + b0c;
           float g = (ec + c0 + i) < n_e ? gh[i] * sg3 * sigmoid_fast(z0) * q0 : 0.f;
-          z[i] = g;
+          gh[i] = g;
           mx = fmaxf(mx, fabsf(g));
         }
-        tc::tmem_st16(G.tl + TM_D0 + ec + c0, z);
+        tc::tmem_st16(G.tl + D2 + ec + c0, gh);
       }
       tc::tmem_st_wait();
-      sh_ = scale_exp(group_amax(mx, &G.meta->amax[2], G.bar_id, GT));
-      tmem_to_act(G.tl + TM_D0, G, pow2f(sh_), true);
-      GRP_ISSUE(G.tmem_g + TM_D3, sbase + SM_W0, W0_BYTES, DR, true, G.sact, D, idesc_g4,
+      PHASE(1, it, 11);
+      sh_ = scale_exp(group_amax(mx, &M->amax[2], G.bar_id, GT));
+      tmem_to_act(G.tl + D2, G, pow2f(sh_), true);
+      GRP_ISSUE(1, G.tmem_g + D3, sbase + SM_W0, W0_BYTES, DR, true, G.shb, D, idesc_g4,
                 nprod_b);
     }
-    GRP_WAIT();
+    PHASE(1, it, 12);
+    // overlap with G4(it): basis of the next tile and its G1 (D0 is free now)
+    if (it + 1 < ntiles) {
+      TcMeta *Mn = G.meta(it + 1);
+      const int n_n = min(TT, tr.ee - (t0 + TT));
+      tile_meta(a, geo, env, G, Mn, t0 + TT, n_n, true);
+      G.sync();
+      tile_basis_tc(a, G, Mn, n_n, quant);
+      GRP_ISSUE(0, G.tmem_g + D0, sbase + SM_W0, W0_BYTES, DR, false, G.sbb, DR, idesc_fwd,
+                nprod_f);
+    }
+    PHASE(1, it, 13);
+    G.wait(1);  // G4
+    PHASE(1, it, 14);
 
     // grad_d[e] = sum_k grad_b[k][e] * db[k][e] (flash.py:293).  M=64 D lives
     // in lanes 32q + (0..15) of each quarter: row k = 16q + lane.
@@ -630,30 +707,31 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
 #pragma unroll
       for (int c0 = 0; c0 < EPT; c0 += 16) {
         float gb[16];
-        tc::tmem_ld16(G.tl + TM_D3 + ec + c0, gb);
+        tc::tmem_ld16(G.tl + D3 + ec + c0, gb);
         tc::tmem_ld_wait();
         if (G.lane < 16) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             int e = ec + c0 + i;
-            float dl = G.meta->d[e] - mu;
+            float dl = M->d[e] - mu;
             float gs = __expf((-a.gamma * dl) * dl);
-            float db = gs * (g2 * dl * G.meta->env[e] + G.meta->denv[e]);  // model.py:289
+            float db = gs * (g2 * dl * M->env[e] + M->denv[e]);  // model.py:289
             red_s[e * RED_LD + k] = gb[i] * s4 * db;
           }
         }
       }
     }
     G.sync();
+    PHASE(1, it, 15);
     if (G.gt < TT && G.gt < n_e) {
       const int e = G.gt;
       float gd = 0.f;
 #pragma unroll 8
       for (int k = 0; k < DR; ++k) gd += red_s[e * RED_LD + k];
-      float d = G.meta->d[e];
+      float d = M->d[e];
       float inv = d > TINY_DISTANCE ? 1.f / d : 0.f;  // _safe_inv, flash.py:176-178
       float s = gd * inv;
-      float4 u = G.meta->u[e];
+      float4 u = M->u[e];
       float4 g = make_float4(s * u.x, s * u.y, s * u.z, 0.f);
       float4 *dst = &gsum[t0 + e];
       if (accumulate) {
@@ -664,6 +742,7 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
     }
     tc::fence_before_sync();
     G.sync();
+    PHASE(1, it, 16);
   }
   if (G.part == 0) finish_rows(crow, cacc, tr.rend, ch, GP);
   tc::fence_before_sync();

@@ -685,6 +685,7 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
   ea.cutoff = m->cutoff; ea.gamma = m->gamma; ea.centers = m->centers;
   const int quant = m->format == FCG_FMT_W16;
   ea.quant = quant;
+  ea.dbg = g_dbg_phase;
   const bool simt = use_simt_edges();
   const int eg = simt ? 2 * sm_count() : sm_count();
   if (!simt) {
