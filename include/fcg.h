@@ -98,6 +98,14 @@ typedef struct {
   /* same images for the node MLPs (pre_linear, post0, post1), [2][D][D] */
   const uint16_t *pre_img, *p0_img, *p1_img;
   int pre_exp, p0_exp, p1_exp;
+  /* Static power-of-two operand scales of the fused edge kernels, chosen on
+   * the host from weight/basis bounds so the kernels need no per-tile max:
+   * f_hexp for h = ssp(filter0(b)) (|h| <= max_c sum_k |W0[c][k]| + |b0[c]|
+   * since 0 <= b <= 1), f_dbexp for the basis derivative db (|db| <=
+   * sqrt(2*gamma/e) + pi/(2*r_cut)); f1_qmax = max W16 row scale of filter
+   * layer 1 (1 for fp32), folded into grad_w's bound. */
+  int f_hexp, f_dbexp;
+  float f1_qmax;
 } fcg_block;
 
 typedef struct {

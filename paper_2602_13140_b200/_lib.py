@@ -32,7 +32,8 @@ class FcgBlock(C.Structure):
         [(n, _f) for n in ("pre_s", "f0_s", "f1_s", "p0_s", "p1_s")] + \
         [("f0_img", _u16), ("f1_img", _u16), ("f0_exp", C.c_int), ("f1_exp", C.c_int),
          ("pre_img", _u16), ("p0_img", _u16), ("p1_img", _u16),
-         ("pre_exp", C.c_int), ("p0_exp", C.c_int), ("p1_exp", C.c_int)]
+         ("pre_exp", C.c_int), ("p0_exp", C.c_int), ("p1_exp", C.c_int),
+         ("f_hexp", C.c_int), ("f_dbexp", C.c_int), ("f1_qmax", C.c_float)]
 
 
 class FcgModel(C.Structure):

@@ -78,6 +78,9 @@ struct EdgeArgs {
   const float *centers;
   fcg_block blk;
   int quant;
+  // device maxima of |P| and |GH| of the current block (written by the node
+  // kernels that produce them): the bound of grad_w = GH[dst] * P[src]
+  const unsigned int *amax_pg;
   unsigned long long *dbg;  // optional phase timestamps (fcg_debug_phase_buffer)
 };
 extern unsigned long long *g_dbg_phase;
@@ -142,13 +145,13 @@ int step_advance(int64_t *step, cudaStream_t s);
 // node_tc.cu
 void node_tc_configure();
 void launch_node_pre_tc(const float *X, const fcg_block &b, int quant, float *P, int nrows,
-                        cudaStream_t s);
+                        unsigned int *amax_p, cudaStream_t s);
 void launch_node_pre_bwd_tc(const float *GP, const fcg_block &b, int quant, float *G, int nrows,
-                            cudaStream_t s);
+                            const int32_t *csr_ptr, cudaStream_t s);
 void launch_node_post_tc(const float *H, const fcg_block &b, int quant, float *Zp, float *X,
-                         int nrows, cudaStream_t s);
+                         int nrows, const int32_t *csr_ptr, cudaStream_t s);
 void launch_node_post_bwd_tc(const float *G, const fcg_block &b, int quant, const float *Zp,
-                             float *GH, int nrows, cudaStream_t s);
+                             float *GH, int nrows, unsigned int *amax_gh, cudaStream_t s);
 void launch_readout_tc(const float *X, const fcg_model &m, float *per_atom, float *G, int nrows,
                        cudaStream_t s);
 // edge_tc.cu

@@ -1,9 +1,9 @@
 // (b)(c)(d) Fused edge passes on the 5th-generation tensor cores.
 //
 // Same contract as the fused edge loop of the reference (flash.py:215-236
-// forward, :272-295 backward) — edge tensors never reach HBM — but the four
-// per-edge filter-MLP GEMMs run as tcgen05.mma (kind::f16, fp32 accumulate
-// in TMEM).
+// forward, :272-295 backward) — edge tensors never reach HBM — with the
+// per-edge filter-MLP GEMMs on tcgen05.mma (kind::f16, fp32 accumulate in
+// TMEM).
 //
 // Formulation ("transposed"): D[channel][edge] = W[channel][k] * X[k][edge].
 //   A = weights, resident in SMEM for the whole kernel (K-major in the
@@ -12,23 +12,32 @@
 //       (MN-major: row = channel, contiguous edges);
 //   D = TMEM, lane = channel, column = edge.
 //
-// Work decomposition: a CTA (one per SM, 16 warps) hosts two independent
-// groups of 8 warps.  Both groups read the same resident weights but own a
-// separate range of CSR rows, 64-edge tiles, B-operand buffer, TMEM columns,
-// mbarrier and named barrier, so one group's MMA and gather latency hides
-// under the other group's epilogue.  Inside a group every thread owns one
-// channel across 32 consecutive edges of the tile (2 threads per channel),
-// so the destination (forward) / source (backward) segment reduction is a
-// running sum per thread plus an ordered 2-way merge, with a single store
-// per CSR row — no atomics.
+// Work decomposition: a CTA (one per SM, 16 warps) hosts four independent
+// groups of 4 warps (one warp per TMEM lane quarter).  All groups read the
+// same resident weights; each owns a range of whole CSR rows (balanced by
+// edge count), walks it in 32-edge tiles, and has its own B-operand
+// buffers, 128 TMEM columns, mbarriers and named barrier, so the MMA and
+// gather latency of one group hides under the epilogues of the other three.
+// Inside a group every thread owns one channel across all 32 edges of a
+// tile, so the destination (forward) / source (backward) segment reduction
+// is a running sum per thread with a single store per CSR row — no atomics,
+// no cross-thread merge.
 //
 // fp32 parity (SURVEY §7 hard part 2): plain fp16/TF32 operands lose ~1e-3;
-// we split both operands as x*2^s = hi + lo (fp16 each, ~22 significant
-// bits) and accumulate hi*hi + hi*lo + lo*hi.  Weights carry a host-chosen
-// power-of-two prescale; activations get a per-tile power-of-two scale from
-// a group max, removed exactly in the epilogue.  W16 weights (quantize.py)
-// use the stored fp16 weights directly: one MMA in the forward (inputs
-// rounded to fp16 as the reference does), two in the backward.
+// both operands are split as x*2^s = hi + lo (fp16 each, ~22 significant
+// bits) and we accumulate hi*hi + hi*lo + lo*hi.  Weights carry a
+// host-chosen power-of-two prescale.  Activation scales are static too —
+// chosen from bounds (host: h from the filter-0 weights, db from gamma and
+// r_cut; device: grad_w from max|GH| * max|P| written by the node kernels) —
+// so no tile needs a max-reduction barrier; the absolute split error stays
+// <= bound * 2^-39.  W16 weights (quantize.py) use the stored fp16 weights
+// directly: one MMA in the forward (inputs rounded to fp16 as the reference
+// does), two in the backward, dequant scales applied per channel.
+//
+// Backward (flash_block_backward): grad_d = sum_k grad_b[k] db[k] with
+// grad_b = W0^T gz is evaluated in forward mode as grad_d = sum_c gz[c] *
+// dz0[c] with dz0 = W0 db (one more K=64 GEMM, G1'), so gz never becomes a
+// tensor-core operand and the reduction over channels is a warp transpose-sum.
 #include <cuda_fp16.h>
 
 #include "common.cuh"
@@ -37,138 +46,85 @@
 
 namespace fcg {
 
-constexpr int TT = 64;           // edges per tile (MMA N)
-constexpr int NGRP = 2;          // independent warp groups per CTA
-constexpr int GT = 256;          // threads per group (8 warps, 2 per lane quarter)
+constexpr int TT = 32;           // edges per tile (MMA N)
+constexpr int NGRP = 4;          // independent warp groups per CTA
+constexpr int GT = 128;          // threads per group: one warp per TMEM lane quarter
 constexpr int TC_THREADS = NGRP * GT;
-constexpr int NPART = 2;         // edge parts per channel within a group
-constexpr int EPT = TT / NPART;  // edges per thread (32)
+constexpr int NMETA = 3;         // tile metadata ring per group
 constexpr uint32_t KSTR = (TT / 8) * 128;  // B operand bytes per 8 K-rows
 constexpr uint32_t SM_W0 = 0;          // W0 hi|lo: 2 x 128x64 fp16
 constexpr uint32_t SM_W1 = 32768;      // W1 hi|lo: 2 x 128x128 fp16
 constexpr uint32_t SM_BUF = 98304;     // per group: basis buffer (K=64) + act buffer (K=128)
-constexpr uint32_t BB_BYTES = 2 * 64 * TT * 2;   // basis hi|lo: 16 KB
-constexpr uint32_t HB_BYTES = 2 * 128 * TT * 2;  // h / grad_w / gz hi|lo, or fp32 scratch: 32 KB
+constexpr uint32_t BB_BYTES = 2 * DR * TT * 2;  // basis / db hi|lo: 8 KB
+constexpr uint32_t HB_BYTES = 2 * D * TT * 2;   // h / grad_w hi|lo: 16 KB
 constexpr uint32_t GBUF_BYTES = BB_BYTES + HB_BYTES;
 constexpr uint32_t SM_META = SM_BUF + NGRP * GBUF_BYTES;
-constexpr uint32_t W0_BYTES = 128 * 64 * 2, W1_BYTES = 128 * 128 * 2;
-constexpr int RED_LD = 65;       // padded stride of the [edge][k] fp32 scratch
+constexpr uint32_t W0_BYTES = D * DR * 2, W1_BYTES = D * D * 2;
+// TMEM columns inside a group's 128: z0 | w then dz0 | grad_h then gz | h (backward)
+constexpr uint32_t S0 = 0, S1 = 32, S2 = 64, S3 = 96;
+enum { BAR_G1 = 0, BAR_G2 = 1, BAR_G3 = 2, BAR_G1P = 3 };
 
-struct TcMeta {  // per tile (double-buffered per group)
+struct TcMeta {  // one tile
   int own[TT], nbr[TT];
   float d[TT], env[TT], denv[TT];
   float4 u[TT];
-  unsigned int amax[4];
-  float xch[NPART - 1][3][128];  // part 1 -> part 0 segment boundary partials
 };
 struct TcShared {
-  TcMeta meta[NGRP][2];
-  uint64_t bar[NGRP][2];  // [0]: GEMM1 commits, [1]: other GEMM commits
+  TcMeta meta[NGRP][NMETA];
+  float xg[NGRP][4][TT];  // per-quarter partial grad_d
+  uint64_t bar[NGRP][4];
   uint32_t tmem;
 };
 constexpr uint32_t SM_TOTAL = SM_META + sizeof(TcShared);
+static_assert(SM_TOTAL + 1024 <= 232448, "shared memory budget");
 
-// ---- CSR segment sums across the edge parts of a tile -------------------------
-// Each (channel, part) thread feeds its 32 edges in order: runs that start
-// and end inside the part are complete and written directly (one store per
-// row, empty rows between them zeroed); the first and last run of the part
-// go to an ordered merge done by the part-0 thread.
-struct Runs {
-  int row, nruns;
-  float acc, head;
-  __device__ __forceinline__ void init() { row = -1; nruns = 0; acc = 0.f; head = 0.f; }
-  __device__ __forceinline__ void begin(int o, int c, float *__restrict__ out) {
-    if (row >= 0) {
-      if (nruns == 0) head = acc; else out[(size_t)row * D + c] = acc;
-#pragma unroll 1
-      for (int z = row + 1; z < o; ++z) out[(size_t)z * D + c] = 0.f;
-      ++nruns;
-    }
-    row = o;
-    acc = 0.f;
-  }
-  // 16 consecutive edges e0.. with values m (first `cnt` valid).  Rows are
-  // warp-uniform; a chunk with one row or one row change avoids per-edge
-  // branches.
-  __device__ __forceinline__ void chunk(const int *own, int e0, int cnt, const float (&m)[16], int c,
-                                        float *__restrict__ out) {
-    if (cnt == 16) {
-      const int o0 = own[e0], o15 = own[e0 + 15];
-      if (o0 == o15) {
-        if (o0 != row) begin(o0, c, out);
+// ---- CSR segment sums -------------------------------------------------------
+// Running sum of one channel over edges in CSR order; each completed row is
+// stored once.  Rows are warp-uniform (all lanes walk the same edges).  Rows
+// without edges are never written: the node kernel that consumes the sums
+// reads them as zero through the CSR degree (an empty segment sums to 0,
+// flash.py:109-135), so the walk needs no zero-fill branches.
+struct SegSum {
+  int row;  // row of the open segment (-1 before the unit's first edge)
+  float acc;
+  __device__ __forceinline__ void tile(const int *own, int n, const float (&m)[TT], int c,
+                                       float *__restrict__ out) {
+#pragma unroll
+    for (int h = 0; h < TT; h += 16) {
+      int o[16];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int4 q = *(const int4 *)&own[h + 4 * j];
+        o[4 * j] = q.x; o[4 * j + 1] = q.y; o[4 * j + 2] = q.z; o[4 * j + 3] = q.w;
+      }
+      if (h + 16 <= n && o[0] == o[15]) {  // one row for all 16 edges
+        if (o[0] != row) {
+          if (row >= 0) out[(size_t)row * D + c] = acc;
+          row = o[0];
+          acc = 0.f;
+        }
         float s[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) s[i] = m[i] + m[i + 8];
+        for (int i = 0; i < 8; ++i) s[i] = m[h + i] + m[h + i + 8];
 #pragma unroll
         for (int i = 0; i < 4; ++i) s[i] += s[i + 4];
         acc += (s[0] + s[2]) + (s[1] + s[3]);
-        return;
-      }
-      // first index whose row equals the chunk's last row
-      int b = 15;
-      while (b > 0 && own[e0 + b - 1] == o15) --b;
-      bool single_change = true;
-#pragma unroll 1
-      for (int i = 1; i < b; ++i) single_change &= own[e0 + i] == o0;
-      if (single_change) {
-        float lo = 0.f, hi = 0.f;
+      } else {
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          if (i < b) lo += m[i]; else hi += m[i];
+          const bool valid = h + i < n;
+          const bool nr = valid && o[i] != row;
+          if (nr && row >= 0) out[(size_t)row * D + c] = acc;
+          acc = nr ? m[h + i] : (valid ? acc + m[h + i] : acc);
+          row = nr ? o[i] : row;
         }
-        if (o0 != row) begin(o0, c, out);
-        acc += lo;
-        begin(o15, c, out);
-        acc += hi;
-        return;
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      if (i < cnt) {
-        int o = own[e0 + i];
-        if (o != row) begin(o, c, out);
-        acc += m[i];
       }
     }
   }
-  __device__ __forceinline__ void close() {
-    if (row >= 0) {
-      if (nruns == 0) head = acc;
-      ++nruns;
-    }
+  __device__ __forceinline__ void finish(int c, float *__restrict__ out) {
+    if (row >= 0) out[(size_t)row * D + c] = acc;
   }
 };
-
-// Ordered merge of one part's boundary runs into the open carry segment.
-__device__ __forceinline__ void merge_part(int &crow, float &cacc, int nruns, float head,
-                                           float tail, int head_row, int tail_row, int c,
-                                           float *__restrict__ out) {
-  if (nruns == 0) return;
-  if (head_row == crow) {
-    cacc += head;
-  } else {
-    out[(size_t)crow * D + c] = cacc;
-#pragma unroll 1
-    for (int z = crow + 1; z < head_row; ++z) out[(size_t)z * D + c] = 0.f;
-    crow = head_row;
-    cacc = head;
-  }
-  if (nruns > 1) {  // head run complete; rows up to the tail were written by the part
-    out[(size_t)crow * D + c] = cacc;
-    crow = tail_row;
-    cacc = tail;
-  }
-}
-
-__device__ __forceinline__ void finish_rows(int crow, float cacc, int rend, int c,
-                                            float *__restrict__ out) {
-  if (crow < rend) {
-    out[(size_t)crow * D + c] = cacc;
-#pragma unroll 1
-    for (int z = crow + 1; z < rend; ++z) out[(size_t)z * D + c] = 0.f;
-  }
-}
 
 // ---- per-step edge geometry (the reference's d cache, flash.py:221-223) ------
 // geo[k] = (u, d) with u = r[own] - r[nbr] for CSR slot k; env[k] = (C, C').
@@ -194,7 +150,7 @@ k_edge_geom(const float *__restrict__ pos, const int32_t *__restrict__ ptr,
     float ux = __fsub_rn(po[0], pn[0]), uy = __fsub_rn(po[1], pn[1]), uz = __fsub_rn(po[2], pn[2]);
     float d = __fsqrt_rn(__fadd_rn(__fadd_rn(__fmul_rn(ux, ux), __fmul_rn(uy, uy)), __fmul_rn(uz, uz)));
     float c = 0.f, dc = 0.f;
-    if (d < cutoff) {  // cutoff_envelope(_grad), model.py:242-252
+    if (d < cutoff) {  // cutoff_envelope(_grad), model.py:110-120
       float sn, cs;
       sincosf((3.14159265358979f * d) / cutoff, &sn, &cs);
       c = 0.5f * (cs + 1.f);
@@ -205,23 +161,71 @@ k_edge_geom(const float *__restrict__ pos, const int32_t *__restrict__ ptr,
   }
 }
 
+// ---- descriptors and MMA chains ------------------------------------------------
+// A descriptor pair (hi image, lo image) and its advance per 16 K-values, in
+// the 16-byte units of the descriptor's address field (smem < 256 KB, so the
+// field never carries into LBO).
+struct Desc {
+  uint64_t hi, lo;
+  uint32_t step;
+};
+__device__ __forceinline__ Desc wdesc_k(uint32_t base, int in_dim, uint32_t lo_off) {
+  return {desc_w_kmajor(base, in_dim, 0), desc_w_kmajor(base + lo_off, in_dim, 0), 16u};
+}
+__device__ __forceinline__ Desc wdesc_mn(uint32_t base, int in_dim, uint32_t lo_off) {
+  return {desc_w_mnmajor(base, in_dim, 0), desc_w_mnmajor(base + lo_off, in_dim, 0),
+          (uint32_t)(in_dim >> 3) * 128u * 2u / 16u};
+}
+__device__ __forceinline__ Desc adesc(uint32_t base, int K) {
+  return {desc_act(base, 0, KSTR), desc_act(base + (uint32_t)K * (KSTR >> 3), 0, KSTR),
+          2u * KSTR / 16u};
+}
+// D (+)= A x B over KS k-steps with the product set {hi*hi, hi*lo, lo*hi}
+// truncated to NP terms.  Issued by one thread, fully unrolled.
+template <int KS, int NP>
+__device__ __forceinline__ void mma_chain(uint32_t d, Desc a, Desc b, uint32_t idesc) {
+#pragma unroll
+  for (int k = 0; k < KS; ++k) {
+    tc::mma_f16_ss(d, a.hi, b.hi, idesc, k > 0);
+    if (NP >= 2) tc::mma_f16_ss(d, a.hi, b.lo, idesc, 1);
+    if (NP >= 3) tc::mma_f16_ss(d, a.lo, b.hi, idesc, 1);
+    a.hi += a.step; a.lo += a.step;
+    b.hi += b.step; b.lo += b.step;
+  }
+}
+
+// Store 8 consecutive edges e0.. of K-row r of a B operand (hi image, and
+// the lo image K*KSTR/8 bytes further when LO), values times `scale`.
+template <bool LO>
+__device__ __forceinline__ void put8(uint8_t *act, int K, int r, int e0, const float *v,
+                                     float scale) {
+  const uint32_t off = (uint32_t)(r >> 3) * KSTR + (uint32_t)(e0 >> 3) * 128u + (uint32_t)(r & 7) * 16u;
+  __half2 hi[4], lo[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float a = v[2 * i] * scale, b = v[2 * i + 1] * scale;
+    hi[i] = __floats2half2_rn(a, b);
+    if (LO) {
+      const float2 hf = __half22float2(hi[i]);
+      lo[i] = __floats2half2_rn(a - hf.x, b - hf.y);
+    }
+  }
+  *(uint4 *)(act + off) = *(uint4 *)hi;
+  if (LO) *(uint4 *)(act + (uint32_t)K * (KSTR >> 3) + off) = *(uint4 *)lo;
+}
+
 // ---- per-group context ---------------------------------------------------------
 struct Grp {
-  int g;              // group index
-  int gt;             // thread index within the group
-  int warp, lane, quarter, part, ch, ec;
-  int bar_id;         // named barrier of the group
-  uint32_t tl;        // TMEM address of this lane quarter + group column base
-  uint32_t tmem_g;    // TMEM base of the group (lane 0)
-  uint8_t *bb, *hb;   // basis buffer, act buffer
-  uint32_t sbb, shb;  // their shared addresses
+  int g, gt, q, lane, ch, bar_id;
+  uint32_t tl;      // TMEM address of this warp's lane quarter at the group's columns
+  uint32_t tmem_g;  // TMEM address of the group's columns, lane 0
+  uint8_t *bb, *hb;
+  uint32_t sbb, shb;
   TcShared *sh;
-  uint32_t ph[2];
   __device__ __forceinline__ void sync() const { named_sync(bar_id, GT); }
-  __device__ __forceinline__ TcMeta *meta(int i) const { return &sh->meta[g][i & 1]; }
-  __device__ __forceinline__ void wait(int which) {
-    tc::mbar_wait(&sh->bar[g][which], ph[which]);
-    ph[which] ^= 1;
+  __device__ __forceinline__ TcMeta *meta(int it) const { return &sh->meta[g][it % NMETA]; }
+  __device__ __forceinline__ void wait(int which, int it) const {
+    tc::mbar_wait(&sh->bar[g][which], (uint32_t)(it & 1));
     tc::fence_after_sync();
   }
 };
@@ -230,36 +234,28 @@ __device__ __forceinline__ Grp make_group(uint8_t *sm, TcShared *sh) {
   Grp G;
   G.g = threadIdx.x / GT;
   G.gt = threadIdx.x % GT;
-  G.warp = G.gt >> 5;
+  G.q = G.gt >> 5;
   G.lane = threadIdx.x & 31;
-  G.quarter = G.warp & 3;
-  G.part = G.warp >> 2;
-  G.ch = 32 * G.quarter + G.lane;
-  G.ec = EPT * G.part;
+  G.ch = 32 * G.q + G.lane;
   G.bar_id = 1 + G.g;
   G.sh = sh;
   G.bb = sm + SM_BUF + G.g * GBUF_BYTES;
   G.hb = G.bb + BB_BYTES;
   G.sbb = tc::smem_u32(G.bb);
   G.shb = tc::smem_u32(G.hb);
-  G.tmem_g = sh->tmem + 256u * G.g;
-  G.tl = G.tmem_g + ((uint32_t)(32 * G.quarter) << 16);
-  G.ph[0] = G.ph[1] = 0;
+  G.tmem_g = sh->tmem + 128u * G.g;
+  G.tl = G.tmem_g + ((uint32_t)(32 * G.q) << 16);
   return G;
 }
 
-__device__ __forceinline__ void stage_weights(uint8_t *sm, const fcg_block &b) {
+__device__ __forceinline__ void kernel_prologue(uint8_t *sm, TcShared *sh, const fcg_block &b) {
   const uint4 *s0 = (const uint4 *)b.f0_img, *s1 = (const uint4 *)b.f1_img;
   uint4 *d0 = (uint4 *)(sm + SM_W0), *d1 = (uint4 *)(sm + SM_W1);
   for (int q = threadIdx.x; q < (int)(2 * W0_BYTES / 16); q += TC_THREADS) d0[q] = __ldg(s0 + q);
   for (int q = threadIdx.x; q < (int)(2 * W1_BYTES / 16); q += TC_THREADS) d1[q] = __ldg(s1 + q);
-}
-
-__device__ __forceinline__ void kernel_prologue(uint8_t *sm, TcShared *sh, const fcg_block &B) {
-  stage_weights(sm, B);
   if (threadIdx.x % GT == 0) {
-    tc::mbar_init(&sh->bar[threadIdx.x / GT][0], 1);
-    tc::mbar_init(&sh->bar[threadIdx.x / GT][1], 1);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) tc::mbar_init(&sh->bar[threadIdx.x / GT][i], 1);
     tc::fence_mbar_init();
   }
   if (threadIdx.x < 32) tc::tmem_alloc<512>(&sh->tmem);
@@ -269,112 +265,113 @@ __device__ __forceinline__ void kernel_prologue(uint8_t *sm, TcShared *sh, const
   tc::fence_after_sync();
 }
 
-__device__ __forceinline__ void tile_meta(const EdgeArgs &a, const float4 *__restrict__ geo,
-                                          const float2 *__restrict__ env, const Grp &G,
-                                          TcMeta *m, int t0, int n_e, bool src_owned) {
-  int t = G.gt;
-  if (t < TT) {
-    int o = -1, n = 0;
-    float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
-    float2 c = make_float2(0.f, 0.f);
-    if (t < n_e) {
-      o = a.own[t0 + t];
-      n = a.nbr[t0 + t];
-      g = geo[t0 + t];
-      c = env[t0 + t];
-    }
-    // backward edge (dst=nbr, src=own): u = r_nbr - r_own (flash.py:279)
-    if (src_owned) { g.x = -g.x; g.y = -g.y; g.z = -g.z; }
-    m->own[t] = o;
-    m->nbr[t] = n;
-    m->d[t] = g.w;
-    m->env[t] = c.x;
-    m->denv[t] = c.y;
-    m->u[t] = make_float4(g.x, g.y, g.z, 0.f);
+// One lane per edge (warp 0 of the group): slot ids and cached geometry of
+// a tile.  Padding edges get own = -1, nbr = 0 and zero geometry.
+__device__ __forceinline__ void load_meta(const EdgeArgs &a, const float4 *__restrict__ geo,
+                                          const float2 *__restrict__ env, TcMeta *m, int t0,
+                                          int n_e, bool src_owned, int lane) {
+  int o = -1, n = 0;
+  float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+  float2 c = make_float2(0.f, 0.f);
+  if (lane < n_e) {
+    o = a.own[t0 + lane];
+    n = a.nbr[t0 + lane];
+    g = geo[t0 + lane];
+    c = env[t0 + lane];
   }
-  if (t < 4) m->amax[t] = 0u;
+  // backward edge (dst=nbr, src=own): u = r_nbr - r_own (flash.py:279)
+  if (src_owned) { g.x = -g.x; g.y = -g.y; g.z = -g.z; }
+  m->own[lane] = o;
+  m->nbr[lane] = n;
+  m->d[lane] = g.w;
+  m->env[lane] = c.x;
+  m->denv[lane] = c.y;
+  m->u[lane] = make_float4(g.x, g.y, g.z, 0.f);
 }
 
-// Basis b[k][e] (model.py:255-265) as the K=64 B operand (basis buffer):
-// fp32 path scaled by 2^14 and split; W16 path rounded to fp16 unscaled
-// (quantize.py:68-71).
-__device__ __forceinline__ void tile_basis_tc(const EdgeArgs &a, const Grp &G, const TcMeta *m,
-                                              int n_e, bool quant) {
-#pragma unroll 2
-  for (int q = G.gt; q < DR * (TT / 8); q += GT) {
-    int k = q % DR, e0 = (q / DR) * 8;
-    float mu = __ldg(&a.centers[k]);
-    float4 d0 = *(const float4 *)&m->d[e0], d1 = *(const float4 *)&m->d[e0 + 4];
-    float4 c0 = *(const float4 *)&m->env[e0], c1 = *(const float4 *)&m->env[e0 + 4];
-    float dd[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
-    float cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-    float v[8];
+// Gaussian basis b[k][e] = exp((-g*dk)*dk) * C(d) (model.py:123-133) or, with
+// DERIV, its derivative db = exp(..) * (-2 g dk C + C') (model.py:148-157),
+// as the K=64 B operand.  Thread gt: k = gt%64, 16 edges.  The fp32 forward
+// basis is scaled 2^14 and split; the W16 forward basis is rounded to fp16
+// unscaled (quantize.py:68-71); db is always split (fp32 backward).  Padding
+// edges carry C = C' = 0, so their columns are zero without a mask.
+template <bool DERIV, bool Q>
+__device__ __forceinline__ void tile_basis(const EdgeArgs &a, const Grp &G, const TcMeta *m,
+                                           float scale) {
+  const int k = G.gt & (DR - 1), e0 = (G.gt / DR) * 16;
+  const float mu = __ldg(&a.centers[k]);
+  const float ngl = -a.gamma * kLog2e, g2 = -2.f * a.gamma;
+  float v[16];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      float dl = dd[i] - mu;
-      v[i] = (e0 + i) < n_e ? __expf((-a.gamma * dl) * dl) * cc[i] : 0.f;
+  for (int j = 0; j < 4; ++j) {
+    const float4 d4 = *(const float4 *)&m->d[e0 + 4 * j];
+    const float4 c4 = *(const float4 *)&m->env[e0 + 4 * j];
+    const float dd[4] = {d4.x, d4.y, d4.z, d4.w}, cc[4] = {c4.x, c4.y, c4.z, c4.w};
+    float pp[4] = {0.f, 0.f, 0.f, 0.f};
+    if (DERIV) {
+      const float4 p4 = *(const float4 *)&m->denv[e0 + 4 * j];
+      pp[0] = p4.x; pp[1] = p4.y; pp[2] = p4.z; pp[3] = p4.w;
     }
-    put_b8n(G.bb, DR, KSTR, k, e0, v, quant ? 1.f : 16384.f, !quant);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float dl = dd[i] - mu;
+      const float gs = (Q && !DERIV) ? expf((-a.gamma * dl) * dl) : ex2_ftz((ngl * dl) * dl);
+      v[4 * j + i] = DERIV ? gs * (g2 * dl * cc[i] + pp[i]) : gs * cc[i];
+    }
   }
+  constexpr bool LO = DERIV || !Q;
+  put8<LO>(G.bb, DR, k, e0, &v[0], scale);
+  put8<LO>(G.bb, DR, k, e0 + 8, &v[8], scale);
 }
 
-// Segment reduction of a [128 ch][64 e] fp32 tile held in TMEM columns
-// starting at tcol: both parts scan, part 1 publishes boundary partials, part
-// 0 merges them into the carry.  Called by every thread of the group.
-__device__ __forceinline__ void reduce_tile(uint32_t tcol, const Grp &G, TcMeta *meta, int n_e,
-                                            int &crow, float &cacc, float *__restrict__ out) {
-  const int lo = EPT * G.part, hi = min(lo + EPT, n_e);
-  Runs r;
-  r.init();
-#pragma unroll 1
-  for (int c0 = 0; c0 < EPT; c0 += 16) {
-    float m[16];
-    tc::tmem_ld16(tcol + lo + c0, m);
-    tc::tmem_ld_wait();
-    r.chunk(meta->own, lo + c0, min(16, hi - lo - c0), m, G.ch, out);
+// h = ssp(z0) for this thread's channel over the tile (z0 = TMEM S0 scaled),
+// as the K=128 B operand (act buffer); padding edges give 0.  With STASH the
+// fp32 h also goes to TMEM S3 (the backward derives ssp'(z0) from it).
+template <bool Q, bool STASH>
+__device__ __forceinline__ void tile_h(const Grp &G, float rs0, float b0c, float hs, int n_e) {
+  float v[TT];
+  tc::tmem_ld32w(G.tl + S0, v);
+#pragma unroll
+  for (int i = 0; i < TT; ++i) {
+    float h;
+    if (Q) h = __half2float(__float2half_rn(ssp_ref(v[i] * rs0 + b0c)));
+    else h = ssp_fast(v[i] * rs0 + b0c);
+    v[i] = i < n_e ? h : 0.f;
   }
-  r.close();
-  if (G.part == 1) {
-    meta->xch[0][0][G.ch] = r.head;
-    meta->xch[0][1][G.ch] = r.acc;
-    meta->xch[0][2][G.ch] = __int_as_float(r.nruns);
-  }
-  G.sync();
-  if (G.part == 0) {
-    merge_part(crow, cacc, r.nruns, r.head, r.acc, meta->own[0], meta->own[max(hi - 1, 0)], G.ch,
-               out);
-    merge_part(crow, cacc, __float_as_int(meta->xch[0][2][G.ch]), meta->xch[0][0][G.ch],
-               meta->xch[0][1][G.ch], meta->own[EPT], meta->own[max(n_e - 1, EPT)], G.ch, out);
-  }
+  if (STASH) tc::tmem_st32(G.tl + S3, v);
+#pragma unroll
+  for (int j = 0; j < TT / 8; ++j) put8<!Q>(G.hb, D, G.ch, 8 * j, &v[8 * j], hs);
+  if (STASH) tc::tmem_st_wait();
 }
 
-// Write this thread's [ch][32 edges] fp32 TMEM block as the hi/lo fp16 B
-// operand (K = 128 rows, act buffer) of the next GEMM with the given scale.
-__device__ __forceinline__ void tmem_to_act(uint32_t tcol, const Grp &G, float scale,
-                                            bool with_lo) {
-#pragma unroll 1
-  for (int c0 = 0; c0 < EPT; c0 += 16) {
-    float v[16];
-    tc::tmem_ld16(tcol + G.ec + c0, v);
-    tc::tmem_ld_wait();
-    put_b8n(G.hb, D, KSTR, G.ch, G.ec + c0, &v[0], scale, with_lo);
-    put_b8n(G.hb, D, KSTR, G.ch, G.ec + c0 + 8, &v[8], scale, with_lo);
+// Sum of p over the 32 lanes of the warp for every edge: a butterfly
+// reduce-scatter leaves edge `lane`'s sum in lane `lane`.
+__device__ __forceinline__ float warp_edge_sum(float (&p)[TT], int lane) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool upper = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < o; ++i) {
+      const float send = upper ? p[i] : p[i + o];
+      const float keep = upper ? p[i + o] : p[i];
+      p[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
   }
+  return p[0];
 }
 
-// all threads of the group: make the smem operand writes visible to the
-// tensor core, then the group's first thread issues the GEMM and commits it
-// to barrier `which`
-#define GRP_ISSUE(which, ...)           \
-  do {                                  \
-    tc::fence_async_smem();             \
-    tc::fence_before_sync();            \
-    G.sync();                           \
-    if (G.gt == 0) {                    \
-      tc::fence_after_sync();           \
-      issue_gemm(__VA_ARGS__, KSTR);    \
-      tc::mma_commit(&G.sh->bar[G.g][which]); \
-    }                                   \
+// all threads of the group: make the smem operand writes (and TMEM reads)
+// visible, then the group's first thread issues the chain and commits it
+#define GRP_ISSUE(which, CHAIN)                     \
+  do {                                              \
+    tc::fence_async_smem();                         \
+    tc::fence_before_sync();                        \
+    G.sync();                                       \
+    if (G.gt == 0) {                                \
+      tc::fence_after_sync();                       \
+      CHAIN;                                        \
+      tc::mma_commit(&G.sh->bar[G.g][which]);       \
+    }                                               \
   } while (0)
 
 // phase timestamps for diagnosis: CTA 0, group 0, first 16 tiles
@@ -402,137 +399,101 @@ __device__ __forceinline__ UnitRange unit_range(const EdgeArgs &a, const int32_t
 }
 
 // ---------------------------------------------------------------------------
-// Forward: per 64-edge tile of dst rows
-//   b -> [G1] z0 -> h=ssp(z0) -> [G2] w -> m = P[src]*w -> H rows.
-// Software-pipelined per group: while G2(i) runs the group builds the basis
-// of tile i+1 and issues G1(i+1); while G1(i+1) runs it finishes tile i
-// (messages + segment sums).  TMEM per group: D0[2] = cols 0/64 (z0, h),
-// D1[2] = 128/192 (w, m), by tile parity.
+// Forward: per 32-edge tile of dst rows
+//   b -> [G1] z0 -> h = ssp(z0) -> [G2] w -> m = P[src]*w -> H rows.
+// While G2(i) runs the group builds the basis of tile i+1 and issues
+// G1(i+1); the gathers P[src] of tile i+1 are in flight during G1(i+1).
+template <bool Q>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_edge_fwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__restrict__ env,
               const int32_t *__restrict__ unit_rows, const float *__restrict__ P,
               float *__restrict__ H) {
   extern __shared__ __align__(1024) uint8_t sm[];
   TcShared *sh = (TcShared *)(sm + SM_META);
-  const bool quant = a.quant != 0;
   const fcg_block &B = a.blk;
   kernel_prologue(sm, sh, B);
-  Grp G = make_group(sm, sh);
+  const Grp G = make_group(sm, sh);
   const uint32_t sbase = tc::smem_u32(sm);
   const uint32_t idesc = tc::idesc_f16(128, TT, 0, 1);
-  const int nprod = quant ? 1 : 3;
+  constexpr int NP = Q ? 1 : 3;
+  const Desc w0 = wdesc_k(sbase + SM_W0, DR, W0_BYTES), w1 = wdesc_k(sbase + SM_W1, D, W1_BYTES);
+  const Desc bb = adesc(G.sbb, DR), hb = adesc(G.shb, D);
 
   const UnitRange tr = unit_range(a, unit_rows, NGRP * blockIdx.x + G.g);
   const int ntiles = (tr.ee - tr.eb + TT - 1) / TT;
-  int crow = tr.rbeg;
-  float cacc = 0.f;
+  SegSum seg;
+  seg.row = -1;
+  seg.acc = 0.f;
 
-  const int ch = G.ch, ec = G.ec;
+  const int ch = G.ch;
   const float b0c = __ldg(&B.f0_b[ch]), b1c = __ldg(&B.f1_b[ch]);
-  const float rs0 = quant ? __ldg(&B.f0_s[ch]) : pow2f(-(B.f0_exp + 14));
-  const float rs1 = quant ? __ldg(&B.f1_s[ch]) : 1.f;
+  const float rs0 = Q ? __ldg(&B.f0_s[ch]) : pow2f(-(B.f0_exp + 14));
+  const float hs = Q ? 1.f : pow2f(B.f_hexp);
+  const float s1 = Q ? __ldg(&B.f1_s[ch]) : pow2f(-(B.f1_exp + B.f_hexp));
 
-  float pv[EPT];  // P[src][ch] of this thread's edges of the current tile
+  float pv[TT];  // P[src][ch] of the current tile
   if (ntiles > 0) {
-    TcMeta *m0 = G.meta(0);
-    tile_meta(a, geo, env, G, m0, tr.eb, min(TT, tr.ee - tr.eb), false);
+    const int n0 = min(TT, tr.ee - tr.eb);
+    if (G.gt < 32) load_meta(a, geo, env, G.meta(0), tr.eb, n0, false, G.lane);
     G.sync();
-    tile_basis_tc(a, G, m0, min(TT, tr.ee - tr.eb), quant);
-    GRP_ISSUE(0, G.tmem_g + 0, sbase + SM_W0, W0_BYTES, DR, false, G.sbb, DR, idesc, nprod);
+    tile_basis<false, Q>(a, G, G.meta(0), Q ? 1.f : 16384.f);
+    GRP_ISSUE(BAR_G1, (mma_chain<DR / 16, NP>(G.tmem_g + S0, w0, bb, idesc)));
+    const TcMeta *M0 = G.meta(0);
 #pragma unroll
-    for (int i = 0; i < EPT; ++i) pv[i] = __ldg(&P[(size_t)m0->nbr[ec + i] * D + ch]);
+    for (int i = 0; i < TT; ++i) pv[i] = __ldg(&P[(size_t)M0->nbr[i] * D + ch]);
   }
   for (int it = 0; it < ntiles; ++it) {
     const int t0 = tr.eb + it * TT;
     const int n_e = min(TT, tr.ee - t0);
-    TcMeta *M = G.meta(it);
-    const uint32_t d0 = 64u * (it & 1), d1 = 128u + 64u * (it & 1);
+    const bool more = it + 1 < ntiles;
+    const TcMeta *M = G.meta(it);
     PHASE(0, it, 0);
-    G.wait(0);  // G1(it)
+    if (more && G.gt < 32)
+      load_meta(a, geo, env, G.meta(it + 1), t0 + TT, min(TT, tr.ee - t0 - TT), false, G.lane);
+    G.wait(BAR_G1, it);
     PHASE(0, it, 1);
-
-    // epilogue 1: h = ssp(W0 b + b0), staged in place in D0, then -> act buffer
-    float mx = 0.f;
-#pragma unroll
-    for (int c0 = 0; c0 < EPT; c0 += 16) {
-      float v[16];
-      tc::tmem_ld16(G.tl + d0 + ec + c0, v);
-      tc::tmem_ld_wait();
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        float h = ssp_fast(v[i] * rs0 + b0c);
-        if (quant) h = __half2float(__float2half_rn(h));
-        v[i] = (ec + c0 + i) < n_e ? h : 0.f;
-        mx = fmaxf(mx, fabsf(v[i]));
-      }
-      tc::tmem_st16(G.tl + d0 + ec + c0, v);
-    }
-    tc::tmem_st_wait();
+    tile_h<Q, false>(G, rs0, b0c, hs, n_e);
     PHASE(0, it, 2);
-    int sh_ = 0;
-    if (!quant) sh_ = scale_exp(group_amax(mx, &M->amax[0], G.bar_id, GT));
+    GRP_ISSUE(BAR_G2, (mma_chain<D / 16, NP>(G.tmem_g + S1, w1, hb, idesc)));
     PHASE(0, it, 3);
-    tmem_to_act(G.tl + d0, G, pow2f(sh_), !quant);
+    if (more) {  // basis + G1 of the next tile overlap G2
+      tile_basis<false, Q>(a, G, G.meta(it + 1), Q ? 1.f : 16384.f);
+      GRP_ISSUE(BAR_G1, (mma_chain<DR / 16, NP>(G.tmem_g + S0, w0, bb, idesc)));
+    }
     PHASE(0, it, 4);
-    GRP_ISSUE(1, G.tmem_g + d1, sbase + SM_W1, W1_BYTES, D, false, G.shb, D, idesc, nprod);
+    G.wait(BAR_G2, it);
     PHASE(0, it, 5);
-
-    // overlap with G2(it): basis of the next tile and its G1
-    if (it + 1 < ntiles) {
-      TcMeta *Mn = G.meta(it + 1);
-      const int n_n = min(TT, tr.ee - (t0 + TT));
-      tile_meta(a, geo, env, G, Mn, t0 + TT, n_n, false);
-      G.sync();
-      PHASE(0, it, 6);
-      tile_basis_tc(a, G, Mn, n_n, quant);
-      PHASE(0, it, 7);
-      GRP_ISSUE(0, G.tmem_g + (64u * ((it + 1) & 1)), sbase + SM_W0, W0_BYTES, DR, false, G.sbb,
-                DR, idesc, nprod);
-    }
-    PHASE(0, it, 8);
-    G.wait(1);  // G2(it)
-    PHASE(0, it, 9);
-
-    // epilogue 2: m = (W1 h + b1) * P[src] (flash.py:229), in place in D1,
-    // then dst segment sums (flash.py:232-234)
-    const float s1 = quant ? rs1 : pow2f(-(B.f1_exp + sh_));
+    // m = (W1 h + b1) * P[src] (flash.py:229), dst segment sums (flash.py:232-234)
+    {
+      float v[TT];
+      tc::tmem_ld32w(G.tl + S1, v);
 #pragma unroll
-    for (int c = 0; c < EPT / 16; ++c) {
-      float v[16];
-      tc::tmem_ld16(G.tl + d1 + ec + 16 * c, v);
-      tc::tmem_ld_wait();
-#pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = (v[i] * s1 + b1c) * pv[16 * c + i];
-      tc::tmem_st16(G.tl + d1 + ec + 16 * c, v);
+      for (int i = 0; i < TT; ++i) v[i] = (v[i] * s1 + b1c) * pv[i];
+      seg.tile(M->own, n_e, v, ch, H);
     }
-    tc::tmem_st_wait();
-    PHASE(0, it, 10);
-    reduce_tile(G.tl + d1, G, M, n_e, crow, cacc, H);
-    PHASE(0, it, 11);
-    if (it + 1 < ntiles) {
+    PHASE(0, it, 6);
+    if (more) {
       const TcMeta *Mn = G.meta(it + 1);
 #pragma unroll
-      for (int i = 0; i < EPT; ++i) pv[i] = __ldg(&P[(size_t)Mn->nbr[ec + i] * D + ch]);
+      for (int i = 0; i < TT; ++i) pv[i] = __ldg(&P[(size_t)Mn->nbr[i] * D + ch]);
     }
-    tc::fence_before_sync();
-    G.sync();
-    PHASE(0, it, 12);
   }
-  if (G.part == 0) finish_rows(crow, cacc, tr.rend, ch, H);
+  seg.finish(ch, H);
   tc::fence_before_sync();
   __syncthreads();
   if (threadIdx.x < 32) tc::tmem_dealloc<512>(sh->tmem);
 }
 
 // ---------------------------------------------------------------------------
-// Backward over src-owned rows (flash_block_backward, flash.py:272-295):
-//   b -> [G1] z0 -> h -> [G2] w;  gH = GH[dst], grad_w = gH*P[src] ->
-//   [G3] grad_h = grad_w W1 -> gz = grad_h*ssp'(z0) -> [G4] grad_b = gz W0
-//   -> grad_d = sum_k grad_b*db -> g_e = grad_d/d * u  (gsum, owner slot);
-//   grad_P rows = src-segment sums of gH*w (computed while G3 runs).  The
-//   basis and G1 of tile i+1 overlap G4 of tile i.
-// TMEM per group: D0 = 0 z0, D1 = 64 w (then gH*w), D2 = 128 h (then
-// grad_h, then gz), D3 = 192 grad_w stash (then grad_b from G4).
+// Backward over src-owned rows (flash_block_backward, flash.py:272-295), per
+// 32-edge tile:
+//   gH = GH[dst]; [G1] z0 (recompute) -> h -> [G2] w;
+//   grad_w = gH*P[src] -> [G3, W1 MN-major] grad_h;
+//   grad_P rows = src-segment sums of gH*w (while G3 runs);
+//   db -> [G1'] dz0 = W0 db;  gz = grad_h * ssp'(z0);
+//   grad_d = sum_c gz*dz0 (= sum_k grad_b*db, flash.py:293) -> g_e = grad_d/d*u.
+// The basis and G1 of tile i+1 overlap the grad_d reduction of tile i.
+template <bool Q>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__restrict__ env,
               const int32_t *__restrict__ unit_rows, const float *__restrict__ P,
@@ -540,211 +501,160 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
               int accumulate) {
   extern __shared__ __align__(1024) uint8_t sm[];
   TcShared *sh = (TcShared *)(sm + SM_META);
-  const bool quant = a.quant != 0;
   const fcg_block &B = a.blk;
   kernel_prologue(sm, sh, B);
-  Grp G = make_group(sm, sh);
-  float *red_s = (float *)G.hb;
+  const Grp G = make_group(sm, sh);
   const uint32_t sbase = tc::smem_u32(sm);
-  const uint32_t idesc_fwd = tc::idesc_f16(128, TT, 0, 1);
-  const uint32_t idesc_g3 = tc::idesc_f16(128, TT, 1, 1);
-  const uint32_t idesc_g4 = tc::idesc_f16(64, TT, 1, 1);
-  const int nprod_f = quant ? 1 : 3, nprod_b = quant ? 2 : 3;
-  constexpr uint32_t D0 = 0, D1 = 64, D2 = 128, D3 = 192;
+  const uint32_t id_f = tc::idesc_f16(128, TT, 0, 1);
+  const uint32_t id_t = tc::idesc_f16(128, TT, 1, 1);
+  constexpr int NPF = Q ? 1 : 3, NPB = Q ? 2 : 3;
+  const Desc w0 = wdesc_k(sbase + SM_W0, DR, W0_BYTES), w1 = wdesc_k(sbase + SM_W1, D, W1_BYTES);
+  const Desc w1t = wdesc_mn(sbase + SM_W1, D, W1_BYTES);
+  const Desc bb = adesc(G.sbb, DR), hb = adesc(G.shb, D);
 
   const UnitRange tr = unit_range(a, unit_rows, NGRP * blockIdx.x + G.g);
   const int ntiles = (tr.ee - tr.eb + TT - 1) / TT;
-  int crow = tr.rbeg;
-  float cacc = 0.f;
+  SegSum seg;
+  seg.row = -1;
+  seg.acc = 0.f;
 
-  const int ch = G.ch, ec = G.ec;
+  const int ch = G.ch;
   const float b0c = __ldg(&B.f0_b[ch]), b1c = __ldg(&B.f1_b[ch]);
-  const float rs0 = quant ? __ldg(&B.f0_s[ch]) : pow2f(-(B.f0_exp + 14));
-  const float rs1 = quant ? __ldg(&B.f1_s[ch]) : 1.f;
+  const float rs0 = Q ? __ldg(&B.f0_s[ch]) : pow2f(-(B.f0_exp + 14));
+  const float hs = Q ? 1.f : pow2f(B.f_hexp);
+  const float s1 = Q ? __ldg(&B.f1_s[ch]) : pow2f(-(B.f1_exp + B.f_hexp));
   // backward GEMMs against the stored fp16 weights fold the W16 dequant
-  // scale into the operand: g @ (s*w16) == (g*s) @ w16
-  const float q1 = quant ? __ldg(&B.f1_s[ch]) : 1.f;
-  const float q0 = quant ? __ldg(&B.f0_s[ch]) : 1.f;
-  const int ew0 = quant ? 0 : B.f0_exp, ew1 = quant ? 0 : B.f1_exp;
+  // scale of the contracted index into the operand: g @ (s*w16) == (g*s) @ w16
+  const float q1 = Q ? __ldg(&B.f1_s[ch]) : 1.f;
+  const float pmax = __uint_as_float(a.amax_pg[0]), ghmax = __uint_as_float(a.amax_pg[1]);
+  const int sg = scale_exp(pmax * ghmax * B.f1_qmax);
+  const float gws = pow2f(sg);
+  const float sg3 = pow2f(-((Q ? 0 : B.f1_exp) + sg));
+  const float dbs = pow2f(B.f_dbexp);
+  const float sdz = (Q ? __ldg(&B.f0_s[ch]) : pow2f(-B.f0_exp)) * pow2f(-B.f_dbexp);
 
   if (ntiles > 0) {
-    TcMeta *m0 = G.meta(0);
-    tile_meta(a, geo, env, G, m0, tr.eb, min(TT, tr.ee - tr.eb), true);
+    const int n0 = min(TT, tr.ee - tr.eb);
+    if (G.gt < 32) load_meta(a, geo, env, G.meta(0), tr.eb, n0, true, G.lane);
     G.sync();
-    tile_basis_tc(a, G, m0, min(TT, tr.ee - tr.eb), quant);
-    GRP_ISSUE(0, G.tmem_g + D0, sbase + SM_W0, W0_BYTES, DR, false, G.sbb, DR, idesc_fwd,
-              nprod_f);
+    tile_basis<false, Q>(a, G, G.meta(0), Q ? 1.f : 16384.f);
+    GRP_ISSUE(BAR_G1, (mma_chain<DR / 16, NPF>(G.tmem_g + S0, w0, bb, id_f)));
   }
   for (int it = 0; it < ntiles; ++it) {
     const int t0 = tr.eb + it * TT;
     const int n_e = min(TT, tr.ee - t0);
-    TcMeta *M = G.meta(it);
+    const bool more = it + 1 < ntiles;
+    const TcMeta *M = G.meta(it);
     PHASE(1, it, 0);
-    // while G1 runs: grad_w[c][e] = gH * P[src][c] (flash.py:291) into the
-    // D3 stash + tile max
-    float mx = 0.f;
+    float gh[TT];  // grad_H[dst][ch] (flash.py:281)
 #pragma unroll
-    for (int c0 = 0; c0 < EPT; c0 += 16) {
-      float v[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        int e = ec + c0 + i;
-        float g = 0.f;
-        if (e < n_e)
-          g = __ldg(&GH[(size_t)M->nbr[e] * D + ch]) * __ldg(&P[(size_t)M->own[e] * D + ch]);
-        v[i] = g * q1;
-        mx = fmaxf(mx, fabsf(v[i]));
-      }
-      tc::tmem_st16(G.tl + D3 + ec + c0, v);
+    for (int i = 0; i < TT; ++i) {
+      const float g = __ldg(&GH[(size_t)M->nbr[i] * D + ch]);
+      gh[i] = i < n_e ? g : 0.f;
     }
-    tc::tmem_st_wait();
+    G.wait(BAR_G1, it);
     PHASE(1, it, 1);
-    const int sg = scale_exp(group_amax(mx, &M->amax[1], G.bar_id, GT));
+    tile_h<Q, !Q>(G, rs0, b0c, hs, n_e);
+    GRP_ISSUE(BAR_G2, (mma_chain<D / 16, NPF>(G.tmem_g + S1, w1, hb, id_f)));
     PHASE(1, it, 2);
-    G.wait(0);  // G1(it)
-    PHASE(1, it, 3);
-
-    // recompute h = ssp(z0) into D2; z0 stays in D0
-    mx = 0.f;
+    if (more && G.gt < 32)
+      load_meta(a, geo, env, G.meta(it + 1), t0 + TT, min(TT, tr.ee - t0 - TT), true, G.lane);
+    // P[src][ch]: src rows change a few times per tile (warp-uniform), so
+    // the row is reloaded only at a change
+    float pw[TT];
+    {
+      int orow = M->own[0];
+      float pc = __ldg(&P[(size_t)max(orow, 0) * D + ch]);
 #pragma unroll
-    for (int c0 = 0; c0 < EPT; c0 += 16) {
-      float v[16];
-      tc::tmem_ld16(G.tl + D0 + ec + c0, v);
-      tc::tmem_ld_wait();
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        float h = ssp_fast(v[i] * rs0 + b0c);
-        if (quant) h = __half2float(__float2half_rn(h));
-        v[i] = (ec + c0 + i) < n_e ? h : 0.f;
-        mx = fmaxf(mx, fabsf(v[i]));
+      for (int i = 0; i < TT; ++i) {
+        const int o = M->own[i];
+        if (o != orow && o >= 0) {
+          orow = o;
+          pc = __ldg(&P[(size_t)o * D + ch]);
+        }
+        pw[i] = pc;
       }
-      tc::tmem_st16(G.tl + D2 + ec + c0, v);
     }
-    tc::tmem_st_wait();
-    int sh_ = 0;
-    if (!quant) sh_ = scale_exp(group_amax(mx, &M->amax[0], G.bar_id, GT));
-    tmem_to_act(G.tl + D2, G, pow2f(sh_), !quant);
+    G.wait(BAR_G2, it);
+    PHASE(1, it, 3);
+    // grad_w = gH * P[src] (flash.py:291) -> B operand of G3 (W1^T)
+#pragma unroll
+    for (int j = 0; j < TT / 8; ++j) {
+      float v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = gh[8 * j + i] * pw[8 * j + i] * q1;
+      put8<true>(G.hb, D, ch, 8 * j, v, gws);
+    }
+    GRP_ISSUE(BAR_G3, (mma_chain<D / 16, NPB>(G.tmem_g + S2, w1t, hb, id_t)));
     PHASE(1, it, 4);
-    GRP_ISSUE(1, G.tmem_g + D1, sbase + SM_W1, W1_BYTES, D, false, G.shb, D, idesc_fwd, nprod_f);
-    PHASE(1, it, 5);
-    G.wait(1);  // G2
-    PHASE(1, it, 6);
-
-    // grad_w (stashed in D3) -> B operand of G3
-    tmem_to_act(G.tl + D3, G, pow2f(sg), true);
-    GRP_ISSUE(1, G.tmem_g + D2, sbase + SM_W1, W1_BYTES, D, true, G.shb, D, idesc_g3, nprod_b);
-    PHASE(1, it, 7);
     // while G3 runs: grad_P rows = src-segment sums of gH * w (flash.py:283-288)
     {
-      const float s1 = quant ? rs1 : pow2f(-(B.f1_exp + sh_));
+      float v[TT];
+      tc::tmem_ld32w(G.tl + S1, v);
 #pragma unroll
-      for (int c0 = 0; c0 < EPT; c0 += 16) {
-        float v[16], g[16];
-        tc::tmem_ld16(G.tl + D1 + ec + c0, v);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) g[i] = __ldg(&GH[(size_t)M->nbr[ec + c0 + i] * D + ch]);
-        tc::tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = g[i] * (v[i] * s1 + b1c);
-        tc::tmem_st16(G.tl + D1 + ec + c0, v);
-      }
-      tc::tmem_st_wait();
-      PHASE(1, it, 8);
-      reduce_tile(G.tl + D1, G, M, n_e, crow, cacc, GP);
+      for (int i = 0; i < TT; ++i) v[i] = gh[i] * (v[i] * s1 + b1c);
+      seg.tile(M->own, n_e, v, ch, GP);
     }
+    PHASE(1, it, 5);
+    // db -> basis buffer (G1 is done), G1': dz0 = W0 db into S1 (w consumed)
+    tile_basis<true, Q>(a, G, M, dbs);
+    GRP_ISSUE(BAR_G1P, (mma_chain<DR / 16, NPB>(G.tmem_g + S1, w0, bb, id_f)));
+    PHASE(1, it, 6);
+    G.wait(BAR_G3, it);
+    PHASE(1, it, 7);
+    // gz = grad_h * ssp'(z0) (mlp_backward_input, model.py:189-200), kept in
+    // S2.  fp32: ssp'(z) = sigmoid(z) = 1 - exp(-ssp(z))/2 from the stashed h;
+    // W16: from z0 itself (h was rounded to fp16).
+    {
+      float gz[TT], x[TT];
+      tc::tmem_ld32w(G.tl + S2, gz);
+      tc::tmem_ld32w(G.tl + (Q ? S0 : S3), x);
+#pragma unroll
+      for (int i = 0; i < TT; ++i) {
+        const float sig = Q ? sigmoid_fast(x[i] * rs0 + b0c) : fmaf(-0.5f, ex2_ftz(x[i] * -kLog2e), 1.f);
+        gz[i] = gz[i] * sg3 * sig;
+      }
+      tc::tmem_st32(G.tl + S2, gz);
+      tc::tmem_st_wait();
+    }
+    PHASE(1, it, 8);
+    G.wait(BAR_G1P, it);
     PHASE(1, it, 9);
-    G.wait(1);  // G3
+    if (more) {  // basis + G1 of the next tile overlap the grad_d reduction
+      tile_basis<false, Q>(a, G, G.meta(it + 1), Q ? 1.f : 16384.f);
+      GRP_ISSUE(BAR_G1, (mma_chain<DR / 16, NPF>(G.tmem_g + S0, w0, bb, id_f)));
+    }
     PHASE(1, it, 10);
-
-    // gz = grad_h * ssp'(z0) (mlp_backward_input, model.py:326-331), in place in D2
+    // grad_d[e] = sum_c gz[c][e] * dz0[c][e]: per-warp transpose-sum, then
+    // the four lane quarters in fixed order
     {
-      const float sg3 = pow2f(-(ew1 + sg));
-      mx = 0.f;
+      float p[TT], dz[TT];
+      tc::tmem_ld32w(G.tl + S2, p);
+      tc::tmem_ld32w(G.tl + S1, dz);
 #pragma unroll
-      for (int c0 = 0; c0 < EPT; c0 += 16) {
-        float gh[16], z[16];
-        tc::tmem_ld16(G.tl + D2 + ec + c0, gh);
-        tc::tmem_ld16(G.tl + D0 + ec + c0, z);
-        tc::tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          float z0 = z[i] * rs0 + b0c;
-          float g = (ec + c0 + i) < n_e ? gh[i] * sg3 * sigmoid_fast(z0) * q0 : 0.f;
-          gh[i] = g;
-          mx = fmaxf(mx, fabsf(g));
-        }
-        tc::tmem_st16(G.tl + D2 + ec + c0, gh);
-      }
-      tc::tmem_st_wait();
-      PHASE(1, it, 11);
-      sh_ = scale_exp(group_amax(mx, &M->amax[2], G.bar_id, GT));
-      tmem_to_act(G.tl + D2, G, pow2f(sh_), true);
-      GRP_ISSUE(1, G.tmem_g + D3, sbase + SM_W0, W0_BYTES, DR, true, G.shb, D, idesc_g4,
-                nprod_b);
-    }
-    PHASE(1, it, 12);
-    // overlap with G4(it): basis of the next tile and its G1 (D0 is free now)
-    if (it + 1 < ntiles) {
-      TcMeta *Mn = G.meta(it + 1);
-      const int n_n = min(TT, tr.ee - (t0 + TT));
-      tile_meta(a, geo, env, G, Mn, t0 + TT, n_n, true);
-      G.sync();
-      tile_basis_tc(a, G, Mn, n_n, quant);
-      GRP_ISSUE(0, G.tmem_g + D0, sbase + SM_W0, W0_BYTES, DR, false, G.sbb, DR, idesc_fwd,
-                nprod_f);
-    }
-    PHASE(1, it, 13);
-    G.wait(1);  // G4
-    PHASE(1, it, 14);
-
-    // grad_d[e] = sum_k grad_b[k][e] * db[k][e] (flash.py:293).  M=64 D lives
-    // in lanes 32q + (0..15) of each quarter: row k = 16q + lane.
-    {
-      const int k = 16 * G.quarter + (G.lane & 15);
-      const float mu = __ldg(&a.centers[k]);
-      const float s4 = pow2f(-(ew0 + sh_));
-      const float g2 = -2.f * a.gamma;
-#pragma unroll
-      for (int c0 = 0; c0 < EPT; c0 += 16) {
-        float gb[16];
-        tc::tmem_ld16(G.tl + D3 + ec + c0, gb);
-        tc::tmem_ld_wait();
-        if (G.lane < 16) {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            int e = ec + c0 + i;
-            float dl = M->d[e] - mu;
-            float gs = __expf((-a.gamma * dl) * dl);
-            float db = gs * (g2 * dl * M->env[e] + M->denv[e]);  // model.py:289
-            red_s[e * RED_LD + k] = gb[i] * s4 * db;
-          }
-        }
-      }
+      for (int i = 0; i < TT; ++i) p[i] *= dz[i] * sdz;
+      sh->xg[G.g][G.q][G.lane] = warp_edge_sum(p, G.lane);
     }
     G.sync();
-    PHASE(1, it, 15);
+    PHASE(1, it, 11);
     if (G.gt < TT && G.gt < n_e) {
       const int e = G.gt;
-      float gd = 0.f;
-#pragma unroll 8
-      for (int k = 0; k < DR; ++k) gd += red_s[e * RED_LD + k];
-      float d = M->d[e];
-      float inv = d > TINY_DISTANCE ? 1.f / d : 0.f;  // _safe_inv, flash.py:176-178
-      float s = gd * inv;
-      float4 u = M->u[e];
-      float4 g = make_float4(s * u.x, s * u.y, s * u.z, 0.f);
+      const float gd = ((sh->xg[G.g][0][e] + sh->xg[G.g][1][e]) + sh->xg[G.g][2][e]) +
+                       sh->xg[G.g][3][e];
+      const float d = M->d[e];
+      const float inv = d > TINY_DISTANCE ? 1.f / d : 0.f;  // _safe_inv, flash.py:176-178
+      const float s = gd * inv;
+      const float4 u = M->u[e];
+      float4 g = make_float4(s * u.x, s * u.y, s * u.z, 0.f);  // flash.py:294
       float4 *dst = &gsum[t0 + e];
       if (accumulate) {
-        float4 o = *dst;
+        const float4 o = *dst;
         g.x += o.x; g.y += o.y; g.z += o.z;
       }
       *dst = g;
     }
-    tc::fence_before_sync();
-    G.sync();
-    PHASE(1, it, 16);
   }
-  if (G.part == 0) finish_rows(crow, cacc, tr.rend, ch, GP);
+  seg.finish(ch, GP);
   tc::fence_before_sync();
   __syncthreads();
   if (threadIdx.x < 32) tc::tmem_dealloc<512>(sh->tmem);
@@ -753,10 +663,11 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
 void edge_tc_configure() {
   static bool done = false;
   if (done) return;
-  cudaFuncSetAttribute(k_edge_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)(SM_TOTAL + 1024));
-  cudaFuncSetAttribute(k_edge_bwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)(SM_TOTAL + 1024));
+  const int smem = (int)(SM_TOTAL + 1024);
+  cudaFuncSetAttribute(k_edge_fwd_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_edge_fwd_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_edge_bwd_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_edge_bwd_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   done = true;
 }
 
@@ -771,14 +682,21 @@ void launch_edge_geom(const EdgeArgs &a, float4 *geo, float2 *env, int32_t *unit
 void launch_edge_fwd_tc(const EdgeArgs &a, const float4 *geo, const float2 *env,
                         const int32_t *unit_rows, const float *P, float *H, int grid,
                         cudaStream_t s) {
-  k_edge_fwd_tc<<<grid, TC_THREADS, SM_TOTAL + 1024, s>>>(a, geo, env, unit_rows, P, H);
+  if (a.quant)
+    k_edge_fwd_tc<true><<<grid, TC_THREADS, SM_TOTAL + 1024, s>>>(a, geo, env, unit_rows, P, H);
+  else
+    k_edge_fwd_tc<false><<<grid, TC_THREADS, SM_TOTAL + 1024, s>>>(a, geo, env, unit_rows, P, H);
 }
 
 void launch_edge_bwd_tc(const EdgeArgs &a, const float4 *geo, const float2 *env,
                         const int32_t *unit_rows, const float *P, const float *GH, float *GP,
                         float4 *gsum, int accumulate, int grid, cudaStream_t s) {
-  k_edge_bwd_tc<<<grid, TC_THREADS, SM_TOTAL + 1024, s>>>(a, geo, env, unit_rows, P, GH, GP,
-                                                         gsum, accumulate);
+  if (a.quant)
+    k_edge_bwd_tc<true><<<grid, TC_THREADS, SM_TOTAL + 1024, s>>>(a, geo, env, unit_rows, P, GH,
+                                                                  GP, gsum, accumulate);
+  else
+    k_edge_bwd_tc<false><<<grid, TC_THREADS, SM_TOTAL + 1024, s>>>(a, geo, env, unit_rows, P, GH,
+                                                                   GP, gsum, accumulate);
 }
 
 }  // namespace fcg

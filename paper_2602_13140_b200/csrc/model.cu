@@ -604,6 +604,7 @@ struct EfBuffers {
   float4 *geo;
   float2 *env;
   int32_t *unit_rows;
+  unsigned int *amax;  // [2*T]: max |P_t|, max |GH_t| (edge-kernel operand bounds)
 };
 
 static EfBuffers carve_ef(Carver &c, int T, size_t RN, int64_t cap_e) {
@@ -622,6 +623,7 @@ static EfBuffers carve_ef(Carver &c, int T, size_t RN, int64_t cap_e) {
   b.geo = c.take<float4>((size_t)cap_e + 1);
   b.env = c.take<float2>((size_t)cap_e + 1);
   b.unit_rows = c.take<int32_t>(4096);
+  b.amax = c.take<unsigned int>(2 * FCG_MAX_BLOCKS);
   return b;
 }
 
@@ -688,6 +690,7 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
   ea.dbg = g_dbg_phase;
   const bool simt = use_simt_edges();
   const int eg = simt ? 2 * sm_count() : sm_count();
+  cudaMemsetAsync(b.amax, 0, sizeof(unsigned int) * 2 * FCG_MAX_BLOCKS, s);
   if (!simt) {
     edge_tc_configure();
     node_tc_configure();
@@ -698,13 +701,14 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
   for (int t = 0; t < T; ++t) {
     const fcg_block &blk = m->blocks[t];
     ea.blk = blk;
+    ea.amax_pg = b.amax + 2 * t;
     {
       FCG_PROF(P_NODE_PRE, s);
       if (simt)
         k_node_linear<true, false><<<node_grid, NT, sm1, s>>>(b.X, blk.pre_wt, blk.pre_b, b.P[t],
                                                              RN, quant);
       else
-        launch_node_pre_tc(b.X, blk, quant, b.P[t], RN, s);
+        launch_node_pre_tc(b.X, blk, quant, b.P[t], RN, b.amax + 2 * t, s);
     }
     {
       FCG_PROF(P_EDGE_FWD, s);
@@ -718,7 +722,7 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
       if (simt)
         k_node_post<<<node_grid, NT, sm2, s>>>(b.H, blk, b.Zp[t], b.X, RN, quant);
       else
-        launch_node_post_tc(b.H, blk, quant, b.Zp[t], b.X, RN, s);
+        launch_node_post_tc(b.H, blk, quant, b.Zp[t], b.X, RN, ptr, s);
     }
   }
   {
@@ -732,12 +736,13 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
   for (int t = T - 1; t >= 0; --t) {
     const fcg_block &blk = m->blocks[t];
     ea.blk = blk;
+    ea.amax_pg = b.amax + 2 * t;
     {
       FCG_PROF(P_NODE_POST_BWD, s);
       if (simt)
         k_node_post_bwd<<<node_grid, NT, sm2, s>>>(b.G, blk, b.Zp[t], b.GH, RN);
       else
-        launch_node_post_bwd_tc(b.G, blk, quant, b.Zp[t], b.GH, RN, s);
+        launch_node_post_bwd_tc(b.G, blk, quant, b.Zp[t], b.GH, RN, b.amax + 2 * t + 1, s);
     }
     {
       FCG_PROF(P_EDGE_BWD, s);
@@ -753,7 +758,7 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
       if (simt)
         k_node_linear<false, true><<<node_grid, NT, sm1, s>>>(b.GP, blk.pre_w, nullptr, b.G, RN, 0);
       else
-        launch_node_pre_bwd_tc(b.GP, blk, quant, b.G, RN, s);
+        launch_node_pre_bwd_tc(b.GP, blk, quant, b.G, RN, ptr, s);
     }
   }
   if (T == 0) cudaMemsetAsync(b.gsum, 0, sizeof(float4) * (size_t)(cap_e + 1), s);

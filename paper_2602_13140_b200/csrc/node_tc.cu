@@ -74,6 +74,18 @@ __device__ __forceinline__ NodeCtx node_prologue(uint8_t *sm, NodeMeta *meta) {
   return c;
 }
 
+// max |v| over the launch into a global slot (float bits of a non-negative
+// value as uint: order-independent, so deterministic).  The fused edge
+// kernels derive their operand scales from these maxima.
+__device__ __forceinline__ void global_amax(float v, unsigned int *slot, unsigned int *cta_slot) {
+  if (!slot) return;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(cta_slot, __float_as_uint(v));
+  __syncthreads();
+  if (threadIdx.x == 0 && *cta_slot) atomicMax(slot, *cta_slot);
+}
+
 __device__ __forceinline__ void node_epilogue_end(NodeMeta *meta, const NodeCtx &c) {
   tc::fence_before_sync();
   __syncthreads();
@@ -83,16 +95,21 @@ __device__ __forceinline__ void node_epilogue_end(NodeMeta *meta, const NodeCtx 
 // Rows [node0, node0+128) of a [nrows][128] fp32 matrix (times a per-channel
 // factor) -> MN-major B operand (row = channel).  Forward W16 operands are
 // fp16-rounded and unscaled; otherwise split hi/lo with a block-max scale.
-// Returns the scale exponent applied.
+// With a CSR row pointer, rows of nodes without edges read as zero: the
+// fused edge kernels write segment sums only for non-empty CSR rows (an
+// empty segment sums to zero, flash.py:109-135).  Returns the scale exponent.
 __device__ __forceinline__ int rows_to_act(const float *__restrict__ src, int node0, int nrows,
                                            const NodeCtx &c, float colscale, bool q16_only,
-                                           unsigned int *slot, uint8_t *act) {
+                                           unsigned int *slot, uint8_t *act,
+                                           const int32_t *__restrict__ csr_ptr = nullptr) {
   float v[NPT];
   float mx = 0.f;
 #pragma unroll
   for (int i = 0; i < NPT; ++i) {
     int n = node0 + c.ec + i;
-    float x = n < nrows ? __ldg(&src[(size_t)n * D + c.ch]) * colscale : 0.f;
+    const bool in = n < nrows;
+    float x = in ? __ldg(&src[(size_t)n * D + c.ch]) * colscale : 0.f;
+    if (csr_ptr && in && __ldg(&csr_ptr[n + 1]) == __ldg(&csr_ptr[n])) x = 0.f;
     if (q16_only) x = __half2float(__float2half_rn(x));
     v[i] = x;
     mx = fmaxf(mx, fabsf(x));
@@ -148,7 +165,8 @@ template <int kMode>
 __global__ void __launch_bounds__(NTH, 1)
 k_node_linear_tc(const float *__restrict__ X, const uint16_t *__restrict__ img, int wexp,
                  const float *__restrict__ bias, const float *__restrict__ rowscale, int quant,
-                 float *__restrict__ Y, int nrows) {
+                 float *__restrict__ Y, int nrows, unsigned int *__restrict__ amax_out,
+                 const int32_t *__restrict__ csr_ptr) {
   extern __shared__ __align__(1024) uint8_t sm[];
   NodeMeta *meta = (NodeMeta *)(sm + NSM_META);
   uint8_t *act = sm + NSM_ACT;
@@ -158,12 +176,13 @@ k_node_linear_tc(const float *__restrict__ X, const uint16_t *__restrict__ img, 
   const bool fwd = kMode == 0;
   // backward folds the W16 row scale of the K index (output channel) into X
   const float fold = (!fwd && quant) ? __ldg(&rowscale[c.ch]) : 1.f;
-  const int s = rows_to_act(X, node0, nrows, c, fold, fwd && quant, &meta->amax[0], act);
+  const int s = rows_to_act(X, node0, nrows, c, fold, fwd && quant, &meta->amax[0], act, csr_ptr);
   NODE_ISSUE(c.tm + NTM_D0, c.sbase + NSM_WA, IMG128, D, !fwd, c.sbase + NSM_ACT, D,
              tc::idesc_f16(128, NN, fwd ? 0 : 1, 1), quant ? (fwd ? 1 : 2) : 3);
   NODE_WAIT();
   const float un = pow2f(-((quant ? 0 : wexp) + s)) * ((fwd && quant) ? __ldg(&rowscale[c.ch]) : 1.f);
   const float b = fwd ? __ldg(&bias[c.ch]) : 0.f;
+  float mx = 0.f;
 #pragma unroll
   for (int c0 = 0; c0 < NPT; c0 += 16) {
     float v[16];
@@ -175,10 +194,13 @@ k_node_linear_tc(const float *__restrict__ X, const uint16_t *__restrict__ img, 
       if (n < nrows) {
         float *y = &Y[(size_t)n * D + c.ch];
         float r = v[i] * un + b;
-        *y = fwd ? r : *y + r;
+        r = fwd ? r : *y + r;
+        *y = r;
+        mx = fmaxf(mx, fabsf(r));
       }
     }
   }
+  global_amax(mx, amax_out, &meta->amax[3]);
   node_epilogue_end(meta, c);
 }
 
@@ -186,7 +208,8 @@ k_node_linear_tc(const float *__restrict__ X, const uint16_t *__restrict__ img, 
 // backward), U = ssp(Zp) Wp1^T + b1, X += U.
 __global__ void __launch_bounds__(NTH, 1)
 k_node_post_tc(const float *__restrict__ H, const fcg_block blk, int quant,
-               float *__restrict__ Zp, float *__restrict__ X, int nrows) {
+               float *__restrict__ Zp, float *__restrict__ X, int nrows,
+               const int32_t *__restrict__ csr_ptr) {
   extern __shared__ __align__(1024) uint8_t sm[];
   NodeMeta *meta = (NodeMeta *)(sm + NSM_META);
   uint8_t *act = sm + NSM_ACT;
@@ -196,7 +219,7 @@ k_node_post_tc(const float *__restrict__ H, const fcg_block blk, int quant,
   const int node0 = blockIdx.x * NN;
   const int np = quant ? 1 : 3;
   const uint32_t idesc = tc::idesc_f16(128, NN, 0, 1);
-  const int s0 = rows_to_act(H, node0, nrows, c, 1.f, quant, &meta->amax[0], act);
+  const int s0 = rows_to_act(H, node0, nrows, c, 1.f, quant, &meta->amax[0], act, csr_ptr);
   NODE_ISSUE(c.tm + NTM_D0, c.sbase + NSM_WA, IMG128, D, false, c.sbase + NSM_ACT, D, idesc, np);
   NODE_WAIT();
   const float un0 = quant ? __ldg(&blk.p0_s[c.ch]) : pow2f(-(blk.p0_exp + s0));
@@ -212,8 +235,7 @@ k_node_post_tc(const float *__restrict__ H, const fcg_block blk, int quant,
       int n = node0 + c.ec + c0 + i;
       float z = v[i] * un0 + b0;
       if (n < nrows) Zp[(size_t)n * D + c.ch] = z;
-      float a = ssp_fast(z);
-      if (quant) a = __half2float(__float2half_rn(a));
+      const float a = quant ? __half2float(__float2half_rn(ssp_ref(z))) : ssp_fast(z);
       v[i] = n < nrows ? a : 0.f;
       mx = fmaxf(mx, fabsf(v[i]));
     }
@@ -245,7 +267,8 @@ k_node_post_tc(const float *__restrict__ H, const fcg_block blk, int quant,
 // flash.py:264): GH = ((G Wp1) * ssp'(Zp)) Wp0, on dequantised weights.
 __global__ void __launch_bounds__(NTH, 1)
 k_node_post_bwd_tc(const float *__restrict__ G, const fcg_block blk, int quant,
-                   const float *__restrict__ Zp, float *__restrict__ GH, int nrows) {
+                   const float *__restrict__ Zp, float *__restrict__ GH, int nrows,
+                   unsigned int *__restrict__ amax_out) {
   extern __shared__ __align__(1024) uint8_t sm[];
   NodeMeta *meta = (NodeMeta *)(sm + NSM_META);
   uint8_t *act = sm + NSM_ACT;
@@ -282,6 +305,7 @@ k_node_post_bwd_tc(const float *__restrict__ G, const fcg_block blk, int quant,
   NODE_ISSUE(c.tm + NTM_D1, c.sbase + NSM_WB, IMG128, D, true, c.sbase + NSM_ACT, D, idesc, np);
   NODE_WAIT();
   const float un1 = pow2f(-((quant ? 0 : blk.p0_exp) + sz));
+  mx = 0.f;
 #pragma unroll
   for (int c0 = 0; c0 < NPT; c0 += 16) {
     float v[16];
@@ -290,9 +314,13 @@ k_node_post_bwd_tc(const float *__restrict__ G, const fcg_block blk, int quant,
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       int n = node0 + c.ec + c0 + i;
-      if (n < nrows) GH[(size_t)n * D + c.ch] = v[i] * un1;
+      if (n < nrows) {
+        GH[(size_t)n * D + c.ch] = v[i] * un1;
+        mx = fmaxf(mx, fabsf(v[i] * un1));
+      }
     }
   }
+  global_amax(mx, amax_out, &meta->amax[3]);
   node_epilogue_end(meta, c);
 }
 
@@ -332,8 +360,7 @@ k_readout_tc(const float *__restrict__ X, const fcg_model m, float *__restrict__
         int e = c.ec + c0 + i;
         bool ok = node0 + e < nrows;
         float z = v[i] * un + b0;
-        float a = ssp_fast(z);
-        if (quant) a = __half2float(__float2half_rn(a));
+        const float a = quant ? __half2float(__float2half_rn(ssp_ref(z))) : ssp_fast(z);
         red[e * 65 + k] = ok ? a * w1 : 0.f;
         v[i] = ok ? w1 * sigmoid_fast(z) * fold : 0.f;
         mx = fmaxf(mx, fabsf(v[i]));
@@ -385,22 +412,24 @@ void node_tc_configure() {
 static inline int node_grid(int nrows) { return (nrows + NN - 1) / NN; }
 
 void launch_node_pre_tc(const float *X, const fcg_block &b, int quant, float *P, int nrows,
-                        cudaStream_t s) {
+                        unsigned int *amax_p, cudaStream_t s) {
   k_node_linear_tc<0><<<node_grid(nrows), NTH, NSM_TOTAL + 1024, s>>>(
-      X, b.pre_img, b.pre_exp, b.pre_b, b.pre_s, quant, P, nrows);
+      X, b.pre_img, b.pre_exp, b.pre_b, b.pre_s, quant, P, nrows, amax_p, nullptr);
 }
 void launch_node_pre_bwd_tc(const float *GP, const fcg_block &b, int quant, float *G, int nrows,
-                            cudaStream_t s) {
+                            const int32_t *csr_ptr, cudaStream_t s) {
   k_node_linear_tc<1><<<node_grid(nrows), NTH, NSM_TOTAL + 1024, s>>>(
-      GP, b.pre_img, b.pre_exp, nullptr, b.pre_s, quant, G, nrows);
+      GP, b.pre_img, b.pre_exp, nullptr, b.pre_s, quant, G, nrows, nullptr, csr_ptr);
 }
 void launch_node_post_tc(const float *H, const fcg_block &b, int quant, float *Zp, float *X,
-                         int nrows, cudaStream_t s) {
-  k_node_post_tc<<<node_grid(nrows), NTH, NSM_TOTAL + 1024, s>>>(H, b, quant, Zp, X, nrows);
+                         int nrows, const int32_t *csr_ptr, cudaStream_t s) {
+  k_node_post_tc<<<node_grid(nrows), NTH, NSM_TOTAL + 1024, s>>>(H, b, quant, Zp, X, nrows,
+                                                                csr_ptr);
 }
 void launch_node_post_bwd_tc(const float *G, const fcg_block &b, int quant, const float *Zp,
-                             float *GH, int nrows, cudaStream_t s) {
-  k_node_post_bwd_tc<<<node_grid(nrows), NTH, NSM_TOTAL + 1024, s>>>(G, b, quant, Zp, GH, nrows);
+                             float *GH, int nrows, unsigned int *amax_gh, cudaStream_t s) {
+  k_node_post_bwd_tc<<<node_grid(nrows), NTH, NSM_TOTAL + 1024, s>>>(G, b, quant, Zp, GH, nrows,
+                                                                    amax_gh);
 }
 void launch_readout_tc(const float *X, const fcg_model &m, float *per_atom, float *G, int nrows,
                        cudaStream_t s) {

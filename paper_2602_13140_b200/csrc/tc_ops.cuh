@@ -109,13 +109,41 @@ __device__ __forceinline__ void issue_gemm(uint32_t d, uint32_t w_base, uint32_t
   }
 }
 
-// shifted softplus and its derivative with MUFU ex2/lg2/rcp (abs. error ~1e-7)
+// MUFU approximations with denormals flushed (the library is built without
+// -ftz, which would make __expf/__logf carry range fix-ups); used only by the
+// tensor-core epilogues, whose parity is tolerance-based.
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float lg2_ftz(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_ftz(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+// shifted softplus max(x,0) + log1p(exp(-|x|)) - ln2 (model.py:93-100) and
+// its derivative sigmoid(x) (model.py:103-107) on MUFU ex2/lg2/rcp (abs.
+// error ~1e-7)
 __device__ __forceinline__ float ssp_fast(float x) {
-  return fmaxf(x, 0.f) + __logf(1.f + __expf(-fabsf(x))) - 0.6931471805599453f;
+  return fmaf(kLn2, lg2_ftz(1.f + ex2_ftz(fabsf(x) * -kLog2e)) - 1.f, fmaxf(x, 0.f));
+}
+// ssp in the reference's fp32 op order with accurate expf/log1pf: the W16
+// path rounds every activation to fp16, which turns MUFU-level error into
+// rounding flips (quantize.py:68-71, :86).
+__device__ __forceinline__ float ssp_ref(float x) {
+  return fmaxf(x, 0.f) + log1pf(expf(-fabsf(x))) - 0.6931471805599453f;
 }
 __device__ __forceinline__ float sigmoid_fast(float x) {
-  return __fdividef(1.f, 1.f + __expf(-x));
+  return rcp_ftz(1.f + ex2_ftz(x * -kLog2e));
 }
-
 
 }  // namespace fcg

@@ -202,6 +202,28 @@ def tc_image(w: np.ndarray, quantized_f16: np.ndarray | None = None):
     return np.concatenate([core_matrix_image(hi), core_matrix_image(lo)]), e
 
 
+def _pow2_exp(bound: float) -> int:
+    """e with bound * 2^e in [2^14, 2^15): the fp16 hi/lo operand split of a
+    value |x| <= bound then never overflows and keeps ~22 bits (absolute
+    error <= bound * 2^-39 below that)."""
+    return 14 - int(np.floor(np.log2(bound))) if bound > 0 else 0
+
+
+def edge_h_exp(w0: np.ndarray, b0: np.ndarray) -> int:
+    """Static scale of h = ssp(W0 b + b0) in the edge kernels: the Gaussian
+    basis times the envelope lies in [0, 1] (model.py:123-133), so |z0[c]| <=
+    sum_k |W0[c,k]| + |b0[c]|, and -ln2 <= ssp(z) <= max(z, 0)."""
+    bz = float(np.max(np.sum(np.abs(w0.astype(np.float64)), axis=1) + np.abs(b0)))
+    return _pow2_exp(max(bz, math.log(2.0)) * 1.001)
+
+
+def edge_db_exp(gamma: float, cutoff: float) -> int:
+    """Static scale of the basis derivative db_k = g_k (-2 gamma delta_k C +
+    C') (model.py:136-157): |2 gamma delta exp(-gamma delta^2)| <=
+    sqrt(2 gamma / e), 0 <= C <= 1, |C'| <= pi / (2 r_cut)."""
+    return _pow2_exp((math.sqrt(2.0 * gamma / math.e) + math.pi / (2.0 * cutoff)) * 1.001)
+
+
 def _is_quantized(params) -> bool:
     return not isinstance(params.readout, tuple)
 
@@ -283,6 +305,10 @@ class DeviceModel:
                 img, e = image_of(lin, shape)
                 setattr(blk, f"{name}_img", _lib.u16ptr(dev(img.view(np.int16), torch.int16)))
                 setattr(blk, f"{name}_exp", e)
+            w0, b0 = dense(f0)
+            blk.f_hexp = edge_h_exp(w0, b0)
+            blk.f_dbexp = edge_db_exp(float(np.float32(params.rbf.gamma)), float(cfg.cutoff))
+            blk.f1_qmax = 1.0 if isinstance(f1, tuple) else float(np.max(f1.scale))
 
         r0, r1 = layers_of(params.readout)
         img, e = image_of(r0, (RH, D))

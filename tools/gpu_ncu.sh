@@ -9,7 +9,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --c
   --log-file gpurun_out/launches_${TAG}.csv $B > gpurun_out/ncu_launch_${TAG}.log 2>&1
 echo "launch list exit $?" >> gpurun_out/ncu_launch_${TAG}.log
 for K in $KERNS; do
-  timeout 1200 ncu --set full --clock-control none --import-source on -k "regex:^${K}\$" -s 3 -c 1 \
+  timeout 1200 ncu --set full --clock-control none --import-source on -k "regex:${K}" -s 3 -c 1 \
     -o gpurun_out/prof_${TAG}_${K} $B > gpurun_out/ncu_full_${TAG}_${K}.log 2>&1
   echo "full $K exit $?" >> gpurun_out/ncu_full_${TAG}_${K}.log
 done
