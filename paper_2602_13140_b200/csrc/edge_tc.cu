@@ -16,12 +16,19 @@
 // groups of 4 warps (one warp per TMEM lane quarter).  All groups read the
 // same resident weights; each owns a range of whole CSR rows (balanced by
 // edge count), walks it in 32-edge tiles, and has its own B-operand
-// buffers, 128 TMEM columns, mbarriers and named barrier, so the MMA and
-// gather latency of one group hides under the epilogues of the other three.
-// Inside a group every thread owns one channel across all 32 edges of a
-// tile, so the destination (forward) / source (backward) segment reduction
-// is a running sum per thread with a single store per CSR row — no atomics,
-// no cross-thread merge.
+// buffers, 128 TMEM columns and mbarriers, so the MMA and gather latency of
+// one group hides under the epilogues of the other three.  Inside a group
+// every thread owns one channel across all 32 edges of a tile, so the
+// destination (forward) / source (backward) segment reduction is a running
+// sum per thread with a single store per CSR row — no atomics, no
+// cross-thread merge.
+//
+// No barriers inside a group: every warp keeps a private copy of the tile
+// metadata, and when a warp has written its quarter of a GEMM's B operand it
+// bumps that GEMM kind's arrival counter; the LAST of the four warps to
+// arrive issues the tcgen05.mma chain and commits it to the kind's
+// mbarrier, on which each warp waits on its own.  Same-kind requests are
+// ordered by those completion waits, so a counter per kind (mod 4) suffices.
 //
 // fp32 parity (SURVEY §7 hard part 2): plain fp16/TF32 operands lose ~1e-3;
 // both operands are split as x*2^s = hi + lo (fp16 each, ~22 significant
@@ -50,7 +57,6 @@ constexpr int TT = 32;           // edges per tile (MMA N)
 constexpr int NGRP = 4;          // independent warp groups per CTA
 constexpr int GT = 128;          // threads per group: one warp per TMEM lane quarter
 constexpr int TC_THREADS = NGRP * GT;
-constexpr int NMETA = 3;         // tile metadata ring per group
 constexpr uint32_t KSTR = (TT / 8) * 128;  // B operand bytes per 8 K-rows
 constexpr uint32_t SM_W0 = 0;          // W0 hi|lo: 2 x 128x64 fp16
 constexpr uint32_t SM_W1 = 32768;      // W1 hi|lo: 2 x 128x128 fp16
@@ -64,15 +70,17 @@ constexpr uint32_t W0_BYTES = D * DR * 2, W1_BYTES = D * D * 2;
 constexpr uint32_t S0 = 0, S1 = 32, S2 = 64, S3 = 96;
 enum { BAR_G1 = 0, BAR_G2 = 1, BAR_G3 = 2, BAR_G1P = 3 };
 
-struct TcMeta {  // one tile
+constexpr int NWARP = TC_THREADS / 32;
+struct WarpMeta {  // one tile, private to a warp (double-buffered)
   int own[TT], nbr[TT];
   float d[TT], env[TT], denv[TT];
-  float4 u[TT];
 };
 struct TcShared {
-  TcMeta meta[NGRP][NMETA];
-  float xg[NGRP][4][TT];  // per-quarter partial grad_d
-  uint64_t bar[NGRP][4];
+  WarpMeta wm[NWARP][2];
+  float xg[NGRP][2][4][TT];   // per-quarter partial grad_d (double-buffered)
+  uint64_t bar[NGRP][4];      // GEMM completion, per kind
+  uint64_t xbar[NGRP];        // the four partial grad_d rows of a tile are written
+  unsigned int req[NGRP][4];  // operand arrivals per GEMM kind (mod 4)
   uint32_t tmem;
 };
 constexpr uint32_t SM_TOTAL = SM_META + sizeof(TcShared);
@@ -181,10 +189,11 @@ __device__ __forceinline__ Desc adesc(uint32_t base, int K) {
           2u * KSTR / 16u};
 }
 // D (+)= A x B over KS k-steps with the product set {hi*hi, hi*lo, lo*hi}
-// truncated to NP terms.  Issued by one thread, fully unrolled.
+// truncated to NP terms.  Issued by one lane; the k loop stays rolled to keep
+// the kernel's code (and i-cache footprint) small.
 template <int KS, int NP>
 __device__ __forceinline__ void mma_chain(uint32_t d, Desc a, Desc b, uint32_t idesc) {
-#pragma unroll
+#pragma unroll 1
   for (int k = 0; k < KS; ++k) {
     tc::mma_f16_ss(d, a.hi, b.hi, idesc, k > 0);
     if (NP >= 2) tc::mma_f16_ss(d, a.hi, b.lo, idesc, 1);
@@ -214,38 +223,63 @@ __device__ __forceinline__ void put8(uint8_t *act, int K, int r, int e0, const f
   if (LO) *(uint4 *)(act + (uint32_t)K * (KSTR >> 3) + off) = *(uint4 *)lo;
 }
 
-// ---- per-group context ---------------------------------------------------------
-struct Grp {
-  int g, gt, q, lane, ch, bar_id;
+// ---- per-warp context ----------------------------------------------------------
+struct Wctx {
+  int w, g, q, lane, ch;
   uint32_t tl;      // TMEM address of this warp's lane quarter at the group's columns
   uint32_t tmem_g;  // TMEM address of the group's columns, lane 0
   uint8_t *bb, *hb;
   uint32_t sbb, shb;
   TcShared *sh;
-  __device__ __forceinline__ void sync() const { named_sync(bar_id, GT); }
-  __device__ __forceinline__ TcMeta *meta(int it) const { return &sh->meta[g][it % NMETA]; }
+  __device__ __forceinline__ WarpMeta *meta(int it) const { return &sh->wm[w][it & 1]; }
   __device__ __forceinline__ void wait(int which, int it) const {
     tc::mbar_wait(&sh->bar[g][which], (uint32_t)(it & 1));
     tc::fence_after_sync();
   }
+  // This warp's part of a GEMM's operands is written (smem) and its TMEM
+  // reads of the columns the GEMM overwrites are done.  True on lane 0 of
+  // the last of the group's four warps to arrive: that lane issues.
+  __device__ __forceinline__ bool arrive(int kind) const {
+    tc::fence_async_smem();
+    tc::fence_before_sync();
+    __syncwarp();
+    bool last = false;
+    if (lane == 0) {
+      __threadfence_block();
+      last = (atomicAdd(&sh->req[g][kind], 1u) & 3u) == 3u;
+      if (last) {
+        __threadfence_block();
+        tc::fence_after_sync();
+      }
+    }
+    return last;
+  }
 };
 
-__device__ __forceinline__ Grp make_group(uint8_t *sm, TcShared *sh) {
-  Grp G;
-  G.g = threadIdx.x / GT;
-  G.gt = threadIdx.x % GT;
-  G.q = G.gt >> 5;
-  G.lane = threadIdx.x & 31;
-  G.ch = 32 * G.q + G.lane;
-  G.bar_id = 1 + G.g;
-  G.sh = sh;
-  G.bb = sm + SM_BUF + G.g * GBUF_BYTES;
-  G.hb = G.bb + BB_BYTES;
-  G.sbb = tc::smem_u32(G.bb);
-  G.shb = tc::smem_u32(G.hb);
-  G.tmem_g = sh->tmem + 128u * G.g;
-  G.tl = G.tmem_g + ((uint32_t)(32 * G.q) << 16);
-  return G;
+#define REQ(kind, CHAIN)                              \
+  do {                                                \
+    if (W.arrive(kind)) {                             \
+      CHAIN;                                          \
+      tc::mma_commit(&W.sh->bar[W.g][kind]);          \
+    }                                                 \
+    __syncwarp();                                     \
+  } while (0)
+
+__device__ __forceinline__ Wctx make_wctx(uint8_t *sm, TcShared *sh) {
+  Wctx W;
+  W.w = threadIdx.x >> 5;
+  W.g = W.w >> 2;
+  W.q = W.w & 3;
+  W.lane = threadIdx.x & 31;
+  W.ch = 32 * W.q + W.lane;
+  W.sh = sh;
+  W.bb = sm + SM_BUF + W.g * GBUF_BYTES;
+  W.hb = W.bb + BB_BYTES;
+  W.sbb = tc::smem_u32(W.bb);
+  W.shb = tc::smem_u32(W.hb);
+  W.tmem_g = sh->tmem + 128u * W.g;
+  W.tl = W.tmem_g + ((uint32_t)(32 * W.q) << 16);
+  return W;
 }
 
 __device__ __forceinline__ void kernel_prologue(uint8_t *sm, TcShared *sh, const fcg_block &b) {
@@ -253,9 +287,13 @@ __device__ __forceinline__ void kernel_prologue(uint8_t *sm, TcShared *sh, const
   uint4 *d0 = (uint4 *)(sm + SM_W0), *d1 = (uint4 *)(sm + SM_W1);
   for (int q = threadIdx.x; q < (int)(2 * W0_BYTES / 16); q += TC_THREADS) d0[q] = __ldg(s0 + q);
   for (int q = threadIdx.x; q < (int)(2 * W1_BYTES / 16); q += TC_THREADS) d1[q] = __ldg(s1 + q);
-  if (threadIdx.x % GT == 0) {
+  if (threadIdx.x < NGRP) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) tc::mbar_init(&sh->bar[threadIdx.x / GT][i], 1);
+    for (int i = 0; i < 4; ++i) {
+      tc::mbar_init(&sh->bar[threadIdx.x][i], 1);
+      sh->req[threadIdx.x][i] = 0u;
+    }
+    tc::mbar_init(&sh->xbar[threadIdx.x], 4);
     tc::fence_mbar_init();
   }
   if (threadIdx.x < 32) tc::tmem_alloc<512>(&sh->tmem);
@@ -265,11 +303,12 @@ __device__ __forceinline__ void kernel_prologue(uint8_t *sm, TcShared *sh, const
   tc::fence_after_sync();
 }
 
-// One lane per edge (warp 0 of the group): slot ids and cached geometry of
-// a tile.  Padding edges get own = -1, nbr = 0 and zero geometry.
-__device__ __forceinline__ void load_meta(const EdgeArgs &a, const float4 *__restrict__ geo,
-                                          const float2 *__restrict__ env, TcMeta *m, int t0,
-                                          int n_e, bool src_owned, int lane) {
+// One lane per edge: slot ids and cached geometry of a tile into the warp's
+// private metadata.  Padding edges get own = -1, nbr = 0 and zero geometry.
+// Returns the lane's (u, d) for the g_e epilogue.
+__device__ __forceinline__ float4 load_meta(const EdgeArgs &a, const float4 *__restrict__ geo,
+                                            const float2 *__restrict__ env, WarpMeta *m, int t0,
+                                            int n_e, bool src_owned, int lane) {
   int o = -1, n = 0;
   float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
   float2 c = make_float2(0.f, 0.f);
@@ -286,19 +325,21 @@ __device__ __forceinline__ void load_meta(const EdgeArgs &a, const float4 *__res
   m->d[lane] = g.w;
   m->env[lane] = c.x;
   m->denv[lane] = c.y;
-  m->u[lane] = make_float4(g.x, g.y, g.z, 0.f);
+  __syncwarp();
+  return g;
 }
 
 // Gaussian basis b[k][e] = exp((-g*dk)*dk) * C(d) (model.py:123-133) or, with
 // DERIV, its derivative db = exp(..) * (-2 g dk C + C') (model.py:148-157),
-// as the K=64 B operand.  Thread gt: k = gt%64, 16 edges.  The fp32 forward
-// basis is scaled 2^14 and split; the W16 forward basis is rounded to fp16
-// unscaled (quantize.py:68-71); db is always split (fp32 backward).  Padding
-// edges carry C = C' = 0, so their columns are zero without a mask.
+// as the K=64 B operand.  Each warp writes 16 of the 64 K-rows: thread
+// (q, lane) covers k = 16q + lane%16 for edges 16*(lane/16)..+15.  The fp32
+// forward basis is scaled 2^14 and split; the W16 forward basis is rounded
+// to fp16 unscaled (quantize.py:68-71); db is always split (fp32 backward).
+// Padding edges carry C = C' = 0, so their columns are zero without a mask.
 template <bool DERIV, bool Q>
-__device__ __forceinline__ void tile_basis(const EdgeArgs &a, const Grp &G, const TcMeta *m,
+__device__ __forceinline__ void tile_basis(const EdgeArgs &a, const Wctx &W, const WarpMeta *m,
                                            float scale) {
-  const int k = G.gt & (DR - 1), e0 = (G.gt / DR) * 16;
+  const int k = 16 * W.q + (W.lane & 15), e0 = (W.lane >> 4) * 16;
   const float mu = __ldg(&a.centers[k]);
   const float ngl = -a.gamma * kLog2e, g2 = -2.f * a.gamma;
   float v[16];
@@ -320,27 +361,26 @@ __device__ __forceinline__ void tile_basis(const EdgeArgs &a, const Grp &G, cons
     }
   }
   constexpr bool LO = DERIV || !Q;
-  put8<LO>(G.bb, DR, k, e0, &v[0], scale);
-  put8<LO>(G.bb, DR, k, e0 + 8, &v[8], scale);
+  put8<LO>(W.bb, DR, k, e0, &v[0], scale);
+  put8<LO>(W.bb, DR, k, e0 + 8, &v[8], scale);
 }
 
 // h = ssp(z0) for this thread's channel over the tile (z0 = TMEM S0 scaled),
-// as the K=128 B operand (act buffer); padding edges give 0.  With STASH the
-// fp32 h also goes to TMEM S3 (the backward derives ssp'(z0) from it).
+// as the K=128 B operand (act buffer).  Padding columns carry finite values
+// that no valid edge reads.  With STASH the fp32 h also goes to TMEM S3 (the
+// backward derives ssp'(z0) from it).
 template <bool Q, bool STASH>
-__device__ __forceinline__ void tile_h(const Grp &G, float rs0, float b0c, float hs, int n_e) {
+__device__ __forceinline__ void tile_h(const Wctx &W, float rs0, float b0c, float hs) {
   float v[TT];
-  tc::tmem_ld32w(G.tl + S0, v);
+  tc::tmem_ld32w(W.tl + S0, v);
 #pragma unroll
   for (int i = 0; i < TT; ++i) {
-    float h;
-    if (Q) h = __half2float(__float2half_rn(ssp_ref(v[i] * rs0 + b0c)));
-    else h = ssp_fast(v[i] * rs0 + b0c);
-    v[i] = i < n_e ? h : 0.f;
+    if (Q) v[i] = __half2float(__float2half_rn(ssp_ref(v[i] * rs0 + b0c)));
+    else v[i] = ssp_fast(v[i] * rs0 + b0c);
   }
-  if (STASH) tc::tmem_st32(G.tl + S3, v);
+  if (STASH) tc::tmem_st32(W.tl + S3, v);
 #pragma unroll
-  for (int j = 0; j < TT / 8; ++j) put8<!Q>(G.hb, D, G.ch, 8 * j, &v[8 * j], hs);
+  for (int j = 0; j < TT / 8; ++j) put8<!Q>(W.hb, D, W.ch, 8 * j, &v[8 * j], hs);
   if (STASH) tc::tmem_st_wait();
 }
 
@@ -360,24 +400,10 @@ __device__ __forceinline__ float warp_edge_sum(float (&p)[TT], int lane) {
   return p[0];
 }
 
-// all threads of the group: make the smem operand writes (and TMEM reads)
-// visible, then the group's first thread issues the chain and commits it
-#define GRP_ISSUE(which, CHAIN)                     \
-  do {                                              \
-    tc::fence_async_smem();                         \
-    tc::fence_before_sync();                        \
-    G.sync();                                       \
-    if (G.gt == 0) {                                \
-      tc::fence_after_sync();                       \
-      CHAIN;                                        \
-      tc::mma_commit(&G.sh->bar[G.g][which]);       \
-    }                                               \
-  } while (0)
-
-// phase timestamps for diagnosis: CTA 0, group 0, first 16 tiles
+// phase timestamps for diagnosis: CTA 0, warp 0, first 16 tiles
 #define PHASE(kind, it, ph)                                                          \
   do {                                                                             \
-    if (a.dbg && blockIdx.x == 0 && threadIdx.x == 0 && (it) < 16)                 \
+    if (a.dbg && blockIdx.x == 0 && threadIdx.x == 0 && (it) >= 0 && (it) < 16)    \
       a.dbg[((kind) * 16 + (it)) * 64 + (ph)] = clock64();                         \
   } while (0)
 
@@ -401,8 +427,9 @@ __device__ __forceinline__ UnitRange unit_range(const EdgeArgs &a, const int32_t
 // ---------------------------------------------------------------------------
 // Forward: per 32-edge tile of dst rows
 //   b -> [G1] z0 -> h = ssp(z0) -> [G2] w -> m = P[src]*w -> H rows.
-// While G2(i) runs the group builds the basis of tile i+1 and issues
-// G1(i+1); the gathers P[src] of tile i+1 are in flight during G1(i+1).
+// While G2(i) runs the warp builds its part of the basis of tile i+1 and
+// requests G1(i+1); the gathers P[src] of tile i+1 are in flight during
+// G1(i+1).  Iteration -1 only prepares tile 0.
 template <bool Q>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_edge_fwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__restrict__ env,
@@ -412,68 +439,60 @@ k_edge_fwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
   TcShared *sh = (TcShared *)(sm + SM_META);
   const fcg_block &B = a.blk;
   kernel_prologue(sm, sh, B);
-  const Grp G = make_group(sm, sh);
+  const Wctx W = make_wctx(sm, sh);
   const uint32_t sbase = tc::smem_u32(sm);
   const uint32_t idesc = tc::idesc_f16(128, TT, 0, 1);
   constexpr int NP = Q ? 1 : 3;
   const Desc w0 = wdesc_k(sbase + SM_W0, DR, W0_BYTES), w1 = wdesc_k(sbase + SM_W1, D, W1_BYTES);
-  const Desc bb = adesc(G.sbb, DR), hb = adesc(G.shb, D);
+  const Desc bb = adesc(W.sbb, DR), hb = adesc(W.shb, D);
 
-  const UnitRange tr = unit_range(a, unit_rows, NGRP * blockIdx.x + G.g);
+  const UnitRange tr = unit_range(a, unit_rows, NGRP * blockIdx.x + W.g);
   const int ntiles = (tr.ee - tr.eb + TT - 1) / TT;
   SegSum seg;
   seg.row = -1;
   seg.acc = 0.f;
 
-  const int ch = G.ch;
+  const int ch = W.ch;
   const float b0c = __ldg(&B.f0_b[ch]), b1c = __ldg(&B.f1_b[ch]);
   const float rs0 = Q ? __ldg(&B.f0_s[ch]) : pow2f(-(B.f0_exp + 14));
   const float hs = Q ? 1.f : pow2f(B.f_hexp);
   const float s1 = Q ? __ldg(&B.f1_s[ch]) : pow2f(-(B.f1_exp + B.f_hexp));
+  const float bsc = Q ? 1.f : 16384.f;
 
   float pv[TT];  // P[src][ch] of the current tile
-  if (ntiles > 0) {
-    const int n0 = min(TT, tr.ee - tr.eb);
-    if (G.gt < 32) load_meta(a, geo, env, G.meta(0), tr.eb, n0, false, G.lane);
-    G.sync();
-    tile_basis<false, Q>(a, G, G.meta(0), Q ? 1.f : 16384.f);
-    GRP_ISSUE(BAR_G1, (mma_chain<DR / 16, NP>(G.tmem_g + S0, w0, bb, idesc)));
-    const TcMeta *M0 = G.meta(0);
-#pragma unroll
-    for (int i = 0; i < TT; ++i) pv[i] = __ldg(&P[(size_t)M0->nbr[i] * D + ch]);
-  }
-  for (int it = 0; it < ntiles; ++it) {
+  for (int it = -1; it < ntiles; ++it) {
     const int t0 = tr.eb + it * TT;
-    const int n_e = min(TT, tr.ee - t0);
     const bool more = it + 1 < ntiles;
-    const TcMeta *M = G.meta(it);
+    const int n_n = min(TT, tr.ee - t0 - TT);
     PHASE(0, it, 0);
-    if (more && G.gt < 32)
-      load_meta(a, geo, env, G.meta(it + 1), t0 + TT, min(TT, tr.ee - t0 - TT), false, G.lane);
-    G.wait(BAR_G1, it);
-    PHASE(0, it, 1);
-    tile_h<Q, false>(G, rs0, b0c, hs, n_e);
-    PHASE(0, it, 2);
-    GRP_ISSUE(BAR_G2, (mma_chain<D / 16, NP>(G.tmem_g + S1, w1, hb, idesc)));
-    PHASE(0, it, 3);
-    if (more) {  // basis + G1 of the next tile overlap G2
-      tile_basis<false, Q>(a, G, G.meta(it + 1), Q ? 1.f : 16384.f);
-      GRP_ISSUE(BAR_G1, (mma_chain<DR / 16, NP>(G.tmem_g + S0, w0, bb, idesc)));
+    if (it < 0) {
+      load_meta(a, geo, env, W.meta(0), tr.eb, n_n, false, W.lane);
+    } else {
+      W.wait(BAR_G1, it);
+      PHASE(0, it, 1);
+      tile_h<Q, false>(W, rs0, b0c, hs);
+      REQ(BAR_G2, (mma_chain<D / 16, NP>(W.tmem_g + S1, w1, hb, idesc)));
+      PHASE(0, it, 2);
+      if (more) load_meta(a, geo, env, W.meta(it + 1), t0 + TT, n_n, false, W.lane);
     }
-    PHASE(0, it, 4);
-    G.wait(BAR_G2, it);
-    PHASE(0, it, 5);
-    // m = (W1 h + b1) * P[src] (flash.py:229), dst segment sums (flash.py:232-234)
-    {
+    if (more) {  // basis + G1 of the next tile overlap G2
+      tile_basis<false, Q>(a, W, W.meta(it + 1), bsc);
+      REQ(BAR_G1, (mma_chain<DR / 16, NP>(W.tmem_g + S0, w0, bb, idesc)));
+    }
+    PHASE(0, it, 3);
+    if (it >= 0) {
+      W.wait(BAR_G2, it);
+      PHASE(0, it, 4);
+      // m = (W1 h + b1) * P[src] (flash.py:229), dst segment sums (flash.py:232-234)
       float v[TT];
-      tc::tmem_ld32w(G.tl + S1, v);
+      tc::tmem_ld32w(W.tl + S1, v);
 #pragma unroll
       for (int i = 0; i < TT; ++i) v[i] = (v[i] * s1 + b1c) * pv[i];
-      seg.tile(M->own, n_e, v, ch, H);
+      seg.tile(W.meta(it)->own, min(TT, tr.ee - t0), v, ch, H);
+      PHASE(0, it, 5);
     }
-    PHASE(0, it, 6);
     if (more) {
-      const TcMeta *Mn = G.meta(it + 1);
+      const WarpMeta *Mn = W.meta(it + 1);
 #pragma unroll
       for (int i = 0; i < TT; ++i) pv[i] = __ldg(&P[(size_t)Mn->nbr[i] * D + ch]);
     }
@@ -503,156 +522,142 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
   TcShared *sh = (TcShared *)(sm + SM_META);
   const fcg_block &B = a.blk;
   kernel_prologue(sm, sh, B);
-  const Grp G = make_group(sm, sh);
+  const Wctx W = make_wctx(sm, sh);
   const uint32_t sbase = tc::smem_u32(sm);
   const uint32_t id_f = tc::idesc_f16(128, TT, 0, 1);
   const uint32_t id_t = tc::idesc_f16(128, TT, 1, 1);
   constexpr int NPF = Q ? 1 : 3, NPB = Q ? 2 : 3;
   const Desc w0 = wdesc_k(sbase + SM_W0, DR, W0_BYTES), w1 = wdesc_k(sbase + SM_W1, D, W1_BYTES);
   const Desc w1t = wdesc_mn(sbase + SM_W1, D, W1_BYTES);
-  const Desc bb = adesc(G.sbb, DR), hb = adesc(G.shb, D);
+  const Desc bb = adesc(W.sbb, DR), hb = adesc(W.shb, D);
 
-  const UnitRange tr = unit_range(a, unit_rows, NGRP * blockIdx.x + G.g);
+  const UnitRange tr = unit_range(a, unit_rows, NGRP * blockIdx.x + W.g);
   const int ntiles = (tr.ee - tr.eb + TT - 1) / TT;
   SegSum seg;
   seg.row = -1;
   seg.acc = 0.f;
 
-  const int ch = G.ch;
+  const int ch = W.ch;
   const float b0c = __ldg(&B.f0_b[ch]), b1c = __ldg(&B.f1_b[ch]);
   const float rs0 = Q ? __ldg(&B.f0_s[ch]) : pow2f(-(B.f0_exp + 14));
   const float hs = Q ? 1.f : pow2f(B.f_hexp);
   const float s1 = Q ? __ldg(&B.f1_s[ch]) : pow2f(-(B.f1_exp + B.f_hexp));
+  const float bsc = Q ? 1.f : 16384.f;
   // backward GEMMs against the stored fp16 weights fold the W16 dequant
   // scale of the contracted index into the operand: g @ (s*w16) == (g*s) @ w16
   const float q1 = Q ? __ldg(&B.f1_s[ch]) : 1.f;
   const float pmax = __uint_as_float(a.amax_pg[0]), ghmax = __uint_as_float(a.amax_pg[1]);
   const int sg = scale_exp(pmax * ghmax * B.f1_qmax);
-  const float gws = pow2f(sg);
+  const float gws = pow2f(sg) * q1;
   const float sg3 = pow2f(-((Q ? 0 : B.f1_exp) + sg));
   const float dbs = pow2f(B.f_dbexp);
   const float sdz = (Q ? __ldg(&B.f0_s[ch]) : pow2f(-B.f0_exp)) * pow2f(-B.f_dbexp);
 
-  if (ntiles > 0) {
-    const int n0 = min(TT, tr.ee - tr.eb);
-    if (G.gt < 32) load_meta(a, geo, env, G.meta(0), tr.eb, n0, true, G.lane);
-    G.sync();
-    tile_basis<false, Q>(a, G, G.meta(0), Q ? 1.f : 16384.f);
-    GRP_ISSUE(BAR_G1, (mma_chain<DR / 16, NPF>(G.tmem_g + S0, w0, bb, id_f)));
-  }
-  for (int it = 0; it < ntiles; ++it) {
+  float4 ue = make_float4(0.f, 0.f, 0.f, 0.f), ue_n = ue;  // this lane's edge: (u, d)
+  for (int it = -1; it < ntiles; ++it) {
     const int t0 = tr.eb + it * TT;
-    const int n_e = min(TT, tr.ee - t0);
     const bool more = it + 1 < ntiles;
-    const TcMeta *M = G.meta(it);
+    const int n_n = min(TT, tr.ee - t0 - TT);
     PHASE(1, it, 0);
-    float gh[TT];  // grad_H[dst][ch] (flash.py:281)
+    if (it < 0) {
+      ue_n = load_meta(a, geo, env, W.meta(0), tr.eb, n_n, true, W.lane);
+    } else {
+      const WarpMeta *M = W.meta(it);
+      float gh[TT];  // grad_H[dst][ch] (flash.py:281)
 #pragma unroll
-    for (int i = 0; i < TT; ++i) {
-      const float g = __ldg(&GH[(size_t)M->nbr[i] * D + ch]);
-      gh[i] = i < n_e ? g : 0.f;
-    }
-    G.wait(BAR_G1, it);
-    PHASE(1, it, 1);
-    tile_h<Q, !Q>(G, rs0, b0c, hs, n_e);
-    GRP_ISSUE(BAR_G2, (mma_chain<D / 16, NPF>(G.tmem_g + S1, w1, hb, id_f)));
-    PHASE(1, it, 2);
-    if (more && G.gt < 32)
-      load_meta(a, geo, env, G.meta(it + 1), t0 + TT, min(TT, tr.ee - t0 - TT), true, G.lane);
-    // P[src][ch]: src rows change a few times per tile (warp-uniform), so
-    // the row is reloaded only at a change
-    float pw[TT];
-    {
-      int orow = M->own[0];
-      float pc = __ldg(&P[(size_t)max(orow, 0) * D + ch]);
+      for (int i = 0; i < TT; ++i) gh[i] = __ldg(&GH[(size_t)M->nbr[i] * D + ch]);
+      W.wait(BAR_G1, it);
+      PHASE(1, it, 1);
+      tile_h<Q, !Q>(W, rs0, b0c, hs);
+      REQ(BAR_G2, (mma_chain<D / 16, NPF>(W.tmem_g + S1, w1, hb, id_f)));
+      PHASE(1, it, 2);
+      if (more) ue_n = load_meta(a, geo, env, W.meta(it + 1), t0 + TT, n_n, true, W.lane);
+      float pw[TT];  // P[src][ch]: src rows repeat inside a tile (L1 hits)
 #pragma unroll
-      for (int i = 0; i < TT; ++i) {
-        const int o = M->own[i];
-        if (o != orow && o >= 0) {
-          orow = o;
-          pc = __ldg(&P[(size_t)o * D + ch]);
+      for (int i = 0; i < TT; ++i) pw[i] = __ldg(&P[(size_t)max(M->own[i], 0) * D + ch]);
+      W.wait(BAR_G2, it);
+      PHASE(1, it, 3);
+      // grad_w = gH * P[src] (flash.py:291) -> B operand of G3 (W1^T)
+#pragma unroll
+      for (int j = 0; j < TT / 8; ++j) {
+        float v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = gh[8 * j + i] * pw[8 * j + i];
+        put8<true>(W.hb, D, ch, 8 * j, v, gws);
+      }
+      REQ(BAR_G3, (mma_chain<D / 16, NPB>(W.tmem_g + S2, w1t, hb, id_t)));
+      PHASE(1, it, 4);
+      // while G3 runs: grad_P rows = src-segment sums of gH * w (flash.py:283-288)
+      {
+        float v[TT];
+        tc::tmem_ld32w(W.tl + S1, v);
+#pragma unroll
+        for (int i = 0; i < TT; ++i) v[i] = gh[i] * (v[i] * s1 + b1c);
+        seg.tile(M->own, min(TT, tr.ee - t0), v, ch, GP);
+      }
+      PHASE(1, it, 5);
+      // db -> basis buffer (G1 is done), G1': dz0 = W0 db into S1 (w consumed)
+      tile_basis<true, Q>(a, W, M, dbs);
+      REQ(BAR_G1P, (mma_chain<DR / 16, NPB>(W.tmem_g + S1, w0, bb, id_f)));
+      PHASE(1, it, 6);
+      W.wait(BAR_G3, it);
+      // gz = grad_h * ssp'(z0) (mlp_backward_input, model.py:189-200), kept in
+      // S2.  fp32: ssp'(z) = sigmoid(z) = 1 - exp(-ssp(z))/2 from the stashed
+      // h; W16: from z0 itself (h was rounded to fp16).
+      {
+        float gz[TT], x[TT];
+        tc::tmem_ld32w(W.tl + S2, gz);
+        tc::tmem_ld32w(W.tl + (Q ? S0 : S3), x);
+#pragma unroll
+        for (int i = 0; i < TT; ++i) {
+          const float sig = Q ? sigmoid_fast(x[i] * rs0 + b0c) : fmaf(-0.5f, ex2_ftz(x[i] * -kLog2e), 1.f);
+          gz[i] = gz[i] * sg3 * sig;
         }
-        pw[i] = pc;
+        tc::tmem_st32(W.tl + S2, gz);
+        tc::tmem_st_wait();
       }
+      PHASE(1, it, 7);
+      W.wait(BAR_G1P, it);
+      PHASE(1, it, 8);
     }
-    G.wait(BAR_G2, it);
-    PHASE(1, it, 3);
-    // grad_w = gH * P[src] (flash.py:291) -> B operand of G3 (W1^T)
-#pragma unroll
-    for (int j = 0; j < TT / 8; ++j) {
-      float v[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = gh[8 * j + i] * pw[8 * j + i] * q1;
-      put8<true>(G.hb, D, ch, 8 * j, v, gws);
-    }
-    GRP_ISSUE(BAR_G3, (mma_chain<D / 16, NPB>(G.tmem_g + S2, w1t, hb, id_t)));
-    PHASE(1, it, 4);
-    // while G3 runs: grad_P rows = src-segment sums of gH * w (flash.py:283-288)
-    {
-      float v[TT];
-      tc::tmem_ld32w(G.tl + S1, v);
-#pragma unroll
-      for (int i = 0; i < TT; ++i) v[i] = gh[i] * (v[i] * s1 + b1c);
-      seg.tile(M->own, n_e, v, ch, GP);
-    }
-    PHASE(1, it, 5);
-    // db -> basis buffer (G1 is done), G1': dz0 = W0 db into S1 (w consumed)
-    tile_basis<true, Q>(a, G, M, dbs);
-    GRP_ISSUE(BAR_G1P, (mma_chain<DR / 16, NPB>(G.tmem_g + S1, w0, bb, id_f)));
-    PHASE(1, it, 6);
-    G.wait(BAR_G3, it);
-    PHASE(1, it, 7);
-    // gz = grad_h * ssp'(z0) (mlp_backward_input, model.py:189-200), kept in
-    // S2.  fp32: ssp'(z) = sigmoid(z) = 1 - exp(-ssp(z))/2 from the stashed h;
-    // W16: from z0 itself (h was rounded to fp16).
-    {
-      float gz[TT], x[TT];
-      tc::tmem_ld32w(G.tl + S2, gz);
-      tc::tmem_ld32w(G.tl + (Q ? S0 : S3), x);
-#pragma unroll
-      for (int i = 0; i < TT; ++i) {
-        const float sig = Q ? sigmoid_fast(x[i] * rs0 + b0c) : fmaf(-0.5f, ex2_ftz(x[i] * -kLog2e), 1.f);
-        gz[i] = gz[i] * sg3 * sig;
-      }
-      tc::tmem_st32(G.tl + S2, gz);
-      tc::tmem_st_wait();
-    }
-    PHASE(1, it, 8);
-    G.wait(BAR_G1P, it);
-    PHASE(1, it, 9);
     if (more) {  // basis + G1 of the next tile overlap the grad_d reduction
-      tile_basis<false, Q>(a, G, G.meta(it + 1), Q ? 1.f : 16384.f);
-      GRP_ISSUE(BAR_G1, (mma_chain<DR / 16, NPF>(G.tmem_g + S0, w0, bb, id_f)));
+      tile_basis<false, Q>(a, W, W.meta(it + 1), bsc);
+      REQ(BAR_G1, (mma_chain<DR / 16, NPF>(W.tmem_g + S0, w0, bb, id_f)));
     }
-    PHASE(1, it, 10);
-    // grad_d[e] = sum_c gz[c][e] * dz0[c][e]: per-warp transpose-sum, then
-    // the four lane quarters in fixed order
-    {
-      float p[TT], dz[TT];
-      tc::tmem_ld32w(G.tl + S2, p);
-      tc::tmem_ld32w(G.tl + S1, dz);
+    PHASE(1, it, 9);
+    if (it >= 0) {
+      // grad_d[e] = sum_c gz[c][e] * dz0[c][e]: per-warp transpose-sum, then
+      // the four lane quarters in fixed order (warp 0 of the group)
+      float *xg = &sh->xg[W.g][it & 1][0][0];
+      {
+        float p[TT], dz[TT];
+        tc::tmem_ld32w(W.tl + S2, p);
+        tc::tmem_ld32w(W.tl + S1, dz);
 #pragma unroll
-      for (int i = 0; i < TT; ++i) p[i] *= dz[i] * sdz;
-      sh->xg[G.g][G.q][G.lane] = warp_edge_sum(p, G.lane);
-    }
-    G.sync();
-    PHASE(1, it, 11);
-    if (G.gt < TT && G.gt < n_e) {
-      const int e = G.gt;
-      const float gd = ((sh->xg[G.g][0][e] + sh->xg[G.g][1][e]) + sh->xg[G.g][2][e]) +
-                       sh->xg[G.g][3][e];
-      const float d = M->d[e];
-      const float inv = d > TINY_DISTANCE ? 1.f / d : 0.f;  // _safe_inv, flash.py:176-178
-      const float s = gd * inv;
-      const float4 u = M->u[e];
-      float4 g = make_float4(s * u.x, s * u.y, s * u.z, 0.f);  // flash.py:294
-      float4 *dst = &gsum[t0 + e];
-      if (accumulate) {
-        const float4 o = *dst;
-        g.x += o.x; g.y += o.y; g.z += o.z;
+        for (int i = 0; i < TT; ++i) p[i] *= dz[i] * sdz;
+        xg[W.q * TT + W.lane] = warp_edge_sum(p, W.lane);
       }
-      *dst = g;
+      __syncwarp();
+      if (W.lane == 0) tc::mbar_arrive(&sh->xbar[W.g]);
+      if (W.q == 0) {
+        tc::mbar_wait(&sh->xbar[W.g], (uint32_t)(it & 1));
+        const int e = W.lane;
+        if (e < min(TT, tr.ee - t0)) {
+          const float gd = ((xg[e] + xg[TT + e]) + xg[2 * TT + e]) + xg[3 * TT + e];
+          const float inv = ue.w > TINY_DISTANCE ? 1.f / ue.w : 0.f;  // _safe_inv, flash.py:176-178
+          const float s = gd * inv;
+          float4 g = make_float4(s * ue.x, s * ue.y, s * ue.z, 0.f);  // flash.py:294
+          float4 *dst = &gsum[t0 + e];
+          if (accumulate) {
+            const float4 o = *dst;
+            g.x += o.x; g.y += o.y; g.z += o.z;
+          }
+          *dst = g;
+        }
+      }
+      PHASE(1, it, 10);
     }
+    ue = ue_n;
   }
   seg.finish(ch, GP);
   tc::fence_before_sync();

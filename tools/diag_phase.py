@@ -21,7 +21,7 @@ eng.evaluate()
 torch.cuda.synchronize()
 lib.fcg_debug_phase_buffer(None)
 b = buf.cpu().numpy().reshape(2, 16, 64)
-for kind, name, nph in ((0, "fwd", 7), (1, "bwd", 12)):
+for kind, name, nph in ((0, "fwd", 6), (1, "bwd", 11)):
     t = b[kind, :, :nph].astype(np.int64)
     ok = t[:, 0] > 0
     t = t[ok]
