@@ -237,20 +237,21 @@ struct Wctx {
     tc::fence_after_sync();
   }
   // This warp's part of a GEMM's operands is written (smem) and its TMEM
-  // reads of the columns the GEMM overwrites are done.  True on lane 0 of
-  // the last of the group's four warps to arrive: that lane issues.
+  // reads of the columns the GEMM overwrites are done.  True (warp-uniform)
+  // for the last of the group's four warps to arrive: its lane 0 issues.
   __device__ __forceinline__ bool arrive(int kind) const {
     tc::fence_async_smem();
     tc::fence_before_sync();
     __syncwarp();
-    bool last = false;
+    unsigned int old = 0u;
     if (lane == 0) {
       __threadfence_block();
-      last = (atomicAdd(&sh->req[g][kind], 1u) & 3u) == 3u;
-      if (last) {
-        __threadfence_block();
-        tc::fence_after_sync();
-      }
+      old = atomicAdd(&sh->req[g][kind], 1u);
+    }
+    const bool last = (__shfl_sync(0xffffffffu, old, 0) & 3u) == 3u;  // warp-uniform
+    if (last) {
+      __threadfence_block();
+      tc::fence_after_sync();
     }
     return last;
   }
@@ -258,7 +259,7 @@ struct Wctx {
 
 #define REQ(kind, CHAIN)                              \
   do {                                                \
-    if (W.arrive(kind)) {                             \
+    if (W.arrive(kind) && W.lane == 0) {              \
       CHAIN;                                          \
       tc::mma_commit(&W.sh->bar[W.g][kind]);          \
     }                                                 \
@@ -267,7 +268,10 @@ struct Wctx {
 
 __device__ __forceinline__ Wctx make_wctx(uint8_t *sm, TcShared *sh) {
   Wctx W;
-  W.w = threadIdx.x >> 5;
+  // warp index through a shuffle: the compiler then knows it (and every
+  // address derived from it) is warp-uniform, so MMA descriptors stay in
+  // uniform registers instead of an R2UR waterfall per tcgen05.mma
+  W.w = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   W.g = W.w >> 2;
   W.q = W.w & 3;
   W.lane = threadIdx.x & 31;
