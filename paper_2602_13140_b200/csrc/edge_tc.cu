@@ -309,10 +309,11 @@ __device__ __forceinline__ void kernel_prologue(uint8_t *sm, TcShared *sh, const
 
 // One lane per edge: slot ids and cached geometry of a tile into the warp's
 // private metadata.  Padding edges get own = -1, nbr = 0 and zero geometry.
-// Returns the lane's (u, d) for the g_e epilogue.
+// Returns the lane's (u, d) for the g_e epilogue; `rows2` tells whether the
+// tile's edges fall in at most two CSR rows (its first and last).
 __device__ __forceinline__ float4 load_meta(const EdgeArgs &a, const float4 *__restrict__ geo,
                                             const float2 *__restrict__ env, WarpMeta *m, int t0,
-                                            int n_e, bool src_owned, int lane) {
+                                            int n_e, bool src_owned, int lane, bool &rows2) {
   int o = -1, n = 0;
   float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
   float2 c = make_float2(0.f, 0.f);
@@ -329,6 +330,8 @@ __device__ __forceinline__ float4 load_meta(const EdgeArgs &a, const float4 *__r
   m->d[lane] = g.w;
   m->env[lane] = c.x;
   m->denv[lane] = c.y;
+  const int first = __shfl_sync(0xffffffffu, o, 0), last = __shfl_sync(0xffffffffu, o, max(n_e - 1, 0));
+  rows2 = __all_sync(0xffffffffu, lane >= n_e || o == first || o == last);
   __syncwarp();
   return g;
 }
@@ -470,14 +473,16 @@ k_edge_fwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
     const int n_n = min(TT, tr.ee - t0 - TT);
     PHASE(0, it, 0);
     if (it < 0) {
-      load_meta(a, geo, env, W.meta(0), tr.eb, n_n, false, W.lane);
+      bool r2;
+      load_meta(a, geo, env, W.meta(0), tr.eb, n_n, false, W.lane, r2);
     } else {
       W.wait(BAR_G1, it);
       PHASE(0, it, 1);
       tile_h<Q, false>(W, rs0, b0c, hs);
       REQ(BAR_G2, (mma_chain<D / 16, NP>(W.tmem_g + S1, w1, hb, idesc)));
       PHASE(0, it, 2);
-      if (more) load_meta(a, geo, env, W.meta(it + 1), t0 + TT, n_n, false, W.lane);
+      bool r2;
+      if (more) load_meta(a, geo, env, W.meta(it + 1), t0 + TT, n_n, false, W.lane, r2);
     }
     if (more) {  // basis + G1 of the next tile overlap G2
       tile_basis<false, Q>(a, W, W.meta(it + 1), bsc);
@@ -558,35 +563,45 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
   const float sdz = (Q ? __ldg(&B.f0_s[ch]) : pow2f(-B.f0_exp)) * pow2f(-B.f_dbexp);
 
   float4 ue = make_float4(0.f, 0.f, 0.f, 0.f), ue_n = ue;  // this lane's edge: (u, d)
+  bool rows2 = true, rows2_n = true;
   for (int it = -1; it < ntiles; ++it) {
     const int t0 = tr.eb + it * TT;
     const bool more = it + 1 < ntiles;
     const int n_n = min(TT, tr.ee - t0 - TT);
     PHASE(1, it, 0);
     if (it < 0) {
-      ue_n = load_meta(a, geo, env, W.meta(0), tr.eb, n_n, true, W.lane);
+      ue_n = load_meta(a, geo, env, W.meta(0), tr.eb, n_n, true, W.lane, rows2_n);
     } else {
       const WarpMeta *M = W.meta(it);
+      const int n_e = min(TT, tr.ee - t0);
       float gh[TT];  // grad_H[dst][ch] (flash.py:281)
 #pragma unroll
       for (int i = 0; i < TT; ++i) gh[i] = __ldg(&GH[(size_t)M->nbr[i] * D + ch]);
+      // P[src][ch] (flash.py:291): src = the tile's CSR rows, usually its
+      // first and last only
+      const int o_f = M->own[0], o_l = M->own[n_e - 1];
+      const float p_f = __ldg(&P[(size_t)o_f * D + ch]), p_l = __ldg(&P[(size_t)o_l * D + ch]);
       W.wait(BAR_G1, it);
       PHASE(1, it, 1);
       tile_h<Q, !Q>(W, rs0, b0c, hs);
       REQ(BAR_G2, (mma_chain<D / 16, NPF>(W.tmem_g + S1, w1, hb, id_f)));
       PHASE(1, it, 2);
-      if (more) ue_n = load_meta(a, geo, env, W.meta(it + 1), t0 + TT, n_n, true, W.lane);
-      float pw[TT];  // P[src][ch]: src rows repeat inside a tile (L1 hits)
-#pragma unroll
-      for (int i = 0; i < TT; ++i) pw[i] = __ldg(&P[(size_t)max(M->own[i], 0) * D + ch]);
+      if (more) ue_n = load_meta(a, geo, env, W.meta(it + 1), t0 + TT, n_n, true, W.lane, rows2_n);
       W.wait(BAR_G2, it);
       PHASE(1, it, 3);
       // grad_w = gH * P[src] (flash.py:291) -> B operand of G3 (W1^T)
 #pragma unroll
       for (int j = 0; j < TT / 8; ++j) {
+        const int4 oa = *(const int4 *)&M->own[8 * j], ob = *(const int4 *)&M->own[8 * j + 4];
+        const int oo[8] = {oa.x, oa.y, oa.z, oa.w, ob.x, ob.y, ob.z, ob.w};
         float v[8];
+        if (rows2) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = gh[8 * j + i] * pw[8 * j + i];
+          for (int i = 0; i < 8; ++i) v[i] = gh[8 * j + i] * (oo[i] == o_l ? p_l : p_f);
+        } else {  // a tile spanning 3+ rows: per-edge loads
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[i] = gh[8 * j + i] * __ldg(&P[(size_t)max(oo[i], 0) * D + ch]);
+        }
         put8<true>(W.hb, D, ch, 8 * j, v, gws);
       }
       REQ(BAR_G3, (mma_chain<D / 16, NPB>(W.tmem_g + S2, w1t, hb, id_t)));
@@ -662,6 +677,7 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
       PHASE(1, it, 10);
     }
     ue = ue_n;
+    rows2 = rows2_n;
   }
   seg.finish(ch, GP);
   tc::fence_before_sync();
