@@ -93,10 +93,12 @@ static_assert(SM_TOTAL + 1024 <= 232448, "shared memory budget");
 // reads them as zero through the CSR degree (an empty segment sums to 0,
 // flash.py:109-135), so the walk needs no zero-fill branches.
 struct SegSum {
-  int row;  // row of the open segment (-1 before the unit's first edge)
+  int row;       // row of the open segment (-1: the unit has no edges)
   float acc;
-  __device__ __forceinline__ void tile(const int *own, int n, const float (&m)[TT], int c,
-                                       float *__restrict__ out) {
+  float *outc;   // out + channel
+  // Tile of TT edges in CSR order with rows own[] (padding edges repeat the
+  // last valid row and carry m = 0).
+  __device__ __forceinline__ void tile(const int *own, const float (&m)[TT]) {
 #pragma unroll
     for (int h = 0; h < TT; h += 16) {
       int o[16];
@@ -105,9 +107,9 @@ struct SegSum {
         const int4 q = *(const int4 *)&own[h + 4 * j];
         o[4 * j] = q.x; o[4 * j + 1] = q.y; o[4 * j + 2] = q.z; o[4 * j + 3] = q.w;
       }
-      if (h + 16 <= n && o[0] == o[15]) {  // one row for all 16 edges
+      if (o[0] == o[15]) {  // one row for all 16 edges
         if (o[0] != row) {
-          if (row >= 0) out[(size_t)row * D + c] = acc;
+          outc[(size_t)row * D] = acc;
           row = o[0];
           acc = 0.f;
         }
@@ -120,17 +122,16 @@ struct SegSum {
       } else {
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const bool valid = h + i < n;
-          const bool nr = valid && o[i] != row;
-          if (nr && row >= 0) out[(size_t)row * D + c] = acc;
-          acc = nr ? m[h + i] : (valid ? acc + m[h + i] : acc);
-          row = nr ? o[i] : row;
+          const bool nr = o[i] != row;
+          if (nr) outc[(size_t)row * D] = acc;
+          acc = (nr ? 0.f : acc) + m[h + i];
+          row = o[i];
         }
       }
     }
   }
-  __device__ __forceinline__ void finish(int c, float *__restrict__ out) {
-    if (row >= 0) out[(size_t)row * D + c] = acc;
+  __device__ __forceinline__ void finish() {
+    if (row >= 0) outc[(size_t)row * D] = acc;
   }
 };
 
@@ -308,7 +309,8 @@ __device__ __forceinline__ void kernel_prologue(uint8_t *sm, TcShared *sh, const
 }
 
 // One lane per edge: slot ids and cached geometry of a tile into the warp's
-// private metadata.  Padding edges get own = -1, nbr = 0 and zero geometry.
+// private metadata.  Padding edges get nbr = 0, zero geometry and the last
+// valid edge's row.
 // Returns the lane's (u, d) for the g_e epilogue; `rows2` tells whether the
 // tile's edges fall in at most two CSR rows (its first and last).
 __device__ __forceinline__ float4 load_meta(const EdgeArgs &a, const float4 *__restrict__ geo,
@@ -325,13 +327,13 @@ __device__ __forceinline__ float4 load_meta(const EdgeArgs &a, const float4 *__r
   }
   // backward edge (dst=nbr, src=own): u = r_nbr - r_own (flash.py:279)
   if (src_owned) { g.x = -g.x; g.y = -g.y; g.z = -g.z; }
-  m->own[lane] = o;
+  const int first = __shfl_sync(0xffffffffu, o, 0), last = __shfl_sync(0xffffffffu, o, max(n_e - 1, 0));
+  rows2 = __all_sync(0xffffffffu, lane >= n_e || o == first || o == last);
+  m->own[lane] = lane < n_e ? o : last;  // padding edges extend the last row (with m = 0)
   m->nbr[lane] = n;
   m->d[lane] = g.w;
   m->env[lane] = c.x;
   m->denv[lane] = c.y;
-  const int first = __shfl_sync(0xffffffffu, o, 0), last = __shfl_sync(0xffffffffu, o, max(n_e - 1, 0));
-  rows2 = __all_sync(0xffffffffu, lane >= n_e || o == first || o == last);
   __syncwarp();
   return g;
 }
@@ -455,11 +457,12 @@ k_edge_fwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
 
   const UnitRange tr = unit_range(a, unit_rows, NGRP * blockIdx.x + W.g);
   const int ntiles = (tr.ee - tr.eb + TT - 1) / TT;
-  SegSum seg;
-  seg.row = -1;
-  seg.acc = 0.f;
-
   const int ch = W.ch;
+  SegSum seg;
+  seg.row = ntiles > 0 ? a.own[tr.eb] : -1;
+  seg.acc = 0.f;
+  seg.outc = H + ch;
+
   const float b0c = __ldg(&B.f0_b[ch]), b1c = __ldg(&B.f1_b[ch]);
   const float rs0 = Q ? __ldg(&B.f0_s[ch]) : pow2f(-(B.f0_exp + 14));
   const float hs = Q ? 1.f : pow2f(B.f_hexp);
@@ -497,7 +500,11 @@ k_edge_fwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
       tc::tmem_ld32w(W.tl + S1, v);
 #pragma unroll
       for (int i = 0; i < TT; ++i) v[i] = (v[i] * s1 + b1c) * pv[i];
-      seg.tile(W.meta(it)->own, min(TT, tr.ee - t0), v, ch, H);
+      if (tr.ee - t0 < TT) {
+#pragma unroll
+        for (int i = 0; i < TT; ++i) v[i] = i < tr.ee - t0 ? v[i] : 0.f;
+      }
+      seg.tile(W.meta(it)->own, v);
       PHASE(0, it, 5);
     }
     if (more) {
@@ -506,7 +513,7 @@ k_edge_fwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
       for (int i = 0; i < TT; ++i) pv[i] = __ldg(&P[(size_t)Mn->nbr[i] * D + ch]);
     }
   }
-  seg.finish(ch, H);
+  seg.finish();
   tc::fence_before_sync();
   __syncthreads();
   if (threadIdx.x < 32) tc::tmem_dealloc<512>(sh->tmem);
@@ -542,11 +549,12 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
 
   const UnitRange tr = unit_range(a, unit_rows, NGRP * blockIdx.x + W.g);
   const int ntiles = (tr.ee - tr.eb + TT - 1) / TT;
-  SegSum seg;
-  seg.row = -1;
-  seg.acc = 0.f;
-
   const int ch = W.ch;
+  SegSum seg;
+  seg.row = ntiles > 0 ? a.own[tr.eb] : -1;
+  seg.acc = 0.f;
+  seg.outc = GP + ch;
+
   const float b0c = __ldg(&B.f0_b[ch]), b1c = __ldg(&B.f1_b[ch]);
   const float rs0 = Q ? __ldg(&B.f0_s[ch]) : pow2f(-(B.f0_exp + 14));
   const float hs = Q ? 1.f : pow2f(B.f_hexp);
@@ -612,7 +620,11 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
         tc::tmem_ld32w(W.tl + S1, v);
 #pragma unroll
         for (int i = 0; i < TT; ++i) v[i] = gh[i] * (v[i] * s1 + b1c);
-        seg.tile(M->own, min(TT, tr.ee - t0), v, ch, GP);
+        if (n_e < TT) {
+#pragma unroll
+          for (int i = 0; i < TT; ++i) v[i] = i < n_e ? v[i] : 0.f;
+        }
+        seg.tile(M->own, v);
       }
       PHASE(1, it, 5);
       // db -> basis buffer (G1 is done), G1': dz0 = W0 db into S1 (w consumed)
@@ -679,7 +691,7 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
     ue = ue_n;
     rows2 = rows2_n;
   }
-  seg.finish(ch, GP);
+  seg.finish();
   tc::fence_before_sync();
   __syncthreads();
   if (threadIdx.x < 32) tc::tmem_dealloc<512>(sh->tmem);
