@@ -196,9 +196,9 @@ template <int KS, int NP>
 __device__ __forceinline__ void mma_chain(uint32_t d, Desc a, Desc b, uint32_t idesc) {
 #pragma unroll 1
   for (int k = 0; k < KS; ++k) {
-    tc::mma_f16_ss(d, a.hi, b.hi, idesc, k > 0);
-    if (NP >= 2) tc::mma_f16_ss(d, a.hi, b.lo, idesc, 1);
-    if (NP >= 3) tc::mma_f16_ss(d, a.lo, b.hi, idesc, 1);
+    tc::mma_f16_ss_warp(d, a.hi, b.hi, idesc, k > 0);
+    if (NP >= 2) tc::mma_f16_ss_warp(d, a.hi, b.lo, idesc, 1);
+    if (NP >= 3) tc::mma_f16_ss_warp(d, a.lo, b.hi, idesc, 1);
     a.hi += a.step; a.lo += a.step;
     b.hi += b.step; b.lo += b.step;
   }
@@ -239,7 +239,8 @@ struct Wctx {
   }
   // This warp's part of a GEMM's operands is written (smem) and its TMEM
   // reads of the columns the GEMM overwrites are done.  True (warp-uniform)
-  // for the last of the group's four warps to arrive: its lane 0 issues.
+  // for the last of the group's four warps to arrive: that warp issues (one
+  // elected lane per instruction).
   __device__ __forceinline__ bool arrive(int kind) const {
     tc::fence_async_smem();
     tc::fence_before_sync();
@@ -260,9 +261,9 @@ struct Wctx {
 
 #define REQ(kind, CHAIN)                              \
   do {                                                \
-    if (W.arrive(kind) && W.lane == 0) {              \
+    if (W.arrive(kind)) {                             \
       CHAIN;                                          \
-      tc::mma_commit(&W.sh->bar[W.g][kind]);          \
+      tc::mma_commit_warp(&W.sh->bar[W.g][kind]);     \
     }                                                 \
     __syncwarp();                                     \
   } while (0)
