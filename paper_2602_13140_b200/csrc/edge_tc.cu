@@ -309,35 +309,45 @@ __device__ __forceinline__ void kernel_prologue(uint8_t *sm, TcShared *sh, const
   tc::fence_after_sync();
 }
 
-// One lane per edge: slot ids and cached geometry of a tile into the warp's
-// private metadata.  Padding edges get nbr = 0, zero geometry and the last
-// valid edge's row.
-// Returns the lane's (u, d) for the g_e epilogue; `rows2` tells whether the
-// tile's edges fall in at most two CSR rows (its first and last).
-__device__ __forceinline__ float4 load_meta(const EdgeArgs &a, const float4 *__restrict__ geo,
-                                            const float2 *__restrict__ env, WarpMeta *m, int t0,
-                                            int n_e, bool src_owned, int lane, bool &rows2) {
-  int o = -1, n = 0;
-  float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
-  float2 c = make_float2(0.f, 0.f);
-  if (lane < n_e) {
-    o = a.own[t0 + lane];
-    n = a.nbr[t0 + lane];
-    g = geo[t0 + lane];
-    c = env[t0 + lane];
+// Raw per-edge metadata of one tile, one lane per edge, held in registers a
+// tile ahead of use so the global-load latency stays off the critical path.
+struct MetaRegs {
+  int o, n, n_e;
+  float4 g;
+  float2 c;
+  __device__ __forceinline__ void load(const EdgeArgs &a, const float4 *__restrict__ geo,
+                                       const float2 *__restrict__ env, int t0, int count,
+                                       int lane) {
+    n_e = count;
+    o = -1; n = 0;
+    g = make_float4(0.f, 0.f, 0.f, 0.f);
+    c = make_float2(0.f, 0.f);
+    if (lane < count) {
+      o = a.own[t0 + lane];
+      n = a.nbr[t0 + lane];
+      g = geo[t0 + lane];
+      c = env[t0 + lane];
+    }
   }
-  // backward edge (dst=nbr, src=own): u = r_nbr - r_own (flash.py:279)
-  if (src_owned) { g.x = -g.x; g.y = -g.y; g.z = -g.z; }
-  const int first = __shfl_sync(0xffffffffu, o, 0), last = __shfl_sync(0xffffffffu, o, max(n_e - 1, 0));
-  rows2 = __all_sync(0xffffffffu, lane >= n_e || o == first || o == last);
-  m->own[lane] = lane < n_e ? o : last;  // padding edges extend the last row (with m = 0)
-  m->nbr[lane] = n;
-  m->d[lane] = g.w;
-  m->env[lane] = c.x;
-  m->denv[lane] = c.y;
-  __syncwarp();
-  return g;
-}
+  // Into the warp's private metadata.  Padding edges get nbr = 0, zero
+  // geometry and the last valid edge's row.  Returns the lane's (u, d) for
+  // the g_e epilogue (u flipped for src-owned rows: the backward edge has
+  // dst = nbr, src = own, u = r_nbr - r_own, flash.py:279); `rows2` tells
+  // whether the tile's edges fall in at most two CSR rows (first and last).
+  __device__ __forceinline__ float4 store(WarpMeta *m, bool src_owned, int lane,
+                                          bool &rows2) const {
+    const int first = __shfl_sync(0xffffffffu, o, 0);
+    const int last = __shfl_sync(0xffffffffu, o, max(n_e - 1, 0));
+    rows2 = __all_sync(0xffffffffu, lane >= n_e || o == first || o == last);
+    m->own[lane] = lane < n_e ? o : last;  // padding edges extend the last row (m = 0)
+    m->nbr[lane] = n;
+    m->d[lane] = g.w;
+    m->env[lane] = c.x;
+    m->denv[lane] = c.y;
+    __syncwarp();
+    return src_owned ? make_float4(-g.x, -g.y, -g.z, g.w) : g;
+  }
+};
 
 // Gaussian basis b[k][e] = exp((-g*dk)*dk) * C(d) (model.py:123-133) or, with
 // DERIV, its derivative db = exp(..) * (-2 g dk C + C') (model.py:148-157),
@@ -471,6 +481,7 @@ k_edge_fwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
   const float bsc = Q ? 1.f : 16384.f;
 
   float pv[TT];  // P[src][ch] of the current tile
+  MetaRegs mr;   // raw metadata of the tile after next
   for (int it = -1; it < ntiles; ++it) {
     const int t0 = tr.eb + it * TT;
     const bool more = it + 1 < ntiles;
@@ -478,15 +489,20 @@ k_edge_fwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
     PHASE(0, it, 0);
     if (it < 0) {
       bool r2;
-      load_meta(a, geo, env, W.meta(0), tr.eb, n_n, false, W.lane, r2);
+      mr.load(a, geo, env, tr.eb, n_n, W.lane);
+      mr.store(W.meta(0), false, W.lane, r2);
+      if (more) mr.load(a, geo, env, tr.eb + TT, min(TT, tr.ee - tr.eb - TT), W.lane);
     } else {
       W.wait(BAR_G1, it);
       PHASE(0, it, 1);
       tile_h<Q, false>(W, rs0, b0c, hs);
       REQ(BAR_G2, (mma_chain<D / 16, NP>(W.tmem_g + S1, w1, hb, idesc)));
       PHASE(0, it, 2);
-      bool r2;
-      if (more) load_meta(a, geo, env, W.meta(it + 1), t0 + TT, n_n, false, W.lane, r2);
+      if (more) {
+        bool r2;
+        mr.store(W.meta(it + 1), false, W.lane, r2);
+        if (it + 2 < ntiles) mr.load(a, geo, env, t0 + 2 * TT, min(TT, tr.ee - t0 - 2 * TT), W.lane);
+      }
     }
     if (more) {  // basis + G1 of the next tile overlap G2
       tile_basis<false, Q>(a, W, W.meta(it + 1), bsc);
@@ -573,13 +589,16 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
 
   float4 ue = make_float4(0.f, 0.f, 0.f, 0.f), ue_n = ue;  // this lane's edge: (u, d)
   bool rows2 = true, rows2_n = true;
+  MetaRegs mr;  // raw metadata of the tile after next
   for (int it = -1; it < ntiles; ++it) {
     const int t0 = tr.eb + it * TT;
     const bool more = it + 1 < ntiles;
     const int n_n = min(TT, tr.ee - t0 - TT);
     PHASE(1, it, 0);
     if (it < 0) {
-      ue_n = load_meta(a, geo, env, W.meta(0), tr.eb, n_n, true, W.lane, rows2_n);
+      mr.load(a, geo, env, tr.eb, n_n, W.lane);
+      ue_n = mr.store(W.meta(0), true, W.lane, rows2_n);
+      if (more) mr.load(a, geo, env, tr.eb + TT, min(TT, tr.ee - tr.eb - TT), W.lane);
     } else {
       const WarpMeta *M = W.meta(it);
       const int n_e = min(TT, tr.ee - t0);
@@ -595,7 +614,10 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
       tile_h<Q, !Q>(W, rs0, b0c, hs);
       REQ(BAR_G2, (mma_chain<D / 16, NPF>(W.tmem_g + S1, w1, hb, id_f)));
       PHASE(1, it, 2);
-      if (more) ue_n = load_meta(a, geo, env, W.meta(it + 1), t0 + TT, n_n, true, W.lane, rows2_n);
+      if (more) {
+        ue_n = mr.store(W.meta(it + 1), true, W.lane, rows2_n);
+        if (it + 2 < ntiles) mr.load(a, geo, env, t0 + 2 * TT, min(TT, tr.ee - t0 - 2 * TT), W.lane);
+      }
       W.wait(BAR_G2, it);
       PHASE(1, it, 3);
       // grad_w = gH * P[src] (flash.py:291) -> B operand of G3 (W1^T)
