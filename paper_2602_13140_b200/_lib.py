@@ -107,7 +107,8 @@ def load(path: os.PathLike | None = None):
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    # FCG_LIB_PATH: diagnostic A/B override (another in-tree build of the same ABI)
+    p = Path(path) if path else Path(os.environ.get("FCG_LIB_PATH", LIB_PATH))
     if not p.exists():
         raise RuntimeError(
             f"libfcg.so not found at {p}; build it with "

@@ -61,12 +61,19 @@ def launch_list(tag):
 
 
 def full_set(tag):
-    p = ROOT / "gpurun_out" / f"prof_{tag}.ncu-rep"
-    if not p.exists():
-        return []
+    reps = sorted((ROOT / "gpurun_out").glob(f"prof_{tag}*.ncu-rep"))
+    res = []
+    for p in reps:
+        res += _full_one(p)
+    return res
+
+
+def _full_one(p):
     out = subprocess.run(["ncu", "-i", str(p), "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
+    if len(rows) < 3:
+        return []
     hdr, units = rows[0], rows[1]
     res = []
     for r in rows[2:]:
@@ -115,6 +122,8 @@ def main(tag):
                     vals.append(f"{v:.1f}")
             lines.append(f"| {d['kernel']} | " + " | ".join(vals) + " |")
             name = d["kernel"].replace("k_", "", 1)
+            if name.endswith("_tc"):  # bench.py's profiler classes drop the suffix
+                name = name[:-3]
             if "dram_read" in d:
                 summary[name] = {"dram_bytes": d.get("dram_read", 0) + d.get("dram_write", 0),
                                  "duration_s": d.get("duration"), "tag": tag}
