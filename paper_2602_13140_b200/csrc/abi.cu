@@ -46,7 +46,7 @@ void prof_mark(int id, bool begin, cudaStream_t s) {
 
 static size_t md_extra_bytes(int R, int N) {
   Carver c(nullptr, 0);
-  c.take<float>((size_t)R * N * 3);  // noise
+  c.take<char>(noise_ring_bytes(R, N));  // noise ring + tag
   c.take<float>((size_t)R * N * 3);  // prior forces
   c.take<float>((size_t)R * N);      // per-atom energies
   return c.off + 256;
@@ -180,15 +180,13 @@ int fcg_md_step(const fcg_model *m, const fcg_prior *pr, const fcg_md_params *p,
   void *ws_nbr = w;
   void *ws_ef = w + ((nb + 255) & ~size_t(255));
   Carver c(w + ((nb + 255) & ~size_t(255)) + ((eb + 255) & ~size_t(255)), md_extra_bytes(R, N));
-  float *noise = c.take<float>((size_t)R * N * 3);
+  void *ring = c.take<char>(noise_ring_bytes(R, N));
   float *fprior = c.take<float>((size_t)R * N * 3);
   float *per_atom = c.take<float>((size_t)R * N);
 
   int rc;
   // leading B + A + O + A with the forces of the current state (md.py:200-202)
-  if ((rc = normal_noise(p->seed, p->rep_offset, step, R, N, noise, s))) return rc;
-  if ((rc = langevin_baoa(p, mass, R, N, forces, noise, pos, vel, s))) return rc;
-  if ((rc = step_advance(step, s))) return rc;
+  if ((rc = langevin_leading(p, mass, R, N, forces, step, pos, vel, ring, s))) return rc;
   // force evaluation at the new positions (md.py:203, _ReplicaForces)
   if ((rc = nbr_build(pos, R, N, r_cut, cap_e, ptr, nbr, rev, own, status, ws_nbr, nb, s, step,
                       p->neighbor_stride)))

@@ -142,6 +142,10 @@ int half_kick(const fcg_md_params *p, const float *mass, int R, int N, const flo
 int prior_forces(const fcg_prior *pr, const float *pos, int R, int N, float *e_prior,
                  float *f_prior, cudaStream_t s);
 int step_advance(int64_t *step, cudaStream_t s);
+size_t noise_ring_bytes(int R, int N);
+int langevin_leading(const fcg_md_params *p, const float *mass, int R, int N,
+                     const float *forces, int64_t *step, float *pos, float *vel, void *ring_ws,
+                     cudaStream_t s);
 // node_tc.cu
 void node_tc_configure();
 void launch_node_pre_tc(const float *X, const fcg_block &b, int quant, float *P, int nrows,

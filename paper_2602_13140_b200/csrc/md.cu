@@ -14,6 +14,8 @@
 
 namespace fcg {
 
+constexpr int NOISE_RING = 16;  // steps of noise generated per refill
+
 // ---- Philox-4x64-10 (Random123 / numpy) ------------------------------------
 struct U64x4 { uint64_t v[4]; };
 
@@ -108,13 +110,9 @@ __device__ double zig_slow(uint64_t seed, uint64_t rep, uint64_t step, uint64_t 
 // the first draw that misses the fast path are consecutive samples; that
 // draw's owner lane resolves numpy's rejection loop alone (reading further
 // words on demand) and the walk resumes after the words it consumed.
-__global__ void __launch_bounds__(256)
-k_normal_noise(uint64_t seed, int rep_offset, const int64_t *__restrict__ stepp, int R, int n3,
-               float *__restrict__ out) {
-  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (warp >= R) return;
-  uint64_t rep = (uint64_t)(rep_offset + warp), step = (uint64_t)*stepp;
-  float *dst = out + (size_t)warp * n3;
+// The warp's walk over one (seed, rep, step) stream, writing n3 samples.
+__device__ __forceinline__ void noise_stream(uint64_t seed, uint64_t rep, uint64_t step, int n3,
+                                             float *__restrict__ dst, int lane) {
   uint64_t pos = 0;  // stream position of the next sample start
   int produced = 0;
   while (produced < n3) {
@@ -164,6 +162,45 @@ k_normal_noise(uint64_t seed, int rep_offset, const int64_t *__restrict__ stepp,
   }
 }
 
+__global__ void __launch_bounds__(256)
+k_normal_noise(uint64_t seed, int rep_offset, const int64_t *__restrict__ stepp, int R, int n3,
+               float *__restrict__ out) {
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= R) return;
+  noise_stream(seed, (uint64_t)(rep_offset + warp), (uint64_t)*stepp, n3,
+               out + (size_t)warp * n3, lane);
+}
+
+// ---- noise ring for fcg_md_step ---------------------------------------------
+// The noise of a step depends only on (seed, replica, step) (md.py:127-131),
+// so the MD step generates it NOISE_RING steps at a time (R x NOISE_RING
+// warps instead of R) into a workspace ring.  A device tag {magic, seed,
+// rep_offset, base step} says which steps the ring holds; the three kernels
+// of the leading half-step all evaluate ring_valid() on the same tag, and
+// only the last of them (step_advance) rewrites it, so they always agree.
+struct NoiseTag {
+  uint64_t magic, seed;
+  int64_t rep_offset, base, layout;  // layout = R * 2^32 + 3N
+};
+constexpr uint64_t kNoiseMagic = 0x4e6f697365526e67ull;  // "NoiseRng"
+__device__ __forceinline__ bool ring_valid(const NoiseTag *t, uint64_t seed, int rep_offset,
+                                           int64_t layout, int64_t step) {
+  return t->magic == kNoiseMagic && t->seed == seed && t->rep_offset == rep_offset &&
+         t->layout == layout && step >= t->base && step < t->base + NOISE_RING;
+}
+
+__global__ void __launch_bounds__(256)
+k_noise_ring(uint64_t seed, int rep_offset, const int64_t *__restrict__ stepp, int R, int n3,
+             const NoiseTag *__restrict__ tag, float *__restrict__ ring) {
+  const int64_t step = *stepp;
+  if (ring_valid(tag, seed, rep_offset, ((int64_t)R << 32) + n3, step)) return;
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= R * NOISE_RING) return;
+  const int j = warp / R, r = warp % R;
+  noise_stream(seed, (uint64_t)(rep_offset + r), (uint64_t)(step + j), n3,
+               ring + ((size_t)j * R + r) * n3, lane);
+}
+
 int normal_noise(uint64_t seed, int rep_offset, const int64_t *step, int R, int N, float *out,
                  cudaStream_t s) {
   if (R < 1 || N < 1) { set_error("normal_noise: bad shape"); return FCG_ERR_ARG; }
@@ -199,6 +236,72 @@ int langevin_baoa(const fcg_md_params *p, const float *mass, int R, int N, const
   FCG_PROF(P_BAOA, s);
   k_baoa<<<ceil_div(n, 256), 256, 0, s>>>(*p, mass, N, n, forces, noise, pos, vel);
   return cuda_status("langevin_baoa");
+}
+
+// BAOA with this step's slot of the noise ring
+__global__ void k_baoa_ring(fcg_md_params p, const float *__restrict__ mass, int N, long long n,
+                            const float *__restrict__ F, const NoiseTag *__restrict__ tag,
+                            const int64_t *__restrict__ stepp, const float *__restrict__ ring,
+                            float *__restrict__ pos, float *__restrict__ vel) {
+  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int64_t step = *stepp;
+  const int64_t slot =
+      ring_valid(tag, p.seed, p.rep_offset, ((int64_t)(n / (3 * N)) << 32) + 3 * N, step)
+          ? step - tag->base : 0;
+  const float *xi = ring + slot * n;
+  int i = (int)((t / 3) % N);
+  float m = mass[i];
+  float v = vel[t], r = pos[t];
+  v = __fadd_rn(v, __fdiv_rn(__fmul_rn(p.half_dt, F[t]), m));
+  r = __fadd_rn(r, __fmul_rn(p.half_dt, v));
+  float c2 = __fsqrt_rn(__fdiv_rn(p.c2_num, m));
+  v = __fadd_rn(__fmul_rn(p.c1, v), __fmul_rn(c2, xi[t]));
+  r = __fadd_rn(r, __fmul_rn(p.half_dt, v));
+  vel[t] = v;
+  pos[t] = r;
+}
+
+__global__ void k_step_advance_ring(int64_t *step, NoiseTag *tag, uint64_t seed, int rep_offset,
+                                    int64_t layout) {
+  const int64_t s = *step;
+  if (!ring_valid(tag, seed, rep_offset, layout, s)) {
+    tag->magic = kNoiseMagic;
+    tag->seed = seed;
+    tag->rep_offset = rep_offset;
+    tag->layout = layout;
+    tag->base = s;
+  }
+  *step = s + 1;
+}
+
+size_t noise_ring_bytes(int R, int N) {
+  return 256 + sizeof(float) * (size_t)NOISE_RING * R * N * 3;
+}
+
+// Leading B + A + O + A of langevin_step (md.py:200-202) for all replicas
+// with the ring noise, then step += 1.
+int langevin_leading(const fcg_md_params *p, const float *mass, int R, int N,
+                     const float *forces, int64_t *step, float *pos, float *vel, void *ring_ws,
+                     cudaStream_t s) {
+  NoiseTag *tag = (NoiseTag *)ring_ws;
+  float *ring = (float *)((char *)ring_ws + 256);
+  const long long n = (long long)R * N * 3;
+  {
+    FCG_PROF(P_NOISE, s);
+    k_noise_ring<<<ceil_div((long long)R * NOISE_RING * 32, 256), 256, 0, s>>>(
+        p->seed, p->rep_offset, step, R, 3 * N, tag, ring);
+  }
+  {
+    FCG_PROF(P_BAOA, s);
+    k_baoa_ring<<<ceil_div(n, 256), 256, 0, s>>>(*p, mass, N, n, forces, tag, step, ring, pos, vel);
+  }
+  {
+    FCG_PROF(P_STEP, s);
+    k_step_advance_ring<<<1, 1, 0, s>>>(step, tag, p->seed, p->rep_offset,
+                                        ((int64_t)R << 32) + 3 * N);
+  }
+  return cuda_status("langevin_leading");
 }
 
 // half_kick, md.py:134-138
