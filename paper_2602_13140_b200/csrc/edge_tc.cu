@@ -80,6 +80,7 @@ struct TcShared {
   float xg[NGRP][2][4][TT];   // per-quarter partial grad_d (double-buffered)
   uint64_t bar[NGRP][4];      // GEMM completion, per kind
   uint64_t xbar[NGRP];        // the four partial grad_d rows of a tile are written
+  uint64_t wbar;              // filter weight images landed (bulk copy)
   unsigned int req[NGRP][4];  // operand arrivals per GEMM kind (mod 4)
   uint32_t tmem;
 };
@@ -288,11 +289,16 @@ __device__ __forceinline__ Wctx make_wctx(uint8_t *sm, TcShared *sh) {
   return W;
 }
 
+// The resident filter weights are staged by the TMA engine (cp.async.bulk);
+// every warp waits on wbar once before its first GEMM request.
 __device__ __forceinline__ void kernel_prologue(uint8_t *sm, TcShared *sh, const fcg_block &b) {
-  const uint4 *s0 = (const uint4 *)b.f0_img, *s1 = (const uint4 *)b.f1_img;
-  uint4 *d0 = (uint4 *)(sm + SM_W0), *d1 = (uint4 *)(sm + SM_W1);
-  for (int q = threadIdx.x; q < (int)(2 * W0_BYTES / 16); q += TC_THREADS) d0[q] = __ldg(s0 + q);
-  for (int q = threadIdx.x; q < (int)(2 * W1_BYTES / 16); q += TC_THREADS) d1[q] = __ldg(s1 + q);
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&sh->wbar, 1);
+    tc::fence_mbar_init();
+    tc::mbar_expect_tx(&sh->wbar, 2 * W0_BYTES + 2 * W1_BYTES);
+    tc::bulk_g2s(sm + SM_W0, b.f0_img, 2 * W0_BYTES, &sh->wbar);
+    tc::bulk_g2s(sm + SM_W1, b.f1_img, 2 * W1_BYTES, &sh->wbar);
+  }
   if (threadIdx.x < NGRP) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -506,6 +512,7 @@ k_edge_fwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
     }
     if (more) {  // basis + G1 of the next tile overlap G2
       tile_basis<false, Q>(a, W, W.meta(it + 1), bsc);
+      if (it < 0) tc::mbar_wait(&sh->wbar, 0);  // weights resident before the first GEMM
       REQ(BAR_G1, (mma_chain<DR / 16, NP>(W.tmem_g + S0, w0, bb, idesc)));
     }
     PHASE(0, it, 3);
@@ -676,6 +683,7 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
     }
     if (more) {  // basis + G1 of the next tile overlap the grad_d reduction
       tile_basis<false, Q>(a, W, W.meta(it + 1), bsc);
+      if (it < 0) tc::mbar_wait(&sh->wbar, 0);  // weights resident before the first GEMM
       REQ(BAR_G1, (mma_chain<DR / 16, NPF>(W.tmem_g + S0, w0, bb, id_f)));
     }
     PHASE(1, it, 9);

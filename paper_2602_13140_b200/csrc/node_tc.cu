@@ -32,7 +32,8 @@ constexpr uint32_t NTM_D0 = 0, NTM_D1 = 128;
 
 struct NodeMeta {
   unsigned int amax[4];
-  uint64_t bar;
+  uint64_t bar;   // MMA completion
+  uint64_t wbar;  // weight images landed (bulk copy)
   uint32_t tmem;
 };
 constexpr uint32_t NSM_TOTAL = NSM_META + sizeof(NodeMeta);
@@ -43,13 +44,13 @@ struct NodeCtx {
   uint32_t phase;
 };
 
-__device__ __forceinline__ void stage(uint8_t *dst, const uint16_t *img, uint32_t bytes) {
-  const uint4 *s = (const uint4 *)img;
-  uint4 *d = (uint4 *)dst;
-  for (int q = threadIdx.x; q < (int)(bytes / 16); q += NTH) d[q] = __ldg(s + q);
-}
-
-__device__ __forceinline__ NodeCtx node_prologue(uint8_t *sm, NodeMeta *meta) {
+// Weight images are staged by the TMA engine (cp.async.bulk) while the
+// threads load their activation rows; the issuing thread waits on wbar
+// before the first MMA.
+__device__ __forceinline__ NodeCtx node_prologue(uint8_t *sm, NodeMeta *meta,
+                                                 const uint16_t *img_a, uint32_t bytes_a,
+                                                 const uint16_t *img_b = nullptr,
+                                                 uint32_t bytes_b = 0) {
   NodeCtx c;
   c.warp = threadIdx.x >> 5;
   c.lane = threadIdx.x & 31;
@@ -59,7 +60,11 @@ __device__ __forceinline__ NodeCtx node_prologue(uint8_t *sm, NodeMeta *meta) {
   c.ec = NPT * c.part;
   if (threadIdx.x == 0) {
     tc::mbar_init(&meta->bar, 1);
+    tc::mbar_init(&meta->wbar, 1);
     tc::fence_mbar_init();
+    tc::mbar_expect_tx(&meta->wbar, bytes_a + bytes_b);
+    tc::bulk_g2s(sm + NSM_WA, img_a, bytes_a, &meta->wbar);
+    if (img_b) tc::bulk_g2s(sm + NSM_WB, img_b, bytes_b, &meta->wbar);
   }
   if (threadIdx.x < 4) meta->amax[threadIdx.x] = 0u;
   if (threadIdx.x < 32) tc::tmem_alloc<256>(&meta->tmem);
@@ -145,6 +150,7 @@ __device__ __forceinline__ void tmem_rows_to_act(uint32_t tcol, uint8_t *act, in
     tc::fence_before_sync();            \
     __syncthreads();                    \
     if (threadIdx.x == 0) {             \
+      tc::mbar_wait(&meta->wbar, 0);    \
       tc::fence_after_sync();           \
       issue_gemm(__VA_ARGS__);          \
       tc::mma_commit(&meta->bar);       \
@@ -170,8 +176,7 @@ k_node_linear_tc(const float *__restrict__ X, const uint16_t *__restrict__ img, 
   extern __shared__ __align__(1024) uint8_t sm[];
   NodeMeta *meta = (NodeMeta *)(sm + NSM_META);
   uint8_t *act = sm + NSM_ACT;
-  stage(sm + NSM_WA, img, 2 * IMG128);
-  NodeCtx c = node_prologue(sm, meta);
+  NodeCtx c = node_prologue(sm, meta, img, 2 * IMG128);
   const int node0 = blockIdx.x * NN;
   const bool fwd = kMode == 0;
   // backward folds the W16 row scale of the K index (output channel) into X
@@ -179,6 +184,13 @@ k_node_linear_tc(const float *__restrict__ X, const uint16_t *__restrict__ img, 
   const int s = rows_to_act(X, node0, nrows, c, fold, fwd && quant, &meta->amax[0], act, csr_ptr);
   NODE_ISSUE(c.tm + NTM_D0, c.sbase + NSM_WA, IMG128, D, !fwd, c.sbase + NSM_ACT, D,
              tc::idesc_f16(128, NN, fwd ? 0 : 1, 1), quant ? (fwd ? 1 : 2) : 3);
+  // the accumulated operand (backward) is fetched while the GEMM runs
+  float yv[NPT];
+#pragma unroll
+  for (int i = 0; i < NPT; ++i) {
+    const int n = node0 + c.ec + i;
+    yv[i] = (!fwd && n < nrows) ? Y[(size_t)n * D + c.ch] : 0.f;
+  }
   NODE_WAIT();
   const float un = pow2f(-((quant ? 0 : wexp) + s)) * ((fwd && quant) ? __ldg(&rowscale[c.ch]) : 1.f);
   const float b = fwd ? __ldg(&bias[c.ch]) : 0.f;
@@ -186,16 +198,14 @@ k_node_linear_tc(const float *__restrict__ X, const uint16_t *__restrict__ img, 
 #pragma unroll
   for (int c0 = 0; c0 < NPT; c0 += 16) {
     float v[16];
-    tc::tmem_ld16(c.tl + NTM_D0 + c.ec + c0, v);
-    tc::tmem_ld_wait();
+    tc::tmem_ld16w(c.tl + NTM_D0 + c.ec + c0, v);
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       int n = node0 + c.ec + c0 + i;
       if (n < nrows) {
-        float *y = &Y[(size_t)n * D + c.ch];
         float r = v[i] * un + b;
-        r = fwd ? r : *y + r;
-        *y = r;
+        r = fwd ? r : yv[c0 + i] + r;
+        Y[(size_t)n * D + c.ch] = r;
         mx = fmaxf(mx, fabsf(r));
       }
     }
@@ -213,9 +223,7 @@ k_node_post_tc(const float *__restrict__ H, const fcg_block blk, int quant,
   extern __shared__ __align__(1024) uint8_t sm[];
   NodeMeta *meta = (NodeMeta *)(sm + NSM_META);
   uint8_t *act = sm + NSM_ACT;
-  stage(sm + NSM_WA, blk.p0_img, 2 * IMG128);
-  stage(sm + NSM_WB, blk.p1_img, 2 * IMG128);
-  NodeCtx c = node_prologue(sm, meta);
+  NodeCtx c = node_prologue(sm, meta, blk.p0_img, 2 * IMG128, blk.p1_img, 2 * IMG128);
   const int node0 = blockIdx.x * NN;
   const int np = quant ? 1 : 3;
   const uint32_t idesc = tc::idesc_f16(128, NN, 0, 1);
@@ -246,18 +254,24 @@ k_node_post_tc(const float *__restrict__ H, const fcg_block blk, int quant,
   if (!quant) s1 = scale_exp(block_amax(mx, &meta->amax[1]));
   tmem_rows_to_act(c.tl + NTM_D0, act, D, c.ch, c.ec, pow2f(s1), !quant);
   NODE_ISSUE(c.tm + NTM_D1, c.sbase + NSM_WB, IMG128, D, false, c.sbase + NSM_ACT, D, idesc, np);
+  // the residual stream is fetched while the GEMM runs
+  float xv[NPT];
+#pragma unroll
+  for (int i = 0; i < NPT; ++i) {
+    const int n = node0 + c.ec + i;
+    xv[i] = n < nrows ? X[(size_t)n * D + c.ch] : 0.f;
+  }
   NODE_WAIT();
   const float un1 = quant ? __ldg(&blk.p1_s[c.ch]) : pow2f(-(blk.p1_exp + s1));
   const float b1 = __ldg(&blk.p1_b[c.ch]);
 #pragma unroll
   for (int c0 = 0; c0 < NPT; c0 += 16) {
     float v[16];
-    tc::tmem_ld16(c.tl + NTM_D1 + c.ec + c0, v);
-    tc::tmem_ld_wait();
+    tc::tmem_ld16w(c.tl + NTM_D1 + c.ec + c0, v);
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       int n = node0 + c.ec + c0 + i;
-      if (n < nrows) X[(size_t)n * D + c.ch] += v[i] * un1 + b1;
+      if (n < nrows) X[(size_t)n * D + c.ch] = xv[c0 + i] + (v[i] * un1 + b1);
     }
   }
   node_epilogue_end(meta, c);
@@ -272,15 +286,20 @@ k_node_post_bwd_tc(const float *__restrict__ G, const fcg_block blk, int quant,
   extern __shared__ __align__(1024) uint8_t sm[];
   NodeMeta *meta = (NodeMeta *)(sm + NSM_META);
   uint8_t *act = sm + NSM_ACT;
-  stage(sm + NSM_WA, blk.p1_img, 2 * IMG128);
-  stage(sm + NSM_WB, blk.p0_img, 2 * IMG128);
-  NodeCtx c = node_prologue(sm, meta);
+  NodeCtx c = node_prologue(sm, meta, blk.p1_img, 2 * IMG128, blk.p0_img, 2 * IMG128);
   const int node0 = blockIdx.x * NN;
   const int np = quant ? 2 : 3;
   const uint32_t idesc = tc::idesc_f16(128, NN, 1, 1);
   const float f1 = quant ? __ldg(&blk.p1_s[c.ch]) : 1.f;
   const int sg = rows_to_act(G, node0, nrows, c, f1, false, &meta->amax[0], act);
   NODE_ISSUE(c.tm + NTM_D0, c.sbase + NSM_WA, IMG128, D, true, c.sbase + NSM_ACT, D, idesc, np);
+  // ssp'(Zp) operands are fetched while the GEMM runs
+  float zv[NPT];
+#pragma unroll
+  for (int i = 0; i < NPT; ++i) {
+    const int n = node0 + c.ec + i;
+    zv[i] = n < nrows ? __ldg(&Zp[(size_t)n * D + c.ch]) : 0.f;
+  }
   NODE_WAIT();
   const float un = pow2f(-((quant ? 0 : blk.p1_exp) + sg));
   const float f0 = quant ? __ldg(&blk.p0_s[c.ch]) : 1.f;
@@ -288,13 +307,11 @@ k_node_post_bwd_tc(const float *__restrict__ G, const fcg_block blk, int quant,
 #pragma unroll
   for (int c0 = 0; c0 < NPT; c0 += 16) {
     float v[16];
-    tc::tmem_ld16(c.tl + NTM_D0 + c.ec + c0, v);
-    tc::tmem_ld_wait();
+    tc::tmem_ld16w(c.tl + NTM_D0 + c.ec + c0, v);
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       int n = node0 + c.ec + c0 + i;
-      float z = n < nrows ? __ldg(&Zp[(size_t)n * D + c.ch]) : 0.f;
-      v[i] = n < nrows ? v[i] * un * sigmoid_fast(z) * f0 : 0.f;
+      v[i] = n < nrows ? v[i] * un * sigmoid_fast(zv[c0 + i]) * f0 : 0.f;
       mx = fmaxf(mx, fabsf(v[i]));
     }
     tc::tmem_st16(c.tl + NTM_D0 + c.ec + c0, v);
@@ -334,8 +351,7 @@ k_readout_tc(const float *__restrict__ X, const fcg_model m, float *__restrict__
   NodeMeta *meta = (NodeMeta *)(sm + NSM_META);
   uint8_t *act = sm + NSM_ACT;
   float *red = (float *)(sm + NSM_ACT);  // [128 nodes][65] after G1 completes
-  stage(sm + NSM_WA, m.r0_img, 2 * IMG64);
-  NodeCtx c = node_prologue(sm, meta);
+  NodeCtx c = node_prologue(sm, meta, m.r0_img, 2 * IMG64);
   const bool quant = m.format == FCG_FMT_W16;
   const int node0 = blockIdx.x * NN;
   const int sx = rows_to_act(X, node0, nrows, c, 1.f, quant, &meta->amax[0], act);
