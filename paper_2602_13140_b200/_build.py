@@ -55,7 +55,8 @@ def build_library(force: bool = False, verbose: bool = False) -> Path:
 
     def compile_one(src: Path):
         obj = BUILD / (src.stem + ".o")
-        cmd = [nvcc, *ARCH, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+        extra = os.environ.get("FCG_NVCC_EXTRA", "").split()  # diagnostic A/B builds
+        cmd = [nvcc, *ARCH, *NVCC_FLAGS, *extra, "-c", str(src), "-o", str(obj)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         logs[src.name] = res.stdout + res.stderr
         if res.returncode != 0:
