@@ -261,6 +261,17 @@ int fcg_md_step(const fcg_model *m, const fcg_prior *pr,
                 int32_t *ptr, int32_t *nbr, int32_t *rev, int32_t *own,
                 int64_t *status, void *ws, size_t ws_bytes, void *stream);
 
+/* ---------------------------------------------------------------------
+ * (f) output pipeline, md.py:224-228 / :312-326.  HOST pointers.
+ * Formats R trajectory frames (replica indices replica0..replica0+R-1) of
+ * float32 positions[R][N][3] exactly as the reference's _format_frame
+ * ("%.9f" coordinates) into out[cap]; returns the byte count, or minus the
+ * required size when out is NULL or too small.  nthreads <= 0: all cores.
+ * ------------------------------------------------------------------- */
+int64_t fcg_format_xyz(const float *pos, const int32_t *types, int R, int N,
+                       int64_t step, int replica0, char *out, int64_t cap,
+                       int nthreads);
+
 /* Diagnostics: tcgen05 (kind::f16) GEMM self-test.  dump[128][N] receives
  * the raw TMEM accumulator lanes of D = A * B^T for A[M][K], B[N][K] fp16
  * staged in the canonical no-swizzle core-matrix layout (K-major or

@@ -86,6 +86,8 @@ _SIGS = {
     "fcg_prior_forces": (C.c_int, [C.POINTER(FcgPrior), _VP, C.c_int, C.c_int, _VP, _VP, _VP]),
     "fcg_selftest_mma": (C.c_int, [_VP, _VP, _VP, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                    C.c_int, C.c_int, C.c_int, C.c_int, _VP]),
+    "fcg_format_xyz": (C.c_int64, [_VP, _VP, C.c_int, C.c_int, C.c_int64, C.c_int, C.c_char_p,
+                                   C.c_int64, C.c_int]),
     "fcg_md_workspace_bytes": (C.c_size_t, [C.POINTER(FcgModel), C.c_int, C.c_int, C.c_int64]),
     "fcg_md_step": (C.c_int, [C.POINTER(FcgModel), C.POINTER(FcgPrior), C.POINTER(FcgMdParams),
                               _VP, _VP, C.c_int, C.c_int, C.c_double, C.c_int64, _VP, _VP, _VP,
@@ -150,6 +152,28 @@ def i32ptr(t):
 
 def vp(t):
     return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p()
+
+
+def format_xyz(positions, types, step: int, replica0: int = 0, nthreads: int = 0) -> bytes:
+    """Trajectory frames of positions[R][N][3] (host float32) in the
+    reference's bytes (md.py:224-228), formatted in C (no GIL held)."""
+    import numpy as np
+    pos = np.ascontiguousarray(positions, dtype=np.float32)
+    if pos.ndim == 2:
+        pos = pos[None]
+    typ = np.ascontiguousarray(types, dtype=np.int32)
+    R, N = pos.shape[0], pos.shape[1]
+    lib = load()
+    args = (C.c_void_p(pos.ctypes.data), C.c_void_p(typ.ctypes.data), R, N, int(step),
+            int(replica0))
+    need = -lib.fcg_format_xyz(*args, None, 0, nthreads)
+    if need < 0:
+        raise ValueError((lib.fcg_last_error() or b"").decode())
+    buf = C.create_string_buffer(int(need))
+    n = lib.fcg_format_xyz(*args, buf, need, nthreads)
+    if n < 0:
+        raise RuntimeError("fcg_format_xyz: buffer too small")
+    return buf.raw[:n]
 
 
 def profile_read(max_classes: int = 32) -> dict:

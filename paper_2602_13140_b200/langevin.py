@@ -10,13 +10,16 @@ Drop-in points (reference md.py):
                        GpuReplicaForces, else GPU integrator + host forces;
   * run_simulation     md.py:276-349, device-resident with host I/O only at
                        output strides; same trajectory.xyz / scalars.csv
-                       formats.
+                       formats, written by a background thread from pinned
+                       snapshots (frames formatted in C, fcg_format_xyz).
 """
 
 from __future__ import annotations
 
 import ctypes as C
 import math
+import queue
+import threading
 import time
 from dataclasses import dataclass, field
 from pathlib import Path
@@ -224,6 +227,77 @@ def _format_frame(types, positions, step, replica):
     return "\n".join(rows) + "\n"
 
 
+class _FrameWriter:
+    """Output pipeline of run_simulation.
+
+    snapshot() enqueues async device->pinned copies of the state on the
+    engine's stream and returns at once; a writer thread waits for them,
+    computes kinetic T (md.py:175-180), formats the frames in C and appends
+    trajectory.xyz / scalars.csv rows in (step, replica) order.  A ring of
+    `depth` pinned slots bounds the memory and applies back-pressure.
+    """
+
+    def __init__(self, eng, types, masses, traj, scal, depth: int = 3):
+        torch = eng.torch
+        R, N = eng.R, eng.N
+        self.eng, self.types, self.masses = eng, np.asarray(types), masses
+        self.traj, self.scal = traj, scal
+        pin = dict(dtype=torch.float32, pin_memory=True)
+        self.slots = [dict(pos=torch.empty(R, N, 3, **pin), vel=torch.empty(R, N, 3, **pin),
+                           pot=torch.empty(R, **pin), pri=torch.empty(R, **pin),
+                           ev=torch.cuda.Event()) for _ in range(depth)]
+        self.free = queue.Queue()
+        for i in range(depth):
+            self.free.put(i)
+        self.work = queue.Queue()
+        self.error = None
+        self.thread = threading.Thread(target=self._run, name="fcg-output", daemon=True)
+        self.thread.start()
+
+    def snapshot(self, step: int, wall_ms: float):
+        i = self.free.get()
+        if self.error is not None:
+            raise self.error
+        s, e = self.slots[i], self.eng
+        s["pos"].copy_(e.pos, non_blocking=True)
+        s["vel"].copy_(e.vel, non_blocking=True)
+        s["pot"].copy_(e.potential, non_blocking=True)
+        s["pri"].copy_(e.prior_e, non_blocking=True)
+        s["ev"].record()
+        self.work.put((i, step, wall_ms))
+
+    def _run(self):
+        while True:
+            item = self.work.get()
+            if item is None:
+                return
+            i, step, wall_ms = item
+            try:
+                if self.error is None:
+                    s = self.slots[i]
+                    s["ev"].synchronize()
+                    pos, vel = s["pos"].numpy(), s["vel"].numpy()
+                    st = SimState(positions=pos, velocities=vel, masses=self.masses, step=step)
+                    kin = kinetic_temperature(st)
+                    pot = s["pot"].numpy().astype(np.float64)
+                    pri = s["pri"].numpy().astype(np.float64)
+                    self.traj.write(_lib.format_xyz(pos, self.types, step))
+                    self.scal.write("".join(
+                        f"{step},{rep},{pot[rep]:.10g},{pri[rep]:.10g},{kin[rep]:.10g},"
+                        f"{wall_ms:.3f}\n" for rep in range(pos.shape[0])))
+            except BaseException as exc:  # surfaced on the next snapshot/close
+                self.error = exc
+            finally:
+                self.free.put(i)
+
+    def close(self):
+        if self.thread.is_alive():
+            self.work.put(None)
+            self.thread.join()
+        if self.error is not None:
+            raise self.error
+
+
 def run_simulation(params, system, config: SimConfig, out_dir, resume_from=None,
                    graph_steps: int = 32, rep_offset: int = 0) -> RunResult:
     """Device-resident run_simulation (md.py:276-349).
@@ -261,9 +335,10 @@ def run_simulation(params, system, config: SimConfig, out_dir, resume_from=None,
     eng.load_state(pos0, vel0, step0)
 
     traj_path, scal_path = out_dir / "trajectory.xyz", out_dir / "scalars.csv"
-    traj = open(traj_path, "w")
+    traj = open(traj_path, "wb")
     scal = open(scal_path, "w")
     scal.write("# flashcg-scalars v1\n" + SCALARS_SCHEMA + "\n")
+    writer = _FrameWriter(eng, system.types, masses, traj, scal)
     t_start = time.perf_counter()
     last = [t_start]
     edge_total = [0, 0]  # (sum of per-replica edge counts, evaluations*replicas)
@@ -272,22 +347,14 @@ def run_simulation(params, system, config: SimConfig, out_dir, resume_from=None,
         now = time.perf_counter()
         wall_ms = (now - last[0]) * 1e3 / max(steps_since, 1)
         last[0] = now
-        pos, vel, _ = eng.read_state()
-        st = SimState(positions=pos, velocities=vel, masses=masses, step=step_done)
-        kin = kinetic_temperature(st)
-        pot = eng.potential.cpu().numpy().astype(np.float64)
-        pri = eng.prior_e.cpu().numpy().astype(np.float64)
-        for rep in range(R):
-            traj.write(_format_frame(system.types, pos[rep], step_done, rep))
-            scal.write(f"{step_done},{rep},{pot[rep]:.10g},{pri[rep]:.10g},"
-                       f"{kin[rep]:.10g},{wall_ms:.3f}\n")
+        writer.snapshot(step_done, wall_ms)
 
     def blowup(step_at):
+        writer.close()  # frames before the blow-up are complete
         pos, _, _ = eng.read_state()
         dump = out_dir / "blowup.xyz"
-        with open(dump, "w") as f:
-            for rep in range(R):
-                f.write(_format_frame(system.types, pos[rep], step_at, rep))
+        with open(dump, "wb") as f:
+            f.write(_lib.format_xyz(pos, system.types, step_at))
         traj.close()
         scal.close()
         raise SimulationBlowupError(f"simulation blew up at step {step_at}; "
@@ -342,7 +409,11 @@ def run_simulation(params, system, config: SimConfig, out_dir, resume_from=None,
             if cur % stride == 0:
                 emit(cur, n)
         eng.torch.cuda.synchronize()
+        writer.close()
     finally:
+        if writer.thread.is_alive():
+            writer.work.put(None)
+            writer.thread.join()
         traj.close()
         scal.close()
 

@@ -212,3 +212,20 @@ def test_workspace_queries_without_gpu():
     lib = _lib.load()
     assert lib.fcg_nbr_workspace_bytes(64, 269) > 64 * 269 * 4
     assert lib.fcg_group_workspace_bytes(1000, 50) > 1000 * 16
+
+
+def test_format_xyz_matches_reference_frame_format():
+    # fcg_format_xyz (host C) vs the reference's _format_frame restated
+    # (md.py:224-228), including non-finite, signed-zero and huge values
+    from paper_2602_13140_b200 import _lib
+    from paper_2602_13140_b200.langevin import _format_frame
+    rng = np.random.default_rng(3)
+    types = rng.integers(0, 8, 37)
+    pos = (rng.standard_normal((5, 37, 3)) * 4).astype(np.float32)
+    pos[0, 0] = (np.nan, np.inf, -np.inf)
+    pos[1, 1, 0], pos[1, 2, 1], pos[1, 3, 2] = -0.0, np.float32(3.4e38), np.float32(-1e-30)
+    pos[2, 4, 0] = -np.float32(np.nan)
+    ref = "".join(_format_frame(types, pos[r], 987654321, 11 + r) for r in range(5)).encode()
+    assert _lib.format_xyz(pos, types, 987654321, 11) == ref
+    assert _lib.format_xyz(pos, types, 987654321, 11, nthreads=1) == ref
+    assert _lib.format_xyz(pos[:0], types, 0) == b""
