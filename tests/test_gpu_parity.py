@@ -389,6 +389,26 @@ def test_run_simulation_outputs(tmp_path, golden):
     assert rep["ns_per_day"] > 0
 
 
+def test_checkpoint_resume_bit_exact(tmp_path, golden):
+    # md.py:289-299, :316-319 and test_md.py:174-193: a run resumed from the
+    # checkpoint written at step k ends bitwise where the uninterrupted run
+    # ends (counter-based noise, device noise ring re-keyed on resume)
+    c = golden["md"].case("traj_tiny")
+    n, sseed, pseed, R, _ = (int(x) for x in c["meta"])
+    sysm = generate_system("coil", n, sseed)
+    params = init_params(ModelConfig(**json.loads(str(c["cfg"]))), pseed)
+    chk = tmp_path / "run.flcg"
+    full = P.run_simulation(params, sysm, P.SimConfig(
+        dt_fs=4.0, n_steps=24, n_replicas=R, seed=9, output_stride=6,
+        checkpoint_path=str(chk), checkpoint_step=13), tmp_path / "a")
+    part = P.run_simulation(params, sysm, P.SimConfig(
+        dt_fs=4.0, n_steps=11, n_replicas=R, seed=9, output_stride=6), tmp_path / "b",
+        resume_from=chk)
+    assert part.final_state.step == full.final_state.step == 24
+    np.testing.assert_array_equal(part.final_state.positions, full.final_state.positions)
+    np.testing.assert_array_equal(part.final_state.velocities, full.final_state.velocities)
+
+
 def test_capacity_overflow_regrows_and_matches(tmp_path, golden, monkeypatch):
     c = golden["md"].case("traj_tiny")
     n, sseed, pseed, R, steps = (int(x) for x in c["meta"])
