@@ -16,6 +16,7 @@ from .schnet import (
     io_model_base,
     io_model_flash,
     segment_reduce,
+    traffic_report,
 )
 from .langevin import (
     KB,
@@ -46,7 +47,7 @@ __all__ = [
     "BlockParams", "ConfigError", "CsrLayout", "EnergyForces", "GpuReplicaForces", "KB",
     "ModelConfig", "ModelParams", "NeighborList", "PipelineMode", "PriorSpec", "RbfSpec",
     "RunResult", "SimConfig", "SimState", "SimulationBlowupError", "SystemSpec",
-    "TrafficReport", "build_neighbors_bruteforce", "build_neighbors_cells",
+    "TrafficReport", "traffic_report", "build_neighbors_bruteforce", "build_neighbors_cells",
     "flash_energy_forces", "generate_system", "group_by_destination", "group_by_source",
     "init_params", "integrate", "io_model_base", "io_model_flash", "kinetic_temperature",
     "make_step_rng", "run_simulation", "segment_reduce", "throughput_report",

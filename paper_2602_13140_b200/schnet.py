@@ -3,10 +3,14 @@
 `flash_energy_forces` keeps the reference signature and return type
 (flash.py:446-501) but evaluates the whole model — embedding, T fused
 interaction blocks, readout, and the force backward — in libfcg.so on
-cuda:0.  Computation is fp32 (the reference's production precision); the
-ablation flags of PipelineMode select reference CPU schedules that have no
-GPU counterpart, so every mode runs the fused, segment-reduced pipeline and
-reports its modelled traffic.
+cuda:0 (fp32, the reference's production precision).  PipelineMode's
+ablation flags pick the schedule as in the reference: fused=False runs the
+materialising schedule on the GPU (ablation.py: stacked edge tensors,
+atomic scatter-add or segmented reduction, autodiff forces — the paper's
+CGSchNet baseline) in the input dtype; fused=True runs the fused kernels
+(a fused atomic scatter has no GPU counterpart: it would only make the sums
+nondeterministic).  Every mode reports the reference's modelled traffic for
+its schedule (traffic_report).
 """
 
 from __future__ import annotations
@@ -89,6 +93,61 @@ def _flash_block_lines(N, E, D):
         ("messages", min(N, E) * D, 0), ("aggregation", 0, nd), ("aggregation", 6 * E, 3 * N),
         ("mlps", nd, nd), ("mlps", 2 * nd, nd),
     ]
+
+
+def _base_block_lines(N, E, D, Dr):
+    """(stage, read, written, atomics) element counts of one materialising
+    block, forward then backward (traffic.py:80-126): stacked basis, filter,
+    gathered-source and message tensors, atomic scatter-adds."""
+    nd, ed, edr = N * D, E * D, E * Dr
+    fwd = [("radial_basis", 6 * E, 3 * E, 0), ("radial_basis", 3 * E, E, 0),
+           ("radial_basis", E, edr, 0), ("radial_basis", E, E, 0),
+           ("radial_basis", edr + E, edr, 0), ("mlps", nd, nd, 0), ("filters", edr, ed, 0),
+           ("filters", ed, ed, 0), ("gather", ed, ed, 0), ("messages", 2 * ed, ed, 0),
+           ("aggregation", 0, nd, 0), ("aggregation", ed, 2 * ed, ed), ("mlps", nd, nd, 0),
+           ("mlps", 2 * nd, nd, 0)]
+    bwd = [("mlps", nd, nd, 0), ("mlps", 2 * nd, nd, 0), ("aggregation", ed, ed, 0),
+           ("messages", 2 * ed, ed, 0), ("messages", 2 * ed, ed, 0),
+           ("filters", ed + edr, edr, 0), ("gather", 0, nd, 0), ("gather", ed, 2 * ed, ed),
+           ("radial_basis", E, edr, 0), ("radial_basis", 2 * edr, E, 0),
+           ("radial_basis", 5 * E, 3 * E, 0), ("radial_basis", 0, 3 * N, 0),
+           ("radial_basis", 6 * E, 12 * E, 6 * E), ("mlps", nd, nd, 0),
+           ("mlps", 2 * nd, nd, 0)]
+    return fwd, bwd
+
+
+def traffic_report(mode: "PipelineMode", N: int, E: int, D: int, D_r: int, T: int,
+                   width: int) -> TrafficReport:
+    """Modelled traffic of one evaluation under the mode's schedule, as the
+    reference records it: fused+segmented (flash.py:446-501), materialised
+    + scatter (reference.py:100-209), fused + scatter (flash.py:373-443),
+    materialised + segmented (flash.py:310-370)."""
+    rep = TrafficReport()
+    fwd, bwd = _base_block_lines(N, E, D, D_r)
+    flash = _flash_block_lines(N, E, D)
+    for _ in range(T):
+        if mode.fused and mode.segred:
+            for stage, r, w in flash:
+                rep.record(stage, r * width, w * width, 0)
+        elif not mode.fused and not mode.segred:
+            for stage, r, w, a in fwd + bwd:
+                rep.record(stage, r * width, w * width, a)
+        elif mode.fused:  # fused tiles, atomic scatter
+            for stage, r, w in flash:
+                rep.record(stage, r * width, w * width, 0)
+            rep.record("aggregation", 0, 2 * E * D * width, E * D)
+            rep.record("aggregation", 0, 0, E * D + 6 * E)
+        else:  # materialised tensors, segmented reduction
+            for stage, r, w, _ in fwd:
+                if stage != "aggregation":
+                    rep.record(stage, r * width, w * width, 0)
+            rep.record("aggregation", 2 * E * D * width, N * D * width, 0)
+            for stage, r, w, _ in bwd:
+                if stage not in ("aggregation", "gather"):
+                    rep.record(stage, r * width, w * width, 0)
+            rep.record("gather", 2 * E * D * width, N * D * width, 0)
+            rep.record("aggregation", 2 * E * D * width, N * D * width, 0)
+    return rep
 
 
 def io_model_flash(N: int, E: int, D: int, D_r: int, T: int, width: int) -> int:
@@ -219,8 +278,37 @@ def flash_energy_forces(positions, types, params, mode: PipelineMode = PipelineM
             if dst_csr.perm.size != nl.num_edges or dst_csr.ptr.size != nl.n + 1:
                 raise ValueError("CSR layout does not match the neighbor list")
         csr = csr_from_neighbor_list(nl)
-    energy, per_atom, forces = _evaluator(params)(positions.astype(np.float32), types, csr)
     E = int(csr[0][-1])
+    width = positions.dtype.itemsize if positions.dtype in (np.float32, np.float64) else 4
+    traffic = traffic_report(mode, N, E, cfg.hidden_dim, cfg.rbf_dim, len(params.blocks), width)
+    if not mode.fused:
+        from .ablation import materialized_energy_forces
+        from .engine import _torch
+        torch = _torch()
+        dt = torch.float64 if positions.dtype == np.float64 else torch.float32
+        dev = lambda a: torch.as_tensor(np.ascontiguousarray(a)).cuda()  # noqa: E731
+        e, pa, f = materialized_energy_forces(
+            _torch_model(params, dt), dev(positions.astype(np.float64 if dt == torch.float64
+                                                           else np.float32)),
+            dev(types.astype(np.int64)), dev(csr[0]), dev(csr[1]), dev(csr[3]), 1, N,
+            mode.segred)
+        return EnergyForces(energy=float(e[0].item()), per_atom=pa.cpu().numpy(),
+                            forces=f.cpu().numpy().astype(positions.dtype, copy=False),
+                            traffic=traffic)
+    energy, per_atom, forces = _evaluator(params)(positions.astype(np.float32), types, csr)
     return EnergyForces(energy=energy, per_atom=per_atom,
-                        forces=forces.astype(positions.dtype, copy=False),
-                        traffic=io_model_flash_report(N, E, params))
+                        forces=forces.astype(positions.dtype, copy=False), traffic=traffic)
+
+
+_TORCH_MODELS: dict = {}
+
+
+def _torch_model(params, dtype):
+    from .ablation import TorchModel
+    key = (id(params), str(dtype))
+    m = _TORCH_MODELS.get(key)
+    if m is None or m[0] is not params:
+        if len(_TORCH_MODELS) > 8:
+            _TORCH_MODELS.clear()
+        m = _TORCH_MODELS[key] = (params, TorchModel(params, dtype))
+    return m[1]

@@ -131,7 +131,8 @@ def test_energy_forces_fp32(golden, name):
     assert out.traffic.atomic_updates == 0
     assert out.traffic.total_bytes == P.io_model_flash(
         c["pos"].shape[0], int(P.build_neighbors_cells(c["pos"], params.config.cutoff).num_edges),
-        params.config.hidden_dim, params.config.rbf_dim, params.config.num_blocks, 4)
+        params.config.hidden_dim, params.config.rbf_dim, params.config.num_blocks,
+        c["pos"].dtype.itemsize)  # the reference models the input dtype's width
 
 
 # W16 energy tolerance.  Every W16 layer rounds its input to fp16
@@ -156,6 +157,32 @@ def test_energy_forces_w16(golden, name):
     if name == "coil269_w16":
         fp = golden["flash"].case("coil269")
         assert rel_rmse(out.forces, fp["forces"]) <= 2e-3
+
+
+@pytest.mark.parametrize("fused,segred", [(False, False), (False, True), (True, False)])
+@pytest.mark.parametrize("name", ["small0", "small64", "coil269", "small_w16"])
+def test_pipeline_mode_ablations(golden, name, fused, segred):
+    # flash.py:446-501 routing: materialising schedules (scatter = the
+    # CGSchNet baseline, or segmented) run on the GPU in the input dtype;
+    # each reports the reference's modelled traffic for its schedule
+    c = golden["flash"].case(name)
+    params = params_for(c)
+    mode = P.PipelineMode(fused=fused, segred=segred)
+    out = P.flash_energy_forces(c["pos"], c["types"], params, mode)
+    if name.endswith("_w16"):
+        etol, ftol = W16_ENERGY_TOL, 5e-4
+    elif c["pos"].dtype == np.float64 and not fused:
+        etol, ftol = 1e-10, 1e-9
+    else:
+        etol, ftol = FP32_TOL, FP32_TOL
+    assert O.energy_rel_err(out.energy, float(c["energy"]), c["per_atom"]) <= etol
+    assert O.force_rel_err(out.forces, c["forces"]) <= ftol
+    assert out.forces.dtype == c["pos"].dtype
+    N, E = c["pos"].shape[0], int(P.build_neighbors_cells(c["pos"], params.config.cutoff).num_edges)
+    cfg = params.config
+    assert out.traffic.as_dict() == P.traffic_report(
+        mode, N, E, cfg.hidden_dim, cfg.rbf_dim, cfg.num_blocks, c["pos"].dtype.itemsize).as_dict()
+    assert (out.traffic.atomic_updates > 0) == (not segred and E > 0)
 
 
 def test_energy_forces_given_neighbor_list(golden):

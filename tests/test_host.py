@@ -229,3 +229,25 @@ def test_format_xyz_matches_reference_frame_format():
     assert _lib.format_xyz(pos, types, 987654321, 11) == ref
     assert _lib.format_xyz(pos, types, 987654321, 11, nthreads=1) == ref
     assert _lib.format_xyz(pos[:0], types, 0) == b""
+
+
+def test_traffic_report_matches_reference_schedules():
+    # traffic_report restates the four PipelineMode schedules' bookkeeping
+    # (flash.py:310-501, reference.py:100-209, traffic.py:80-182); the golden
+    # reports come from running the reference (tests/golden/make_traffic_golden.py)
+    import json
+    from oracle import flashcg_oracle as O
+    from paper_2602_13140_b200.inputs import generate_system
+    from paper_2602_13140_b200.modelparams import ModelConfig
+    from paper_2602_13140_b200.schnet import PipelineMode, traffic_report
+    from conftest import GOLDEN
+    cases = json.loads((GOLDEN / "traffic_modes.json").read_text())
+    assert len(cases) == 16
+    for c in cases:
+        cfg = ModelConfig(**c["cfg"])
+        sysm = generate_system(c["kind"], c["n"], c["seed"])
+        src, _ = O.neighbor_list(sysm.positions.astype(c["dtype"]), cfg.cutoff)
+        rep = traffic_report(PipelineMode(fused=c["fused"], segred=c["segred"]), c["n"],
+                             len(src), cfg.hidden_dim, cfg.rbf_dim, cfg.num_blocks,
+                             np.dtype(c["dtype"]).itemsize)
+        assert rep.as_dict() == c["traffic"], (c["kind"], c["dtype"], c["fused"], c["segred"])
