@@ -201,6 +201,8 @@ def main():
     ap.add_argument("--profile-steps", type=int, default=3)
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-gpu-baseline", action="store_true",
+                    help="skip the same-GPU materialising (CGSchNet-style) comparison")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -361,6 +363,9 @@ def main():
                    "peak_mem_bytes": int(peak_mem),
                    "flags": {k: flags[k] for k in ("overflow", "blowup", "max_degree")},
                    "energy_mean": float(energies.double().mean().item())}
+        if world == 1 and not args.no_gpu_baseline:
+            from paper_2602_13140_b200.ablation import compare_on_engine
+            sysline["gpu_materialized_baseline"] = compare_on_engine(eng, params)
         if world == 1 and not args.no_cpu_baseline:
             sysline["cpu_baseline"] = cpu_baseline(sysm, params, R)
         print(json.dumps(sysline), flush=True)

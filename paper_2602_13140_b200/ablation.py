@@ -134,7 +134,10 @@ def materialized_energy_forces(model: TorchModel, pos, types, ptr, nbr, own, R: 
                         0.5 * (torch.cos(math.pi * d / model.cutoff) + 1.0), torch.zeros_like(d))
         delta = d[:, None] - model.centers[None, :]
         basis = torch.exp(-model.gamma * delta * delta) * c[:, None]  # [E, Dr]
-        X = model.embedding[types.long()]
+        types = types.long()
+        if types.numel() == N and R > 1:  # per-bead types shared by the replicas
+            types = types.repeat(R)
+        X = model.embedding[types]
         if segred and _SEG is None:
             _SEG = _SegmentSum.make()
         ptr64 = ptr.long()
@@ -154,3 +157,61 @@ def materialized_energy_forces(model: TorchModel, pos, types, ptr, nbr, own, R: 
         return energy.detach(), per_atom.detach(), -grad
     finally:
         torch.backends.cuda.matmul.allow_tf32 = prev_tf32
+
+
+def compare_on_engine(eng, params, reps: int = 5) -> dict:
+    """Device time and peak memory of one energy+forces evaluation of the
+    engine's replica batch with the fused kernels (fcg_energy_forces) and
+    with the materialising schedules (scatter = CGSchNet, segmented), on the
+    same positions and CSR.  CUDA events around each call; the materialising
+    path's peak is measured above the memory already allocated."""
+    torch = _torch()
+    R, N = eng.R, eng.N
+    c = eng.csr
+    pos = eng.pos.reshape(R * N, 3)
+    stream = torch.cuda.current_stream()
+    L = _lib.load()
+    ef = L.fcg_ef_workspace_bytes(C.byref(eng.model.desc), R, N, c.cap_e)
+    ws = torch.empty(int(ef), dtype=torch.uint8, device=pos.device)
+    per_atom = torch.empty(R * N, dtype=torch.float32, device=pos.device)
+    energy = torch.empty(R, dtype=torch.float32, device=pos.device)
+    forces = torch.empty(R * N, 3, dtype=torch.float32, device=pos.device)
+    v = _lib.vp
+
+    def flash():
+        _lib.check(L.fcg_energy_forces(C.byref(eng.model.desc), v(pos), v(eng.types), R, N,
+                                       v(c.ptr), v(c.nbr), v(c.rev), v(c.own), c.cap_e,
+                                       v(per_atom), v(energy), v(forces), v(ws), ef,
+                                       C.c_void_p(stream.cuda_stream)), "fcg_energy_forces")
+
+    model = TorchModel(params, torch.float32)
+    E = int(c.ptr[-1].item())
+    nbr, own = c.nbr[:E], c.own[:E]
+
+    def mat(segred):
+        return lambda: materialized_energy_forces(model, pos, eng.types, c.ptr, nbr, own, R, N,
+                                                  segred)
+
+    def timed(fn):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        base = torch.cuda.memory_allocated()
+        torch.cuda.reset_peak_memory_stats()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(reps):
+            fn()
+        t1.record()
+        torch.cuda.synchronize()
+        return t0.elapsed_time(t1) / reps, torch.cuda.max_memory_allocated() - base
+
+    f_ms, f_mem = timed(flash)
+    s_ms, s_mem = timed(mat(False))
+    g_ms, g_mem = timed(mat(True))
+    return {"what": "one energy+forces evaluation of the replica batch, same positions and CSR",
+            "replicas": R, "edges": int(c.ptr[-1].item()),
+            "fused_ms": f_ms, "materialized_scatter_ms": s_ms, "materialized_segred_ms": g_ms,
+            "speedup_vs_scatter": s_ms / f_ms, "speedup_vs_segred": g_ms / f_ms,
+            "extra_peak_bytes": {"fused": int(f_mem), "materialized_scatter": int(s_mem),
+                                 "materialized_segred": int(g_mem)}}
