@@ -178,13 +178,19 @@ int fcg_group_by(const int64_t *key, int64_t E, int n, int64_t *ptr,
                  int64_t *perm, void *ws, size_t ws_bytes, void *stream);
 
 /* (d) CSR segment reduce, flash.py:109-135: out[s] = sum values[ptr[s]:ptr[s+1]]
- * (rows of width k, fp32), empty segments -> 0, no atomics. */
+ * (rows of width k), empty segments -> 0, no atomics, fixed summation order.
+ * Segments are cut into chunks of <= 256 rows reduced by separate CTAs and
+ * combined in chunk order (the reference's segment_split partials), so the
+ * cost does not depend on the degree distribution (bench.py:91-118).
+ * Workspace: fcg_segment_reduce_workspace_bytes (valid for both widths). */
+size_t fcg_segment_reduce_workspace_bytes(int64_t E, int k, int nseg);
 int fcg_segment_reduce(const float *values, int64_t E, int k,
-                       const int64_t *ptr, int nseg, float *out, void *stream);
+                       const int64_t *ptr, int nseg, float *out, void *ws,
+                       size_t ws_bytes, void *stream);
 
 int fcg_segment_reduce_f64(const double *values, int64_t E, int k,
-                           const int64_t *ptr, int nseg, double *out,
-                           void *stream);
+                           const int64_t *ptr, int nseg, double *out, void *ws,
+                           size_t ws_bytes, void *stream);
 
 /* ---------------------------------------------------------------------
  * (b)(c)(d)(e) energy and forces of the SchNet model, flash.py:446-501.

@@ -74,8 +74,11 @@ _SIGS = {
                                     _VP, _VP, _VP, _VP, C.c_size_t, _VP]),
     "fcg_group_workspace_bytes": (C.c_size_t, [C.c_int64, C.c_int]),
     "fcg_group_by": (C.c_int, [_VP, C.c_int64, C.c_int, _VP, _VP, _VP, C.c_size_t, _VP]),
-    "fcg_segment_reduce": (C.c_int, [_VP, C.c_int64, C.c_int, _VP, C.c_int, _VP, _VP]),
-    "fcg_segment_reduce_f64": (C.c_int, [_VP, C.c_int64, C.c_int, _VP, C.c_int, _VP, _VP]),
+    "fcg_segment_reduce_workspace_bytes": (C.c_size_t, [C.c_int64, C.c_int, C.c_int]),
+    "fcg_segment_reduce": (C.c_int, [_VP, C.c_int64, C.c_int, _VP, C.c_int, _VP, _VP,
+                                     C.c_size_t, _VP]),
+    "fcg_segment_reduce_f64": (C.c_int, [_VP, C.c_int64, C.c_int, _VP, C.c_int, _VP, _VP,
+                                         C.c_size_t, _VP]),
     "fcg_ef_workspace_bytes": (C.c_size_t, [C.POINTER(FcgModel), C.c_int, C.c_int, C.c_int64]),
     "fcg_energy_forces": (C.c_int, [C.POINTER(FcgModel), _VP, _VP, C.c_int, C.c_int, _VP, _VP,
                                     _VP, _VP, C.c_int64, _VP, _VP, _VP, _VP, C.c_size_t, _VP]),

@@ -95,7 +95,10 @@ class _SegmentSum:
                 fn = lib.fcg_segment_reduce_f64 if values.dtype == torch.float64 \
                     else lib.fcg_segment_reduce
                 v = values.contiguous()
+                wb = lib.fcg_segment_reduce_workspace_bytes(v.shape[0], k, nseg)
+                ws = torch.empty(int(wb), dtype=torch.uint8, device=values.device)
                 _lib.check(fn(_lib.vp(v), v.shape[0], k, _lib.vp(ptr64), nseg, _lib.vp(out),
+                              _lib.vp(ws), wb,
                               C.c_void_p(torch.cuda.current_stream().cuda_stream)),
                            "fcg_segment_reduce")
                 ctx.save_for_backward(own)

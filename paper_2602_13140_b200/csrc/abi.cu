@@ -117,14 +117,18 @@ int fcg_group_by(const int64_t *key, int64_t E, int n, int64_t *ptr, int64_t *pe
   return group_by(key, E, n, ptr, perm, ws, ws_bytes, (cudaStream_t)stream);
 }
 
+size_t fcg_segment_reduce_workspace_bytes(int64_t E, int k, int nseg) {
+  return segment_reduce_ws_bytes(E, k, nseg, sizeof(double));
+}
+
 int fcg_segment_reduce(const float *values, int64_t E, int k, const int64_t *ptr, int nseg,
-                       float *out, void *stream) {
-  return segment_reduce(values, E, k, ptr, nseg, out, (cudaStream_t)stream);
+                       float *out, void *ws, size_t ws_bytes, void *stream) {
+  return segment_reduce(values, E, k, ptr, nseg, out, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 int fcg_segment_reduce_f64(const double *values, int64_t E, int k, const int64_t *ptr, int nseg,
-                           double *out, void *stream) {
-  return segment_reduce_f64(values, E, k, ptr, nseg, out, (cudaStream_t)stream);
+                           double *out, void *ws, size_t ws_bytes, void *stream) {
+  return segment_reduce_f64(values, E, k, ptr, nseg, out, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 size_t fcg_ef_workspace_bytes(const fcg_model *m, int R, int N, int64_t cap_e) {

@@ -120,10 +120,11 @@ int nbr_build_f64(const double *pos, int R, int N, double r_cut, int64_t cap_e, 
 size_t group_ws_bytes(int64_t E, int n);
 int group_by(const int64_t *key, int64_t E, int n, int64_t *ptr, int64_t *perm, void *ws,
              size_t ws_bytes, cudaStream_t s);
+size_t segment_reduce_ws_bytes(int64_t E, int k, int nseg, size_t elem);
 int segment_reduce(const float *values, int64_t E, int k, const int64_t *ptr, int nseg,
-                   float *out, cudaStream_t s);
+                   float *out, void *ws, size_t ws_bytes, cudaStream_t s);
 int segment_reduce_f64(const double *values, int64_t E, int k, const int64_t *ptr, int nseg,
-                       double *out, cudaStream_t s);
+                       double *out, void *ws, size_t ws_bytes, cudaStream_t s);
 // model.cu
 size_t ef_ws_bytes(const fcg_model *m, int R, int N, int64_t cap_e);
 int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, int R, int N,

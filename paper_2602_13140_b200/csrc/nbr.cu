@@ -277,35 +277,202 @@ int group_by(const int64_t *key, int64_t E, int n, int64_t *ptr, int64_t *perm, 
 }
 
 // ---------------------------------------------------------------------------
-// (d) segment reduce, flash.py:109-135.  One thread per (segment, column),
-// summing its segment in order; a single writer per output element.
-template <typename T>
-__global__ void k_segment_reduce(const T *__restrict__ v, int k, const int64_t *__restrict__ ptr,
-                                 int nseg, T *__restrict__ out) {
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= (int64_t)nseg * k) return;
-  int sgm = (int)(t / k), col = (int)(t % k);
-  T acc = 0;
-  for (int64_t e = ptr[sgm]; e < ptr[sgm + 1]; ++e) acc += v[e * k + col];
-  out[(int64_t)sgm * k + col] = acc;
+// (d) segment reduce, flash.py:109-135: out[s] = sum of values[ptr[s]:ptr[s+1]]
+// (rows of width k), empty segments -> 0, no atomics, fixed summation order.
+//
+// Degree-skew robust (bench.py:91-118, test_acceptance.py:292-301): every
+// segment is cut into chunks of at most SEG_CHUNK rows (the reference's
+// segment_split partials, flash.py:130-134), one CTA per chunk, so a
+// power-law head segment spreads over many SMs.  Chunk c of segment s is
+// found from a device scan of the per-segment chunk counts; single-chunk
+// segments are written directly, longer ones through per-chunk partials
+// that a second kernel adds in chunk order.
+constexpr int SEG_CHUNK = 256;
+constexpr int SEG_THREADS = 256;
+
+__global__ void k_seg_chunks(const int64_t *__restrict__ ptr, int nseg, int64_t *__restrict__ cnt) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < nseg) {
+    long long len = ptr[s + 1] - ptr[s];
+    cnt[s] = (len + SEG_CHUNK - 1) / SEG_CHUNK;
+  } else if (s == nseg) {
+    cnt[s] = 0;
+  }
+}
+
+// One CTA per chunk.  Rows are read as VW-wide vectors (16-byte loads when
+// k % 4 == 0 for fp32): thread t owns vector column t % kv (kv = k / VW) and
+// the chunk rows t/kv, t/kv + 256/kv, ... with four independent
+// accumulators; the per-thread partials of a column are then added in
+// thread order (fixed order: deterministic).  Wider rows loop over column
+// blocks of 256 vectors.
+template <typename T, int VW>
+struct SegVec {
+  T x[VW];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int i = 0; i < VW; ++i) x[i] = 0;
+  }
+  __device__ __forceinline__ void add(const SegVec &o) {
+#pragma unroll
+    for (int i = 0; i < VW; ++i) x[i] += o.x[i];
+  }
+};
+
+template <typename T, int VW>
+__global__ void __launch_bounds__(SEG_THREADS)
+k_seg_chunk_reduce(const T *__restrict__ v, int k, const int64_t *__restrict__ ptr, int nseg,
+                   const int64_t *__restrict__ cstart, T *__restrict__ out,
+                   T *__restrict__ partial) {
+  using V = SegVec<T, VW>;
+  __shared__ V red[SEG_THREADS];
+  __shared__ int s_seg;
+  const long long c = blockIdx.x;
+  if (c >= cstart[nseg]) return;
+  if (threadIdx.x == 0) {  // segment of chunk c: last s with cstart[s] <= c
+    int lo = 0, hi = nseg - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (cstart[mid] <= c) lo = mid; else hi = mid - 1;
+    }
+    s_seg = lo;
+  }
+  __syncthreads();
+  const int sg = s_seg;
+  const long long j = c - cstart[sg];
+  const long long n_chunks = cstart[sg + 1] - cstart[sg];
+  const long long e0 = ptr[sg] + j * SEG_CHUNK;
+  const long long e1 = min((long long)ptr[sg + 1], e0 + SEG_CHUNK);
+  const int kvec = k / VW;
+  const V *vv = (const V *)v;
+  for (int c0 = 0; c0 < kvec; c0 += SEG_THREADS) {
+    const int kk = min(SEG_THREADS, kvec - c0);
+    const int lanes = SEG_THREADS / kk;  // edge strides per vector column
+    const int col = threadIdx.x % kk, sub = threadIdx.x / kk;
+    V a0, a1, a2, a3;
+    a0.zero(); a1.zero(); a2.zero(); a3.zero();
+    if (sub < lanes) {
+      long long e = e0 + sub;
+      for (; e + 3 * lanes < e1; e += 4 * lanes) {
+        a0.add(vv[e * kvec + c0 + col]);
+        a1.add(vv[(e + lanes) * kvec + c0 + col]);
+        a2.add(vv[(e + 2 * lanes) * kvec + c0 + col]);
+        a3.add(vv[(e + 3 * lanes) * kvec + c0 + col]);
+      }
+      for (; e < e1; e += lanes) a0.add(vv[e * kvec + c0 + col]);
+    }
+    a0.add(a1);
+    a2.add(a3);
+    a0.add(a2);
+    red[threadIdx.x] = a0;
+    __syncthreads();
+    if (threadIdx.x < kk) {
+      V tot;
+      tot.zero();
+      for (int q = 0; q < lanes; ++q) tot.add(red[q * kk + threadIdx.x]);
+      V *dst = n_chunks == 1 ? (V *)out + (long long)sg * kvec : (V *)partial + c * kvec;
+      dst[c0 + threadIdx.x] = tot;
+    }
+    __syncthreads();
+  }
+}
+
+// Second level, one CTA per segment: multi-chunk segments sum their chunk
+// partials (rows cstart[s]..cstart[s+1] of `partial`) with the same strided
+// scheme; empty segments get zeros; single-chunk ones are already written.
+template <typename T, int VW>
+__global__ void __launch_bounds__(SEG_THREADS)
+k_seg_combine(int k, int nseg, const int64_t *__restrict__ cstart, const T *__restrict__ partial,
+              T *__restrict__ out) {
+  using V = SegVec<T, VW>;
+  __shared__ V red[SEG_THREADS];
+  const int sg = blockIdx.x;
+  const long long r0 = cstart[sg], r1 = cstart[sg + 1];
+  if (r1 - r0 == 1) return;
+  const int kvec = k / VW;
+  const V *pv = (const V *)partial;
+  V *ov = (V *)out + (long long)sg * kvec;
+  for (int c0 = 0; c0 < kvec; c0 += SEG_THREADS) {
+    const int kk = min(SEG_THREADS, kvec - c0);
+    const int lanes = SEG_THREADS / kk;
+    const int col = threadIdx.x % kk, sub = threadIdx.x / kk;
+    V a0, a1;
+    a0.zero(); a1.zero();
+    if (sub < lanes) {
+      long long r = r0 + sub;
+      for (; r + lanes < r1; r += 2 * lanes) {
+        a0.add(pv[r * kvec + c0 + col]);
+        a1.add(pv[(r + lanes) * kvec + c0 + col]);
+      }
+      for (; r < r1; r += lanes) a0.add(pv[r * kvec + c0 + col]);
+    }
+    a0.add(a1);
+    red[threadIdx.x] = a0;
+    __syncthreads();
+    if (threadIdx.x < kk) {
+      V tot;
+      tot.zero();
+      for (int q = 0; q < lanes; ++q) tot.add(red[q * kk + threadIdx.x]);
+      ov[c0 + threadIdx.x] = tot;
+    }
+    __syncthreads();
+  }
+}
+
+static size_t seg_cub_bytes(int nseg) {
+  size_t b = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, b, (int64_t *)nullptr, (int64_t *)nullptr, nseg + 1);
+  return b;
+}
+
+size_t segment_reduce_ws_bytes(int64_t E, int k, int nseg, size_t elem) {
+  Carver c(nullptr, 0);
+  c.take<int64_t>((size_t)nseg + 1);                       // chunk counts
+  c.take<int64_t>((size_t)nseg + 1);                       // chunk starts
+  c.take<char>(seg_cub_bytes(nseg));                       // scan scratch
+  c.take<char>(elem * (size_t)(E / SEG_CHUNK + nseg + 1) * (size_t)(k > 0 ? k : 1));  // partials
+  return c.off + 256;
 }
 
 template <typename T>
 int segment_reduce_t(const T *values, int64_t E, int k, const int64_t *ptr, int nseg, T *out,
-                     cudaStream_t s) {
-  if (k < 1 || nseg < 0) { set_error("segment_reduce: bad shape"); return FCG_ERR_ARG; }
+                     void *ws, size_t ws_bytes, cudaStream_t s) {
+  if (k < 1 || nseg < 0 || E < 0) { set_error("segment_reduce: bad shape"); return FCG_ERR_ARG; }
   if (nseg == 0) return FCG_OK;
-  long long tot = (long long)nseg * k;
-  k_segment_reduce<<<ceil_div(tot, 256), 256, 0, s>>>(values, k, ptr, nseg, out);
+  Carver c(ws, ws_bytes);
+  int64_t *cnt = c.take<int64_t>((size_t)nseg + 1);
+  int64_t *cstart = c.take<int64_t>((size_t)nseg + 1);
+  size_t cub_b = seg_cub_bytes(nseg);
+  void *cub_tmp = c.take<char>(cub_b);
+  T *partial = (T *)c.take<char>(sizeof(T) * (size_t)(E / SEG_CHUNK + nseg + 1) * (size_t)k);
+  if (!ws || !c.ok()) { set_error("segment_reduce: workspace too small"); return FCG_ERR_ARG; }
+  k_seg_chunks<<<ceil_div((long long)nseg + 1, 256), 256, 0, s>>>(ptr, nseg, cnt);
+  cub::DeviceScan::ExclusiveSum(cub_tmp, cub_b, cnt, cstart, nseg + 1, s);
+  // upper bound of the chunk count: sum of ceil(len/C) <= E/C + nseg
+  const long long max_chunks = E / SEG_CHUNK + nseg;
+  const bool vec4 = sizeof(T) == 4 && k % 4 == 0 && ((uintptr_t)values % 16) == 0 &&
+                    ((uintptr_t)out % 16) == 0 && ((uintptr_t)partial % 16) == 0;
+  if (max_chunks > 0) {
+    if (vec4)
+      k_seg_chunk_reduce<T, 4><<<(unsigned)max_chunks, SEG_THREADS, 0, s>>>(
+          values, k, ptr, nseg, cstart, out, partial);
+    else
+      k_seg_chunk_reduce<T, 1><<<(unsigned)max_chunks, SEG_THREADS, 0, s>>>(
+          values, k, ptr, nseg, cstart, out, partial);
+  }
+  if (vec4)
+    k_seg_combine<T, 4><<<nseg, SEG_THREADS, 0, s>>>(k, nseg, cstart, partial, out);
+  else
+    k_seg_combine<T, 1><<<nseg, SEG_THREADS, 0, s>>>(k, nseg, cstart, partial, out);
   return cuda_status("segment_reduce");
 }
 int segment_reduce(const float *values, int64_t E, int k, const int64_t *ptr, int nseg,
-                   float *out, cudaStream_t s) {
-  return segment_reduce_t(values, E, k, ptr, nseg, out, s);
+                   float *out, void *ws, size_t ws_bytes, cudaStream_t s) {
+  return segment_reduce_t(values, E, k, ptr, nseg, out, ws, ws_bytes, s);
 }
 int segment_reduce_f64(const double *values, int64_t E, int k, const int64_t *ptr, int nseg,
-                       double *out, cudaStream_t s) {
-  return segment_reduce_t(values, E, k, ptr, nseg, out, s);
+                       double *out, void *ws, size_t ws_bytes, cudaStream_t s) {
+  return segment_reduce_t(values, E, k, ptr, nseg, out, ws, ws_bytes, s);
 }
 
 }  // namespace fcg

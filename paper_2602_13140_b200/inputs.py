@@ -107,3 +107,21 @@ def generate_system(kind: str, n: int, seed: int, bonded: bool = True) -> System
     return SystemSpec(types=types, masses=np.full(n, DEFAULT_MASS),
                       prior=chain_prior(n) if bonded and n > 1 else None,
                       positions=pos, native=pos.copy())
+
+
+def skewed_segments(n_segments: int, n_edges: int, kind: str):
+    """Segment-size layouts for degree-skew experiments at a fixed edge count
+    (systems.py:202-221): "uniform" spreads edges evenly, "powerlaw" gives
+    Zipf(1.1) sizes with the remainder on the head.  Returns (ptr, dst)."""
+    if kind == "uniform":
+        sizes = np.full(n_segments, n_edges // n_segments, dtype=np.int64)
+        sizes[:n_edges % n_segments] += 1
+    elif kind == "powerlaw":
+        w = 1.0 / np.arange(1, n_segments + 1, dtype=np.float64) ** 1.1
+        sizes = np.floor(w / w.sum() * n_edges).astype(np.int64)
+        sizes[0] += n_edges - sizes.sum()
+    else:
+        raise ValueError(f"unknown layout kind {kind!r}")
+    ptr = np.zeros(n_segments + 1, dtype=np.int64)
+    np.cumsum(sizes, out=ptr[1:])
+    return ptr, np.repeat(np.arange(n_segments, dtype=np.int64), sizes)

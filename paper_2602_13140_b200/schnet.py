@@ -200,8 +200,11 @@ def segment_reduce(values: np.ndarray, ptr: np.ndarray, split: int = DEFAULT_SEG
     dptr = torch.as_tensor(ptr).cuda()
     out = torch.empty(nseg * k, dtype=dv.dtype, device="cuda")
     fn = lib.fcg_segment_reduce_f64 if f64 else lib.fcg_segment_reduce
+    wb = lib.fcg_segment_reduce_workspace_bytes(values.shape[0], k, nseg)
+    ws = torch.empty(int(wb), dtype=torch.uint8, device="cuda")
     _lib.check(fn(_lib.vp(dv), values.shape[0], k, _lib.vp(dptr), nseg, _lib.vp(out),
-                  C.c_void_p(torch.cuda.current_stream().cuda_stream)), "fcg_segment_reduce")
+                  _lib.vp(ws), wb, C.c_void_p(torch.cuda.current_stream().cuda_stream)),
+               "fcg_segment_reduce")
     return out.cpu().numpy().reshape(out_shape)
 
 

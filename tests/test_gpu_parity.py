@@ -534,3 +534,21 @@ def test_large_system_sweep(kind, n, rc, bonded):
     assert eng.flags()["max_degree"] >= 40
     eng.run(3, graph_steps=3)
     assert not eng.flags()["blowup"]
+
+
+def test_segment_reduce_power_law_parity_and_skew_robustness():
+    # chunked segment reduce: a Zipf head segment of ~30k rows sums like the
+    # oracle, and uniform vs power-law layouts at fixed E cost the same
+    # within the reference's 25% bound (test_acceptance.py:292-301)
+    from paper_2602_13140_b200.benchmarks import degree_skew_report
+    from paper_2602_13140_b200.inputs import skewed_segments
+    rng = np.random.default_rng(1)
+    ptr, _ = skewed_segments(2000, 200_000, "powerlaw")
+    assert ptr[1] > 20_000
+    v = rng.standard_normal((200_000, 3))
+    np.testing.assert_allclose(P.segment_reduce(v, ptr), O.segment_sum(v, ptr), rtol=1e-9,
+                               atol=1e-9)
+    v32 = v.astype(np.float32)
+    np.testing.assert_array_equal(P.segment_reduce(v32, ptr), P.segment_reduce(v32, ptr))
+    rep = degree_skew_report(n_segments=2000, e=200_000, d=64, repeats=5, seed=0)
+    assert rep["segment_reduce_variation"] <= 0.25, rep
