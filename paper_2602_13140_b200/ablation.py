@@ -218,3 +218,46 @@ def compare_on_engine(eng, params, reps: int = 5) -> dict:
             "speedup_vs_scatter": s_ms / f_ms, "speedup_vs_segred": g_ms / f_ms,
             "extra_peak_bytes": {"fused": int(f_mem), "materialized_scatter": int(s_mem),
                                  "materialized_segred": int(g_mem)}}
+
+
+class MaterializedReplicaForces:
+    """force_fn(positions[R,N,3], step) -> (forces, {"potential", "prior"})
+    with the materialising schedule (the reference's _ReplicaForces under a
+    fused=False backend, md.py:231-273): device neighbour build, GPU
+    materialised model forces, device harmonic prior."""
+
+    def __init__(self, params, types, prior, config, segred: bool):
+        from .prior import DevicePrior
+        torch = _torch()
+        self.torch, self.params, self.config, self.segred = torch, params, config, segred
+        self.types = torch.as_tensor(np.asarray(types).astype(np.int64)).cuda()
+        self.N = int(np.asarray(types).size)
+        self.prior = DevicePrior(prior, self.N)
+        self.model = TorchModel(params, torch.float32)
+        self.edge_counts = []
+        self._csr = None
+
+    def __call__(self, positions, step):
+        from .csr import device_csr
+        torch = self.torch
+        pos = np.asarray(positions, np.float32)
+        R, N = pos.shape[0], pos.shape[1]
+        if self._csr is None or step % max(self.config.neighbor_stride, 1) == 0:  # md.py:245
+            p, nbr, _rev, own = device_csr(pos, self.model.cutoff)
+            self._csr = tuple(torch.as_tensor(a).cuda() for a in (p, nbr, own))
+            counts = p[N::N] - p[0:-1:N][:R]
+            self._counts = [int(x) for x in counts]
+        self.edge_counts.extend(self._counts)
+        ptr, nbr, own = self._csr
+        dpos = torch.as_tensor(pos).cuda()
+        e, _pa, f = materialized_energy_forces(self.model, dpos.reshape(R * N, 3), self.types,
+                                               ptr, nbr, own, R, N, self.segred)
+        e_prior = torch.empty(R, device="cuda")
+        f_prior = torch.empty(R, N, 3, device="cuda")
+        _lib.check(_lib.load().fcg_prior_forces(C.byref(self.prior.desc), _lib.vp(dpos), R, N,
+                                                _lib.vp(e_prior), _lib.vp(f_prior),
+                                                C.c_void_p(torch.cuda.current_stream().cuda_stream)),
+                   "fcg_prior_forces")
+        forces = (f.reshape(R, N, 3).float() + f_prior).cpu().numpy()
+        return forces, {"potential": e.double().cpu().numpy(),
+                        "prior": e_prior.double().cpu().numpy()}

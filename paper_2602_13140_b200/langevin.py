@@ -314,6 +314,8 @@ def run_simulation(params, system, config: SimConfig, out_dir, resume_from=None,
     from . import checkpoint as params_io
 
     _require_fp32(config)
+    if not config.backend.fused:
+        return _run_simulation_materialized(params, system, config, out_dir, resume_from)
     out_dir = Path(out_dir)
     out_dir.mkdir(parents=True, exist_ok=True)
     masses = np.asarray(system.masses, np.float64)
@@ -425,6 +427,69 @@ def run_simulation(params, system, config: SimConfig, out_dir, resume_from=None,
                      final_state=SimState(positions=pos, velocities=vel, masses=masses, step=step),
                      traffic=traffic,
                      mean_edges=edge_total[0] / edge_total[1] if edge_total[1] else 0.0)
+
+
+def _run_simulation_materialized(params, system, config: SimConfig, out_dir, resume_from=None):
+    """run_simulation under a fused=False backend (the reference's ablation
+    cells, bench.py:121-192): the reference observer loop over integrate()
+    with the GPU integrator and GPU materialising forces (ablation.py)."""
+    from . import checkpoint as params_io
+    from .ablation import MaterializedReplicaForces
+
+    out_dir = Path(out_dir)
+    out_dir.mkdir(parents=True, exist_ok=True)
+    masses = np.asarray(system.masses, np.float64)
+    if resume_from is not None:
+        chk = params_io.load_checkpoint(resume_from)
+        pos0, vel0 = chk["positions"].astype(np.float32), chk["velocities"].astype(np.float32)
+        masses, step0 = chk["masses"].astype(np.float64), int(chk["step"])
+    else:
+        r0 = system.initial_positions()
+        pos0 = np.repeat(r0[None, :, :], config.n_replicas, axis=0).astype(np.float32)
+        vel0, step0 = np.zeros_like(pos0), 0
+    state = SimState(positions=pos0, velocities=vel0, masses=masses, step=step0)
+    provider = MaterializedReplicaForces(params, system.types, system.prior, config,
+                                         segred=config.backend.segred)
+    traj_path, scal_path = out_dir / "trajectory.xyz", out_dir / "scalars.csv"
+    traj = open(traj_path, "wb")
+    scal = open(scal_path, "w")
+    scal.write("# flashcg-scalars v1\n" + SCALARS_SCHEMA + "\n")
+    t_start = time.perf_counter()
+    last = [t_start]
+
+    def observer(st, forces, info, initial):  # md.py:312-326
+        now = time.perf_counter()
+        wall_ms = (now - last[0]) * 1e3
+        last[0] = now
+        if config.checkpoint_step is not None and st.step == config.checkpoint_step \
+                and config.checkpoint_path:
+            params_io.save_checkpoint(config.checkpoint_path, st.positions, st.velocities,
+                                      st.masses, st.step, config.seed)
+        if not (initial or st.step % max(config.output_stride, 1) == 0):
+            return
+        kin = kinetic_temperature(st)
+        traj.write(_lib.format_xyz(st.positions, system.types, st.step))
+        scal.write("".join(f"{st.step},{rep},{info['potential'][rep]:.10g},"
+                           f"{info['prior'][rep]:.10g},{kin[rep]:.10g},{wall_ms:.3f}\n"
+                           for rep in range(st.n_replicas)))
+
+    try:
+        state = integrate(provider, state, config, observer=observer)
+    except SimulationBlowupError:  # md.py:330-339 (dumps the state it holds)
+        dump = out_dir / "blowup.xyz"
+        with open(dump, "wb") as f:
+            f.write(_lib.format_xyz(state.positions, system.types, state.step))
+        raise SimulationBlowupError(
+            f"simulation blew up at step {state.step}; diagnostic frame in {dump}")
+    finally:
+        traj.close()
+        scal.close()
+    wall = time.perf_counter() - t_start
+    counts = provider.edge_counts
+    return RunResult(trajectory_path=traj_path, scalars_path=scal_path, steps=config.n_steps,
+                     replicas=state.n_replicas, wall_seconds=wall, dt_fs=config.dt_fs,
+                     final_state=state, traffic=TrafficReport(),
+                     mean_edges=float(np.mean(counts)) if counts else 0.0)
 
 
 def throughput_report(result: RunResult) -> dict:

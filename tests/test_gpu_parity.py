@@ -552,3 +552,28 @@ def test_segment_reduce_power_law_parity_and_skew_robustness():
     np.testing.assert_array_equal(P.segment_reduce(v32, ptr), P.segment_reduce(v32, ptr))
     rep = degree_skew_report(n_segments=2000, e=200_000, d=64, repeats=5, seed=0)
     assert rep["segment_reduce_variation"] <= 0.25, rep
+
+
+def test_run_simulation_materialized_backend_and_bench_csv(tmp_path, golden):
+    # SimConfig.backend with fused=False: the reference's ablation cell runs
+    # the materialising schedule (md.py + flash.py:310-370); same trajectory
+    # as the fused engine within fp32 round-off; run_bench writes the
+    # reference's bench CSV (bench.py:22-28, :121-192)
+    from paper_2602_13140_b200.benchmarks import BENCH_SCHEMA, run_bench, write_bench_csv
+    c = golden["md"].case("traj_tiny")
+    n, sseed, pseed, R, steps = (int(x) for x in c["meta"])
+    sysm = generate_system("coil", n, sseed)
+    params = init_params(ModelConfig(**json.loads(str(c["cfg"]))), pseed)
+    sim = P.SimConfig(dt_fs=4.0, n_steps=steps, n_replicas=R, seed=9, output_stride=5,
+                      backend=P.PipelineMode(fused=False, segred=False))
+    res = P.run_simulation(params, sysm, sim, tmp_path / "mat")
+    assert np.max(np.abs(res.final_state.positions - c["pos"])) <= 1e-5
+    assert res.trajectory_path.read_text().count("step=") == R * (steps // 5 + 1)
+    assert abs(res.mean_edges - float(c["mean_edges"])) <= 1e-9
+    rows = run_bench(params, sysm, {"name": "tiny", "out": str(tmp_path / "b")}, [2],
+                     [(False, False, False), (True, True, False)], steps=3)
+    write_bench_csv(rows, tmp_path / "bench.csv")
+    lines = (tmp_path / "bench.csv").read_text().splitlines()
+    assert lines[0] == "# flashcg-bench v1" and lines[1] == BENCH_SCHEMA and len(lines) == 4
+    assert rows[0]["speedup_vs_reference"] == 1.0 and rows[1]["io_ratio"] > 1.0
+    assert min(r["peak_edge_alloc_bytes"] for r in rows) >= 0
