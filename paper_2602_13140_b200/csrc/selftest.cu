@@ -51,7 +51,8 @@ k_selftest_mma(const uint16_t *A, const uint16_t *B, float *dump, int M, int N, 
   __shared__ uint64_t bar;
   __shared__ uint32_t tmem_base;
   uint8_t *As = sm, *Bs = sm + M * K * 2;
-  st_fill(oa, A, M, K, As);
+  const bool a_tmem = oa.core_rows_fastest == 2;  // A operand from TMEM (M = 128)
+  if (!a_tmem) st_fill(oa, A, M, K, As);
   st_fill(ob, B, N, K, Bs);
   tc::fence_async_smem();
   if (threadIdx.x == 0) {
@@ -63,10 +64,31 @@ k_selftest_mma(const uint16_t *A, const uint16_t *B, float *dump, int M, int N, 
   __syncthreads();
   tc::fence_after_sync();
   uint32_t tbase = tmem_base;
+  const uint32_t a_col = 128;  // A in TMEM columns [128, 128 + K/2)
+  if (a_tmem) {
+    // lane m = row m; column j packs (A[m][2j], A[m][2j+1])
+    const int m = threadIdx.x;
+    for (int j0 = 0; j0 < K / 2; j0 += 16) {
+      float v[16];
+      for (int j = 0; j < 16; ++j) {
+        uint32_t lo = A[m * K + 2 * (j0 + j)], hi = A[m * K + 2 * (j0 + j) + 1];
+        v[j] = __uint_as_float(lo | (hi << 16));
+      }
+      tc::tmem_st16(tbase + ((uint32_t)(32 * (threadIdx.x >> 5)) << 16) + a_col + j0, v);
+    }
+    tc::tmem_st_wait();
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+  }
   if (threadIdx.x == 0) {
-    uint32_t idesc = tc::idesc_f16(M, N, oa.mn_major, ob.mn_major);
+    uint32_t idesc = tc::idesc_f16(M, N, a_tmem ? 0 : oa.mn_major, ob.mn_major);
     for (int k0 = 0; k0 < K; k0 += 16) {
-      tc::mma_f16_ss(tbase, st_desc(oa, As, M, K, k0), st_desc(ob, Bs, N, K, k0), idesc, k0 > 0);
+      if (a_tmem)
+        tc::mma_f16_ts(tbase, tbase + a_col + k0 / 2, st_desc(ob, Bs, N, K, k0), idesc, k0 > 0);
+      else
+        tc::mma_f16_ss(tbase, st_desc(oa, As, M, K, k0), st_desc(ob, Bs, N, K, k0), idesc,
+                       k0 > 0);
     }
     tc::mma_commit(&bar);
   }
@@ -90,7 +112,8 @@ extern "C" int fcg_selftest_mma(const uint16_t *A, const uint16_t *B, float *dum
                                 int K, int a_mn, int a_order, int a_swap, int b_mn, int b_order,
                                 int b_swap, void *stream) {
   using namespace fcg;
-  if ((M != 64 && M != 128) || N % 16 || N < 16 || N > 256 || K % 16 || K > 256) {
+  if ((M != 64 && M != 128) || N % 16 || N < 16 || N > 256 || K % 16 || K > 256 ||
+      (a_order == 2 && (M != 128 || N > 128 || K > 256))) {
     set_error("selftest_mma: unsupported shape");
     return FCG_ERR_ARG;
   }

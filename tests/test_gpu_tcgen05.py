@@ -14,7 +14,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def _run(M, N, K, a_mn, b_mn, seed=0):
+def _run(M, N, K, a_mn, b_mn, seed=0, a_order=0):
     import torch
     from paper_2602_13140_b200 import _lib
     rng = np.random.default_rng(seed)
@@ -25,8 +25,8 @@ def _run(M, N, K, a_mn, b_mn, seed=0):
     dump = torch.zeros(128, N, dtype=torch.float32, device="cuda")
     lib = _lib.load()
     # swap=1 on an MN-major operand selects LBO=K stride / SBO=MN stride
-    _lib.check(lib.fcg_selftest_mma(_lib.vp(dA), _lib.vp(dB), _lib.vp(dump), M, N, K, a_mn, 0,
-                                    a_mn, b_mn, 0, b_mn,
+    _lib.check(lib.fcg_selftest_mma(_lib.vp(dA), _lib.vp(dB), _lib.vp(dump), M, N, K, a_mn,
+                                    a_order, a_mn, b_mn, 0, b_mn,
                                     C.c_void_p(torch.cuda.current_stream().cuda_stream)))
     torch.cuda.synchronize()
     return A.astype(np.float64) @ B.astype(np.float64).T, dump.cpu().numpy()
@@ -44,3 +44,12 @@ def test_m64_lane_map(a_mn, b_mn):
     ref, dump = _run(64, 128, 128, a_mn, b_mn)
     lanes = [32 * (m // 16) + m % 16 for m in range(64)]
     np.testing.assert_array_equal(dump[lanes], ref)
+
+
+@pytest.mark.parametrize("b_mn", [0, 1])
+@pytest.mark.parametrize("N", [32, 128])
+def test_a_operand_in_tmem(b_mn, N):
+    # kind::f16 with A from TMEM (K-major): row m in lane m, element k in
+    # column k/2, low half for even k
+    ref, dump = _run(128, N, 128, 0, b_mn, a_order=2)
+    np.testing.assert_array_equal(dump, ref)
