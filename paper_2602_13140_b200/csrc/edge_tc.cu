@@ -269,7 +269,7 @@ struct Wctx {
     __syncwarp();                                     \
   } while (0)
 
-__device__ __forceinline__ Wctx make_wctx(uint8_t *sm, TcShared *sh) {
+__device__ __forceinline__ Wctx make_wctx(uint8_t *sm, TcShared *sh, uint32_t gcols = 128u) {
   Wctx W;
   // warp index through a shuffle: the compiler then knows it (and every
   // address derived from it) is warp-uniform, so MMA descriptors stay in
@@ -284,15 +284,17 @@ __device__ __forceinline__ Wctx make_wctx(uint8_t *sm, TcShared *sh) {
   W.hb = W.bb + BB_BYTES;
   W.sbb = tc::smem_u32(W.bb);
   W.shb = tc::smem_u32(W.hb);
-  W.tmem_g = sh->tmem + 128u * W.g;
+  W.tmem_g = sh->tmem + gcols * W.g;
   W.tl = W.tmem_g + ((uint32_t)(32 * W.q) << 16);
   return W;
 }
 
 // The resident filter weights are staged by the TMA engine (cp.async.bulk);
-// every warp waits on wbar once before its first GEMM request.
+// every warp waits on wbar once before its first GEMM request.  kSmemW=false
+// (forward): the weights live in TMEM instead (load_weights_tmem).
+template <bool kSmemW = true>
 __device__ __forceinline__ void kernel_prologue(uint8_t *sm, TcShared *sh, const fcg_block &b) {
-  if (threadIdx.x == 0) {
+  if (kSmemW && threadIdx.x == 0) {
     tc::mbar_init(&sh->wbar, 1);
     tc::fence_mbar_init();
     tc::mbar_expect_tx(&sh->wbar, 2 * W0_BYTES + 2 * W1_BYTES);
@@ -313,6 +315,55 @@ __device__ __forceinline__ void kernel_prologue(uint8_t *sm, TcShared *sh, const
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
+}
+
+// ---- weights as the TMEM-resident A operand (forward) ---------------------------
+// Columns [TW0, TW0+64): W0 hi | lo (K=64: 32 columns each); [TW1, TW1+128):
+// W1 hi | lo (K=128).  Row m of a weight lives in lane m, element k in
+// column k/2 (pinned by tests/test_gpu_tcgen05.py::test_a_operand_in_tmem),
+// so an MMA reads its A slice from TMEM and only B (1 KB per MMA) from
+// shared memory, instead of 4 KB of A + 1 KB of B.
+constexpr uint32_t FWD_GCOLS = 64;  // forward groups: slots S0, S1 only
+constexpr uint32_t TW0 = NGRP * FWD_GCOLS, TW1 = TW0 + 64;
+static_assert(TW1 + 128 <= 512, "TMEM budget");
+
+// One image row (core-matrix order, element (r,c) at ((r/8)*(in/8)+c/8)*64 +
+// (r%8)*8 + c%8) -> this lane's TMEM row.  Warp w loads image (w / 4) % 4.
+__device__ __forceinline__ void load_weights_tmem(const fcg_block &b, uint32_t tmem) {
+  const int w = threadIdx.x >> 5, q = w & 3, lane = threadIdx.x & 31, m = 32 * q + lane;
+  const int img = (w >> 2) & 3;  // 0: W0 hi, 1: W0 lo, 2: W1 hi, 3: W1 lo
+  const int K = img < 2 ? DR : D;
+  const uint16_t *base = img < 2 ? b.f0_img + (img & 1) * (D * DR) : b.f1_img + (img & 1) * (D * D);
+  const uint32_t col = img < 2 ? TW0 + (img & 1) * (DR / 2) : TW1 + (img & 1) * (D / 2);
+  const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + col;
+#pragma unroll 1
+  for (int j0 = 0; j0 < K / 8; j0 += 4) {  // 4 chunks of 8 halves = 16 columns
+    float v[16];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint4 u = __ldg((const uint4 *)(base + ((m / 8) * (K / 8) + j0 + j) * 64 + (m % 8) * 8));
+      v[4 * j] = __uint_as_float(u.x); v[4 * j + 1] = __uint_as_float(u.y);
+      v[4 * j + 2] = __uint_as_float(u.z); v[4 * j + 3] = __uint_as_float(u.w);
+    }
+    tc::tmem_st16(taddr + j0 * 4, v);
+  }
+  tc::tmem_st_wait();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+}
+
+// D (+)= A(TMEM columns a_hi / a_lo) x B over KS k-steps (8 A columns each)
+template <int KS, int NP>
+__device__ __forceinline__ void mma_chain_ts(uint32_t d, uint32_t a_hi, uint32_t a_lo, Desc b,
+                                             uint32_t idesc) {
+#pragma unroll 1
+  for (int k = 0; k < KS; ++k) {
+    tc::mma_f16_ts_warp(d, a_hi + 8 * k, b.hi, idesc, k > 0);
+    if (NP >= 2) tc::mma_f16_ts_warp(d, a_hi + 8 * k, b.lo, idesc, 1);
+    if (NP >= 3) tc::mma_f16_ts_warp(d, a_lo + 8 * k, b.hi, idesc, 1);
+    b.hi += b.step; b.lo += b.step;
+  }
 }
 
 // Raw per-edge metadata of one tile, one lane per edge, held in registers a
@@ -464,12 +515,12 @@ k_edge_fwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
   extern __shared__ __align__(1024) uint8_t sm[];
   TcShared *sh = (TcShared *)(sm + SM_META);
   const fcg_block &B = a.blk;
-  kernel_prologue(sm, sh, B);
-  const Wctx W = make_wctx(sm, sh);
-  const uint32_t sbase = tc::smem_u32(sm);
+  kernel_prologue<false>(sm, sh, B);
+  load_weights_tmem(B, sh->tmem);
+  const Wctx W = make_wctx(sm, sh, FWD_GCOLS);
   const uint32_t idesc = tc::idesc_f16(128, TT, 0, 1);
   constexpr int NP = Q ? 1 : 3;
-  const Desc w0 = wdesc_k(sbase + SM_W0, DR, W0_BYTES), w1 = wdesc_k(sbase + SM_W1, D, W1_BYTES);
+  const uint32_t w0h = sh->tmem + TW0, w0l = w0h + DR / 2, w1h = sh->tmem + TW1, w1l = w1h + D / 2;
   const Desc bb = adesc(W.sbb, DR), hb = adesc(W.shb, D);
 
   const UnitRange tr = unit_range(a, unit_rows, NGRP * blockIdx.x + W.g);
@@ -502,7 +553,7 @@ k_edge_fwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
       W.wait(BAR_G1, it);
       PHASE(0, it, 1);
       tile_h<Q, false>(W, rs0, b0c, hs);
-      REQ(BAR_G2, (mma_chain<D / 16, NP>(W.tmem_g + S1, w1, hb, idesc)));
+      REQ(BAR_G2, (mma_chain_ts<D / 16, NP>(W.tmem_g + S1, w1h, w1l, hb, idesc)));
       PHASE(0, it, 2);
       if (more) {
         bool r2;
@@ -512,8 +563,7 @@ k_edge_fwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
     }
     if (more) {  // basis + G1 of the next tile overlap G2
       tile_basis<false, Q>(a, W, W.meta(it + 1), bsc);
-      if (it < 0) tc::mbar_wait(&sh->wbar, 0);  // weights resident before the first GEMM
-      REQ(BAR_G1, (mma_chain<DR / 16, NP>(W.tmem_g + S0, w0, bb, idesc)));
+      REQ(BAR_G1, (mma_chain_ts<DR / 16, NP>(W.tmem_g + S0, w0h, w0l, bb, idesc)));
     }
     PHASE(0, it, 3);
     if (it >= 0) {
