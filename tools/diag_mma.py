@@ -1,4 +1,5 @@
-"""MMA issue->commit and completion timing of CTA 0 / group 0 (diagnostic build)."""
+"""Cycles the issuing warp spends in each tcgen05.mma chain (CTA 0, group 0),
+by kernel and GEMM kind (diagnostic build with the REQ timing hook)."""
 import os, sys
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -23,17 +24,12 @@ lib.fcg_debug_phase_buffer(None)
 b = buf.cpu().numpy()
 n = int(b[4095])
 rec = b[1000:1000 + 3 * min(n, 900)].reshape(-1, 3)
-print("records", n)
-for k in range(4):
-    r = rec[rec[:, 0] == k]
-    if len(r):
-        print("  kind", k, "issue cycles median", int(np.median(r[:, 2] - r[:, 1])), "count", len(r))
-# last launch = bwd of block 0: its records are the last ones; wake times b[3800 + k*64 + it]
-nt = sum(1 for x in rec[-200:] if x[0] == 3)  # G1' count in tail ~ ntiles of last launch
-last = rec[-4 * nt - 1:] if nt else rec
-for k in range(4):
-    r = last[last[:, 0] == k]
-    wake = b[3800 + k * 64: 3800 + k * 64 + len(r)]
-    # G1 records include the prologue G1 of tile 0 (it=-1 -> tile 0)
-    lat = [int(w - c) for w, c in zip(wake, r[:, 2]) if w > 0]
-    print("  bwd kind", k, "commit->wake first tiles:", lat[:10], "median", int(np.median(lat)) if lat else None)
+names = {0: "G1", 1: "G2", 2: "G3", 3: "G1'"}
+mmas = {(0, 0): 12, (0, 1): 24, (1, 0): 12, (1, 1): 24, (1, 2): 24, (1, 3): 12}
+for kern in (0, 1):
+    for k in range(4):
+        r = rec[rec[:, 0] == k + 10 * kern]
+        if len(r):
+            med = int(np.median(r[:, 2] - r[:, 1]))
+            print(("fwd", "bwd")[kern], names[k], "chain issue cycles median", med,
+                  "per MMA", med // mmas[(kern, k)], "n", len(r))
