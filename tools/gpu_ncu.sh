@@ -4,7 +4,7 @@
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 TAG=${1:-r01}; KERNS=${2:-k_edge_bwd_tc k_edge_fwd_tc}; shift 2
 mkdir -p gpurun_out
-B="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --e2e-steps 1 --profile-steps 1 $*"
+B="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-gpu-baseline --e2e-steps 1 --profile-steps 1 $*"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
   --log-file gpurun_out/launches_${TAG}.csv $B > gpurun_out/ncu_launch_${TAG}.log 2>&1
 echo "launch list exit $?" >> gpurun_out/ncu_launch_${TAG}.log
