@@ -596,12 +596,89 @@ k_edge_fwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
 // ---------------------------------------------------------------------------
 // Backward over src-owned rows (flash_block_backward, flash.py:272-295), per
 // 32-edge tile:
-//   gH = GH[dst]; [G1] z0 (recompute) -> h -> [G2] w;
-//   grad_w = gH*P[src] -> [G3, W1 MN-major] grad_h;
+//   gH = GH[dst]; [G1] z0 (recompute) -> h, ssp'(z0) -> [G2] w;
+//   grad_w = gH*P[src] -> [G3, W1^T] grad_h;
 //   grad_P rows = src-segment sums of gH*w (while G3 runs);
 //   db -> [G1'] dz0 = W0 db;  gz = grad_h * ssp'(z0);
 //   grad_d = sum_c gz*dz0 (= sum_k grad_b*db, flash.py:293) -> g_e = grad_d/d*u.
-// The basis and G1 of tile i+1 overlap the grad_d reduction of tile i.
+//
+// With N = 32 edges per MMA the A operand dominates the tensor core's
+// shared-memory reads (4 KB of weights per 1 KB of edges), so W1 and W1^T —
+// the A operands of G2 and G3, two thirds of the MMAs — are TMEM-resident
+// (columns [TB1, 512)), and W0 stays in shared memory.  That leaves each group
+// two 32-column slots: SA holds z0, then w, then dz0; SB holds grad_h, then
+// gz.  ssp'(z0) is stashed in the shared memory W1 was staged through.  G1 of
+// tile i+1 is issued as soon as the grad_d operands of tile i are in registers
+// and overlaps the reduction.
+constexpr uint32_t BWD_GCOLS = 64, SA = 0, SB = 32;
+constexpr uint32_t TB1 = NGRP * BWD_GCOLS, TB1T = TB1 + 128;
+static_assert(TB1T + 128 <= 512, "TMEM budget");
+constexpr uint32_t STASH_BYTES = D * TT * 4;
+static_assert(NGRP * STASH_BYTES <= 2 * W1_BYTES, "stash fits in the W1 staging area");
+
+// W1 (K-major rows) and W1^T (row m = column m of W1) hi | lo from the staged
+// shared-memory images into TMEM; warp w loads image w / 4 for its lane quarter.
+__device__ __forceinline__ void load_w1_tmem(const uint8_t *sm, uint32_t tmem) {
+  const int w = threadIdx.x >> 5, q = w & 3, lane = threadIdx.x & 31, m = 32 * q + lane;
+  const int img = (w >> 2) & 3;  // 0: W1 hi, 1: W1 lo, 2: W1^T hi, 3: W1^T lo
+  const uint16_t *base = (const uint16_t *)(sm + SM_W1 + (img & 1) * W1_BYTES);
+  const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (img < 2 ? TB1 : TB1T) + (img & 1) * (D / 2);
+#pragma unroll 1
+  for (int c0 = 0; c0 < D / 2; c0 += 16) {  // 16 columns = 32 K-values
+    float v[16];
+    if (img < 2) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint4 u = *(const uint4 *)(base + ((m / 8) * (D / 8) + c0 / 4 + j) * 64 + (m % 8) * 8);
+        v[4 * j] = __uint_as_float(u.x); v[4 * j + 1] = __uint_as_float(u.y);
+        v[4 * j + 2] = __uint_as_float(u.z); v[4 * j + 3] = __uint_as_float(u.w);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int k = 2 * (c0 + j);  // W1^T[m][k] = W1[k][m], k and k+1 in one column
+        const uint32_t e0 = base[((k / 8) * (D / 8) + m / 8) * 64 + (k % 8) * 8 + m % 8];
+        const uint32_t e1 = base[(((k + 1) / 8) * (D / 8) + m / 8) * 64 + ((k + 1) % 8) * 8 + m % 8];
+        v[j] = __uint_as_float(e0 | (e1 << 16));
+      }
+    }
+    tc::tmem_st16(taddr + c0, v);
+  }
+  tc::tmem_st_wait();
+  tc::fence_before_sync();
+  __syncthreads();  // W1 staging area free: it becomes the ssp' stash
+  tc::fence_after_sync();
+}
+
+// h = ssp(z0) as the K=128 B operand (act buffer) and ssp'(z0) into the
+// thread's stash entries ([edge/4][channel] float4s, conflict-free).  fp32:
+// ssp'(z) = sigmoid(z) = 1 - exp(-ssp(z))/2 from h; W16: from z0 itself (h is
+// rounded to fp16).
+template <bool Q>
+__device__ __forceinline__ void tile_h_bwd(const Wctx &W, float rs0, float b0c, float hs,
+                                           float4 *stash) {
+  float v[TT];
+  tc::tmem_ld32w(W.tl + SA, v);
+#pragma unroll
+  for (int i = 0; i < TT; i += 4) {
+    float s[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float z = v[i + j] * rs0 + b0c;
+      if (Q) {
+        s[j] = sigmoid_fast(z);
+        v[i + j] = __half2float(__float2half_rn(ssp_ref(z)));
+      } else {
+        v[i + j] = ssp_fast(z);
+        s[j] = fmaf(-0.5f, ex2_ftz(v[i + j] * -kLog2e), 1.f);
+      }
+    }
+    stash[(i / 4) * D + W.ch] = make_float4(s[0], s[1], s[2], s[3]);
+  }
+#pragma unroll
+  for (int j = 0; j < TT / 8; ++j) put8<!Q>(W.hb, D, W.ch, 8 * j, &v[8 * j], hs);
+}
+
 template <bool Q>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__restrict__ env,
@@ -612,13 +689,15 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
   TcShared *sh = (TcShared *)(sm + SM_META);
   const fcg_block &B = a.blk;
   kernel_prologue(sm, sh, B);
-  const Wctx W = make_wctx(sm, sh);
+  tc::mbar_wait(&sh->wbar, 0);
+  load_w1_tmem(sm, sh->tmem);
+  const Wctx W = make_wctx(sm, sh, BWD_GCOLS);
+  float4 *stash = (float4 *)(sm + SM_W1 + W.g * STASH_BYTES);
   const uint32_t sbase = tc::smem_u32(sm);
   const uint32_t id_f = tc::idesc_f16(128, TT, 0, 1);
-  const uint32_t id_t = tc::idesc_f16(128, TT, 1, 1);
   constexpr int NPF = Q ? 1 : 3, NPB = Q ? 2 : 3;
-  const Desc w0 = wdesc_k(sbase + SM_W0, DR, W0_BYTES), w1 = wdesc_k(sbase + SM_W1, D, W1_BYTES);
-  const Desc w1t = wdesc_mn(sbase + SM_W1, D, W1_BYTES);
+  const Desc w0 = wdesc_k(sbase + SM_W0, DR, W0_BYTES);
+  const uint32_t w1h = sh->tmem + TB1, w1l = w1h + D / 2, w1th = sh->tmem + TB1T, w1tl = w1th + D / 2;
   const Desc bb = adesc(W.sbb, DR), hb = adesc(W.shb, D);
 
   const UnitRange tr = unit_range(a, unit_rows, NGRP * blockIdx.x + W.g);
@@ -647,130 +726,125 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
   float4 ue = make_float4(0.f, 0.f, 0.f, 0.f), ue_n = ue;  // this lane's edge: (u, d)
   bool rows2 = true, rows2_n = true;
   MetaRegs mr;  // raw metadata of the tile after next
-  for (int it = -1; it < ntiles; ++it) {
-    const int t0 = tr.eb + it * TT;
-    const bool more = it + 1 < ntiles;
-    const int n_n = min(TT, tr.ee - t0 - TT);
-    PHASE(1, it, 0);
-    if (it < 0) {
-      mr.load(a, geo, env, tr.eb, n_n, W.lane);
-      ue_n = mr.store(W.meta(0), true, W.lane, rows2_n);
-      if (more) mr.load(a, geo, env, tr.eb + TT, min(TT, tr.ee - tr.eb - TT), W.lane);
-    } else {
-      const WarpMeta *M = W.meta(it);
-      const int n_e = min(TT, tr.ee - t0);
-      float gh[TT];  // grad_H[dst][ch] (flash.py:281)
-#pragma unroll
-      for (int i = 0; i < TT; ++i) gh[i] = __ldg(&GH[(size_t)M->nbr[i] * D + ch]);
-      // P[src][ch] (flash.py:291): src = the tile's CSR rows, usually its
-      // first and last only
-      const int o_f = M->own[0], o_l = M->own[n_e - 1];
-      const float p_f = __ldg(&P[(size_t)o_f * D + ch]), p_l = __ldg(&P[(size_t)o_l * D + ch]);
-      W.wait(BAR_G1, it);
-      PHASE(1, it, 1);
-      tile_h<Q, !Q>(W, rs0, b0c, hs);
-      REQ(BAR_G2, (mma_chain<D / 16, NPF>(W.tmem_g + S1, w1, hb, id_f)));
-      PHASE(1, it, 2);
-      if (more) {
-        ue_n = mr.store(W.meta(it + 1), true, W.lane, rows2_n);
-        if (it + 2 < ntiles) mr.load(a, geo, env, t0 + 2 * TT, min(TT, tr.ee - t0 - 2 * TT), W.lane);
-      }
-      W.wait(BAR_G2, it);
-      PHASE(1, it, 3);
-      // grad_w = gH * P[src] (flash.py:291) -> B operand of G3 (W1^T)
-#pragma unroll
-      for (int j = 0; j < TT / 8; ++j) {
-        const int4 oa = *(const int4 *)&M->own[8 * j], ob = *(const int4 *)&M->own[8 * j + 4];
-        const int oo[8] = {oa.x, oa.y, oa.z, oa.w, ob.x, ob.y, ob.z, ob.w};
-        float v[8];
-        if (rows2) {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) v[i] = gh[8 * j + i] * (oo[i] == o_l ? p_l : p_f);
-        } else {  // a tile spanning 3+ rows: per-edge loads
-#pragma unroll
-          for (int i = 0; i < 8; ++i) v[i] = gh[8 * j + i] * __ldg(&P[(size_t)max(oo[i], 0) * D + ch]);
-        }
-        put8<true>(W.hb, D, ch, 8 * j, v, gws);
-      }
-      REQ(BAR_G3, (mma_chain<D / 16, NPB>(W.tmem_g + S2, w1t, hb, id_t)));
-      PHASE(1, it, 4);
-      // while G3 runs: grad_P rows = src-segment sums of gH * w (flash.py:283-288)
-      {
-        float v[TT];
-        tc::tmem_ld32w(W.tl + S1, v);
-#pragma unroll
-        for (int i = 0; i < TT; ++i) v[i] = gh[i] * (v[i] * s1 + b1c);
-        if (n_e < TT) {
-#pragma unroll
-          for (int i = 0; i < TT; ++i) v[i] = i < n_e ? v[i] : 0.f;
-        }
-        seg.tile(M->own, v);
-      }
-      PHASE(1, it, 5);
-      // db -> basis buffer (G1 is done), G1': dz0 = W0 db into S1 (w consumed)
-      tile_basis<true, Q>(a, W, M, dbs);
-      REQ(BAR_G1P, (mma_chain<DR / 16, NPB>(W.tmem_g + S1, w0, bb, id_f)));
-      PHASE(1, it, 6);
-      W.wait(BAR_G3, it);
-      // gz = grad_h * ssp'(z0) (mlp_backward_input, model.py:189-200), kept in
-      // S2.  fp32: ssp'(z) = sigmoid(z) = 1 - exp(-ssp(z))/2 from the stashed
-      // h; W16: from z0 itself (h was rounded to fp16).
-      {
-        float gz[TT], x[TT];
-        tc::tmem_ld32w(W.tl + S2, gz);
-        tc::tmem_ld32w(W.tl + (Q ? S0 : S3), x);
-#pragma unroll
-        for (int i = 0; i < TT; ++i) {
-          const float sig = Q ? sigmoid_fast(x[i] * rs0 + b0c) : fmaf(-0.5f, ex2_ftz(x[i] * -kLog2e), 1.f);
-          gz[i] = gz[i] * sg3 * sig;
-        }
-        tc::tmem_st32(W.tl + S2, gz);
-        tc::tmem_st_wait();
-      }
-      PHASE(1, it, 7);
-      W.wait(BAR_G1P, it);
-      PHASE(1, it, 8);
-    }
-    if (more) {  // basis + G1 of the next tile overlap the grad_d reduction
-      tile_basis<false, Q>(a, W, W.meta(it + 1), bsc);
-      if (it < 0) tc::mbar_wait(&sh->wbar, 0);  // weights resident before the first GEMM
-      REQ(BAR_G1, (mma_chain<DR / 16, NPF>(W.tmem_g + S0, w0, bb, id_f)));
-    }
-    PHASE(1, it, 9);
-    if (it >= 0) {
-      // grad_d[e] = sum_c gz[c][e] * dz0[c][e]: per-warp transpose-sum, then
-      // the four lane quarters in fixed order (warp 0 of the group)
-      float *xg = &sh->xg[W.g][it & 1][0][0];
-      {
-        float p[TT], dz[TT];
-        tc::tmem_ld32w(W.tl + S2, p);
-        tc::tmem_ld32w(W.tl + S1, dz);
-#pragma unroll
-        for (int i = 0; i < TT; ++i) p[i] *= dz[i] * sdz;
-        xg[W.q * TT + W.lane] = warp_edge_sum(p, W.lane);
-      }
-      __syncwarp();
-      if (W.lane == 0) tc::mbar_arrive(&sh->xbar[W.g]);
-      if (W.q == 0) {
-        tc::mbar_wait(&sh->xbar[W.g], (uint32_t)(it & 1));
-        const int e = W.lane;
-        if (e < min(TT, tr.ee - t0)) {
-          const float gd = ((xg[e] + xg[TT + e]) + xg[2 * TT + e]) + xg[3 * TT + e];
-          const float inv = ue.w > TINY_DISTANCE ? 1.f / ue.w : 0.f;  // _safe_inv, flash.py:176-178
-          const float s = gd * inv;
-          float4 g = make_float4(s * ue.x, s * ue.y, s * ue.z, 0.f);  // flash.py:294
-          float4 *dst = &gsum[t0 + e];
-          if (accumulate) {
-            const float4 o = *dst;
-            g.x += o.x; g.y += o.y; g.z += o.z;
-          }
-          *dst = g;
-        }
-      }
-      PHASE(1, it, 10);
-    }
+  if (ntiles > 0) {  // tile 0: metadata, basis, G1
+    mr.load(a, geo, env, tr.eb, min(TT, tr.ee - tr.eb), W.lane);
+    ue_n = mr.store(W.meta(0), true, W.lane, rows2_n);
+    if (ntiles > 1) mr.load(a, geo, env, tr.eb + TT, min(TT, tr.ee - tr.eb - TT), W.lane);
+    tile_basis<false, Q>(a, W, W.meta(0), bsc);
+    REQ(BAR_G1, (mma_chain<DR / 16, NPF>(W.tmem_g + SA, w0, bb, id_f)));
+  }
+  for (int it = 0; it < ntiles; ++it) {
     ue = ue_n;
     rows2 = rows2_n;
+    const int t0 = tr.eb + it * TT;
+    const bool more = it + 1 < ntiles;
+    PHASE(1, it, 0);
+    const WarpMeta *M = W.meta(it);
+    const int n_e = min(TT, tr.ee - t0);
+    float gh[TT];  // grad_H[dst][ch] (flash.py:281)
+#pragma unroll
+    for (int i = 0; i < TT; ++i) gh[i] = __ldg(&GH[(size_t)M->nbr[i] * D + ch]);
+    // P[src][ch] (flash.py:291): src = the tile's CSR rows, usually its
+    // first and last only
+    const int o_f = M->own[0], o_l = M->own[n_e - 1];
+    const float p_f = __ldg(&P[(size_t)o_f * D + ch]), p_l = __ldg(&P[(size_t)o_l * D + ch]);
+    W.wait(BAR_G1, it);
+    PHASE(1, it, 1);
+    tile_h_bwd<Q>(W, rs0, b0c, hs, stash);
+    REQ(BAR_G2, (mma_chain_ts<D / 16, NPF>(W.tmem_g + SA, w1h, w1l, hb, id_f)));
+    PHASE(1, it, 2);
+    if (more) {
+      ue_n = mr.store(W.meta(it + 1), true, W.lane, rows2_n);
+      if (it + 2 < ntiles) mr.load(a, geo, env, t0 + 2 * TT, min(TT, tr.ee - t0 - 2 * TT), W.lane);
+    }
+    W.wait(BAR_G2, it);
+    PHASE(1, it, 3);
+    // grad_w = gH * P[src] (flash.py:291) -> B operand of G3 (W1^T)
+#pragma unroll
+    for (int j = 0; j < TT / 8; ++j) {
+      const int4 oa = *(const int4 *)&M->own[8 * j], ob = *(const int4 *)&M->own[8 * j + 4];
+      const int oo[8] = {oa.x, oa.y, oa.z, oa.w, ob.x, ob.y, ob.z, ob.w};
+      float v[8];
+      if (rows2) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = gh[8 * j + i] * (oo[i] == o_l ? p_l : p_f);
+      } else {  // a tile spanning 3+ rows: per-edge loads
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = gh[8 * j + i] * __ldg(&P[(size_t)max(oo[i], 0) * D + ch]);
+      }
+      put8<true>(W.hb, D, ch, 8 * j, v, gws);
+    }
+    REQ(BAR_G3, (mma_chain_ts<D / 16, NPB>(W.tmem_g + SB, w1th, w1tl, hb, id_f)));
+    PHASE(1, it, 4);
+    // while G3 runs: grad_P rows = src-segment sums of gH * w (flash.py:283-288)
+    {
+      float v[TT];
+      tc::tmem_ld32w(W.tl + SA, v);
+#pragma unroll
+      for (int i = 0; i < TT; ++i) v[i] = gh[i] * (v[i] * s1 + b1c);
+      if (n_e < TT) {
+#pragma unroll
+        for (int i = 0; i < TT; ++i) v[i] = i < n_e ? v[i] : 0.f;
+      }
+      seg.tile(M->own, v);
+    }
+    PHASE(1, it, 5);
+    // db -> basis buffer (G1 is done), G1': dz0 = W0 db into SA (w consumed)
+    tile_basis<true, Q>(a, W, M, dbs);
+    REQ(BAR_G1P, (mma_chain<DR / 16, NPB>(W.tmem_g + SA, w0, bb, id_f)));
+    PHASE(1, it, 6);
+    W.wait(BAR_G3, it);
+    // gz = grad_h * ssp'(z0) (mlp_backward_input, model.py:189-200), kept in SB
+    {
+      float gz[TT];
+      tc::tmem_ld32w(W.tl + SB, gz);
+#pragma unroll
+      for (int i = 0; i < TT; i += 4) {
+        const float4 s = stash[(i / 4) * D + ch];
+        gz[i] *= sg3 * s.x; gz[i + 1] *= sg3 * s.y; gz[i + 2] *= sg3 * s.z; gz[i + 3] *= sg3 * s.w;
+      }
+      tc::tmem_st32(W.tl + SB, gz);
+      tc::tmem_st_wait();
+    }
+    PHASE(1, it, 7);
+    W.wait(BAR_G1P, it);
+    PHASE(1, it, 8);
+    // grad_d[e] = sum_c gz[c][e] * dz0[c][e]: per-warp transpose-sum, then
+    // the four lane quarters in fixed order (warp 0 of the group)
+    float p[TT];
+    {
+      float dz[TT];
+      tc::tmem_ld32w(W.tl + SB, p);
+      tc::tmem_ld32w(W.tl + SA, dz);
+#pragma unroll
+      for (int i = 0; i < TT; ++i) p[i] *= dz[i] * sdz;
+    }
+    if (more) {  // basis + G1 of the next tile (SA is read) overlap the reduction
+      tile_basis<false, Q>(a, W, W.meta(it + 1), bsc);
+      REQ(BAR_G1, (mma_chain<DR / 16, NPF>(W.tmem_g + SA, w0, bb, id_f)));
+    }
+    PHASE(1, it, 9);
+    float *xg = &sh->xg[W.g][it & 1][0][0];
+    xg[W.q * TT + W.lane] = warp_edge_sum(p, W.lane);
+    __syncwarp();
+    if (W.lane == 0) tc::mbar_arrive(&sh->xbar[W.g]);
+    if (W.q == 0) {
+      tc::mbar_wait(&sh->xbar[W.g], (uint32_t)(it & 1));
+      const int e = W.lane;
+      if (e < n_e) {
+        const float gd = ((xg[e] + xg[TT + e]) + xg[2 * TT + e]) + xg[3 * TT + e];
+        const float inv = ue.w > TINY_DISTANCE ? 1.f / ue.w : 0.f;  // _safe_inv, flash.py:176-178
+        const float s = gd * inv;
+        float4 g = make_float4(s * ue.x, s * ue.y, s * ue.z, 0.f);  // flash.py:294
+        float4 *dst = &gsum[t0 + e];
+        if (accumulate) {
+          const float4 o = *dst;
+          g.x += o.x; g.y += o.y; g.z += o.z;
+        }
+        *dst = g;
+      }
+    }
+    PHASE(1, it, 10);
   }
   seg.finish();
   tc::fence_before_sync();
