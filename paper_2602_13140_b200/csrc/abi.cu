@@ -1,4 +1,6 @@
 // extern "C" entry points of libfcg.so (declared in include/fcg.h).
+#include <stdlib.h>
+
 #include <string>
 
 #include "common.cuh"
@@ -16,6 +18,15 @@ int cuda_status(const char *where) {
     return FCG_ERR_CUDA;
   }
   return FCG_OK;
+}
+
+// FCG_PDL: bitmask of launch sites using PDL (PdlSite); default all, 0 = off.
+bool pdl_enabled(int site) {
+  static const unsigned mask = [] {
+    const char *v = getenv("FCG_PDL");
+    return v ? (unsigned)strtoul(v, nullptr, 0) : ~0u;
+  }();
+  return (mask >> site) & 1u;
 }
 
 // ---- profiler ----------------------------------------------------------

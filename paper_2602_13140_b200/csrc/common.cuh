@@ -20,6 +20,55 @@ int cuda_status(const char *where);  // FCG_OK or FCG_ERR_CUDA (sets message)
 
 inline int ceil_div(long long a, long long b) { return int((a + b - 1) / b); }
 
+// ---- programmatic dependent launch (PDL) ------------------------------------
+// The step's kernels are a serial chain.  Launched with PDL, a kernel's CTAs
+// may start while its predecessor drains: each kernel lets its dependents
+// launch at entry (pdl_trigger) and runs only its static prologue — TMEM
+// allocation, weight staging from the immutable model images — before
+// pdl_wait, which returns once the predecessor grid has completed and its
+// writes are visible.  Every CTA of a PDL-launched kernel passes pdl_wait
+// before touching step data and before exiting, so completion stays
+// transitive along the chain.  Both are no-ops without the launch attribute.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Loads in PDL-launched kernels are coherent (ld.global), never
+// ld.global.nc: ptxas treats .nc data as read-only for the kernel's whole
+// lifetime and hoists such loads above griddepcontrol.wait and even bar.sync,
+// i.e. before the predecessor's writes are visible.  So those kernels use
+// ld_dep instead of __ldg and no const __restrict__ pointers (checked on the
+// SASS by tools/check_pdl.py, run by tests/test_host.py).
+template <class T>
+__device__ __forceinline__ T ld_dep(const T *p) {
+  return __ldca(p);  // ld.global.ca: coherent, L1-cached
+}
+// Gathers whose ADDRESS derives from data loaded after the wait (CSR
+// metadata staged in shared memory) cannot be hoisted above it, so they keep
+// the read-only path.
+template <class T>
+__device__ __forceinline__ T ld_gather(const T *p) {
+  return __ldg(p);
+}
+enum PdlSite { PDL_GEOM, PDL_EDGE_FWD, PDL_EDGE_BWD, PDL_NODE_PRE, PDL_NODE_PRE_BWD,
+               PDL_NODE_POST, PDL_NODE_POST_BWD, PDL_READOUT };
+bool pdl_enabled(int site);  // FCG_PDL=<bitmask of sites> in the environment (A/B)
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(int site, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t s, Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled(site) ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 // Workspace carving: bump allocator over a caller buffer, 256-byte aligned.
 struct Carver {
   char *base;
@@ -51,7 +100,7 @@ __device__ __forceinline__ int lower_bound_i32(const int32_t *a, int n, long lon
   int lo = 0, hi = n;
   while (lo < hi) {
     int mid = (lo + hi) >> 1;
-    if ((long long)a[mid] < v) lo = mid + 1; else hi = mid;
+    if ((long long)ld_dep(&a[mid]) < v) lo = mid + 1; else hi = mid;
   }
   return lo;
 }

@@ -66,8 +66,8 @@ constexpr uint32_t HB_BYTES = 2 * D * TT * 2;   // h / grad_w hi|lo: 16 KB
 constexpr uint32_t GBUF_BYTES = BB_BYTES + HB_BYTES;
 constexpr uint32_t SM_META = SM_BUF + NGRP * GBUF_BYTES;
 constexpr uint32_t W0_BYTES = D * DR * 2, W1_BYTES = D * D * 2;
-// TMEM columns inside a group's 128: z0 | w then dz0 | grad_h then gz | h (backward)
-constexpr uint32_t S0 = 0, S1 = 32, S2 = 64, S3 = 96;
+// forward TMEM slots inside a group's columns: z0 | w
+constexpr uint32_t S0 = 0, S1 = 32;
 enum { BAR_G1 = 0, BAR_G2 = 1, BAR_G3 = 2, BAR_G1P = 3 };
 
 constexpr int NWARP = TC_THREADS / 32;
@@ -138,21 +138,32 @@ struct SegSum {
 
 // ---- per-step edge geometry (the reference's d cache, flash.py:221-223) ------
 // geo[k] = (u, d) with u = r[own] - r[nbr] for CSR slot k; env[k] = (C, C').
-// Block 0 also computes the row range of every work unit (balanced by edge
-// count) once per step for the six edge launches that follow.
+// Also the row range of every work unit, balanced by edge count, for the
+// edge launches that follow: unit u starts at the first row r with
+// ptr[r] >= t_u = e_tot * u / G (cta_row_range's split).  Each row writes the
+// boundaries t_u in (ptr[r-1], ptr[r]] — one coalesced pass instead of G
+// dependent binary searches.
 __global__ void __launch_bounds__(256)
-k_edge_geom(const float *__restrict__ pos, const int32_t *__restrict__ ptr,
-            const int32_t *__restrict__ nbr, const int32_t *__restrict__ own, int nrows,
-            int64_t cap_e, float cutoff, float4 *__restrict__ geo, float2 *__restrict__ env,
-            int32_t *__restrict__ unit_rows, int nunits) {
-  long long e_tot = ptr[nrows];
+k_edge_geom(const float *pos, const int32_t *ptr, const int32_t *nbr, const int32_t *own,
+            int nrows, int64_t cap_e, float cutoff, float4 *geo, float2 *env,
+            int32_t *unit_rows, int nunits) {
+  pdl_trigger();
+  pdl_wait();
+  __syncthreads();  // keeps ptxas from hoisting loads above the wait
+  long long e_tot = ld_dep(&ptr[nrows]);
   if (e_tot > cap_e) e_tot = cap_e;
-  if (blockIdx.x == 0) {
-    for (int u = threadIdx.x; u <= nunits; u += blockDim.x) {
-      int rb, re;
-      cta_row_range(ptr, nrows, e_tot, u < nunits ? u : nunits - 1, nunits, rb, re);
-      unit_rows[u] = u < nunits ? rb : re;
+  const long long G = nunits;
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r <= nrows;
+       r += (long long)gridDim.x * blockDim.x) {
+    const long long lo = r == 0 ? -1 : ld_dep(&ptr[r - 1]), hi = ld_dep(&ptr[r]);
+    if (r == 0) {
+      unit_rows[0] = 0;
+      unit_rows[G] = nrows;
     }
+    if (hi <= lo) continue;  // empty row: no boundary maps to it
+    long long u = lo < 0 ? 1 : (e_tot > 0 ? ((lo + 1) * G + e_tot - 1) / e_tot : G);
+    if (u < 1) u = 1;
+    for (; u < G && e_tot * u / G <= hi; ++u) unit_rows[u] = (int32_t)r;
   }
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < e_tot;
        k += (long long)gridDim.x * blockDim.x) {
@@ -289,12 +300,10 @@ __device__ __forceinline__ Wctx make_wctx(uint8_t *sm, TcShared *sh, uint32_t gc
   return W;
 }
 
-// The resident filter weights are staged by the TMA engine (cp.async.bulk);
-// every warp waits on wbar once before its first GEMM request.  kSmemW=false
-// (forward): the weights live in TMEM instead (load_weights_tmem).
-template <bool kSmemW = true>
+// The filter weight images are staged by the TMA engine (cp.async.bulk);
+// every thread waits on wbar before reading them.
 __device__ __forceinline__ void kernel_prologue(uint8_t *sm, TcShared *sh, const fcg_block &b) {
-  if (kSmemW && threadIdx.x == 0) {
+  if (threadIdx.x == 0) {
     tc::mbar_init(&sh->wbar, 1);
     tc::fence_mbar_init();
     tc::mbar_expect_tx(&sh->wbar, 2 * W0_BYTES + 2 * W1_BYTES);
@@ -317,40 +326,72 @@ __device__ __forceinline__ void kernel_prologue(uint8_t *sm, TcShared *sh, const
   tc::fence_after_sync();
 }
 
-// ---- weights as the TMEM-resident A operand (forward) ---------------------------
-// Columns [TW0, TW0+64): W0 hi | lo (K=64: 32 columns each); [TW1, TW1+128):
-// W1 hi | lo (K=128).  Row m of a weight lives in lane m, element k in
-// column k/2 (pinned by tests/test_gpu_tcgen05.py::test_a_operand_in_tmem),
-// so an MMA reads its A slice from TMEM and only B (1 KB per MMA) from
-// shared memory, instead of 4 KB of A + 1 KB of B.
+// ---- weights as the TMEM-resident A operand ----------------------------------------
+// Row m of a weight lives in lane m, element k in column k/2 (pinned by
+// tests/test_gpu_tcgen05.py::test_a_operand_in_tmem), so an MMA reads its A
+// slice from TMEM and only B (1 KB per MMA) from shared memory, instead of
+// 4 KB of A + 1 KB of B.  The images are staged in shared memory by the bulk
+// copy of kernel_prologue and moved to TMEM by the lanes that own the rows.
+// Forward columns: [TW0, TW0+64) W0 hi | lo (K=64: 32 columns each),
+// [TW1, TW1+128) W1 hi | lo (K=128).
 constexpr uint32_t FWD_GCOLS = 64;  // forward groups: slots S0, S1 only
 constexpr uint32_t TW0 = NGRP * FWD_GCOLS, TW1 = TW0 + 64;
 static_assert(TW1 + 128 <= 512, "TMEM budget");
 
-// One image row (core-matrix order, element (r,c) at ((r/8)*(in/8)+c/8)*64 +
-// (r%8)*8 + c%8) -> this lane's TMEM row.  Warp w loads image (w / 4) % 4.
-__device__ __forceinline__ void load_weights_tmem(const fcg_block &b, uint32_t tmem) {
-  const int w = threadIdx.x >> 5, q = w & 3, lane = threadIdx.x & 31, m = 32 * q + lane;
-  const int img = (w >> 2) & 3;  // 0: W0 hi, 1: W0 lo, 2: W1 hi, 3: W1 lo
-  const int K = img < 2 ? DR : D;
-  const uint16_t *base = img < 2 ? b.f0_img + (img & 1) * (D * DR) : b.f1_img + (img & 1) * (D * D);
-  const uint32_t col = img < 2 ? TW0 + (img & 1) * (DR / 2) : TW1 + (img & 1) * (D / 2);
-  const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + col;
+// Row m of a staged core-matrix image with K inputs (element (r,c) at
+// ((r/8)*(K/8)+c/8)*64 + (r%8)*8 + c%8) -> TMEM columns from taddr; TRANS
+// moves row m of W^T (column m of a square image) instead.
+template <bool TRANS>
+__device__ __forceinline__ void image_row_to_tmem(const uint16_t *img, int K, int m,
+                                                  uint32_t taddr) {
 #pragma unroll 1
-  for (int j0 = 0; j0 < K / 8; j0 += 4) {  // 4 chunks of 8 halves = 16 columns
+  for (int c0 = 0; c0 < K / 2; c0 += 16) {  // 16 columns = 32 K-values
     float v[16];
+    if (!TRANS) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint4 u = __ldg((const uint4 *)(base + ((m / 8) * (K / 8) + j0 + j) * 64 + (m % 8) * 8));
-      v[4 * j] = __uint_as_float(u.x); v[4 * j + 1] = __uint_as_float(u.y);
-      v[4 * j + 2] = __uint_as_float(u.z); v[4 * j + 3] = __uint_as_float(u.w);
+      for (int j = 0; j < 4; ++j) {
+        const uint4 u = *(const uint4 *)(img + ((m / 8) * (K / 8) + c0 / 4 + j) * 64 + (m % 8) * 8);
+        v[4 * j] = __uint_as_float(u.x); v[4 * j + 1] = __uint_as_float(u.y);
+        v[4 * j + 2] = __uint_as_float(u.z); v[4 * j + 3] = __uint_as_float(u.w);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int k = 2 * (c0 + j);  // W^T[m][k] = W[k][m], k and k+1 in one column
+        const uint32_t e0 = img[((k / 8) * (K / 8) + m / 8) * 64 + (k % 8) * 8 + m % 8];
+        const uint32_t e1 = img[(((k + 1) / 8) * (K / 8) + m / 8) * 64 + ((k + 1) % 8) * 8 + m % 8];
+        v[j] = __uint_as_float(e0 | (e1 << 16));
+      }
     }
-    tc::tmem_st16(taddr + j0 * 4, v);
+    tc::tmem_st16(taddr + c0, v);
   }
+}
+
+// End of the static prologue: TMEM stores done, then the PDL wait right
+// before a block barrier (ptxas does not hoist loads across bar.sync, while
+// it does move ld.global.nc across griddepcontrol.wait alone;
+// tools/check_pdl.py / tests/test_host.py check the SASS).
+__device__ __forceinline__ void prologue_done() {
   tc::tmem_st_wait();
   tc::fence_before_sync();
+  pdl_wait();
   __syncthreads();
   tc::fence_after_sync();
+}
+
+// Forward: warp w moves image (w / 4) % 4 (W0 hi, W0 lo, W1 hi, W1 lo) for
+// its lane quarter.
+__device__ __forceinline__ void load_fwd_weights_tmem(const uint8_t *sm, uint32_t tmem) {
+  const int w = threadIdx.x >> 5, q = w & 3, m = 32 * q + (threadIdx.x & 31);
+  const int img = (w >> 2) & 3;
+  const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16);
+  if (img < 2)
+    image_row_to_tmem<false>((const uint16_t *)(sm + SM_W0 + (img & 1) * W0_BYTES), DR, m,
+                             lane_base + TW0 + (img & 1) * (DR / 2));
+  else
+    image_row_to_tmem<false>((const uint16_t *)(sm + SM_W1 + (img & 1) * W1_BYTES), D, m,
+                             lane_base + TW1 + (img & 1) * (D / 2));
+  prologue_done();
 }
 
 // D (+)= A(TMEM columns a_hi / a_lo) x B over KS k-steps (8 A columns each)
@@ -372,8 +413,8 @@ struct MetaRegs {
   int o, n, n_e;
   float4 g;
   float2 c;
-  __device__ __forceinline__ void load(const EdgeArgs &a, const float4 *__restrict__ geo,
-                                       const float2 *__restrict__ env, int t0, int count,
+  __device__ __forceinline__ void load(const EdgeArgs &a, const float4 *geo,
+                                       const float2 *env, int t0, int count,
                                        int lane) {
     n_e = count;
     o = -1; n = 0;
@@ -417,7 +458,7 @@ template <bool DERIV, bool Q>
 __device__ __forceinline__ void tile_basis(const EdgeArgs &a, const Wctx &W, const WarpMeta *m,
                                            float scale) {
   const int k = 16 * W.q + (W.lane & 15), e0 = (W.lane >> 4) * 16;
-  const float mu = __ldg(&a.centers[k]);
+  const float mu = ld_dep(&a.centers[k]);
   const float ngl = -a.gamma * kLog2e, g2 = -2.f * a.gamma;
   float v[16];
 #pragma unroll
@@ -444,9 +485,8 @@ __device__ __forceinline__ void tile_basis(const EdgeArgs &a, const Wctx &W, con
 
 // h = ssp(z0) for this thread's channel over the tile (z0 = TMEM S0 scaled),
 // as the K=128 B operand (act buffer).  Padding columns carry finite values
-// that no valid edge reads.  With STASH the fp32 h also goes to TMEM S3 (the
-// backward derives ssp'(z0) from it).
-template <bool Q, bool STASH>
+// that no valid edge reads.
+template <bool Q>
 __device__ __forceinline__ void tile_h(const Wctx &W, float rs0, float b0c, float hs) {
   float v[TT];
   tc::tmem_ld32w(W.tl + S0, v);
@@ -455,10 +495,8 @@ __device__ __forceinline__ void tile_h(const Wctx &W, float rs0, float b0c, floa
     if (Q) v[i] = __half2float(__float2half_rn(ssp_ref(v[i] * rs0 + b0c)));
     else v[i] = ssp_fast(v[i] * rs0 + b0c);
   }
-  if (STASH) tc::tmem_st32(W.tl + S3, v);
 #pragma unroll
   for (int j = 0; j < TT / 8; ++j) put8<!Q>(W.hb, D, W.ch, 8 * j, &v[8 * j], hs);
-  if (STASH) tc::tmem_st_wait();
 }
 
 // Sum of p over the 32 lanes of the warp for every edge: a butterfly
@@ -509,14 +547,16 @@ __device__ __forceinline__ UnitRange unit_range(const EdgeArgs &a, const int32_t
 // G1(i+1).  Iteration -1 only prepares tile 0.
 template <bool Q>
 __global__ void __launch_bounds__(TC_THREADS, 1)
-k_edge_fwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__restrict__ env,
-              const int32_t *__restrict__ unit_rows, const float *__restrict__ P,
-              float *__restrict__ H) {
+k_edge_fwd_tc(const EdgeArgs a, const float4 *geo, const float2 *env,
+              const int32_t *unit_rows, const float *P,
+              float *H) {
   extern __shared__ __align__(1024) uint8_t sm[];
   TcShared *sh = (TcShared *)(sm + SM_META);
   const fcg_block &B = a.blk;
-  kernel_prologue<false>(sm, sh, B);
-  load_weights_tmem(B, sh->tmem);
+  pdl_trigger();
+  kernel_prologue(sm, sh, B);
+  tc::mbar_wait(&sh->wbar, 0);
+  load_fwd_weights_tmem(sm, sh->tmem);  // ends with the PDL wait
   const Wctx W = make_wctx(sm, sh, FWD_GCOLS);
   const uint32_t idesc = tc::idesc_f16(128, TT, 0, 1);
   constexpr int NP = Q ? 1 : 3;
@@ -531,10 +571,10 @@ k_edge_fwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
   seg.acc = 0.f;
   seg.outc = H + ch;
 
-  const float b0c = __ldg(&B.f0_b[ch]), b1c = __ldg(&B.f1_b[ch]);
-  const float rs0 = Q ? __ldg(&B.f0_s[ch]) : pow2f(-(B.f0_exp + 14));
+  const float b0c = ld_dep(&B.f0_b[ch]), b1c = ld_dep(&B.f1_b[ch]);
+  const float rs0 = Q ? ld_dep(&B.f0_s[ch]) : pow2f(-(B.f0_exp + 14));
   const float hs = Q ? 1.f : pow2f(B.f_hexp);
-  const float s1 = Q ? __ldg(&B.f1_s[ch]) : pow2f(-(B.f1_exp + B.f_hexp));
+  const float s1 = Q ? ld_dep(&B.f1_s[ch]) : pow2f(-(B.f1_exp + B.f_hexp));
   const float bsc = Q ? 1.f : 16384.f;
 
   float pv[TT];  // P[src][ch] of the current tile
@@ -552,7 +592,7 @@ k_edge_fwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
     } else {
       W.wait(BAR_G1, it);
       PHASE(0, it, 1);
-      tile_h<Q, false>(W, rs0, b0c, hs);
+      tile_h<Q>(W, rs0, b0c, hs);
       REQ(BAR_G2, (mma_chain_ts<D / 16, NP>(W.tmem_g + S1, w1h, w1l, hb, idesc)));
       PHASE(0, it, 2);
       if (more) {
@@ -584,7 +624,7 @@ k_edge_fwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
     if (more) {
       const WarpMeta *Mn = W.meta(it + 1);
 #pragma unroll
-      for (int i = 0; i < TT; ++i) pv[i] = __ldg(&P[(size_t)Mn->nbr[i] * D + ch]);
+      for (int i = 0; i < TT; ++i) pv[i] = ld_gather(&P[(size_t)Mn->nbr[i] * D + ch]);
     }
   }
   seg.finish();
@@ -617,37 +657,16 @@ constexpr uint32_t STASH_BYTES = D * TT * 4;
 static_assert(NGRP * STASH_BYTES <= 2 * W1_BYTES, "stash fits in the W1 staging area");
 
 // W1 (K-major rows) and W1^T (row m = column m of W1) hi | lo from the staged
-// shared-memory images into TMEM; warp w loads image w / 4 for its lane quarter.
+// shared-memory images into TMEM; warp w moves image w / 4 for its lane
+// quarter.  The W1 staging area becomes the ssp' stash afterwards.
 __device__ __forceinline__ void load_w1_tmem(const uint8_t *sm, uint32_t tmem) {
-  const int w = threadIdx.x >> 5, q = w & 3, lane = threadIdx.x & 31, m = 32 * q + lane;
+  const int w = threadIdx.x >> 5, q = w & 3, m = 32 * q + (threadIdx.x & 31);
   const int img = (w >> 2) & 3;  // 0: W1 hi, 1: W1 lo, 2: W1^T hi, 3: W1^T lo
   const uint16_t *base = (const uint16_t *)(sm + SM_W1 + (img & 1) * W1_BYTES);
   const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (img < 2 ? TB1 : TB1T) + (img & 1) * (D / 2);
-#pragma unroll 1
-  for (int c0 = 0; c0 < D / 2; c0 += 16) {  // 16 columns = 32 K-values
-    float v[16];
-    if (img < 2) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint4 u = *(const uint4 *)(base + ((m / 8) * (D / 8) + c0 / 4 + j) * 64 + (m % 8) * 8);
-        v[4 * j] = __uint_as_float(u.x); v[4 * j + 1] = __uint_as_float(u.y);
-        v[4 * j + 2] = __uint_as_float(u.z); v[4 * j + 3] = __uint_as_float(u.w);
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int k = 2 * (c0 + j);  // W1^T[m][k] = W1[k][m], k and k+1 in one column
-        const uint32_t e0 = base[((k / 8) * (D / 8) + m / 8) * 64 + (k % 8) * 8 + m % 8];
-        const uint32_t e1 = base[(((k + 1) / 8) * (D / 8) + m / 8) * 64 + ((k + 1) % 8) * 8 + m % 8];
-        v[j] = __uint_as_float(e0 | (e1 << 16));
-      }
-    }
-    tc::tmem_st16(taddr + c0, v);
-  }
-  tc::tmem_st_wait();
-  tc::fence_before_sync();
-  __syncthreads();  // W1 staging area free: it becomes the ssp' stash
-  tc::fence_after_sync();
+  if (img < 2) image_row_to_tmem<false>(base, D, m, taddr);
+  else image_row_to_tmem<true>(base, D, m, taddr);
+  prologue_done();
 }
 
 // h = ssp(z0) as the K=128 B operand (act buffer) and ssp'(z0) into the
@@ -681,16 +700,17 @@ __device__ __forceinline__ void tile_h_bwd(const Wctx &W, float rs0, float b0c, 
 
 template <bool Q>
 __global__ void __launch_bounds__(TC_THREADS, 1)
-k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__restrict__ env,
-              const int32_t *__restrict__ unit_rows, const float *__restrict__ P,
-              const float *__restrict__ GH, float *__restrict__ GP, float4 *__restrict__ gsum,
+k_edge_bwd_tc(const EdgeArgs a, const float4 *geo, const float2 *env,
+              const int32_t *unit_rows, const float *P,
+              const float *GH, float *GP, float4 *gsum,
               int accumulate) {
   extern __shared__ __align__(1024) uint8_t sm[];
   TcShared *sh = (TcShared *)(sm + SM_META);
   const fcg_block &B = a.blk;
+  pdl_trigger();
   kernel_prologue(sm, sh, B);
   tc::mbar_wait(&sh->wbar, 0);
-  load_w1_tmem(sm, sh->tmem);
+  load_w1_tmem(sm, sh->tmem);  // ends with the PDL wait
   const Wctx W = make_wctx(sm, sh, BWD_GCOLS);
   float4 *stash = (float4 *)(sm + SM_W1 + W.g * STASH_BYTES);
   const uint32_t sbase = tc::smem_u32(sm);
@@ -708,20 +728,20 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
   seg.acc = 0.f;
   seg.outc = GP + ch;
 
-  const float b0c = __ldg(&B.f0_b[ch]), b1c = __ldg(&B.f1_b[ch]);
-  const float rs0 = Q ? __ldg(&B.f0_s[ch]) : pow2f(-(B.f0_exp + 14));
+  const float b0c = ld_dep(&B.f0_b[ch]), b1c = ld_dep(&B.f1_b[ch]);
+  const float rs0 = Q ? ld_dep(&B.f0_s[ch]) : pow2f(-(B.f0_exp + 14));
   const float hs = Q ? 1.f : pow2f(B.f_hexp);
-  const float s1 = Q ? __ldg(&B.f1_s[ch]) : pow2f(-(B.f1_exp + B.f_hexp));
+  const float s1 = Q ? ld_dep(&B.f1_s[ch]) : pow2f(-(B.f1_exp + B.f_hexp));
   const float bsc = Q ? 1.f : 16384.f;
   // backward GEMMs against the stored fp16 weights fold the W16 dequant
   // scale of the contracted index into the operand: g @ (s*w16) == (g*s) @ w16
-  const float q1 = Q ? __ldg(&B.f1_s[ch]) : 1.f;
+  const float q1 = Q ? ld_dep(&B.f1_s[ch]) : 1.f;
   const float pmax = __uint_as_float(a.amax_pg[0]), ghmax = __uint_as_float(a.amax_pg[1]);
   const int sg = scale_exp(pmax * ghmax * B.f1_qmax);
   const float gws = pow2f(sg) * q1;
   const float sg3 = pow2f(-((Q ? 0 : B.f1_exp) + sg));
   const float dbs = pow2f(B.f_dbexp);
-  const float sdz = (Q ? __ldg(&B.f0_s[ch]) : pow2f(-B.f0_exp)) * pow2f(-B.f_dbexp);
+  const float sdz = (Q ? ld_dep(&B.f0_s[ch]) : pow2f(-B.f0_exp)) * pow2f(-B.f_dbexp);
 
   float4 ue = make_float4(0.f, 0.f, 0.f, 0.f), ue_n = ue;  // this lane's edge: (u, d)
   bool rows2 = true, rows2_n = true;
@@ -743,11 +763,11 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
     const int n_e = min(TT, tr.ee - t0);
     float gh[TT];  // grad_H[dst][ch] (flash.py:281)
 #pragma unroll
-    for (int i = 0; i < TT; ++i) gh[i] = __ldg(&GH[(size_t)M->nbr[i] * D + ch]);
+    for (int i = 0; i < TT; ++i) gh[i] = ld_gather(&GH[(size_t)M->nbr[i] * D + ch]);
     // P[src][ch] (flash.py:291): src = the tile's CSR rows, usually its
     // first and last only
     const int o_f = M->own[0], o_l = M->own[n_e - 1];
-    const float p_f = __ldg(&P[(size_t)o_f * D + ch]), p_l = __ldg(&P[(size_t)o_l * D + ch]);
+    const float p_f = ld_gather(&P[(size_t)o_f * D + ch]), p_l = ld_gather(&P[(size_t)o_l * D + ch]);
     W.wait(BAR_G1, it);
     PHASE(1, it, 1);
     tile_h_bwd<Q>(W, rs0, b0c, hs, stash);
@@ -770,7 +790,7 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *__restrict__ geo, const float2 *__
         for (int i = 0; i < 8; ++i) v[i] = gh[8 * j + i] * (oo[i] == o_l ? p_l : p_f);
       } else {  // a tile spanning 3+ rows: per-edge loads
 #pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = gh[8 * j + i] * __ldg(&P[(size_t)max(oo[i], 0) * D + ch]);
+        for (int i = 0; i < 8; ++i) v[i] = gh[8 * j + i] * ld_gather(&P[(size_t)max(oo[i], 0) * D + ch]);
       }
       put8<true>(W.hb, D, ch, 8 * j, v, gws);
     }
@@ -867,28 +887,22 @@ int edge_tc_units(int grid) { return NGRP * grid; }
 
 void launch_edge_geom(const EdgeArgs &a, float4 *geo, float2 *env, int32_t *unit_rows,
                       int nunits, cudaStream_t s) {
-  k_edge_geom<<<1184, 256, 0, s>>>(a.pos, a.ptr, a.nbr, a.own, a.nrows, a.cap_e, a.cutoff, geo,
-                                   env, unit_rows, nunits);
+  launch_pdl(PDL_GEOM, k_edge_geom, 1184, 256, 0, s, a.pos, a.ptr, a.nbr, a.own, a.nrows, a.cap_e, a.cutoff,
+             geo, env, unit_rows, nunits);
 }
 
 void launch_edge_fwd_tc(const EdgeArgs &a, const float4 *geo, const float2 *env,
                         const int32_t *unit_rows, const float *P, float *H, int grid,
                         cudaStream_t s) {
-  if (a.quant)
-    k_edge_fwd_tc<true><<<grid, TC_THREADS, SM_TOTAL + 1024, s>>>(a, geo, env, unit_rows, P, H);
-  else
-    k_edge_fwd_tc<false><<<grid, TC_THREADS, SM_TOTAL + 1024, s>>>(a, geo, env, unit_rows, P, H);
+  launch_pdl(PDL_EDGE_FWD, a.quant ? k_edge_fwd_tc<true> : k_edge_fwd_tc<false>, grid, TC_THREADS,
+             SM_TOTAL + 1024, s, a, geo, env, unit_rows, P, H);
 }
 
 void launch_edge_bwd_tc(const EdgeArgs &a, const float4 *geo, const float2 *env,
                         const int32_t *unit_rows, const float *P, const float *GH, float *GP,
                         float4 *gsum, int accumulate, int grid, cudaStream_t s) {
-  if (a.quant)
-    k_edge_bwd_tc<true><<<grid, TC_THREADS, SM_TOTAL + 1024, s>>>(a, geo, env, unit_rows, P, GH,
-                                                                  GP, gsum, accumulate);
-  else
-    k_edge_bwd_tc<false><<<grid, TC_THREADS, SM_TOTAL + 1024, s>>>(a, geo, env, unit_rows, P, GH,
-                                                                   GP, gsum, accumulate);
+  launch_pdl(PDL_EDGE_BWD, a.quant ? k_edge_bwd_tc<true> : k_edge_bwd_tc<false>, grid, TC_THREADS,
+             SM_TOTAL + 1024, s, a, geo, env, unit_rows, P, GH, GP, gsum, accumulate);
 }
 
 }  // namespace fcg

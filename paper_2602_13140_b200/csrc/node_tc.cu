@@ -51,6 +51,7 @@ __device__ __forceinline__ NodeCtx node_prologue(uint8_t *sm, NodeMeta *meta,
                                                  const uint16_t *img_a, uint32_t bytes_a,
                                                  const uint16_t *img_b = nullptr,
                                                  uint32_t bytes_b = 0) {
+  pdl_trigger();
   NodeCtx c;
   c.warp = threadIdx.x >> 5;
   c.lane = threadIdx.x & 31;
@@ -68,6 +69,10 @@ __device__ __forceinline__ NodeCtx node_prologue(uint8_t *sm, NodeMeta *meta,
   }
   if (threadIdx.x < 4) meta->amax[threadIdx.x] = 0u;
   if (threadIdx.x < 32) tc::tmem_alloc<256>(&meta->tmem);
+  // PDL wait right before the block barrier: ptxas moves ld.global.nc
+  // above griddepcontrol.wait alone, but not above bar.sync
+  // (tools/check_pdl.py); the weight images are in flight meanwhile.
+  pdl_wait();
   tc::fence_async_smem();
   tc::fence_before_sync();
   __syncthreads();
@@ -103,18 +108,18 @@ __device__ __forceinline__ void node_epilogue_end(NodeMeta *meta, const NodeCtx 
 // With a CSR row pointer, rows of nodes without edges read as zero: the
 // fused edge kernels write segment sums only for non-empty CSR rows (an
 // empty segment sums to zero, flash.py:109-135).  Returns the scale exponent.
-__device__ __forceinline__ int rows_to_act(const float *__restrict__ src, int node0, int nrows,
+__device__ __forceinline__ int rows_to_act(const float *src, int node0, int nrows,
                                            const NodeCtx &c, float colscale, bool q16_only,
                                            unsigned int *slot, uint8_t *act,
-                                           const int32_t *__restrict__ csr_ptr = nullptr) {
+                                           const int32_t *csr_ptr = nullptr) {
   float v[NPT];
   float mx = 0.f;
 #pragma unroll
   for (int i = 0; i < NPT; ++i) {
     int n = node0 + c.ec + i;
     const bool in = n < nrows;
-    float x = in ? __ldg(&src[(size_t)n * D + c.ch]) * colscale : 0.f;
-    if (csr_ptr && in && __ldg(&csr_ptr[n + 1]) == __ldg(&csr_ptr[n])) x = 0.f;
+    float x = in ? ld_dep(&src[(size_t)n * D + c.ch]) * colscale : 0.f;
+    if (csr_ptr && in && ld_dep(&csr_ptr[n + 1]) == ld_dep(&csr_ptr[n])) x = 0.f;
     if (q16_only) x = __half2float(__float2half_rn(x));
     v[i] = x;
     mx = fmaxf(mx, fabsf(x));
@@ -169,10 +174,10 @@ __device__ __forceinline__ void tmem_rows_to_act(uint32_t tcol, uint8_t *act, in
 // Y += G_in W   (grad_X += grad_P @ W_pre, flash.py:300)        [mode 1]
 template <int kMode>
 __global__ void __launch_bounds__(NTH, 1)
-k_node_linear_tc(const float *__restrict__ X, const uint16_t *__restrict__ img, int wexp,
-                 const float *__restrict__ bias, const float *__restrict__ rowscale, int quant,
-                 float *__restrict__ Y, int nrows, unsigned int *__restrict__ amax_out,
-                 const int32_t *__restrict__ csr_ptr) {
+k_node_linear_tc(const float *X, const uint16_t *img, int wexp,
+                 const float *bias, const float *rowscale, int quant,
+                 float *Y, int nrows, unsigned int *amax_out,
+                 const int32_t *csr_ptr) {
   extern __shared__ __align__(1024) uint8_t sm[];
   NodeMeta *meta = (NodeMeta *)(sm + NSM_META);
   uint8_t *act = sm + NSM_ACT;
@@ -180,7 +185,7 @@ k_node_linear_tc(const float *__restrict__ X, const uint16_t *__restrict__ img, 
   const int node0 = blockIdx.x * NN;
   const bool fwd = kMode == 0;
   // backward folds the W16 row scale of the K index (output channel) into X
-  const float fold = (!fwd && quant) ? __ldg(&rowscale[c.ch]) : 1.f;
+  const float fold = (!fwd && quant) ? ld_dep(&rowscale[c.ch]) : 1.f;
   const int s = rows_to_act(X, node0, nrows, c, fold, fwd && quant, &meta->amax[0], act, csr_ptr);
   NODE_ISSUE(c.tm + NTM_D0, c.sbase + NSM_WA, IMG128, D, !fwd, c.sbase + NSM_ACT, D,
              tc::idesc_f16(128, NN, fwd ? 0 : 1, 1), quant ? (fwd ? 1 : 2) : 3);
@@ -192,8 +197,8 @@ k_node_linear_tc(const float *__restrict__ X, const uint16_t *__restrict__ img, 
     yv[i] = (!fwd && n < nrows) ? Y[(size_t)n * D + c.ch] : 0.f;
   }
   NODE_WAIT();
-  const float un = pow2f(-((quant ? 0 : wexp) + s)) * ((fwd && quant) ? __ldg(&rowscale[c.ch]) : 1.f);
-  const float b = fwd ? __ldg(&bias[c.ch]) : 0.f;
+  const float un = pow2f(-((quant ? 0 : wexp) + s)) * ((fwd && quant) ? ld_dep(&rowscale[c.ch]) : 1.f);
+  const float b = fwd ? ld_dep(&bias[c.ch]) : 0.f;
   float mx = 0.f;
 #pragma unroll
   for (int c0 = 0; c0 < NPT; c0 += 16) {
@@ -217,9 +222,9 @@ k_node_linear_tc(const float *__restrict__ X, const uint16_t *__restrict__ img, 
 // post MLP + residual (flash.py:240-241): Zp = H Wp0^T + b0 (kept for the
 // backward), U = ssp(Zp) Wp1^T + b1, X += U.
 __global__ void __launch_bounds__(NTH, 1)
-k_node_post_tc(const float *__restrict__ H, const fcg_block blk, int quant,
-               float *__restrict__ Zp, float *__restrict__ X, int nrows,
-               const int32_t *__restrict__ csr_ptr) {
+k_node_post_tc(const float *H, const fcg_block blk, int quant,
+               float *Zp, float *X, int nrows,
+               const int32_t *csr_ptr) {
   extern __shared__ __align__(1024) uint8_t sm[];
   NodeMeta *meta = (NodeMeta *)(sm + NSM_META);
   uint8_t *act = sm + NSM_ACT;
@@ -230,8 +235,8 @@ k_node_post_tc(const float *__restrict__ H, const fcg_block blk, int quant,
   const int s0 = rows_to_act(H, node0, nrows, c, 1.f, quant, &meta->amax[0], act, csr_ptr);
   NODE_ISSUE(c.tm + NTM_D0, c.sbase + NSM_WA, IMG128, D, false, c.sbase + NSM_ACT, D, idesc, np);
   NODE_WAIT();
-  const float un0 = quant ? __ldg(&blk.p0_s[c.ch]) : pow2f(-(blk.p0_exp + s0));
-  const float b0 = __ldg(&blk.p0_b[c.ch]);
+  const float un0 = quant ? ld_dep(&blk.p0_s[c.ch]) : pow2f(-(blk.p0_exp + s0));
+  const float b0 = ld_dep(&blk.p0_b[c.ch]);
   float mx = 0.f;
 #pragma unroll
   for (int c0 = 0; c0 < NPT; c0 += 16) {
@@ -262,8 +267,8 @@ k_node_post_tc(const float *__restrict__ H, const fcg_block blk, int quant,
     xv[i] = n < nrows ? X[(size_t)n * D + c.ch] : 0.f;
   }
   NODE_WAIT();
-  const float un1 = quant ? __ldg(&blk.p1_s[c.ch]) : pow2f(-(blk.p1_exp + s1));
-  const float b1 = __ldg(&blk.p1_b[c.ch]);
+  const float un1 = quant ? ld_dep(&blk.p1_s[c.ch]) : pow2f(-(blk.p1_exp + s1));
+  const float b1 = ld_dep(&blk.p1_b[c.ch]);
 #pragma unroll
   for (int c0 = 0; c0 < NPT; c0 += 16) {
     float v[16];
@@ -280,9 +285,9 @@ k_node_post_tc(const float *__restrict__ H, const fcg_block blk, int quant,
 // Backward of the post MLP (mlp_backward_input, model.py:321-332; called at
 // flash.py:264): GH = ((G Wp1) * ssp'(Zp)) Wp0, on dequantised weights.
 __global__ void __launch_bounds__(NTH, 1)
-k_node_post_bwd_tc(const float *__restrict__ G, const fcg_block blk, int quant,
-                   const float *__restrict__ Zp, float *__restrict__ GH, int nrows,
-                   unsigned int *__restrict__ amax_out) {
+k_node_post_bwd_tc(const float *G, const fcg_block blk, int quant,
+                   const float *Zp, float *GH, int nrows,
+                   unsigned int *amax_out) {
   extern __shared__ __align__(1024) uint8_t sm[];
   NodeMeta *meta = (NodeMeta *)(sm + NSM_META);
   uint8_t *act = sm + NSM_ACT;
@@ -290,7 +295,7 @@ k_node_post_bwd_tc(const float *__restrict__ G, const fcg_block blk, int quant,
   const int node0 = blockIdx.x * NN;
   const int np = quant ? 2 : 3;
   const uint32_t idesc = tc::idesc_f16(128, NN, 1, 1);
-  const float f1 = quant ? __ldg(&blk.p1_s[c.ch]) : 1.f;
+  const float f1 = quant ? ld_dep(&blk.p1_s[c.ch]) : 1.f;
   const int sg = rows_to_act(G, node0, nrows, c, f1, false, &meta->amax[0], act);
   NODE_ISSUE(c.tm + NTM_D0, c.sbase + NSM_WA, IMG128, D, true, c.sbase + NSM_ACT, D, idesc, np);
   // ssp'(Zp) operands are fetched while the GEMM runs
@@ -298,11 +303,11 @@ k_node_post_bwd_tc(const float *__restrict__ G, const fcg_block blk, int quant,
 #pragma unroll
   for (int i = 0; i < NPT; ++i) {
     const int n = node0 + c.ec + i;
-    zv[i] = n < nrows ? __ldg(&Zp[(size_t)n * D + c.ch]) : 0.f;
+    zv[i] = n < nrows ? ld_dep(&Zp[(size_t)n * D + c.ch]) : 0.f;
   }
   NODE_WAIT();
   const float un = pow2f(-((quant ? 0 : blk.p1_exp) + sg));
-  const float f0 = quant ? __ldg(&blk.p0_s[c.ch]) : 1.f;
+  const float f0 = quant ? ld_dep(&blk.p0_s[c.ch]) : 1.f;
   float mx = 0.f;
 #pragma unroll
   for (int c0 = 0; c0 < NPT; c0 += 16) {
@@ -345,8 +350,8 @@ k_node_post_bwd_tc(const float *__restrict__ G, const fcg_block blk, int quant,
 // the ones-seeded backward G = (wr1 * ssp'(zr)) Wr0.  Layer 0 has 64
 // outputs: an M=64 GEMM whose row k lives in TMEM lane 32(k/16) + k%16.
 __global__ void __launch_bounds__(NTH, 1)
-k_readout_tc(const float *__restrict__ X, const fcg_model m, float *__restrict__ per_atom,
-             float *__restrict__ G, int nrows) {
+k_readout_tc(const float *X, const fcg_model m, float *per_atom,
+             float *G, int nrows) {
   extern __shared__ __align__(1024) uint8_t sm[];
   NodeMeta *meta = (NodeMeta *)(sm + NSM_META);
   uint8_t *act = sm + NSM_ACT;
@@ -360,10 +365,10 @@ k_readout_tc(const float *__restrict__ X, const fcg_model m, float *__restrict__
   NODE_WAIT();
   const int k = 16 * c.quarter + (c.lane & 15);
   const bool row_lane = c.lane < 16;
-  const float un = quant ? __ldg(&m.r0_s[k]) : pow2f(-(m.r0_exp + sx));
-  const float b0 = __ldg(&m.r0_b[k]);
-  const float w1 = __ldg(&m.r1_w[k]);
-  const float fold = quant ? __ldg(&m.r0_s[k]) : 1.f;
+  const float un = quant ? ld_dep(&m.r0_s[k]) : pow2f(-(m.r0_exp + sx));
+  const float b0 = ld_dep(&m.r0_b[k]);
+  const float w1 = ld_dep(&m.r1_w[k]);
+  const float fold = quant ? ld_dep(&m.r0_s[k]) : 1.f;
   float mx = 0.f;
 #pragma unroll
   for (int c0 = 0; c0 < NPT; c0 += 16) {
@@ -429,27 +434,27 @@ static inline int node_grid(int nrows) { return (nrows + NN - 1) / NN; }
 
 void launch_node_pre_tc(const float *X, const fcg_block &b, int quant, float *P, int nrows,
                         unsigned int *amax_p, cudaStream_t s) {
-  k_node_linear_tc<0><<<node_grid(nrows), NTH, NSM_TOTAL + 1024, s>>>(
+  launch_pdl(PDL_NODE_PRE, k_node_linear_tc<0>, node_grid(nrows), NTH, NSM_TOTAL + 1024, s,
       X, b.pre_img, b.pre_exp, b.pre_b, b.pre_s, quant, P, nrows, amax_p, nullptr);
 }
 void launch_node_pre_bwd_tc(const float *GP, const fcg_block &b, int quant, float *G, int nrows,
                             const int32_t *csr_ptr, cudaStream_t s) {
-  k_node_linear_tc<1><<<node_grid(nrows), NTH, NSM_TOTAL + 1024, s>>>(
+  launch_pdl(PDL_NODE_PRE_BWD, k_node_linear_tc<1>, node_grid(nrows), NTH, NSM_TOTAL + 1024, s,
       GP, b.pre_img, b.pre_exp, nullptr, b.pre_s, quant, G, nrows, nullptr, csr_ptr);
 }
 void launch_node_post_tc(const float *H, const fcg_block &b, int quant, float *Zp, float *X,
                          int nrows, const int32_t *csr_ptr, cudaStream_t s) {
-  k_node_post_tc<<<node_grid(nrows), NTH, NSM_TOTAL + 1024, s>>>(H, b, quant, Zp, X, nrows,
-                                                                csr_ptr);
+  launch_pdl(PDL_NODE_POST, k_node_post_tc, node_grid(nrows), NTH, NSM_TOTAL + 1024, s, H, b, quant, Zp, X,
+             nrows, csr_ptr);
 }
 void launch_node_post_bwd_tc(const float *G, const fcg_block &b, int quant, const float *Zp,
                              float *GH, int nrows, unsigned int *amax_gh, cudaStream_t s) {
-  k_node_post_bwd_tc<<<node_grid(nrows), NTH, NSM_TOTAL + 1024, s>>>(G, b, quant, Zp, GH, nrows,
-                                                                    amax_gh);
+  launch_pdl(PDL_NODE_POST_BWD, k_node_post_bwd_tc, node_grid(nrows), NTH, NSM_TOTAL + 1024, s, G, b, quant, Zp, GH,
+             nrows, amax_gh);
 }
 void launch_readout_tc(const float *X, const fcg_model &m, float *per_atom, float *G, int nrows,
                        cudaStream_t s) {
-  k_readout_tc<<<node_grid(nrows), NTH, NSM_TOTAL + 1024, s>>>(X, m, per_atom, G, nrows);
+  launch_pdl(PDL_READOUT, k_readout_tc, node_grid(nrows), NTH, NSM_TOTAL + 1024, s, X, m, per_atom, G, nrows);
 }
 
 }  // namespace fcg

@@ -251,3 +251,22 @@ def test_traffic_report_matches_reference_schedules():
                              len(src), cfg.hidden_dim, cfg.rbf_dim, cfg.num_blocks,
                              np.dtype(c["dtype"]).itemsize)
         assert rep.as_dict() == c["traffic"], (c["kind"], c["dtype"], c["fused"], c["segred"])
+
+
+def test_pdl_kernels_load_nothing_before_the_grid_dependency_wait():
+    """PDL-launched kernels must not read step data before griddepcontrol.wait
+    (ACQBULK): ptxas hoists ld.global.nc above it (tools/check_pdl.py)."""
+    import importlib.util
+    import shutil
+
+    lib = ROOT / "paper_2602_13140_b200" / "libfcg.so"
+    if not lib.exists() or not shutil.which("cuobjdump"):
+        pytest.skip("needs the built library and cuobjdump")
+    spec = importlib.util.spec_from_file_location("check_pdl", ROOT / "tools" / "check_pdl.py")
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    res = mod.early_loads(str(lib))
+    assert {k for k in mod.PDL_KERNELS if any(k in f for f in res)} == set(mod.PDL_KERNELS)
+    for fn, r in res.items():
+        assert r["wait"], fn
+        assert not r["early"], (fn, r["early"][:4])
