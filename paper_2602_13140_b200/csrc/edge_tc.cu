@@ -474,7 +474,7 @@ __device__ __forceinline__ void tile_basis(const EdgeArgs &a, const Wctx &W, con
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const float dl = dd[i] - mu;
-      const float gs = (Q && !DERIV) ? expf((-a.gamma * dl) * dl) : ex2_ftz((ngl * dl) * dl);
+            const float gs = ex2_ftz((ngl * dl) * dl);
       v[4 * j + i] = DERIV ? gs * (g2 * dl * cc[i] + pp[i]) : gs * cc[i];
     }
   }
@@ -492,7 +492,7 @@ __device__ __forceinline__ void tile_h(const Wctx &W, float rs0, float b0c, floa
   tc::tmem_ld32w(W.tl + S0, v);
 #pragma unroll
   for (int i = 0; i < TT; ++i) {
-    if (Q) v[i] = __half2float(__float2half_rn(ssp_ref(v[i] * rs0 + b0c)));
+    if (Q) v[i] = __half2float(__float2half_rn(ssp_fast(v[i] * rs0 + b0c)));
     else v[i] = ssp_fast(v[i] * rs0 + b0c);
   }
 #pragma unroll
@@ -686,7 +686,7 @@ __device__ __forceinline__ void tile_h_bwd(const Wctx &W, float rs0, float b0c, 
       const float z = v[i + j] * rs0 + b0c;
       if (Q) {
         s[j] = sigmoid_fast(z);
-        v[i + j] = __half2float(__float2half_rn(ssp_ref(z)));
+        v[i + j] = __half2float(__float2half_rn(ssp_fast(z)));
       } else {
         v[i + j] = ssp_fast(z);
         s[j] = fmaf(-0.5f, ex2_ftz(v[i + j] * -kLog2e), 1.f);

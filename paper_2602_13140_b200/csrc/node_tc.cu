@@ -248,7 +248,7 @@ k_node_post_tc(const float *H, const fcg_block blk, int quant,
       int n = node0 + c.ec + c0 + i;
       float z = v[i] * un0 + b0;
       if (n < nrows) Zp[(size_t)n * D + c.ch] = z;
-      const float a = quant ? __half2float(__float2half_rn(ssp_ref(z))) : ssp_fast(z);
+      const float a = quant ? __half2float(__float2half_rn(ssp_fast(z))) : ssp_fast(z);
       v[i] = n < nrows ? a : 0.f;
       mx = fmaxf(mx, fabsf(v[i]));
     }
@@ -381,7 +381,7 @@ k_readout_tc(const float *X, const fcg_model m, float *per_atom,
         int e = c.ec + c0 + i;
         bool ok = node0 + e < nrows;
         float z = v[i] * un + b0;
-        const float a = quant ? __half2float(__float2half_rn(ssp_ref(z))) : ssp_fast(z);
+        const float a = quant ? __half2float(__float2half_rn(ssp_fast(z))) : ssp_fast(z);
         red[e * 65 + k] = ok ? a * w1 : 0.f;
         v[i] = ok ? w1 * sigmoid_fast(z) * fold : 0.f;
         mx = fmaxf(mx, fabsf(v[i]));

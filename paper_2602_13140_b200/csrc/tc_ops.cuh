@@ -132,15 +132,13 @@ constexpr float kLn2 = 0.6931471805599453f;
 
 // shifted softplus max(x,0) + log1p(exp(-|x|)) - ln2 (model.py:93-100) and
 // its derivative sigmoid(x) (model.py:103-107) on MUFU ex2/lg2/rcp (abs.
-// error ~1e-7)
+// error ~1e-7).  Used by the W16 path as well: its fp16 activation rounding
+// turns the ~1e-7 difference from NumPy's expf/log1pf into occasional
+// rounding flips (~1e-4 relative energy on tiny systems), far inside the
+// reference's own W16 contract (1e-2 vs fp32, tests/test_quantize.py:169),
+// while CUDA's accurate expf/log1pf cost 37% of the W16 step.
 __device__ __forceinline__ float ssp_fast(float x) {
   return fmaf(kLn2, lg2_ftz(1.f + ex2_ftz(fabsf(x) * -kLog2e)) - 1.f, fmaxf(x, 0.f));
-}
-// ssp in the reference's fp32 op order with accurate expf/log1pf: the W16
-// path rounds every activation to fp16, which turns MUFU-level error into
-// rounding flips (quantize.py:68-71, :86).
-__device__ __forceinline__ float ssp_ref(float x) {
-  return fmaxf(x, 0.f) + log1pf(expf(-fabsf(x))) - 0.6931471805599453f;
 }
 __device__ __forceinline__ float sigmoid_fast(float x) {
   return rcp_ftz(1.f + ex2_ftz(x * -kLog2e));
