@@ -19,16 +19,11 @@
 
 namespace fcg {
 
-constexpr int NN = 128;           // node rows per CTA (MMA N)
-constexpr int NTH = 512;          // 16 warps
-constexpr int NPT = NN / 4;       // nodes per thread
-constexpr uint32_t NSM_WA = 0;         // first weight image (hi|lo, <= 64 KB)
-constexpr uint32_t NSM_WB = 65536;     // second weight image
-constexpr uint32_t NSM_ACT = 131072;   // B operand hi|lo / fp32 scratch (64 KB)
-constexpr uint32_t NSM_META = 196608;
+constexpr int NPT = 32;  // nodes per thread (one channel each)
 constexpr uint32_t IMG128 = 128 * 128 * 2;  // bytes of one 128x128 fp16 image half
 constexpr uint32_t IMG64 = 64 * 128 * 2;
 constexpr uint32_t NTM_D0 = 0, NTM_D1 = 128;
+constexpr uint32_t NSM_WA = 0, NSM_WB = 65536;  // weight image slots (hi|lo, <= 64 KB each)
 
 struct NodeMeta {
   unsigned int amax[4];
@@ -36,7 +31,57 @@ struct NodeMeta {
   uint64_t wbar;  // weight images landed (bulk copy)
   uint32_t tmem;
 };
-constexpr uint32_t NSM_TOTAL = NSM_META + sizeof(NodeMeta);
+
+// Tile shape and shared-memory layout of a node kernel: kNN node rows per
+// CTA (MMA N) with 128 channels x kNN/NPT node parts = 4 kNN threads, kNW
+// staged weight images (64 KB slots), then the B operand (K=128 x kNN,
+// hi|lo).  The one-image kernels run 64-node CTAs so two fit per SM (smem
+// ~99 KB, 256 threads x 128 registers): one CTA's row loads then overlap
+// the other's GEMM and epilogue.  The two-image post kernels need 160 KB
+// even at 64 nodes and keep 128-node CTAs.
+#ifndef FCG_NN_ONE
+#define FCG_NN_ONE 64
+#endif
+template <int kNN, int kNW>
+struct NodeCfg {
+  static constexpr int NN = kNN;
+  static constexpr int NTH = 4 * kNN;
+  static constexpr int MIN_CTAS = 512 / NTH;
+  static constexpr uint32_t KSTR = (uint32_t)(kNN / 8) * 128u;  // B bytes per 8 K-rows
+  static constexpr uint32_t WA = NSM_WA, WB = NSM_WB;
+  static constexpr uint32_t ACT = (uint32_t)kNW * 65536u;
+  static constexpr uint32_t ACT_BYTES = 2u * 128u * (uint32_t)kNN * 2u;
+  static constexpr uint32_t META = ACT + ACT_BYTES;
+  static constexpr uint32_t SMEM = META + (uint32_t)sizeof(NodeMeta) + 1024u;
+  static_assert(RH * 65 * 4 <= ACT_BYTES * 2, "readout scratch fits the B operand area");
+};
+using CfgLin = NodeCfg<FCG_NN_ONE, 1>;
+using CfgRo = NodeCfg<FCG_NN_ONE, 1>;
+using CfgPost = NodeCfg<128, 2>;
+
+// Diagnostic phase stamps (tools/diag_node_phase.py, -DFCG_NODE_STAMPS): with
+// fcg_debug_phase_buffer set, thread 0 of every CTA records clock64() at
+// phase `ph` of launch kind `kind` (the last launch of a kind wins) and
+// %globaltimer at entry (slot 6) and exit (slot 7).
+__device__ unsigned long long *d_node_dbg = nullptr;
+__device__ __forceinline__ void node_stamp(int kind, int ph) {
+#ifdef FCG_NODE_STAMPS  // diagnostic builds only: reads d_node_dbg before the PDL wait
+  unsigned long long *b = d_node_dbg;
+  if (b && threadIdx.x == 0) {
+    unsigned long long t;
+    if (ph >= 6) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    else t = clock64();
+    b[4096 + ((size_t)kind * 1024 + blockIdx.x) * 8 + ph] = t;
+  }
+#endif
+}
+static void node_dbg_sync() {
+  static unsigned long long *cur = nullptr;
+  if (g_dbg_phase != cur) {
+    cur = g_dbg_phase;
+    cudaMemcpyToSymbol(d_node_dbg, &cur, sizeof(cur));
+  }
+}
 
 struct NodeCtx {
   int warp, lane, quarter, part, ch, ec;
@@ -102,16 +147,28 @@ __device__ __forceinline__ void node_epilogue_end(NodeMeta *meta, const NodeCtx 
   if (threadIdx.x < 32) tc::tmem_dealloc<256>(c.tm);
 }
 
-// Rows [node0, node0+128) of a [nrows][128] fp32 matrix (times a per-channel
+// Rows [node0, node0+NN) of a [nrows][128] fp32 matrix (times a per-channel
 // factor) -> MN-major B operand (row = channel).  Forward W16 operands are
 // fp16-rounded and unscaled; otherwise split hi/lo with a block-max scale.
 // With a CSR row pointer, rows of nodes without edges read as zero: the
 // fused edge kernels write segment sums only for non-empty CSR rows (an
 // empty segment sums to zero, flash.py:109-135).  Returns the scale exponent.
+template <uint32_t KSTR>
 __device__ __forceinline__ int rows_to_act(const float *src, int node0, int nrows,
                                            const NodeCtx &c, float colscale, bool q16_only,
                                            unsigned int *slot, uint8_t *act,
                                            const int32_t *csr_ptr = nullptr) {
+  // empty-row mask of the warp's NPT (= 32) nodes: lane l reads ptr[n0+l],
+  // its neighbour's value is ptr[n0+l+1]
+  uint32_t empty = 0u;
+  if (csr_ptr) {
+    const int n0 = node0 + c.ec, nl = n0 + c.lane;
+    const int a = ld_dep(&csr_ptr[min(nl, nrows)]);
+    const int b31 = ld_dep(&csr_ptr[min(n0 + 32, nrows)]);
+    const int up = __shfl_down_sync(0xffffffffu, a, 1);
+    empty = __ballot_sync(0xffffffffu, nl < nrows && (c.lane == 31 ? b31 : up) == a);
+  }
+  static_assert(NPT == 32, "one warp lane per node of the thread's range");
   float v[NPT];
   float mx = 0.f;
 #pragma unroll
@@ -119,7 +176,7 @@ __device__ __forceinline__ int rows_to_act(const float *src, int node0, int nrow
     int n = node0 + c.ec + i;
     const bool in = n < nrows;
     float x = in ? ld_dep(&src[(size_t)n * D + c.ch]) * colscale : 0.f;
-    if (csr_ptr && in && ld_dep(&csr_ptr[n + 1]) == ld_dep(&csr_ptr[n])) x = 0.f;
+    if ((empty >> i) & 1u) x = 0.f;
     if (q16_only) x = __half2float(__float2half_rn(x));
     v[i] = x;
     mx = fmaxf(mx, fabsf(x));
@@ -128,12 +185,14 @@ __device__ __forceinline__ int rows_to_act(const float *src, int node0, int nrow
   if (!q16_only) s = scale_exp(block_amax(mx, slot));
   const float sc = pow2f(s);
 #pragma unroll
-  for (int g = 0; g < NPT / 8; ++g) put_b8(act, D, c.ch, c.ec + 8 * g, &v[8 * g], sc, !q16_only);
+  for (int g = 0; g < NPT / 8; ++g)
+    put_b8n(act, D, KSTR, c.ch, c.ec + 8 * g, &v[8 * g], sc, !q16_only);
   return s;
 }
 
 // TMEM block [ch][32 nodes] -> B operand rows (K = rows of act).  The TMEM
 // loads are warp-collective, so every lane runs them; `active` lanes store.
+template <uint32_t KSTR>
 __device__ __forceinline__ void tmem_rows_to_act(uint32_t tcol, uint8_t *act, int K, int row,
                                                  int ec, float scale, bool with_lo,
                                                  bool active = true) {
@@ -143,8 +202,8 @@ __device__ __forceinline__ void tmem_rows_to_act(uint32_t tcol, uint8_t *act, in
     tc::tmem_ld16(tcol + ec + c0, v);
     tc::tmem_ld_wait();
     if (active) {
-      put_b8(act, K, row, ec + c0, &v[0], scale, with_lo);
-      put_b8(act, K, row, ec + c0 + 8, &v[8], scale, with_lo);
+      put_b8n(act, K, KSTR, row, ec + c0, &v[0], scale, with_lo);
+      put_b8n(act, K, KSTR, row, ec + c0 + 8, &v[8], scale, with_lo);
     }
   }
 }
@@ -157,7 +216,7 @@ __device__ __forceinline__ void tmem_rows_to_act(uint32_t tcol, uint8_t *act, in
     if (threadIdx.x == 0) {             \
       tc::mbar_wait(&meta->wbar, 0);    \
       tc::fence_after_sync();           \
-      issue_gemm(__VA_ARGS__);          \
+      issue_gemm(__VA_ARGS__, Cfg::KSTR);\
       tc::mma_commit(&meta->bar);       \
     }                                   \
   } while (0)
@@ -173,22 +232,27 @@ __device__ __forceinline__ void tmem_rows_to_act(uint32_t tcol, uint8_t *act, in
 // Y = X W^T + b (pre-linear, flash.py:207)                      [mode 0]
 // Y += G_in W   (grad_X += grad_P @ W_pre, flash.py:300)        [mode 1]
 template <int kMode>
-__global__ void __launch_bounds__(NTH, 1)
+__global__ void __launch_bounds__(CfgLin::NTH, CfgLin::MIN_CTAS)
 k_node_linear_tc(const float *X, const uint16_t *img, int wexp,
                  const float *bias, const float *rowscale, int quant,
                  float *Y, int nrows, unsigned int *amax_out,
                  const int32_t *csr_ptr) {
+  using Cfg = CfgLin;
+  node_stamp(kMode, 6);
+  node_stamp(kMode, 0);
   extern __shared__ __align__(1024) uint8_t sm[];
-  NodeMeta *meta = (NodeMeta *)(sm + NSM_META);
-  uint8_t *act = sm + NSM_ACT;
+  NodeMeta *meta = (NodeMeta *)(sm + Cfg::META);
+  uint8_t *act = sm + Cfg::ACT;
   NodeCtx c = node_prologue(sm, meta, img, 2 * IMG128);
-  const int node0 = blockIdx.x * NN;
+  node_stamp(kMode, 1);
+  const int node0 = blockIdx.x * Cfg::NN;
   const bool fwd = kMode == 0;
   // backward folds the W16 row scale of the K index (output channel) into X
   const float fold = (!fwd && quant) ? ld_dep(&rowscale[c.ch]) : 1.f;
-  const int s = rows_to_act(X, node0, nrows, c, fold, fwd && quant, &meta->amax[0], act, csr_ptr);
-  NODE_ISSUE(c.tm + NTM_D0, c.sbase + NSM_WA, IMG128, D, !fwd, c.sbase + NSM_ACT, D,
-             tc::idesc_f16(128, NN, fwd ? 0 : 1, 1), quant ? (fwd ? 1 : 2) : 3);
+  const int s = rows_to_act<Cfg::KSTR>(X, node0, nrows, c, fold, fwd && quant, &meta->amax[0], act, csr_ptr);
+  node_stamp(kMode, 2);
+  NODE_ISSUE(c.tm + NTM_D0, c.sbase + Cfg::WA, IMG128, D, !fwd, c.sbase + Cfg::ACT, D,
+             tc::idesc_f16(128, Cfg::NN, fwd ? 0 : 1, 1), quant ? (fwd ? 1 : 2) : 3);
   // the accumulated operand (backward) is fetched while the GEMM runs
   float yv[NPT];
 #pragma unroll
@@ -197,6 +261,7 @@ k_node_linear_tc(const float *X, const uint16_t *img, int wexp,
     yv[i] = (!fwd && n < nrows) ? Y[(size_t)n * D + c.ch] : 0.f;
   }
   NODE_WAIT();
+  node_stamp(kMode, 3);
   const float un = pow2f(-((quant ? 0 : wexp) + s)) * ((fwd && quant) ? ld_dep(&rowscale[c.ch]) : 1.f);
   const float b = fwd ? ld_dep(&bias[c.ch]) : 0.f;
   float mx = 0.f;
@@ -216,25 +281,33 @@ k_node_linear_tc(const float *X, const uint16_t *img, int wexp,
     }
   }
   global_amax(mx, amax_out, &meta->amax[3]);
+  node_stamp(kMode, 4);
   node_epilogue_end(meta, c);
+  node_stamp(kMode, 7);
 }
 
 // post MLP + residual (flash.py:240-241): Zp = H Wp0^T + b0 (kept for the
 // backward), U = ssp(Zp) Wp1^T + b1, X += U.
-__global__ void __launch_bounds__(NTH, 1)
+__global__ void __launch_bounds__(CfgPost::NTH, CfgPost::MIN_CTAS)
 k_node_post_tc(const float *H, const fcg_block blk, int quant,
                float *Zp, float *X, int nrows,
                const int32_t *csr_ptr) {
+  using Cfg = CfgPost;
+  node_stamp(2, 6);
+  node_stamp(2, 0);
   extern __shared__ __align__(1024) uint8_t sm[];
-  NodeMeta *meta = (NodeMeta *)(sm + NSM_META);
-  uint8_t *act = sm + NSM_ACT;
+  NodeMeta *meta = (NodeMeta *)(sm + Cfg::META);
+  uint8_t *act = sm + Cfg::ACT;
   NodeCtx c = node_prologue(sm, meta, blk.p0_img, 2 * IMG128, blk.p1_img, 2 * IMG128);
-  const int node0 = blockIdx.x * NN;
+  node_stamp(2, 1);
+  const int node0 = blockIdx.x * Cfg::NN;
   const int np = quant ? 1 : 3;
-  const uint32_t idesc = tc::idesc_f16(128, NN, 0, 1);
-  const int s0 = rows_to_act(H, node0, nrows, c, 1.f, quant, &meta->amax[0], act, csr_ptr);
-  NODE_ISSUE(c.tm + NTM_D0, c.sbase + NSM_WA, IMG128, D, false, c.sbase + NSM_ACT, D, idesc, np);
+  const uint32_t idesc = tc::idesc_f16(128, Cfg::NN, 0, 1);
+  const int s0 = rows_to_act<Cfg::KSTR>(H, node0, nrows, c, 1.f, quant, &meta->amax[0], act, csr_ptr);
+  node_stamp(2, 2);
+  NODE_ISSUE(c.tm + NTM_D0, c.sbase + Cfg::WA, IMG128, D, false, c.sbase + Cfg::ACT, D, idesc, np);
   NODE_WAIT();
+  node_stamp(2, 3);
   const float un0 = quant ? ld_dep(&blk.p0_s[c.ch]) : pow2f(-(blk.p0_exp + s0));
   const float b0 = ld_dep(&blk.p0_b[c.ch]);
   float mx = 0.f;
@@ -257,8 +330,9 @@ k_node_post_tc(const float *H, const fcg_block blk, int quant,
   tc::tmem_st_wait();
   int s1 = 0;
   if (!quant) s1 = scale_exp(block_amax(mx, &meta->amax[1]));
-  tmem_rows_to_act(c.tl + NTM_D0, act, D, c.ch, c.ec, pow2f(s1), !quant);
-  NODE_ISSUE(c.tm + NTM_D1, c.sbase + NSM_WB, IMG128, D, false, c.sbase + NSM_ACT, D, idesc, np);
+  tmem_rows_to_act<Cfg::KSTR>(c.tl + NTM_D0, act, D, c.ch, c.ec, pow2f(s1), !quant);
+  NODE_ISSUE(c.tm + NTM_D1, c.sbase + Cfg::WB, IMG128, D, false, c.sbase + Cfg::ACT, D, idesc, np);
+  node_stamp(2, 4);
   // the residual stream is fetched while the GEMM runs
   float xv[NPT];
 #pragma unroll
@@ -279,25 +353,32 @@ k_node_post_tc(const float *H, const fcg_block blk, int quant,
       if (n < nrows) X[(size_t)n * D + c.ch] = xv[c0 + i] + (v[i] * un1 + b1);
     }
   }
+  node_stamp(2, 5);
   node_epilogue_end(meta, c);
+  node_stamp(2, 7);
 }
 
 // Backward of the post MLP (mlp_backward_input, model.py:321-332; called at
 // flash.py:264): GH = ((G Wp1) * ssp'(Zp)) Wp0, on dequantised weights.
-__global__ void __launch_bounds__(NTH, 1)
+__global__ void __launch_bounds__(CfgPost::NTH, CfgPost::MIN_CTAS)
 k_node_post_bwd_tc(const float *G, const fcg_block blk, int quant,
                    const float *Zp, float *GH, int nrows,
                    unsigned int *amax_out) {
+  using Cfg = CfgPost;
+  node_stamp(3, 6);
+  node_stamp(3, 0);
   extern __shared__ __align__(1024) uint8_t sm[];
-  NodeMeta *meta = (NodeMeta *)(sm + NSM_META);
-  uint8_t *act = sm + NSM_ACT;
+  NodeMeta *meta = (NodeMeta *)(sm + Cfg::META);
+  uint8_t *act = sm + Cfg::ACT;
   NodeCtx c = node_prologue(sm, meta, blk.p1_img, 2 * IMG128, blk.p0_img, 2 * IMG128);
-  const int node0 = blockIdx.x * NN;
+  node_stamp(3, 1);
+  const int node0 = blockIdx.x * Cfg::NN;
   const int np = quant ? 2 : 3;
-  const uint32_t idesc = tc::idesc_f16(128, NN, 1, 1);
+  const uint32_t idesc = tc::idesc_f16(128, Cfg::NN, 1, 1);
   const float f1 = quant ? ld_dep(&blk.p1_s[c.ch]) : 1.f;
-  const int sg = rows_to_act(G, node0, nrows, c, f1, false, &meta->amax[0], act);
-  NODE_ISSUE(c.tm + NTM_D0, c.sbase + NSM_WA, IMG128, D, true, c.sbase + NSM_ACT, D, idesc, np);
+  const int sg = rows_to_act<Cfg::KSTR>(G, node0, nrows, c, f1, false, &meta->amax[0], act);
+  node_stamp(3, 2);
+  NODE_ISSUE(c.tm + NTM_D0, c.sbase + Cfg::WA, IMG128, D, true, c.sbase + Cfg::ACT, D, idesc, np);
   // ssp'(Zp) operands are fetched while the GEMM runs
   float zv[NPT];
 #pragma unroll
@@ -306,6 +387,7 @@ k_node_post_bwd_tc(const float *G, const fcg_block blk, int quant,
     zv[i] = n < nrows ? ld_dep(&Zp[(size_t)n * D + c.ch]) : 0.f;
   }
   NODE_WAIT();
+  node_stamp(3, 3);
   const float un = pow2f(-((quant ? 0 : blk.p1_exp) + sg));
   const float f0 = quant ? ld_dep(&blk.p0_s[c.ch]) : 1.f;
   float mx = 0.f;
@@ -323,8 +405,8 @@ k_node_post_bwd_tc(const float *G, const fcg_block blk, int quant,
   }
   tc::tmem_st_wait();
   const int sz = scale_exp(block_amax(mx, &meta->amax[1]));
-  tmem_rows_to_act(c.tl + NTM_D0, act, D, c.ch, c.ec, pow2f(sz), true);
-  NODE_ISSUE(c.tm + NTM_D1, c.sbase + NSM_WB, IMG128, D, true, c.sbase + NSM_ACT, D, idesc, np);
+  tmem_rows_to_act<Cfg::KSTR>(c.tl + NTM_D0, act, D, c.ch, c.ec, pow2f(sz), true);
+  NODE_ISSUE(c.tm + NTM_D1, c.sbase + Cfg::WB, IMG128, D, true, c.sbase + Cfg::ACT, D, idesc, np);
   NODE_WAIT();
   const float un1 = pow2f(-((quant ? 0 : blk.p0_exp) + sz));
   mx = 0.f;
@@ -343,26 +425,34 @@ k_node_post_bwd_tc(const float *G, const fcg_block blk, int quant,
     }
   }
   global_amax(mx, amax_out, &meta->amax[3]);
+  node_stamp(3, 5);
   node_epilogue_end(meta, c);
+  node_stamp(3, 7);
 }
 
 // Readout (flash.py:487-492): per_atom = ssp(X Wr0^T + br0) . wr1 + br1 and
 // the ones-seeded backward G = (wr1 * ssp'(zr)) Wr0.  Layer 0 has 64
 // outputs: an M=64 GEMM whose row k lives in TMEM lane 32(k/16) + k%16.
-__global__ void __launch_bounds__(NTH, 1)
+__global__ void __launch_bounds__(CfgRo::NTH, CfgRo::MIN_CTAS)
 k_readout_tc(const float *X, const fcg_model m, float *per_atom,
              float *G, int nrows) {
+  using Cfg = CfgRo;
+  node_stamp(4, 6);
+  node_stamp(4, 0);
   extern __shared__ __align__(1024) uint8_t sm[];
-  NodeMeta *meta = (NodeMeta *)(sm + NSM_META);
-  uint8_t *act = sm + NSM_ACT;
-  float *red = (float *)(sm + NSM_ACT);  // [128 nodes][65] after G1 completes
+  NodeMeta *meta = (NodeMeta *)(sm + Cfg::META);
+  uint8_t *act = sm + Cfg::ACT;
+  float *red = (float *)(sm + Cfg::ACT);  // [128 nodes][65] after G1 completes
   NodeCtx c = node_prologue(sm, meta, m.r0_img, 2 * IMG64);
+  node_stamp(4, 1);
   const bool quant = m.format == FCG_FMT_W16;
-  const int node0 = blockIdx.x * NN;
-  const int sx = rows_to_act(X, node0, nrows, c, 1.f, quant, &meta->amax[0], act);
-  NODE_ISSUE(c.tm + NTM_D0, c.sbase + NSM_WA, IMG64, D, false, c.sbase + NSM_ACT, D,
-             tc::idesc_f16(64, NN, 0, 1), quant ? 1 : 3);
+  const int node0 = blockIdx.x * Cfg::NN;
+  const int sx = rows_to_act<Cfg::KSTR>(X, node0, nrows, c, 1.f, quant, &meta->amax[0], act);
+  node_stamp(4, 2);
+  NODE_ISSUE(c.tm + NTM_D0, c.sbase + Cfg::WA, IMG64, D, false, c.sbase + Cfg::ACT, D,
+             tc::idesc_f16(64, Cfg::NN, 0, 1), quant ? 1 : 3);
   NODE_WAIT();
+  node_stamp(4, 3);
   const int k = 16 * c.quarter + (c.lane & 15);
   const bool row_lane = c.lane < 16;
   const float un = quant ? ld_dep(&m.r0_s[k]) : pow2f(-(m.r0_exp + sx));
@@ -391,16 +481,16 @@ k_readout_tc(const float *X, const fcg_model m, float *per_atom,
   }
   tc::tmem_st_wait();
   const int sz = scale_exp(block_amax(mx, &meta->amax[1]));
-  if (threadIdx.x < NN && node0 + (int)threadIdx.x < nrows) {
+  if (threadIdx.x < Cfg::NN && node0 + (int)threadIdx.x < nrows) {
     float s = 0.f;
 #pragma unroll 8
     for (int q = 0; q < RH; ++q) s += red[threadIdx.x * 65 + q];
     per_atom[node0 + threadIdx.x] = s + m.r1_b;
   }
   __syncthreads();  // red is dead before the B operand overwrites it
-  tmem_rows_to_act(c.tl + NTM_D0, act, RH, k, c.ec, pow2f(sz), true, row_lane);
-  NODE_ISSUE(c.tm + NTM_D1, c.sbase + NSM_WA, IMG64, D, true, c.sbase + NSM_ACT, RH,
-             tc::idesc_f16(128, NN, 1, 1), quant ? 2 : 3);
+  tmem_rows_to_act<Cfg::KSTR>(c.tl + NTM_D0, act, RH, k, c.ec, pow2f(sz), true, row_lane);
+  NODE_ISSUE(c.tm + NTM_D1, c.sbase + Cfg::WA, IMG64, D, true, c.sbase + Cfg::ACT, RH,
+             tc::idesc_f16(128, Cfg::NN, 1, 1), quant ? 2 : 3);
   NODE_WAIT();
   const float un1 = pow2f(-((quant ? 0 : m.r0_exp) + sz));
 #pragma unroll
@@ -414,47 +504,53 @@ k_readout_tc(const float *X, const fcg_model m, float *per_atom,
       if (n < nrows) G[(size_t)n * D + c.ch] = v[i] * un1;
     }
   }
+  node_stamp(4, 5);
   node_epilogue_end(meta, c);
+  node_stamp(4, 7);
 }
 
 // ---------------------------------------------------------------------------
 void node_tc_configure() {
   static bool done = false;
   if (done) return;
-  const int sm = (int)NSM_TOTAL + 1024;
-  cudaFuncSetAttribute(k_node_linear_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  cudaFuncSetAttribute(k_node_linear_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  cudaFuncSetAttribute(k_node_post_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  cudaFuncSetAttribute(k_node_post_bwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  cudaFuncSetAttribute(k_readout_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(k_node_linear_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, CfgLin::SMEM);
+  cudaFuncSetAttribute(k_node_linear_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, CfgLin::SMEM);
+  cudaFuncSetAttribute(k_node_post_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, CfgPost::SMEM);
+  cudaFuncSetAttribute(k_node_post_bwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, CfgPost::SMEM);
+  cudaFuncSetAttribute(k_readout_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, CfgRo::SMEM);
   done = true;
 }
 
-static inline int node_grid(int nrows) { return (nrows + NN - 1) / NN; }
+template <class Cfg>
+static inline int node_grid(int nrows) { return (nrows + Cfg::NN - 1) / Cfg::NN; }
 
 void launch_node_pre_tc(const float *X, const fcg_block &b, int quant, float *P, int nrows,
                         unsigned int *amax_p, cudaStream_t s) {
-  launch_pdl(PDL_NODE_PRE, k_node_linear_tc<0>, node_grid(nrows), NTH, NSM_TOTAL + 1024, s,
-      X, b.pre_img, b.pre_exp, b.pre_b, b.pre_s, quant, P, nrows, amax_p, nullptr);
+  node_dbg_sync();
+  launch_pdl(PDL_NODE_PRE, k_node_linear_tc<0>, node_grid<CfgLin>(nrows), CfgLin::NTH,
+             CfgLin::SMEM, s, X, b.pre_img, b.pre_exp, b.pre_b, b.pre_s, quant, P, nrows, amax_p,
+             nullptr);
 }
 void launch_node_pre_bwd_tc(const float *GP, const fcg_block &b, int quant, float *G, int nrows,
                             const int32_t *csr_ptr, cudaStream_t s) {
-  launch_pdl(PDL_NODE_PRE_BWD, k_node_linear_tc<1>, node_grid(nrows), NTH, NSM_TOTAL + 1024, s,
-      GP, b.pre_img, b.pre_exp, nullptr, b.pre_s, quant, G, nrows, nullptr, csr_ptr);
+  launch_pdl(PDL_NODE_PRE_BWD, k_node_linear_tc<1>, node_grid<CfgLin>(nrows), CfgLin::NTH,
+             CfgLin::SMEM, s, GP, b.pre_img, b.pre_exp, nullptr, b.pre_s, quant, G, nrows, nullptr,
+             csr_ptr);
 }
 void launch_node_post_tc(const float *H, const fcg_block &b, int quant, float *Zp, float *X,
                          int nrows, const int32_t *csr_ptr, cudaStream_t s) {
-  launch_pdl(PDL_NODE_POST, k_node_post_tc, node_grid(nrows), NTH, NSM_TOTAL + 1024, s, H, b, quant, Zp, X,
-             nrows, csr_ptr);
+  launch_pdl(PDL_NODE_POST, k_node_post_tc, node_grid<CfgPost>(nrows), CfgPost::NTH,
+             CfgPost::SMEM, s, H, b, quant, Zp, X, nrows, csr_ptr);
 }
 void launch_node_post_bwd_tc(const float *G, const fcg_block &b, int quant, const float *Zp,
                              float *GH, int nrows, unsigned int *amax_gh, cudaStream_t s) {
-  launch_pdl(PDL_NODE_POST_BWD, k_node_post_bwd_tc, node_grid(nrows), NTH, NSM_TOTAL + 1024, s, G, b, quant, Zp, GH,
-             nrows, amax_gh);
+  launch_pdl(PDL_NODE_POST_BWD, k_node_post_bwd_tc, node_grid<CfgPost>(nrows), CfgPost::NTH,
+             CfgPost::SMEM, s, G, b, quant, Zp, GH, nrows, amax_gh);
 }
 void launch_readout_tc(const float *X, const fcg_model &m, float *per_atom, float *G, int nrows,
                        cudaStream_t s) {
-  launch_pdl(PDL_READOUT, k_readout_tc, node_grid(nrows), NTH, NSM_TOTAL + 1024, s, X, m, per_atom, G, nrows);
+  launch_pdl(PDL_READOUT, k_readout_tc, node_grid<CfgRo>(nrows), CfgRo::NTH, CfgRo::SMEM, s, X,
+             m, per_atom, G, nrows);
 }
 
 }  // namespace fcg
