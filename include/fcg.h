@@ -278,6 +278,31 @@ int64_t fcg_format_xyz(const float *pos, const int32_t *types, int R, int N,
                        int64_t step, int replica0, char *out, int64_t cap,
                        int nthreads);
 
+/* ---- trajectory analysis (analysis.py) ----------
+ * Batched over F frames x[F][N][3] (fp64, device) against one reference
+ * structure ref[N][3].  Replaces the per-frame numpy loops of
+ * analysis.py:56-143 / :260-276.
+ *
+ * fcg_kabsch: optimal proper superposition of every frame onto ref
+ * (kabsch_align, analysis.py:56-81): rmsd[F]; rot[F][3][3] and trans[F][3]
+ * (nullable) with moved = R x + t; degenerate[F] = 1 where the reference
+ * raises DegenerateStructureError (fewer than 3 beads or s1 <= 1e-12 s0). */
+int fcg_kabsch(const double *x, const double *ref, int F, int N, double *rmsd,
+               double *rot, double *trans, int32_t *degenerate, void *stream);
+/* fcg_gdt_counts: the GDT-TS seed search of gdt_ts (analysis.py:115-143):
+ * windows[W][2] = (start, length) seeds; best[F][4] = the largest number of
+ * beads within cutoffs[c] (<=) over all non-degenerate seeds.  GDT-TS of a
+ * frame = mean_c(best[c] / N) (done by the caller). */
+int fcg_gdt_counts(const double *x, const double *ref, int F, int N,
+                   const int32_t *windows, int W, const double *cutoffs,
+                   int32_t *best, void *stream);
+/* fcg_native_q: fraction of native contacts (fraction_native_contacts,
+ * analysis.py:100-108): q[f] = mean_c 1/(1+exp(beta (r_c - lam r0_c))) over
+ * pairs[C][2]; C >= 1 (an empty contact set is a ValueError upstream). */
+int fcg_native_q(const double *x, int F, int N, const int32_t *pairs,
+                 const double *ref_dist, int C, double beta, double lam, double *q,
+                 void *stream);
+
 /* Diagnostics: tcgen05 (kind::f16) GEMM self-test.  dump[128][N] receives
  * the raw TMEM accumulator lanes of D = A * B^T for A[M][K], B[N][K] fp16
  * staged in the canonical no-swizzle core-matrix layout (K-major or

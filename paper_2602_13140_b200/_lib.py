@@ -89,6 +89,10 @@ _SIGS = {
     "fcg_prior_forces": (C.c_int, [C.POINTER(FcgPrior), _VP, C.c_int, C.c_int, _VP, _VP, _VP]),
     "fcg_selftest_mma": (C.c_int, [_VP, _VP, _VP, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                    C.c_int, C.c_int, C.c_int, C.c_int, _VP]),
+    "fcg_kabsch": (C.c_int, [_VP, _VP, C.c_int, C.c_int, _VP, _VP, _VP, _VP, _VP]),
+    "fcg_gdt_counts": (C.c_int, [_VP, _VP, C.c_int, C.c_int, _VP, C.c_int, _VP, _VP, _VP]),
+    "fcg_native_q": (C.c_int, [_VP, C.c_int, C.c_int, _VP, _VP, C.c_int, C.c_double, C.c_double,
+                               _VP, _VP]),
     "fcg_format_xyz": (C.c_int64, [_VP, _VP, C.c_int, C.c_int, C.c_int64, C.c_int, C.c_char_p,
                                    C.c_int64, C.c_int]),
     "fcg_md_workspace_bytes": (C.c_size_t, [C.POINTER(FcgModel), C.c_int, C.c_int, C.c_int64]),
