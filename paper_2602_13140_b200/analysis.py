@@ -284,10 +284,18 @@ def graph_stats(frames, r_cut: float):
     """Per-frame E, mean/max degree and mean/max sequence separation of the
     cutoff graph (analysis.py:208-231), all frames built in one
     fcg_nbr_build call (frames as replicas)."""
-    from .csr import device_csr
     x = np.asarray([np.asarray(f) for f in frames])
     if x.ndim != 3 or x.shape[2] != 3:
         raise ValueError("frames must share an N x 3 shape")
+    # the builder sizes its edge buffers for the dense worst case F*N*(N-1):
+    # batch the frames so that stays ~64M slots
+    step = max(1, (64 << 20) // max(x.shape[1] * max(x.shape[1] - 1, 1), 1))
+    parts = [_graph_stats_batch(x[a:a + step], r_cut) for a in range(0, x.shape[0], step)]
+    return {k: np.concatenate([p[k] for p in parts]) for k in parts[0]}
+
+
+def _graph_stats_batch(x, r_cut):
+    from .csr import device_csr
     F, n = x.shape[0], x.shape[1]
     ptr, nbr, _rev, own = device_csr(x, r_cut)
     starts = ptr[0:F * n:n]

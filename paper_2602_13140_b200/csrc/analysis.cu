@@ -12,14 +12,14 @@
 // (s1 <= 1e-12 max(s0, 1), analysis.py:74-75) uses singular values from a
 // 3x3 Jacobi on H^T H.
 //
-// Work decomposition: one warp per superposition (a frame for RMSD, a
-// (frame, window) pair for GDT), lane-strided passes over the beads with
-// warp-shuffle fp64 sums (centroids first, then the centred covariance, as
-// the reference does); every lane solves the small eigenproblems
-// redundantly, so no broadcast is needed.  GDT counts beads within the
-// 0.1/0.2/0.4/0.8 nm ladder with ballots and keeps the best window per
-// cutoff by atomicMax on integer counts; the host forms count/n and the
-// mean exactly as the reference does.  Q: one CTA per frame.
+// Work decomposition: lane-strided passes over the beads with warp-shuffle
+// fp64 sums (centroids first, then the centred covariance, as the reference
+// does).  RMSD: one warp per frame, every lane solving the frame's small
+// eigenproblems.  GDT: one warp per 32 seeds of a frame, one seed's
+// eigenproblems per lane, then warp-cooperative counting of the beads within
+// the 0.1/0.2/0.4/0.8 nm ladder with ballots; the best seed per cutoff is an
+// atomicMax on integer counts and the host forms count/n and the mean
+// exactly as the reference does.  Q: one CTA per frame.
 #include "common.cuh"
 
 namespace fcg {
@@ -220,40 +220,108 @@ k_kabsch(const double *x, const double *ref, int F, int n, double *rmsd, double 
 }
 
 // ---- GDT-TS window search (gdt_ts, analysis.py:115-143) ----------------------
-// One warp per (frame, window); windows[w] = (start, length).
+// One warp per 32 seeds of one frame (windows[w] = (start, length)).  The
+// covariances are warp-cooperative sums (lane j keeps seed j's), the
+// eigen-solves then run one seed per lane — 32 at once instead of 32 lanes
+// repeating one — and each rotation is broadcast in turn to count the beads
+// within the cutoff ladder; the per-cutoff maxima stay in registers until one
+// atomicMax per warp.
 __global__ void __launch_bounds__(256)
 k_gdt(const double *x, const double *ref, int F, int n, const int32_t *windows, int W,
       double c0, double c1, double c2, double c3, int32_t *best) {
   const int lane = threadIdx.x & 31;
+  const int nblk = (W + 31) / 32;
   const long long t = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  if (t >= (long long)F * W) return;
-  const int f = (int)(t / W), w = (int)(t % W);
+  if (t >= (long long)F * nblk) return;
+  const int f = (int)(t / nblk), wb = (int)(t % nblk) * 32;
+  const int nw = min(32, W - wb);
   const double *xf = x + (size_t)f * n * 3;
-  const Superpose sp = superpose_warp(xf, ref, windows[2 * w], windows[2 * w + 1], lane);
-  if (!sp.ok) return;  // a degenerate seed is skipped (analysis.py:133-134)
-  double tr[3];
+  double mh[3][3], mxm[3], mym[3];
+  int mlen = 0;
+  for (int j = 0; j < nw; ++j) {
+    const int b0 = windows[2 * (wb + j)], len = windows[2 * (wb + j) + 1];
+    double sx[3] = {0, 0, 0}, sy[3] = {0, 0, 0};
+    for (int i = lane; i < len; i += 32) {
 #pragma unroll
-  for (int a = 0; a < 3; ++a)
-    tr[a] = sp.ym[a] - (sp.r[a][0] * sp.xm[0] + sp.r[a][1] * sp.xm[1] + sp.r[a][2] * sp.xm[2]);
-  int cnt[4] = {0, 0, 0, 0};
-  for (int i0 = 0; i0 < n; i0 += 32) {
-    const int i = i0 + lane;
-    double dist = 1e300;
-    if (i < n) {
-      const double px = xf[(size_t)i * 3], py = xf[(size_t)i * 3 + 1], pz = xf[(size_t)i * 3 + 2];
-      double d[3];
+      for (int a = 0; a < 3; ++a) {
+        sx[a] += xf[(size_t)(b0 + i) * 3 + a];
+        sy[a] += ref[(size_t)(b0 + i) * 3 + a];
+      }
+    }
+    double xm[3], ym[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      xm[a] = warp_sum_d(sx[a]) / len;
+      ym[a] = warp_sum_d(sy[a]) / len;
+    }
+    double h[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+    for (int i = lane; i < len; i += 32) {
+      double xc[3], yc[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        xc[a] = xf[(size_t)(b0 + i) * 3 + a] - xm[a];
+        yc[a] = ref[(size_t)(b0 + i) * 3 + a] - ym[a];
+      }
 #pragma unroll
       for (int a = 0; a < 3; ++a)
-        d[a] = (sp.r[a][0] * px + sp.r[a][1] * py + sp.r[a][2] * pz + tr[a]) - ref[(size_t)i * 3 + a];
-      dist = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]), __dmul_rn(d[1], d[1])),
-                            __dmul_rn(d[2], d[2])));
+#pragma unroll
+        for (int b = 0; b < 3; ++b) h[a][b] += xc[a] * yc[b];
     }
-    cnt[0] += __popc(__ballot_sync(0xffffffffu, dist <= c0));
-    cnt[1] += __popc(__ballot_sync(0xffffffffu, dist <= c1));
-    cnt[2] += __popc(__ballot_sync(0xffffffffu, dist <= c2));
-    cnt[3] += __popc(__ballot_sync(0xffffffffu, dist <= c3));
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) h[a][b] = warp_sum_d(h[a][b]);
+    if (lane == j) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        mxm[a] = xm[a];
+        mym[a] = ym[a];
+#pragma unroll
+        for (int b = 0; b < 3; ++b) mh[a][b] = h[a][b];
+      }
+      mlen = len;
+    }
   }
-  if (lane < 4) atomicMax(&best[(size_t)f * 4 + lane], cnt[lane]);
+  // one seed per lane
+  double r[3][3], tr[3];
+  const bool ok = lane < nw && mlen >= 3 && rotation_from_cov(mh, r);
+  if (ok) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) tr[a] = mym[a] - (r[a][0] * mxm[0] + r[a][1] * mxm[1] + r[a][2] * mxm[2]);
+  }
+  const unsigned okmask = __ballot_sync(0xffffffffu, ok);
+  int keep = 0;  // lane c < 4: best count for cutoff c over this warp's seeds
+  for (int j = 0; j < nw; ++j) {
+    if (!((okmask >> j) & 1u)) continue;  // a degenerate seed is skipped (analysis.py:133-134)
+    double rj[3][3], tj[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      tj[a] = __shfl_sync(0xffffffffu, tr[a], j);
+#pragma unroll
+      for (int b = 0; b < 3; ++b) rj[a][b] = __shfl_sync(0xffffffffu, r[a][b], j);
+    }
+    int cnt[4] = {0, 0, 0, 0};
+    for (int i0 = 0; i0 < n; i0 += 32) {
+      const int i = i0 + lane;
+      double dist = 1e300;
+      if (i < n) {
+        const double px = xf[(size_t)i * 3], py = xf[(size_t)i * 3 + 1], pz = xf[(size_t)i * 3 + 2];
+        double d[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+          d[a] = (rj[a][0] * px + rj[a][1] * py + rj[a][2] * pz + tj[a]) - ref[(size_t)i * 3 + a];
+        dist = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]), __dmul_rn(d[1], d[1])),
+                              __dmul_rn(d[2], d[2])));
+      }
+      cnt[0] += __popc(__ballot_sync(0xffffffffu, dist <= c0));
+      cnt[1] += __popc(__ballot_sync(0xffffffffu, dist <= c1));
+      cnt[2] += __popc(__ballot_sync(0xffffffffu, dist <= c2));
+      cnt[3] += __popc(__ballot_sync(0xffffffffu, dist <= c3));
+    }
+    const int mine = lane == 0 ? cnt[0] : lane == 1 ? cnt[1] : lane == 2 ? cnt[2] : cnt[3];
+    keep = max(keep, mine);
+  }
+  if (lane < 4 && okmask) atomicMax(&best[(size_t)f * 4 + lane], keep);
 }
 
 // ---- native-contact fraction (fraction_native_contacts, analysis.py:100-108) --
@@ -309,9 +377,8 @@ extern "C" int fcg_gdt_counts(const double *x, const double *ref, int F, int N,
   if (F == 0) return FCG_OK;
   cudaMemsetAsync(best, 0, sizeof(int32_t) * 4 * (size_t)F, s);
   if (W > 0)
-    k_gdt<<<ceil_div((long long)F * W * 32, 256), 256, 0, s>>>(x, ref, F, N, windows, W, cutoffs[0],
-                                                               cutoffs[1], cutoffs[2], cutoffs[3],
-                                                               best);
+    k_gdt<<<ceil_div((long long)F * ((W + 31) / 32) * 32, 256), 256, 0, s>>>(
+        x, ref, F, N, windows, W, cutoffs[0], cutoffs[1], cutoffs[2], cutoffs[3], best);
   return cuda_status("gdt_counts");
 }
 
