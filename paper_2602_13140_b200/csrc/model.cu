@@ -519,25 +519,37 @@ k_edge_bwd(const EdgeArgs a, const float *__restrict__ P, const float *__restric
 // grad_r[x] = sum_{k in row x} (gsum[rev[k]] - gsum[k])  (flash.py:298-299,
 // dst-segment sum minus src-segment sum), forces = -grad_r (+ f_extra), then
 // optionally the trailing half-kick (md.py:134-138) and the blow-up check
-// (md.py:183-185).  One thread per node; single writer per output.
+// (md.py:183-185).  One warp per node; single writer per output.
 __global__ void __launch_bounds__(256)
 k_forces_finish(const int32_t *__restrict__ ptr, const int32_t *__restrict__ rev,
                 const float4 *__restrict__ gsum, int N, int RN, int64_t cap_e,
                 const float *__restrict__ f_extra, float *__restrict__ forces,
                 fcg_md_params kick, int do_kick, const float *__restrict__ mass,
                 float *__restrict__ vel, int64_t *__restrict__ status, const int64_t *step) {
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  // one warp per node: lanes stride the node's CSR row, then a fixed-order
+  // butterfly sum (deterministic; replaces a serial per-thread walk that left
+  // most SMs idle)
+  const int g = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
   if (g >= RN) return;
   const bool valid = (long long)ptr[RN] <= cap_e;
   float gx = 0.f, gy = 0.f, gz = 0.f;
   if (valid) {
-    for (int k = ptr[g]; k < ptr[g + 1]; ++k) {
+    const int k1 = ptr[g + 1];
+    for (int k = ptr[g] + lane; k < k1; k += 32) {
       float4 a = gsum[rev[k]], b = gsum[k];
       gx += a.x - b.x;
       gy += a.y - b.y;
       gz += a.z - b.z;
     }
   }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    gx += __shfl_xor_sync(0xffffffffu, gx, o);
+    gy += __shfl_xor_sync(0xffffffffu, gy, o);
+    gz += __shfl_xor_sync(0xffffffffu, gz, o);
+  }
+  if (lane != 0) return;
   float f[3] = {-gx, -gy, -gz};
   bool bad = false;
   const int i = g % N;
@@ -765,9 +777,8 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
   fcg_md_params kp{};
   if (kick) kp = *kick;
   FCG_PROF(P_FORCES, s);
-  k_forces_finish<<<ceil_div(RN, 256), 256, 0, s>>>(ptr, rev, b.gsum, N, RN, cap_e, f_extra,
-                                                    forces, kp, kick != nullptr, mass, vel, status,
-                                                    step);
+  k_forces_finish<<<ceil_div((long long)RN * 32, 256), 256, 0, s>>>(
+      ptr, rev, b.gsum, N, RN, cap_e, f_extra, forces, kp, kick != nullptr, mass, vel, status, step);
   k_replica_energy<<<R, 256, 0, s>>>(per_atom, N, energy);
   return cuda_status("energy_forces");
 }

@@ -14,6 +14,8 @@
 // (dx*dx + dz*dz) + dy*dy with separate roundings (pinned in
 // tests/test_oracle_golden.py against the reference).  We reproduce it with
 // explicit _rn intrinsics so nvcc cannot contract to DFMA.
+#include <stdlib.h>
+
 #include <cub/cub.cuh>
 
 #include "common.cuh"
@@ -38,7 +40,8 @@ __global__ void __launch_bounds__(NBR_WARPS * 32)
 k_scan_rows(const T *__restrict__ pos, int N, double rc2, int32_t *__restrict__ cnt,
             const int32_t *__restrict__ ptr, int64_t cap_e, int32_t *__restrict__ nbr,
             int32_t *__restrict__ own, int64_t *__restrict__ status, const int64_t *gate,
-            int stride) {
+            int stride, uint32_t *__restrict__ masks = nullptr,
+            int32_t *__restrict__ rep_total = nullptr) {
   __shared__ double sx[NBR_TILE], sy[NBR_TILE], sz[NBR_TILE];
   const int r = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -96,6 +99,8 @@ k_scan_rows(const T *__restrict__ pos, int N, double rc2, int32_t *__restrict__ 
         bool e = (jl < tn) && (j != i) && (i < N) &&
                  within_cutoff(xi[q], yi[q], zi[q], xj, yj, zj, rc2);
         unsigned m = __ballot_sync(0xffffffffu, e);
+        if (!kFill && masks && lane == 0 && i < N)  // fused build: keep the row's bits
+          masks[((size_t)r * N + i) * ((N + 31) / 32) + ((t0 + c0) >> 5)] = m;
         if (kFill) {
           if (e && write_ok[q]) {
             int slot = base[q] + __popc(m & ((1u << lane) - 1u));
@@ -108,15 +113,17 @@ k_scan_rows(const T *__restrict__ pos, int N, double rc2, int32_t *__restrict__ 
     }
   }
   if (!kFill && lane == 0) {
-    int mx = 0;
+    int mx = 0, sum = 0;
 #pragma unroll
     for (int q = 0; q < NBR_ROWS_PER_WARP; ++q) {
       if (row0 + q < N) {
         cnt[(size_t)r * N + row0 + q] = base[q];
         mx = max(mx, base[q]);
+        sum += base[q];
       }
     }
     atomicMax((unsigned long long *)&status[FCG_ST_MAXDEG], (unsigned long long)mx);
+    if (rep_total) atomicAdd(&rep_total[r], sum);
   }
 }
 
@@ -153,6 +160,121 @@ k_rev(const int32_t *__restrict__ ptr, const int32_t *__restrict__ nbr, int nrow
   }
 }
 
+// ---- fused assembly for N <= NBR_FUSED_MAX (a few CTAs per replica) --------
+// After the count pass has stored every row's ballot words, one CTA per
+// replica turns them into the CSR: the replica's base is the sum of the
+// preceding replicas' totals, the row offsets a shared-memory scan of the
+// row popcounts, nbr/own come from the set bits in ascending order, and
+// rev[k] (edge j -> i at slot k) = ptr[j] + rank of i among row j's
+// sources = ptr[j] + popcount of row j's bits below i — the same value
+// k_rev's binary search finds.  Replaces the scan, finalize, fill and rev
+// launches (and the second fp64 predicate pass) of the general path.
+constexpr int NBR_FUSED_MAX = 512;
+static size_t nbr_assemble_smem(int N) {
+  const size_t W = (size_t)(N + 31) / 32;
+  return (2 * (size_t)N * W + (size_t)N + 1) * 4;
+}
+
+__global__ void __launch_bounds__(512)
+k_nbr_assemble(const uint32_t *__restrict__ masks, const int32_t *__restrict__ rep_total, int R,
+               int N, int64_t cap_e, int32_t *__restrict__ ptr, int32_t *__restrict__ nbr,
+               int32_t *__restrict__ rev, int32_t *__restrict__ own, int64_t *__restrict__ status,
+               const int64_t *gate, int stride) {
+  // dynamic smem: bit words [N*W] | exclusive popcount per word [N*W] | row offsets [N+1]
+  extern __shared__ uint32_t dsm[];
+  const int W = (N + 31) / 32;
+  uint32_t *sm_mask = dsm;
+  int32_t *sm_pre = (int32_t *)(dsm + N * W);
+  int32_t *sm_off = sm_pre + N * W;
+  __shared__ long long red[2][16];
+  const int r = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long RN = (long long)R * N;
+  if (gate && stride > 1 && (*gate % stride) != 0) {  // list kept: only account the step
+    if (r == 0 && blockIdx.y == 0 && tid == 0) {
+      const long long e = ptr[RN];
+      status[FCG_ST_EDGES] = e;
+      if (e > cap_e) status[FCG_ST_OVERFLOW] = 1;
+      status[FCG_ST_EDGE_SUM] += e;
+      status[FCG_ST_BUILDS] += 1;
+    }
+    return;
+  }
+  // replica base and grand total
+  long long before = 0, total = 0;
+  for (int q = tid; q < R; q += blockDim.x) {
+    const long long v = rep_total[q];
+    total += v;
+    if (q < r) before += v;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    before += __shfl_xor_sync(0xffffffffu, before, o);
+    total += __shfl_xor_sync(0xffffffffu, total, o);
+  }
+  if (lane == 0) { red[0][warp] = before; red[1][warp] = total; }
+  // the replica's bit rows and per-row counts
+  const uint32_t *mr = masks + (size_t)r * N * W;
+  for (int k = tid; k < N * W; k += blockDim.x) sm_mask[k] = mr[k];
+  __syncthreads();
+  before = 0; total = 0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { before += red[0][w]; total += red[1][w]; }
+  // row counts -> exclusive scan (one thread per row, N <= 512 = blockDim)
+  int c = 0;
+  if (tid < N) {
+    for (int t = 0; t < W; ++t) {
+      sm_pre[tid * W + t] = c;
+      c += __popc(sm_mask[tid * W + t]);
+    }
+  }
+  int incl = c;  // block-wide inclusive scan of c
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  __shared__ int32_t wsum[16];
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  int wbase = 0;
+  for (int w = 0; w < warp; ++w) wbase += wsum[w];
+  if (tid < N) sm_off[tid] = wbase + incl - c;
+  if (tid == N - 1) sm_off[N] = wbase + incl;
+  __syncthreads();
+  const long long base = before;
+  // this CTA's rows (every CTA of the replica derives the full row table:
+  // rev needs any row j of the replica)
+  const int rows_per = (N + (int)gridDim.y - 1) / (int)gridDim.y;
+  const int i0 = (int)blockIdx.y * rows_per, i1 = min(N, i0 + rows_per);
+  if (tid >= i0 && tid < i1) ptr[(long long)r * N + tid] = (int32_t)(base + sm_off[tid]);
+  if (r == R - 1 && blockIdx.y == 0 && tid == 0) {
+    ptr[RN] = (int32_t)total;
+    status[FCG_ST_EDGES] = total;
+    if (total > cap_e) status[FCG_ST_OVERFLOW] = 1;
+    status[FCG_ST_EDGE_SUM] += total;
+    status[FCG_ST_BUILDS] += 1;
+  }
+  // fill: one warp per row, lane = source candidate of each 32-bit word, so
+  // the lanes of a word write consecutive slots
+  const bool rev_ok = total <= cap_e;
+  const uint32_t below = (1u << lane) - 1u;
+  for (int i = i0 + warp; i < i1; i += (int)(blockDim.x >> 5)) {
+    if (base + sm_off[i + 1] > cap_e) continue;  // row past capacity: CSR invalid
+    const int row_slot = (int)(base + sm_off[i]);
+    const int ti = i >> 5;
+    const uint32_t ibit = (1u << (i & 31)) - 1u;
+    for (int t = 0; t < W; ++t) {
+      const uint32_t m = sm_mask[i * W + t];
+      if (!((m >> lane) & 1u)) continue;
+      const int j = 32 * t + lane;
+      const int slot = row_slot + sm_pre[i * W + t] + __popc(m & below);
+      nbr[slot] = (int32_t)((long long)r * N + j);
+      own[slot] = (int32_t)((long long)r * N + i);
+      if (rev_ok)
+        rev[slot] = (int32_t)(base + sm_off[j] + sm_pre[j * W + ti] + __popc(sm_mask[j * W + ti] & ibit));
+    }
+  }
+}
+
 size_t nbr_ws_bytes(int R, int N) {
   size_t n = (size_t)R * N + 1;
   size_t tmp = 0;
@@ -160,7 +282,20 @@ size_t nbr_ws_bytes(int R, int N) {
   Carver c(nullptr, 0);
   c.take<int32_t>(n);
   c.take<char>(tmp);
+  if (N <= NBR_FUSED_MAX) {
+    c.take<uint32_t>((size_t)R * N * ((N + 31) / 32));
+    c.take<int32_t>((size_t)R);
+  }
   return c.off + 256;
+}
+
+// FCG_NBR_FUSED=0 forces the general (count / scan / fill / rev) path (A/B).
+static bool nbr_fused_disabled() {
+  static const bool off = [] {
+    const char *v = getenv("FCG_NBR_FUSED");
+    return v && v[0] == '0';
+  }();
+  return off;
 }
 
 template <typename T>
@@ -169,6 +304,10 @@ int nbr_build_t(const T *pos, int R, int N, double r_cut, int64_t cap_e, int32_t
                 size_t ws_bytes, cudaStream_t s, const int64_t *gate = nullptr,
                 int stride = 1) {
   if (R < 1 || N < 1) { set_error("nbr_build: need R >= 1 and N >= 1"); return FCG_ERR_ARG; }
+#ifdef FCG_DIAG_NO_NBR  // timing diagnosis only: keep the first list forever
+  static int diag_calls = 0;
+  if (diag_calls++ > 0) return FCG_OK;
+#endif
   if ((long long)R * N >= (1ll << 31)) { set_error("nbr_build: R*N too large"); return FCG_ERR_ARG; }
   size_t n = (size_t)R * N + 1;
   size_t tmp = 0;
@@ -176,10 +315,39 @@ int nbr_build_t(const T *pos, int R, int N, double r_cut, int64_t cap_e, int32_t
   Carver c(ws, ws_bytes);
   int32_t *cnt = c.take<int32_t>(n);
   void *cub_tmp = c.take<char>(tmp);
+  const bool fused = N <= NBR_FUSED_MAX && !nbr_fused_disabled();
+  uint32_t *masks = nullptr;
+  int32_t *rep_total = nullptr;
+  if (N <= NBR_FUSED_MAX) {
+    masks = c.take<uint32_t>((size_t)R * N * ((N + 31) / 32));
+    rep_total = c.take<int32_t>((size_t)R);
+  }
   if (!c.ok()) { set_error("nbr_build: workspace too small"); return FCG_ERR_ARG; }
   double rc2 = r_cut * r_cut;  // Python float product, neighbors.py:89
 
   dim3 grid(ceil_div(N, NBR_ROWS_PER_CTA), R);
+  if (fused) {
+    cudaMemsetAsync(rep_total, 0, sizeof(int32_t) * (size_t)R, s);
+    {
+      FCG_PROF(P_NBR_COUNT, s);
+      k_scan_rows<T, false><<<grid, NBR_WARPS * 32, 0, s>>>(pos, N, rc2, cnt, ptr, cap_e, nullptr,
+                                                            nullptr, status, gate, stride, masks,
+                                                            rep_total);
+    }
+    {
+      FCG_PROF(P_NBR_FILL, s);
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(k_nbr_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)nbr_assemble_smem(NBR_FUSED_MAX));
+        attr = true;
+      }
+      const dim3 agrid(R, (N + 95) / 96);  // ~96 rows per CTA
+      k_nbr_assemble<<<agrid, 512, nbr_assemble_smem(N), s>>>(masks, rep_total, R, N, cap_e, ptr,
+                                                              nbr, rev, own, status, gate, stride);
+    }
+    return cuda_status("nbr_build");
+  }
   cudaMemsetAsync(cnt + (n - 1), 0, sizeof(int32_t), s);
   {
     FCG_PROF(P_NBR_COUNT, s);
