@@ -15,9 +15,10 @@ Timing: W untimed warm-up steps, then K steps, each a replay of a captured
 one-step CUDA graph bracketed by CUDA events on the replay stream, with a
 256 MiB L2 flush (outside the events) before every step; barrier +
 synchronize around the timed region; max over ranks.  `e2e` repeats the
-step through the engine's host-buffer API (H2D of positions+velocities
-from pinned memory, fcg_md_step, D2H of the new state and per-replica
-energies) timed by the host clock.  Multi-GPU: one process per GPU
+step through the engine's public API with host buffers (H2D of
+positions+velocities from pinned memory, MDEngine.run(1) = one graph replay
+of fcg_md_step, D2H of the new state and per-replica energies) timed by the
+host clock.  Multi-GPU: one process per GPU
 (torchrun), replicas sharded with no per-step collective; an NCCL
 all_gather of per-replica energies happens after the timed region.
 """
@@ -279,7 +280,7 @@ def main():
         for _ in range(args.e2e_steps):
             eng.pos.copy_(hpos, non_blocking=True)
             eng.vel.copy_(hvel, non_blocking=True)
-            eng._md_step()
+            eng.run(1, graph_steps=1)  # the public stepping call (graph replay)
             hpos.copy_(eng.pos, non_blocking=True)
             hvel.copy_(eng.vel, non_blocking=True)
             hpot.copy_(eng.potential, non_blocking=True)
