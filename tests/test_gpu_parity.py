@@ -83,6 +83,31 @@ def test_large_n_csr_matches_oracle():
     np.testing.assert_array_equal(nl.dst, dst)
 
 
+@pytest.mark.parametrize("n,reps", [(512, 3), (513, 2), (37, 5)])
+def test_batched_csr_both_build_paths_match_oracle(n, reps):
+    # N <= 512 runs the fused assembly (ballot words -> ptr/nbr/own/rev by
+    # popcount rank), N > 512 the count / scan / fill / rev kernels; both
+    # must give the oracle's canonical CSR and reverse map bit for bit
+    from paper_2602_13140_b200.csr import device_csr
+    rng = np.random.default_rng(n)
+    pos = rng.uniform(0.0, 0.45 * n ** (1.0 / 3.0), (reps, n, 3)).astype(np.float32)
+    ptr, nbr, rev, own = device_csr(pos, 1.0)
+    E = int(ptr[-1])
+    off = 0
+    for r in range(reps):
+        src, dst = O.neighbor_list(pos[r], 1.0)
+        k = slice(off, off + src.size)
+        np.testing.assert_array_equal(nbr[k] - r * n, src)
+        np.testing.assert_array_equal(own[k] - r * n, dst)
+        np.testing.assert_array_equal(ptr[r * n:(r + 1) * n] - off,
+                                      np.searchsorted(dst, np.arange(n)))
+        off += src.size
+    assert off == E
+    # rev[k] is the slot of the reverse edge
+    np.testing.assert_array_equal(own[rev[:E]], nbr[:E])
+    np.testing.assert_array_equal(nbr[rev[:E]], own[:E])
+
+
 def test_group_by_arbitrary_lists():
     rng = np.random.default_rng(5)
     for _ in range(30):
