@@ -51,7 +51,8 @@ __device__ __forceinline__ T ld_gather(const T *p) {
   return __ldg(p);
 }
 enum PdlSite { PDL_GEOM, PDL_EDGE_FWD, PDL_EDGE_BWD, PDL_NODE_PRE, PDL_NODE_PRE_BWD,
-               PDL_NODE_POST, PDL_NODE_POST_BWD, PDL_READOUT };
+               PDL_NODE_POST, PDL_NODE_POST_BWD, PDL_READOUT,
+               PDL_SMALL };  // integrator, prior, neighbour, embed and finish kernels
 bool pdl_enabled(int site);  // FCG_PDL=<bitmask of sites> in the environment (A/B)
 template <typename... KArgs, typename... Args>
 inline void launch_pdl(int site, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,

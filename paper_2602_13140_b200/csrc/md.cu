@@ -190,8 +190,10 @@ __device__ __forceinline__ bool ring_valid(const NoiseTag *t, uint64_t seed, int
 }
 
 __global__ void __launch_bounds__(256)
-k_noise_ring(uint64_t seed, int rep_offset, const int64_t *__restrict__ stepp, int R, int n3,
-             const NoiseTag *__restrict__ tag, float *__restrict__ ring) {
+k_noise_ring(uint64_t seed, int rep_offset, const int64_t *stepp, int R, int n3,
+             const NoiseTag *tag, float *ring) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t step = *stepp;
   if (ring_valid(tag, seed, rep_offset, ((int64_t)R << 32) + n3, step)) return;
   int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
@@ -239,10 +241,12 @@ int langevin_baoa(const fcg_md_params *p, const float *mass, int R, int N, const
 }
 
 // BAOA with this step's slot of the noise ring
-__global__ void k_baoa_ring(fcg_md_params p, const float *__restrict__ mass, int N, long long n,
-                            const float *__restrict__ F, const NoiseTag *__restrict__ tag,
-                            const int64_t *__restrict__ stepp, const float *__restrict__ ring,
-                            float *__restrict__ pos, float *__restrict__ vel) {
+__global__ void k_baoa_ring(fcg_md_params p, const float *mass, int N, long long n,
+                            const float *F, const NoiseTag *tag,
+                            const int64_t *stepp, const float *ring,
+                            float *pos, float *vel) {
+  pdl_trigger();
+  pdl_wait();
   long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t >= n) return;
   const int64_t step = *stepp;
@@ -264,6 +268,8 @@ __global__ void k_baoa_ring(fcg_md_params p, const float *__restrict__ mass, int
 
 __global__ void k_step_advance_ring(int64_t *step, NoiseTag *tag, uint64_t seed, int rep_offset,
                                     int64_t layout) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t s = *step;
   if (!ring_valid(tag, seed, rep_offset, layout, s)) {
     tag->magic = kNoiseMagic;
@@ -289,17 +295,18 @@ int langevin_leading(const fcg_md_params *p, const float *mass, int R, int N,
   const long long n = (long long)R * N * 3;
   {
     FCG_PROF(P_NOISE, s);
-    k_noise_ring<<<ceil_div((long long)R * NOISE_RING * 32, 256), 256, 0, s>>>(
-        p->seed, p->rep_offset, step, R, 3 * N, tag, ring);
+    launch_pdl(PDL_SMALL, k_noise_ring, ceil_div((long long)R * NOISE_RING * 32, 256), 256, 0, s,
+               p->seed, p->rep_offset, step, R, 3 * N, tag, ring);
   }
   {
     FCG_PROF(P_BAOA, s);
-    k_baoa_ring<<<ceil_div(n, 256), 256, 0, s>>>(*p, mass, N, n, forces, tag, step, ring, pos, vel);
+    launch_pdl(PDL_SMALL, k_baoa_ring, ceil_div(n, 256), 256, 0, s, *p, mass, N, n, forces, tag,
+               step, ring, pos, vel);
   }
   {
     FCG_PROF(P_STEP, s);
-    k_step_advance_ring<<<1, 1, 0, s>>>(step, tag, p->seed, p->rep_offset,
-                                        ((int64_t)R << 32) + 3 * N);
+    launch_pdl(PDL_SMALL, k_step_advance_ring, 1, 1, 0, s, step, tag, p->seed, p->rep_offset,
+               ((int64_t)R << 32) + 3 * N);
   }
   return cuda_status("langevin_leading");
 }
@@ -343,8 +350,10 @@ __device__ __forceinline__ BondVec bond_eval(const fcg_prior &pr, const float *P
 // "+fvec" for bonds where it is atom i, then "-fvec" where it is atom j), so
 // the per-bead sums are bitwise the reference's.
 __global__ void __launch_bounds__(256)
-k_prior(const fcg_prior pr, const float *__restrict__ pos, int N, int RN,
-        float *__restrict__ f_prior) {
+k_prior(const fcg_prior pr, const float *pos, int N, int RN,
+        float *f_prior) {
+  pdl_trigger();
+  pdl_wait();
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= RN) return;
   const int r = g / N, i = g % N;
@@ -366,8 +375,10 @@ k_prior(const fcg_prior pr, const float *__restrict__ pos, int N, int RN,
 
 // Prior energy 0.5 * sum k*s^2 per replica (md.py:118), one CTA per replica.
 __global__ void __launch_bounds__(256)
-k_prior_energy(const fcg_prior pr, const float *__restrict__ pos, int N,
-               float *__restrict__ e_prior) {
+k_prior_energy(const fcg_prior pr, const float *pos, int N,
+               float *e_prior) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   const float *P = pos + (size_t)r * N * 3;
   __shared__ float red[256];
@@ -385,8 +396,9 @@ k_prior_energy(const fcg_prior pr, const float *__restrict__ pos, int N,
 int prior_forces(const fcg_prior *pr, const float *pos, int R, int N, float *e_prior,
                  float *f_prior, cudaStream_t s) {
   FCG_PROF(P_PRIOR, s);
-  k_prior<<<ceil_div((long long)R * N, 256), 256, 0, s>>>(*pr, pos, N, R * N, f_prior);
-  k_prior_energy<<<R, 256, 0, s>>>(*pr, pos, N, e_prior);
+  launch_pdl(PDL_SMALL, k_prior, ceil_div((long long)R * N, 256), 256, 0, s, *pr, pos, N, R * N,
+             f_prior);
+  launch_pdl(PDL_SMALL, k_prior_energy, R, 256, 0, s, *pr, pos, N, e_prior);
   return cuda_status("prior_forces");
 }
 

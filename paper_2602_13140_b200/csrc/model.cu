@@ -101,13 +101,16 @@ __device__ __forceinline__ void load_rows(float *As, const float *__restrict__ s
 
 // ---------------------------------------------------------------------------
 // node kernels
-__global__ void k_embed(const float *__restrict__ emb, const int32_t *__restrict__ types, int N,
-                        int RN, float *__restrict__ X) {
+__global__ void k_embed(const float *emb, const int32_t *types, int N,
+                        int RN, float *X, unsigned int *amax, int namax) {
+  pdl_trigger();
+  pdl_wait();
+  if (blockIdx.x == 0 && (int)threadIdx.x < namax) amax[threadIdx.x] = 0u;  // scale maxima
   int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= RN * (D / 4)) return;
   int g = q / (D / 4), c4 = q % (D / 4);
   int t = types[g % N];
-  *(float4 *)&X[(size_t)g * D + c4 * 4] = __ldg((const float4 *)&emb[(size_t)t * D + c4 * 4]);
+  *(float4 *)&X[(size_t)g * D + c4 * 4] = ld_dep((const float4 *)&emb[(size_t)t * D + c4 * 4]);
 }
 
 // Y = A W^T + b (pre-linear, flash.py:207), or with kAccumulate: Y += A W
@@ -521,11 +524,13 @@ k_edge_bwd(const EdgeArgs a, const float *__restrict__ P, const float *__restric
 // optionally the trailing half-kick (md.py:134-138) and the blow-up check
 // (md.py:183-185).  One warp per node; single writer per output.
 __global__ void __launch_bounds__(256)
-k_forces_finish(const int32_t *__restrict__ ptr, const int32_t *__restrict__ rev,
-                const float4 *__restrict__ gsum, int N, int RN, int64_t cap_e,
-                const float *__restrict__ f_extra, float *__restrict__ forces,
-                fcg_md_params kick, int do_kick, const float *__restrict__ mass,
-                float *__restrict__ vel, int64_t *__restrict__ status, const int64_t *step) {
+k_forces_finish(const int32_t *ptr, const int32_t *rev,
+                const float4 *gsum, int N, int RN, int64_t cap_e,
+                const float *f_extra, float *forces,
+                fcg_md_params kick, int do_kick, const float *mass,
+                float *vel, int64_t *status, const int64_t *step) {
+  pdl_trigger();
+  pdl_wait();
   // one warp per node: lanes stride the node's CSR row, then a fixed-order
   // butterfly sum (deterministic; replaces a serial per-thread walk that left
   // most SMs idle)
@@ -571,7 +576,9 @@ k_forces_finish(const int32_t *__restrict__ ptr, const int32_t *__restrict__ rev
 
 // energy[r] = sum_i per_atom[r*N + i] (flash.py:489), fixed tree order.
 __global__ void __launch_bounds__(256)
-k_replica_energy(const float *__restrict__ per_atom, int N, float *__restrict__ energy) {
+k_replica_energy(const float *per_atom, int N, float *energy) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float red[256];
   const int r = blockIdx.x;
   float acc = 0.f;
@@ -690,8 +697,8 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
   const size_t sm1 = TE * LDH * sizeof(float), sm2 = 2 * sm1;
   {
     FCG_PROF(P_EMBED, s);
-    k_embed<<<ceil_div((long long)RN * (D / 4), 256), 256, 0, s>>>(m->embedding, types, N, RN,
-                                                                   b.X);
+    launch_pdl(PDL_SMALL, k_embed, ceil_div((long long)RN * (D / 4), 256), 256, 0, s, m->embedding,
+               types, N, RN, b.X, b.amax, 2 * FCG_MAX_BLOCKS);
   }
 
   EdgeArgs ea;
@@ -702,7 +709,6 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
   ea.dbg = g_dbg_phase;
   const bool simt = use_simt_edges();
   const int eg = simt ? 2 * sm_count() : sm_count();
-  cudaMemsetAsync(b.amax, 0, sizeof(unsigned int) * 2 * FCG_MAX_BLOCKS, s);
   if (!simt) {
     edge_tc_configure();
     node_tc_configure();
@@ -777,9 +783,10 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
   fcg_md_params kp{};
   if (kick) kp = *kick;
   FCG_PROF(P_FORCES, s);
-  k_forces_finish<<<ceil_div((long long)RN * 32, 256), 256, 0, s>>>(
-      ptr, rev, b.gsum, N, RN, cap_e, f_extra, forces, kp, kick != nullptr, mass, vel, status, step);
-  k_replica_energy<<<R, 256, 0, s>>>(per_atom, N, energy);
+  launch_pdl(PDL_SMALL, k_forces_finish, ceil_div((long long)RN * 32, 256), 256, 0, s, ptr, rev,
+             b.gsum, N, RN, cap_e, f_extra, forces, kp, (int)(kick != nullptr), mass, vel, status,
+             step);
+  launch_pdl(PDL_SMALL, k_replica_energy, R, 256, 0, s, per_atom, N, energy);
   return cuda_status("energy_forces");
 }
 

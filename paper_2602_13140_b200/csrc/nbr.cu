@@ -37,11 +37,13 @@ __device__ __forceinline__ bool within_cutoff(double xi, double yi, double zi, d
 // kFill=false: count row lengths into cnt[]; kFill=true: write nbr/own at ptr[row].
 template <typename T, bool kFill>
 __global__ void __launch_bounds__(NBR_WARPS * 32)
-k_scan_rows(const T *__restrict__ pos, int N, double rc2, int32_t *__restrict__ cnt,
-            const int32_t *__restrict__ ptr, int64_t cap_e, int32_t *__restrict__ nbr,
-            int32_t *__restrict__ own, int64_t *__restrict__ status, const int64_t *gate,
-            int stride, uint32_t *__restrict__ masks = nullptr,
-            int32_t *__restrict__ rep_total = nullptr) {
+k_scan_rows(const T *pos, int N, double rc2, int32_t *cnt,
+            const int32_t *ptr, int64_t cap_e, int32_t *nbr,
+            int32_t *own, int64_t *status, const int64_t *gate,
+            int stride, uint32_t *masks = nullptr,
+            int32_t *rep_total = nullptr) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ double sx[NBR_TILE], sy[NBR_TILE], sz[NBR_TILE];
   const int r = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -127,8 +129,10 @@ k_scan_rows(const T *__restrict__ pos, int N, double rc2, int32_t *__restrict__ 
   }
 }
 
-__global__ void k_finalize(const int32_t *__restrict__ ptr, int nrows, int64_t cap_e,
-                           int64_t *__restrict__ status) {
+__global__ void k_finalize(const int32_t *ptr, int nrows, int64_t cap_e,
+                           int64_t *status) {
+  pdl_trigger();
+  pdl_wait();
   if (threadIdx.x == 0) {
     long long e = ptr[nrows];
     status[FCG_ST_EDGES] = e;
@@ -141,8 +145,10 @@ __global__ void k_finalize(const int32_t *__restrict__ ptr, int nrows, int64_t c
 // rev[k] for slot k of row i (edge j -> i) = slot of edge i -> j in row j,
 // i.e. the reference's group_by_source perm (neighbors.py:129-132).
 __global__ void __launch_bounds__(256)
-k_rev(const int32_t *__restrict__ ptr, const int32_t *__restrict__ nbr, int nrows,
-      int64_t cap_e, int32_t *__restrict__ rev, const int64_t *gate, int stride) {
+k_rev(const int32_t *ptr, const int32_t *nbr, int nrows,
+      int64_t cap_e, int32_t *rev, const int64_t *gate, int stride) {
+  pdl_trigger();
+  pdl_wait();
   if (gate && stride > 1 && (*gate % stride) != 0) return;
   int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= nrows) return;
@@ -176,10 +182,12 @@ static size_t nbr_assemble_smem(int N) {
 }
 
 __global__ void __launch_bounds__(512)
-k_nbr_assemble(const uint32_t *__restrict__ masks, const int32_t *__restrict__ rep_total, int R,
-               int N, int64_t cap_e, int32_t *__restrict__ ptr, int32_t *__restrict__ nbr,
-               int32_t *__restrict__ rev, int32_t *__restrict__ own, int64_t *__restrict__ status,
+k_nbr_assemble(const uint32_t *masks, const int32_t *rep_total, int R,
+               int N, int64_t cap_e, int32_t *ptr, int32_t *nbr,
+               int32_t *rev, int32_t *own, int64_t *status,
                const int64_t *gate, int stride) {
+  pdl_trigger();
+  pdl_wait();
   // dynamic smem: bit words [N*W] | exclusive popcount per word [N*W] | row offsets [N+1]
   extern __shared__ uint32_t dsm[];
   const int W = (N + 31) / 32;
@@ -330,9 +338,9 @@ int nbr_build_t(const T *pos, int R, int N, double r_cut, int64_t cap_e, int32_t
     cudaMemsetAsync(rep_total, 0, sizeof(int32_t) * (size_t)R, s);
     {
       FCG_PROF(P_NBR_COUNT, s);
-      k_scan_rows<T, false><<<grid, NBR_WARPS * 32, 0, s>>>(pos, N, rc2, cnt, ptr, cap_e, nullptr,
-                                                            nullptr, status, gate, stride, masks,
-                                                            rep_total);
+      launch_pdl(PDL_SMALL, k_scan_rows<T, false>, grid, NBR_WARPS * 32, 0, s, pos, N, rc2, cnt,
+                 (const int32_t *)ptr, cap_e, (int32_t *)nullptr, (int32_t *)nullptr, status, gate,
+                 stride, masks, rep_total);
     }
     {
       FCG_PROF(P_NBR_FILL, s);
@@ -343,8 +351,9 @@ int nbr_build_t(const T *pos, int R, int N, double r_cut, int64_t cap_e, int32_t
         attr = true;
       }
       const dim3 agrid(R, (N + 95) / 96);  // ~96 rows per CTA
-      k_nbr_assemble<<<agrid, 512, nbr_assemble_smem(N), s>>>(masks, rep_total, R, N, cap_e, ptr,
-                                                              nbr, rev, own, status, gate, stride);
+      launch_pdl(PDL_SMALL, k_nbr_assemble, agrid, 512, nbr_assemble_smem(N), s,
+                 (const uint32_t *)masks, (const int32_t *)rep_total, R, N, cap_e, ptr, nbr, rev,
+                 own, status, gate, stride);
     }
     return cuda_status("nbr_build");
   }
