@@ -211,9 +211,10 @@ void launch_readout_tc(const float *X, const fcg_model &m, float *per_atom, floa
                        cudaStream_t s);
 // edge_tc.cu
 void edge_tc_configure();
-int edge_tc_units(int grid);
+int edge_tc_units(int grid);      // work units of the backward edge kernel
+int edge_tc_units_fwd(int grid);  // work units of the forward edge kernel
 void launch_edge_geom(const EdgeArgs &a, float4 *geo, float2 *env, int32_t *unit_rows,
-                      int nunits, cudaStream_t s);
+                      int nunits, int32_t *unit_rows_fwd, int nunits_fwd, cudaStream_t s);
 void launch_edge_fwd_tc(const EdgeArgs &a, const float4 *geo, const float2 *env,
                         const int32_t *unit_rows, const float *P, float *H, int grid,
                         cudaStream_t s);

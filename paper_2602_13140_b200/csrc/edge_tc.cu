@@ -54,9 +54,18 @@
 namespace fcg {
 
 constexpr int TT = 32;           // edges per tile (MMA N)
-constexpr int NGRP = 4;          // independent warp groups per CTA
+constexpr int NGRP = 4;          // independent warp groups per CTA (backward)
+// The forward's TMEM map and aliased smem layout also fit a fifth group
+// (-DFCG_FWD_GROUPS=5: 640 threads at 96 registers), measured slower
+// (1.136 vs 1.111 ms/step: the spills cost more than the extra warps hide).
+#ifndef FCG_FWD_GROUPS
+#define FCG_FWD_GROUPS 4
+#endif
+constexpr int FWD_NGRP = FCG_FWD_GROUPS;
+constexpr int MAX_NGRP = FWD_NGRP > NGRP ? FWD_NGRP : NGRP;
 constexpr int GT = 128;          // threads per group: one warp per TMEM lane quarter
 constexpr int TC_THREADS = NGRP * GT;
+constexpr int FWD_THREADS = FWD_NGRP * GT;
 constexpr uint32_t KSTR = (TT / 8) * 128;  // B operand bytes per 8 K-rows
 constexpr uint32_t SM_W0 = 0;          // W0 hi|lo: 2 x 128x64 fp16
 constexpr uint32_t SM_W1 = 32768;      // W1 hi|lo: 2 x 128x128 fp16
@@ -70,22 +79,30 @@ constexpr uint32_t W0_BYTES = D * DR * 2, W1_BYTES = D * D * 2;
 constexpr uint32_t S0 = 0, S1 = 32;
 enum { BAR_G1 = 0, BAR_G2 = 1, BAR_G3 = 2, BAR_G1P = 3 };
 
-constexpr int NWARP = TC_THREADS / 32;
+constexpr int NWARP = MAX_NGRP * GT / 32;
 struct WarpMeta {  // one tile, private to a warp (double-buffered)
   int own[TT], nbr[TT];
   float d[TT], env[TT], denv[TT];
 };
 struct TcShared {
   WarpMeta wm[NWARP][2];
-  float xg[NGRP][2][4][TT];   // per-quarter partial grad_d (double-buffered)
-  uint64_t bar[NGRP][4];      // GEMM completion, per kind
-  uint64_t xbar[NGRP];        // the four partial grad_d rows of a tile are written
-  uint64_t wbar;              // filter weight images landed (bulk copy)
-  unsigned int req[NGRP][4];  // operand arrivals per GEMM kind (mod 4)
+  float xg[MAX_NGRP][2][4][TT];   // per-quarter partial grad_d (double-buffered)
+  uint64_t bar[MAX_NGRP][4];      // GEMM completion, per kind
+  uint64_t xbar[MAX_NGRP];        // the four partial grad_d rows of a tile are written
+  uint64_t wbar;                  // filter weight images landed (bulk copy)
+  unsigned int req[MAX_NGRP][4];  // operand arrivals per GEMM kind (mod 4)
   uint32_t tmem;
 };
 constexpr uint32_t SM_TOTAL = SM_META + sizeof(TcShared);
 static_assert(SM_TOTAL + 1024 <= 232448, "shared memory budget");
+// Forward layout: group buffers from offset 0; the weight images are staged
+// over them (SM_W0/SM_W1 < FWD_SM_META) and moved to TMEM before any group
+// writes its buffers.
+constexpr uint32_t FWD_SM_BUF = 0;
+constexpr uint32_t FWD_SM_META = FWD_SM_BUF + FWD_NGRP * GBUF_BYTES;
+constexpr uint32_t FWD_SM_TOTAL = FWD_SM_META + sizeof(TcShared);
+static_assert(SM_W1 + 2 * W1_BYTES <= FWD_SM_META, "forward staging aliases the group buffers");
+static_assert(FWD_SM_TOTAL + 1024 <= 232448, "forward shared memory budget");
 
 // ---- CSR segment sums -------------------------------------------------------
 // Running sum of one channel over edges in CSR order; each completed row is
@@ -146,24 +163,29 @@ struct SegSum {
 __global__ void __launch_bounds__(256)
 k_edge_geom(const float *pos, const int32_t *ptr, const int32_t *nbr, const int32_t *own,
             int nrows, int64_t cap_e, float cutoff, float4 *geo, float2 *env,
-            int32_t *unit_rows, int nunits) {
+            int32_t *unit_rows, int nunits, int32_t *unit_rows2, int nunits2) {
   pdl_trigger();
   pdl_wait();
   __syncthreads();  // keeps ptxas from hoisting loads above the wait
   long long e_tot = ld_dep(&ptr[nrows]);
   if (e_tot > cap_e) e_tot = cap_e;
-  const long long G = nunits;
   for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r <= nrows;
        r += (long long)gridDim.x * blockDim.x) {
     const long long lo = r == 0 ? -1 : ld_dep(&ptr[r - 1]), hi = ld_dep(&ptr[r]);
-    if (r == 0) {
-      unit_rows[0] = 0;
-      unit_rows[G] = nrows;
+#pragma unroll 1
+    for (int part = 0; part < 2; ++part) {  // backward (4 groups) / forward partitions
+      int32_t *ur = part ? unit_rows2 : unit_rows;
+      const long long G = part ? nunits2 : nunits;
+      if (!ur) continue;
+      if (r == 0) {
+        ur[0] = 0;
+        ur[G] = nrows;
+      }
+      if (hi <= lo) continue;  // empty row: no boundary maps to it
+      long long u = lo < 0 ? 1 : (e_tot > 0 ? ((lo + 1) * G + e_tot - 1) / e_tot : G);
+      if (u < 1) u = 1;
+      for (; u < G && e_tot * u / G <= hi; ++u) ur[u] = (int32_t)r;
     }
-    if (hi <= lo) continue;  // empty row: no boundary maps to it
-    long long u = lo < 0 ? 1 : (e_tot > 0 ? ((lo + 1) * G + e_tot - 1) / e_tot : G);
-    if (u < 1) u = 1;
-    for (; u < G && e_tot * u / G <= hi; ++u) unit_rows[u] = (int32_t)r;
   }
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < e_tot;
        k += (long long)gridDim.x * blockDim.x) {
@@ -280,7 +302,8 @@ struct Wctx {
     __syncwarp();                                     \
   } while (0)
 
-__device__ __forceinline__ Wctx make_wctx(uint8_t *sm, TcShared *sh, uint32_t gcols = 128u) {
+__device__ __forceinline__ Wctx make_wctx(uint8_t *sm, TcShared *sh, uint32_t gcols,
+                                          uint32_t buf_base) {
   Wctx W;
   // warp index through a shuffle: the compiler then knows it (and every
   // address derived from it) is warp-uniform, so MMA descriptors stay in
@@ -291,7 +314,7 @@ __device__ __forceinline__ Wctx make_wctx(uint8_t *sm, TcShared *sh, uint32_t gc
   W.lane = threadIdx.x & 31;
   W.ch = 32 * W.q + W.lane;
   W.sh = sh;
-  W.bb = sm + SM_BUF + W.g * GBUF_BYTES;
+  W.bb = sm + buf_base + W.g * GBUF_BYTES;
   W.hb = W.bb + BB_BYTES;
   W.sbb = tc::smem_u32(W.bb);
   W.shb = tc::smem_u32(W.hb);
@@ -302,7 +325,8 @@ __device__ __forceinline__ Wctx make_wctx(uint8_t *sm, TcShared *sh, uint32_t gc
 
 // The filter weight images are staged by the TMA engine (cp.async.bulk);
 // every thread waits on wbar before reading them.
-__device__ __forceinline__ void kernel_prologue(uint8_t *sm, TcShared *sh, const fcg_block &b) {
+__device__ __forceinline__ void kernel_prologue(uint8_t *sm, TcShared *sh, const fcg_block &b,
+                                                int ngrp) {
   if (threadIdx.x == 0) {
     tc::mbar_init(&sh->wbar, 1);
     tc::fence_mbar_init();
@@ -310,7 +334,7 @@ __device__ __forceinline__ void kernel_prologue(uint8_t *sm, TcShared *sh, const
     tc::bulk_g2s(sm + SM_W0, b.f0_img, 2 * W0_BYTES, &sh->wbar);
     tc::bulk_g2s(sm + SM_W1, b.f1_img, 2 * W1_BYTES, &sh->wbar);
   }
-  if (threadIdx.x < NGRP) {
+  if ((int)threadIdx.x < ngrp) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       tc::mbar_init(&sh->bar[threadIdx.x][i], 1);
@@ -335,7 +359,7 @@ __device__ __forceinline__ void kernel_prologue(uint8_t *sm, TcShared *sh, const
 // Forward columns: [TW0, TW0+64) W0 hi | lo (K=64: 32 columns each),
 // [TW1, TW1+128) W1 hi | lo (K=128).
 constexpr uint32_t FWD_GCOLS = 64;  // forward groups: slots S0, S1 only
-constexpr uint32_t TW0 = NGRP * FWD_GCOLS, TW1 = TW0 + 64;
+constexpr uint32_t TW0 = FWD_NGRP * FWD_GCOLS, TW1 = TW0 + 64;
 static_assert(TW1 + 128 <= 512, "TMEM budget");
 
 // Row m of a staged core-matrix image with K inputs (element (r,c) at
@@ -385,7 +409,9 @@ __device__ __forceinline__ void load_fwd_weights_tmem(const uint8_t *sm, uint32_
   const int w = threadIdx.x >> 5, q = w & 3, m = 32 * q + (threadIdx.x & 31);
   const int img = (w >> 2) & 3;
   const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16);
-  if (img < 2)
+  if (w >= 16) {
+    // a fifth group has nothing to move
+  } else if (img < 2)
     image_row_to_tmem<false>((const uint16_t *)(sm + SM_W0 + (img & 1) * W0_BYTES), DR, m,
                              lane_base + TW0 + (img & 1) * (DR / 2));
   else
@@ -546,24 +572,24 @@ __device__ __forceinline__ UnitRange unit_range(const EdgeArgs &a, const int32_t
 // requests G1(i+1); the gathers P[src] of tile i+1 are in flight during
 // G1(i+1).  Iteration -1 only prepares tile 0.
 template <bool Q>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+__global__ void __launch_bounds__(FWD_THREADS, 1)
 k_edge_fwd_tc(const EdgeArgs a, const float4 *geo, const float2 *env,
               const int32_t *unit_rows, const float *P,
               float *H) {
   extern __shared__ __align__(1024) uint8_t sm[];
-  TcShared *sh = (TcShared *)(sm + SM_META);
+  TcShared *sh = (TcShared *)(sm + FWD_SM_META);
   const fcg_block &B = a.blk;
   pdl_trigger();
-  kernel_prologue(sm, sh, B);
+  kernel_prologue(sm, sh, B, FWD_NGRP);
   tc::mbar_wait(&sh->wbar, 0);
   load_fwd_weights_tmem(sm, sh->tmem);  // ends with the PDL wait
-  const Wctx W = make_wctx(sm, sh, FWD_GCOLS);
+  const Wctx W = make_wctx(sm, sh, FWD_GCOLS, FWD_SM_BUF);
   const uint32_t idesc = tc::idesc_f16(128, TT, 0, 1);
   constexpr int NP = Q ? 1 : 3;
   const uint32_t w0h = sh->tmem + TW0, w0l = w0h + DR / 2, w1h = sh->tmem + TW1, w1l = w1h + D / 2;
   const Desc bb = adesc(W.sbb, DR), hb = adesc(W.shb, D);
 
-  const UnitRange tr = unit_range(a, unit_rows, NGRP * blockIdx.x + W.g);
+  const UnitRange tr = unit_range(a, unit_rows, FWD_NGRP * blockIdx.x + W.g);
   const int ntiles = (tr.ee - tr.eb + TT - 1) / TT;
   const int ch = W.ch;
   SegSum seg;
@@ -708,10 +734,10 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *geo, const float2 *env,
   TcShared *sh = (TcShared *)(sm + SM_META);
   const fcg_block &B = a.blk;
   pdl_trigger();
-  kernel_prologue(sm, sh, B);
+  kernel_prologue(sm, sh, B, NGRP);
   tc::mbar_wait(&sh->wbar, 0);
   load_w1_tmem(sm, sh->tmem);  // ends with the PDL wait
-  const Wctx W = make_wctx(sm, sh, BWD_GCOLS);
+  const Wctx W = make_wctx(sm, sh, BWD_GCOLS, SM_BUF);
   float4 *stash = (float4 *)(sm + SM_W1 + W.g * STASH_BYTES);
   const uint32_t sbase = tc::smem_u32(sm);
   const uint32_t id_f = tc::idesc_f16(128, TT, 0, 1);
@@ -875,27 +901,28 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *geo, const float2 *env,
 void edge_tc_configure() {
   static bool done = false;
   if (done) return;
-  const int smem = (int)(SM_TOTAL + 1024);
-  cudaFuncSetAttribute(k_edge_fwd_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_edge_fwd_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int smem = (int)(SM_TOTAL + 1024), fsmem = (int)(FWD_SM_TOTAL + 1024);
+  cudaFuncSetAttribute(k_edge_fwd_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
+  cudaFuncSetAttribute(k_edge_fwd_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
   cudaFuncSetAttribute(k_edge_bwd_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_edge_bwd_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   done = true;
 }
 
 int edge_tc_units(int grid) { return NGRP * grid; }
+int edge_tc_units_fwd(int grid) { return FWD_NGRP * grid; }
 
 void launch_edge_geom(const EdgeArgs &a, float4 *geo, float2 *env, int32_t *unit_rows,
-                      int nunits, cudaStream_t s) {
-  launch_pdl(PDL_GEOM, k_edge_geom, 1184, 256, 0, s, a.pos, a.ptr, a.nbr, a.own, a.nrows, a.cap_e, a.cutoff,
-             geo, env, unit_rows, nunits);
+                      int nunits, int32_t *unit_rows_fwd, int nunits_fwd, cudaStream_t s) {
+  launch_pdl(PDL_GEOM, k_edge_geom, 1184, 256, 0, s, a.pos, a.ptr, a.nbr, a.own, a.nrows, a.cap_e,
+             a.cutoff, geo, env, unit_rows, nunits, unit_rows_fwd, nunits_fwd);
 }
 
 void launch_edge_fwd_tc(const EdgeArgs &a, const float4 *geo, const float2 *env,
                         const int32_t *unit_rows, const float *P, float *H, int grid,
                         cudaStream_t s) {
-  launch_pdl(PDL_EDGE_FWD, a.quant ? k_edge_fwd_tc<true> : k_edge_fwd_tc<false>, grid, TC_THREADS,
-             SM_TOTAL + 1024, s, a, geo, env, unit_rows, P, H);
+  launch_pdl(PDL_EDGE_FWD, a.quant ? k_edge_fwd_tc<true> : k_edge_fwd_tc<false>, grid,
+             FWD_THREADS, FWD_SM_TOTAL + 1024, s, a, geo, env, unit_rows, P, H);
 }
 
 void launch_edge_bwd_tc(const EdgeArgs &a, const float4 *geo, const float2 *env,

@@ -641,7 +641,7 @@ static EfBuffers carve_ef(Carver &c, int T, size_t RN, int64_t cap_e) {
   b.gsum = c.take<float4>((size_t)cap_e + 1);
   b.geo = c.take<float4>((size_t)cap_e + 1);
   b.env = c.take<float2>((size_t)cap_e + 1);
-  b.unit_rows = c.take<int32_t>(4096);
+  b.unit_rows = c.take<int32_t>(4096);  // backward partition at 0, forward at 2048
   b.amax = c.take<unsigned int>(2 * FCG_MAX_BLOCKS);
   return b;
 }
@@ -713,7 +713,8 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
     edge_tc_configure();
     node_tc_configure();
     FCG_PROF(P_EDGE_GEOM, s);
-    launch_edge_geom(ea, b.geo, b.env, b.unit_rows, edge_tc_units(eg), s);
+    launch_edge_geom(ea, b.geo, b.env, b.unit_rows, edge_tc_units(eg), b.unit_rows + 2048,
+                     edge_tc_units_fwd(eg), s);
   }
 
   for (int t = 0; t < T; ++t) {
@@ -733,7 +734,7 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
       if (simt)
         k_edge_fwd<<<eg, NT, (TE * LDR + TE * LDH) * sizeof(float), s>>>(ea, b.P[t], b.H);
       else
-        launch_edge_fwd_tc(ea, b.geo, b.env, b.unit_rows, b.P[t], b.H, eg, s);
+        launch_edge_fwd_tc(ea, b.geo, b.env, b.unit_rows + 2048, b.P[t], b.H, eg, s);
     }
     {
       FCG_PROF(P_NODE_POST, s);
