@@ -81,7 +81,7 @@ enum { BAR_G1 = 0, BAR_G2 = 1, BAR_G3 = 2, BAR_G1P = 3 };
 
 constexpr int NWARP = MAX_NGRP * GT / 32;
 struct WarpMeta {  // one tile, private to a warp (double-buffered)
-  int own[TT], nbr[TT];
+  int own[TT], nbr[TT];  // nbr holds row offsets nbr * D
   float d[TT], env[TT], denv[TT];
 };
 struct TcShared {
@@ -464,7 +464,7 @@ struct MetaRegs {
     const int last = __shfl_sync(0xffffffffu, o, max(n_e - 1, 0));
     rows2 = __all_sync(0xffffffffu, lane >= n_e || o == first || o == last);
     m->own[lane] = lane < n_e ? o : last;  // padding edges extend the last row (m = 0)
-    m->nbr[lane] = n;
+    m->nbr[lane] = n * D;  // row offset of the gathered operand (P[src] / GH[dst])
     m->d[lane] = g.w;
     m->env[lane] = c.x;
     m->denv[lane] = c.y;
@@ -512,17 +512,25 @@ __device__ __forceinline__ void tile_basis(const EdgeArgs &a, const Wctx &W, con
 // h = ssp(z0) for this thread's channel over the tile (z0 = TMEM S0 scaled),
 // as the K=128 B operand (act buffer).  Padding columns carry finite values
 // that no valid edge reads.
+// The fp32 split needs h * 2^f_hexp: the power-of-two scale is folded into
+// z's constants and ssp's (HScale), so no separate multiply per element.
+struct HScale {
+  float rs, b, c_ln2, c_e;  // z*hs = acc*rs + b; ssp_scaled constants
+  __device__ __forceinline__ HScale(float rs0, float b0c, float hs)
+      : rs(rs0 * hs), b(b0c * hs), c_ln2(kLn2 * hs), c_e(-kLog2e / hs) {}
+};
+
 template <bool Q>
-__device__ __forceinline__ void tile_h(const Wctx &W, float rs0, float b0c, float hs) {
+__device__ __forceinline__ void tile_h(const Wctx &W, float rs0, float b0c, const HScale &hk) {
   float v[TT];
   tc::tmem_ld32w(W.tl + S0, v);
 #pragma unroll
   for (int i = 0; i < TT; ++i) {
     if (Q) v[i] = __half2float(__float2half_rn(ssp_fast(v[i] * rs0 + b0c)));
-    else v[i] = ssp_fast(v[i] * rs0 + b0c);
+    else v[i] = ssp_scaled(v[i] * hk.rs + hk.b, hk.c_ln2, hk.c_e);  // = hs * ssp(z)
   }
 #pragma unroll
-  for (int j = 0; j < TT / 8; ++j) put8<!Q>(W.hb, D, W.ch, 8 * j, &v[8 * j], hs);
+  for (int j = 0; j < TT / 8; ++j) put8<!Q>(W.hb, D, W.ch, 8 * j, &v[8 * j], 1.f);
 }
 
 // Sum of p over the 32 lanes of the warp for every edge: a butterfly
@@ -592,6 +600,7 @@ k_edge_fwd_tc(const EdgeArgs a, const float4 *geo, const float2 *env,
   const UnitRange tr = unit_range(a, unit_rows, FWD_NGRP * blockIdx.x + W.g);
   const int ntiles = (tr.ee - tr.eb + TT - 1) / TT;
   const int ch = W.ch;
+  const float *Pch = P + ch;  // gathers: Pch + nbr row offset
   SegSum seg;
   seg.row = ntiles > 0 ? a.own[tr.eb] : -1;
   seg.acc = 0.f;
@@ -600,6 +609,7 @@ k_edge_fwd_tc(const EdgeArgs a, const float4 *geo, const float2 *env,
   const float b0c = ld_dep(&B.f0_b[ch]), b1c = ld_dep(&B.f1_b[ch]);
   const float rs0 = Q ? ld_dep(&B.f0_s[ch]) : pow2f(-(B.f0_exp + 14));
   const float hs = Q ? 1.f : pow2f(B.f_hexp);
+  const HScale hk(rs0, b0c, hs);
   const float s1 = Q ? ld_dep(&B.f1_s[ch]) : pow2f(-(B.f1_exp + B.f_hexp));
   const float bsc = Q ? 1.f : 16384.f;
 
@@ -618,7 +628,7 @@ k_edge_fwd_tc(const EdgeArgs a, const float4 *geo, const float2 *env,
     } else {
       W.wait(BAR_G1, it);
       PHASE(0, it, 1);
-      tile_h<Q>(W, rs0, b0c, hs);
+      tile_h<Q>(W, rs0, b0c, hk);
       REQ(BAR_G2, (mma_chain_ts<D / 16, NP>(W.tmem_g + S1, w1h, w1l, hb, idesc)));
       PHASE(0, it, 2);
       if (more) {
@@ -650,7 +660,7 @@ k_edge_fwd_tc(const EdgeArgs a, const float4 *geo, const float2 *env,
     if (more) {
       const WarpMeta *Mn = W.meta(it + 1);
 #pragma unroll
-      for (int i = 0; i < TT; ++i) pv[i] = ld_gather(&P[(size_t)Mn->nbr[i] * D + ch]);
+      for (int i = 0; i < TT; ++i) pv[i] = ld_gather(Pch + Mn->nbr[i]);
     }
   }
   seg.finish();
@@ -700,7 +710,7 @@ __device__ __forceinline__ void load_w1_tmem(const uint8_t *sm, uint32_t tmem) {
 // ssp'(z) = sigmoid(z) = 1 - exp(-ssp(z))/2 from h; W16: from z0 itself (h is
 // rounded to fp16).
 template <bool Q>
-__device__ __forceinline__ void tile_h_bwd(const Wctx &W, float rs0, float b0c, float hs,
+__device__ __forceinline__ void tile_h_bwd(const Wctx &W, float rs0, float b0c, const HScale &hk,
                                            float4 *stash) {
   float v[TT];
   tc::tmem_ld32w(W.tl + SA, v);
@@ -709,19 +719,19 @@ __device__ __forceinline__ void tile_h_bwd(const Wctx &W, float rs0, float b0c, 
     float s[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const float z = v[i + j] * rs0 + b0c;
       if (Q) {
+        const float z = v[i + j] * rs0 + b0c;
         s[j] = sigmoid_fast(z);
         v[i + j] = __half2float(__float2half_rn(ssp_fast(z)));
       } else {
-        v[i + j] = ssp_fast(z);
-        s[j] = fmaf(-0.5f, ex2_ftz(v[i + j] * -kLog2e), 1.f);
+        v[i + j] = ssp_scaled(v[i + j] * hk.rs + hk.b, hk.c_ln2, hk.c_e);  // hs * h
+        s[j] = fmaf(-0.5f, ex2_ftz(v[i + j] * hk.c_e), 1.f);            // 1 - e^-h / 2
       }
     }
     stash[(i / 4) * D + W.ch] = make_float4(s[0], s[1], s[2], s[3]);
   }
 #pragma unroll
-  for (int j = 0; j < TT / 8; ++j) put8<!Q>(W.hb, D, W.ch, 8 * j, &v[8 * j], hs);
+  for (int j = 0; j < TT / 8; ++j) put8<!Q>(W.hb, D, W.ch, 8 * j, &v[8 * j], 1.f);
 }
 
 template <bool Q>
@@ -749,6 +759,7 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *geo, const float2 *env,
   const UnitRange tr = unit_range(a, unit_rows, NGRP * blockIdx.x + W.g);
   const int ntiles = (tr.ee - tr.eb + TT - 1) / TT;
   const int ch = W.ch;
+  const float *GHch = GH + ch;  // gathers: GHch + dst row offset
   SegSum seg;
   seg.row = ntiles > 0 ? a.own[tr.eb] : -1;
   seg.acc = 0.f;
@@ -757,6 +768,7 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *geo, const float2 *env,
   const float b0c = ld_dep(&B.f0_b[ch]), b1c = ld_dep(&B.f1_b[ch]);
   const float rs0 = Q ? ld_dep(&B.f0_s[ch]) : pow2f(-(B.f0_exp + 14));
   const float hs = Q ? 1.f : pow2f(B.f_hexp);
+  const HScale hk(rs0, b0c, hs);
   const float s1 = Q ? ld_dep(&B.f1_s[ch]) : pow2f(-(B.f1_exp + B.f_hexp));
   const float bsc = Q ? 1.f : 16384.f;
   // backward GEMMs against the stored fp16 weights fold the W16 dequant
@@ -789,14 +801,14 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *geo, const float2 *env,
     const int n_e = min(TT, tr.ee - t0);
     float gh[TT];  // grad_H[dst][ch] (flash.py:281)
 #pragma unroll
-    for (int i = 0; i < TT; ++i) gh[i] = ld_gather(&GH[(size_t)M->nbr[i] * D + ch]);
+    for (int i = 0; i < TT; ++i) gh[i] = ld_gather(GHch + M->nbr[i]);
     // P[src][ch] (flash.py:291): src = the tile's CSR rows, usually its
     // first and last only
     const int o_f = M->own[0], o_l = M->own[n_e - 1];
     const float p_f = ld_gather(&P[(size_t)o_f * D + ch]), p_l = ld_gather(&P[(size_t)o_l * D + ch]);
     W.wait(BAR_G1, it);
     PHASE(1, it, 1);
-    tile_h_bwd<Q>(W, rs0, b0c, hs, stash);
+    tile_h_bwd<Q>(W, rs0, b0c, hk, stash);
     REQ(BAR_G2, (mma_chain_ts<D / 16, NPF>(W.tmem_g + SA, w1h, w1l, hb, id_f)));
     PHASE(1, it, 2);
     if (more) {

@@ -137,8 +137,14 @@ constexpr float kLn2 = 0.6931471805599453f;
 // rounding flips (~1e-4 relative energy on tiny systems), far inside the
 // reference's own W16 contract (1e-2 vs fp32, tests/test_quantize.py:169),
 // while CUDA's accurate expf/log1pf cost 37% of the W16 step.
+// ln2 * (lg2(1 + t) - 1) = ln2 * lg2(0.5 t + 0.5): the -1 folds into one FFMA.
 __device__ __forceinline__ float ssp_fast(float x) {
-  return fmaf(kLn2, lg2_ftz(1.f + ex2_ftz(fabsf(x) * -kLog2e)) - 1.f, fmaxf(x, 0.f));
+  return fmaf(kLn2, lg2_ftz(fmaf(ex2_ftz(fabsf(x) * -kLog2e), 0.5f, 0.5f)), fmaxf(x, 0.f));
+}
+// s * ssp(x) for a power-of-two s > 0 from xs = s * x (exact): the scale rides
+// in the constants, c_ln2 = s ln2 and c_e = -log2(e) / s.
+__device__ __forceinline__ float ssp_scaled(float xs, float c_ln2, float c_e) {
+  return fmaf(c_ln2, lg2_ftz(fmaf(ex2_ftz(fabsf(xs) * c_e), 0.5f, 0.5f)), fmaxf(xs, 0.f));
 }
 __device__ __forceinline__ float sigmoid_fast(float x) {
   return rcp_ftz(1.f + ex2_ftz(x * -kLog2e));
