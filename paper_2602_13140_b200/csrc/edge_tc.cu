@@ -482,7 +482,7 @@ struct MetaRegs {
 // Padding edges carry C = C' = 0, so their columns are zero without a mask.
 template <bool DERIV, bool Q>
 __device__ __forceinline__ void tile_basis(const EdgeArgs &a, const Wctx &W, const WarpMeta *m,
-                                           float scale) {
+                                           float log2_scale) {
   const int k = 16 * W.q + (W.lane & 15), e0 = (W.lane >> 4) * 16;
   const float mu = ld_dep(&a.centers[k]);
   const float ngl = -a.gamma * kLog2e, g2 = -2.f * a.gamma;
@@ -500,13 +500,14 @@ __device__ __forceinline__ void tile_basis(const EdgeArgs &a, const Wctx &W, con
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const float dl = dd[i] - mu;
-            const float gs = ex2_ftz((ngl * dl) * dl);
+      // exp(-g dl^2) * 2^log2_scale in one ex2: the operand scale is free
+      const float gs = ex2_ftz(fmaf(ngl * dl, dl, log2_scale));
       v[4 * j + i] = DERIV ? gs * (g2 * dl * cc[i] + pp[i]) : gs * cc[i];
     }
   }
   constexpr bool LO = DERIV || !Q;
-  put8<LO>(W.bb, DR, k, e0, &v[0], scale);
-  put8<LO>(W.bb, DR, k, e0 + 8, &v[8], scale);
+  put8<LO>(W.bb, DR, k, e0, &v[0], 1.f);
+  put8<LO>(W.bb, DR, k, e0 + 8, &v[8], 1.f);
 }
 
 // h = ssp(z0) for this thread's channel over the tile (z0 = TMEM S0 scaled),
@@ -611,7 +612,7 @@ k_edge_fwd_tc(const EdgeArgs a, const float4 *geo, const float2 *env,
   const float hs = Q ? 1.f : pow2f(B.f_hexp);
   const HScale hk(rs0, b0c, hs);
   const float s1 = Q ? ld_dep(&B.f1_s[ch]) : pow2f(-(B.f1_exp + B.f_hexp));
-  const float bsc = Q ? 1.f : 16384.f;
+  const float bsc = Q ? 0.f : 14.f;  // log2 of the forward basis scale
 
   float pv[TT];  // P[src][ch] of the current tile
   MetaRegs mr;   // raw metadata of the tile after next
@@ -709,9 +710,11 @@ __device__ __forceinline__ void load_w1_tmem(const uint8_t *sm, uint32_t tmem) {
 // thread's stash entries ([edge/4][channel] float4s, conflict-free).  fp32:
 // ssp'(z) = sigmoid(z) = 1 - exp(-ssp(z))/2 from h; W16: from z0 itself (h is
 // rounded to fp16).
+// The stash holds ssp'(z0) * kz, kz = the scales of grad_h (sg3) and dz0
+// (sdz), so gz and the grad_d product need no separate multiplies.
 template <bool Q>
 __device__ __forceinline__ void tile_h_bwd(const Wctx &W, float rs0, float b0c, const HScale &hk,
-                                           float4 *stash) {
+                                           float kz, float4 *stash) {
   float v[TT];
   tc::tmem_ld32w(W.tl + SA, v);
 #pragma unroll
@@ -721,11 +724,11 @@ __device__ __forceinline__ void tile_h_bwd(const Wctx &W, float rs0, float b0c, 
     for (int j = 0; j < 4; ++j) {
       if (Q) {
         const float z = v[i + j] * rs0 + b0c;
-        s[j] = sigmoid_fast(z);
+        s[j] = sigmoid_fast(z) * kz;
         v[i + j] = __half2float(__float2half_rn(ssp_fast(z)));
       } else {
         v[i + j] = ssp_scaled(v[i + j] * hk.rs + hk.b, hk.c_ln2, hk.c_e);  // hs * h
-        s[j] = fmaf(-0.5f, ex2_ftz(v[i + j] * hk.c_e), 1.f);            // 1 - e^-h / 2
+        s[j] = fmaf(-0.5f * kz, ex2_ftz(v[i + j] * hk.c_e), kz);        // kz (1 - e^-h / 2)
       }
     }
     stash[(i / 4) * D + W.ch] = make_float4(s[0], s[1], s[2], s[3]);
@@ -770,7 +773,7 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *geo, const float2 *env,
   const float hs = Q ? 1.f : pow2f(B.f_hexp);
   const HScale hk(rs0, b0c, hs);
   const float s1 = Q ? ld_dep(&B.f1_s[ch]) : pow2f(-(B.f1_exp + B.f_hexp));
-  const float bsc = Q ? 1.f : 16384.f;
+  const float bsc = Q ? 0.f : 14.f;  // log2 of the forward basis scale
   // backward GEMMs against the stored fp16 weights fold the W16 dequant
   // scale of the contracted index into the operand: g @ (s*w16) == (g*s) @ w16
   const float q1 = Q ? ld_dep(&B.f1_s[ch]) : 1.f;
@@ -778,8 +781,8 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *geo, const float2 *env,
   const int sg = scale_exp(pmax * ghmax * B.f1_qmax);
   const float gws = pow2f(sg) * q1;
   const float sg3 = pow2f(-((Q ? 0 : B.f1_exp) + sg));
-  const float dbs = pow2f(B.f_dbexp);
   const float sdz = (Q ? ld_dep(&B.f0_s[ch]) : pow2f(-B.f0_exp)) * pow2f(-B.f_dbexp);
+  const float kz = sg3 * sdz;
 
   float4 ue = make_float4(0.f, 0.f, 0.f, 0.f), ue_n = ue;  // this lane's edge: (u, d)
   bool rows2 = true, rows2_n = true;
@@ -806,9 +809,10 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *geo, const float2 *env,
     // first and last only
     const int o_f = M->own[0], o_l = M->own[n_e - 1];
     const float p_f = ld_gather(&P[(size_t)o_f * D + ch]), p_l = ld_gather(&P[(size_t)o_l * D + ch]);
+    const float pf_s = p_f * gws, pl_s = p_l * gws;  // grad_w operand scale folded in
     W.wait(BAR_G1, it);
     PHASE(1, it, 1);
-    tile_h_bwd<Q>(W, rs0, b0c, hk, stash);
+    tile_h_bwd<Q>(W, rs0, b0c, hk, kz, stash);
     REQ(BAR_G2, (mma_chain_ts<D / 16, NPF>(W.tmem_g + SA, w1h, w1l, hb, id_f)));
     PHASE(1, it, 2);
     if (more) {
@@ -825,12 +829,13 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *geo, const float2 *env,
       float v[8];
       if (rows2) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = gh[8 * j + i] * (oo[i] == o_l ? p_l : p_f);
+        for (int i = 0; i < 8; ++i) v[i] = gh[8 * j + i] * (oo[i] == o_l ? pl_s : pf_s);
+        put8<true>(W.hb, D, ch, 8 * j, v, 1.f);
       } else {  // a tile spanning 3+ rows: per-edge loads
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[i] = gh[8 * j + i] * ld_gather(&P[(size_t)max(oo[i], 0) * D + ch]);
+        put8<true>(W.hb, D, ch, 8 * j, v, gws);
       }
-      put8<true>(W.hb, D, ch, 8 * j, v, gws);
     }
     REQ(BAR_G3, (mma_chain_ts<D / 16, NPB>(W.tmem_g + SB, w1th, w1tl, hb, id_f)));
     PHASE(1, it, 4);
@@ -848,7 +853,7 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *geo, const float2 *env,
     }
     PHASE(1, it, 5);
     // db -> basis buffer (G1 is done), G1': dz0 = W0 db into SA (w consumed)
-    tile_basis<true, Q>(a, W, M, dbs);
+    tile_basis<true, Q>(a, W, M, (float)B.f_dbexp);
     REQ(BAR_G1P, (mma_chain<DR / 16, NPB>(W.tmem_g + SA, w0, bb, id_f)));
     PHASE(1, it, 6);
     W.wait(BAR_G3, it);
@@ -859,7 +864,7 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *geo, const float2 *env,
 #pragma unroll
       for (int i = 0; i < TT; i += 4) {
         const float4 s = stash[(i / 4) * D + ch];
-        gz[i] *= sg3 * s.x; gz[i + 1] *= sg3 * s.y; gz[i + 2] *= sg3 * s.z; gz[i + 3] *= sg3 * s.w;
+        gz[i] *= s.x; gz[i + 1] *= s.y; gz[i + 2] *= s.z; gz[i + 3] *= s.w;
       }
       tc::tmem_st32(W.tl + SB, gz);
       tc::tmem_st_wait();
@@ -875,7 +880,7 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *geo, const float2 *env,
       tc::tmem_ld32w(W.tl + SB, p);
       tc::tmem_ld32w(W.tl + SA, dz);
 #pragma unroll
-      for (int i = 0; i < TT; ++i) p[i] *= dz[i] * sdz;
+      for (int i = 0; i < TT; ++i) p[i] *= dz[i];  // sdz rides in the stash
     }
     if (more) {  // basis + G1 of the next tile (SA is read) overlap the reduction
       tile_basis<false, Q>(a, W, W.meta(it + 1), bsc);
