@@ -50,6 +50,15 @@ template <class T>
 __device__ __forceinline__ T ld_gather(const T *p) {
   return __ldg(p);
 }
+// A per-thread base pointer the compiler cannot re-associate with the
+// offsets added to it: base + (uint32_t)off then compiles to a single
+// IMAD.WIDE.U32 per gather instead of a 64-bit sign-extended add chain.
+template <class T>
+__device__ __forceinline__ const T *opaque_ptr(const T *p) {
+  const T *q;
+  asm("mov.b64 %0, %1;" : "=l"(q) : "l"(p));
+  return q;
+}
 enum PdlSite { PDL_GEOM, PDL_EDGE_FWD, PDL_EDGE_BWD, PDL_NODE_PRE, PDL_NODE_PRE_BWD,
                PDL_NODE_POST, PDL_NODE_POST_BWD, PDL_READOUT,
                PDL_SMALL };  // integrator, prior, neighbour, embed and finish kernels

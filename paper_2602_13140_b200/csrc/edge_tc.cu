@@ -601,7 +601,7 @@ k_edge_fwd_tc(const EdgeArgs a, const float4 *geo, const float2 *env,
   const UnitRange tr = unit_range(a, unit_rows, FWD_NGRP * blockIdx.x + W.g);
   const int ntiles = (tr.ee - tr.eb + TT - 1) / TT;
   const int ch = W.ch;
-  const float *Pch = P + ch;  // gathers: Pch + nbr row offset
+  const float *Pch = opaque_ptr(P + ch);  // gathers: Pch + nbr row offset
   SegSum seg;
   seg.row = ntiles > 0 ? a.own[tr.eb] : -1;
   seg.acc = 0.f;
@@ -661,7 +661,7 @@ k_edge_fwd_tc(const EdgeArgs a, const float4 *geo, const float2 *env,
     if (more) {
       const WarpMeta *Mn = W.meta(it + 1);
 #pragma unroll
-      for (int i = 0; i < TT; ++i) pv[i] = ld_gather(Pch + Mn->nbr[i]);
+      for (int i = 0; i < TT; ++i) pv[i] = ld_gather(Pch + (uint32_t)Mn->nbr[i]);
     }
   }
   seg.finish();
@@ -762,7 +762,7 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *geo, const float2 *env,
   const UnitRange tr = unit_range(a, unit_rows, NGRP * blockIdx.x + W.g);
   const int ntiles = (tr.ee - tr.eb + TT - 1) / TT;
   const int ch = W.ch;
-  const float *GHch = GH + ch;  // gathers: GHch + dst row offset
+  const float *GHch = opaque_ptr(GH + ch);  // gathers: GHch + dst row offset
   SegSum seg;
   seg.row = ntiles > 0 ? a.own[tr.eb] : -1;
   seg.acc = 0.f;
@@ -804,7 +804,7 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *geo, const float2 *env,
     const int n_e = min(TT, tr.ee - t0);
     float gh[TT];  // grad_H[dst][ch] (flash.py:281)
 #pragma unroll
-    for (int i = 0; i < TT; ++i) gh[i] = ld_gather(GHch + M->nbr[i]);
+    for (int i = 0; i < TT; ++i) gh[i] = ld_gather(GHch + (uint32_t)M->nbr[i]);
     // P[src][ch] (flash.py:291): src = the tile's CSR rows, usually its
     // first and last only
     const int o_f = M->own[0], o_l = M->own[n_e - 1];
