@@ -54,8 +54,8 @@ __device__ __forceinline__ T ld_gather(const T *p) {
 // offsets added to it: base + (uint32_t)off then compiles to a single
 // IMAD.WIDE.U32 per gather instead of a 64-bit sign-extended add chain.
 template <class T>
-__device__ __forceinline__ const T *opaque_ptr(const T *p) {
-  const T *q;
+__device__ __forceinline__ T *opaque_ptr(T *p) {
+  T *q;
   asm("mov.b64 %0, %1;" : "=l"(q) : "l"(p));
   return q;
 }

@@ -127,7 +127,7 @@ struct SegSum {
       }
       if (o[0] == o[15]) {  // one row for all 16 edges
         if (o[0] != row) {
-          outc[(size_t)row * D] = acc;
+          outc[(uint32_t)row * D] = acc;
           row = o[0];
           acc = 0.f;
         }
@@ -141,7 +141,7 @@ struct SegSum {
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const bool nr = o[i] != row;
-          if (nr) outc[(size_t)row * D] = acc;
+          if (nr) outc[(uint32_t)row * D] = acc;
           acc = (nr ? 0.f : acc) + m[h + i];
           row = o[i];
         }
@@ -149,7 +149,7 @@ struct SegSum {
     }
   }
   __device__ __forceinline__ void finish() {
-    if (row >= 0) outc[(size_t)row * D] = acc;
+    if (row >= 0) outc[(uint32_t)row * D] = acc;
   }
 };
 
@@ -605,7 +605,7 @@ k_edge_fwd_tc(const EdgeArgs a, const float4 *geo, const float2 *env,
   SegSum seg;
   seg.row = ntiles > 0 ? a.own[tr.eb] : -1;
   seg.acc = 0.f;
-  seg.outc = H + ch;
+  seg.outc = opaque_ptr(H + ch);
 
   const float b0c = ld_dep(&B.f0_b[ch]), b1c = ld_dep(&B.f1_b[ch]);
   const float rs0 = Q ? ld_dep(&B.f0_s[ch]) : pow2f(-(B.f0_exp + 14));
@@ -763,10 +763,11 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *geo, const float2 *env,
   const int ntiles = (tr.ee - tr.eb + TT - 1) / TT;
   const int ch = W.ch;
   const float *GHch = opaque_ptr(GH + ch);  // gathers: GHch + dst row offset
+  const float *Pch = opaque_ptr(P + ch);    // P[src] rows of the tile
   SegSum seg;
   seg.row = ntiles > 0 ? a.own[tr.eb] : -1;
   seg.acc = 0.f;
-  seg.outc = GP + ch;
+  seg.outc = opaque_ptr(GP + ch);
 
   const float b0c = ld_dep(&B.f0_b[ch]), b1c = ld_dep(&B.f1_b[ch]);
   const float rs0 = Q ? ld_dep(&B.f0_s[ch]) : pow2f(-(B.f0_exp + 14));
@@ -808,7 +809,7 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *geo, const float2 *env,
     // P[src][ch] (flash.py:291): src = the tile's CSR rows, usually its
     // first and last only
     const int o_f = M->own[0], o_l = M->own[n_e - 1];
-    const float p_f = ld_gather(&P[(size_t)o_f * D + ch]), p_l = ld_gather(&P[(size_t)o_l * D + ch]);
+    const float p_f = ld_gather(Pch + (uint32_t)o_f * D), p_l = ld_gather(Pch + (uint32_t)o_l * D);
     const float pf_s = p_f * gws, pl_s = p_l * gws;  // grad_w operand scale folded in
     W.wait(BAR_G1, it);
     PHASE(1, it, 1);
@@ -833,7 +834,7 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *geo, const float2 *env,
         put8<true>(W.hb, D, ch, 8 * j, v, 1.f);
       } else {  // a tile spanning 3+ rows: per-edge loads
 #pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = gh[8 * j + i] * ld_gather(&P[(size_t)max(oo[i], 0) * D + ch]);
+        for (int i = 0; i < 8; ++i) v[i] = gh[8 * j + i] * ld_gather(Pch + (uint32_t)max(oo[i], 0) * D);
         put8<true>(W.hb, D, ch, 8 * j, v, gws);
       }
     }
