@@ -171,11 +171,13 @@ __device__ __forceinline__ int rows_to_act(const float *src, int node0, int nrow
   static_assert(NPT == 32, "one warp lane per node of the thread's range");
   float v[NPT];
   float mx = 0.f;
+  // the thread's rows are consecutive: one base, immediate offsets i * D
+  const float *rb = opaque_ptr(src + (size_t)(node0 + c.ec) * D + c.ch);
 #pragma unroll
   for (int i = 0; i < NPT; ++i) {
     int n = node0 + c.ec + i;
     const bool in = n < nrows;
-    float x = in ? ld_dep(&src[(size_t)n * D + c.ch]) * colscale : 0.f;
+    float x = in ? ld_dep(rb + i * D) * colscale : 0.f;
     if ((empty >> i) & 1u) x = 0.f;
     if (q16_only) x = __half2float(__float2half_rn(x));
     v[i] = x;
@@ -246,6 +248,8 @@ k_node_linear_tc(const float *X, const uint16_t *img, int wexp,
   NodeCtx c = node_prologue(sm, meta, img, 2 * IMG128);
   node_stamp(kMode, 1);
   const int node0 = blockIdx.x * Cfg::NN;
+  const size_t r0 = (size_t)(node0 + c.ec) * D + c.ch;  // this thread: rows r0 + i*D
+  float *Yr = opaque_ptr(Y + r0);
   const bool fwd = kMode == 0;
   // backward folds the W16 row scale of the K index (output channel) into X
   const float fold = (!fwd && quant) ? ld_dep(&rowscale[c.ch]) : 1.f;
@@ -258,7 +262,7 @@ k_node_linear_tc(const float *X, const uint16_t *img, int wexp,
 #pragma unroll
   for (int i = 0; i < NPT; ++i) {
     const int n = node0 + c.ec + i;
-    yv[i] = (!fwd && n < nrows) ? Y[(size_t)n * D + c.ch] : 0.f;
+    yv[i] = (!fwd && n < nrows) ? Yr[i * D] : 0.f;
   }
   NODE_WAIT();
   node_stamp(kMode, 3);
@@ -275,7 +279,7 @@ k_node_linear_tc(const float *X, const uint16_t *img, int wexp,
       if (n < nrows) {
         float r = v[i] * un + b;
         r = fwd ? r : yv[c0 + i] + r;
-        Y[(size_t)n * D + c.ch] = r;
+        Yr[(c0 + i) * D] = r;
         mx = fmaxf(mx, fabsf(r));
       }
     }
@@ -301,6 +305,8 @@ k_node_post_tc(const float *H, const fcg_block blk, int quant,
   NodeCtx c = node_prologue(sm, meta, blk.p0_img, 2 * IMG128, blk.p1_img, 2 * IMG128);
   node_stamp(2, 1);
   const int node0 = blockIdx.x * Cfg::NN;
+  const size_t r0 = (size_t)(node0 + c.ec) * D + c.ch;  // this thread: rows r0 + i*D
+  float *Zpr = opaque_ptr(Zp + r0), *Xr = opaque_ptr(X + r0);
   const int np = quant ? 1 : 3;
   const uint32_t idesc = tc::idesc_f16(128, Cfg::NN, 0, 1);
   const int s0 = rows_to_act<Cfg::KSTR>(H, node0, nrows, c, 1.f, quant, &meta->amax[0], act, csr_ptr);
@@ -320,7 +326,7 @@ k_node_post_tc(const float *H, const fcg_block blk, int quant,
     for (int i = 0; i < 16; ++i) {
       int n = node0 + c.ec + c0 + i;
       float z = v[i] * un0 + b0;
-      if (n < nrows) Zp[(size_t)n * D + c.ch] = z;
+      if (n < nrows) Zpr[(c0 + i) * D] = z;
       const float a = quant ? __half2float(__float2half_rn(ssp_fast(z))) : ssp_fast(z);
       v[i] = n < nrows ? a : 0.f;
       mx = fmaxf(mx, fabsf(v[i]));
@@ -338,7 +344,7 @@ k_node_post_tc(const float *H, const fcg_block blk, int quant,
 #pragma unroll
   for (int i = 0; i < NPT; ++i) {
     const int n = node0 + c.ec + i;
-    xv[i] = n < nrows ? X[(size_t)n * D + c.ch] : 0.f;
+    xv[i] = n < nrows ? Xr[i * D] : 0.f;
   }
   NODE_WAIT();
   const float un1 = quant ? ld_dep(&blk.p1_s[c.ch]) : pow2f(-(blk.p1_exp + s1));
@@ -350,7 +356,7 @@ k_node_post_tc(const float *H, const fcg_block blk, int quant,
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       int n = node0 + c.ec + c0 + i;
-      if (n < nrows) X[(size_t)n * D + c.ch] = xv[c0 + i] + (v[i] * un1 + b1);
+      if (n < nrows) Xr[(c0 + i) * D] = xv[c0 + i] + (v[i] * un1 + b1);
     }
   }
   node_stamp(2, 5);
@@ -373,6 +379,9 @@ k_node_post_bwd_tc(const float *G, const fcg_block blk, int quant,
   NodeCtx c = node_prologue(sm, meta, blk.p1_img, 2 * IMG128, blk.p0_img, 2 * IMG128);
   node_stamp(3, 1);
   const int node0 = blockIdx.x * Cfg::NN;
+  const size_t r0 = (size_t)(node0 + c.ec) * D + c.ch;  // this thread: rows r0 + i*D
+  const float *Zpr = opaque_ptr(Zp + r0);
+  float *GHr = opaque_ptr(GH + r0);
   const int np = quant ? 2 : 3;
   const uint32_t idesc = tc::idesc_f16(128, Cfg::NN, 1, 1);
   const float f1 = quant ? ld_dep(&blk.p1_s[c.ch]) : 1.f;
@@ -384,7 +393,7 @@ k_node_post_bwd_tc(const float *G, const fcg_block blk, int quant,
 #pragma unroll
   for (int i = 0; i < NPT; ++i) {
     const int n = node0 + c.ec + i;
-    zv[i] = n < nrows ? ld_dep(&Zp[(size_t)n * D + c.ch]) : 0.f;
+    zv[i] = n < nrows ? ld_dep(Zpr + i * D) : 0.f;
   }
   NODE_WAIT();
   node_stamp(3, 3);
@@ -419,7 +428,7 @@ k_node_post_bwd_tc(const float *G, const fcg_block blk, int quant,
     for (int i = 0; i < 16; ++i) {
       int n = node0 + c.ec + c0 + i;
       if (n < nrows) {
-        GH[(size_t)n * D + c.ch] = v[i] * un1;
+        GHr[(c0 + i) * D] = v[i] * un1;
         mx = fmaxf(mx, fabsf(v[i] * un1));
       }
     }
@@ -447,6 +456,8 @@ k_readout_tc(const float *X, const fcg_model m, float *per_atom,
   node_stamp(4, 1);
   const bool quant = m.format == FCG_FMT_W16;
   const int node0 = blockIdx.x * Cfg::NN;
+  const size_t r0 = (size_t)(node0 + c.ec) * D + c.ch;  // this thread: rows r0 + i*D
+  float *Gr = opaque_ptr(G + r0);
   const int sx = rows_to_act<Cfg::KSTR>(X, node0, nrows, c, 1.f, quant, &meta->amax[0], act);
   node_stamp(4, 2);
   NODE_ISSUE(c.tm + NTM_D0, c.sbase + Cfg::WA, IMG64, D, false, c.sbase + Cfg::ACT, D,
@@ -501,7 +512,7 @@ k_readout_tc(const float *X, const fcg_model m, float *per_atom,
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       int n = node0 + c.ec + c0 + i;
-      if (n < nrows) G[(size_t)n * D + c.ch] = v[i] * un1;
+      if (n < nrows) Gr[(c0 + i) * D] = v[i] * un1;
     }
   }
   node_stamp(4, 5);
