@@ -117,20 +117,16 @@ struct SegSum {
   // Tile of TT edges in CSR order with rows own[] (padding edges repeat the
   // last valid row and carry m = 0).
   __device__ __forceinline__ void tile(const int *own, const float (&m)[TT]) {
+    // All lanes walk the same edges, so the edges that start a new row form
+    // one warp-uniform mask (a ballot): halves without a row start are a
+    // tree sum, others test a uniform bit per edge instead of comparing rows.
+    const int lane = threadIdx.x & 31;
+    const int cur = own[lane];
+    const unsigned starts = __ballot_sync(0xffffffffu, cur != (lane ? own[lane - 1] : row));
 #pragma unroll
     for (int h = 0; h < TT; h += 16) {
-      int o[16];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int4 q = *(const int4 *)&own[h + 4 * j];
-        o[4 * j] = q.x; o[4 * j + 1] = q.y; o[4 * j + 2] = q.z; o[4 * j + 3] = q.w;
-      }
-      if (o[0] == o[15]) {  // one row for all 16 edges
-        if (o[0] != row) {
-          outc[(uint32_t)row * D] = acc;
-          row = o[0];
-          acc = 0.f;
-        }
+      const unsigned hb = (starts >> h) & 0xffffu;
+      if (hb == 0u) {  // the open row continues through all 16 edges
         float s[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) s[i] = m[h + i] + m[h + i + 8];
@@ -140,10 +136,12 @@ struct SegSum {
       } else {
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const bool nr = o[i] != row;
-          if (nr) outc[(uint32_t)row * D] = acc;
-          acc = (nr ? 0.f : acc) + m[h + i];
-          row = o[i];
+          if ((hb >> i) & 1u) {  // edge h+i starts a row (warp-uniform)
+            if (row >= 0) outc[(uint32_t)row * D] = acc;
+            row = own[h + i];
+            acc = 0.f;
+          }
+          acc += m[h + i];
         }
       }
     }
