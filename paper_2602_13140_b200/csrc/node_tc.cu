@@ -173,15 +173,20 @@ __device__ __forceinline__ int rows_to_act(const float *src, int node0, int nrow
   float mx = 0.f;
   // the thread's rows are consecutive: one base, immediate offsets i * D
   const float *rb = opaque_ptr(src + (size_t)(node0 + c.ec) * D + c.ch);
+  if (node0 + c.ec + NPT <= nrows && empty == 0u) {  // warp-uniform: no checks needed
+#pragma unroll
+    for (int i = 0; i < NPT; ++i) v[i] = ld_dep(rb + i * D) * colscale;
+  } else {
+#pragma unroll
+    for (int i = 0; i < NPT; ++i) {
+      const bool in = node0 + c.ec + i < nrows && !((empty >> i) & 1u);
+      v[i] = in ? ld_dep(rb + i * D) * colscale : 0.f;
+    }
+  }
 #pragma unroll
   for (int i = 0; i < NPT; ++i) {
-    int n = node0 + c.ec + i;
-    const bool in = n < nrows;
-    float x = in ? ld_dep(rb + i * D) * colscale : 0.f;
-    if ((empty >> i) & 1u) x = 0.f;
-    if (q16_only) x = __half2float(__float2half_rn(x));
-    v[i] = x;
-    mx = fmaxf(mx, fabsf(x));
+    if (q16_only) v[i] = __half2float(__float2half_rn(v[i]));
+    mx = fmaxf(mx, fabsf(v[i]));
   }
   int s = 0;
   if (!q16_only) s = scale_exp(block_amax(mx, slot));
