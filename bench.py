@@ -280,25 +280,19 @@ def main():
     value = ns_per_day(R * world * args.steps, ms_max / 1e3)
 
     # ---- end-to-end through the host-buffer API --------------------------
-    hpos = torch.empty((R, N, 3), dtype=torch.float32).pin_memory()
-    hvel = torch.empty_like(hpos).pin_memory()
-    hpot = torch.empty(R, dtype=torch.float32).pin_memory()
-    hpri = torch.empty(R, dtype=torch.float32).pin_memory()
-    hpos.copy_(eng.pos)
-    hvel.copy_(eng.vel)
+    hstate = torch.empty((2, R, N, 3), dtype=torch.float32).pin_memory()  # positions, velocities
+    hen = torch.empty((2, R), dtype=torch.float32).pin_memory()            # potential, prior
+    hstate.copy_(eng.state)
     with torch.cuda.stream(stream):
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            eng.pos.copy_(hpos, non_blocking=True)
-            eng.vel.copy_(hvel, non_blocking=True)
+            eng.state.copy_(hstate, non_blocking=True)
             eng.run(1, graph_steps=1)  # the public stepping call (graph replay)
-            hpos.copy_(eng.pos, non_blocking=True)
-            hvel.copy_(eng.vel, non_blocking=True)
-            hpot.copy_(eng.potential, non_blocking=True)
-            hpri.copy_(eng.prior_e, non_blocking=True)
+            hstate.copy_(eng.state, non_blocking=True)
+            hen.copy_(eng.energies, non_blocking=True)
             stream.synchronize()
         e2e_s = time.perf_counter() - t0
     t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)

@@ -97,11 +97,14 @@ class MDEngine:
         self.masses64 = np.asarray(masses, np.float64)
         self.types = torch.as_tensor(types.astype(np.int32), device=self.device)
         f32 = dict(dtype=torch.float32, device=self.device)
-        self.pos = torch.zeros(R, N, 3, **f32)
-        self.vel = torch.zeros(R, N, 3, **f32)
+        # positions and velocities are views of one buffer (and the two
+        # per-replica energies of another), so host I/O of a step's state is
+        # one copy per direction
+        self.state = torch.zeros(2, R, N, 3, **f32)
+        self.pos, self.vel = self.state[0], self.state[1]
         self.forces = torch.zeros(R, N, 3, **f32)
-        self.potential = torch.zeros(R, **f32)
-        self.prior_e = torch.zeros(R, **f32)
+        self.energies = torch.zeros(2, R, **f32)
+        self.potential, self.prior_e = self.energies[0], self.energies[1]
         self.step = torch.zeros(1, dtype=torch.int64, device=self.device)
         self.status = torch.zeros(_lib.FCG_STATUS_WORDS, dtype=torch.int64, device=self.device)
         self._alloc(cap_e or default_capacity(R, N))
