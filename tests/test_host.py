@@ -270,3 +270,21 @@ def test_pdl_kernels_load_nothing_before_the_grid_dependency_wait():
     for fn, r in res.items():
         assert r["wait"], fn
         assert not r["early"], (fn, r["early"][:4])
+
+
+def test_hot_kernels_do_not_spill():
+    """ptxas report of the in-tree build: the edge and node kernels keep
+    everything in registers (a spill in these latency-bound kernels cost
+    2-3% of the step when it happened)."""
+    log = ROOT / "build" / "fcg" / "ptxas.log"
+    if not log.exists():
+        pytest.skip("needs the in-tree build log (python -m paper_2602_13140_b200._build)")
+    text = log.read_text()
+    spills = {}
+    for m in re.finditer(r"Function properties for (\S+)\n\s+(\d+) bytes stack frame, (\d+) bytes "
+                         r"spill stores, (\d+) bytes spill loads", text):
+        name, stores, loads = m.group(1), int(m.group(3)), int(m.group(4))
+        if any(k in name for k in ("k_edge_fwd_tc", "k_edge_bwd_tc", "k_node_", "k_readout_tc")):
+            spills[name] = (stores, loads)
+    assert spills, "no hot kernels found in the ptxas log"
+    assert all(v == (0, 0) for v in spills.values()), spills
