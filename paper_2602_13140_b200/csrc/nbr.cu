@@ -283,6 +283,82 @@ k_nbr_assemble(const uint32_t *masks, const int32_t *rep_total, int R,
   }
 }
 
+// ---- general path (N > 512) from the count pass's bit words ----------------
+// The count pass stores every row's ballot words in global memory; the fill
+// then walks them (no second fp64 predicate pass) and records each word's
+// exclusive popcount within its row, so rev[k] for edge j -> i is
+// ptr[j] + pre[j][i/32] + popcount(row j's word i/32 below bit i%32).
+constexpr size_t NBR_MASK_BYTES_MAX = size_t(2) << 30;  // words + prefixes, else two passes
+static bool nbr_masks_general(int R, int N) {
+  const size_t W = (size_t)(N + 31) / 32;
+  return N > NBR_FUSED_MAX && 2 * (size_t)R * N * W * 4 <= NBR_MASK_BYTES_MAX;
+}
+
+// one warp per row; lane l takes bit l of each 32-source word
+__global__ void __launch_bounds__(256)
+k_fill_masks(const uint32_t *masks, const int32_t *ptr, int R, int N, int64_t cap_e,
+             int32_t *nbr, int32_t *own, int32_t *pre, const int64_t *gate, int stride) {
+  pdl_trigger();
+  pdl_wait();
+  if (gate && stride > 1 && (*gate % stride) != 0) return;
+  const long long row = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= (long long)R * N) return;
+  const int W = (N + 31) / 32;
+  const long long r = row / N;
+  const uint32_t *mr = masks + row * W;
+  int32_t *pr = pre + row * W;
+  const bool ok = (long long)ptr[row + 1] <= cap_e;  // rows past capacity are not written
+  const uint32_t below = (1u << lane) - 1u;
+  int slot = 0;  // within the row
+  const int32_t row_base = ptr[row];
+  for (int w0 = 0; w0 < W; w0 += 32) {
+    // 32 words at once (one coalesced load), their offsets by a warp scan
+    const int wl = w0 + lane;
+    const uint32_t mw = wl < W ? mr[wl] : 0u;
+    const int cnt = __popc(mw);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int wbase = slot + incl - cnt;
+    if (wl < W) pr[wl] = wbase;
+    const int nw = min(32, W - w0);
+    for (int t = 0; t < nw; ++t) {
+      const uint32_t m = __shfl_sync(0xffffffffu, mw, t);
+      const int b = __shfl_sync(0xffffffffu, wbase, t);
+      if (ok && ((m >> lane) & 1u)) {
+        const int k = row_base + b + __popc(m & below);
+        nbr[k] = (int32_t)(r * N + 32 * (w0 + t) + lane);
+        own[k] = (int32_t)row;
+      }
+    }
+    slot += __shfl_sync(0xffffffffu, incl, 31);
+  }
+}
+
+__global__ void __launch_bounds__(256)
+k_rev_masks(const uint32_t *masks, const int32_t *pre, const int32_t *ptr, const int32_t *nbr,
+            const int32_t *own, int R, int N, int64_t cap_e, int32_t *rev, const int64_t *gate,
+            int stride) {
+  pdl_trigger();
+  pdl_wait();
+  if (gate && stride > 1 && (*gate % stride) != 0) return;
+  const long long RN = (long long)R * N;
+  const long long e_tot = ptr[RN];
+  if (e_tot > cap_e) return;  // overflow: CSR invalid
+  const int W = (N + 31) / 32;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < e_tot;
+       k += (long long)gridDim.x * blockDim.x) {
+    const int j = nbr[k], i = own[k];              // edge j -> i
+    const int il = i % N, t = il >> 5;
+    const size_t wj = (size_t)j * W + t;
+    rev[k] = ptr[j] + pre[wj] + __popc(masks[wj] & ((1u << (il & 31)) - 1u));
+  }
+}
+
 size_t nbr_ws_bytes(int R, int N) {
   size_t n = (size_t)R * N + 1;
   size_t tmp = 0;
@@ -293,6 +369,9 @@ size_t nbr_ws_bytes(int R, int N) {
   if (N <= NBR_FUSED_MAX) {
     c.take<uint32_t>((size_t)R * N * ((N + 31) / 32));
     c.take<int32_t>((size_t)R);
+  } else if (nbr_masks_general(R, N)) {
+    c.take<uint32_t>((size_t)R * N * ((N + 31) / 32));
+    c.take<int32_t>((size_t)R * N * ((N + 31) / 32));
   }
   return c.off + 256;
 }
@@ -325,11 +404,15 @@ int nbr_build_t(const T *pos, int R, int N, double r_cut, int64_t cap_e, int32_t
   void *cub_tmp = c.take<char>(tmp);
   const bool fused = N <= NBR_FUSED_MAX && !nbr_fused_disabled();
   uint32_t *masks = nullptr;
-  int32_t *rep_total = nullptr;
+  int32_t *rep_total = nullptr, *wpre = nullptr;
   if (N <= NBR_FUSED_MAX) {
     masks = c.take<uint32_t>((size_t)R * N * ((N + 31) / 32));
     rep_total = c.take<int32_t>((size_t)R);
+  } else if (nbr_masks_general(R, N)) {
+    masks = c.take<uint32_t>((size_t)R * N * ((N + 31) / 32));
+    wpre = c.take<int32_t>((size_t)R * N * ((N + 31) / 32));
   }
+  const bool gen_masks = wpre != nullptr && !nbr_fused_disabled();
   if (!c.ok()) { set_error("nbr_build: workspace too small"); return FCG_ERR_ARG; }
   double rc2 = r_cut * r_cut;  // Python float product, neighbors.py:89
 
@@ -361,12 +444,28 @@ int nbr_build_t(const T *pos, int R, int N, double r_cut, int64_t cap_e, int32_t
   {
     FCG_PROF(P_NBR_COUNT, s);
     k_scan_rows<T, false><<<grid, NBR_WARPS * 32, 0, s>>>(pos, N, rc2, cnt, ptr, cap_e,
-                                                          nullptr, nullptr, status, gate, stride);
+                                                          nullptr, nullptr, status, gate, stride,
+                                                          gen_masks ? masks : nullptr);
   }
   {
     FCG_PROF(P_NBR_SCAN, s);
     cub::DeviceScan::ExclusiveSum(cub_tmp, tmp, cnt, ptr, (int)n, s);
     k_finalize<<<1, 32, 0, s>>>(ptr, (int)(n - 1), cap_e, status);
+  }
+  if (gen_masks) {
+    {
+      FCG_PROF(P_NBR_FILL, s);
+      launch_pdl(PDL_SMALL, k_fill_masks, ceil_div((long long)(n - 1) * 32, 256), 256, 0, s,
+                 (const uint32_t *)masks, (const int32_t *)ptr, R, N, cap_e, nbr, own, wpre, gate,
+                 stride);
+    }
+    {
+      FCG_PROF(P_NBR_REV, s);
+      launch_pdl(PDL_SMALL, k_rev_masks, 4 * 148, 256, 0, s, (const uint32_t *)masks,
+                 (const int32_t *)wpre, (const int32_t *)ptr, (const int32_t *)nbr,
+                 (const int32_t *)own, R, N, cap_e, rev, gate, stride);
+    }
+    return cuda_status("nbr_build");
   }
   {
     FCG_PROF(P_NBR_FILL, s);
