@@ -359,6 +359,101 @@ k_rev_masks(const uint32_t *masks, const int32_t *pre, const int32_t *ptr, const
   }
 }
 
+// ---- windowed count for N > 512 (sort by x) -----------------------------------
+// Candidates of row i are the beads with |x_j - x_i| <= r_cut: a contiguous
+// range of the replica's beads sorted by x.  Exact because d2 < r_cut^2
+// implies |dx| <= r_cut under monotone rounding (fl(dx^2) >= fl(r_cut^2)
+// otherwise), and the reference's fp64 predicate then decides every pair.
+// Hits are set in a per-row bitmask in shared memory, so the row's sources
+// come out in ascending order as the ballot words the fill kernel reads.
+constexpr int NBR_WINDOW_MAX = 16384;  // bitmask of a row: <= 2 KB per warp
+static bool nbr_window_disabled() {
+  static const bool off = [] {
+    const char *v = getenv("FCG_NBR_WINDOW");
+    return v && v[0] == '0';
+  }();
+  return off;
+}
+
+template <typename T>
+__global__ void k_sort_keys(const T *pos, int R, int N, T *keys, int32_t *vals, int32_t *offs) {
+  pdl_trigger();
+  pdl_wait();
+  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (g <= R) offs[g] = (int32_t)(g * N);
+  if (g >= (long long)R * N) return;
+  keys[g] = pos[3 * g];
+  vals[g] = (int32_t)(g % N);
+}
+
+template <typename T>
+__device__ __forceinline__ int lower_bound_x(const T *x, int n, double v) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if ((double)x[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_window_count(const T *pos, const T *xs, const int32_t *perm, int R, int N, double rc,
+               double rc2, int32_t *cnt, uint32_t *masks, int64_t *status, const int64_t *gate,
+               int stride, const int32_t *ptr) {
+  pdl_trigger();
+  pdl_wait();
+  extern __shared__ uint32_t bits_all[];  // [8 warps][W]
+  const int W = (N + 31) / 32, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long g = blockIdx.x * 8ll + warp;
+  if (g >= (long long)R * N) return;
+  if (gate && stride > 1 && (*gate % stride) != 0) {  // list kept: counts from the live ptr
+    if (lane == 0) cnt[g] = ptr[g + 1] - ptr[g];
+    return;
+  }
+  const long long r = g / N;
+  const int i = (int)(g % N);
+  const T *P = pos + r * N * 3;
+  const double xi = (double)P[3 * i], yi = (double)P[3 * i + 1], zi = (double)P[3 * i + 2];
+  uint32_t *bits = bits_all + warp * W;
+  for (int w = lane; w < W; w += 32) bits[w] = 0u;
+  __syncwarp();
+  const T *xr = xs + r * N;
+  const double win = rc * (1.0 + 1e-9) + 1e-12;  // conservative: the predicate decides
+  const int lo = lower_bound_x(xr, N, xi - win), hi = lower_bound_x(xr, N, nextafter(xi + win, 1e300));
+  const int32_t *pr = perm + r * N;
+  for (int q = lo + lane; q < hi; q += 32) {
+    const int j = pr[q];
+    if (j != i && within_cutoff(xi, yi, zi, (double)P[3 * j], (double)P[3 * j + 1],
+                                (double)P[3 * j + 2], rc2))
+      atomicOr(&bits[j >> 5], 1u << (j & 31));
+  }
+  __syncwarp();
+  int c = 0;
+  for (int w = lane; w < W; w += 32) {
+    const uint32_t m = bits[w];
+    masks[g * W + w] = m;
+    c += __popc(m);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0) {
+    cnt[g] = c;
+    atomicMax((unsigned long long *)&status[FCG_ST_MAXDEG], (unsigned long long)c);
+  }
+}
+
+static size_t window_sort_temp(int R, int N) {
+  size_t a = 0, b = 0;
+  cub::DeviceSegmentedRadixSort::SortPairs(nullptr, a, (const float *)nullptr, (float *)nullptr,
+                                           (const int32_t *)nullptr, (int32_t *)nullptr, R * N, R,
+                                           (const int32_t *)nullptr, (const int32_t *)nullptr);
+  cub::DeviceSegmentedRadixSort::SortPairs(nullptr, b, (const double *)nullptr, (double *)nullptr,
+                                           (const int32_t *)nullptr, (int32_t *)nullptr, R * N, R,
+                                           (const int32_t *)nullptr, (const int32_t *)nullptr);
+  return a > b ? a : b;
+}
+
 size_t nbr_ws_bytes(int R, int N) {
   size_t n = (size_t)R * N + 1;
   size_t tmp = 0;
@@ -372,6 +467,12 @@ size_t nbr_ws_bytes(int R, int N) {
   } else if (nbr_masks_general(R, N)) {
     c.take<uint32_t>((size_t)R * N * ((N + 31) / 32));
     c.take<int32_t>((size_t)R * N * ((N + 31) / 32));
+    if (N <= NBR_WINDOW_MAX) {  // x-sorted keys/values (double-sized) + offsets + sort temp
+      c.take<double>((size_t)R * N * 2);
+      c.take<int32_t>((size_t)R * N * 2);
+      c.take<int32_t>((size_t)R + 1);
+      c.take<char>(window_sort_temp(R, N));
+    }
   }
   return c.off + 256;
 }
@@ -413,6 +514,19 @@ int nbr_build_t(const T *pos, int R, int N, double r_cut, int64_t cap_e, int32_t
     wpre = c.take<int32_t>((size_t)R * N * ((N + 31) / 32));
   }
   const bool gen_masks = wpre != nullptr && !nbr_fused_disabled();
+  T *wkeys = nullptr;
+  int32_t *wvals = nullptr, *woffs = nullptr;
+  void *wtemp = nullptr;
+  size_t wtemp_bytes = 0;
+  if (wpre && N <= NBR_WINDOW_MAX) {
+    double *kd = c.take<double>((size_t)R * N * 2);
+    wkeys = (T *)kd;
+    wvals = c.take<int32_t>((size_t)R * N * 2);
+    woffs = c.take<int32_t>((size_t)R + 1);
+    wtemp_bytes = window_sort_temp(R, N);
+    wtemp = c.take<char>(wtemp_bytes);
+  }
+  const bool windowed = gen_masks && wkeys && !nbr_window_disabled();
   if (!c.ok()) { set_error("nbr_build: workspace too small"); return FCG_ERR_ARG; }
   double rc2 = r_cut * r_cut;  // Python float product, neighbors.py:89
 
@@ -441,7 +555,30 @@ int nbr_build_t(const T *pos, int R, int N, double r_cut, int64_t cap_e, int32_t
     return cuda_status("nbr_build");
   }
   cudaMemsetAsync(cnt + (n - 1), 0, sizeof(int32_t), s);
-  {
+  if (windowed) {
+    FCG_PROF(P_NBR_COUNT, s);
+    const size_t RN = (size_t)R * N;
+    T *keys_in = wkeys, *keys_out = wkeys + RN;
+    int32_t *vals_in = wvals, *vals_out = wvals + RN;
+    launch_pdl(PDL_SMALL, k_sort_keys<T>, ceil_div((long long)RN + 1, 256), 256, 0, s, pos, R, N,
+               keys_in, vals_in, woffs);
+    cub::DeviceSegmentedRadixSort::SortPairs(wtemp, wtemp_bytes, (const T *)keys_in, keys_out,
+                                             (const int32_t *)vals_in, vals_out, (int)RN, R,
+                                             (const int32_t *)woffs, (const int32_t *)woffs + 1,
+                                             0, (int)sizeof(T) * 8, s);
+    const int W = (N + 31) / 32;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_window_count<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           8 * (NBR_WINDOW_MAX / 32) * 4);
+      cudaFuncSetAttribute(k_window_count<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           8 * (NBR_WINDOW_MAX / 32) * 4);
+      attr = true;
+    }
+    launch_pdl(PDL_SMALL, k_window_count<T>, ceil_div((long long)RN, 8), 256,
+               (size_t)8 * W * 4, s, pos, (const T *)keys_out, (const int32_t *)vals_out, R, N,
+               r_cut, rc2, cnt, masks, status, gate, stride, (const int32_t *)ptr);
+  } else {
     FCG_PROF(P_NBR_COUNT, s);
     k_scan_rows<T, false><<<grid, NBR_WARPS * 32, 0, s>>>(pos, N, rc2, cnt, ptr, cap_e,
                                                           nullptr, nullptr, status, gate, stride,
