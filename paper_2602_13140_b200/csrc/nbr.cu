@@ -359,14 +359,20 @@ k_rev_masks(const uint32_t *masks, const int32_t *pre, const int32_t *ptr, const
   }
 }
 
-// ---- windowed count for N > 512 (sort by x) -----------------------------------
-// Candidates of row i are the beads with |x_j - x_i| <= r_cut: a contiguous
-// range of the replica's beads sorted by x.  Exact because d2 < r_cut^2
-// implies |dx| <= r_cut under monotone rounding (fl(dx^2) >= fl(r_cut^2)
-// otherwise), and the reference's fp64 predicate then decides every pair.
-// Hits are set in a per-row bitmask in shared memory, so the row's sources
-// come out in ascending order as the ballot words the fill kernel reads.
+// ---- cell-list count for 512 < N <= 16384 -------------------------------------
+// Beads are sorted by a packed key (replica in the top 10 bits, then
+// floor(coord / cs) per axis, 18 bits each; cs = r_cut (1 + 1e-6) so a true
+// neighbour is always within +-1 cell despite rounding), one global radix
+// sort for all replicas.  A row's candidates are then the 9
+// contiguous key runs (cx+a, cy+b, cz-1 .. cz+1), found by one binary-search
+// pair per lane.  Exactness: d2 < r_cut^2 implies |d axis| <= r_cut under
+// monotone rounding, and the reference's fp64 predicate decides every
+// candidate.  Hits are set in a per-row bitmask in shared memory, so the
+// row's sources come out ascending as the ballot words the fill reads.
 constexpr int NBR_WINDOW_MAX = 16384;  // bitmask of a row: <= 2 KB per warp
+constexpr int NBR_WINDOW_MIN = 2048;   // below this the all-pairs count is cheaper than the sort
+constexpr int NBR_WINDOW_MAXR = 1024;  // replica id in the key's top 10 bits
+constexpr long long NBR_CELL_BIAS = 1ll << 17;  // 18 bits per axis
 static bool nbr_window_disabled() {
   static const bool off = [] {
     const char *v = getenv("FCG_NBR_WINDOW");
@@ -375,32 +381,43 @@ static bool nbr_window_disabled() {
   return off;
 }
 
+__device__ __forceinline__ unsigned long long cell_key(long long r, long long cx, long long cy,
+                                                     long long cz) {
+  return ((unsigned long long)r << 54) | ((unsigned long long)(cx + NBR_CELL_BIAS) << 36) |
+         ((unsigned long long)(cy + NBR_CELL_BIAS) << 18) | (unsigned long long)(cz + NBR_CELL_BIAS);
+}
+__device__ __forceinline__ long long cell_of(double v, double inv_cs) {
+  return (long long)floor(v * inv_cs);
+}
+
 template <typename T>
-__global__ void k_sort_keys(const T *pos, int R, int N, T *keys, int32_t *vals, int32_t *offs) {
+__global__ void k_sort_keys(const T *pos, int R, int N, double inv_cs, unsigned long long *keys,
+                            int32_t *vals, int32_t *offs) {
   pdl_trigger();
   pdl_wait();
   const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (g <= R) offs[g] = (int32_t)(g * N);
   if (g >= (long long)R * N) return;
-  keys[g] = pos[3 * g];
+  keys[g] = cell_key(g / N, cell_of((double)pos[3 * g], inv_cs),
+                     cell_of((double)pos[3 * g + 1], inv_cs), cell_of((double)pos[3 * g + 2], inv_cs));
   vals[g] = (int32_t)(g % N);
 }
 
-template <typename T>
-__device__ __forceinline__ int lower_bound_x(const T *x, int n, double v) {
+__device__ __forceinline__ int lower_bound_key(const unsigned long long *k, int n,
+                                               unsigned long long v) {
   int lo = 0, hi = n;
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
-    if ((double)x[mid] < v) lo = mid + 1; else hi = mid;
+    if (k[mid] < v) lo = mid + 1; else hi = mid;
   }
   return lo;
 }
 
 template <typename T>
 __global__ void __launch_bounds__(256)
-k_window_count(const T *pos, const T *xs, const int32_t *perm, int R, int N, double rc,
-               double rc2, int32_t *cnt, uint32_t *masks, int64_t *status, const int64_t *gate,
-               int stride, const int32_t *ptr) {
+k_window_count(const T *pos, const unsigned long long *keys, const int32_t *perm, int R, int N,
+               double inv_cs, double rc2, int32_t *cnt, uint32_t *masks, int64_t *status,
+               const int64_t *gate, int stride, const int32_t *ptr) {
   pdl_trigger();
   pdl_wait();
   extern __shared__ uint32_t bits_all[];  // [8 warps][W]
@@ -417,16 +434,26 @@ k_window_count(const T *pos, const T *xs, const int32_t *perm, int R, int N, dou
   const double xi = (double)P[3 * i], yi = (double)P[3 * i + 1], zi = (double)P[3 * i + 2];
   uint32_t *bits = bits_all + warp * W;
   for (int w = lane; w < W; w += 32) bits[w] = 0u;
+  // lane l < 9: the key run of cell column (cx + l/3 - 1, cy + l%3 - 1, cz-1..cz+1)
+  const unsigned long long *kr = keys + r * N;
+  int run_a = 0, run_b = 0;
+  if (lane < 9) {
+    const long long cx = cell_of(xi, inv_cs) + lane / 3 - 1, cy = cell_of(yi, inv_cs) + lane % 3 - 1;
+    const long long cz = cell_of(zi, inv_cs);
+    run_a = lower_bound_key(kr, N, cell_key(r, cx, cy, cz - 1));
+    run_b = lower_bound_key(kr, N, cell_key(r, cx, cy, cz + 1) + 1);
+  }
   __syncwarp();
-  const T *xr = xs + r * N;
-  const double win = rc * (1.0 + 1e-9) + 1e-12;  // conservative: the predicate decides
-  const int lo = lower_bound_x(xr, N, xi - win), hi = lower_bound_x(xr, N, nextafter(xi + win, 1e300));
   const int32_t *pr = perm + r * N;
-  for (int q = lo + lane; q < hi; q += 32) {
-    const int j = pr[q];
-    if (j != i && within_cutoff(xi, yi, zi, (double)P[3 * j], (double)P[3 * j + 1],
-                                (double)P[3 * j + 2], rc2))
-      atomicOr(&bits[j >> 5], 1u << (j & 31));
+#pragma unroll 1
+  for (int run = 0; run < 9; ++run) {
+    const int a = __shfl_sync(0xffffffffu, run_a, run), b = __shfl_sync(0xffffffffu, run_b, run);
+    for (int q = a + lane; q < b; q += 32) {
+      const int j = pr[q];
+      if (j != i && within_cutoff(xi, yi, zi, (double)P[3 * j], (double)P[3 * j + 1],
+                                  (double)P[3 * j + 2], rc2))
+        atomicOr(&bits[j >> 5], 1u << (j & 31));
+    }
   }
   __syncwarp();
   int c = 0;
@@ -444,14 +471,11 @@ k_window_count(const T *pos, const T *xs, const int32_t *perm, int R, int N, dou
 }
 
 static size_t window_sort_temp(int R, int N) {
-  size_t a = 0, b = 0;
-  cub::DeviceSegmentedRadixSort::SortPairs(nullptr, a, (const float *)nullptr, (float *)nullptr,
-                                           (const int32_t *)nullptr, (int32_t *)nullptr, R * N, R,
-                                           (const int32_t *)nullptr, (const int32_t *)nullptr);
-  cub::DeviceSegmentedRadixSort::SortPairs(nullptr, b, (const double *)nullptr, (double *)nullptr,
-                                           (const int32_t *)nullptr, (int32_t *)nullptr, R * N, R,
-                                           (const int32_t *)nullptr, (const int32_t *)nullptr);
-  return a > b ? a : b;
+  size_t a = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, a, (const unsigned long long *)nullptr,
+                                  (unsigned long long *)nullptr, (const int32_t *)nullptr,
+                                  (int32_t *)nullptr, R * N);
+  return a;
 }
 
 size_t nbr_ws_bytes(int R, int N) {
@@ -467,7 +491,7 @@ size_t nbr_ws_bytes(int R, int N) {
   } else if (nbr_masks_general(R, N)) {
     c.take<uint32_t>((size_t)R * N * ((N + 31) / 32));
     c.take<int32_t>((size_t)R * N * ((N + 31) / 32));
-    if (N <= NBR_WINDOW_MAX) {  // x-sorted keys/values (double-sized) + offsets + sort temp
+    if (N >= NBR_WINDOW_MIN && N <= NBR_WINDOW_MAX && R <= NBR_WINDOW_MAXR) {  // cell keys/values
       c.take<double>((size_t)R * N * 2);
       c.take<int32_t>((size_t)R * N * 2);
       c.take<int32_t>((size_t)R + 1);
@@ -514,13 +538,12 @@ int nbr_build_t(const T *pos, int R, int N, double r_cut, int64_t cap_e, int32_t
     wpre = c.take<int32_t>((size_t)R * N * ((N + 31) / 32));
   }
   const bool gen_masks = wpre != nullptr && !nbr_fused_disabled();
-  T *wkeys = nullptr;
+  unsigned long long *wkeys = nullptr;
   int32_t *wvals = nullptr, *woffs = nullptr;
   void *wtemp = nullptr;
   size_t wtemp_bytes = 0;
-  if (wpre && N <= NBR_WINDOW_MAX) {
-    double *kd = c.take<double>((size_t)R * N * 2);
-    wkeys = (T *)kd;
+  if (wpre && N >= NBR_WINDOW_MIN && N <= NBR_WINDOW_MAX && R <= NBR_WINDOW_MAXR) {
+    wkeys = c.take<unsigned long long>((size_t)R * N * 2);
     wvals = c.take<int32_t>((size_t)R * N * 2);
     woffs = c.take<int32_t>((size_t)R + 1);
     wtemp_bytes = window_sort_temp(R, N);
@@ -558,14 +581,17 @@ int nbr_build_t(const T *pos, int R, int N, double r_cut, int64_t cap_e, int32_t
   if (windowed) {
     FCG_PROF(P_NBR_COUNT, s);
     const size_t RN = (size_t)R * N;
-    T *keys_in = wkeys, *keys_out = wkeys + RN;
+    unsigned long long *keys_in = wkeys, *keys_out = wkeys + RN;
     int32_t *vals_in = wvals, *vals_out = wvals + RN;
+    const double inv_cs = 1.0 / (r_cut * (1.0 + 1e-6));  // cells slightly wider than r_cut
     launch_pdl(PDL_SMALL, k_sort_keys<T>, ceil_div((long long)RN + 1, 256), 256, 0, s, pos, R, N,
-               keys_in, vals_in, woffs);
-    cub::DeviceSegmentedRadixSort::SortPairs(wtemp, wtemp_bytes, (const T *)keys_in, keys_out,
-                                             (const int32_t *)vals_in, vals_out, (int)RN, R,
-                                             (const int32_t *)woffs, (const int32_t *)woffs + 1,
-                                             0, (int)sizeof(T) * 8, s);
+               inv_cs, keys_in, vals_in, woffs);
+    // one global sort: the replica id in the key's top bits keeps replicas apart
+    int end_bit = 54;
+    while ((1ll << (end_bit - 54)) < R) ++end_bit;
+    cub::DeviceRadixSort::SortPairs(wtemp, wtemp_bytes, (const unsigned long long *)keys_in,
+                                    keys_out, (const int32_t *)vals_in, vals_out, (int)RN, 0,
+                                    end_bit, s);
     const int W = (N + 31) / 32;
     static bool attr = false;
     if (!attr) {
@@ -576,8 +602,9 @@ int nbr_build_t(const T *pos, int R, int N, double r_cut, int64_t cap_e, int32_t
       attr = true;
     }
     launch_pdl(PDL_SMALL, k_window_count<T>, ceil_div((long long)RN, 8), 256,
-               (size_t)8 * W * 4, s, pos, (const T *)keys_out, (const int32_t *)vals_out, R, N,
-               r_cut, rc2, cnt, masks, status, gate, stride, (const int32_t *)ptr);
+               (size_t)8 * W * 4, s, pos, (const unsigned long long *)keys_out,
+               (const int32_t *)vals_out, R, N, inv_cs, rc2, cnt, masks, status, gate, stride,
+               (const int32_t *)ptr);
   } else {
     FCG_PROF(P_NBR_COUNT, s);
     k_scan_rows<T, false><<<grid, NBR_WARPS * 32, 0, s>>>(pos, N, rc2, cnt, ptr, cap_e,
