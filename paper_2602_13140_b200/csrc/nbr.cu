@@ -325,8 +325,11 @@ k_fill_masks(const uint32_t *masks, const int32_t *ptr, int R, int N, int64_t ca
     }
     const int wbase = slot + incl - cnt;
     if (wl < W) pr[wl] = wbase;
-    const int nw = min(32, W - w0);
-    for (int t = 0; t < nw; ++t) {
+    // visit only the non-zero words (a row of ~60 sources among N has few)
+    unsigned nz = __ballot_sync(0xffffffffu, mw != 0u);
+    while (nz) {
+      const int t = __ffs(nz) - 1;
+      nz &= nz - 1u;
       const uint32_t m = __shfl_sync(0xffffffffu, mw, t);
       const int b = __shfl_sync(0xffffffffu, wbase, t);
       if (ok && ((m >> lane) & 1u)) {
