@@ -524,7 +524,7 @@ struct HScale {
       : rs(rs0 * hs), b(b0c * hs), c_ln2(kLn2 * hs), c_e(-kLog2e / hs) {}
 };
 
-template <bool Q>
+template <bool Q, uint32_t KS = KSTR>
 __device__ __forceinline__ void tile_h(const Wctx &W, float rs0, float b0c, const HScale &hk) {
   float v[TT];
   tc::tmem_ld32w(W.tl + S0, v);
@@ -534,7 +534,7 @@ __device__ __forceinline__ void tile_h(const Wctx &W, float rs0, float b0c, cons
     else v[i] = ssp_scaled(v[i] * hk.rs + hk.b, hk.c_ln2, hk.c_e);  // = hs * ssp(z)
   }
 #pragma unroll
-  for (int j = 0; j < TT / 8; ++j) put8<!Q>(W.hb, D, W.ch, 8 * j, &v[8 * j], 1.f);
+  for (int j = 0; j < TT / 8; ++j) put8<!Q, KS>(W.hb, D, W.ch, W.eo + 8 * j, &v[8 * j], 1.f);
 }
 
 // Sum of p over the 32 lanes of the warp for every edge: a butterfly
@@ -919,6 +919,126 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *geo, const float2 *env,
   if (threadIdx.x < 32) tc::tmem_dealloc<512>(sh->tmem);
 }
 
+constexpr uint32_t KSTR64 = (64 / 8) * 128;  // B operand bytes per 8 K-rows, 64 edges
+
+// ---------------------------------------------------------------------------
+// Forward with 64-edge MMAs (the default; FCG_FWD64=0 selects k_edge_fwd_tc):
+// 2 groups x 8 warps, each group's tile = 32 edges of each of its two work
+// units, as in k_edge_bwd64.  TMEM: 2 x 128 group columns (z0 | w, 64 wide)
+// + W0 | W1 at TW0; shared memory: the forward layout (buffers 2 x 48 KB).
+template <bool Q>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+k_edge_fwd64(const EdgeArgs a, const float4 *geo, const float2 *env,
+             const int32_t *unit_rows, const float *P, float *H) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  TcShared *sh = (TcShared *)(sm + FWD_SM_META);
+  const fcg_block &B = a.blk;
+  pdl_trigger();
+  kernel_prologue(sm, sh, B, FWD_NGRP);
+  tc::mbar_wait(&sh->wbar, 0);
+  load_fwd_weights_tmem(sm, sh->tmem);  // ends with the PDL wait
+  Wctx W;
+  W.w = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+  W.g = W.w >> 3;
+  const int hf = (W.w >> 2) & 1;
+  const int u = 2 * W.g + hf;
+  W.q = W.w & 3;
+  W.lane = threadIdx.x & 31;
+  W.ch = 32 * W.q + W.lane;
+  W.eo = 32 * hf;
+  W.amask = 7u;
+  W.sh = sh;
+  W.bb = sm + FWD_SM_BUF + W.g * 2 * GBUF_BYTES;
+  W.hb = W.bb + 2 * BB_BYTES;
+  W.sbb = tc::smem_u32(W.bb);
+  W.shb = tc::smem_u32(W.hb);
+  W.tmem_g = sh->tmem + 128u * W.g;
+  W.tl = W.tmem_g + ((uint32_t)(32 * W.q) << 16) + 32u * hf;
+  const uint32_t idesc = tc::idesc_f16(128, 64, 0, 1);
+  constexpr int NP = Q ? 1 : 3;
+  constexpr uint32_t Z0 = 0, WS = 64;  // TMEM slots: z0 | w, 64 columns each
+  const uint32_t w0h = sh->tmem + TW0, w0l = w0h + DR / 2, w1h = sh->tmem + TW1, w1l = w1h + D / 2;
+  const Desc bb = adesc<KSTR64>(W.sbb, DR), hb = adesc<KSTR64>(W.shb, D);
+
+  const UnitRange tr = unit_range(a, unit_rows, FWD_NGRP * blockIdx.x + u);
+  const UnitRange to = unit_range(a, unit_rows, FWD_NGRP * blockIdx.x + (u ^ 1));
+  const int ntiles = (tr.ee - tr.eb + TT - 1) / TT;
+  const int nt_all = max(ntiles, (to.ee - to.eb + TT - 1) / TT);
+  const int ch = W.ch;
+  const float *Pch = opaque_ptr(P + ch);
+  SegSum seg;
+  seg.row = ntiles > 0 ? a.own[tr.eb] : -1;
+  seg.acc = 0.f;
+  seg.outc = opaque_ptr(H + ch);
+
+  const float b0c = ld_dep(&B.f0_b[ch]), b1c = ld_dep(&B.f1_b[ch]);
+  const float rs0 = Q ? ld_dep(&B.f0_s[ch]) : pow2f(-(B.f0_exp + 14));
+  const float hs = Q ? 1.f : pow2f(B.f_hexp);
+  const HScale hk(rs0, b0c, hs);
+  const float s1 = Q ? ld_dep(&B.f1_s[ch]) : pow2f(-(B.f1_exp + B.f_hexp));
+  const float bsc = Q ? 0.f : 14.f;
+
+  float pv[TT];
+  MetaRegs mr;
+  for (int it = -1; it < nt_all; ++it) {
+    const int t0 = tr.eb + it * TT;
+    const bool more = it + 1 < nt_all;
+    if (it < 0) {
+      bool r2;
+      mr.load(a, geo, env, tr.eb, min(TT, tr.ee - tr.eb), W.lane);
+      mr.store(W.meta(0), false, W.lane, r2);
+      mr.load(a, geo, env, tr.eb + TT, min(TT, tr.ee - tr.eb - TT), W.lane);
+    } else {
+      W.wait(BAR_G1, it);
+      tile_h<Q, KSTR64>(W, rs0, b0c, hk);
+      REQ(BAR_G2, (mma_chain_ts<D / 16, NP>(W.tmem_g + WS, w1h, w1l, hb, idesc)));
+      if (more) {
+        bool r2;
+        mr.store(W.meta(it + 1), false, W.lane, r2);
+        mr.load(a, geo, env, t0 + 2 * TT, min(TT, tr.ee - t0 - 2 * TT), W.lane);
+      }
+    }
+    if (more) {  // basis + G1 of the next tile overlap G2
+      tile_basis<false, Q, KSTR64>(a, W, W.meta(it + 1), bsc);
+      REQ(BAR_G1, (mma_chain_ts<DR / 16, NP>(W.tmem_g + Z0, w0h, w0l, bb, idesc)));
+    }
+    if (it >= 0) {
+      W.wait(BAR_G2, it);
+      float v[TT];
+      tc::tmem_ld32w(W.tl + WS, v);
+      const int n_e = min(TT, tr.ee - t0);
+      if (n_e > 0) {  // m = (W1 h + b1) * P[src], dst segment sums
+#pragma unroll
+        for (int i = 0; i < TT; ++i) v[i] = (v[i] * s1 + b1c) * pv[i];
+        if (n_e < TT) {
+#pragma unroll
+          for (int i = 0; i < TT; ++i) v[i] = i < n_e ? v[i] : 0.f;
+        }
+        seg.tile(W.meta(it)->own, v);
+      }
+    }
+    if (more) {
+      const WarpMeta *Mn = W.meta(it + 1);
+      if (tr.ee - (t0 + TT) > 0) {
+#pragma unroll
+        for (int i = 0; i < TT; ++i) pv[i] = ld_gather(Pch + (uint32_t)Mn->nbr[i]);
+      }
+    }
+  }
+  seg.finish();
+  tc::fence_before_sync();
+  __syncthreads();
+  if (threadIdx.x < 32) tc::tmem_dealloc<512>(sh->tmem);
+}
+
+static bool fwd64_enabled() {
+  static const bool on = [] {
+    const char *v = getenv("FCG_FWD64");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 // ---------------------------------------------------------------------------
 // Backward with 64-edge MMAs (the default; FCG_BWD64=0 selects k_edge_bwd_tc):
 // 2 groups x 8 warps.
@@ -927,7 +1047,6 @@ k_edge_bwd_tc(const EdgeArgs a, const float4 *geo, const float2 *env,
 // each GEMM is N = 64 and a group issues half the MMAs per edge.  TMEM: 2 x
 // 128 accumulator columns (SA, SB 64 wide) + W1 | W1^T; the shared-memory
 // layout is the 4-group one (buffers 2 x 48 KB, stash per unit).
-constexpr uint32_t KSTR64 = (64 / 8) * 128;
 template <bool Q>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_edge_bwd64(const EdgeArgs a, const float4 *geo, const float2 *env,
@@ -1133,6 +1252,8 @@ void edge_tc_configure() {
   const int smem = (int)(SM_TOTAL + 1024), fsmem = (int)(FWD_SM_TOTAL + 1024);
   cudaFuncSetAttribute(k_edge_fwd_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
   cudaFuncSetAttribute(k_edge_fwd_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
+  cudaFuncSetAttribute(k_edge_fwd64<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
+  cudaFuncSetAttribute(k_edge_fwd64<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
   cudaFuncSetAttribute(k_edge_bwd_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_edge_bwd_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_edge_bwd64<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1152,8 +1273,12 @@ void launch_edge_geom(const EdgeArgs &a, float4 *geo, float2 *env, int32_t *unit
 void launch_edge_fwd_tc(const EdgeArgs &a, const float4 *geo, const float2 *env,
                         const int32_t *unit_rows, const float *P, float *H, int grid,
                         cudaStream_t s) {
-  launch_pdl(PDL_EDGE_FWD, a.quant ? k_edge_fwd_tc<true> : k_edge_fwd_tc<false>, grid,
-             FWD_THREADS, FWD_SM_TOTAL + 1024, s, a, geo, env, unit_rows, P, H);
+  if (fwd64_enabled() && FWD_NGRP == 4)  // the 64-edge kernel uses the 4-unit partition
+    launch_pdl(PDL_EDGE_FWD, a.quant ? k_edge_fwd64<true> : k_edge_fwd64<false>, grid,
+               TC_THREADS, FWD_SM_TOTAL + 1024, s, a, geo, env, unit_rows, P, H);
+  else
+    launch_pdl(PDL_EDGE_FWD, a.quant ? k_edge_fwd_tc<true> : k_edge_fwd_tc<false>, grid,
+               FWD_THREADS, FWD_SM_TOTAL + 1024, s, a, geo, env, unit_rows, P, H);
 }
 
 void launch_edge_bwd_tc(const EdgeArgs &a, const float4 *geo, const float2 *env,
