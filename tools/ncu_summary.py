@@ -122,8 +122,9 @@ def main(tag):
                     vals.append(f"{v:.1f}")
             lines.append(f"| {d['kernel']} | " + " | ".join(vals) + " |")
             name = d["kernel"].replace("k_", "", 1)
-            if name.endswith("_tc"):  # bench.py's profiler classes drop the suffix
-                name = name[:-3]
+            for suf in ("_tc", "64"):  # bench.py's profiler classes drop the suffix
+                if name.endswith(suf):
+                    name = name[:-len(suf)]
             if "dram_read" in d:
                 summary[name] = {"dram_bytes": d.get("dram_read", 0) + d.get("dram_write", 0),
                                  "duration_s": d.get("duration"), "tag": tag}
