@@ -522,7 +522,9 @@ k_edge_bwd(const EdgeArgs a, const float *__restrict__ P, const float *__restric
 // grad_r[x] = sum_{k in row x} (gsum[rev[k]] - gsum[k])  (flash.py:298-299,
 // dst-segment sum minus src-segment sum), forces = -grad_r (+ f_extra), then
 // optionally the trailing half-kick (md.py:134-138) and the blow-up check
-// (md.py:183-185).  One warp per node; single writer per output.
+// (md.py:183-185).  FF_LPN lanes per node; single writer per output.
+constexpr int FF_LPN = 8;  // lanes per node in k_forces_finish
+
 __global__ void __launch_bounds__(256)
 k_forces_finish(const int32_t *ptr, const int32_t *rev,
                 const float4 *gsum, int N, int RN, int64_t cap_e,
@@ -531,30 +533,41 @@ k_forces_finish(const int32_t *ptr, const int32_t *rev,
                 float *vel, int64_t *status, const int64_t *step) {
   pdl_trigger();
   pdl_wait();
-  // one warp per node: lanes stride the node's CSR row, then a fixed-order
-  // butterfly sum (deterministic; replaces a serial per-thread walk that left
-  // most SMs idle)
-  const int g = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
-  const int lane = threadIdx.x & 31;
-  if (g >= RN) return;
-  const bool valid = (long long)ptr[RN] <= cap_e;
+  // FF_LPN lanes per node: each lane gathers up to four of the node's CSR
+  // slots per pass with all loads issued before use, then a fixed-order
+  // butterfly over the node's lanes (deterministic; replaces a serial
+  // per-thread walk, then a warp per node that left lanes and SMs idle)
+  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int g = (int)(tid / FF_LPN);
+  const int lane = threadIdx.x & (FF_LPN - 1);
   float gx = 0.f, gy = 0.f, gz = 0.f;
-  if (valid) {
+  if (g < RN && (long long)ptr[RN] <= cap_e) {
     const int k1 = ptr[g + 1];
-    for (int k = ptr[g] + lane; k < k1; k += 32) {
-      float4 a = gsum[rev[k]], b = gsum[k];
-      gx += a.x - b.x;
-      gy += a.y - b.y;
-      gz += a.z - b.z;
+    for (int k0 = ptr[g] + lane; k0 < k1; k0 += 4 * FF_LPN) {
+      int r[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) r[j] = k0 + j * FF_LPN < k1 ? rev[k0 + j * FF_LPN] : -1;
+      float4 av[4], bv[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        av[j] = r[j] >= 0 ? gsum[r[j]] : make_float4(0.f, 0.f, 0.f, 0.f);
+        bv[j] = r[j] >= 0 ? gsum[k0 + j * FF_LPN] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        gx += av[j].x - bv[j].x;
+        gy += av[j].y - bv[j].y;
+        gz += av[j].z - bv[j].z;
+      }
     }
   }
 #pragma unroll
-  for (int o = 16; o; o >>= 1) {
+  for (int o = FF_LPN / 2; o; o >>= 1) {
     gx += __shfl_xor_sync(0xffffffffu, gx, o);
     gy += __shfl_xor_sync(0xffffffffu, gy, o);
     gz += __shfl_xor_sync(0xffffffffu, gz, o);
   }
-  if (lane != 0) return;
+  if (lane != 0 || g >= RN) return;
   float f[3] = {-gx, -gy, -gz};
   bool bad = false;
   const int i = g % N;
@@ -784,7 +797,7 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
   fcg_md_params kp{};
   if (kick) kp = *kick;
   FCG_PROF(P_FORCES, s);
-  launch_pdl(PDL_SMALL, k_forces_finish, ceil_div((long long)RN * 32, 256), 256, 0, s, ptr, rev,
+  launch_pdl(PDL_SMALL, k_forces_finish, ceil_div((long long)RN * FF_LPN, 256), 256, 0, s, ptr, rev,
              b.gsum, N, RN, cap_e, f_extra, forces, kp, (int)(kick != nullptr), mass, vel, status,
              step);
   launch_pdl(PDL_SMALL, k_replica_energy, R, 256, 0, s, per_atom, N, energy);
