@@ -349,12 +349,8 @@ __device__ __forceinline__ BondVec bond_eval(const fcg_prior &pr, const float *P
 // One thread per bead: it applies its incident bonds in np.add.at order (all
 // "+fvec" for bonds where it is atom i, then "-fvec" where it is atom j), so
 // the per-bead sums are bitwise the reference's.
-__global__ void __launch_bounds__(256)
-k_prior(const fcg_prior pr, const float *pos, int N, int RN,
-        float *f_prior) {
-  pdl_trigger();
-  pdl_wait();
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+__device__ __forceinline__ void prior_bead(const fcg_prior &pr, const float *pos, int N, int RN,
+                                           float *f_prior, int g) {
   if (g >= RN) return;
   const int r = g / N, i = g % N;
   const float *P = pos + (size_t)r * N * 3;
@@ -374,12 +370,8 @@ k_prior(const fcg_prior pr, const float *pos, int N, int RN,
 }
 
 // Prior energy 0.5 * sum k*s^2 per replica (md.py:118), one CTA per replica.
-__global__ void __launch_bounds__(256)
-k_prior_energy(const fcg_prior pr, const float *pos, int N,
-               float *e_prior) {
-  pdl_trigger();
-  pdl_wait();
-  const int r = blockIdx.x;
+__device__ __forceinline__ void prior_energy(const fcg_prior &pr, const float *pos, int N,
+                                             float *e_prior, int r) {
   const float *P = pos + (size_t)r * N * 3;
   __shared__ float red[256];
   float acc = 0.f;
@@ -393,12 +385,25 @@ k_prior_energy(const fcg_prior pr, const float *pos, int N,
   if (threadIdx.x == 0) e_prior[r] = 0.5f * red[0];
 }
 
+// Both in one launch (they only read positions): blocks [0, nbead) do the
+// per-bead forces, the last R blocks the per-replica energies.
+__global__ void __launch_bounds__(256)
+k_prior(const fcg_prior pr, const float *pos, int N, int RN, int nbead, float *f_prior,
+        float *e_prior) {
+  pdl_trigger();
+  pdl_wait();
+  if ((int)blockIdx.x < nbead)
+    prior_bead(pr, pos, N, RN, f_prior, blockIdx.x * blockDim.x + threadIdx.x);
+  else
+    prior_energy(pr, pos, N, e_prior, blockIdx.x - nbead);
+}
+
 int prior_forces(const fcg_prior *pr, const float *pos, int R, int N, float *e_prior,
                  float *f_prior, cudaStream_t s) {
   FCG_PROF(P_PRIOR, s);
-  launch_pdl(PDL_SMALL, k_prior, ceil_div((long long)R * N, 256), 256, 0, s, *pr, pos, N, R * N,
-             f_prior);
-  launch_pdl(PDL_SMALL, k_prior_energy, R, 256, 0, s, *pr, pos, N, e_prior);
+  const int nbead = (int)ceil_div((long long)R * N, 256);
+  launch_pdl(PDL_SMALL, k_prior, nbead + R, 256, 0, s, *pr, pos, N, R * N, nbead, f_prior,
+             e_prior);
   return cuda_status("prior_forces");
 }
 
