@@ -525,14 +525,12 @@ k_edge_bwd(const EdgeArgs a, const float *__restrict__ P, const float *__restric
 // (md.py:183-185).  FF_LPN lanes per node; single writer per output.
 constexpr int FF_LPN = 8;  // lanes per node in k_forces_finish
 
-__global__ void __launch_bounds__(256)
-k_forces_finish(const int32_t *ptr, const int32_t *rev,
-                const float4 *gsum, int N, int RN, int64_t cap_e,
-                const float *f_extra, float *forces,
-                fcg_md_params kick, int do_kick, const float *mass,
-                float *vel, int64_t *status, const int64_t *step) {
-  pdl_trigger();
-  pdl_wait();
+__device__ __forceinline__ void forces_node(const int32_t *ptr, const int32_t *rev,
+                                            const float4 *gsum, int N, int RN, int64_t cap_e,
+                                            const float *f_extra, float *forces,
+                                            const fcg_md_params &kick, int do_kick,
+                                            const float *mass, float *vel, int64_t *status,
+                                            const int64_t *step) {
   // FF_LPN lanes per node: each lane gathers up to four of the node's CSR
   // slots per pass with all loads issued before use, then a fixed-order
   // butterfly over the node's lanes (deterministic; replaces a serial
@@ -588,12 +586,9 @@ k_forces_finish(const int32_t *ptr, const int32_t *rev,
 }
 
 // energy[r] = sum_i per_atom[r*N + i] (flash.py:489), fixed tree order.
-__global__ void __launch_bounds__(256)
-k_replica_energy(const float *per_atom, int N, float *energy) {
-  pdl_trigger();
-  pdl_wait();
+__device__ __forceinline__ void replica_energy(const float *per_atom, int N, float *energy,
+                                               int r) {
   __shared__ float red[256];
-  const int r = blockIdx.x;
   float acc = 0.f;
   for (int i = threadIdx.x; i < N; i += blockDim.x) acc += per_atom[(size_t)r * N + i];
   red[threadIdx.x] = acc;
@@ -603,6 +598,22 @@ k_replica_energy(const float *per_atom, int N, float *energy) {
     __syncthreads();
   }
   if (threadIdx.x == 0) energy[r] = red[0];
+}
+
+// Forces and replica energies in one launch (independent outputs): blocks
+// [0, nff) run forces_node, the last R blocks replica_energy.
+__global__ void __launch_bounds__(256)
+k_forces_finish(const int32_t *ptr, const int32_t *rev, const float4 *gsum, int N, int RN,
+                int64_t cap_e, const float *f_extra, float *forces, fcg_md_params kick,
+                int do_kick, const float *mass, float *vel, int64_t *status, const int64_t *step,
+                int nff, const float *per_atom, float *energy) {
+  pdl_trigger();
+  pdl_wait();
+  if ((int)blockIdx.x < nff)
+    forces_node(ptr, rev, gsum, N, RN, cap_e, f_extra, forces, kick, do_kick, mass, vel, status,
+                step);
+  else
+    replica_energy(per_atom, N, energy, blockIdx.x - nff);
 }
 
 // ---------------------------------------------------------------------------
@@ -797,10 +808,10 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
   fcg_md_params kp{};
   if (kick) kp = *kick;
   FCG_PROF(P_FORCES, s);
-  launch_pdl(PDL_SMALL, k_forces_finish, ceil_div((long long)RN * FF_LPN, 256), 256, 0, s, ptr, rev,
-             b.gsum, N, RN, cap_e, f_extra, forces, kp, (int)(kick != nullptr), mass, vel, status,
-             step);
-  launch_pdl(PDL_SMALL, k_replica_energy, R, 256, 0, s, per_atom, N, energy);
+  const int nff = (int)ceil_div((long long)RN * FF_LPN, 256);
+  launch_pdl(PDL_SMALL, k_forces_finish, nff + R, 256, 0, s, ptr, rev, b.gsum, N, RN, cap_e,
+             f_extra, forces, kp, (int)(kick != nullptr), mass, vel, status, step, nff, per_atom,
+             energy);
   return cuda_status("energy_forces");
 }
 
