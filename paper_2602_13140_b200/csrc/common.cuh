@@ -222,8 +222,18 @@ void launch_readout_tc(const float *X, const fcg_model &m, float *per_atom, floa
 void edge_tc_configure();
 int edge_tc_units(int grid);      // work units of the backward edge kernel
 int edge_tc_units_fwd(int grid);  // work units of the forward edge kernel
+// Optional embedding lookup riding on k_edge_geom's launch (X == nullptr: none).
+struct EmbedJob {
+  const float *emb;
+  const int32_t *types;
+  int N;
+  float *X;
+  unsigned int *amax;
+  int namax;
+};
 void launch_edge_geom(const EdgeArgs &a, float4 *geo, float2 *env, int32_t *unit_rows,
-                      int nunits, int32_t *unit_rows_fwd, int nunits_fwd, cudaStream_t s);
+                      int nunits, int32_t *unit_rows_fwd, int nunits_fwd, const EmbedJob &ej,
+                      cudaStream_t s);
 void launch_edge_fwd_tc(const EdgeArgs &a, const float4 *geo, const float2 *env,
                         const int32_t *unit_rows, const float *P, float *H, int grid,
                         cudaStream_t s);

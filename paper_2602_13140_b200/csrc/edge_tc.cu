@@ -162,7 +162,7 @@ struct SegSum {
 __global__ void __launch_bounds__(256)
 k_edge_geom(const float *pos, const int32_t *ptr, const int32_t *nbr, const int32_t *own,
             int nrows, int64_t cap_e, float cutoff, float4 *geo, float2 *env,
-            int32_t *unit_rows, int nunits, int32_t *unit_rows2, int nunits2) {
+            int32_t *unit_rows, int nunits, int32_t *unit_rows2, int nunits2, const EmbedJob ej) {
   pdl_trigger();
   pdl_wait();
   __syncthreads();  // keeps ptxas from hoisting loads above the wait
@@ -200,6 +200,16 @@ k_edge_geom(const float *pos, const int32_t *ptr, const int32_t *nbr, const int3
     }
     geo[k] = make_float4(ux, uy, uz, d);
     env[k] = make_float2(c, dc);
+  }
+  if (ej.X) {  // X = embedding[types] (flash.py:201) and the operand-bound words reset
+    if (blockIdx.x == 0 && (int)threadIdx.x < ej.namax) ej.amax[threadIdx.x] = 0u;
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+         q < (long long)nrows * (D / 4); q += (long long)gridDim.x * blockDim.x) {
+      const long long g = q / (D / 4);
+      const int c4 = (int)(q % (D / 4));
+      const int t = ld_dep(&ej.types[g % ej.N]);
+      *(float4 *)&ej.X[g * D + c4 * 4] = ld_dep((const float4 *)&ej.emb[(size_t)t * D + c4 * 4]);
+    }
   }
 }
 
@@ -1265,9 +1275,10 @@ int edge_tc_units(int grid) { return NGRP * grid; }
 int edge_tc_units_fwd(int grid) { return FWD_NGRP * grid; }
 
 void launch_edge_geom(const EdgeArgs &a, float4 *geo, float2 *env, int32_t *unit_rows,
-                      int nunits, int32_t *unit_rows_fwd, int nunits_fwd, cudaStream_t s) {
+                      int nunits, int32_t *unit_rows_fwd, int nunits_fwd, const EmbedJob &ej,
+                      cudaStream_t s) {
   launch_pdl(PDL_GEOM, k_edge_geom, 1184, 256, 0, s, a.pos, a.ptr, a.nbr, a.own, a.nrows, a.cap_e,
-             a.cutoff, geo, env, unit_rows, nunits, unit_rows_fwd, nunits_fwd);
+             a.cutoff, geo, env, unit_rows, nunits, unit_rows_fwd, nunits_fwd, ej);
 }
 
 void launch_edge_fwd_tc(const EdgeArgs &a, const float4 *geo, const float2 *env,

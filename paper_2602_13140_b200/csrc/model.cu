@@ -719,11 +719,6 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
 
   const int node_grid = ceil_div(RN, TE);
   const size_t sm1 = TE * LDH * sizeof(float), sm2 = 2 * sm1;
-  {
-    FCG_PROF(P_EMBED, s);
-    launch_pdl(PDL_SMALL, k_embed, ceil_div((long long)RN * (D / 4), 256), 256, 0, s, m->embedding,
-               types, N, RN, b.X, b.amax, 2 * FCG_MAX_BLOCKS);
-  }
 
   EdgeArgs ea;
   ea.pos = pos; ea.ptr = ptr; ea.nbr = nbr; ea.own = own; ea.nrows = RN; ea.cap_e = cap_e;
@@ -733,12 +728,18 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
   ea.dbg = g_dbg_phase;
   const bool simt = use_simt_edges();
   const int eg = simt ? 2 * sm_count() : sm_count();
+  const EmbedJob ej{m->embedding, types, N, b.X, b.amax, 2 * FCG_MAX_BLOCKS};
+  if (simt) {  // the tcgen05 path does the lookup inside k_edge_geom
+    FCG_PROF(P_EMBED, s);
+    launch_pdl(PDL_SMALL, k_embed, ceil_div((long long)RN * (D / 4), 256), 256, 0, s, m->embedding,
+               types, N, RN, b.X, b.amax, 2 * FCG_MAX_BLOCKS);
+  }
   if (!simt) {
     edge_tc_configure();
     node_tc_configure();
     FCG_PROF(P_EDGE_GEOM, s);
     launch_edge_geom(ea, b.geo, b.env, b.unit_rows, edge_tc_units(eg), b.unit_rows + 2048,
-                     edge_tc_units_fwd(eg), s);
+                     edge_tc_units_fwd(eg), ej, s);
   }
 
   for (int t = 0; t < T; ++t) {
