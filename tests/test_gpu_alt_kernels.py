@@ -1,0 +1,33 @@
+"""The selectable alternative edge kernels keep parity.
+
+The library reads its kernel switches once per process, so each setting runs
+the fp32 / W16 energy-force parity tests and the batched-engine test of
+test_gpu_parity.py in a subprocess:
+
+  * FCG_FWD64=0: the 4-group, 32-edge forward (k_edge_fwd_tc);
+  * FCG_BWD64=0: the 4-group, 32-edge backward (k_edge_bwd_tc);
+  * FCG_EDGE_IMPL=simt: the SIMT edge kernels (with the separate k_embed).
+"""
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+@pytest.mark.parametrize("setting", ["FCG_FWD64=0", "FCG_BWD64=0", "FCG_EDGE_IMPL=simt"])
+def test_alternative_edge_kernels_match_oracle(setting):
+    key, val = setting.split("=")
+    env = dict(os.environ, **{key: val})
+    sel = "energy_forces_fp32 or energy_forces_w16 or batched_engine_matches_oracle"
+    r = subprocess.run([sys.executable, "-m", "pytest", "tests/test_gpu_parity.py", "-m", "gpu",
+                        "-q", "-x", "-p", "no:cacheprovider", "-k", sel],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout and "deselected" in r.stdout
