@@ -6,7 +6,9 @@ test_gpu_parity.py in a subprocess:
 
   * FCG_FWD64=0: the 4-group, 32-edge forward (k_edge_fwd_tc);
   * FCG_BWD64=0: the 4-group, 32-edge backward (k_edge_bwd_tc);
-  * FCG_EDGE_IMPL=simt: the SIMT edge kernels (with the separate k_embed).
+  * FCG_EDGE_IMPL=simt: the SIMT edge kernels (with the separate k_embed);
+  * FCG_NBR_FUSED=0 / FCG_NBR_WINDOW=0: the general neighbour builds, run
+    through the CSR and large-system tests instead.
 """
 
 import os
@@ -21,13 +23,21 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parents[1]
 
 
-@pytest.mark.parametrize("setting", ["FCG_FWD64=0", "FCG_BWD64=0", "FCG_EDGE_IMPL=simt"])
-def test_alternative_edge_kernels_match_oracle(setting):
+def _run(setting, sel):
     key, val = setting.split("=")
     env = dict(os.environ, **{key: val})
-    sel = "energy_forces_fp32 or energy_forces_w16 or batched_engine_matches_oracle"
     r = subprocess.run([sys.executable, "-m", "pytest", "tests/test_gpu_parity.py", "-m", "gpu",
                         "-q", "-x", "-p", "no:cacheprovider", "-k", sel],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert " passed" in r.stdout and "deselected" in r.stdout
+
+
+@pytest.mark.parametrize("setting", ["FCG_FWD64=0", "FCG_BWD64=0", "FCG_EDGE_IMPL=simt"])
+def test_alternative_edge_kernels_match_oracle(setting):
+    _run(setting, "energy_forces_fp32 or energy_forces_w16 or batched_engine_matches_oracle")
+
+
+@pytest.mark.parametrize("setting", ["FCG_NBR_FUSED=0", "FCG_NBR_WINDOW=0"])
+def test_alternative_neighbour_builds_match_oracle(setting):
+    _run(setting, "csr or large_system_sweep or neighbor")
