@@ -39,8 +39,15 @@ def _deps():
         + [ROOT / "include" / "fcg.h", Path(__file__)]
 
 
+def _extra_flags() -> list:
+    return os.environ.get("FCG_NVCC_EXTRA", "").split()  # diagnostic A/B builds
+
+
 def up_to_date() -> bool:
     if not LIB.exists():
+        return False
+    stamp = BUILD / "flags.txt"  # a build with other flags is stale, whatever the mtimes say
+    if (stamp.read_text() if stamp.exists() else "") != " ".join(_extra_flags()):
         return False
     t = LIB.stat().st_mtime
     return all(p.stat().st_mtime <= t for p in _deps())
@@ -55,7 +62,7 @@ def build_library(force: bool = False, verbose: bool = False) -> Path:
 
     def compile_one(src: Path):
         obj = BUILD / (src.stem + ".o")
-        extra = os.environ.get("FCG_NVCC_EXTRA", "").split()  # diagnostic A/B builds
+        extra = _extra_flags()
         cmd = [nvcc, *ARCH, *NVCC_FLAGS, *extra, "-c", str(src), "-o", str(obj)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         logs[src.name] = res.stdout + res.stderr
@@ -71,6 +78,7 @@ def build_library(force: bool = False, verbose: bool = False) -> Path:
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stderr}")
     os.replace(tmp, LIB)
+    (BUILD / "flags.txt").write_text(" ".join(_extra_flags()))
     (BUILD / "ptxas.log").write_text("\n".join(f"== {k}\n{v}" for k, v in sorted(logs.items())))
     if verbose:
         print((BUILD / "ptxas.log").read_text())
