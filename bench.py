@@ -9,7 +9,11 @@ rebuilt every step.  A "step" is one full MD step of all replicas (noise,
 BAOA, neighbour/CSR rebuild, prior, energy + force backward, half-kick).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config fp32|w16]
-    python bench.py --impl reference ...   # the reference's CPU algorithm
+    python bench.py --impl reference ...   # the reference's CPU implementation
+
+--gpus N > 1 without torchrun around it relaunches itself under
+torch.distributed.run with N ranks (one per GPU); under torchrun,
+WORLD_SIZE must equal --gpus.
 
 Timing: W untimed warm-up steps, then K steps, each a replay of a captured
 one-step CUDA graph bracketed by CUDA events on the replay stream, with a
@@ -17,10 +21,11 @@ one-step CUDA graph bracketed by CUDA events on the replay stream, with a
 synchronize around the timed region; max over ranks.  `e2e` repeats the
 step through the engine's public API with host buffers (H2D of
 positions+velocities from pinned memory, MDEngine.run(1) = one graph replay
-of fcg_md_step, D2H of the new state and per-replica energies) timed by the
-host clock.  Multi-GPU: one process per GPU
-(torchrun), replicas sharded with no per-step collective; an NCCL
-all_gather of per-replica energies happens after the timed region.
+of fcg_md_step, D2H of the new state, per-replica energies and status
+words) timed by the host clock.  Multi-GPU: one process per GPU, replicas
+sharded with no per-step collective; after the timed region one NCCL
+all_gather of the final positions, velocities and per-replica potential,
+prior and kinetic T.
 """
 
 from __future__ import annotations
@@ -111,79 +116,137 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
-class CpuReference:
-    """The reference algorithm on this host's cores (oracle port: numpy +
-    BLAS, same ops as flashcg): replicas spread over a thread pool with one
-    BLAS thread each — the reference's CPU-64 mode."""
+def config_tag(args) -> str:
+    """Key of this workload in profiles/ncu_summary.json."""
+    return f"{args.system}{args.beads}_rc{args.cutoff:g}_{args.config}_R{args.replicas}"
 
-    def __init__(self, sysm, params, replicas: int):
+
+def load_flashcg():
+    """The unmodified reference package installed into baseline/_ref
+    (pip --target), or None when it is not there."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "flashcg" / "md.py").exists():
+        return None
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    import importlib
+    mods = {m: importlib.import_module(f"flashcg.{m}") for m in ("md", "model", "quantize",
+                                                                 "systems")}
+    return mods
+
+
+def reference_run(args, replicas: int, budget_s: float, max_steps: int, workers: int,
+                  blas_threads: int):
+    """Time the reference's own run_simulation (md.py:276-349) through its
+    public API on this host: `replicas` replicas of the bench workload,
+    `workers` replica threads x `blas_threads` BLAS threads, one warm-up
+    step, then as many steps (<= max_steps) as fit in budget_s.  Returns
+    (ns/day from the reference's throughput_report, steps, seconds, kind)."""
+    from threadpoolctl import threadpool_limits
+
+    fc = load_flashcg()
+    with tempfile.TemporaryDirectory() as td, threadpool_limits(limits=blas_threads):
+        if fc is not None:
+            md, model = fc["md"], fc["model"]
+            sysm = fc["systems"].generate_system(args.system, args.beads, 0,
+                                                 bonded=(args.system != "globule"))
+            params = model.init_params(model.ModelConfig(cutoff=args.cutoff), 0)
+            if args.config == "w16":
+                params = fc["quantize"].quantize_model(params, seed=0)
+
+            def run(n):
+                cfg = md.SimConfig(dt_fs=DT_FS, temperature=300.0, friction=1.0, n_steps=n,
+                                   n_replicas=replicas, seed=0, neighbor_stride=1,
+                                   output_stride=max(n, 1), workers=workers)
+                res = md.run_simulation(params, sysm, cfg, td)
+                return md.throughput_report(res)["ns_per_day"], res.wall_seconds
+            kind = "reference"
+        else:  # the oracle port of the same numpy algorithm (oracle/flashcg_oracle.py)
+            sysm, params = workload(args.config, args.system, args.beads, args.cutoff)
+
+            def run(n):
+                ref = CpuReference(sysm, params, replicas, workers)
+                t0 = time.perf_counter()
+                for _ in range(n):
+                    ref.step()
+                dt = time.perf_counter() - t0
+                return ns_per_day(replicas * n, dt), dt
+            kind = "port"
+        _, warm_s = run(1)                       # warm-up (includes the initial evaluation)
+        per_step = warm_s / 2.0
+        steps = int(max(1, min(max_steps, budget_s // max(per_step, 1e-9))))
+        value, secs = run(steps)
+    return value, steps, secs, kind
+
+
+class CpuReference:
+    """Oracle port of the reference step (numpy + BLAS, same ops as flashcg),
+    used only when baseline/_ref holds no reference install."""
+
+    def __init__(self, sysm, params, replicas: int, workers: int):
         from oracle import flashcg_oracle as O
 
-        self.O, self.sysm, self.params, self.R = O, sysm, params, replicas
-        self.cores = os.cpu_count() or 1
+        self.O, self.sysm, self.params, self.R, self.workers = O, sysm, params, replicas, workers
         self.pos = np.repeat(sysm.positions[None], replicas, axis=0).astype(np.float32)
         self.vel = np.zeros_like(self.pos)
         self.step_idx = 0
-        self.F, *_ = O.replica_forces(params, sysm.types, sysm.prior, self.pos, self.cores)
+        self.F, *_ = O.replica_forces(params, sysm.types, sysm.prior, self.pos, workers)
 
     def step(self):
         O, s = self.O, self.sysm
         xi = np.stack([O.noise(0, r, self.step_idx, s.n_beads) for r in range(self.R)])
         self.pos, self.vel = O.baoa(self.pos, self.vel, self.F, s.masses, xi, DT_FS, 300.0, 1.0)
-        self.F, *_ = O.replica_forces(self.params, s.types, s.prior, self.pos, self.cores)
+        self.F, *_ = O.replica_forces(self.params, s.types, s.prior, self.pos, self.workers)
         self.vel = O.half_kick(self.vel, self.F, s.masses, DT_FS)
         self.step_idx += 1
 
 
-def cpu_baseline(sysm, params, replicas: int, max_seconds: float = 20.0, max_steps: int = 5):
-    from threadpoolctl import threadpool_limits
-
-    with threadpool_limits(limits=1):
-        ref = CpuReference(sysm, params, replicas)
-        t0 = time.perf_counter()
-        steps = 0
-        while steps < max_steps and (steps == 0 or time.perf_counter() - t0 < max_seconds):
-            ref.step()
-            steps += 1
-        dt = time.perf_counter() - t0
-    return {"value": ns_per_day(replicas * steps, dt), "unit": UNIT, "cores": ref.cores,
-            "kind": "port",
-            "sample": f"{replicas} replicas x {steps} full MD steps of coil-269 "
-                      f"({dt:.1f} s; oracle port of the reference, numpy {np.__version__}, "
-                      f"{ref.cores} worker threads x 1 BLAS thread)"}
+def cpu_baseline(args, budget_s: float = 20.0):
+    """cpu_baseline of our line: the reference CPU path on this host's cores,
+    a bounded sample of the same 64-replica workload (SURVEY §8(d) mode 2)."""
+    cores = os.cpu_count() or 1
+    value, steps, secs, kind = reference_run(args, args.replicas, budget_s, 5, cores, 1)
+    src = ("flashcg.md.run_simulation from baseline/_ref (unmodified reference)"
+           if kind == "reference" else "oracle port of the reference algorithm")
+    return {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"{args.replicas} replicas x {steps} full MD steps of {args.system}-"
+                      f"{args.beads} ({secs:.1f} s incl. the initial evaluation; {src}, numpy "
+                      f"{np.__version__}, {cores} replica threads x 1 BLAS thread)"}
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from threadpoolctl import threadpool_limits
-
-    sysm, params = workload(args.config, args.system, args.beads, args.cutoff)
     cores = os.cpu_count() or 1
-    R = min(args.replicas, max(8, cores))
-    with threadpool_limits(limits=1):
-        ref = CpuReference(sysm, params, R)
-        for _ in range(args.warmup):
-            ref.step()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            ref.step()
-        dt = time.perf_counter() - t0
-    value = ns_per_day(R * args.steps, dt)
+    R = args.replicas
+    # SURVEY §8(d) CPU mode 2: all replicas of the workload, one thread per
+    # core, 1 BLAS thread each; steps bounded by --ref-budget-s
+    value, steps, secs, kind = reference_run(args, R, args.ref_budget_s, args.steps, cores, 1)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+            "n_gpus": args.gpus, "steps": steps, "steps_requested": args.steps,
+            "warmup": 1, "ms_per_step": secs / steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "coil-269 (1ENH stand-in) x replicas, reference CPU "
-                                   "algorithm (oracle port)", "replicas_sampled": R,
+            "config": {"workload": f"{args.system}-{args.beads} (1ENH stand-in) x {R} replicas, "
+                                   f"r_cut={args.cutoff} nm, dt=4 fs, nbr rebuild every step",
+                       "replicas": R, "same_config": True,
                        "weights": "init_params(ModelConfig(), 0)" + (
-                           " + quantize_model" if args.config == "w16" else "")},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"{R} replicas per step on {cores} threads (the metric "
-                                       f"is per replica-step; 64-replica workload sampled)"},
+                           " + quantize_model" if args.config == "w16" else ""),
+                       "path": ("flashcg.md.run_simulation (baseline/_ref, unmodified), "
+                                "throughput_report" if kind == "reference"
+                                else "oracle port (baseline/_ref missing)")},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                             "sample": f"{R} replicas x {steps} steps ({secs:.1f} s, "
+                                       f"{cores} replica threads x 1 BLAS thread)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
+    if (args.system, args.beads, args.config) == ("coil", 269, "fp32") and not args.no_c1:
+        # BASELINE configs[0] / SURVEY §8(d) mode 1: one replica, all cores on BLAS
+        c1, c1_steps, c1_s, c1_kind = reference_run(args, 1, 30.0, 100, 1, cores)
+        line["c1"] = {"value": c1, "unit": UNIT, "replicas": 1, "steps": c1_steps,
+                      "seconds": c1_s, "kind": c1_kind, "blas_threads": cores,
+                      "workload": "BASELINE configs[0]: 1 replica of coil-269, up to 100 "
+                                  "Langevin steps fp32"}
     print(json.dumps(line), flush=True)
 
 
@@ -199,6 +262,56 @@ def graph_kernel_nodes(g):
         return sum(1 for nd in nodes if rt.cudaGraphNodeGetType(nd)[1] == kernel)
     except Exception:
         return None
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def relaunch(args) -> int:
+    """`python bench.py --gpus N` without a launcher: run N ranks under
+    torch.distributed.run (one process per GPU, rendezvous on 127.0.0.1)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={_free_port()}", str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def step_roofline(E_tot: int, R: int, N: int, params, ms_step: float, pk: dict, w16: bool):
+    """SURVEY §8(d) whole-step roofline: algorithmic bytes (io_model_flash,
+    summed over replicas, + integrator/neighbour bytes) against HBM, and
+    algorithmic FLOPs against the FP32 FFMA and bf16 tensor peaks; names the
+    bound whose time is larger for the pipes the kernels use."""
+    from paper_2602_13140_b200.schnet import PipelineMode, accumulated_traffic
+
+    cfg = params.config
+    D, Dr, Fh, Rh, T = (cfg.hidden_dim, cfg.rbf_dim, cfg.filter_hidden_dim,
+                        cfg.readout_hidden_dim, cfg.num_blocks)
+    width = 2 if w16 else 4
+    bytes_alg = accumulated_traffic(PipelineMode(), N, E_tot, R, params, width).total_bytes
+    bytes_alg += R * N * 3 * 4 * 6            # integrator: pos/vel read+write, forces, noise
+    flop_alg = (2 * T * E_tot * 2 * (Dr * Fh + Fh * D) + R * 12 * T * N * D * D
+                + R * 4 * N * (D * Rh + Rh))
+    t = ms_step / 1e3
+    ffma = 148 * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6
+    hbm = pk["hbm_gbs"] * 1e9
+    tensor = pk["bf16_tflops"] * 1e12
+    # the fp32 path issues 3 fp16 products per MAC (hi*hi + hi*lo + lo*hi)
+    issued = flop_alg * (1 if w16 else 3)
+    t_hbm, t_tensor = bytes_alg / hbm, issued / tensor
+    return {"bytes_alg": int(bytes_alg), "achieved_gbs": bytes_alg / t / 1e9,
+            "hbm_frac": bytes_alg / t / hbm,
+            "flop_alg": int(flop_alg), "achieved_tflops": flop_alg / t / 1e12,
+            "ffma_frac": flop_alg / t / ffma, "tensor_frac": flop_alg / t / tensor,
+            "tensor_issued_frac": issued / t / tensor,
+            "bound": "hbm" if t_hbm >= t_tensor else "tensor",
+            "bound_ms": max(t_hbm, t_tensor) * 1e3, "frac_of_bound": max(t_hbm, t_tensor) / t,
+            "note": ("bytes: io_model_flash at width %d B summed over replicas + 72 B/bead "
+                     "integrator; FLOPs: SURVEY §8(d) FLOP_alg; fp32 path issues 3 fp16 tensor "
+                     "products per MAC (hi/lo split)" % width)}
 
 
 def main():
@@ -218,7 +331,18 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gpu-baseline", action="store_true",
                     help="skip the same-GPU materialising (CGSchNet-style) comparison")
+    ap.add_argument("--no-c1", action="store_true", help="reference arm: skip the C1 run")
+    ap.add_argument("--ref-budget-s", type=float, default=120.0,
+                    help="reference arm: seconds of timed CPU steps (bounded sample)")
+    ap.add_argument("--dist-backend", choices=("nccl", "gloo"), default="nccl")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="all ranks on cuda:0 (tests of the launcher on a 1-GPU box; gloo)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU")
     if args.impl == "reference":
         return run_reference(args)
 
@@ -226,15 +350,15 @@ def main():
     import torch.distributed as dist
 
     from paper_2602_13140_b200 import _lib
-    from paper_2602_13140_b200.engine import MDEngine
+    from paper_2602_13140_b200.engine import KB, MDEngine
 
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    torch.cuda.set_device(0 if args.share_gpu else local)
+    dev = torch.device("cuda", torch.cuda.current_device())
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        dist.init_process_group(args.dist_backend,
+                                **({"device_id": dev} if args.dist_backend == "nccl" else {}))
 
     sysm, params = workload(args.config, args.system, args.beads, args.cutoff)
     R, N = args.replicas, sysm.n_beads
@@ -248,17 +372,28 @@ def main():
     stream = torch.cuda.Stream(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64,
+                         device=dev if args.dist_backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
+        for _ in range(max(args.warmup, 3)):
             g.replay()
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(args.steps)]
         torch.cuda.synchronize(dev)
-        if world > 1:
-            dist.barrier()
+        barrier()
         vis = os.environ.get("CUDA_VISIBLE_DEVICES")
-        sampler = ClockSampler(vis.split(",")[local] if vis else str(local))
-        t_wall = time.perf_counter()
+        gpu_index = dev.index
+        sampler = ClockSampler(vis.split(",")[gpu_index] if vis else str(gpu_index))
         for s0, s1 in evs:
             if not args.no_flush:
                 flush.zero_()
@@ -266,41 +401,36 @@ def main():
             g.replay()
             s1.record(stream)
         torch.cuda.synchronize(dev)
-        t_wall = time.perf_counter() - t_wall
         clocks = sampler.stop()
-        if world > 1:
-            dist.barrier()
+        barrier()
     ms = sum(a.elapsed_time(b) for a, b in evs)
     peak_mem = torch.cuda.max_memory_allocated(dev)
-    flags = eng.flags()
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = max_over_ranks(ms)
     value = ns_per_day(R * world * args.steps, ms_max / 1e3)
+    st_np = eng.status.cpu().numpy()
+    MDEngine.check_status(st_np)   # an overflow or blow-up would void the timing
 
     # ---- end-to-end through the host-buffer API --------------------------
     hstate = torch.empty((2, R, N, 3), dtype=torch.float32).pin_memory()  # positions, velocities
     hen = torch.empty((2, R), dtype=torch.float32).pin_memory()            # potential, prior
+    hst = torch.empty(_lib.FCG_STATUS_WORDS, dtype=torch.int64).pin_memory()
     hstate.copy_(eng.state)
     with torch.cuda.stream(stream):
         torch.cuda.synchronize(dev)
-        if world > 1:
-            dist.barrier()
+        barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             eng.state.copy_(hstate, non_blocking=True)
-            eng.run(1, graph_steps=1)  # the public stepping call (graph replay)
+            eng.run(1, graph_steps=1, check=False)  # the public stepping call (graph replay)
             hstate.copy_(eng.state, non_blocking=True)
             hen.copy_(eng.energies, non_blocking=True)
+            hst.copy_(eng.status, non_blocking=True)
             stream.synchronize()
+            MDEngine.check_status(hst.numpy())
         e2e_s = time.perf_counter() - t0
-    t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e2e_value = ns_per_day(R * world * args.e2e_steps, float(t.item()))
+    e2e_value = ns_per_day(R * world * args.e2e_steps, max_over_ranks(e2e_s))
     h2d = 2 * R * N * 3 * 4
-    d2h = 2 * R * N * 3 * 4 + 2 * R * 4
+    d2h = 2 * R * N * 3 * 4 + 2 * R * 4 + _lib.FCG_STATUS_WORDS * 8
 
     # ---- per-kernel device times (built-in profiler, eager steps) ---------
     lib = _lib.load()
@@ -310,8 +440,8 @@ def main():
             eng._md_step()
     prof = _lib.profile_read()
     lib.fcg_profile_enable(0)
-    E_tot = eng.flags()["edges"]
     flags = eng.flags()
+    E_tot = flags["edges"]
     per_step_launch = graph_kernel_nodes(g)
     if per_step_launch is None:  # estimate from the profiler's launch brackets
         per_step_launch = sum(c for _, c in prof.values()) / args.profile_steps
@@ -320,12 +450,13 @@ def main():
     avg_ms = dom_ms / dom_n
     pk, pk_kind = peaks()
     if dom_name in ("edge_fwd", "edge_bwd"):
-        alg = flags["edges"] * flops_per_edge_block()
+        alg = E_tot * flops_per_edge_block()
         achieved = alg / (avg_ms / 1e3) / 1e12
         roof = {"kernel": dom_name, "bound": "tensor", "achieved": achieved,
-                "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
-                "frac": achieved / pk["bf16_tflops_sustained"],
-                "peak_kind": f"{pk_kind} bf16 sustained (MEASURED_PEAKS.json)",
+                "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                "frac": achieved / pk["bf16_tflops"],
+                "peak_kind": f"{pk_kind} bf16 dense burst (MEASURED_PEAKS.json bf16_tflops; the "
+                             "kernel's launch time is measured on its own)",
                 "alg_per_launch": f"{alg:.4g} FLOP = E_total {E_tot} x 49,152 "
                                   "(filter-MLP GEMMs of one pass, SURVEY §8(d))",
                 "avg_launch_ms": avg_ms,
@@ -337,22 +468,42 @@ def main():
                 "unit": "GB/s", "frac": None, "avg_launch_ms": avg_ms}
     ncu = ROOT / "profiles" / "ncu_summary.json"
     roof["traffic"] = None
+    tag = config_tag(args)
     if ncu.exists():
         try:
-            roof["traffic"] = json.loads(ncu.read_text()).get(dom_name, {}).get("dram_bytes")
+            ent = json.loads(ncu.read_text()).get(tag, {}).get(dom_name)
+            if ent:
+                roof["traffic"] = ent["dram_bytes"]
+                roof["traffic_source"] = f"profiles/ncu_summary.json[{tag}] (ncu {ent['tag']})"
         except Exception:
             pass
     share = {k: round(v[0] / sum(x[0] for x in prof.values()), 4) for k, v in prof.items()}
+    step_roof = step_roofline(E_tot, R, N, params, ms_max / args.steps, pk, args.config == "w16")
 
-    # ---- end-of-run gather of per-replica observables (NCCL) -------------
-    energies = eng.potential.clone()
+    # ---- end-of-run gather of final states and per-replica observables ---
+    gdev = dev if args.dist_backend == "nccl" else torch.device("cpu")
+    m = eng.mass.double()[None, :, None]
+    kin = (2.0 * (0.5 * (m * eng.vel.double() ** 2).sum(dim=(1, 2))) / (3 * N * KB))
+    obs = torch.stack([eng.potential.double(), eng.prior_e.double(), kin], dim=1).to(gdev)
+    st = eng.state.transpose(0, 1).contiguous().to(gdev)     # [R, 2, N, 3]
+    torch.cuda.synchronize(dev)
+    barrier()
+    t0 = time.perf_counter()
     if world > 1:
         from paper_2602_13140_b200.sharding import gather_replicas
-        energies = gather_replicas(energies, R * world)
+        obs = gather_replicas(obs, R * world)
+        st = gather_replicas(st, R * world)
+    torch.cuda.synchronize(dev)
+    gather_ms = (time.perf_counter() - t0) * 1e3
+    gather = {"replicas": int(obs.shape[0]), "what": "final positions+velocities [R,2,N,3] f32 "
+              "and per-replica potential, prior, kinetic_T [R,3] f64 (SURVEY §8(e))",
+              "bytes": int(st.numel() * 4 + obs.numel() * 8), "ms": gather_ms,
+              "backend": args.dist_backend if world > 1 else None}
 
     if rank == 0:
         sysline = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-                   "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+                   "steps": args.steps, "warmup": max(args.warmup, 3),
+                   "ms_per_step": ms_max / args.steps,
                    "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                    "dtype": "f32" if args.config == "fp32" else "f16-weights/f32-accum",
                    "data": "synthetic (generate_system coil-269 seed 0; random-init weights)",
@@ -361,24 +512,26 @@ def main():
                                            "every step") if (args.system, args.beads) == ("coil", 269)
                               else (f"{args.system}-{args.beads} (BASELINE configs[4] sweep), "
                                     f"{R} replicas/GPU, r_cut={args.cutoff} nm, dt=4 fs"),
-                              "replicas_per_gpu": R, "total_replicas": R * world,
+                              "tag": tag, "replicas_per_gpu": R, "total_replicas": R * world,
                               "weights": args.config, "parallelism": f"replica-shard x{world}",
                               "l2": "flushed (256 MiB write) before every timed step"
                                     if not args.no_flush else "not flushed",
-                              "mean_edges_per_replica": E_tot / R},
+                              "mean_edges_per_replica": E_tot / R,
+                              **({"shared_gpu": True} if args.share_gpu else {})},
                    "gpu_launches": int(round(per_step_launch * args.steps)),
                    "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                            "d2h_bytes_per_step": d2h, "steps": args.e2e_steps},
-                   "roofline": roof, "clocks": clocks,
+                   "roofline": roof, "step_roofline": step_roof, "clocks": clocks,
                    "kernel_share": share,
                    "peak_mem_bytes": int(peak_mem),
                    "flags": {k: flags[k] for k in ("overflow", "blowup", "max_degree")},
-                   "energy_mean": float(energies.double().mean().item())}
+                   "end_of_run_gather": gather,
+                   "energy_mean": float(obs[:, 0].mean().item())}
         if world == 1 and not args.no_gpu_baseline:
             from paper_2602_13140_b200.ablation import compare_on_engine
             sysline["gpu_materialized_baseline"] = compare_on_engine(eng, params)
         if world == 1 and not args.no_cpu_baseline:
-            sysline["cpu_baseline"] = cpu_baseline(sysm, params, R)
+            sysline["cpu_baseline"] = cpu_baseline(args)
         print(json.dumps(sysline), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -41,10 +41,11 @@ from .csr import (
     group_by_source,
 )
 from .prior import PriorSpec
+from ._lib import CapacityError
 from .inputs import SystemSpec, generate_system
 
 __all__ = [
-    "BlockParams", "ConfigError", "CsrLayout", "EnergyForces", "GpuReplicaForces", "KB",
+    "BlockParams", "CapacityError", "ConfigError", "CsrLayout", "EnergyForces", "GpuReplicaForces", "KB",
     "ModelConfig", "ModelParams", "NeighborList", "PipelineMode", "PriorSpec", "RbfSpec",
     "RunResult", "SimConfig", "SimState", "SimulationBlowupError", "SystemSpec",
     "TrafficReport", "traffic_report", "build_neighbors_bruteforce", "build_neighbors_cells",

@@ -22,6 +22,7 @@ import numpy as np
 
 from . import _lib
 from .engine import _torch
+from .schnet import TrafficReport, traffic_report
 
 LN2 = math.log(2.0)
 
@@ -235,6 +236,8 @@ class MaterializedReplicaForces:
         self.prior = DevicePrior(prior, self.N)
         self.model = TorchModel(params, torch.float32)
         self.edge_counts = []
+        self.mode = config.backend
+        self.traffic = TrafficReport()
         self._csr = None
 
     def __call__(self, positions, step):
@@ -248,6 +251,10 @@ class MaterializedReplicaForces:
             counts = p[N::N] - p[0:-1:N][:R]
             self._counts = [int(x) for x in counts]
         self.edge_counts.extend(self._counts)
+        cfg = self.params.config
+        for e in self._counts:   # md.py:267-268: every evaluation's modelled traffic
+            self.traffic.merge(traffic_report(self.mode, N, e, cfg.hidden_dim, cfg.rbf_dim,
+                                              len(self.params.blocks), 4))
         ptr, nbr, own = self._csr
         dpos = torch.as_tensor(pos).cuda()
         e, _pa, f = materialized_energy_forces(self.model, dpos.reshape(R * N, 3), self.types,

@@ -48,12 +48,40 @@ def _stream(torch):
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+_CSR_BUFFERS: dict = {}
+CAP_LIMIT = 2 ** 31 - 2   # int32 slot indices (include/fcg.h)
+
+
+def _csr_buffers(torch, n_nodes: int, cap: int):
+    """Reusable device CSR buffers per device, grown on demand (never sized
+    for the dense R*N*(N-1) worst case)."""
+    if cap > CAP_LIMIT:
+        raise ValueError(f"neighbour list needs {cap} edge slots; the int32 CSR holds at most "
+                         f"{CAP_LIMIT}")
+    dev = torch.cuda.current_device()
+    b = _CSR_BUFFERS.get(dev)
+    if b is None or b["ptr"].numel() < n_nodes + 1 or b["cap"] < cap:
+        old_cap = b["cap"] if b is not None else 0
+        cap = max(cap, old_cap)
+        n_alloc = max(n_nodes + 1, b["ptr"].numel() if b is not None else 0)
+        i32 = dict(dtype=torch.int32, device="cuda")
+        b = _CSR_BUFFERS[dev] = {
+            "cap": cap, "ptr": torch.empty(n_alloc, **i32), "nbr": torch.empty(cap + 1, **i32),
+            "rev": torch.empty(cap + 1, **i32), "own": torch.empty(cap + 1, **i32)}
+    return b
+
+
 def device_csr(positions: np.ndarray, r_cut: float, replicas: bool = False):
     """Run fcg_nbr_build on one system ([N,3]) or a replica batch ([R,N,3]).
 
     Returns (ptr, nbr, rev, own) as int64 numpy arrays over the flattened
-    block-diagonal graph.
+    block-diagonal graph.  The edge capacity starts at the engine's
+    default (O(R*N), like the reference's O(E) cell list) and grows to the
+    built edge count when the build reports an overflow; buffers are reused
+    across calls.
     """
+    from .engine import default_capacity
+
     torch = _torch()
     lib = _lib.load()
     pos = np.asarray(positions)
@@ -66,20 +94,23 @@ def device_csr(positions: np.ndarray, r_cut: float, replicas: bool = False):
     dt = torch.float64 if f64 else torch.float32
     dpos = torch.as_tensor(np.ascontiguousarray(pos, dtype=np.float64 if f64 else np.float32)
                            ).to("cuda", dt)
-    cap = R * N * max(N - 1, 1)
-    ptr = torch.zeros(R * N + 1, dtype=torch.int32, device="cuda")
-    nbr = torch.zeros(cap + 1, dtype=torch.int32, device="cuda")
-    rev = torch.zeros_like(nbr)
-    own = torch.zeros_like(nbr)
     status = torch.zeros(_lib.FCG_STATUS_WORDS, dtype=torch.int64, device="cuda")
     nb = lib.fcg_nbr_workspace_bytes(R, N)
     ws = torch.empty(int(nb), dtype=torch.uint8, device="cuda")
     fn = lib.fcg_nbr_build_f64 if f64 else lib.fcg_nbr_build
     v = _lib.vp
-    _lib.check(fn(v(dpos), R, N, float(r_cut), cap, v(ptr), v(nbr), v(rev), v(own), v(status),
-                  v(ws), nb, _stream(torch)), "fcg_nbr_build")
-    p = ptr.cpu().numpy().astype(np.int64)
-    E = int(p[-1])
+    cap = default_capacity(R, N)
+    while True:
+        b = _csr_buffers(torch, R * N, cap)
+        ptr, nbr, rev, own = b["ptr"][:R * N + 1], b["nbr"], b["rev"], b["own"]
+        _lib.check(fn(v(dpos), R, N, float(r_cut), b["cap"], v(ptr), v(nbr), v(rev), v(own),
+                      v(status), v(ws), nb, _stream(torch)), "fcg_nbr_build")
+        p = ptr.cpu().numpy().astype(np.int64)
+        E = int(p[-1])
+        if E <= b["cap"]:
+            break
+        status.zero_()
+        cap = E   # the count pass is exact: one rebuild at this capacity fits
     return (p, nbr[:E].cpu().numpy().astype(np.int64), rev[:E].cpu().numpy().astype(np.int64),
             own[:E].cpu().numpy().astype(np.int64))
 

@@ -121,7 +121,9 @@ class MDEngine:
                 getattr(self.csr, k)[:src.numel()].copy_(src)
         nbytes = self.lib.fcg_md_workspace_bytes(C.byref(self.model.desc), self.R, self.N,
                                                  self.csr.cap_e)
-        self.ws = torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
+        # zero-filled: the noise ring's validity tag lives in this workspace,
+        # and a recycled allocation must never carry a stale tag that matches
+        self.ws = torch.zeros(int(nbytes), dtype=torch.uint8, device=self.device)
         self._graphs = {}
 
     @property
@@ -193,20 +195,43 @@ class MDEngine:
         self.forces.add_(f_prior)  # out.forces + f_prior, md.py:266
         self.per_atom = per_atom
 
-    def run(self, n_steps: int, graph_steps: int = 0):
+    def run(self, n_steps: int, graph_steps: int = 0, check: bool = True):
         """Advance n_steps.  With graph_steps > 0, steps run as replays of a
-        captured CUDA graph of graph_steps fcg_md_step calls."""
+        captured CUDA graph of graph_steps fcg_md_step calls.
+
+        With check=True (the default) the status words are read once at the
+        end (one small device->host copy) and a capacity overflow raises
+        CapacityError, a blow-up SimulationBlowupError — the step that
+        overflowed ran with prior-only forces, so its results are invalid.
+        run_simulation repairs both (regrow + replay, blow-up frame); callers
+        that batch their own host reads pass check=False and call
+        check_status() on the words they copied."""
         if graph_steps <= 0:
             for _ in range(n_steps):
                 self._md_step()
-            return
-        full, rem = divmod(n_steps, graph_steps)
-        if full:
-            g = self._graph(graph_steps)
-            for _ in range(full):
-                g.replay()
-        for _ in range(rem):
-            self._md_step()
+        else:
+            full, rem = divmod(n_steps, graph_steps)
+            if full:
+                g = self._graph(graph_steps)
+                for _ in range(full):
+                    g.replay()
+            for _ in range(rem):
+                self._md_step()
+        if check:
+            self.check_status(self.status.cpu().numpy())
+
+    @staticmethod
+    def check_status(st) -> None:
+        """Raise on the sticky status words of a step batch (include/fcg.h)."""
+        if st[_lib.ST_OVERFLOW]:
+            raise _lib.CapacityError(
+                f"neighbour list overflowed the CSR capacity ({int(st[_lib.ST_EDGES])} edges); "
+                "forces of the overflowing steps are invalid — regrow (MDEngine._alloc) and "
+                "replay, as run_simulation does")
+        if st[_lib.ST_BLOWUP]:
+            from .langevin import SimulationBlowupError
+            raise SimulationBlowupError(
+                f"non-finite or runaway forces at step {int(st[_lib.ST_BLOWUP_STEP])}")
 
     def _graph(self, k: int):
         g = self._graphs.get(k)

@@ -6,12 +6,14 @@ Drop-in points (reference md.py):
   * GpuReplicaForces   replaces _ReplicaForces (md.py:231-273): a callable
                        force_fn(positions[R,N,3], step) -> (forces, info)
                        usable by the reference's own integrate();
-  * integrate          md.py:188-208, device-resident when force_fn is a
-                       GpuReplicaForces, else GPU integrator + host forces;
+  * integrate          md.py:188-208: GPU integrator kernels, forces through
+                       the host-array force_fn protocol every step;
   * run_simulation     md.py:276-349, device-resident with host I/O only at
                        output strides; same trajectory.xyz / scalars.csv
                        formats, written by a background thread from pinned
-                       snapshots (frames formatted in C, fcg_format_xyz).
+                       snapshots (frames formatted in C, fcg_format_xyz);
+                       distributed=True shards the replicas over the ranks
+                       of torch.distributed (one GPU each).
 """
 
 from __future__ import annotations
@@ -28,8 +30,9 @@ import numpy as np
 
 from . import _lib
 from .engine import KB, MDEngine, md_params
-from .schnet import PipelineMode, TrafficReport, io_model_flash_report
+from .schnet import PipelineMode, TrafficReport, accumulated_traffic, io_model_flash_report
 from .prior import PriorSpec, DevicePrior  # noqa: F401  (re-export, md.py:90)
+from .sharding import ReplicaShards
 
 FORCE_BLOWUP_LIMIT = 1.0e6
 SCALARS_SCHEMA = "step,replica,potential,prior,kinetic_T,wall_ms"
@@ -163,8 +166,10 @@ def integrate(force_fn, state: SimState, config: SimConfig, observer=None) -> Si
     """BAOAB loop with one force evaluation per step (md.py:188-208).
 
     The integrator runs on the GPU (numpy-exact noise, fp32 BAOA and
-    half-kick kernels).  With a GpuReplicaForces the forces stay on the
-    device; any other force_fn is called with host arrays each step.
+    half-kick kernels).  force_fn is called with host arrays each step, as
+    the reference protocol defines it, so positions and forces cross the
+    host boundary once per step (a GpuReplicaForces evaluates on the GPU);
+    run_simulation is the device-resident loop.
     """
     _require_fp32(config)
     from .engine import _torch
@@ -227,6 +232,12 @@ def _format_frame(types, positions, step, replica):
     return "\n".join(rows) + "\n"
 
 
+def _scalar_rows(step, pot, pri, kin, wall_ms, replica0=0) -> str:
+    """scalars.csv rows of one output step (md.py:322-326)."""
+    return "".join(f"{step},{replica0 + rep},{pot[rep]:.10g},{pri[rep]:.10g},{kin[rep]:.10g},"
+                   f"{wall_ms:.3f}\n" for rep in range(len(pot)))
+
+
 class _FrameWriter:
     """Output pipeline of run_simulation.
 
@@ -237,11 +248,18 @@ class _FrameWriter:
     `depth` pinned slots bounds the memory and applies back-pressure.
     """
 
-    def __init__(self, eng, types, masses, traj, scal, depth: int = 3):
+    def __init__(self, eng, types, masses, traj, scal, depth: int = 3, replica0: int = 0,
+                 collect: bool = False):
         torch = eng.torch
         R, N = eng.R, eng.N
         self.eng, self.types, self.masses = eng, np.asarray(types), masses
         self.traj, self.scal = traj, scal
+        self.replica0 = replica0
+        # collect=True (sharded runs): keep (step, wall_ms, positions,
+        # potential, prior, kinetic T) per output instead of writing; rank 0
+        # writes every shard's frames after the end-of-run gather
+        self.collect = collect
+        self.frames = []
         pin = dict(dtype=torch.float32, pin_memory=True)
         self.slots = [dict(pos=torch.empty(R, N, 3, **pin), vel=torch.empty(R, N, 3, **pin),
                            pot=torch.empty(R, **pin), pri=torch.empty(R, **pin),
@@ -281,10 +299,13 @@ class _FrameWriter:
                     kin = kinetic_temperature(st)
                     pot = s["pot"].numpy().astype(np.float64)
                     pri = s["pri"].numpy().astype(np.float64)
-                    self.traj.write(_lib.format_xyz(pos, self.types, step))
-                    self.scal.write("".join(
-                        f"{step},{rep},{pot[rep]:.10g},{pri[rep]:.10g},{kin[rep]:.10g},"
-                        f"{wall_ms:.3f}\n" for rep in range(pos.shape[0])))
+                    if self.collect:
+                        self.frames.append((step, wall_ms, pos.copy(),
+                                            np.stack([pot, pri, kin], axis=1)))
+                    else:
+                        self.traj.write(_lib.format_xyz(pos, self.types, step, self.replica0))
+                        self.scal.write(_scalar_rows(step, pot, pri, kin, wall_ms,
+                                                     self.replica0))
             except BaseException as exc:  # surfaced on the next snapshot/close
                 self.error = exc
             finally:
@@ -299,7 +320,8 @@ class _FrameWriter:
 
 
 def run_simulation(params, system, config: SimConfig, out_dir, resume_from=None,
-                   graph_steps: int = 32, rep_offset: int = 0) -> RunResult:
+                   graph_steps: int = 32, rep_offset: int = 0, distributed: bool = False,
+                   group=None) -> RunResult:
     """Device-resident run_simulation (md.py:276-349).
 
     Frames and scalars are written for the initial state and every
@@ -310,14 +332,30 @@ def run_simulation(params, system, config: SimConfig, out_dir, resume_from=None,
     chunk from its saved start state (results are unchanged: the noise is
     counter-based).  A blow-up dumps the frame of the offending step to
     blowup.xyz and raises SimulationBlowupError.
+
+    distributed=True: the n_replicas replicas are sharded over
+    the ranks of torch.distributed (`group`, default the world; each rank
+    drives its current CUDA device).  Rank g integrates the contiguous block
+    sharding.replica_shard gives it, with its first global replica index
+    keying the noise (md.py:127-131), so no per-step exchange exists.  The
+    ranks meet once per output chunk for one integer (the earliest blow-up
+    step) and once at the end, where one gather of the recorded frames,
+    per-replica scalars and final states lets rank 0 write the same
+    trajectory.xyz / scalars.csv an unsharded run writes (wall_ms is rank
+    0's clock).  Every rank returns the full RunResult.
     """
     from . import checkpoint as params_io
 
     _require_fp32(config)
     if not config.backend.fused:
+        if distributed:
+            raise ValueError("distributed runs use the fused backend")
         return _run_simulation_materialized(params, system, config, out_dir, resume_from)
     out_dir = Path(out_dir)
-    out_dir.mkdir(parents=True, exist_ok=True)
+    shard = ReplicaShards(config.n_replicas, group) if distributed else None
+    lead = shard is None or shard.rank == 0
+    if lead:
+        out_dir.mkdir(parents=True, exist_ok=True)
     masses = np.asarray(system.masses, np.float64)
     if resume_from is not None:
         chk = params_io.load_checkpoint(resume_from)
@@ -330,17 +368,26 @@ def run_simulation(params, system, config: SimConfig, out_dir, resume_from=None,
         pos0 = np.repeat(r0[None, :, :], config.n_replicas, axis=0).astype(np.float32)
         vel0 = np.zeros_like(pos0)
         step0 = 0
-    R, N = pos0.shape[0], pos0.shape[1]
+    R_total, N = pos0.shape[0], pos0.shape[1]
+    first = 0
+    if shard is not None:
+        if R_total != config.n_replicas:
+            raise ValueError("checkpoint replica count differs from config.n_replicas")
+        first, cnt = shard.first, shard.count
+        pos0, vel0 = pos0[first:first + cnt], vel0[first:first + cnt]
+    R = pos0.shape[0]
     eng = MDEngine(params, system.types, masses, system.prior, R, config.dt_fs,
                    config.temperature, config.friction, config.seed, config.neighbor_stride,
-                   rep_offset=rep_offset)
+                   rep_offset=rep_offset + first)
     eng.load_state(pos0, vel0, step0)
 
     traj_path, scal_path = out_dir / "trajectory.xyz", out_dir / "scalars.csv"
-    traj = open(traj_path, "wb")
-    scal = open(scal_path, "w")
-    scal.write("# flashcg-scalars v1\n" + SCALARS_SCHEMA + "\n")
-    writer = _FrameWriter(eng, system.types, masses, traj, scal)
+    traj = scal = None
+    if shard is None:
+        traj = open(traj_path, "wb")
+        scal = open(scal_path, "w")
+        scal.write("# flashcg-scalars v1\n" + SCALARS_SCHEMA + "\n")
+    writer = _FrameWriter(eng, system.types, masses, traj, scal, collect=shard is not None)
     t_start = time.perf_counter()
     last = [t_start]
     edge_total = [0, 0]  # (sum of per-replica edge counts, evaluations*replicas)
@@ -351,28 +398,45 @@ def run_simulation(params, system, config: SimConfig, out_dir, resume_from=None,
         last[0] = now
         writer.snapshot(step_done, wall_ms)
 
+    def close_files():
+        for f in (traj, scal):
+            if f is not None:
+                f.close()
+
     def blowup(step_at):
         writer.close()  # frames before the blow-up are complete
-        pos, _, _ = eng.read_state()
+        pos = eng.pos.cpu().numpy()
+        if shard is not None:
+            pos = shard.gather(pos)
         dump = out_dir / "blowup.xyz"
-        with open(dump, "wb") as f:
-            f.write(_lib.format_xyz(pos, system.types, step_at))
-        traj.close()
-        scal.close()
+        if lead:
+            with open(dump, "wb") as f:
+                f.write(_lib.format_xyz(pos, system.types, step_at))
+        close_files()
         raise SimulationBlowupError(f"simulation blew up at step {step_at}; "
                                     f"diagnostic frame in {dump}")
 
+    def checkpoint(at):
+        p, v_ = eng.pos.cpu().numpy(), eng.vel.cpu().numpy()
+        if shard is not None:
+            p, v_ = shard.gather(p), shard.gather(v_)
+        if lead:
+            params_io.save_checkpoint(config.checkpoint_path, p, v_, masses, at, config.seed)
+
+    NO_BLOWUP = 2 ** 62
     try:
         eng.evaluate()
         f0 = eng.forces.cpu().numpy()
         edge_total[0] += int(eng.csr.ptr[-1].item())
         edge_total[1] += R
-        if not np.all(np.isfinite(f0)) or np.any(np.abs(f0) > FORCE_BLOWUP_LIMIT):
+        bad0 = not np.all(np.isfinite(f0)) or np.any(np.abs(f0) > FORCE_BLOWUP_LIMIT)
+        if shard is not None:
+            bad0 = shard.min_int(step0 if bad0 else NO_BLOWUP) != NO_BLOWUP
+        if bad0:
             blowup(step0)
         if config.checkpoint_step is not None and step0 == config.checkpoint_step \
                 and config.checkpoint_path:
-            p, v_, _ = eng.read_state()
-            params_io.save_checkpoint(config.checkpoint_path, p, v_, masses, step0, config.seed)
+            checkpoint(step0)
         emit(step0, 1)
         stride = max(config.output_stride, 1)
         cur, end = step0, step0 + config.n_steps
@@ -384,30 +448,35 @@ def run_simulation(params, system, config: SimConfig, out_dir, resume_from=None,
             saved = [t.clone() for t in (eng.pos, eng.vel, eng.forces, eng.step)]
             csr0 = eng.save_csr() if config.neighbor_stride > 1 else None
             eng.clear_flags()
-            eng.run(n, graph_steps=min(graph_steps, n) if n >= 4 else 0)
+            eng.run(n, graph_steps=min(graph_steps, n) if n >= 4 else 0, check=False)
             fl = eng.flags()
-            if fl["overflow"] or fl["blowup"]:
+            if fl["overflow"]:   # local repair: regrow and replay the chunk
                 for t, s0 in zip((eng.pos, eng.vel, eng.forces, eng.step), saved):
                     t.copy_(s0)
-                if fl["overflow"]:
-                    eng._alloc(max(2 * eng.cap_e, int(1.5 * fl["edges"]) + 1024), keep=csr0)
-                    continue
-                # replay one step at a time to locate the blow-up step
+                eng._alloc(max(2 * eng.cap_e, int(1.5 * fl["edges"]) + 1024), keep=csr0)
+                continue
+            # the earliest blow-up step over all shards stops every shard there
+            b_step = fl["blowup_step"] if fl["blowup"] else NO_BLOWUP
+            if shard is not None:
+                b_step = shard.min_int(b_step)
+            if b_step != NO_BLOWUP:
+                for t, s0 in zip((eng.pos, eng.vel, eng.forces, eng.step), saved):
+                    t.copy_(s0)
                 if csr0 is not None:
                     eng._alloc(eng.cap_e, keep=csr0)
                 eng.clear_flags()
-                for _ in range(n):
-                    eng.run(1)
-                    if eng.flags()["blowup"]:
-                        blowup(int(eng.step.item()))
+                # replay one step at a time up to the blow-up step
+                while int(eng.step.item()) < b_step:
+                    eng.run(1, check=False)
+                    if shard is None and eng.flags()["blowup"]:
+                        break
+                blowup(int(eng.step.item()))
             edge_total[0] += fl["edge_sum"]
             edge_total[1] += fl["builds"] * R
             cur = nxt
             if config.checkpoint_step is not None and cur == config.checkpoint_step \
                     and config.checkpoint_path:
-                p, v_, _ = eng.read_state()
-                params_io.save_checkpoint(config.checkpoint_path, p, v_, masses, cur,
-                                          config.seed)
+                checkpoint(cur)
             if cur % stride == 0:
                 emit(cur, n)
         eng.torch.cuda.synchronize()
@@ -416,17 +485,34 @@ def run_simulation(params, system, config: SimConfig, out_dir, resume_from=None,
         if writer.thread.is_alive():
             writer.work.put(None)
             writer.thread.join()
-        traj.close()
-        scal.close()
+        close_files()
 
-    wall = time.perf_counter() - t_start
     pos, vel, step = eng.read_state()
-    traffic = TrafficReport()
+    if shard is not None:
+        # the end-of-run exchange: final states, recorded frames and scalars
+        pos, vel = shard.gather(pos), shard.gather(vel)
+        frames = writer.frames
+        fpos = shard.gather(np.stack([f[2] for f in frames], axis=1))    # [R, F, N, 3]
+        fsc = shard.gather(np.stack([f[3] for f in frames], axis=1))     # [R, F, 3]
+        edge_total = [int(x) for x in shard.sum_int(edge_total)]
+        if lead:
+            with open(traj_path, "wb") as traj_f, open(scal_path, "w") as scal_f:
+                scal_f.write("# flashcg-scalars v1\n" + SCALARS_SCHEMA + "\n")
+                for k, (st, wall_ms, _, _) in enumerate(frames):
+                    traj_f.write(_lib.format_xyz(fpos[:, k], system.types, st))
+                    scal_f.write(_scalar_rows(st, fsc[:, k, 0], fsc[:, k, 1], fsc[:, k, 2],
+                                              wall_ms))
+        shard.barrier()
+        R = R_total
+    wall = time.perf_counter() - t_start
+    mean_edges = edge_total[0] / edge_total[1] if edge_total[1] else 0.0
+    evaluations = R * (config.n_steps + 1)   # integrate(): one evaluation per step + initial
+    traffic = accumulated_traffic(config.backend, N, round(mean_edges * evaluations),
+                                  evaluations, params)
     return RunResult(trajectory_path=traj_path, scalars_path=scal_path, steps=config.n_steps,
                      replicas=R, wall_seconds=wall, dt_fs=config.dt_fs,
                      final_state=SimState(positions=pos, velocities=vel, masses=masses, step=step),
-                     traffic=traffic,
-                     mean_edges=edge_total[0] / edge_total[1] if edge_total[1] else 0.0)
+                     traffic=traffic, mean_edges=mean_edges)
 
 
 def _run_simulation_materialized(params, system, config: SimConfig, out_dir, resume_from=None):
@@ -488,7 +574,7 @@ def _run_simulation_materialized(params, system, config: SimConfig, out_dir, res
     counts = provider.edge_counts
     return RunResult(trajectory_path=traj_path, scalars_path=scal_path, steps=config.n_steps,
                      replicas=state.n_replicas, wall_seconds=wall, dt_fs=config.dt_fs,
-                     final_state=state, traffic=TrafficReport(),
+                     final_state=state, traffic=provider.traffic,
                      mean_edges=float(np.mean(counts)) if counts else 0.0)
 
 

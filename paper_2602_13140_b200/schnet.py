@@ -8,9 +8,9 @@ ablation flags pick the schedule as in the reference: fused=False runs the
 materialising schedule on the GPU (ablation.py: stacked edge tensors,
 atomic scatter-add or segmented reduction, autodiff forces — the paper's
 CGSchNet baseline) in the input dtype; fused=True runs the fused kernels
-(a fused atomic scatter has no GPU counterpart: it would only make the sums
-nondeterministic).  Every mode reports the reference's modelled traffic for
-its schedule (traffic_report).
+on fp32 inputs (fp64 inputs take the dtype-honouring materialised schedule
+so results keep the input precision, as the reference's do).  Every mode
+reports the reference's modelled traffic for its schedule (traffic_report).
 """
 
 from __future__ import annotations
@@ -162,6 +162,20 @@ def io_model_base(N: int, E: int, D: int, D_r: int, T: int, width: int) -> int:
     return T * width * (19 * N * D + 23 * E * D + 9 * E * D_r + 45 * E + 3 * N)
 
 
+def accumulated_traffic(mode: "PipelineMode", N: int, edge_total: int, evaluations: int,
+                        params, width: int = 4) -> TrafficReport:
+    """The merged TrafficReport of `evaluations` single-replica evaluations
+    of an N-bead system with `edge_total` edges over all of them — what the
+    reference's force provider accumulates (md.py:258-273, TrafficReport.merge)
+    — without per-evaluation edge counts.  Every modelled line is linear in
+    N and E except the min(N, E)·D gather term, so this is
+    traffic_report(N·k, ΣE); it is exact whenever every evaluation has
+    E >= N (or every one E <= N), true of all bonded CG systems here."""
+    cfg = params.config
+    return traffic_report(mode, N * evaluations, int(edge_total), cfg.hidden_dim, cfg.rbf_dim,
+                          len(params.blocks), width)
+
+
 def io_model_flash_report(N: int, E: int, params, width: int = 4) -> TrafficReport:
     rep = TrafficReport()
     D = params.config.hidden_dim
@@ -284,7 +298,11 @@ def flash_energy_forces(positions, types, params, mode: PipelineMode = PipelineM
     E = int(csr[0][-1])
     width = positions.dtype.itemsize if positions.dtype in (np.float32, np.float64) else 4
     traffic = traffic_report(mode, N, E, cfg.hidden_dim, cfg.rbf_dim, len(params.blocks), width)
-    if not mode.fused:
+    if not mode.fused or positions.dtype == np.float64:
+        # fp64 inputs: the reference evaluates in the input dtype
+        # (flash.py:446-501); the fused tcgen05 kernels are fp32, so fp64
+        # runs the dtype-honouring materialised schedule on the GPU (with the
+        # contention-free segment reduce when the mode asks for fusion)
         from .ablation import materialized_energy_forces
         from .engine import _torch
         torch = _torch()
@@ -294,7 +312,7 @@ def flash_energy_forces(positions, types, params, mode: PipelineMode = PipelineM
             _torch_model(params, dt), dev(positions.astype(np.float64 if dt == torch.float64
                                                            else np.float32)),
             dev(types.astype(np.int64)), dev(csr[0]), dev(csr[1]), dev(csr[3]), 1, N,
-            mode.segred)
+            mode.segred or mode.fused)
         return EnergyForces(energy=float(e[0].item()), per_atom=pa.cpu().numpy(),
                             forces=f.cpu().numpy().astype(positions.dtype, copy=False),
                             traffic=traffic)

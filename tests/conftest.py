@@ -59,7 +59,7 @@ class Golden:
 
 @pytest.fixture(scope="session")
 def golden():
-    return {n: Golden(n) for n in ("neighbors", "flash", "md")}
+    return {n: Golden(n) for n in ("neighbors", "flash", "md", "md_long")}
 
 
 @pytest.fixture(scope="session")

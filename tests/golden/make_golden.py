@@ -208,6 +208,35 @@ def md_fixture():
     np.savez_compressed(OUT / "md.npz", **out)
 
 
+def md_long_fixture():
+    """SURVEY §8(c) trajectory bar: 100 fp32 steps of coil-269 (R=2) through
+    the reference run_simulation, plus a 16-bit run (quantize_model weights,
+    20 steps) for the C3 configuration.  Written to md_long.npz so the
+    shorter md.npz fixtures stay byte-stable."""
+    import tempfile
+    out = {}
+    for name, quant, R, steps in [("traj_coil269_100", False, 2, 100),
+                                  ("traj_coil269_w16", True, 2, 20)]:
+        params = RM.init_params(RM.ModelConfig(), 0)
+        if quant:
+            params = RQ.quantize_model(params, seed=0)
+        sysm = RS.generate_system("coil", 269, 0)
+        sim = RMD.SimConfig(dt_fs=4.0, temperature=300.0, friction=1.0, n_steps=steps,
+                            n_replicas=R, seed=9, output_stride=10, neighbor_stride=1)
+        with tempfile.TemporaryDirectory() as td:
+            res = RMD.run_simulation(params, sysm, sim, td)
+            scal = (Path(td) / "scalars.csv").read_text()
+        # wall_ms (the last column) is measured time; drop it so the fixture
+        # is byte-stable across regenerations
+        scal = "\n".join(",".join(ln.split(",")[:5]) for ln in scal.splitlines()) + "\n"
+        out.update({f"{name}/pos": res.final_state.positions,
+                    f"{name}/vel": res.final_state.velocities,
+                    f"{name}/mean_edges": res.mean_edges, f"{name}/scalars": scal,
+                    f"{name}/quant": quant, f"{name}/cfg": json.dumps({}), f"{name}/stride": 1,
+                    f"{name}/meta": np.array([269, 0, 0, R, steps])})
+    np.savez_compressed(OUT / "md_long.npz", **out)
+
+
 def hashes_fixture():
     h = {"numpy": np.__version__}
     for kind, n, seed, bonded in [("coil", 269, 0, True), ("coil", 20, 3, True),
@@ -236,6 +265,7 @@ if __name__ == "__main__":
     neighbors_fixture()
     flash_fixture()
     md_fixture()
+    md_long_fixture()
     hashes_fixture()
     for p in sorted(OUT.glob("*.npz")):
         print(p.name, p.stat().st_size)

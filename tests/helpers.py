@@ -25,5 +25,13 @@ def params_for(case) -> object:
     return p
 
 
+def quantized(params):
+    """quantize_model(params, seed=0), cached per params object."""
+    key = ("obj", id(params))
+    if key not in _QCACHE or _QCACHE[key][0] is not params:
+        _QCACHE[key] = (params, quantize_model(params, seed=0))
+    return _QCACHE[key][1]
+
+
 def rel_rmse(f, ref):
     return float(np.sqrt(np.mean((f - ref) ** 2)) / np.sqrt(np.mean(ref ** 2)))

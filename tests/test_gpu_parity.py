@@ -5,7 +5,8 @@ Bars (BASELINE north star / SURVEY §8(c)):
   * neighbour list, CSR ptr/perm, noise, one integrator step, prior:
     bit-exact;
   * fp32 energies / forces: energy_rel_err and force_rel_err <= 1e-5;
-  * 16-bit weights: energy <= 5e-4 (see W16_ENERGY_TOL), force <= 5e-4 vs the quantized oracle;
+  * 16-bit weights: energy <= 1e-4 (5e-4 for the 24-atom case, see
+    W16_ENERGY_TOL), force <= 5e-4 vs the quantized oracle;
     vs fp32: relative force RMSE <= 2e-3 and the reference's W16 contract
     (energy <= 1e-2, force p95 <= 3e-2);
   * trajectories: max |dr| <= 1e-5 nm after the golden run lengths.
@@ -170,8 +171,10 @@ def test_energy_forces_fp32(golden, name):
 # relative metric) and 2.5e-5 on coil269_w16; CUDA's accurate expf/log1pf
 # only reach 1.1e-4 / 3.8e-5 at 37% more step time.  The reference holds W16
 # to 1e-2 energy / 3e-2 force-p95 against fp32 (tests/test_quantize.py:
-# 169-173, verify.py:274-307), checked below as well.
-W16_ENERGY_TOL = 5e-4
+# 169-173, verify.py:274-307), checked below as well.  The survey's bound
+# (energy <= 1e-4) holds for the 1ENH-size case; only the
+# 24-atom case keeps the looser bound, for the cancellation above.
+W16_ENERGY_TOL = {"small_w16": 5e-4, "coil269_w16": 1e-4}
 
 
 @pytest.mark.parametrize("name", ["small_w16", "coil269_w16"])
@@ -179,7 +182,7 @@ def test_energy_forces_w16(golden, name):
     c = golden["flash"].case(name)
     params = params_for(c)
     out = P.flash_energy_forces(c["pos"], c["types"], params, P.PipelineMode())
-    assert O.energy_rel_err(out.energy, float(c["energy"]), c["per_atom"]) <= W16_ENERGY_TOL
+    assert O.energy_rel_err(out.energy, float(c["energy"]), c["per_atom"]) <= W16_ENERGY_TOL[name]
     assert O.force_rel_err(out.forces, c["forces"]) <= 5e-4
     if name == "coil269_w16":
         fp = golden["flash"].case("coil269")
@@ -203,7 +206,7 @@ def test_pipeline_mode_ablations(golden, name, fused, segred):
     mode = P.PipelineMode(fused=fused, segred=segred)
     out = P.flash_energy_forces(c["pos"], c["types"], params, mode)
     if name.endswith("_w16"):
-        etol, ftol = W16_ENERGY_TOL, 5e-4
+        etol, ftol = W16_ENERGY_TOL[name], 5e-4
     elif c["pos"].dtype == np.float64 and not fused:
         etol, ftol = 1e-10, 1e-9
     else:
@@ -480,7 +483,8 @@ def test_capacity_overflow_regrows_and_matches(tmp_path, golden, monkeypatch):
     e0 = int(eng.csr.ptr[-1].item())
     eng._alloc(e0 - 1)
     eng.clear_flags()
-    eng.run(1)
+    with pytest.raises(P.CapacityError):   # MDEngine.run checks the status words
+        eng.run(1)
     assert eng.flags()["overflow"]
     # run_simulation detects it inside a chunk, regrows and replays the chunk
     orig = MDEngine.evaluate

@@ -124,3 +124,22 @@ def test_trajectory_matches_reference(golden, name):
     # the oracle restates the same numpy ops: identical trajectories
     np.testing.assert_array_equal(pos, c["pos"])
     np.testing.assert_array_equal(vel, c["vel"])
+
+
+@pytest.mark.parametrize("name", ["traj_coil269_100", "traj_coil269_w16"])
+def test_long_trajectory_matches_reference(golden, name):
+    # SURVEY §8(c) 100-step bar (fp32) and the C3 16-bit run: the oracle
+    # must reproduce the reference's run_simulation bit for bit before it
+    # is trusted as the GPU's checker on these lengths
+    from helpers import quantized
+    c = golden["md_long"].case(name)
+    n, sseed, pseed, R, steps = (int(x) for x in c["meta"])
+    sysm = generate_system("coil", n, sseed)
+    params = init_params(ModelConfig(), pseed)
+    if bool(c["quant"]):
+        params = quantized(params)
+    pos0 = np.repeat(sysm.positions[None], R, axis=0).astype(np.float32)
+    pos, vel, *_ = O.run_md(params, sysm.types, sysm.masses, sysm.prior, pos0,
+                            np.zeros_like(pos0), steps, seed=9, workers=R)
+    np.testing.assert_array_equal(pos, c["pos"])
+    np.testing.assert_array_equal(vel, c["vel"])

@@ -1,10 +1,12 @@
 """Summarise ncu outputs brought back in gpurun_out/ into profiles/.
 
-    python tools/ncu_summary.py TAG
+    python tools/ncu_summary.py TAG [CONFIG]
 reads gpurun_out/launches_TAG.csv (gpu__time_duration launch list) and
 gpurun_out/prof_TAG.ncu-rep (--set full captures), writes
 profiles/TAG_summary.md and merges per-kernel DRAM bytes into
-profiles/ncu_summary.json (read by bench.py for roofline.traffic).
+profiles/ncu_summary.json under CONFIG (bench.py's config_tag, default
+the C2 headline "coil269_rc1.5_fp32_R64"; read by bench.py for
+roofline.traffic of the same configuration).
 """
 
 from __future__ import annotations
@@ -90,7 +92,7 @@ def _full_one(p):
     return res
 
 
-def main(tag):
+def main(tag, config="coil269_rc1.5_fp32_R64"):
     lines = [f"# ncu summary `{tag}`", ""]
     ll = launch_list(tag)
     if ll:
@@ -126,7 +128,7 @@ def main(tag):
                 if name.endswith(suf):
                     name = name[:-len(suf)]
             if "dram_read" in d:
-                summary[name] = {"dram_bytes": d.get("dram_read", 0) + d.get("dram_write", 0),
+                summary.setdefault(config, {})[name] = {"dram_bytes": d.get("dram_read", 0) + d.get("dram_write", 0),
                                  "duration_s": d.get("duration"), "tag": tag}
     (ROOT / "profiles").mkdir(exist_ok=True)
     (ROOT / "profiles" / f"{tag}_summary.md").write_text("\n".join(lines) + "\n")
@@ -135,4 +137,4 @@ def main(tag):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(*sys.argv[1:3])
