@@ -103,9 +103,12 @@ typedef struct {
    * f_hexp for h = ssp(filter0(b)) (|h| <= max_c sum_k |W0[c][k]| + |b0[c]|
    * since 0 <= b <= 1), f_dbexp for the basis derivative db (|db| <=
    * sqrt(2*gamma/e) + pi/(2*r_cut)); f1_qmax = max W16 row scale of filter
-   * layer 1 (1 for fp32), folded into grad_w's bound. */
+   * layer 1 (1 for fp32), folded into grad_w's bound; f_vexp for
+   * v = ssp'(z0) * (W0 db), the operand of the forward-mode backward
+   * (|v[c]| <= max_d sum_k |W0[c][k]| |db_k(d)|, evaluated on the host). */
   int f_hexp, f_dbexp;
   float f1_qmax;
+  int f_vexp;
 } fcg_block;
 
 typedef struct {
@@ -206,6 +209,25 @@ int fcg_energy_forces(const fcg_model *m, const float *pos,
                       float *energy, float *forces, void *ws, size_t ws_bytes,
                       void *stream);
 
+/* The same evaluation under an explicit aggregation schedule
+ * (PipelineMode(fused=True, segred=...), flash.py:446-501):
+ *   FCG_SCHED_SEGRED  the contention-free CSR segment sums (the product
+ *                     path, flash.py:192-307; = fcg_energy_forces);
+ *   FCG_SCHED_SCATTER the "fused but scatter" ablation (flash.py:373-443):
+ *                     the same fused tcgen05 edge kernels, but messages,
+ *                     grad_P rows and the position gradient are aggregated
+ *                     with atomic adds (np.add.at per tile in the
+ *                     reference), so sums are order-dependent at fp32
+ *                     round-off. */
+enum { FCG_SCHED_SEGRED = 0, FCG_SCHED_SCATTER = 1 };
+int fcg_energy_forces_sched(const fcg_model *m, const float *pos,
+                            const int32_t *types, int R, int N,
+                            const int32_t *ptr, const int32_t *nbr,
+                            const int32_t *rev, const int32_t *own,
+                            int64_t cap_e, float *per_atom, float *energy,
+                            float *forces, void *ws, size_t ws_bytes,
+                            int schedule, void *stream);
+
 /* ---------------------------------------------------------------------
  * (f) batched Langevin integrator, md.py:109-208.
  * ------------------------------------------------------------------- */
@@ -230,6 +252,7 @@ typedef struct {
   uint64_t seed;   /* SimConfig.seed                          (md.py:127-131) */
   int rep_offset;  /* global index of replica 0 of this shard                 */
   int neighbor_stride;
+  int schedule;    /* FCG_SCHED_* of the force evaluation in fcg_md_step      */
 } fcg_md_params;
 
 /* numpy-exact noise: out[r][k] = float32(Generator(Philox(key=[seed, rep],

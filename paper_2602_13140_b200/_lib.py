@@ -17,6 +17,7 @@ FCG_D, FCG_DR, FCG_RH, FCG_MAX_BLOCKS = 128, 64, 64, 8
 FCG_OK, FCG_ERR_CAPACITY, FCG_ERR_ARG, FCG_ERR_CUDA = 0, 1, 2, 3
 FCG_FMT_FP32, FCG_FMT_W16 = 0, 1
 FCG_STATUS_WORDS = 8
+FCG_SCHED_SEGRED, FCG_SCHED_SCATTER = 0, 1   # include/fcg.h
 ST_EDGES, ST_OVERFLOW, ST_MAXDEG, ST_BLOWUP, ST_BLOWUP_STEP, ST_EDGE_SUM, ST_BUILDS = range(7)
 
 _f = C.POINTER(C.c_float)
@@ -33,7 +34,8 @@ class FcgBlock(C.Structure):
         [("f0_img", _u16), ("f1_img", _u16), ("f0_exp", C.c_int), ("f1_exp", C.c_int),
          ("pre_img", _u16), ("p0_img", _u16), ("p1_img", _u16),
          ("pre_exp", C.c_int), ("p0_exp", C.c_int), ("p1_exp", C.c_int),
-         ("f_hexp", C.c_int), ("f_dbexp", C.c_int), ("f1_qmax", C.c_float)]
+         ("f_hexp", C.c_int), ("f_dbexp", C.c_int), ("f1_qmax", C.c_float),
+         ("f_vexp", C.c_int)]
 
 
 class FcgModel(C.Structure):
@@ -56,7 +58,8 @@ class FcgPrior(C.Structure):
 
 class FcgMdParams(C.Structure):
     _fields_ = [("half_dt", C.c_float), ("c1", C.c_float), ("c2_num", C.c_float),
-                ("seed", C.c_uint64), ("rep_offset", C.c_int), ("neighbor_stride", C.c_int)]
+                ("seed", C.c_uint64), ("rep_offset", C.c_int), ("neighbor_stride", C.c_int),
+                ("schedule", C.c_int)]
 
 
 _VP = C.c_void_p
@@ -82,6 +85,9 @@ _SIGS = {
     "fcg_ef_workspace_bytes": (C.c_size_t, [C.POINTER(FcgModel), C.c_int, C.c_int, C.c_int64]),
     "fcg_energy_forces": (C.c_int, [C.POINTER(FcgModel), _VP, _VP, C.c_int, C.c_int, _VP, _VP,
                                     _VP, _VP, C.c_int64, _VP, _VP, _VP, _VP, C.c_size_t, _VP]),
+    "fcg_energy_forces_sched": (C.c_int, [C.POINTER(FcgModel), _VP, _VP, C.c_int, C.c_int, _VP,
+                                          _VP, _VP, _VP, C.c_int64, _VP, _VP, _VP, _VP,
+                                          C.c_size_t, C.c_int, _VP]),
     "fcg_normal_noise": (C.c_int, [C.c_uint64, C.c_int, _VP, C.c_int, C.c_int, _VP, _VP]),
     "fcg_langevin_baoa": (C.c_int, [C.POINTER(FcgMdParams), _VP, C.c_int, C.c_int, _VP, _VP,
                                     _VP, _VP, _VP]),

@@ -165,8 +165,9 @@ def materialized_energy_forces(model: TorchModel, pos, types, ptr, nbr, own, R: 
 
 def compare_on_engine(eng, params, reps: int = 5) -> dict:
     """Device time and peak memory of one energy+forces evaluation of the
-    engine's replica batch with the fused kernels (fcg_energy_forces) and
-    with the materialising schedules (scatter = CGSchNet, segmented), on the
+    engine's replica batch with the fused kernels (segment sums, and the
+    fused-scatter ablation with atomics: fcg_energy_forces_sched) and with
+    the materialising schedules (scatter = CGSchNet, segmented), on the
     same positions and CSR.  CUDA events around each call; the materialising
     path's peak is measured above the memory already allocated."""
     torch = _torch()
@@ -182,11 +183,11 @@ def compare_on_engine(eng, params, reps: int = 5) -> dict:
     forces = torch.empty(R * N, 3, dtype=torch.float32, device=pos.device)
     v = _lib.vp
 
-    def flash():
-        _lib.check(L.fcg_energy_forces(C.byref(eng.model.desc), v(pos), v(eng.types), R, N,
-                                       v(c.ptr), v(c.nbr), v(c.rev), v(c.own), c.cap_e,
-                                       v(per_atom), v(energy), v(forces), v(ws), ef,
-                                       C.c_void_p(stream.cuda_stream)), "fcg_energy_forces")
+    def flash(schedule=_lib.FCG_SCHED_SEGRED):
+        return lambda: _lib.check(L.fcg_energy_forces_sched(
+            C.byref(eng.model.desc), v(pos), v(eng.types), R, N, v(c.ptr), v(c.nbr), v(c.rev),
+            v(c.own), c.cap_e, v(per_atom), v(energy), v(forces), v(ws), ef, schedule,
+            C.c_void_p(stream.cuda_stream)), "fcg_energy_forces")
 
     model = TorchModel(params, torch.float32)
     E = int(c.ptr[-1].item())
@@ -210,12 +211,15 @@ def compare_on_engine(eng, params, reps: int = 5) -> dict:
         torch.cuda.synchronize()
         return t0.elapsed_time(t1) / reps, torch.cuda.max_memory_allocated() - base
 
-    f_ms, f_mem = timed(flash)
+    f_ms, f_mem = timed(flash())
+    fs_ms, fs_mem = timed(flash(_lib.FCG_SCHED_SCATTER))
     s_ms, s_mem = timed(mat(False))
     g_ms, g_mem = timed(mat(True))
     return {"what": "one energy+forces evaluation of the replica batch, same positions and CSR",
             "replicas": R, "edges": int(c.ptr[-1].item()),
-            "fused_ms": f_ms, "materialized_scatter_ms": s_ms, "materialized_segred_ms": g_ms,
+            "fused_ms": f_ms, "fused_scatter_ms": fs_ms,
+            "materialized_scatter_ms": s_ms, "materialized_segred_ms": g_ms,
+            "speedup_vs_fused_scatter": fs_ms / f_ms,
             "speedup_vs_scatter": s_ms / f_ms, "speedup_vs_segred": g_ms / f_ms,
             "extra_peak_bytes": {"fused": int(f_mem), "materialized_scatter": int(s_mem),
                                  "materialized_segred": int(g_mem)}}

@@ -155,6 +155,16 @@ int fcg_energy_forces(const fcg_model *m, const float *pos, const int32_t *types
                        nullptr, nullptr);
 }
 
+int fcg_energy_forces_sched(const fcg_model *m, const float *pos, const int32_t *types, int R,
+                            int N, const int32_t *ptr, const int32_t *nbr, const int32_t *rev,
+                            const int32_t *own, int64_t cap_e, float *per_atom, float *energy,
+                            float *forces, void *ws, size_t ws_bytes, int schedule,
+                            void *stream) {
+  return energy_forces(m, pos, types, R, N, ptr, nbr, rev, own, cap_e, per_atom, energy, forces,
+                       ws, ws_bytes, (cudaStream_t)stream, nullptr, nullptr, nullptr, nullptr,
+                       nullptr, nullptr, schedule);
+}
+
 int fcg_normal_noise(uint64_t seed, int rep_offset, const int64_t *step, int R, int N, float *out,
                      void *stream) {
   return normal_noise(seed, rep_offset, step, R, N, out, (cudaStream_t)stream);
@@ -209,7 +219,7 @@ int fcg_md_step(const fcg_model *m, const fcg_prior *pr, const fcg_md_params *p,
   if ((rc = prior_forces(pr, pos, R, N, prior, fprior, s))) return rc;
   // model forces + prior, blow-up check and the trailing half-kick (md.py:204-205)
   return energy_forces(m, pos, types, R, N, ptr, nbr, rev, own, cap_e, per_atom, potential,
-                       forces, ws_ef, eb, s, fprior, p, mass, vel, status, step);
+                       forces, ws_ef, eb, s, fprior, p, mass, vel, status, step, p->schedule);
 }
 
 }  // extern "C"

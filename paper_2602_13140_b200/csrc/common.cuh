@@ -191,7 +191,7 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
                   const int32_t *own, int64_t cap_e, float *per_atom, float *energy,
                   float *forces, void *ws, size_t ws_bytes, cudaStream_t s,
                   const float *f_extra, const fcg_md_params *kick, const float *mass,
-                  float *vel, int64_t *status, const int64_t *step);
+                  float *vel, int64_t *status, const int64_t *step, int schedule = 0);
 // md.cu
 int normal_noise(uint64_t seed, int rep_offset, const int64_t *step, int R, int N, float *out,
                  cudaStream_t s);
@@ -236,8 +236,9 @@ void launch_edge_geom(const EdgeArgs &a, float4 *geo, float2 *env, int32_t *unit
                       cudaStream_t s);
 void launch_edge_fwd_tc(const EdgeArgs &a, const float4 *geo, const float2 *env,
                         const int32_t *unit_rows, const float *P, float *H, int grid,
-                        cudaStream_t s);
+                        cudaStream_t s, bool scatter = false);
 void launch_edge_bwd_tc(const EdgeArgs &a, const float4 *geo, const float2 *env,
                         const int32_t *unit_rows, const float *P, const float *GH, float *GP,
-                        float4 *gsum, int accumulate, int grid, cudaStream_t s);
+                        float4 *gsum, int accumulate, int grid, cudaStream_t s,
+                        float4 *gr = nullptr);
 }  // namespace fcg

@@ -147,10 +147,51 @@ struct SegSum {
       }
     }
   }
+  // The same walk split in two: starts(own) once per tile, then half(h)
+  // for edges h..h+15 (h = 0, 16) with only those 16 values live.
+  __device__ __forceinline__ unsigned starts(const int *own) const {
+    const int lane = threadIdx.x & 31;
+    const int cur = own[lane];
+    return __ballot_sync(0xffffffffu, cur != (lane ? own[lane - 1] : row));
+  }
+  __device__ __forceinline__ void half(const int *own, const float (&m)[16], int h,
+                                       unsigned st) {
+    const unsigned hb = (st >> h) & 0xffffu;
+    if (hb == 0u) {
+      float s[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s[i] = m[i] + m[i + 8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) s[i] += s[i + 4];
+      acc += (s[0] + s[2]) + (s[1] + s[3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        if ((hb >> i) & 1u) {
+          if (row >= 0) outc[(uint32_t)row * D] = acc;
+          row = own[h + i];
+          acc = 0.f;
+        }
+        acc += m[i];
+      }
+    }
+  }
   __device__ __forceinline__ void finish() {
     if (row >= 0) outc[(uint32_t)row * D] = acc;
   }
 };
+
+// Atomic scatter of one tile (the "fused but scatter" ablation schedule,
+// flash.py:373-443: np.add.at per tile instead of segment sums): every valid
+// edge adds its message to its row with a red.global.add; the 32 lanes of a
+// warp hold 32 consecutive channels of one row, so each instruction is one
+// coalesced 128-byte reduction.  Summation order is the arrival order.
+__device__ __forceinline__ void scatter_tile(float *outc, const int *own, const float (&m)[TT],
+                                             int n_e) {
+#pragma unroll
+  for (int i = 0; i < TT; ++i)
+    if (i < n_e) atomicAdd(outc + (uint32_t)own[i] * D, m[i]);
+}
 
 // ---- per-step edge geometry (the reference's d cache, flash.py:221-223) ------
 // geo[k] = (u, d) with u = r[own] - r[nbr] for CSR slot k; env[k] = (C, C').
@@ -483,6 +524,20 @@ struct MetaRegs {
     m->denv[lane] = c.y;
     __syncwarp();
     return src_owned ? make_float4(-g.x, -g.y, -g.z, g.w) : g;
+  }
+  // As store(), plus whether the tile's edges fall in at most three CSR
+  // rows (first, `mid`, last): 95% of coil-269 tiles; their P[src] values
+  // are then three loads per thread instead of 32 gathers.
+  __device__ __forceinline__ float4 store3(WarpMeta *m, bool src_owned, int lane, bool &rows3,
+                                           int &mid) const {
+    bool r2;
+    const float4 u = store(m, src_owned, lane, r2);
+    const int first = __shfl_sync(0xffffffffu, o, 0);
+    const int last = __shfl_sync(0xffffffffu, o, max(n_e - 1, 0));
+    const unsigned other = __ballot_sync(0xffffffffu, lane < n_e && o != first && o != last);
+    mid = other ? __shfl_sync(0xffffffffu, o, __ffs(other) - 1) : first;
+    rows3 = __all_sync(0xffffffffu, lane >= n_e || o == first || o == last || o == mid);
+    return u;
   }
 };
 
@@ -936,7 +991,7 @@ constexpr uint32_t KSTR64 = (64 / 8) * 128;  // B operand bytes per 8 K-rows, 64
 // 2 groups x 8 warps, each group's tile = 32 edges of each of its two work
 // units, as in k_edge_bwd64.  TMEM: 2 x 128 group columns (z0 | w, 64 wide)
 // + W0 | W1 at TW0; shared memory: the forward layout (buffers 2 x 48 KB).
-template <bool Q>
+template <bool Q, bool SC>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_edge_fwd64(const EdgeArgs a, const float4 *geo, const float2 *env,
              const int32_t *unit_rows, const float *P, float *H) {
@@ -1020,11 +1075,15 @@ k_edge_fwd64(const EdgeArgs a, const float4 *geo, const float2 *env,
       if (n_e > 0) {  // m = (W1 h + b1) * P[src], dst segment sums
 #pragma unroll
         for (int i = 0; i < TT; ++i) v[i] = (v[i] * s1 + b1c) * pv[i];
-        if (n_e < TT) {
+        if (SC) {
+          scatter_tile(seg.outc, W.meta(it)->own, v, n_e);
+        } else {
+          if (n_e < TT) {
 #pragma unroll
-          for (int i = 0; i < TT; ++i) v[i] = i < n_e ? v[i] : 0.f;
+            for (int i = 0; i < TT; ++i) v[i] = i < n_e ? v[i] : 0.f;
+          }
+          seg.tile(W.meta(it)->own, v);
         }
-        seg.tile(W.meta(it)->own, v);
       }
     }
     if (more) {
@@ -1035,7 +1094,7 @@ k_edge_fwd64(const EdgeArgs a, const float4 *geo, const float2 *env,
       }
     }
   }
-  seg.finish();
+  if (!SC) seg.finish();
   tc::fence_before_sync();
   __syncthreads();
   if (threadIdx.x < 32) tc::tmem_dealloc<512>(sh->tmem);
@@ -1057,12 +1116,16 @@ static bool fwd64_enabled() {
 // each GEMM is N = 64 and a group issues half the MMAs per edge.  TMEM: 2 x
 // 128 accumulator columns (SA, SB 64 wide) + W1 | W1^T; the shared-memory
 // layout is the 4-group one (buffers 2 x 48 KB, stash per unit).
-template <bool Q>
+// SC (the fused-scatter ablation, flash.py:373-443): grad_P rows and the
+// position gradient are accumulated with atomics — grad_P[src] += gH*w per
+// channel, grad_r[dst] += g_e, grad_r[src] -= g_e (gr, float4 per node) —
+// instead of segment sums and the per-slot gsum the force assembly gathers.
+template <bool Q, bool SC>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_edge_bwd64(const EdgeArgs a, const float4 *geo, const float2 *env,
              const int32_t *unit_rows, const float *P,
              const float *GH, float *GP, float4 *gsum,
-             int accumulate) {
+             int accumulate, float4 *gr) {
   extern __shared__ __align__(1024) uint8_t sm[];
   TcShared *sh = (TcShared *)(sm + SM_META);
   const fcg_block &B = a.blk;
@@ -1182,11 +1245,15 @@ k_edge_bwd64(const EdgeArgs a, const float4 *geo, const float2 *env,
       tc::tmem_ld32w(W.tl + SA64, v);
 #pragma unroll
       for (int i = 0; i < TT; ++i) v[i] = gh[i] * (v[i] * s1 + b1c);
-      if (n_e < TT) {
+      if (SC) {
+        scatter_tile(seg.outc, M->own, v, n_e);
+      } else {
+        if (n_e < TT) {
 #pragma unroll
-        for (int i = 0; i < TT; ++i) v[i] = i < n_e ? v[i] : 0.f;
+          for (int i = 0; i < TT; ++i) v[i] = i < n_e ? v[i] : 0.f;
+        }
+        seg.tile(M->own, v);
       }
-      seg.tile(M->own, v);
     } else {
       float v[TT];
       tc::tmem_ld32w(W.tl + SA64, v);  // warp-collective order kept; values unused
@@ -1231,6 +1298,278 @@ k_edge_bwd64(const EdgeArgs a, const float4 *geo, const float2 *env,
         const float inv = ue.w > TINY_DISTANCE ? 1.f / ue.w : 0.f;
         const float sc = gd * inv;
         float4 g = make_float4(sc * ue.x, sc * ue.y, sc * ue.z, 0.f);
+        if (SC) {  // np.add.at(grad_r, dst, gu); np.add.at(grad_r, src, -gu)
+          float *gd_ = (float *)&gr[(uint32_t)M->nbr[e] / D];
+          float *gs_ = (float *)&gr[M->own[e]];
+          atomicAdd(gd_, g.x); atomicAdd(gd_ + 1, g.y); atomicAdd(gd_ + 2, g.z);
+          atomicAdd(gs_, -g.x); atomicAdd(gs_ + 1, -g.y); atomicAdd(gs_ + 2, -g.z);
+        } else {
+          float4 *dst = &gsum[t0 + e];
+          if (accumulate) {
+            const float4 o = *dst;
+            g.x += o.x; g.y += o.y; g.z += o.z;
+          }
+          *dst = g;
+        }
+      }
+    }
+  }
+  if (!SC) seg.finish();
+  tc::fence_before_sync();
+  __syncthreads();
+  if (threadIdx.x < 32) tc::tmem_dealloc<512>(sh->tmem);
+}
+
+// ---------------------------------------------------------------------------
+// Backward in forward mode (the default; FCG_BWD_FM=0 selects k_edge_bwd64).
+//
+// flash_block_backward (flash.py:272-295) needs, per edge, grad_P rows
+// (src-segment sums of gH*w) and grad_d = sum_c grad_w[c] dw[c]/dd with
+// grad_w = gH[dst] * P[src].  The reference reaches grad_d in reverse mode
+// (grad_b = filter backward of grad_w, then grad_b . db); here the
+// derivative of the filter output is propagated forward instead:
+//   dw/dd = W1 (ssp'(z0) * (W0 db)) = W1 v,
+// so one tile needs two MMA chains, both with weights as the A operand:
+//   [G1 | G1'] = W0 [b | db]  -> z0 | dz0    (K = 64, N = 2 x 64 edges)
+//   [G2 | G3 ] = W1 [h | v ]  -> w  | u      (K = 128, N = 2 x 64 edges)
+// with h = ssp(z0), v = ssp'(z0) dz0; then grad_P += gH*(w + b1) and
+// grad_d = sum_c gH[c] P[src][c] u[c].  Compared with k_edge_bwd64 that is
+// the same number of MMAs (72 per tile, fp32), but two completion waits per
+// tile instead of four, no W1^T (TMEM holds W1 and W0, 192 columns), no
+// ssp' stash and no TMEM store; grad_w never becomes an MMA operand.
+//
+// Work decomposition as k_edge_bwd64: 2 groups x 8 warps, a group tile = 32
+// edges of each of its two work units (warps 0-3 / 4-7), one walker per CSR
+// row.  TMEM: group g owns columns [128g, 128g+128): [0, 64) z0 then w,
+// [64, 128) dz0 then u (unit half hf at +32 hf); W1 hi|lo at 256, W0 hi|lo at
+// 384.  Shared memory per group: the K=64 basis operand [b | db] (N = 128)
+// and the K=128 operand [h | v] (N = 128), hi and lo images.
+constexpr uint32_t FM_TW1 = 256, FM_TW0 = 384;
+constexpr uint32_t KSTR128 = (128 / 8) * 128;                 // bytes per 8 K-rows, N = 128
+constexpr uint32_t FM_BB = 2 * DR * 128 * 2;                  // [b | db] hi|lo: 32 KB
+constexpr uint32_t FM_HV = 2 * D * 128 * 2;                   // [h | v] hi|lo: 64 KB
+constexpr uint32_t FM_GBUF = FM_BB + FM_HV;
+constexpr uint32_t FM_SM_META = 2 * FM_GBUF;
+constexpr uint32_t FM_SM_TOTAL = FM_SM_META + sizeof(TcShared);
+static_assert(SM_W1 + 2 * W1_BYTES <= FM_SM_META, "weight staging aliases the group buffers");
+static_assert(FM_SM_TOTAL + 1024 <= 232448, "forward-mode backward shared memory budget");
+static_assert(FM_TW0 + DR <= 512, "TMEM budget");
+
+// W1 hi | lo and W0 hi | lo from the staged images into TMEM: warp w moves
+// image (w / 4) % 4 for its lane quarter.
+__device__ __forceinline__ void load_fm_weights_tmem(const uint8_t *sm, uint32_t tmem) {
+  const int w = threadIdx.x >> 5, q = w & 3, m = 32 * q + (threadIdx.x & 31);
+  const int img = (w >> 2) & 3;  // 0: W1 hi, 1: W1 lo, 2: W0 hi, 3: W0 lo
+  const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16);
+  if (img < 2)
+    image_row_to_tmem<false>((const uint16_t *)(sm + SM_W1 + (img & 1) * W1_BYTES), D, m,
+                             lane_base + FM_TW1 + (img & 1) * (D / 2));
+  else
+    image_row_to_tmem<false>((const uint16_t *)(sm + SM_W0 + (img & 1) * W0_BYTES), DR, m,
+                             lane_base + FM_TW0 + (img & 1) * (DR / 2));
+  prologue_done();
+}
+
+// One tile's pair of chains into the group's 128 columns: the left half
+// (z0 / w, NPL products) and the right half (dz0 / u, NPR products).  Equal
+// product counts issue one N = 128 chain.
+template <int KS, int NPL, int NPR>
+__device__ __forceinline__ void mma_pair_ts(uint32_t d, uint32_t a_hi, uint32_t a_lo, Desc b) {
+  if (NPL == NPR) {
+    mma_chain_ts<KS, NPL>(d, a_hi, a_lo, b, tc::idesc_f16(128, 128, 0, 1));
+  } else {
+    const uint32_t id64 = tc::idesc_f16(128, 64, 0, 1);
+    mma_chain_ts<KS, NPL>(d, a_hi, a_lo, b, id64);
+    Desc br = b;
+    br.hi += 1024u / 16u;  // columns 64.. of the N = 128 operand (8 core rows of 128 B)
+    br.lo += 1024u / 16u;
+    mma_chain_ts<KS, NPR>(d + 64, a_hi, a_lo, br, id64);
+  }
+}
+
+template <bool Q>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+k_edge_bwd_fm(const EdgeArgs a, const float4 *geo, const float2 *env,
+              const int32_t *unit_rows, const float *P,
+              const float *GH, float *GP, float4 *gsum,
+              int accumulate) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  TcShared *sh = (TcShared *)(sm + FM_SM_META);
+  const fcg_block &B = a.blk;
+  pdl_trigger();
+  kernel_prologue(sm, sh, B, NGRP);  // bar[0..1] per group, xbar[0..3] per unit
+  tc::mbar_wait(&sh->wbar, 0);
+  load_fm_weights_tmem(sm, sh->tmem);  // ends with the PDL wait
+  Wctx W;
+  W.w = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+  W.g = W.w >> 3;
+  const int hf = (W.w >> 2) & 1;
+  const int u = 2 * W.g + hf;  // work unit / grad_d partials of this warp
+  W.q = W.w & 3;
+  W.lane = threadIdx.x & 31;
+  W.ch = 32 * W.q + W.lane;
+  W.eo = 32 * hf;
+  W.amask = 7u;
+  W.sh = sh;
+  W.bb = sm + W.g * FM_GBUF;
+  W.hb = W.bb + FM_BB;
+  W.sbb = tc::smem_u32(W.bb);
+  W.shb = tc::smem_u32(W.hb);
+  W.tmem_g = sh->tmem + 128u * W.g;
+  W.tl = W.tmem_g + ((uint32_t)(32 * W.q) << 16) + 32u * hf;
+  constexpr int NB = Q ? 1 : 3, NDB = Q ? 2 : 3, NH = Q ? 1 : 3, NV = Q ? 2 : 3;
+  const uint32_t w0h = sh->tmem + FM_TW0, w0l = w0h + DR / 2;
+  const uint32_t w1h = sh->tmem + FM_TW1, w1l = w1h + D / 2;
+  const Desc bb = adesc<KSTR128>(W.sbb, DR), hb = adesc<KSTR128>(W.shb, D);
+
+  const UnitRange tr = unit_range(a, unit_rows, NGRP * blockIdx.x + u);
+  const UnitRange to = unit_range(a, unit_rows, NGRP * blockIdx.x + (u ^ 1));
+  const int ntiles = (tr.ee - tr.eb + TT - 1) / TT;
+  const int nt_all = max(ntiles, (to.ee - to.eb + TT - 1) / TT);  // the group's iterations
+  const int ch = W.ch;
+  const float *GHch = opaque_ptr(GH + ch);
+  const float *Pch = opaque_ptr(P + ch);
+  SegSum seg;
+  seg.row = ntiles > 0 ? a.own[tr.eb] : -1;
+  seg.acc = 0.f;
+  seg.outc = opaque_ptr(GP + ch);
+
+  // E1 constants (this thread's channel = hidden unit k of filter layer 0)
+  const float b0c = ld_dep(&B.f0_b[ch]);
+  const float rs0 = Q ? ld_dep(&B.f0_s[ch]) : pow2f(-(B.f0_exp + 14));
+  const float hs = Q ? 1.f : pow2f(B.f_hexp);
+  const HScale hk(rs0, b0c, hs);
+  // v * 2^f_vexp from the dz0 accumulator (W0 * 2^f0_exp (fp32) or w16 (W16,
+  // row scale s0) times db * 2^f_dbexp)
+  const float kv = Q ? ld_dep(&B.f0_s[ch]) * pow2f(B.f_vexp - B.f_dbexp)
+                     : pow2f(B.f_vexp - B.f0_exp - B.f_dbexp);
+  // E2 constants (this thread's channel = output channel c of filter layer 1)
+  const float b1c = ld_dep(&B.f1_b[ch]);
+  const float s1 = Q ? ld_dep(&B.f1_s[ch]) : pow2f(-(B.f1_exp + B.f_hexp));
+  const float ku = Q ? ld_dep(&B.f1_s[ch]) * pow2f(-B.f_vexp) : pow2f(-(B.f1_exp + B.f_vexp));
+  const float bsc = Q ? 0.f : 14.f;
+
+  float4 ue = make_float4(0.f, 0.f, 0.f, 0.f), ue_n = ue;
+  bool rows3 = true, rows3_n = true;
+  int mid = 0, mid_n = 0;
+  MetaRegs mr;
+  if (nt_all > 0) {  // tile 0 (possibly empty for this half): metadata, [b | db], G1 | G1'
+    mr.load(a, geo, env, tr.eb, min(TT, tr.ee - tr.eb), W.lane);
+    ue_n = mr.store3(W.meta(0), true, W.lane, rows3_n, mid_n);
+    mr.load(a, geo, env, tr.eb + TT, min(TT, tr.ee - tr.eb - TT), W.lane);
+    tile_basis<false, Q, KSTR128>(a, W, W.meta(0), bsc);
+    W.eo += 64;
+    tile_basis<true, false, KSTR128>(a, W, W.meta(0), (float)B.f_dbexp);
+    W.eo -= 64;
+    REQ(BAR_G1, (mma_pair_ts<DR / 16, NB, NDB>(W.tmem_g, w0h, w0l, bb)));
+  }
+  for (int it = 0; it < nt_all; ++it) {
+    ue = ue_n;
+    rows3 = rows3_n;
+    mid = mid_n;
+    const int t0 = tr.eb + it * TT;
+    const bool more = it + 1 < nt_all;
+    const WarpMeta *M = W.meta(it);
+    const int n_e = min(TT, tr.ee - t0);  // <= 0: this half has no tile this iteration
+
+    // ---- E1: h = ssp(z0), v = ssp'(z0) dz0 -> [h | v] -----------------------
+    W.wait(BAR_G1, it);
+#pragma unroll
+    for (int c0 = 0; c0 < TT; c0 += 16) {
+      float z[16], dz[16];
+      tc::tmem_ld16w(W.tl + c0, z);
+      tc::tmem_ld16w(W.tl + 64 + c0, dz);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        float sp;
+        if (Q) {
+          const float zz = z[i] * rs0 + b0c;
+          sp = sigmoid_fast(zz);
+          z[i] = __half2float(__float2half_rn(ssp_fast(zz)));
+        } else {
+          z[i] = ssp_scaled(z[i] * hk.rs + hk.b, hk.c_ln2, hk.c_e);  // hs * h
+          sp = fmaf(-0.5f, ex2_ftz(z[i] * hk.c_e), 1.f);             // 1 - e^-h / 2
+        }
+        dz[i] = sp * dz[i] * kv;
+      }
+#pragma unroll
+      for (int j = 0; j < 16; j += 8) {
+        put8<!Q, KSTR128>(W.hb, D, ch, W.eo + c0 + j, &z[j], 1.f);
+        put8<true, KSTR128>(W.hb, D, ch, 64 + W.eo + c0 + j, &dz[j], 1.f);
+      }
+    }
+    REQ(BAR_G2, (mma_pair_ts<D / 16, NH, NV>(W.tmem_g, w1h, w1l, hb)));
+
+    // ---- gathers of this tile (consumed after the [G2 | G3] wait) ------------
+    float gh[TT];
+    float pf = 0.f, pm = 0.f, pl = 0.f;  // P[src] of the first, middle and last row
+    int o_f = -1, o_l = -1;
+    if (n_e > 0) {
+#pragma unroll
+      for (int i = 0; i < TT; ++i) gh[i] = ld_gather(GHch + (uint32_t)M->nbr[i]);
+      o_f = M->own[0];
+      o_l = M->own[n_e - 1];
+      pf = ld_gather(Pch + (uint32_t)o_f * D);
+      pm = ld_gather(Pch + (uint32_t)mid * D);
+      pl = ld_gather(Pch + (uint32_t)o_l * D);
+    } else {
+#pragma unroll
+      for (int i = 0; i < TT; ++i) gh[i] = 0.f;
+    }
+    if (more) {  // next tile's metadata and [b | db] (the basis buffer is free: G1 done)
+      ue_n = mr.store3(W.meta(it + 1), true, W.lane, rows3_n, mid_n);
+      mr.load(a, geo, env, t0 + 2 * TT, min(TT, tr.ee - t0 - 2 * TT), W.lane);
+      tile_basis<false, Q, KSTR128>(a, W, W.meta(it + 1), bsc);
+      W.eo += 64;
+      tile_basis<true, false, KSTR128>(a, W, W.meta(it + 1), (float)B.f_dbexp);
+      W.eo -= 64;
+    }
+
+    // ---- E2: grad_P segment sums, grad_d partials --------------------------
+    W.wait(BAR_G2, it);
+    float q[TT];
+    {
+      const unsigned st = n_e > 0 ? seg.starts(M->own) : 0u;
+#pragma unroll
+      for (int h = 0; h < TT; h += 16) {
+        float v[16];
+        tc::tmem_ld16w(W.tl + h, v);  // w accumulator
+        if (n_e > 0) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = h + i < n_e ? gh[h + i] * (v[i] * s1 + b1c) : 0.f;
+          seg.half(M->own, v, h, st);
+        }
+      }
+      tc::tmem_ld32w(W.tl + 64, q);  // u accumulator
+    }
+    if (more)  // TMEM columns read: the next tile's G1 | G1' may overwrite them
+      REQ(BAR_G1, (mma_pair_ts<DR / 16, NB, NDB>(W.tmem_g, w0h, w0l, bb)));
+    if (rows3) {
+#pragma unroll
+      for (int j = 0; j < TT; j += 4) {
+        const int4 o4 = *(const int4 *)&M->own[j];
+        const int oo[4] = {o4.x, o4.y, o4.z, o4.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          q[j + i] *= gh[j + i] * (oo[i] == o_l ? pl : (oo[i] == o_f ? pf : pm)) * ku;
+      }
+    } else {  // four or more rows (~5% of tiles): per-edge gathers
+#pragma unroll
+      for (int i = 0; i < TT; ++i)
+        q[i] *= gh[i] * ld_gather(Pch + (uint32_t)M->own[i] * D) * ku;
+    }
+    float *xg = &sh->xg[u][it & 1][0][0];
+    xg[W.q * TT + W.lane] = warp_edge_sum(q, W.lane);
+    __syncwarp();
+    if (W.lane == 0) tc::mbar_arrive(&sh->xbar[u]);
+    if (W.q == 0) {
+      tc::mbar_wait(&sh->xbar[u], (uint32_t)(it & 1));
+      const int e = W.lane;
+      if (e < n_e) {
+        const float gd = ((xg[e] + xg[TT + e]) + xg[2 * TT + e]) + xg[3 * TT + e];
+        const float inv = ue.w > TINY_DISTANCE ? 1.f / ue.w : 0.f;
+        const float sc = gd * inv;
+        float4 g = make_float4(sc * ue.x, sc * ue.y, sc * ue.z, 0.f);
         float4 *dst = &gsum[t0 + e];
         if (accumulate) {
           const float4 o = *dst;
@@ -1244,6 +1583,14 @@ k_edge_bwd64(const EdgeArgs a, const float4 *geo, const float2 *env,
   tc::fence_before_sync();
   __syncthreads();
   if (threadIdx.x < 32) tc::tmem_dealloc<512>(sh->tmem);
+}
+
+static bool bwd_fm_enabled() {
+  static const bool on = [] {
+    const char *v = getenv("FCG_BWD_FM");
+    return !(v && v[0] == '0');
+  }();
+  return on;
 }
 
 // Default on (1.0415 -> 1.0251 ms/step at C2); FCG_BWD64=0 runs the 4-group
@@ -1262,12 +1609,20 @@ void edge_tc_configure() {
   const int smem = (int)(SM_TOTAL + 1024), fsmem = (int)(FWD_SM_TOTAL + 1024);
   cudaFuncSetAttribute(k_edge_fwd_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
   cudaFuncSetAttribute(k_edge_fwd_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
-  cudaFuncSetAttribute(k_edge_fwd64<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
-  cudaFuncSetAttribute(k_edge_fwd64<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
+  cudaFuncSetAttribute(k_edge_fwd64<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
+  cudaFuncSetAttribute(k_edge_fwd64<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
+  cudaFuncSetAttribute(k_edge_fwd64<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
+  cudaFuncSetAttribute(k_edge_fwd64<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
   cudaFuncSetAttribute(k_edge_bwd_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_edge_bwd_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_edge_bwd64<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_edge_bwd64<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_edge_bwd_fm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(FM_SM_TOTAL + 1024));
+  cudaFuncSetAttribute(k_edge_bwd_fm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(FM_SM_TOTAL + 1024));
+  cudaFuncSetAttribute(k_edge_bwd64<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_edge_bwd64<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_edge_bwd64<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_edge_bwd64<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   done = true;
 }
 
@@ -1283,10 +1638,13 @@ void launch_edge_geom(const EdgeArgs &a, float4 *geo, float2 *env, int32_t *unit
 
 void launch_edge_fwd_tc(const EdgeArgs &a, const float4 *geo, const float2 *env,
                         const int32_t *unit_rows, const float *P, float *H, int grid,
-                        cudaStream_t s) {
-  if (fwd64_enabled() && FWD_NGRP == 4)  // the 64-edge kernel uses the 4-unit partition
-    launch_pdl(PDL_EDGE_FWD, a.quant ? k_edge_fwd64<true> : k_edge_fwd64<false>, grid,
-               TC_THREADS, FWD_SM_TOTAL + 1024, s, a, geo, env, unit_rows, P, H);
+                        cudaStream_t s, bool scatter) {
+  if (scatter)  // H zeroed by the caller; the scatter schedule exists for the 64-edge kernel
+    launch_pdl(PDL_EDGE_FWD, a.quant ? k_edge_fwd64<true, true> : k_edge_fwd64<false, true>,
+               grid, TC_THREADS, FWD_SM_TOTAL + 1024, s, a, geo, env, unit_rows, P, H);
+  else if (fwd64_enabled() && FWD_NGRP == 4)  // the 64-edge kernel uses the 4-unit partition
+    launch_pdl(PDL_EDGE_FWD, a.quant ? k_edge_fwd64<true, false> : k_edge_fwd64<false, false>,
+               grid, TC_THREADS, FWD_SM_TOTAL + 1024, s, a, geo, env, unit_rows, P, H);
   else
     launch_pdl(PDL_EDGE_FWD, a.quant ? k_edge_fwd_tc<true> : k_edge_fwd_tc<false>, grid,
                FWD_THREADS, FWD_SM_TOTAL + 1024, s, a, geo, env, unit_rows, P, H);
@@ -1294,11 +1652,19 @@ void launch_edge_fwd_tc(const EdgeArgs &a, const float4 *geo, const float2 *env,
 
 void launch_edge_bwd_tc(const EdgeArgs &a, const float4 *geo, const float2 *env,
                         const int32_t *unit_rows, const float *P, const float *GH, float *GP,
-                        float4 *gsum, int accumulate, int grid, cudaStream_t s) {
-  if (bwd64_enabled())
-    launch_pdl(PDL_EDGE_BWD, a.quant ? k_edge_bwd64<true> : k_edge_bwd64<false>, grid,
-               TC_THREADS, SM_TOTAL + 1024, s, a, geo, env, unit_rows, P, GH, GP, gsum,
+                        float4 *gsum, int accumulate, int grid, cudaStream_t s, float4 *gr) {
+  if (gr)  // scatter schedule: GP and gr zeroed by the caller
+    launch_pdl(PDL_EDGE_BWD, a.quant ? k_edge_bwd64<true, true> : k_edge_bwd64<false, true>,
+               grid, TC_THREADS, SM_TOTAL + 1024, s, a, geo, env, unit_rows, P, GH, GP, gsum,
+               accumulate, gr);
+  else if (bwd_fm_enabled())
+    launch_pdl(PDL_EDGE_BWD, a.quant ? k_edge_bwd_fm<true> : k_edge_bwd_fm<false>, grid,
+               TC_THREADS, FM_SM_TOTAL + 1024, s, a, geo, env, unit_rows, P, GH, GP, gsum,
                accumulate);
+  else if (bwd64_enabled())
+    launch_pdl(PDL_EDGE_BWD, a.quant ? k_edge_bwd64<true, false> : k_edge_bwd64<false, false>,
+               grid, TC_THREADS, SM_TOTAL + 1024, s, a, geo, env, unit_rows, P, GH, GP, gsum,
+               accumulate, (float4 *)nullptr);
   else
     launch_pdl(PDL_EDGE_BWD, a.quant ? k_edge_bwd_tc<true> : k_edge_bwd_tc<false>, grid,
                TC_THREADS, SM_TOTAL + 1024, s, a, geo, env, unit_rows, P, GH, GP, gsum, accumulate);

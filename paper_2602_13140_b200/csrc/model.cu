@@ -526,7 +526,8 @@ k_edge_bwd(const EdgeArgs a, const float *__restrict__ P, const float *__restric
 constexpr int FF_LPN = 8;  // lanes per node in k_forces_finish
 
 __device__ __forceinline__ void forces_node(const int32_t *ptr, const int32_t *rev,
-                                            const float4 *gsum, int N, int RN, int64_t cap_e,
+                                            const float4 *gsum, const float4 *gr, int N,
+                                            int RN, int64_t cap_e,
                                             const float *f_extra, float *forces,
                                             const fcg_md_params &kick, int do_kick,
                                             const float *mass, float *vel, int64_t *status,
@@ -539,7 +540,12 @@ __device__ __forceinline__ void forces_node(const int32_t *ptr, const int32_t *r
   const int g = (int)(tid / FF_LPN);
   const int lane = threadIdx.x & (FF_LPN - 1);
   float gx = 0.f, gy = 0.f, gz = 0.f;
-  if (g < RN && (long long)ptr[RN] <= cap_e) {
+  if (gr) {  // scatter schedule: grad_r accumulated by atomics in the edge kernels
+    if (g < RN && lane == 0) {
+      const float4 v = gr[g];
+      gx = v.x; gy = v.y; gz = v.z;
+    }
+  } else if (g < RN && (long long)ptr[RN] <= cap_e) {
     const int k1 = ptr[g + 1];
     for (int k0 = ptr[g] + lane; k0 < k1; k0 += 4 * FF_LPN) {
       int r[4];
@@ -603,15 +609,16 @@ __device__ __forceinline__ void replica_energy(const float *per_atom, int N, flo
 // Forces and replica energies in one launch (independent outputs): blocks
 // [0, nff) run forces_node, the last R blocks replica_energy.
 __global__ void __launch_bounds__(256)
-k_forces_finish(const int32_t *ptr, const int32_t *rev, const float4 *gsum, int N, int RN,
+k_forces_finish(const int32_t *ptr, const int32_t *rev, const float4 *gsum, const float4 *gr,
+                int N, int RN,
                 int64_t cap_e, const float *f_extra, float *forces, fcg_md_params kick,
                 int do_kick, const float *mass, float *vel, int64_t *status, const int64_t *step,
                 int nff, const float *per_atom, float *energy) {
   pdl_trigger();
   pdl_wait();
   if ((int)blockIdx.x < nff)
-    forces_node(ptr, rev, gsum, N, RN, cap_e, f_extra, forces, kick, do_kick, mass, vel, status,
-                step);
+    forces_node(ptr, rev, gsum, gr, N, RN, cap_e, f_extra, forces, kick, do_kick, mass, vel,
+                status, step);
   else
     replica_energy(per_atom, N, energy, blockIdx.x - nff);
 }
@@ -644,6 +651,7 @@ struct EfBuffers {
   float *X, *H, *G, *GH, *GP;
   float *P[FCG_MAX_BLOCKS], *Zp[FCG_MAX_BLOCKS];
   float4 *gsum;
+  float4 *gr;  // [RN] grad_r of the scatter schedule
   float4 *geo;
   float2 *env;
   int32_t *unit_rows;
@@ -663,6 +671,7 @@ static EfBuffers carve_ef(Carver &c, int T, size_t RN, int64_t cap_e) {
     b.Zp[t] = c.take<float>(rows * D);
   }
   b.gsum = c.take<float4>((size_t)cap_e + 1);
+  b.gr = c.take<float4>(rows);
   b.geo = c.take<float4>((size_t)cap_e + 1);
   b.env = c.take<float2>((size_t)cap_e + 1);
   b.unit_rows = c.take<int32_t>(4096);  // backward partition at 0, forward at 2048
@@ -701,7 +710,7 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
                   const int32_t *own, int64_t cap_e, float *per_atom, float *energy,
                   float *forces, void *ws, size_t ws_bytes, cudaStream_t s,
                   const float *f_extra, const fcg_md_params *kick, const float *mass,
-                  float *vel, int64_t *status, const int64_t *step) {
+                  float *vel, int64_t *status, const int64_t *step, int schedule) {
   if (!m || m->num_blocks < 0 || m->num_blocks > FCG_MAX_BLOCKS) {
     set_error("energy_forces: bad model descriptor");
     return FCG_ERR_ARG;
@@ -726,7 +735,14 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
   const int quant = m->format == FCG_FMT_W16;
   ea.quant = quant;
   ea.dbg = g_dbg_phase;
-  const bool simt = use_simt_edges();
+  if (schedule != FCG_SCHED_SEGRED && schedule != FCG_SCHED_SCATTER) {
+    set_error("energy_forces: unknown schedule");
+    return FCG_ERR_ARG;
+  }
+  // the fused-scatter ablation (flash.py:373-443) runs the 64-edge tcgen05 kernels
+  const bool scatter = schedule == FCG_SCHED_SCATTER;
+  const bool simt = !scatter && use_simt_edges();
+  if (scatter) cudaMemsetAsync(b.gr, 0, sizeof(float4) * (size_t)RN, s);
   const int eg = simt ? 2 * sm_count() : sm_count();
   const EmbedJob ej{m->embedding, types, N, b.X, b.amax, 2 * FCG_MAX_BLOCKS};
   if (simt) {  // the tcgen05 path does the lookup inside k_edge_geom
@@ -759,7 +775,10 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
       if (simt)
         k_edge_fwd<<<eg, NT, (TE * LDR + TE * LDH) * sizeof(float), s>>>(ea, b.P[t], b.H);
       else
-        launch_edge_fwd_tc(ea, b.geo, b.env, b.unit_rows + 2048, b.P[t], b.H, eg, s);
+      {
+        if (scatter) cudaMemsetAsync(b.H, 0, sizeof(float) * (size_t)RN * D, s);
+        launch_edge_fwd_tc(ea, b.geo, b.env, b.unit_rows + 2048, b.P[t], b.H, eg, s, scatter);
+      }
     }
     {
       FCG_PROF(P_NODE_POST, s);
@@ -794,8 +813,11 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
         k_edge_bwd<<<eg, NT, 3 * TE * LDH * sizeof(float), s>>>(ea, b.P[t], b.GH, b.GP, b.gsum,
                                                                t != T - 1);
       else
+      {
+        if (scatter) cudaMemsetAsync(b.GP, 0, sizeof(float) * (size_t)RN * D, s);
         launch_edge_bwd_tc(ea, b.geo, b.env, b.unit_rows, b.P[t], b.GH, b.GP, b.gsum, t != T - 1,
-                           eg, s);
+                           eg, s, scatter ? b.gr : nullptr);
+      }
     }
     {
       FCG_PROF(P_NODE_PRE_BWD, s);
@@ -810,7 +832,8 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
   if (kick) kp = *kick;
   FCG_PROF(P_FORCES, s);
   const int nff = (int)ceil_div((long long)RN * FF_LPN, 256);
-  launch_pdl(PDL_SMALL, k_forces_finish, nff + R, 256, 0, s, ptr, rev, b.gsum, N, RN, cap_e,
+  launch_pdl(PDL_SMALL, k_forces_finish, nff + R, 256, 0, s, ptr, rev, b.gsum,
+             (const float4 *)(scatter ? b.gr : nullptr), N, RN, cap_e,
              f_extra, forces, kp, (int)(kick != nullptr), mass, vel, status, step, nff, per_atom,
              energy);
   return cuda_status("energy_forces");

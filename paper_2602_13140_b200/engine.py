@@ -77,7 +77,7 @@ def default_capacity(R: int, N: int) -> int:
 class MDEngine:
     def __init__(self, params, types, masses, prior, n_replicas: int, dt_fs=4.0,
                  temperature=300.0, friction=1.0, seed=0, neighbor_stride=1, rep_offset=0,
-                 cap_e: int | None = None, device="cuda"):
+                 cap_e: int | None = None, device="cuda", schedule: int = _lib.FCG_SCHED_SEGRED):
         torch = _torch()
         self.torch = torch
         self.lib = _lib.load()
@@ -92,6 +92,10 @@ class MDEngine:
         self.model = DeviceModel(params, self.device)
         self.prior = DevicePrior(prior, N, self.device)
         self.p = md_params(dt_fs, temperature, friction, seed, rep_offset, neighbor_stride)
+        # aggregation schedule of the force evaluation: segment sums (the
+        # product path) or the fused-scatter ablation (include/fcg.h)
+        self.schedule = int(schedule)
+        self.p.schedule = self.schedule
         self.mass = torch.as_tensor(np.asarray(masses, np.float64).astype(np.float32),
                                     device=self.device)
         self.masses64 = np.asarray(masses, np.float64)
@@ -187,10 +191,10 @@ class MDEngine:
         per_atom = torch.empty(self.R * self.N, dtype=torch.float32, device=self.device)
         ef = L.fcg_ef_workspace_bytes(C.byref(self.model.desc), self.R, self.N, c.cap_e)
         ws_ef = torch.empty(int(ef), dtype=torch.uint8, device=self.device)
-        _lib.check(L.fcg_energy_forces(C.byref(self.model.desc), v(self.pos), v(self.types),
-                                       self.R, self.N, v(c.ptr), v(c.nbr), v(c.rev), v(c.own),
-                                       c.cap_e, v(per_atom), v(self.potential), v(self.forces),
-                                       v(ws_ef), ef, self.stream()), "fcg_energy_forces")
+        _lib.check(L.fcg_energy_forces_sched(
+            C.byref(self.model.desc), v(self.pos), v(self.types), self.R, self.N, v(c.ptr),
+            v(c.nbr), v(c.rev), v(c.own), c.cap_e, v(per_atom), v(self.potential), v(self.forces),
+            v(ws_ef), ef, self.schedule, self.stream()), "fcg_energy_forces")
         self.model_forces = self.forces.clone()
         self.forces.add_(f_prior)  # out.forces + f_prior, md.py:266
         self.per_atom = per_atom

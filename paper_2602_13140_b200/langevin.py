@@ -92,6 +92,12 @@ class SimConfig:
         return self.dt_fs * 1.0e-3
 
 
+def _schedule(config: SimConfig) -> int:
+    """Aggregation schedule of a fused backend: segment sums, or atomic
+    scatter for PipelineMode(fused=True, segred=False) (flash.py:373-443)."""
+    return _lib.FCG_SCHED_SEGRED if config.backend.segred else _lib.FCG_SCHED_SCATTER
+
+
 def _require_fp32(config: SimConfig):
     if config.mode != "32bit":
         raise ValueError("the B200 path integrates in fp32 (mode='32bit'); "
@@ -139,7 +145,8 @@ class GpuReplicaForces:
             c = self.config
             self.engine = MDEngine(self.params, self.types, np.full(self.types.size, 1.0),
                                    self.prior, R, c.dt_fs, c.temperature, c.friction, c.seed,
-                                   c.neighbor_stride, device=self.device)
+                                   c.neighbor_stride, device=self.device,
+                                   schedule=_schedule(c))
         return self.engine
 
     def __call__(self, positions, step):
@@ -158,7 +165,8 @@ class GpuReplicaForces:
         counts = ptr[N::N] - ptr[0:-1:N][:R]
         self.edge_counts.extend(int(x) for x in counts)
         for e in counts:
-            self.traffic.merge(io_model_flash_report(N, int(e), self.params))
+            self.traffic.merge(accumulated_traffic(self.config.backend, N, int(e), 1,
+                                                   self.params))
         return forces.astype(positions.dtype, copy=False), info
 
 
@@ -378,7 +386,7 @@ def run_simulation(params, system, config: SimConfig, out_dir, resume_from=None,
     R = pos0.shape[0]
     eng = MDEngine(params, system.types, masses, system.prior, R, config.dt_fs,
                    config.temperature, config.friction, config.seed, config.neighbor_stride,
-                   rep_offset=rep_offset + first)
+                   rep_offset=rep_offset + first, schedule=_schedule(config))
     eng.load_state(pos0, vel0, step0)
 
     traj_path, scal_path = out_dir / "trajectory.xyz", out_dir / "scalars.csv"

@@ -224,6 +224,22 @@ def edge_db_exp(gamma: float, cutoff: float) -> int:
     return _pow2_exp((math.sqrt(2.0 * gamma / math.e) + math.pi / (2.0 * cutoff)) * 1.001)
 
 
+def edge_v_exp(w0: np.ndarray, centers: np.ndarray, gamma: float, cutoff: float) -> int:
+    """Static scale of v = ssp'(z0) * (W0 db) in the forward-mode backward
+    edge kernel (csrc/edge_tc.cu, k_edge_bwd_fm): 0 < ssp' < 1, so |v[c]| <=
+    max over d of sum_k |W0[c,k]| |db_k(d)| (model.py:136-157), evaluated on
+    a grid 2,000x finer than the basis width (the function moves < 0.5%
+    between points; 5% margin, and the split tolerates 2x before fp16
+    overflows)."""
+    d = np.linspace(0.0, float(cutoff), 30001)
+    delta = d[:, None] - np.asarray(centers, np.float64)[None, :]
+    env = 0.5 * (np.cos(np.pi * d / cutoff) + 1.0)
+    denv = -0.5 * np.pi / cutoff * np.sin(np.pi * d / cutoff)
+    db = np.exp(-gamma * delta * delta) * (-2.0 * gamma * delta * env[:, None] + denv[:, None])
+    bound = float(np.max(np.abs(db) @ np.abs(w0.astype(np.float64)).T))
+    return _pow2_exp(bound * 1.05)
+
+
 def _is_quantized(params) -> bool:
     return not isinstance(params.readout, tuple)
 
@@ -309,6 +325,8 @@ class DeviceModel:
             blk.f_hexp = edge_h_exp(w0, b0)
             blk.f_dbexp = edge_db_exp(float(np.float32(params.rbf.gamma)), float(cfg.cutoff))
             blk.f1_qmax = 1.0 if isinstance(f1, tuple) else float(np.max(f1.scale))
+            blk.f_vexp = edge_v_exp(w0, params.rbf.centers, float(params.rbf.gamma),
+                                    float(cfg.cutoff))
 
         r0, r1 = layers_of(params.readout)
         img, e = image_of(r0, (RH, D))

@@ -7,9 +7,11 @@ cuda:0 (fp32, the reference's production precision).  PipelineMode's
 ablation flags pick the schedule as in the reference: fused=False runs the
 materialising schedule on the GPU (ablation.py: stacked edge tensors,
 atomic scatter-add or segmented reduction, autodiff forces — the paper's
-CGSchNet baseline) in the input dtype; fused=True runs the fused kernels
-on fp32 inputs (fp64 inputs take the dtype-honouring materialised schedule
-so results keep the input precision, as the reference's do).  Every mode
+CGSchNet baseline) in the input dtype; fused=True runs the fused tcgen05
+kernels on fp32 inputs, aggregating with segment sums (segred=True) or
+atomic scatter-adds (segred=False, the fused-scatter ablation); fp64 inputs
+take the dtype-honouring materialised schedule so results keep the input
+precision, as the reference's do.  Every mode
 reports the reference's modelled traffic for its schedule (traffic_report).
 """
 
@@ -234,7 +236,7 @@ class _Evaluator:
         self.dm = DeviceModel(params)
         self.lib = _lib.load()
 
-    def __call__(self, pos32: np.ndarray, types: np.ndarray, csr):
+    def __call__(self, pos32: np.ndarray, types: np.ndarray, csr, schedule: int = 0):
         torch, lib, v = self.torch, self.lib, _lib.vp
         ptr, nbr, rev, own = csr
         N = pos32.shape[0]
@@ -252,11 +254,10 @@ class _Evaluator:
         forces = torch.empty(N, 3, dtype=torch.float32, device=dev)
         nb = lib.fcg_ef_workspace_bytes(C.byref(self.dm.desc), 1, N, cap)
         ws = torch.empty(int(nb), dtype=torch.uint8, device=dev)
-        _lib.check(lib.fcg_energy_forces(C.byref(self.dm.desc), v(dpos), v(dtypes), 1, N,
-                                         v(dptr), v(dnbr), v(drev), v(down), cap, v(per_atom),
-                                         v(energy), v(forces), v(ws), nb,
-                                         C.c_void_p(torch.cuda.current_stream().cuda_stream)),
-                   "fcg_energy_forces")
+        _lib.check(lib.fcg_energy_forces_sched(
+            C.byref(self.dm.desc), v(dpos), v(dtypes), 1, N, v(dptr), v(dnbr), v(drev), v(down),
+            cap, v(per_atom), v(energy), v(forces), v(ws), nb, schedule,
+            C.c_void_p(torch.cuda.current_stream().cuda_stream)), "fcg_energy_forces")
         return float(energy.item()), per_atom.cpu().numpy(), forces.cpu().numpy()
 
 
@@ -316,7 +317,11 @@ def flash_energy_forces(positions, types, params, mode: PipelineMode = PipelineM
         return EnergyForces(energy=float(e[0].item()), per_atom=pa.cpu().numpy(),
                             forces=f.cpu().numpy().astype(positions.dtype, copy=False),
                             traffic=traffic)
-    energy, per_atom, forces = _evaluator(params)(positions.astype(np.float32), types, csr)
+    # fused: segment sums (the product path) or, for segred=False, the
+    # fused-scatter ablation with atomic aggregation (flash.py:373-443)
+    schedule = _lib.FCG_SCHED_SEGRED if mode.segred else _lib.FCG_SCHED_SCATTER
+    energy, per_atom, forces = _evaluator(params)(positions.astype(np.float32), types, csr,
+                                                  schedule)
     return EnergyForces(energy=energy, per_atom=per_atom,
                         forces=forces.astype(positions.dtype, copy=False), traffic=traffic)
 

@@ -221,6 +221,20 @@ def test_pipeline_mode_ablations(golden, name, fused, segred):
     assert (out.traffic.atomic_updates > 0) == (not segred and E > 0)
 
 
+def test_run_simulation_fused_scatter_backend(tmp_path, golden):
+    # the engine under PipelineMode(fused=True, segred=False): atomic
+    # aggregation, same trajectory within fp32 round-off
+    c = golden["md"].case("traj_tiny")
+    n, sseed, pseed, R, steps = (int(x) for x in c["meta"])
+    sysm = generate_system("coil", n, sseed)
+    params = init_params(ModelConfig(**json.loads(str(c["cfg"]))), pseed)
+    sim = P.SimConfig(dt_fs=4.0, temperature=300.0, friction=1.0, n_steps=steps, n_replicas=R,
+                      seed=9, output_stride=5, backend=P.PipelineMode(segred=False))
+    res = P.run_simulation(params, sysm, sim, tmp_path)
+    assert np.max(np.abs(res.final_state.positions - c["pos"])) <= 1e-5
+    assert res.traffic.atomic_updates > 0
+
+
 def test_energy_forces_given_neighbor_list(golden):
     c = golden["flash"].case("star")
     params = params_for(c)
