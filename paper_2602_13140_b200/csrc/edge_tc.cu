@@ -154,6 +154,14 @@ struct SegSum {
     const int cur = own[lane];
     return __ballot_sync(0xffffffffu, cur != (lane ? own[lane - 1] : row));
   }
+  // starts() for a tile whose slots from n_e on are padding: they never
+  // start a row (their messages are zero).
+  __device__ __forceinline__ unsigned starts_n(const int *own, int n_e) const {
+    const int lane = threadIdx.x & 31;
+    const int cur = own[lane];
+    return __ballot_sync(0xffffffffu,
+                         lane < n_e && cur != (lane ? own[lane - 1] : row));
+  }
   __device__ __forceinline__ void half(const int *own, const float (&m)[16], int h,
                                        unsigned st) {
     const unsigned hb = (st >> h) & 0xffffu;
@@ -327,6 +335,24 @@ struct Wctx {
   // reads of the columns the GEMM overwrites are done.  True (warp-uniform)
   // for the last of the group's four warps to arrive: that warp issues (one
   // elected lane per instruction).
+  // arrive() with the request counters passed explicitly (kernels whose
+  // shared layout is not TcShared)
+  __device__ __forceinline__ bool arrive_fm(unsigned int *req, int kind) const {
+    tc::fence_async_smem();
+    tc::fence_before_sync();
+    __syncwarp();
+    unsigned int old = 0u;
+    if (lane == 0) {
+      __threadfence_block();
+      old = atomicAdd(&req[kind], 1u);
+    }
+    const bool last = (__shfl_sync(0xffffffffu, old, 0) & amask) == amask;  // warp-uniform
+    if (last) {
+      __threadfence_block();
+      tc::fence_after_sync();
+    }
+    return last;
+  }
   __device__ __forceinline__ bool arrive(int kind) const {
     tc::fence_async_smem();
     tc::fence_before_sync();
@@ -1350,10 +1376,58 @@ constexpr uint32_t FM_BB = 2 * DR * 128 * 2;                  // [b | db] hi|lo:
 constexpr uint32_t FM_HV = 2 * D * 128 * 2;                   // [h | v] hi|lo: 64 KB
 constexpr uint32_t FM_GBUF = FM_BB + FM_HV;
 constexpr uint32_t FM_SM_META = 2 * FM_GBUF;
-constexpr uint32_t FM_SM_TOTAL = FM_SM_META + sizeof(TcShared);
+constexpr int FM_MBUF = 3;  // metadata buffers per work unit (tiles it, it+1, it+2)
+
+// Tile metadata of one work unit, shared by its four warps and filled by
+// cp.async (no registers in flight): raw CSR columns of the tile's edges.
+// Slots past the unit's edge count keep values of an earlier tile (zero at
+// start) — valid indices and finite geometry; every consumer masks them.
+struct UnitMeta {
+  int own[TT], nbr[TT];
+  float d[TT], env[TT], denv[TT];
+};
+struct FmShared {
+  UnitMeta um[4][FM_MBUF];
+  float xg[4][2][4][TT];     // per-quarter partial grad_d (double-buffered)
+  uint64_t bar[2][4];        // GEMM completion per group, per kind
+  uint64_t xbar[4];          // the four partial grad_d rows of a unit's tile are written
+  uint64_t mbar[4][FM_MBUF]; // a metadata buffer's copies landed (128 noinc arrivals)
+  uint64_t wbar;             // weight images landed
+  unsigned int req[2][4];    // operand arrivals per GEMM kind
+  uint32_t tmem;
+};
+constexpr uint32_t FM_SM_TOTAL = FM_SM_META + sizeof(FmShared);
 static_assert(SM_W1 + 2 * W1_BYTES <= FM_SM_META, "weight staging aliases the group buffers");
 static_assert(FM_SM_TOTAL + 1024 <= 232448, "forward-mode backward shared memory budget");
 static_assert(FM_TW0 + DR <= 512, "TMEM budget");
+
+__device__ __forceinline__ void cp_async4(void *dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(tc::smem_u32(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t *bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(tc::smem_u32(bar))
+               : "memory");
+}
+
+// Copies of tile columns [t0, t0+count) into a unit buffer: warp quarter q
+// moves one or two of the five columns, one element per lane; every thread
+// of the unit's four warps then arrives (noinc) on the buffer's mbarrier.
+__device__ __forceinline__ void meta_issue(const EdgeArgs &a, const float4 *geo, const float2 *env,
+                                           UnitMeta *m, uint64_t *bar, int t0, int count, int q,
+                                           int lane) {
+  if (lane < count) {
+    const int k = t0 + lane;
+    if (q == 0) cp_async4(&m->own[lane], &a.own[k]);
+    else if (q == 1) cp_async4(&m->nbr[lane], &a.nbr[k]);
+    else if (q == 2) cp_async4(&m->d[lane], &geo[k].w);
+    else {
+      cp_async4(&m->env[lane], &env[k].x);
+      cp_async4(&m->denv[lane], &env[k].y);
+    }
+  }
+  cp_async_arrive_noinc(bar);
+}
 
 // W1 hi | lo and W0 hi | lo from the staged images into TMEM: warp w moves
 // image (w / 4) % 4 for its lane quarter.
@@ -1387,6 +1461,16 @@ __device__ __forceinline__ void mma_pair_ts(uint32_t d, uint32_t a_hi, uint32_t 
   }
 }
 
+// Basis [b | db] of one tile from a unit buffer into the group's K=64 operand.
+template <bool Q>
+__device__ __forceinline__ void tile_basis_pair(const EdgeArgs &a, Wctx &W, const UnitMeta *m,
+                                                float bsc, float dbsc) {
+  tile_basis<false, Q, KSTR128>(a, W, (const WarpMeta *)m, bsc);
+  W.eo += 64;
+  tile_basis<true, Q, KSTR128>(a, W, (const WarpMeta *)m, dbsc);
+  W.eo -= 64;
+}
+
 template <bool Q>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_edge_bwd_fm(const EdgeArgs a, const float4 *geo, const float2 *env,
@@ -1394,23 +1478,51 @@ k_edge_bwd_fm(const EdgeArgs a, const float4 *geo, const float2 *env,
               const float *GH, float *GP, float4 *gsum,
               int accumulate) {
   extern __shared__ __align__(1024) uint8_t sm[];
-  TcShared *sh = (TcShared *)(sm + FM_SM_META);
+  FmShared *sh = (FmShared *)(sm + FM_SM_META);
   const fcg_block &B = a.blk;
   pdl_trigger();
-  kernel_prologue(sm, sh, B, NGRP);  // bar[0..1] per group, xbar[0..3] per unit
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&sh->wbar, 1);
+    tc::fence_mbar_init();
+    tc::mbar_expect_tx(&sh->wbar, 2 * W0_BYTES + 2 * W1_BYTES);
+    tc::bulk_g2s(sm + SM_W0, B.f0_img, 2 * W0_BYTES, &sh->wbar);
+    tc::bulk_g2s(sm + SM_W1, B.f1_img, 2 * W1_BYTES, &sh->wbar);
+  }
+  if (threadIdx.x < 4) {
+    const int u0 = threadIdx.x;
+    if (u0 < 2) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        tc::mbar_init(&sh->bar[u0][i], 1);
+        sh->req[u0][i] = 0u;
+      }
+    }
+    tc::mbar_init(&sh->xbar[u0], 4);
+#pragma unroll
+    for (int b = 0; b < FM_MBUF; ++b) tc::mbar_init(&sh->mbar[u0][b], 128);
+    tc::fence_mbar_init();
+  }
+  for (int i = threadIdx.x; i < (int)(sizeof(sh->um) / 4); i += blockDim.x)
+    ((int *)sh->um)[i] = 0;
+  if (threadIdx.x < 32) tc::tmem_alloc<512>(&sh->tmem);
+  tc::fence_async_smem();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
   tc::mbar_wait(&sh->wbar, 0);
   load_fm_weights_tmem(sm, sh->tmem);  // ends with the PDL wait
+
   Wctx W;
   W.w = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   W.g = W.w >> 3;
   const int hf = (W.w >> 2) & 1;
-  const int u = 2 * W.g + hf;  // work unit / grad_d partials of this warp
+  const int u = 2 * W.g + hf;  // work unit / metadata / grad_d partials of this warp
   W.q = W.w & 3;
   W.lane = threadIdx.x & 31;
   W.ch = 32 * W.q + W.lane;
   W.eo = 32 * hf;
   W.amask = 7u;
-  W.sh = sh;
+  W.sh = (TcShared *)nullptr;
   W.bb = sm + W.g * FM_GBUF;
   W.hb = W.bb + FM_BB;
   W.sbb = tc::smem_u32(W.bb);
@@ -1427,6 +1539,7 @@ k_edge_bwd_fm(const EdgeArgs a, const float4 *geo, const float2 *env,
   const int ntiles = (tr.ee - tr.eb + TT - 1) / TT;
   const int nt_all = max(ntiles, (to.ee - to.eb + TT - 1) / TT);  // the group's iterations
   const int ch = W.ch;
+  const int lane = W.lane;
   const float *GHch = opaque_ptr(GH + ch);
   const float *Pch = opaque_ptr(P + ch);
   SegSum seg;
@@ -1447,33 +1560,34 @@ k_edge_bwd_fm(const EdgeArgs a, const float4 *geo, const float2 *env,
   const float b1c = ld_dep(&B.f1_b[ch]);
   const float s1 = Q ? ld_dep(&B.f1_s[ch]) : pow2f(-(B.f1_exp + B.f_hexp));
   const float ku = Q ? ld_dep(&B.f1_s[ch]) * pow2f(-B.f_vexp) : pow2f(-(B.f1_exp + B.f_vexp));
-  const float bsc = Q ? 0.f : 14.f;
+  const float bsc = Q ? 0.f : 14.f, dbsc = (float)B.f_dbexp;
+  auto count_of = [&](int t) { return min(TT, tr.ee - (tr.eb + t * TT)); };
+  auto um = [&](int t) { return &sh->um[u][t % FM_MBUF]; };
+  auto meta_wait = [&](int t) {
+    tc::mbar_wait(&sh->mbar[u][t % FM_MBUF], (uint32_t)((t / FM_MBUF) & 1));
+  };
 
-  float4 ue = make_float4(0.f, 0.f, 0.f, 0.f), ue_n = ue;
-  bool rows3 = true, rows3_n = true;
-  int mid = 0, mid_n = 0;
-  MetaRegs mr;
-  if (nt_all > 0) {  // tile 0 (possibly empty for this half): metadata, [b | db], G1 | G1'
-    mr.load(a, geo, env, tr.eb, min(TT, tr.ee - tr.eb), W.lane);
-    ue_n = mr.store3(W.meta(0), true, W.lane, rows3_n, mid_n);
-    mr.load(a, geo, env, tr.eb + TT, min(TT, tr.ee - tr.eb - TT), W.lane);
-    tile_basis<false, Q, KSTR128>(a, W, W.meta(0), bsc);
-    W.eo += 64;
-    tile_basis<true, false, KSTR128>(a, W, W.meta(0), (float)B.f_dbexp);
-    W.eo -= 64;
-    REQ(BAR_G1, (mma_pair_ts<DR / 16, NB, NDB>(W.tmem_g, w0h, w0l, bb)));
+  if (nt_all > 0) {  // tiles 0 and 1 in flight; tile 0's [b | db] and G1 | G1'
+    meta_issue(a, geo, env, um(0), &sh->mbar[u][0], tr.eb, count_of(0), W.q, lane);
+    if (nt_all > 1)
+      meta_issue(a, geo, env, um(1), &sh->mbar[u][1], tr.eb + TT, count_of(1), W.q, lane);
+    meta_wait(0);
+    tile_basis_pair<Q>(a, W, um(0), bsc, dbsc);
+    if (W.arrive_fm(sh->req[W.g], BAR_G1)) {
+      mma_pair_ts<DR / 16, NB, NDB>(W.tmem_g, w0h, w0l, bb);
+      tc::mma_commit_warp(&sh->bar[W.g][BAR_G1]);
+    }
+    __syncwarp();
   }
   for (int it = 0; it < nt_all; ++it) {
-    ue = ue_n;
-    rows3 = rows3_n;
-    mid = mid_n;
     const int t0 = tr.eb + it * TT;
     const bool more = it + 1 < nt_all;
-    const WarpMeta *M = W.meta(it);
-    const int n_e = min(TT, tr.ee - t0);  // <= 0: this half has no tile this iteration
+    const UnitMeta *M = um(it);
+    const int n_e = count_of(it);  // <= 0: this half has no tile this iteration
 
     // ---- E1: h = ssp(z0), v = ssp'(z0) dz0 -> [h | v] -----------------------
-    W.wait(BAR_G1, it);
+    tc::mbar_wait(&sh->bar[W.g][BAR_G1], (uint32_t)(it & 1));
+    tc::fence_after_sync();
 #pragma unroll
     for (int c0 = 0; c0 < TT; c0 += 16) {
       float z[16], dz[16];
@@ -1498,38 +1612,51 @@ k_edge_bwd_fm(const EdgeArgs a, const float4 *geo, const float2 *env,
         put8<true, KSTR128>(W.hb, D, ch, 64 + W.eo + c0 + j, &dz[j], 1.f);
       }
     }
-    REQ(BAR_G2, (mma_pair_ts<D / 16, NH, NV>(W.tmem_g, w1h, w1l, hb)));
+    if (W.arrive_fm(sh->req[W.g], BAR_G2)) {
+      mma_pair_ts<D / 16, NH, NV>(W.tmem_g, w1h, w1l, hb);
+      tc::mma_commit_warp(&sh->bar[W.g][BAR_G2]);
+    }
+    __syncwarp();
 
     // ---- gathers of this tile (consumed after the [G2 | G3] wait) ------------
     float gh[TT];
     float pf = 0.f, pm = 0.f, pl = 0.f;  // P[src] of the first, middle and last row
     int o_f = -1, o_l = -1;
+    bool rows3 = true;
+    float4 ue = make_float4(0.f, 0.f, 0.f, 0.f);
     if (n_e > 0) {
-#pragma unroll
-      for (int i = 0; i < TT; ++i) gh[i] = ld_gather(GHch + (uint32_t)M->nbr[i]);
+      const int o = M->own[lane];
       o_f = M->own[0];
       o_l = M->own[n_e - 1];
+      const unsigned other = __ballot_sync(0xffffffffu, lane < n_e && o != o_f && o != o_l);
+      const int mid = other ? __shfl_sync(0xffffffffu, o, __ffs(other) - 1) : o_f;
+      rows3 = __all_sync(0xffffffffu, lane >= n_e || o == o_f || o == o_l || o == mid);
+#pragma unroll
+      for (int i = 0; i < TT; ++i) gh[i] = ld_gather(GHch + ((uint32_t)M->nbr[i] << 7));
       pf = ld_gather(Pch + (uint32_t)o_f * D);
       pm = ld_gather(Pch + (uint32_t)mid * D);
       pl = ld_gather(Pch + (uint32_t)o_l * D);
+      if (W.q == 0 && lane < n_e) ue = ld_dep(&geo[t0 + lane]);
     } else {
 #pragma unroll
       for (int i = 0; i < TT; ++i) gh[i] = 0.f;
     }
-    if (more) {  // next tile's metadata and [b | db] (the basis buffer is free: G1 done)
-      ue_n = mr.store3(W.meta(it + 1), true, W.lane, rows3_n, mid_n);
-      mr.load(a, geo, env, t0 + 2 * TT, min(TT, tr.ee - t0 - 2 * TT), W.lane);
-      tile_basis<false, Q, KSTR128>(a, W, W.meta(it + 1), bsc);
-      W.eo += 64;
-      tile_basis<true, false, KSTR128>(a, W, W.meta(it + 1), (float)B.f_dbexp);
-      W.eo -= 64;
+    if (more) {  // next tile's [b | db] (the basis buffer is free: G1 done)
+      meta_wait(it + 1);
+      tile_basis_pair<Q>(a, W, um(it + 1), bsc, dbsc);
     }
 
     // ---- E2: grad_P segment sums, grad_d partials --------------------------
-    W.wait(BAR_G2, it);
+    tc::mbar_wait(&sh->bar[W.g][BAR_G2], (uint32_t)(it & 1));
+    tc::fence_after_sync();
+    // every warp of the group is past iteration it-1: tile it+2's copies may
+    // reuse the buffer of tile it-1
+    if (it + 2 < nt_all)
+      meta_issue(a, geo, env, um(it + 2), &sh->mbar[u][(it + 2) % FM_MBUF], t0 + 2 * TT,
+                 count_of(it + 2), W.q, lane);
     float q[TT];
     {
-      const unsigned st = n_e > 0 ? seg.starts(M->own) : 0u;
+      const unsigned st = n_e > 0 ? seg.starts_n(M->own, n_e) : 0u;
 #pragma unroll
       for (int h = 0; h < TT; h += 16) {
         float v[16];
@@ -1542,8 +1669,13 @@ k_edge_bwd_fm(const EdgeArgs a, const float4 *geo, const float2 *env,
       }
       tc::tmem_ld32w(W.tl + 64, q);  // u accumulator
     }
-    if (more)  // TMEM columns read: the next tile's G1 | G1' may overwrite them
-      REQ(BAR_G1, (mma_pair_ts<DR / 16, NB, NDB>(W.tmem_g, w0h, w0l, bb)));
+    if (more) {  // TMEM columns read: the next tile's G1 | G1' may overwrite them
+      if (W.arrive_fm(sh->req[W.g], BAR_G1)) {
+        mma_pair_ts<DR / 16, NB, NDB>(W.tmem_g, w0h, w0l, bb);
+        tc::mma_commit_warp(&sh->bar[W.g][BAR_G1]);
+      }
+      __syncwarp();
+    }
     if (rows3) {
 #pragma unroll
       for (int j = 0; j < TT; j += 4) {
@@ -1553,22 +1685,23 @@ k_edge_bwd_fm(const EdgeArgs a, const float4 *geo, const float2 *env,
         for (int i = 0; i < 4; ++i)
           q[j + i] *= gh[j + i] * (oo[i] == o_l ? pl : (oo[i] == o_f ? pf : pm)) * ku;
       }
-    } else {  // four or more rows (~5% of tiles): per-edge gathers
+    } else {  // four or more rows (~5% of coil-269 tiles): per-edge gathers
 #pragma unroll
       for (int i = 0; i < TT; ++i)
         q[i] *= gh[i] * ld_gather(Pch + (uint32_t)M->own[i] * D) * ku;
     }
     float *xg = &sh->xg[u][it & 1][0][0];
-    xg[W.q * TT + W.lane] = warp_edge_sum(q, W.lane);
+    xg[W.q * TT + lane] = warp_edge_sum(q, lane);
     __syncwarp();
-    if (W.lane == 0) tc::mbar_arrive(&sh->xbar[u]);
+    if (lane == 0) tc::mbar_arrive(&sh->xbar[u]);
     if (W.q == 0) {
       tc::mbar_wait(&sh->xbar[u], (uint32_t)(it & 1));
-      const int e = W.lane;
+      const int e = lane;
       if (e < n_e) {
         const float gd = ((xg[e] + xg[TT + e]) + xg[2 * TT + e]) + xg[3 * TT + e];
+        // backward edge: dst = nbr, src = own, u = r_nbr - r_own (flash.py:279)
         const float inv = ue.w > TINY_DISTANCE ? 1.f / ue.w : 0.f;
-        const float sc = gd * inv;
+        const float sc = -gd * inv;
         float4 g = make_float4(sc * ue.x, sc * ue.y, sc * ue.z, 0.f);
         float4 *dst = &gsum[t0 + e];
         if (accumulate) {
