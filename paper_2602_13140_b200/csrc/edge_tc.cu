@@ -1372,10 +1372,20 @@ k_edge_bwd64(const EdgeArgs a, const float4 *geo, const float2 *env,
 // and the K=128 operand [h | v] (N = 128), hi and lo images.
 constexpr uint32_t FM_TW1 = 256, FM_TW0 = 384;
 constexpr uint32_t KSTR128 = (128 / 8) * 128;                 // bytes per 8 K-rows, N = 128
-constexpr uint32_t FM_BB = 2 * DR * 128 * 2;                  // [b | db] hi|lo: 32 KB
-constexpr uint32_t FM_HV = 2 * D * 128 * 2;                   // [h | v] hi|lo: 64 KB
-constexpr uint32_t FM_GBUF = FM_BB + FM_HV;
-constexpr uint32_t FM_SM_META = 2 * FM_GBUF;
+// Group shape: UPG work units per group (2: two groups of 8 warps, N = 128
+// operands; 1: four groups of 4 warps, N = 64).  Per group: the basis
+// operand [b | db] (K = 64) and [h | v] (K = 128), N = 64 UPG, hi|lo.
+template <int UPG>
+struct FmCfg {
+  static constexpr int NGRP = 4 / UPG;
+  static constexpr uint32_t N = 64u * UPG;          // operand columns: 32 UPG edges x 2
+  static constexpr uint32_t RH = 32u * UPG;         // right half: dz0 / u columns
+  static constexpr uint32_t KS = (N / 8) * 128;     // bytes per 8 K-rows
+  static constexpr uint32_t BB = 2 * DR * N * 2;
+  static constexpr uint32_t HV = 2 * D * N * 2;
+  static constexpr uint32_t GBUF = BB + HV;
+};
+constexpr uint32_t FM_SM_META = 4 * (2 * DR * 64 * 2 + 2 * D * 64 * 2);  // 192 KB either shape
 constexpr int FM_MBUF = 3;  // metadata buffers per work unit (tiles it, it+1, it+2)
 
 // Tile metadata of one work unit, shared by its four warps and filled by
@@ -1389,11 +1399,11 @@ struct UnitMeta {
 struct FmShared {
   UnitMeta um[4][FM_MBUF];
   float xg[4][2][4][TT];     // per-quarter partial grad_d (double-buffered)
-  uint64_t bar[2][4];        // GEMM completion per group, per kind
+  uint64_t bar[4][4];        // GEMM completion per group, per kind
   uint64_t xbar[4];          // the four partial grad_d rows of a unit's tile are written
   uint64_t mbar[4][FM_MBUF]; // a metadata buffer's copies landed (128 noinc arrivals)
   uint64_t wbar;             // weight images landed
-  unsigned int req[2][4];    // operand arrivals per GEMM kind
+  unsigned int req[4][4];    // operand arrivals per GEMM kind
   uint32_t tmem;
 };
 constexpr uint32_t FM_SM_TOTAL = FM_SM_META + sizeof(FmShared);
@@ -1444,34 +1454,35 @@ __device__ __forceinline__ void load_fm_weights_tmem(const uint8_t *sm, uint32_t
   prologue_done();
 }
 
-// One tile's pair of chains into the group's 128 columns: the left half
-// (z0 / w, NPL products) and the right half (dz0 / u, NPR products).  Equal
-// product counts issue one N = 128 chain.
-template <int KS, int NPL, int NPR>
+// One tile's pair of chains into the group's columns: the left half (z0 /
+// w, NPL products) and the right half (dz0 / u, NPR products), N/2 columns
+// each.  Equal product counts issue one chain over both halves.
+template <int KS, int NPL, int NPR, int N>
 __device__ __forceinline__ void mma_pair_ts(uint32_t d, uint32_t a_hi, uint32_t a_lo, Desc b) {
   if (NPL == NPR) {
-    mma_chain_ts<KS, NPL>(d, a_hi, a_lo, b, tc::idesc_f16(128, 128, 0, 1));
+    mma_chain_ts<KS, NPL>(d, a_hi, a_lo, b, tc::idesc_f16(128, N, 0, 1));
   } else {
-    const uint32_t id64 = tc::idesc_f16(128, 64, 0, 1);
-    mma_chain_ts<KS, NPL>(d, a_hi, a_lo, b, id64);
+    const uint32_t idh = tc::idesc_f16(128, N / 2, 0, 1);
+    mma_chain_ts<KS, NPL>(d, a_hi, a_lo, b, idh);
     Desc br = b;
-    br.hi += 1024u / 16u;  // columns 64.. of the N = 128 operand (8 core rows of 128 B)
-    br.lo += 1024u / 16u;
-    mma_chain_ts<KS, NPR>(d + 64, a_hi, a_lo, br, id64);
+    br.hi += (N / 2 / 8) * 128u / 16u;  // columns N/2.. of the operand (core rows of 128 B)
+    br.lo += (N / 2 / 8) * 128u / 16u;
+    mma_chain_ts<KS, NPR>(d + N / 2, a_hi, a_lo, br, idh);
   }
 }
 
 // Basis [b | db] of one tile from a unit buffer into the group's K=64 operand.
-template <bool Q>
+template <bool Q, int UPG>
 __device__ __forceinline__ void tile_basis_pair(const EdgeArgs &a, Wctx &W, const UnitMeta *m,
                                                 float bsc, float dbsc) {
-  tile_basis<false, Q, KSTR128>(a, W, (const WarpMeta *)m, bsc);
-  W.eo += 64;
-  tile_basis<true, Q, KSTR128>(a, W, (const WarpMeta *)m, dbsc);
-  W.eo -= 64;
+  using C = FmCfg<UPG>;
+  tile_basis<false, Q, C::KS>(a, W, (const WarpMeta *)m, bsc);
+  W.eo += C::RH;
+  tile_basis<true, Q, C::KS>(a, W, (const WarpMeta *)m, dbsc);
+  W.eo -= C::RH;
 }
 
-template <bool Q>
+template <bool Q, int UPG>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_edge_bwd_fm(const EdgeArgs a, const float4 *geo, const float2 *env,
               const int32_t *unit_rows, const float *P,
@@ -1488,14 +1499,13 @@ k_edge_bwd_fm(const EdgeArgs a, const float4 *geo, const float2 *env,
     tc::bulk_g2s(sm + SM_W0, B.f0_img, 2 * W0_BYTES, &sh->wbar);
     tc::bulk_g2s(sm + SM_W1, B.f1_img, 2 * W1_BYTES, &sh->wbar);
   }
+  using C = FmCfg<UPG>;
   if (threadIdx.x < 4) {
     const int u0 = threadIdx.x;
-    if (u0 < 2) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        tc::mbar_init(&sh->bar[u0][i], 1);
-        sh->req[u0][i] = 0u;
-      }
+    for (int i = 0; i < 4; ++i) {
+      tc::mbar_init(&sh->bar[u0][i], 1);
+      sh->req[u0][i] = 0u;
     }
     tc::mbar_init(&sh->xbar[u0], 4);
 #pragma unroll
@@ -1514,30 +1524,33 @@ k_edge_bwd_fm(const EdgeArgs a, const float4 *geo, const float2 *env,
 
   Wctx W;
   W.w = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
-  W.g = W.w >> 3;
-  const int hf = (W.w >> 2) & 1;
-  const int u = 2 * W.g + hf;  // work unit / metadata / grad_d partials of this warp
+  W.g = W.w / (4 * UPG);
+  const int hf = UPG == 2 ? (W.w >> 2) & 1 : 0;
+  const int u = UPG * W.g + hf;  // work unit / metadata / grad_d partials of this warp
   W.q = W.w & 3;
   W.lane = threadIdx.x & 31;
   W.ch = 32 * W.q + W.lane;
   W.eo = 32 * hf;
-  W.amask = 7u;
+  W.amask = 4u * UPG - 1u;
   W.sh = (TcShared *)nullptr;
-  W.bb = sm + W.g * FM_GBUF;
-  W.hb = W.bb + FM_BB;
+  W.bb = sm + W.g * C::GBUF;
+  W.hb = W.bb + C::BB;
   W.sbb = tc::smem_u32(W.bb);
   W.shb = tc::smem_u32(W.hb);
-  W.tmem_g = sh->tmem + 128u * W.g;
+  W.tmem_g = sh->tmem + 2u * C::RH * W.g;
   W.tl = W.tmem_g + ((uint32_t)(32 * W.q) << 16) + 32u * hf;
   constexpr int NB = Q ? 1 : 3, NDB = Q ? 2 : 3, NH = Q ? 1 : 3, NV = Q ? 2 : 3;
   const uint32_t w0h = sh->tmem + FM_TW0, w0l = w0h + DR / 2;
   const uint32_t w1h = sh->tmem + FM_TW1, w1l = w1h + D / 2;
-  const Desc bb = adesc<KSTR128>(W.sbb, DR), hb = adesc<KSTR128>(W.shb, D);
+  const Desc bb = adesc<C::KS>(W.sbb, DR), hb = adesc<C::KS>(W.shb, D);
 
   const UnitRange tr = unit_range(a, unit_rows, NGRP * blockIdx.x + u);
-  const UnitRange to = unit_range(a, unit_rows, NGRP * blockIdx.x + (u ^ 1));
   const int ntiles = (tr.ee - tr.eb + TT - 1) / TT;
-  const int nt_all = max(ntiles, (to.ee - to.eb + TT - 1) / TT);  // the group's iterations
+  int nt_all = ntiles;  // the group's iterations
+  if (UPG == 2) {
+    const UnitRange to = unit_range(a, unit_rows, NGRP * blockIdx.x + (u ^ 1));
+    nt_all = max(ntiles, (to.ee - to.eb + TT - 1) / TT);
+  }
   const int ch = W.ch;
   const int lane = W.lane;
   const float *GHch = opaque_ptr(GH + ch);
@@ -1572,9 +1585,9 @@ k_edge_bwd_fm(const EdgeArgs a, const float4 *geo, const float2 *env,
     if (nt_all > 1)
       meta_issue(a, geo, env, um(1), &sh->mbar[u][1], tr.eb + TT, count_of(1), W.q, lane);
     meta_wait(0);
-    tile_basis_pair<Q>(a, W, um(0), bsc, dbsc);
+    tile_basis_pair<Q, UPG>(a, W, um(0), bsc, dbsc);
     if (W.arrive_fm(sh->req[W.g], BAR_G1)) {
-      mma_pair_ts<DR / 16, NB, NDB>(W.tmem_g, w0h, w0l, bb);
+      mma_pair_ts<DR / 16, NB, NDB, C::N>(W.tmem_g, w0h, w0l, bb);
       tc::mma_commit_warp(&sh->bar[W.g][BAR_G1]);
     }
     __syncwarp();
@@ -1592,7 +1605,7 @@ k_edge_bwd_fm(const EdgeArgs a, const float4 *geo, const float2 *env,
     for (int c0 = 0; c0 < TT; c0 += 16) {
       float z[16], dz[16];
       tc::tmem_ld16w(W.tl + c0, z);
-      tc::tmem_ld16w(W.tl + 64 + c0, dz);
+      tc::tmem_ld16w(W.tl + C::RH + c0, dz);
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         float sp;
@@ -1608,12 +1621,12 @@ k_edge_bwd_fm(const EdgeArgs a, const float4 *geo, const float2 *env,
       }
 #pragma unroll
       for (int j = 0; j < 16; j += 8) {
-        put8<!Q, KSTR128>(W.hb, D, ch, W.eo + c0 + j, &z[j], 1.f);
-        put8<true, KSTR128>(W.hb, D, ch, 64 + W.eo + c0 + j, &dz[j], 1.f);
+        put8<!Q, C::KS>(W.hb, D, ch, W.eo + c0 + j, &z[j], 1.f);
+        put8<true, C::KS>(W.hb, D, ch, C::RH + W.eo + c0 + j, &dz[j], 1.f);
       }
     }
     if (W.arrive_fm(sh->req[W.g], BAR_G2)) {
-      mma_pair_ts<D / 16, NH, NV>(W.tmem_g, w1h, w1l, hb);
+      mma_pair_ts<D / 16, NH, NV, C::N>(W.tmem_g, w1h, w1l, hb);
       tc::mma_commit_warp(&sh->bar[W.g][BAR_G2]);
     }
     __syncwarp();
@@ -1643,7 +1656,7 @@ k_edge_bwd_fm(const EdgeArgs a, const float4 *geo, const float2 *env,
     }
     if (more) {  // next tile's [b | db] (the basis buffer is free: G1 done)
       meta_wait(it + 1);
-      tile_basis_pair<Q>(a, W, um(it + 1), bsc, dbsc);
+      tile_basis_pair<Q, UPG>(a, W, um(it + 1), bsc, dbsc);
     }
 
     // ---- E2: grad_P segment sums, grad_d partials --------------------------
@@ -1667,11 +1680,11 @@ k_edge_bwd_fm(const EdgeArgs a, const float4 *geo, const float2 *env,
           seg.half(M->own, v, h, st);
         }
       }
-      tc::tmem_ld32w(W.tl + 64, q);  // u accumulator
+      tc::tmem_ld32w(W.tl + C::RH, q);  // u accumulator
     }
     if (more) {  // TMEM columns read: the next tile's G1 | G1' may overwrite them
       if (W.arrive_fm(sh->req[W.g], BAR_G1)) {
-        mma_pair_ts<DR / 16, NB, NDB>(W.tmem_g, w0h, w0l, bb);
+        mma_pair_ts<DR / 16, NB, NDB, C::N>(W.tmem_g, w0h, w0l, bb);
         tc::mma_commit_warp(&sh->bar[W.g][BAR_G1]);
       }
       __syncwarp();
@@ -1718,6 +1731,15 @@ k_edge_bwd_fm(const EdgeArgs a, const float4 *geo, const float2 *env,
   if (threadIdx.x < 32) tc::tmem_dealloc<512>(sh->tmem);
 }
 
+// FCG_BWD_UPG=1: four groups of 4 warps (one work unit each) instead of two of 8
+static int bwd_fm_upg() {
+  static const int v = [] {
+    const char *e = getenv("FCG_BWD_UPG");
+    return (e && e[0] == '1') ? 1 : 2;
+  }();
+  return v;
+}
+
 static bool bwd_fm_enabled() {
   static const bool on = [] {
     const char *v = getenv("FCG_BWD_FM");
@@ -1748,9 +1770,13 @@ void edge_tc_configure() {
   cudaFuncSetAttribute(k_edge_fwd64<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
   cudaFuncSetAttribute(k_edge_bwd_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_edge_bwd_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_edge_bwd_fm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(k_edge_bwd_fm<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(FM_SM_TOTAL + 1024));
-  cudaFuncSetAttribute(k_edge_bwd_fm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(k_edge_bwd_fm<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(FM_SM_TOTAL + 1024));
+  cudaFuncSetAttribute(k_edge_bwd_fm<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(FM_SM_TOTAL + 1024));
+  cudaFuncSetAttribute(k_edge_bwd_fm<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(FM_SM_TOTAL + 1024));
   cudaFuncSetAttribute(k_edge_bwd64<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_edge_bwd64<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1790,8 +1816,12 @@ void launch_edge_bwd_tc(const EdgeArgs &a, const float4 *geo, const float2 *env,
     launch_pdl(PDL_EDGE_BWD, a.quant ? k_edge_bwd64<true, true> : k_edge_bwd64<false, true>,
                grid, TC_THREADS, SM_TOTAL + 1024, s, a, geo, env, unit_rows, P, GH, GP, gsum,
                accumulate, gr);
+  else if (bwd_fm_enabled() && bwd_fm_upg() == 1)
+    launch_pdl(PDL_EDGE_BWD, a.quant ? k_edge_bwd_fm<true, 1> : k_edge_bwd_fm<false, 1>, grid,
+               TC_THREADS, FM_SM_TOTAL + 1024, s, a, geo, env, unit_rows, P, GH, GP, gsum,
+               accumulate);
   else if (bwd_fm_enabled())
-    launch_pdl(PDL_EDGE_BWD, a.quant ? k_edge_bwd_fm<true> : k_edge_bwd_fm<false>, grid,
+    launch_pdl(PDL_EDGE_BWD, a.quant ? k_edge_bwd_fm<true, 2> : k_edge_bwd_fm<false, 2>, grid,
                TC_THREADS, FM_SM_TOTAL + 1024, s, a, geo, env, unit_rows, P, GH, GP, gsum,
                accumulate);
   else if (bwd64_enabled())
