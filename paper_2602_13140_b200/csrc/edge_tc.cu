@@ -1371,7 +1371,6 @@ k_edge_bwd64(const EdgeArgs a, const float4 *geo, const float2 *env,
 // 384.  Shared memory per group: the K=64 basis operand [b | db] (N = 128)
 // and the K=128 operand [h | v] (N = 128), hi and lo images.
 constexpr uint32_t FM_TW1 = 256, FM_TW0 = 384;
-constexpr uint32_t KSTR128 = (128 / 8) * 128;                 // bytes per 8 K-rows, N = 128
 // Group shape: UPG work units per group (2: two groups of 8 warps, N = 128
 // operands; 1: four groups of 4 warps, N = 64).  Per group: the basis
 // operand [b | db] (K = 64) and [h | v] (K = 128), N = 64 UPG, hi|lo.
@@ -1561,18 +1560,13 @@ k_edge_bwd_fm(const EdgeArgs a, const float4 *geo, const float2 *env,
   seg.outc = opaque_ptr(GP + ch);
 
   // E1 constants (this thread's channel = hidden unit k of filter layer 0)
+  // (the W16 row scales are re-read from L1 where they are used: held
+  // across the loop they cost the kernel its last registers)
   const float b0c = ld_dep(&B.f0_b[ch]);
-  const float rs0 = Q ? ld_dep(&B.f0_s[ch]) : pow2f(-(B.f0_exp + 14));
   const float hs = Q ? 1.f : pow2f(B.f_hexp);
-  const HScale hk(rs0, b0c, hs);
-  // v * 2^f_vexp from the dz0 accumulator (W0 * 2^f0_exp (fp32) or w16 (W16,
-  // row scale s0) times db * 2^f_dbexp)
-  const float kv = Q ? ld_dep(&B.f0_s[ch]) * pow2f(B.f_vexp - B.f_dbexp)
-                     : pow2f(B.f_vexp - B.f0_exp - B.f_dbexp);
+  const HScale hk(Q ? 1.f : pow2f(-(B.f0_exp + 14)), b0c, hs);
   // E2 constants (this thread's channel = output channel c of filter layer 1)
   const float b1c = ld_dep(&B.f1_b[ch]);
-  const float s1 = Q ? ld_dep(&B.f1_s[ch]) : pow2f(-(B.f1_exp + B.f_hexp));
-  const float ku = Q ? ld_dep(&B.f1_s[ch]) * pow2f(-B.f_vexp) : pow2f(-(B.f1_exp + B.f_vexp));
   const float bsc = Q ? 0.f : 14.f, dbsc = (float)B.f_dbexp;
   auto count_of = [&](int t) { return min(TT, tr.ee - (tr.eb + t * TT)); };
   auto um = [&](int t) { return &sh->um[u][t % FM_MBUF]; };
@@ -1599,6 +1593,11 @@ k_edge_bwd_fm(const EdgeArgs a, const float4 *geo, const float2 *env,
     const int n_e = count_of(it);  // <= 0: this half has no tile this iteration
 
     // ---- E1: h = ssp(z0), v = ssp'(z0) dz0 -> [h | v] -----------------------
+    // z0 = acc * rs0 + b0; v * 2^f_vexp from the dz0 accumulator (W0 *
+    // 2^f0_exp (fp32) or w16 (W16, row scale s0) times db * 2^f_dbexp)
+    const float rs0 = Q ? ld_dep(&B.f0_s[ch]) : pow2f(-(B.f0_exp + 14));
+    const float kv = Q ? rs0 * pow2f(B.f_vexp - B.f_dbexp)
+                       : pow2f(B.f_vexp - B.f0_exp - B.f_dbexp);
     tc::mbar_wait(&sh->bar[W.g][BAR_G1], (uint32_t)(it & 1));
     tc::fence_after_sync();
 #pragma unroll
@@ -1660,6 +1659,8 @@ k_edge_bwd_fm(const EdgeArgs a, const float4 *geo, const float2 *env,
     }
 
     // ---- E2: grad_P segment sums, grad_d partials --------------------------
+    const float s1 = Q ? ld_dep(&B.f1_s[ch]) : pow2f(-(B.f1_exp + B.f_hexp));
+    const float ku = Q ? s1 * pow2f(-B.f_vexp) : pow2f(-(B.f1_exp + B.f_vexp));
     tc::mbar_wait(&sh->bar[W.g][BAR_G2], (uint32_t)(it & 1));
     tc::fence_after_sync();
     // every warp of the group is past iteration it-1: tile it+2's copies may

@@ -5,7 +5,7 @@ The generators are host-side input preparation.  They must reproduce the
 reference's coordinates bit for bit because the benchmark stand-in for 1ENH
 is generate_system("coil", 269, 0); the numpy operation
 sequence therefore follows the reference exactly and is pinned by
-tests/test_host_golden.py.
+tests/test_host.py (hash-pinned: test_init_params_bit_identical, test_generate_system_bit_identical, test_quantize_model_bit_identical).
 """
 
 from __future__ import annotations

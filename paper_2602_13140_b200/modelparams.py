@@ -4,7 +4,7 @@ Host-side only: the types and the seeded initialiser are what a caller of
 the reference constructs (model.py:164-459 of the reference); the compute
 (basis, filter MLPs, node MLPs and their backward) runs in libfcg.so.
 `init_params` reproduces the reference's draws bit for bit (pinned by
-tests/test_host_golden.py against fixtures generated from the reference).
+tests/test_host.py (hash-pinned: test_init_params_bit_identical, test_generate_system_bit_identical, test_quantize_model_bit_identical) against fixtures generated from the reference).
 `DeviceModel` packs a parameter set into zero-padded device tensors plus
 the `fcg_model` descriptor the C ABI consumes.
 """

@@ -6,7 +6,7 @@ The GPU consumes these through DeviceModel: fp16 stored weights plus fp32
 per-output-channel scales for the forward, and the fp32 dequantised matrix
 scale[:,None]*fp32(w16) for the backward.  Calibration is a one-off CPU
 step; it reproduces the reference's choice of scales bit for bit (pinned by
-tests/test_host_golden.py) so the C3 benchmark weights are the reference's.
+tests/test_host.py (hash-pinned: test_init_params_bit_identical, test_generate_system_bit_identical, test_quantize_model_bit_identical)) so the C3 benchmark weights are the reference's.
 """
 
 from __future__ import annotations
