@@ -127,6 +127,14 @@ typedef struct {
   const uint16_t *r1_h; float r1_s;        /* W16 only */
   const uint16_t *r0_img;                  /* readout layer 0 image, [2][RH][D] */
   int r0_exp;
+  /* Optional (NULL: computed every step by the pre-linear kernel): block 0's
+   * pre-linear P = X W_pre^T + b of every embedding row, [num_types][D].
+   * X of block 0 is embedding[types] (flash.py:201), which does not depend
+   * on positions, so P_0 is a per-model table the geometry kernel gathers;
+   * pre0_amax = max |table| (an upper bound of max |P_0| for the edge
+   * kernels' operand scales). */
+  const float *pre0_table;
+  float pre0_amax;
 } fcg_model;
 
 /* Library identity. */

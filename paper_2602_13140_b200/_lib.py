@@ -47,6 +47,7 @@ class FcgModel(C.Structure):
         ("r0_w", _f), ("r0_wt", _f), ("r0_b", _f), ("r1_w", _f), ("r1_b", C.c_float),
         ("r0_h", _u16), ("r0_s", _f), ("r1_h", _u16), ("r1_s", C.c_float),
         ("r0_img", _u16), ("r0_exp", C.c_int),
+        ("pre0_table", _f), ("pre0_amax", C.c_float),
     ]
 
 

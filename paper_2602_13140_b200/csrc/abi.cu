@@ -216,10 +216,13 @@ int fcg_md_step(const fcg_model *m, const fcg_prior *pr, const fcg_md_params *p,
   if ((rc = nbr_build(pos, R, N, r_cut, cap_e, ptr, nbr, rev, own, status, ws_nbr, nb, s, step,
                       p->neighbor_stride)))
     return rc;
-  if ((rc = prior_forces(pr, pos, R, N, prior, fprior, s))) return rc;
-  // model forces + prior, blow-up check and the trailing half-kick (md.py:204-205)
+  (void)fprior;
+  // model forces + prior (evaluated inline by the force assembly, which also
+  // sums the prior energies), blow-up check and the trailing half-kick
+  // (md.py:204-205)
   return energy_forces(m, pos, types, R, N, ptr, nbr, rev, own, cap_e, per_atom, potential,
-                       forces, ws_ef, eb, s, fprior, p, mass, vel, status, step, p->schedule);
+                       forces, ws_ef, eb, s, nullptr, p, mass, vel, status, step, p->schedule,
+                       pr, prior);
 }
 
 }  // extern "C"

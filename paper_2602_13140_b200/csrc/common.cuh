@@ -191,7 +191,8 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
                   const int32_t *own, int64_t cap_e, float *per_atom, float *energy,
                   float *forces, void *ws, size_t ws_bytes, cudaStream_t s,
                   const float *f_extra, const fcg_md_params *kick, const float *mass,
-                  float *vel, int64_t *status, const int64_t *step, int schedule = 0);
+                  float *vel, int64_t *status, const int64_t *step, int schedule = 0,
+                  const fcg_prior *prior = nullptr, float *prior_e = nullptr);
 // md.cu
 int normal_noise(uint64_t seed, int rep_offset, const int64_t *step, int R, int N, float *out,
                  cudaStream_t s);
@@ -230,6 +231,9 @@ struct EmbedJob {
   float *X;
   unsigned int *amax;
   int namax;
+  const float *p0_table;  // optional: block 0's pre-linear per type -> P0
+  float *P0;
+  float p0_amax;
 };
 void launch_edge_geom(const EdgeArgs &a, float4 *geo, float2 *env, int32_t *unit_rows,
                       int nunits, int32_t *unit_rows_fwd, int nunits_fwd, const EmbedJob &ej,

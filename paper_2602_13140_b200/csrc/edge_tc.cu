@@ -251,13 +251,17 @@ k_edge_geom(const float *pos, const int32_t *ptr, const int32_t *nbr, const int3
     env[k] = make_float2(c, dc);
   }
   if (ej.X) {  // X = embedding[types] (flash.py:201) and the operand-bound words reset
-    if (blockIdx.x == 0 && (int)threadIdx.x < ej.namax) ej.amax[threadIdx.x] = 0u;
+    if (blockIdx.x == 0 && (int)threadIdx.x < ej.namax)
+      ej.amax[threadIdx.x] = (threadIdx.x == 0 && ej.P0) ? __float_as_uint(ej.p0_amax) : 0u;
     for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
          q < (long long)nrows * (D / 4); q += (long long)gridDim.x * blockDim.x) {
       const long long g = q / (D / 4);
       const int c4 = (int)(q % (D / 4));
       const int t = ld_dep(&ej.types[g % ej.N]);
       *(float4 *)&ej.X[g * D + c4 * 4] = ld_dep((const float4 *)&ej.emb[(size_t)t * D + c4 * 4]);
+      if (ej.P0)  // block 0's pre-linear from the per-type table
+        *(float4 *)&ej.P0[g * D + c4 * 4] =
+            ld_dep((const float4 *)&ej.p0_table[(size_t)t * D + c4 * 4]);
     }
   }
 }

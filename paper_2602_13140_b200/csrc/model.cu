@@ -25,6 +25,7 @@
 #include <stdlib.h>
 
 #include "common.cuh"
+#include "prior.cuh"
 
 namespace fcg {
 
@@ -528,7 +529,8 @@ constexpr int FF_LPN = 8;  // lanes per node in k_forces_finish
 __device__ __forceinline__ void forces_node(const int32_t *ptr, const int32_t *rev,
                                             const float4 *gsum, const float4 *gr, int N,
                                             int RN, int64_t cap_e,
-                                            const float *f_extra, float *forces,
+                                            const float *f_extra, const fcg_prior &pr,
+                                            int use_prior, const float *pos, float *forces,
                                             const fcg_md_params &kick, int do_kick,
                                             const float *mass, float *vel, int64_t *status,
                                             const int64_t *step) {
@@ -575,9 +577,15 @@ __device__ __forceinline__ void forces_node(const int32_t *ptr, const int32_t *r
   float f[3] = {-gx, -gy, -gz};
   bool bad = false;
   const int i = g % N;
+  float fp[3] = {0.f, 0.f, 0.f};
+  if (use_prior) {  // the prior forces of this bead, as k_prior computes them
+    const float3 v = prior_bead_force(pr, pos, N, g);
+    fp[0] = v.x; fp[1] = v.y; fp[2] = v.z;
+  }
 #pragma unroll
   for (int q = 0; q < 3; ++q) {
-    if (f_extra) f[q] = __fadd_rn(f[q], f_extra[(size_t)g * 3 + q]);  // out.forces + f_prior
+    if (use_prior) f[q] = __fadd_rn(f[q], fp[q]);                    // out.forces + f_prior
+    else if (f_extra) f[q] = __fadd_rn(f[q], f_extra[(size_t)g * 3 + q]);
     forces[(size_t)g * 3 + q] = f[q];
     bad |= !(fabsf(f[q]) <= FORCE_BLOWUP_LIMIT);  // catches NaN too
     if (do_kick) {
@@ -607,20 +615,26 @@ __device__ __forceinline__ void replica_energy(const float *per_atom, int N, flo
 }
 
 // Forces and replica energies in one launch (independent outputs): blocks
-// [0, nff) run forces_node, the last R blocks replica_energy.
+// [0, nff) run forces_node, the next R blocks replica_energy, and with a
+// prior (the fused MD step) the last R blocks the prior energies — the
+// prior forces are evaluated inline by forces_node, so the step has no
+// separate prior launch.
 __global__ void __launch_bounds__(256)
 k_forces_finish(const int32_t *ptr, const int32_t *rev, const float4 *gsum, const float4 *gr,
                 int N, int RN,
-                int64_t cap_e, const float *f_extra, float *forces, fcg_md_params kick,
+                int64_t cap_e, const float *f_extra, const fcg_prior pr, int use_prior,
+                const float *pos, float *e_prior, float *forces, fcg_md_params kick,
                 int do_kick, const float *mass, float *vel, int64_t *status, const int64_t *step,
-                int nff, const float *per_atom, float *energy) {
+                int nff, int R, const float *per_atom, float *energy) {
   pdl_trigger();
   pdl_wait();
   if ((int)blockIdx.x < nff)
-    forces_node(ptr, rev, gsum, gr, N, RN, cap_e, f_extra, forces, kick, do_kick, mass, vel,
-                status, step);
-  else
+    forces_node(ptr, rev, gsum, gr, N, RN, cap_e, f_extra, pr, use_prior, pos, forces, kick,
+                do_kick, mass, vel, status, step);
+  else if ((int)blockIdx.x < nff + R)
     replica_energy(per_atom, N, energy, blockIdx.x - nff);
+  else
+    prior_energy(pr, pos, N, e_prior, blockIdx.x - nff - R);
 }
 
 // ---------------------------------------------------------------------------
@@ -710,7 +724,8 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
                   const int32_t *own, int64_t cap_e, float *per_atom, float *energy,
                   float *forces, void *ws, size_t ws_bytes, cudaStream_t s,
                   const float *f_extra, const fcg_md_params *kick, const float *mass,
-                  float *vel, int64_t *status, const int64_t *step, int schedule) {
+                  float *vel, int64_t *status, const int64_t *step, int schedule,
+                  const fcg_prior *prior, float *prior_e) {
   if (!m || m->num_blocks < 0 || m->num_blocks > FCG_MAX_BLOCKS) {
     set_error("energy_forces: bad model descriptor");
     return FCG_ERR_ARG;
@@ -744,7 +759,11 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
   const bool simt = !scatter && use_simt_edges();
   if (scatter) cudaMemsetAsync(b.gr, 0, sizeof(float4) * (size_t)RN, s);
   const int eg = simt ? 2 * sm_count() : sm_count();
-  const EmbedJob ej{m->embedding, types, N, b.X, b.amax, 2 * FCG_MAX_BLOCKS};
+  // block 0's pre-linear comes from the per-type table when the model has
+  // one (tcgen05 path: k_edge_geom gathers it with the embedding)
+  const bool p0_tab = m->pre0_table != nullptr && T > 0;
+  const EmbedJob ej{m->embedding, types, N, b.X, b.amax, 2 * FCG_MAX_BLOCKS,
+                    m->pre0_table, p0_tab ? b.P[0] : nullptr, m->pre0_amax};
   if (simt) {  // the tcgen05 path does the lookup inside k_edge_geom
     FCG_PROF(P_EMBED, s);
     launch_pdl(PDL_SMALL, k_embed, ceil_div((long long)RN * (D / 4), 256), 256, 0, s, m->embedding,
@@ -762,7 +781,7 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
     const fcg_block &blk = m->blocks[t];
     ea.blk = blk;
     ea.amax_pg = b.amax + 2 * t;
-    {
+    if (!(t == 0 && p0_tab && !simt)) {
       FCG_PROF(P_NODE_PRE, s);
       if (simt)
         k_node_linear<true, false><<<node_grid, NT, sm1, s>>>(b.X, blk.pre_wt, blk.pre_b, b.P[t],
@@ -819,7 +838,10 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
                            eg, s, scatter ? b.gr : nullptr);
       }
     }
-    {
+    // grad_X of block 0 (flash.py:300) is the gradient with respect to the
+    // embedding output, which has no position dependence: forces never read
+    // it, so the last pre-linear backward is skipped
+    if (t > 0) {
       FCG_PROF(P_NODE_PRE_BWD, s);
       if (simt)
         k_node_linear<false, true><<<node_grid, NT, sm1, s>>>(b.GP, blk.pre_w, nullptr, b.G, RN, 0);
@@ -832,10 +854,13 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
   if (kick) kp = *kick;
   FCG_PROF(P_FORCES, s);
   const int nff = (int)ceil_div((long long)RN * FF_LPN, 256);
-  launch_pdl(PDL_SMALL, k_forces_finish, nff + R, 256, 0, s, ptr, rev, b.gsum,
-             (const float4 *)(scatter ? b.gr : nullptr), N, RN, cap_e,
-             f_extra, forces, kp, (int)(kick != nullptr), mass, vel, status, step, nff, per_atom,
-             energy);
+  fcg_prior pr{};
+  if (prior) pr = *prior;
+  const int use_prior = prior != nullptr;
+  launch_pdl(PDL_SMALL, k_forces_finish, nff + R + (use_prior ? R : 0), 256, 0, s, ptr, rev,
+             b.gsum, (const float4 *)(scatter ? b.gr : nullptr), N, RN, cap_e, f_extra, pr,
+             use_prior, pos, prior_e, forces, kp, (int)(kick != nullptr), mass, vel, status, step,
+             nff, R, per_atom, energy);
   return cuda_status("energy_forces");
 }
 

@@ -328,6 +328,23 @@ class DeviceModel:
             blk.f_vexp = edge_v_exp(w0, params.rbf.centers, float(params.rbf.gamma),
                                     float(cfg.cutoff))
 
+        # block 0's pre-linear of every embedding row (fcg_model.pre0_table):
+        # X_0 = embedding[types] is position-independent, so P_0 is a table
+        # gathered per step instead of a GEMM (evaluated in fp64 from the
+        # reference's operands, W16: fp16-rounded inputs and dequantised
+        # weights as quantize.py:68-71, then rounded to fp32)
+        if params.blocks:
+            lin0 = params.blocks[0].pre_linear
+            emb = np.asarray(params.embedding, np.float32)
+            if isinstance(lin0, tuple):
+                x, (w, b) = emb.astype(np.float64), (np.asarray(lin0[0]), np.asarray(lin0[1]))
+            else:
+                x = emb.astype(np.float16).astype(np.float64)
+                w, b = lin0.dequant(), np.asarray(lin0.bias)
+            tab = (x @ np.asarray(w, np.float64).T + np.asarray(b, np.float64)).astype(np.float32)
+            m.pre0_table = _lib.fptr(dev(_pad(tab, (m.num_types, D))))
+            m.pre0_amax = float(np.max(np.abs(tab))) if tab.size else 0.0
+
         r0, r1 = layers_of(params.readout)
         img, e = image_of(r0, (RH, D))
         m.r0_img = _lib.u16ptr(dev(img.view(np.int16), torch.int16))
