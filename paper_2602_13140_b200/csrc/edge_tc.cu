@@ -655,6 +655,21 @@ __device__ __forceinline__ float warp_edge_sum(float (&p)[TT], int lane) {
       a.dbg[((kind) * 16 + (it)) * 64 + (ph)] = clock64();                         \
   } while (0)
 
+// Timeline stamps of the 64-edge forward and the forward-mode backward
+// (diagnostic builds only, -DFCG_EDGE_STAMPS; tools/diag_edge_timeline.py):
+// lane 0 of the first warp of each group in CTA 0 records clock64() at phase
+// `ph` of iteration `it` (< 32) into dbg[((kind*2 + group)*32 + it)*16 + ph].
+#ifdef FCG_EDGE_STAMPS
+#define STAMP(kind, grp_first, g, it, ph)                                                  \
+  do {                                                                                    \
+    if (a.dbg && blockIdx.x == 0 && (grp_first) && (threadIdx.x & 31) == 0 && (it) >= 0 && \
+        (it) < 32)                                                                         \
+      a.dbg[(((kind) * 2 + (g)) * 32 + (it)) * 16 + (ph)] = clock64();                     \
+  } while (0)
+#else
+#define STAMP(kind, grp_first, g, it, ph) do { } while (0)
+#endif
+
 struct UnitRange {
   int rbeg, rend, eb, ee;
 };
@@ -1084,9 +1099,13 @@ k_edge_fwd64(const EdgeArgs a, const float4 *geo, const float2 *env,
       mr.store(W.meta(0), false, W.lane, r2);
       mr.load(a, geo, env, tr.eb + TT, min(TT, tr.ee - tr.eb - TT), W.lane);
     } else {
+      STAMP(0, (W.w & 7) == 0, W.g, it, 0);
       W.wait(BAR_G1, it);
+      STAMP(0, (W.w & 7) == 0, W.g, it, 1);
       tile_h<Q, KSTR64>(W, rs0, b0c, hk);
+      STAMP(0, (W.w & 7) == 0, W.g, it, 2);
       REQ(BAR_G2, (mma_chain_ts<D / 16, NP>(W.tmem_g + WS, w1h, w1l, hb, idesc)));
+      STAMP(0, (W.w & 7) == 0, W.g, it, 3);
       if (more) {
         bool r2;
         mr.store(W.meta(it + 1), false, W.lane, r2);
@@ -1097,8 +1116,10 @@ k_edge_fwd64(const EdgeArgs a, const float4 *geo, const float2 *env,
       tile_basis<false, Q, KSTR64>(a, W, W.meta(it + 1), bsc);
       REQ(BAR_G1, (mma_chain_ts<DR / 16, NP>(W.tmem_g + Z0, w0h, w0l, bb, idesc)));
     }
+    STAMP(0, (W.w & 7) == 0, W.g, it, 4);
     if (it >= 0) {
       W.wait(BAR_G2, it);
+      STAMP(0, (W.w & 7) == 0, W.g, it, 5);
       float v[TT];
       tc::tmem_ld32w(W.tl + WS, v);
       const int n_e = min(TT, tr.ee - t0);
@@ -1116,6 +1137,7 @@ k_edge_fwd64(const EdgeArgs a, const float4 *geo, const float2 *env,
         }
       }
     }
+    STAMP(0, (W.w & 7) == 0, W.g, it, 6);
     if (more) {
       const WarpMeta *Mn = W.meta(it + 1);
       if (tr.ee - (t0 + TT) > 0) {
@@ -1123,6 +1145,7 @@ k_edge_fwd64(const EdgeArgs a, const float4 *geo, const float2 *env,
         for (int i = 0; i < TT; ++i) pv[i] = ld_gather(Pch + (uint32_t)Mn->nbr[i]);
       }
     }
+    STAMP(0, (W.w & 7) == 0, W.g, it, 7);
   }
   if (!SC) seg.finish();
   tc::fence_before_sync();
@@ -1602,8 +1625,10 @@ k_edge_bwd_fm(const EdgeArgs a, const float4 *geo, const float2 *env,
     const float rs0 = Q ? ld_dep(&B.f0_s[ch]) : pow2f(-(B.f0_exp + 14));
     const float kv = Q ? rs0 * pow2f(B.f_vexp - B.f_dbexp)
                        : pow2f(B.f_vexp - B.f0_exp - B.f_dbexp);
+    STAMP(1, (W.w & 7) == 0, W.g, it, 0);
     tc::mbar_wait(&sh->bar[W.g][BAR_G1], (uint32_t)(it & 1));
     tc::fence_after_sync();
+    STAMP(1, (W.w & 7) == 0, W.g, it, 1);
 #pragma unroll
     for (int c0 = 0; c0 < TT; c0 += 16) {
       float z[16], dz[16];
@@ -1628,11 +1653,13 @@ k_edge_bwd_fm(const EdgeArgs a, const float4 *geo, const float2 *env,
         put8<true, C::KS>(W.hb, D, ch, C::RH + W.eo + c0 + j, &dz[j], 1.f);
       }
     }
+    STAMP(1, (W.w & 7) == 0, W.g, it, 2);
     if (W.arrive_fm(sh->req[W.g], BAR_G2)) {
       mma_pair_ts<D / 16, NH, NV, C::N>(W.tmem_g, w1h, w1l, hb);
       tc::mma_commit_warp(&sh->bar[W.g][BAR_G2]);
     }
     __syncwarp();
+    STAMP(1, (W.w & 7) == 0, W.g, it, 3);
 
     // ---- gathers of this tile (consumed after the [G2 | G3] wait) ------------
     float gh[TT];
@@ -1665,8 +1692,10 @@ k_edge_bwd_fm(const EdgeArgs a, const float4 *geo, const float2 *env,
     // ---- E2: grad_P segment sums, grad_d partials --------------------------
     const float s1 = Q ? ld_dep(&B.f1_s[ch]) : pow2f(-(B.f1_exp + B.f_hexp));
     const float ku = Q ? s1 * pow2f(-B.f_vexp) : pow2f(-(B.f1_exp + B.f_vexp));
+    STAMP(1, (W.w & 7) == 0, W.g, it, 4);
     tc::mbar_wait(&sh->bar[W.g][BAR_G2], (uint32_t)(it & 1));
     tc::fence_after_sync();
+    STAMP(1, (W.w & 7) == 0, W.g, it, 5);
     // every warp of the group is past iteration it-1: tile it+2's copies may
     // reuse the buffer of tile it-1
     if (it + 2 < nt_all)
@@ -1687,6 +1716,7 @@ k_edge_bwd_fm(const EdgeArgs a, const float4 *geo, const float2 *env,
       }
       tc::tmem_ld32w(W.tl + C::RH, q);  // u accumulator
     }
+    STAMP(1, (W.w & 7) == 0, W.g, it, 6);
     if (more) {  // TMEM columns read: the next tile's G1 | G1' may overwrite them
       if (W.arrive_fm(sh->req[W.g], BAR_G1)) {
         mma_pair_ts<DR / 16, NB, NDB, C::N>(W.tmem_g, w0h, w0l, bb);
@@ -1708,6 +1738,7 @@ k_edge_bwd_fm(const EdgeArgs a, const float4 *geo, const float2 *env,
       for (int i = 0; i < TT; ++i)
         q[i] *= gh[i] * ld_gather(Pch + (uint32_t)M->own[i] * D) * ku;
     }
+    STAMP(1, (W.w & 7) == 0, W.g, it, 7);
     float *xg = &sh->xg[u][it & 1][0][0];
     xg[W.q * TT + lane] = warp_edge_sum(q, lane);
     __syncwarp();
@@ -1729,6 +1760,7 @@ k_edge_bwd_fm(const EdgeArgs a, const float4 *geo, const float2 *env,
         *dst = g;
       }
     }
+    STAMP(1, (W.w & 7) == 0, W.g, it, 8);
   }
   seg.finish();
   tc::fence_before_sync();
