@@ -1636,16 +1636,16 @@ k_edge_bwd_fm(const EdgeArgs a, const float4 *geo, const float2 *env,
       tc::tmem_ld16w(W.tl + C::RH + c0, dz);
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
-        float sp;
+        float sp;  // kv * ssp'(z0)
         if (Q) {
           const float zz = z[i] * rs0 + b0c;
-          sp = sigmoid_fast(zz);
+          sp = sigmoid_fast(zz) * kv;
           z[i] = __half2float(__float2half_rn(ssp_fast(zz)));
         } else {
           z[i] = ssp_scaled(z[i] * hk.rs + hk.b, hk.c_ln2, hk.c_e);  // hs * h
-          sp = fmaf(-0.5f, ex2_ftz(z[i] * hk.c_e), 1.f);             // 1 - e^-h / 2
+          sp = fmaf(-0.5f * kv, ex2_ftz(z[i] * hk.c_e), kv);         // kv (1 - e^-h / 2)
         }
-        dz[i] = sp * dz[i] * kv;
+        dz[i] *= sp;
       }
 #pragma unroll
       for (int j = 0; j < 16; j += 8) {
@@ -1676,7 +1676,7 @@ k_edge_bwd_fm(const EdgeArgs a, const float4 *geo, const float2 *env,
       rows3 = __all_sync(0xffffffffu, lane >= n_e || o == o_f || o == o_l || o == mid);
 #pragma unroll
       for (int i = 0; i < TT; ++i) gh[i] = ld_gather(GHch + ((uint32_t)M->nbr[i] << 7));
-      pf = ld_gather(Pch + (uint32_t)o_f * D);
+      pf = ld_gather(Pch + (uint32_t)o_f * D);  // scaled by ku where used
       pm = ld_gather(Pch + (uint32_t)mid * D);
       pl = ld_gather(Pch + (uint32_t)o_l * D);
       if (W.q == 0 && lane < n_e) ue = ld_dep(&geo[t0 + lane]);
@@ -1725,13 +1725,14 @@ k_edge_bwd_fm(const EdgeArgs a, const float4 *geo, const float2 *env,
       __syncwarp();
     }
     if (rows3) {
+      pf *= ku; pm *= ku; pl *= ku;
 #pragma unroll
       for (int j = 0; j < TT; j += 4) {
         const int4 o4 = *(const int4 *)&M->own[j];
         const int oo[4] = {o4.x, o4.y, o4.z, o4.w};
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          q[j + i] *= gh[j + i] * (oo[i] == o_l ? pl : (oo[i] == o_f ? pf : pm)) * ku;
+          q[j + i] *= gh[j + i] * (oo[i] == o_l ? pl : (oo[i] == o_f ? pf : pm));
       }
     } else {  // four or more rows (~5% of coil-269 tiles): per-edge gathers
 #pragma unroll

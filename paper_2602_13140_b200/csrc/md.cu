@@ -176,9 +176,9 @@ k_normal_noise(uint64_t seed, int rep_offset, const int64_t *__restrict__ stepp,
 // The noise of a step depends only on (seed, replica, step) (md.py:127-131),
 // so the MD step generates it NOISE_RING steps at a time (R x NOISE_RING
 // warps instead of R) into a workspace ring.  A device tag {magic, seed,
-// rep_offset, base step} says which steps the ring holds; the three kernels
-// of the leading half-step all evaluate ring_valid() on the same tag, and
-// only the last of them (step_advance) rewrites it, so they always agree.
+// rep_offset, base step} says which steps the ring holds; the two kernels
+// of the leading half-step (noise + BAOA, step advance) evaluate
+// ring_valid() on the same tag, and only the step advance rewrites it.
 struct NoiseTag {
   uint64_t magic, seed;
   int64_t rep_offset, base, layout;  // layout = R * 2^32 + 3N
@@ -190,19 +190,6 @@ __device__ __forceinline__ bool ring_valid(const NoiseTag *t, uint64_t seed, int
          t->layout == layout && step >= t->base && step < t->base + NOISE_RING;
 }
 
-__global__ void __launch_bounds__(256)
-k_noise_ring(uint64_t seed, int rep_offset, const int64_t *stepp, int R, int n3,
-             const NoiseTag *tag, float *ring) {
-  pdl_trigger();
-  pdl_wait();
-  const int64_t step = *stepp;
-  if (ring_valid(tag, seed, rep_offset, ((int64_t)R << 32) + n3, step)) return;
-  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (warp >= R * NOISE_RING) return;
-  const int j = warp / R, r = warp % R;
-  noise_stream(seed, (uint64_t)(rep_offset + r), (uint64_t)(step + j), n3,
-               ring + ((size_t)j * R + r) * n3, lane);
-}
 
 int normal_noise(uint64_t seed, int rep_offset, const int64_t *step, int R, int N, float *out,
                  cudaStream_t s) {
@@ -241,30 +228,44 @@ int langevin_baoa(const fcg_md_params *p, const float *mass, int R, int N, const
   return cuda_status("langevin_baoa");
 }
 
-// BAOA with this step's slot of the noise ring
-__global__ void k_baoa_ring(fcg_md_params p, const float *mass, int N, long long n,
-                            const float *F, const NoiseTag *tag,
-                            const int64_t *stepp, const float *ring,
-                            float *pos, float *vel) {
+// Noise refill and BAOA in one launch: CTA r owns replica r.  On a refill
+// step its NOISE_RING warps each generate one step of the replica's noise
+// (the same warps per refill as a separate noise launch would use), then the CTA
+// applies BAOA to the replica's 3N coordinates with this step's slot —
+// only replica r's noise is read, so a CTA barrier orders the two.
+static_assert(NOISE_RING * 32 <= 1024, "one warp per ring step");
+__global__ void __launch_bounds__(NOISE_RING * 32)
+k_noise_baoa_ring(fcg_md_params p, const float *mass, int N, int R, const float *F,
+                  const NoiseTag *tag, const int64_t *stepp, float *ring, float *pos,
+                  float *vel) {
   pdl_trigger();
   pdl_wait();
-  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (t >= n) return;
+  const int r = blockIdx.x;
+  const int n3 = 3 * N;
+  const long long n = (long long)R * n3;
   const int64_t step = *stepp;
-  const int64_t slot =
-      ring_valid(tag, p.seed, p.rep_offset, ((int64_t)(n / (3 * N)) << 32) + 3 * N, step)
-          ? step - tag->base : 0;
-  const float *xi = ring + slot * n;
-  int i = (int)((t / 3) % N);
-  float m = mass[i];
-  float v = vel[t], r = pos[t];
-  v = __fadd_rn(v, __fdiv_rn(__fmul_rn(p.half_dt, F[t]), m));
-  r = __fadd_rn(r, __fmul_rn(p.half_dt, v));
-  float c2 = __fsqrt_rn(__fdiv_rn(p.c2_num, m));
-  v = __fadd_rn(__fmul_rn(p.c1, v), __fmul_rn(c2, xi[t]));
-  r = __fadd_rn(r, __fmul_rn(p.half_dt, v));
-  vel[t] = v;
-  pos[t] = r;
+  const bool valid = ring_valid(tag, p.seed, p.rep_offset, ((int64_t)R << 32) + n3, step);
+  if (!valid) {
+    const int j = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    noise_stream(p.seed, (uint64_t)(p.rep_offset + r), (uint64_t)(step + j), n3,
+                 ring + ((size_t)j * R + r) * n3, lane);
+    __syncthreads();
+  }
+  const int64_t slot = valid ? step - tag->base : 0;
+  const float *xi = ring + slot * n + (size_t)r * n3;
+  float *pr = pos + (size_t)r * n3, *vr = vel + (size_t)r * n3;
+  const float *Fr = F + (size_t)r * n3;
+  for (int k = threadIdx.x; k < n3; k += blockDim.x) {
+    const float m = mass[k / 3];
+    float v = vr[k], x = pr[k];
+    v = __fadd_rn(v, __fdiv_rn(__fmul_rn(p.half_dt, Fr[k]), m));
+    x = __fadd_rn(x, __fmul_rn(p.half_dt, v));
+    const float c2 = __fsqrt_rn(__fdiv_rn(p.c2_num, m));
+    v = __fadd_rn(__fmul_rn(p.c1, v), __fmul_rn(c2, xi[k]));
+    x = __fadd_rn(x, __fmul_rn(p.half_dt, v));
+    vr[k] = v;
+    pr[k] = x;
+  }
 }
 
 __global__ void k_step_advance_ring(int64_t *step, NoiseTag *tag, uint64_t seed, int rep_offset,
@@ -294,15 +295,11 @@ int langevin_leading(const fcg_md_params *p, const float *mass, int R, int N,
   NoiseTag *tag = (NoiseTag *)ring_ws;
   float *ring = (float *)((char *)ring_ws + 256);
   const long long n = (long long)R * N * 3;
+  (void)n;
   {
-    FCG_PROF(P_NOISE, s);
-    launch_pdl(PDL_SMALL, k_noise_ring, ceil_div((long long)R * NOISE_RING * 32, 256), 256, 0, s,
-               p->seed, p->rep_offset, step, R, 3 * N, tag, ring);
-  }
-  {
-    FCG_PROF(P_BAOA, s);
-    launch_pdl(PDL_SMALL, k_baoa_ring, ceil_div(n, 256), 256, 0, s, *p, mass, N, n, forces, tag,
-               step, ring, pos, vel);
+    FCG_PROF(P_BAOA, s);  // noise refill (every NOISE_RING steps) + BAOA
+    launch_pdl(PDL_SMALL, k_noise_baoa_ring, R, NOISE_RING * 32, 0, s, *p, mass, N, R, forces,
+               tag, step, ring, pos, vel);
   }
   {
     FCG_PROF(P_STEP, s);
