@@ -1153,6 +1153,207 @@ k_edge_fwd64(const EdgeArgs a, const float4 *geo, const float2 *env,
   if (threadIdx.x < 32) tc::tmem_dealloc<512>(sh->tmem);
 }
 
+// ---------------------------------------------------------------------------
+// Forward with a dedicated MMA warp (the default; FCG_FWD_WS=0 selects
+// k_edge_fwd64).  With last-arriver issue, the warp that issues a chain
+// stays blocked in tcgen05.mma for about the chain's duration, and the
+// group's next request waits for that warp's share of the epilogue
+// (timeline stamps: ~1k cycles per G2 chain, tools/diag_edge_timeline.py).
+// Here a fifth warpgroup issues every chain: the 16 epilogue warps only
+// arrive on a per-group "operands ready" mbarrier (8 arrivals) and never
+// block on the tensor pipe.  Registers: the CTA holds 640 x 96; the issuer
+// warpgroup drops to 24 and the four epilogue warpgroups grow to 112
+// (setmaxnreg; 112 is the most the pool released by the issuer covers).
+constexpr int WS_THREADS = TC_THREADS + 128;
+struct FwdWsShared {
+  TcShared t;
+  uint64_t ready[2][4];  // operands of a group's chain written (8 warp arrivals)
+};
+static_assert(FWD_SM_META + sizeof(FwdWsShared) + 1024 <= 232448, "forward WS smem budget");
+
+__device__ __forceinline__ bool mbar_try(uint64_t *bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(tc::smem_u32(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+// An epilogue warp's operands for a chain are in shared memory (generic
+// proxy writes made visible to the tensor core) and its TMEM reads of the
+// columns the chain overwrites are complete: one arrival per warp.
+__device__ __forceinline__ void ws_ready(uint64_t *bar) {
+  tc::fence_async_smem();
+  tc::fence_before_sync();
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) tc::mbar_arrive(bar);
+}
+
+template <bool Q, bool SC>
+__global__ void __launch_bounds__(WS_THREADS, 1)
+k_edge_fwd_ws(const EdgeArgs a, const float4 *geo, const float2 *env,
+              const int32_t *unit_rows, const float *P, float *H) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  FwdWsShared *ws = (FwdWsShared *)(sm + FWD_SM_META);
+  TcShared *sh = &ws->t;
+  const fcg_block &B = a.blk;
+  pdl_trigger();
+  if (threadIdx.x < 2) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) tc::mbar_init(&ws->ready[threadIdx.x][i], 8);
+  }
+  kernel_prologue(sm, sh, B, FWD_NGRP);
+  tc::mbar_wait(&sh->wbar, 0);
+  load_fwd_weights_tmem(sm, sh->tmem);  // ends with the PDL wait
+  const uint32_t idesc = tc::idesc_f16(128, 64, 0, 1);
+  constexpr int NP = Q ? 1 : 3;
+  constexpr uint32_t Z0 = 0, WS = 64;  // TMEM slots: z0 | w, 64 columns each
+  const uint32_t w0h = sh->tmem + TW0, w0l = w0h + DR / 2, w1h = sh->tmem + TW1, w1l = w1h + D / 2;
+  if (threadIdx.x >= TC_THREADS) {
+    // ---- the MMA warpgroup: warp 16 issues every chain of both groups --------
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 24;\n" ::: "memory");
+    if (threadIdx.x >= TC_THREADS + 32) return;
+    int nt[2], c[2] = {0, 0};
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+      const UnitRange r0 = unit_range(a, unit_rows, FWD_NGRP * blockIdx.x + 2 * g);
+      const UnitRange r1 = unit_range(a, unit_rows, FWD_NGRP * blockIdx.x + 2 * g + 1);
+      nt[g] = max((r0.ee - r0.eb + TT - 1) / TT, (r1.ee - r1.eb + TT - 1) / TT);
+    }
+    while (c[0] < 2 * nt[0] || c[1] < 2 * nt[1]) {
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        if (c[g] >= 2 * nt[g]) continue;
+        const int kind = (c[g] & 1) ? BAR_G2 : BAR_G1;
+        if (!mbar_try(&ws->ready[g][kind], (uint32_t)((c[g] >> 1) & 1))) continue;
+        tc::fence_after_sync();
+        const uint32_t sb = tc::smem_u32(sm + FWD_SM_BUF + g * 2 * GBUF_BYTES);
+        const uint32_t tg = sh->tmem + 128u * g;
+        if (kind == BAR_G1)
+          mma_chain_ts<DR / 16, NP>(tg + Z0, w0h, w0l, adesc<KSTR64>(sb, DR), idesc);
+        else
+          mma_chain_ts<D / 16, NP>(tg + WS, w1h, w1l, adesc<KSTR64>(sb + 2 * BB_BYTES, D), idesc);
+        tc::mma_commit_warp(&sh->bar[g][kind]);
+        ++c[g];
+      }
+    }
+    return;
+  }
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 112;\n" ::: "memory");
+  Wctx W;
+  W.w = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+  W.g = W.w >> 3;
+  const int hf = (W.w >> 2) & 1;
+  const int u = 2 * W.g + hf;
+  W.q = W.w & 3;
+  W.lane = threadIdx.x & 31;
+  W.ch = 32 * W.q + W.lane;
+  W.eo = 32 * hf;
+  W.amask = 7u;
+  W.sh = sh;
+  W.bb = sm + FWD_SM_BUF + W.g * 2 * GBUF_BYTES;
+  W.hb = W.bb + 2 * BB_BYTES;
+  W.sbb = tc::smem_u32(W.bb);
+  W.shb = tc::smem_u32(W.hb);
+  W.tmem_g = sh->tmem + 128u * W.g;
+  W.tl = W.tmem_g + ((uint32_t)(32 * W.q) << 16) + 32u * hf;
+
+  const UnitRange tr = unit_range(a, unit_rows, FWD_NGRP * blockIdx.x + u);
+  const UnitRange to = unit_range(a, unit_rows, FWD_NGRP * blockIdx.x + (u ^ 1));
+  const int ntiles = (tr.ee - tr.eb + TT - 1) / TT;
+  const int nt_all = max(ntiles, (to.ee - to.eb + TT - 1) / TT);
+  const int ch = W.ch;
+  const float *Pch = opaque_ptr(P + ch);
+  SegSum seg;
+  seg.row = ntiles > 0 ? a.own[tr.eb] : -1;
+  seg.acc = 0.f;
+  seg.outc = opaque_ptr(H + ch);
+
+  const float b0c = ld_dep(&B.f0_b[ch]), b1c = ld_dep(&B.f1_b[ch]);
+  const float rs0 = Q ? ld_dep(&B.f0_s[ch]) : pow2f(-(B.f0_exp + 14));
+  const float hs = Q ? 1.f : pow2f(B.f_hexp);
+  const HScale hk(rs0, b0c, hs);
+  const float s1 = Q ? ld_dep(&B.f1_s[ch]) : pow2f(-(B.f1_exp + B.f_hexp));
+  const float bsc = Q ? 0.f : 14.f;
+
+  float pv[TT];
+  MetaRegs mr;
+  for (int it = -1; it < nt_all; ++it) {
+    const int t0 = tr.eb + it * TT;
+    const bool more = it + 1 < nt_all;
+    if (it < 0) {
+      bool r2;
+      mr.load(a, geo, env, tr.eb, min(TT, tr.ee - tr.eb), W.lane);
+      mr.store(W.meta(0), false, W.lane, r2);
+      mr.load(a, geo, env, tr.eb + TT, min(TT, tr.ee - tr.eb - TT), W.lane);
+    } else {
+      STAMP(0, (W.w & 7) == 0, W.g, it, 0);
+      W.wait(BAR_G1, it);
+      STAMP(0, (W.w & 7) == 0, W.g, it, 1);
+      tile_h<Q, KSTR64>(W, rs0, b0c, hk);
+      STAMP(0, (W.w & 7) == 0, W.g, it, 2);
+      ws_ready(&ws->ready[W.g][BAR_G2]);
+      STAMP(0, (W.w & 7) == 0, W.g, it, 3);
+      if (more) {
+        bool r2;
+        mr.store(W.meta(it + 1), false, W.lane, r2);
+        mr.load(a, geo, env, t0 + 2 * TT, min(TT, tr.ee - t0 - 2 * TT), W.lane);
+      }
+    }
+    if (more) {  // basis + G1 of the next tile overlap G2
+      tile_basis<false, Q, KSTR64>(a, W, W.meta(it + 1), bsc);
+      ws_ready(&ws->ready[W.g][BAR_G1]);
+    }
+    STAMP(0, (W.w & 7) == 0, W.g, it, 4);
+    if (it >= 0) {
+      W.wait(BAR_G2, it);
+      STAMP(0, (W.w & 7) == 0, W.g, it, 5);
+      float v[TT];
+      tc::tmem_ld32w(W.tl + WS, v);
+      const int n_e = min(TT, tr.ee - t0);
+      if (n_e > 0) {  // m = (W1 h + b1) * P[src], dst segment sums
+#pragma unroll
+        for (int i = 0; i < TT; ++i) v[i] = (v[i] * s1 + b1c) * pv[i];
+        if (SC) {
+          scatter_tile(seg.outc, W.meta(it)->own, v, n_e);
+        } else {
+          if (n_e < TT) {
+#pragma unroll
+            for (int i = 0; i < TT; ++i) v[i] = i < n_e ? v[i] : 0.f;
+          }
+          seg.tile(W.meta(it)->own, v);
+        }
+      }
+    }
+    STAMP(0, (W.w & 7) == 0, W.g, it, 6);
+    if (more) {
+      const WarpMeta *Mn = W.meta(it + 1);
+      if (tr.ee - (t0 + TT) > 0) {
+#pragma unroll
+        for (int i = 0; i < TT; ++i) pv[i] = ld_gather(Pch + (uint32_t)Mn->nbr[i]);
+      }
+    }
+    STAMP(0, (W.w & 7) == 0, W.g, it, 7);
+  }
+  if (!SC) seg.finish();
+  tc::fence_before_sync();
+  // the issuer warpgroup has returned: sync the epilogue threads only
+  asm volatile("bar.sync 1, %0;" ::"r"(TC_THREADS) : "memory");
+  if (threadIdx.x < 32) tc::tmem_dealloc<512>(sh->tmem);
+}
+
+
+static bool fwd_ws_enabled() {
+  static const bool on = [] {
+    const char *v = getenv("FCG_FWD_WS");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 static bool fwd64_enabled() {
   static const bool on = [] {
     const char *v = getenv("FCG_FWD64");
@@ -1802,6 +2003,10 @@ void edge_tc_configure() {
   const int smem = (int)(SM_TOTAL + 1024), fsmem = (int)(FWD_SM_TOTAL + 1024);
   cudaFuncSetAttribute(k_edge_fwd_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
   cudaFuncSetAttribute(k_edge_fwd_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
+  for (auto k : {k_edge_fwd_ws<false, false>, k_edge_fwd_ws<true, false>,
+                 k_edge_fwd_ws<false, true>, k_edge_fwd_ws<true, true>})
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(FWD_SM_META + sizeof(FwdWsShared) + 1024));
   cudaFuncSetAttribute(k_edge_fwd64<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
   cudaFuncSetAttribute(k_edge_fwd64<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
   cudaFuncSetAttribute(k_edge_fwd64<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
@@ -1836,7 +2041,15 @@ void launch_edge_geom(const EdgeArgs &a, float4 *geo, float2 *env, int32_t *unit
 void launch_edge_fwd_tc(const EdgeArgs &a, const float4 *geo, const float2 *env,
                         const int32_t *unit_rows, const float *P, float *H, int grid,
                         cudaStream_t s, bool scatter) {
-  if (scatter)  // H zeroed by the caller; the scatter schedule exists for the 64-edge kernel
+  if (fwd_ws_enabled() && fwd64_enabled() && FWD_NGRP == 4) {  // H zeroed by the caller (scatter)
+    const uint32_t wsm = (uint32_t)(FWD_SM_META + sizeof(FwdWsShared) + 1024);
+    if (scatter)
+      launch_pdl(PDL_EDGE_FWD, a.quant ? k_edge_fwd_ws<true, true> : k_edge_fwd_ws<false, true>,
+                 grid, WS_THREADS, wsm, s, a, geo, env, unit_rows, P, H);
+    else
+      launch_pdl(PDL_EDGE_FWD, a.quant ? k_edge_fwd_ws<true, false> : k_edge_fwd_ws<false, false>,
+                 grid, WS_THREADS, wsm, s, a, geo, env, unit_rows, P, H);
+  } else if (scatter)
     launch_pdl(PDL_EDGE_FWD, a.quant ? k_edge_fwd64<true, true> : k_edge_fwd64<false, true>,
                grid, TC_THREADS, FWD_SM_TOTAL + 1024, s, a, geo, env, unit_rows, P, H);
   else if (fwd64_enabled() && FWD_NGRP == 4)  // the 64-edge kernel uses the 4-unit partition
