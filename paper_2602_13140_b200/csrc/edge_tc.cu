@@ -1970,6 +1970,315 @@ k_edge_bwd_fm(const EdgeArgs a, const float4 *geo, const float2 *env,
   if (threadIdx.x < 32) tc::tmem_dealloc<512>(sh->tmem);
 }
 
+// Forward-mode backward with the dedicated MMA warpgroup of k_edge_fwd_ws
+// (the default; FCG_BWD_WS=0 selects k_edge_bwd_fm with last-arriver issue).
+// Without the MMA issue code the epilogue fits the 112 registers with no
+// spills: 0.848 -> 0.814 ms/step at C2.
+struct BwdWsShared {
+  FmShared fm;
+  uint64_t ready[2][4];
+};
+static_assert(FM_SM_META + sizeof(BwdWsShared) + 1024 <= 232448, "backward WS smem budget");
+
+template <bool Q, int UPG>
+__global__ void __launch_bounds__(WS_THREADS, 1)
+k_edge_bwd_fmws(const EdgeArgs a, const float4 *geo, const float2 *env,
+                const int32_t *unit_rows, const float *P,
+                const float *GH, float *GP, float4 *gsum,
+                int accumulate) {
+  static_assert(UPG == 2, "two groups of 8 warps");
+  extern __shared__ __align__(1024) uint8_t sm[];
+  BwdWsShared *wsh = (BwdWsShared *)(sm + FM_SM_META);
+  FmShared *sh = &wsh->fm;
+  const fcg_block &B = a.blk;
+  pdl_trigger();
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&sh->wbar, 1);
+    tc::fence_mbar_init();
+    tc::mbar_expect_tx(&sh->wbar, 2 * W0_BYTES + 2 * W1_BYTES);
+    tc::bulk_g2s(sm + SM_W0, B.f0_img, 2 * W0_BYTES, &sh->wbar);
+    tc::bulk_g2s(sm + SM_W1, B.f1_img, 2 * W1_BYTES, &sh->wbar);
+  }
+  using C = FmCfg<UPG>;
+  if (threadIdx.x < 4) {
+    const int u0 = threadIdx.x;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      tc::mbar_init(&sh->bar[u0][i], 1);
+      sh->req[u0][i] = 0u;
+    }
+    tc::mbar_init(&sh->xbar[u0], 4);
+#pragma unroll
+    for (int b = 0; b < FM_MBUF; ++b) tc::mbar_init(&sh->mbar[u0][b], 128);
+    if (u0 < 2) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) tc::mbar_init(&wsh->ready[u0][i], 8);
+    }
+    tc::fence_mbar_init();
+  }
+  for (int i = threadIdx.x; i < (int)(sizeof(sh->um) / 4); i += blockDim.x)
+    ((int *)sh->um)[i] = 0;
+  if (threadIdx.x < 32) tc::tmem_alloc<512>(&sh->tmem);
+  tc::fence_async_smem();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  tc::mbar_wait(&sh->wbar, 0);
+  if (threadIdx.x < TC_THREADS) {
+    load_fm_weights_tmem(sm, sh->tmem);  // ends with the PDL wait + block barrier
+  } else {
+    tc::fence_before_sync();
+    pdl_wait();
+    __syncthreads();
+    tc::fence_after_sync();
+  }
+  constexpr int NB = Q ? 1 : 3, NDB = Q ? 2 : 3, NH = Q ? 1 : 3, NV = Q ? 2 : 3;
+  const uint32_t w0h = sh->tmem + FM_TW0, w0l = w0h + DR / 2;
+  const uint32_t w1h = sh->tmem + FM_TW1, w1l = w1h + D / 2;
+  if (threadIdx.x >= TC_THREADS) {  // the MMA warpgroup (see k_edge_fwd_ws)
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 24;\n" ::: "memory");
+    if (threadIdx.x >= TC_THREADS + 32) return;
+    int nt[2], c[2] = {0, 0};
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+      const UnitRange r0 = unit_range(a, unit_rows, NGRP * blockIdx.x + 2 * g);
+      const UnitRange r1 = unit_range(a, unit_rows, NGRP * blockIdx.x + 2 * g + 1);
+      nt[g] = max((r0.ee - r0.eb + TT - 1) / TT, (r1.ee - r1.eb + TT - 1) / TT);
+    }
+    while (c[0] < 2 * nt[0] || c[1] < 2 * nt[1]) {
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        if (c[g] >= 2 * nt[g]) continue;
+        const int kind = (c[g] & 1) ? BAR_G2 : BAR_G1;
+        if (!mbar_try(&wsh->ready[g][kind], (uint32_t)((c[g] >> 1) & 1))) continue;
+        tc::fence_after_sync();
+        const uint8_t *bbp = sm + g * C::GBUF;
+        const uint32_t tg = sh->tmem + 2u * C::RH * g;
+        if (kind == BAR_G1)
+          mma_pair_ts<DR / 16, NB, NDB, C::N>(tg, w0h, w0l, adesc<C::KS>(tc::smem_u32(bbp), DR));
+        else
+          mma_pair_ts<D / 16, NH, NV, C::N>(tg, w1h, w1l,
+                                            adesc<C::KS>(tc::smem_u32(bbp + C::BB), D));
+        tc::mma_commit_warp(&sh->bar[g][kind]);
+        ++c[g];
+      }
+    }
+    return;
+  }
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 112;\n" ::: "memory");
+
+  Wctx W;
+  W.w = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+  W.g = W.w / (4 * UPG);
+  const int hf = UPG == 2 ? (W.w >> 2) & 1 : 0;
+  const int u = UPG * W.g + hf;  // work unit / metadata / grad_d partials of this warp
+  W.q = W.w & 3;
+  W.lane = threadIdx.x & 31;
+  W.ch = 32 * W.q + W.lane;
+  W.eo = 32 * hf;
+  W.amask = 4u * UPG - 1u;
+  W.sh = (TcShared *)nullptr;
+  W.bb = sm + W.g * C::GBUF;
+  W.hb = W.bb + C::BB;
+  W.sbb = tc::smem_u32(W.bb);
+  W.shb = tc::smem_u32(W.hb);
+  W.tmem_g = sh->tmem + 2u * C::RH * W.g;
+  W.tl = W.tmem_g + ((uint32_t)(32 * W.q) << 16) + 32u * hf;
+
+  const UnitRange tr = unit_range(a, unit_rows, NGRP * blockIdx.x + u);
+  const int ntiles = (tr.ee - tr.eb + TT - 1) / TT;
+  int nt_all = ntiles;  // the group's iterations
+  if (UPG == 2) {
+    const UnitRange to = unit_range(a, unit_rows, NGRP * blockIdx.x + (u ^ 1));
+    nt_all = max(ntiles, (to.ee - to.eb + TT - 1) / TT);
+  }
+  const int ch = W.ch;
+  const int lane = W.lane;
+  const float *GHch = opaque_ptr(GH + ch);
+  const float *Pch = opaque_ptr(P + ch);
+  SegSum seg;
+  seg.row = ntiles > 0 ? a.own[tr.eb] : -1;
+  seg.acc = 0.f;
+  seg.outc = opaque_ptr(GP + ch);
+
+  // E1 constants (this thread's channel = hidden unit k of filter layer 0)
+  // (the W16 row scales are re-read from L1 where they are used: held
+  // across the loop they cost the kernel its last registers)
+  const float b0c = ld_dep(&B.f0_b[ch]);
+  const float hs = Q ? 1.f : pow2f(B.f_hexp);
+  const HScale hk(Q ? 1.f : pow2f(-(B.f0_exp + 14)), b0c, hs);
+  // E2 constants (this thread's channel = output channel c of filter layer 1)
+  const float b1c = ld_dep(&B.f1_b[ch]);
+  const float bsc = Q ? 0.f : 14.f, dbsc = (float)B.f_dbexp;
+  auto count_of = [&](int t) { return min(TT, tr.ee - (tr.eb + t * TT)); };
+  auto um = [&](int t) { return &sh->um[u][t % FM_MBUF]; };
+  auto meta_wait = [&](int t) {
+    tc::mbar_wait(&sh->mbar[u][t % FM_MBUF], (uint32_t)((t / FM_MBUF) & 1));
+  };
+
+  if (nt_all > 0) {  // tiles 0 and 1 in flight; tile 0's [b | db] and G1 | G1'
+    meta_issue(a, geo, env, um(0), &sh->mbar[u][0], tr.eb, count_of(0), W.q, lane);
+    if (nt_all > 1)
+      meta_issue(a, geo, env, um(1), &sh->mbar[u][1], tr.eb + TT, count_of(1), W.q, lane);
+    meta_wait(0);
+    tile_basis_pair<Q, UPG>(a, W, um(0), bsc, dbsc);
+    ws_ready(&wsh->ready[W.g][BAR_G1]);
+  }
+  for (int it = 0; it < nt_all; ++it) {
+    const int t0 = tr.eb + it * TT;
+    const bool more = it + 1 < nt_all;
+    const UnitMeta *M = um(it);
+    const int n_e = count_of(it);  // <= 0: this half has no tile this iteration
+
+    // ---- E1: h = ssp(z0), v = ssp'(z0) dz0 -> [h | v] -----------------------
+    // z0 = acc * rs0 + b0; v * 2^f_vexp from the dz0 accumulator (W0 *
+    // 2^f0_exp (fp32) or w16 (W16, row scale s0) times db * 2^f_dbexp)
+    const float rs0 = Q ? ld_dep(&B.f0_s[ch]) : pow2f(-(B.f0_exp + 14));
+    const float kv = Q ? rs0 * pow2f(B.f_vexp - B.f_dbexp)
+                       : pow2f(B.f_vexp - B.f0_exp - B.f_dbexp);
+    STAMP(1, (W.w & 7) == 0, W.g, it, 0);
+    tc::mbar_wait(&sh->bar[W.g][BAR_G1], (uint32_t)(it & 1));
+    tc::fence_after_sync();
+    STAMP(1, (W.w & 7) == 0, W.g, it, 1);
+#pragma unroll
+    for (int c0 = 0; c0 < TT; c0 += 16) {
+      float z[16], dz[16];
+      tc::tmem_ld16w(W.tl + c0, z);
+      tc::tmem_ld16w(W.tl + C::RH + c0, dz);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        float sp;  // kv * ssp'(z0)
+        if (Q) {
+          const float zz = z[i] * rs0 + b0c;
+          sp = sigmoid_fast(zz) * kv;
+          z[i] = __half2float(__float2half_rn(ssp_fast(zz)));
+        } else {
+          z[i] = ssp_scaled(z[i] * hk.rs + hk.b, hk.c_ln2, hk.c_e);  // hs * h
+          sp = fmaf(-0.5f * kv, ex2_ftz(z[i] * hk.c_e), kv);         // kv (1 - e^-h / 2)
+        }
+        dz[i] *= sp;
+      }
+#pragma unroll
+      for (int j = 0; j < 16; j += 8) {
+        put8<!Q, C::KS>(W.hb, D, ch, W.eo + c0 + j, &z[j], 1.f);
+        put8<true, C::KS>(W.hb, D, ch, C::RH + W.eo + c0 + j, &dz[j], 1.f);
+      }
+    }
+    STAMP(1, (W.w & 7) == 0, W.g, it, 2);
+    ws_ready(&wsh->ready[W.g][BAR_G2]);
+    STAMP(1, (W.w & 7) == 0, W.g, it, 3);
+
+    // ---- gathers of this tile (consumed after the [G2 | G3] wait) ------------
+    float gh[TT];
+    float pf = 0.f, pm = 0.f, pl = 0.f;  // P[src] of the first, middle and last row
+    int o_f = -1, o_l = -1;
+    bool rows3 = true;
+    float4 ue = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (n_e > 0) {
+      const int o = M->own[lane];
+      o_f = M->own[0];
+      o_l = M->own[n_e - 1];
+      const unsigned other = __ballot_sync(0xffffffffu, lane < n_e && o != o_f && o != o_l);
+      const int mid = other ? __shfl_sync(0xffffffffu, o, __ffs(other) - 1) : o_f;
+      rows3 = __all_sync(0xffffffffu, lane >= n_e || o == o_f || o == o_l || o == mid);
+#pragma unroll
+      for (int i = 0; i < TT; ++i) gh[i] = ld_gather(GHch + ((uint32_t)M->nbr[i] << 7));
+      pf = ld_gather(Pch + (uint32_t)o_f * D);  // scaled by ku where used
+      pm = ld_gather(Pch + (uint32_t)mid * D);
+      pl = ld_gather(Pch + (uint32_t)o_l * D);
+      if (W.q == 0 && lane < n_e) ue = ld_dep(&geo[t0 + lane]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < TT; ++i) gh[i] = 0.f;
+    }
+    if (more) {  // next tile's [b | db] (the basis buffer is free: G1 done)
+      meta_wait(it + 1);
+      tile_basis_pair<Q, UPG>(a, W, um(it + 1), bsc, dbsc);
+    }
+
+    // ---- E2: grad_P segment sums, grad_d partials --------------------------
+    const float s1 = Q ? ld_dep(&B.f1_s[ch]) : pow2f(-(B.f1_exp + B.f_hexp));
+    const float ku = Q ? s1 * pow2f(-B.f_vexp) : pow2f(-(B.f1_exp + B.f_vexp));
+    STAMP(1, (W.w & 7) == 0, W.g, it, 4);
+    tc::mbar_wait(&sh->bar[W.g][BAR_G2], (uint32_t)(it & 1));
+    tc::fence_after_sync();
+    STAMP(1, (W.w & 7) == 0, W.g, it, 5);
+    // every warp of the group is past iteration it-1: tile it+2's copies may
+    // reuse the buffer of tile it-1
+    if (it + 2 < nt_all)
+      meta_issue(a, geo, env, um(it + 2), &sh->mbar[u][(it + 2) % FM_MBUF], t0 + 2 * TT,
+                 count_of(it + 2), W.q, lane);
+    float q[TT];
+    {
+      const unsigned st = n_e > 0 ? seg.starts_n(M->own, n_e) : 0u;
+#pragma unroll
+      for (int h = 0; h < TT; h += 16) {
+        float v[16];
+        tc::tmem_ld16w(W.tl + h, v);  // w accumulator
+        if (n_e > 0) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = h + i < n_e ? gh[h + i] * (v[i] * s1 + b1c) : 0.f;
+          seg.half(M->own, v, h, st);
+        }
+      }
+      tc::tmem_ld32w(W.tl + C::RH, q);  // u accumulator
+    }
+    STAMP(1, (W.w & 7) == 0, W.g, it, 6);
+    if (more) ws_ready(&wsh->ready[W.g][BAR_G1]);  // TMEM read: next G1 | G1' may write
+    if (rows3) {
+      pf *= ku; pm *= ku; pl *= ku;
+#pragma unroll
+      for (int j = 0; j < TT; j += 4) {
+        const int4 o4 = *(const int4 *)&M->own[j];
+        const int oo[4] = {o4.x, o4.y, o4.z, o4.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          q[j + i] *= gh[j + i] * (oo[i] == o_l ? pl : (oo[i] == o_f ? pf : pm));
+      }
+    } else {  // four or more rows (~5% of coil-269 tiles): per-edge gathers
+#pragma unroll
+      for (int i = 0; i < TT; ++i)
+        q[i] *= gh[i] * ld_gather(Pch + (uint32_t)M->own[i] * D) * ku;
+    }
+    STAMP(1, (W.w & 7) == 0, W.g, it, 7);
+    float *xg = &sh->xg[u][it & 1][0][0];
+    xg[W.q * TT + lane] = warp_edge_sum(q, lane);
+    __syncwarp();
+    if (lane == 0) tc::mbar_arrive(&sh->xbar[u]);
+    if (W.q == 0) {
+      tc::mbar_wait(&sh->xbar[u], (uint32_t)(it & 1));
+      const int e = lane;
+      if (e < n_e) {
+        const float gd = ((xg[e] + xg[TT + e]) + xg[2 * TT + e]) + xg[3 * TT + e];
+        // backward edge: dst = nbr, src = own, u = r_nbr - r_own (flash.py:279)
+        const float inv = ue.w > TINY_DISTANCE ? 1.f / ue.w : 0.f;
+        const float sc = -gd * inv;
+        float4 g = make_float4(sc * ue.x, sc * ue.y, sc * ue.z, 0.f);
+        float4 *dst = &gsum[t0 + e];
+        if (accumulate) {
+          const float4 o = *dst;
+          g.x += o.x; g.y += o.y; g.z += o.z;
+        }
+        *dst = g;
+      }
+    }
+    STAMP(1, (W.w & 7) == 0, W.g, it, 8);
+  }
+  seg.finish();
+  tc::fence_before_sync();
+  asm volatile("bar.sync 1, %0;" ::"r"(TC_THREADS) : "memory");
+  if (threadIdx.x < 32) tc::tmem_dealloc<512>(sh->tmem);
+}
+
+
+static bool bwd_ws_enabled() {  // default on; FCG_BWD_WS=0 selects k_edge_bwd_fm
+  static const bool on = [] {
+    const char *v = getenv("FCG_BWD_WS");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 // FCG_BWD_UPG=1: four groups of 4 warps (one work unit each) instead of two of 8
 static int bwd_fm_upg() {
   static const int v = [] {
@@ -2013,6 +2322,10 @@ void edge_tc_configure() {
   cudaFuncSetAttribute(k_edge_fwd64<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
   cudaFuncSetAttribute(k_edge_bwd_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_edge_bwd_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_edge_bwd_fmws<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(FM_SM_META + sizeof(BwdWsShared) + 1024));
+  cudaFuncSetAttribute(k_edge_bwd_fmws<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(FM_SM_META + sizeof(BwdWsShared) + 1024));
   cudaFuncSetAttribute(k_edge_bwd_fm<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(FM_SM_TOTAL + 1024));
   cudaFuncSetAttribute(k_edge_bwd_fm<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2067,6 +2380,10 @@ void launch_edge_bwd_tc(const EdgeArgs &a, const float4 *geo, const float2 *env,
     launch_pdl(PDL_EDGE_BWD, a.quant ? k_edge_bwd64<true, true> : k_edge_bwd64<false, true>,
                grid, TC_THREADS, SM_TOTAL + 1024, s, a, geo, env, unit_rows, P, GH, GP, gsum,
                accumulate, gr);
+  else if (bwd_fm_enabled() && bwd_ws_enabled())
+    launch_pdl(PDL_EDGE_BWD, a.quant ? k_edge_bwd_fmws<true, 2> : k_edge_bwd_fmws<false, 2>, grid,
+               WS_THREADS, (uint32_t)(FM_SM_META + sizeof(BwdWsShared) + 1024), s, a, geo, env,
+               unit_rows, P, GH, GP, gsum, accumulate);
   else if (bwd_fm_enabled() && bwd_fm_upg() == 1)
     launch_pdl(PDL_EDGE_BWD, a.quant ? k_edge_bwd_fm<true, 1> : k_edge_bwd_fm<false, 1>, grid,
                TC_THREADS, FM_SM_TOTAL + 1024, s, a, geo, env, unit_rows, P, GH, GP, gsum,

@@ -285,7 +285,7 @@ def test_hot_kernels_do_not_spill():
                          r"spill stores, (\d+) bytes spill loads", text):
         name, stores, loads = m.group(1), int(m.group(3)), int(m.group(4))
         if any(k in name for k in ("k_edge_fwd_tc", "k_edge_bwd_tc", "k_edge_bwd64", "k_edge_fwd64",
-                                   "k_edge_bwd_fm", "k_node_",
+                                   "k_edge_bwd_fm", "k_edge_fwd_ws", "k_node_",
                                    "k_readout_tc")):
             spills[name] = (stores, loads)
     assert spills, "no hot kernels found in the ptxas log"
