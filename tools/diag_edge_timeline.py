@@ -27,8 +27,8 @@ eng.evaluate()
 torch.cuda.synchronize()
 lib.fcg_debug_phase_buffer(None)
 b = buf.cpu().numpy().reshape(2, 2, 32, 16).astype(np.int64)
-names = {0: ("fwd64", ["wait G1", "E1 h", "REQ G2", "basis+G1", "wait G2", "E2", "gathers"]),
-         1: ("bwd_fm", ["wait G1", "E1 h,v", "REQ G2|G3", "gathers+basis", "wait G2|G3", "E2 seg+u", "q+G1+red", "xg exchange"])}
+names = {0: ("fwd64", ["wait G1", "E1 h", "ready G2", "basis+ready G1", "wait G2", "E2", "gathers"]),
+         1: ("bwd_fm", ["wait G1", "E1 h,v", "ready G2|G3", "gathers+basis", "wait G2|G3", "E2 seg+u", "q+G1+red", "xg exchange"])}
 for k, (nm, ph) in names.items():
     for g in range(2):
         t = b[k, g]
