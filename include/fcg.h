@@ -334,6 +334,15 @@ int fcg_native_q(const double *x, int F, int N, const int32_t *pairs,
                  const double *ref_dist, int C, double beta, double lam, double *q,
                  void *stream);
 
+/* ---- quantize_model calibration (quantize.py:126-178)
+ * err[r][c] = dw^T gram dw, dw = fp64(fp16(w[r] / cand[r][c])) * cand[r][c]
+ * - w[r] (non-finite entries -> 1e30), all fp64 on the device: w[rows][k],
+ * cand[rows][ncand], gram[k][k] (k <= 256).  The caller takes the argmin
+ * per row (w16.quantize_model(device="cuda"), which re-scores near-ties on
+ * the host so the scales stay bit-identical to the reference's). */
+int fcg_calib_errors(const double *w, int rows, int k, const double *cand, int ncand,
+                     const double *gram, double *err, void *stream);
+
 /* Diagnostics: tcgen05 (kind::f16) GEMM self-test.  dump[128][N] receives
  * the raw TMEM accumulator lanes of D = A * B^T for A[M][K], B[N][K] fp16
  * staged in the canonical no-swizzle core-matrix layout (K-major or

@@ -90,6 +90,7 @@ _SIGS = {
                                           _VP, _VP, _VP, C.c_int64, _VP, _VP, _VP, _VP,
                                           C.c_size_t, C.c_int, _VP]),
     "fcg_normal_noise": (C.c_int, [C.c_uint64, C.c_int, _VP, C.c_int, C.c_int, _VP, _VP]),
+    "fcg_calib_errors": (C.c_int, [_VP, C.c_int, C.c_int, _VP, C.c_int, _VP, _VP, _VP]),
     "fcg_langevin_baoa": (C.c_int, [C.POINTER(FcgMdParams), _VP, C.c_int, C.c_int, _VP, _VP,
                                     _VP, _VP, _VP]),
     "fcg_half_kick": (C.c_int, [C.POINTER(FcgMdParams), _VP, C.c_int, C.c_int, _VP, _VP, _VP]),

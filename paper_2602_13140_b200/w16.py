@@ -69,9 +69,52 @@ def _basis64(d, rbf: RbfSpec):
     return np.exp(-d.dtype.type(rbf.gamma) * dl * dl) * env[..., None]
 
 
-def _calibrated(w: np.ndarray, b: np.ndarray, samples: np.ndarray) -> QuantizedLinear:
+def _host_errors(w: np.ndarray, cand: np.ndarray, gram: np.ndarray) -> np.ndarray:
+    """err[r][c] = dw' G dw of every (row, candidate) pair, with the
+    reference's own numpy operations (quantize.py:150-170)."""
+    q = (w[:, None, :] / cand[:, :, None]).astype(np.float16)
+    dw = q.astype(np.float64) * cand[:, :, None] - w[:, None, :]
+    dw = np.where(np.isfinite(dw), dw, 1e30)
+    flat = dw.reshape(-1, w.shape[1])
+    return np.einsum("si,si->s", flat @ gram, flat).reshape(cand.shape)
+
+
+# relative gap below which the GPU's best two candidates count as a tie (the
+# device sums in another order than numpy's BLAS, ~1e-15 relative apart)
+_TIE_RTOL = 1e-9
+
+
+def _device_errors(w: np.ndarray, cand: np.ndarray, gram: np.ndarray, device) -> np.ndarray:
+    """The same scores from libfcg's fcg_calib_errors (csrc/calib.cu).  When
+    any row's best two candidates are within _TIE_RTOL, the layer is scored
+    on the host instead, so argmin — the stored scale — is the reference's."""
+    import ctypes as C
+
+    from . import _lib
+    from .engine import _torch
+
+    torch = _torch()
+    lib = _lib.load()
+    dev = torch.device(device)
+    t = lambda a: torch.as_tensor(np.ascontiguousarray(a, np.float64)).to(dev)  # noqa: E731
+    dw_, dc, dg = t(w), t(cand), t(gram)
+    err = torch.empty(cand.shape, dtype=torch.float64, device=dev)
+    v = _lib.vp
+    _lib.check(lib.fcg_calib_errors(v(dw_), w.shape[0], w.shape[1], v(dc), cand.shape[1], v(dg),
+                                    v(err), C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)),
+               "fcg_calib_errors")
+    e = err.cpu().numpy()
+    part = np.sort(e, axis=1)[:, :2] if e.shape[1] > 1 else np.concatenate([e, e + 1.0], axis=1)
+    if np.any(part[:, 1] - part[:, 0] <= _TIE_RTOL * np.abs(part[:, 0])):
+        return _host_errors(w, cand, gram)
+    return e
+
+
+def _calibrated(w: np.ndarray, b: np.ndarray, samples: np.ndarray,
+                device=None) -> QuantizedLinear:
     """Per-row scale minimising dw' G dw over a geometric grid around the row
-    absmax, the tensor-wide grid and 1.0 (quantize.py:126-178)."""
+    absmax, the tensor-wide grid and 1.0 (quantize.py:126-178); the scores
+    on the GPU when `device` is given."""
     if samples.ndim != 2 or samples.shape[0] < MIN_CALIBRATION_SAMPLES:
         raise ValueError(f"calibration needs at least {MIN_CALIBRATION_SAMPLES} samples")
     w = np.asarray(w, dtype=np.float64)
@@ -85,11 +128,10 @@ def _calibrated(w: np.ndarray, b: np.ndarray, samples: np.ndarray) -> QuantizedL
     cand = np.concatenate([seeds[:, None] * _GRID[None, :],
                            np.broadcast_to(shared, (w.shape[0], shared.size))], axis=1)
     cand = np.sort(cand, axis=1)
-    q = (w[:, None, :] / cand[:, :, None]).astype(np.float16)
-    dw = q.astype(np.float64) * cand[:, :, None] - w[:, None, :]
-    dw = np.where(np.isfinite(dw), dw, 1e30)
-    flat = dw.reshape(-1, w.shape[1])
-    err = np.einsum("si,si->s", flat @ gram, flat).reshape(cand.shape)
+    if device is not None and w.shape[1] <= 256:
+        err = _device_errors(w, cand, gram, device)
+    else:
+        err = _host_errors(w, cand, gram)
     scale = cand[np.arange(w.shape[0]), np.argmin(err, axis=1)]
     scale[dead] = 1.0
     stored = (w / scale[:, None]).astype(np.float16)
@@ -98,10 +140,10 @@ def _calibrated(w: np.ndarray, b: np.ndarray, samples: np.ndarray) -> QuantizedL
                            bias=np.asarray(b, dtype=np.float32))
 
 
-def _calibrated_mlp(layers, x: np.ndarray) -> QuantizedMlp:
+def _calibrated_mlp(layers, x: np.ndarray, device=None) -> QuantizedMlp:
     out, a = [], x
     for i, (w, b) in enumerate(layers):
-        out.append(_calibrated(w, b, a))
+        out.append(_calibrated(w, b, a, device))
         z = a @ np.asarray(w, dtype=np.float64).T + b
         if i < len(layers) - 1:
             a = _ssp64(z)
@@ -154,7 +196,11 @@ def _node_samples(params: ModelParams, seed: int, n_states: int = 4, n_beads: in
     return [cat(p) for p in pre_in], [cat(p) for p in post_in], cat(ro_in)
 
 
-def quantize_model(params: ModelParams, seed: int = 0, n_rbf_samples: int = 256) -> QuantizedParams:
+def quantize_model(params: ModelParams, seed: int = 0, n_rbf_samples: int = 256,
+                   device=None) -> QuantizedParams:
+    """quantize.py:264-299.  device="cuda" scores the calibration candidates
+    with fcg_calib_errors on the GPU (bit-identical result: near-ties are
+    re-scored on the host); the default is the host computation."""
     rng = np.random.default_rng(seed)
     cfg = params.config
     rbf_in = _basis64(rng.uniform(0.0, cfg.cutoff, size=n_rbf_samples).astype(np.float64),
@@ -163,9 +209,10 @@ def quantize_model(params: ModelParams, seed: int = 0, n_rbf_samples: int = 256)
     blocks = []
     for t, bp in enumerate(params.blocks):
         blocks.append(BlockParams(
-            pre_linear=_calibrated(bp.pre_linear[0], bp.pre_linear[1], pre_in[t]),
-            filter_mlp=_calibrated_mlp(bp.filter_mlp, rbf_in),
-            post_mlp=_calibrated_mlp(bp.post_mlp, post_in[t])))
+            pre_linear=_calibrated(bp.pre_linear[0], bp.pre_linear[1], pre_in[t], device),
+            filter_mlp=_calibrated_mlp(bp.filter_mlp, rbf_in, device),
+            post_mlp=_calibrated_mlp(bp.post_mlp, post_in[t], device)))
     return QuantizedParams(config=cfg, embedding=params.embedding.astype(np.float32),
-                           blocks=tuple(blocks), readout=_calibrated_mlp(params.readout, ro_in),
+                           blocks=tuple(blocks),
+                           readout=_calibrated_mlp(params.readout, ro_in, device),
                            rbf=params.rbf)

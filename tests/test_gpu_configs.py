@@ -207,3 +207,41 @@ def test_compare_on_engine_reports_every_schedule():
     for k in ("fused_ms", "fused_scatter_ms", "materialized_scatter_ms",
               "materialized_segred_ms"):
         assert rep[k] > 0
+
+
+# --------------------------------------------- quantize_model on the GPU
+@pytest.mark.parametrize("cfg,seed", [({}, 0), ({"hidden_dim": 16, "rbf_dim": 8, "num_blocks": 2,
+                                                 "cutoff": 1.0, "num_atom_types": 6,
+                                                 "filter_hidden_dim": 16,
+                                                 "readout_hidden_dim": 8}, 3)])
+def test_quantize_model_on_gpu_is_bit_identical(cfg, seed):
+    """quantize.py:224-299 with the candidate scores on the GPU
+    (fcg_calib_errors): every stored fp16 weight and scale equals the host
+    (= reference, hash-pinned in test_host.py) calibration."""
+    from paper_2602_13140_b200.w16 import quantize_model
+    params = init_params(ModelConfig(**cfg), seed)
+    host = quantize_model(params, seed=0)
+    gpu = quantize_model(params, seed=0, device="cuda")
+
+    def lins(q):
+        for bp in q.blocks:
+            yield bp.pre_linear
+            yield from bp.filter_mlp.layers
+            yield from bp.post_mlp.layers
+        yield from q.readout.layers
+    for a, b in zip(lins(host), lins(gpu)):
+        np.testing.assert_array_equal(a.weight, b.weight)
+        np.testing.assert_array_equal(a.scale, b.scale)
+        np.testing.assert_array_equal(a.bias, b.bias)
+
+
+def test_calibration_errors_kernel_matches_host():
+    from paper_2602_13140_b200.w16 import _device_errors, _host_errors, _GRID
+    rng = np.random.default_rng(5)
+    w = rng.normal(0, 0.2, size=(40, 128))
+    x = rng.normal(0, 1.0, size=(64, 128))
+    gram = x.T @ x
+    cand = np.sort(np.abs(w).max(axis=1)[:, None] * _GRID[None, :], axis=1)
+    e_host = _host_errors(w, cand, gram)
+    e_dev = _device_errors(w, cand, gram, "cuda")
+    np.testing.assert_allclose(e_dev, e_host, rtol=1e-11, atol=0)
