@@ -96,7 +96,7 @@ def device_csr(positions: np.ndarray, r_cut: float, replicas: bool = False):
                            ).to("cuda", dt)
     status = torch.zeros(_lib.FCG_STATUS_WORDS, dtype=torch.int64, device="cuda")
     nb = lib.fcg_nbr_workspace_bytes(R, N)
-    ws = torch.empty(int(nb), dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(int(nb), dtype=torch.uint8, device="cuda")  # zero before first use
     fn = lib.fcg_nbr_build_f64 if f64 else lib.fcg_nbr_build
     v = _lib.vp
     cap = default_capacity(R, N)

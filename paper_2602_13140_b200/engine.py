@@ -174,7 +174,7 @@ class MDEngine:
         while rebuild:
             c = self.csr  # re-read: a regrow below replaces the buffers
             nb = L.fcg_nbr_workspace_bytes(self.R, self.N)
-            ws_nb = torch.empty(int(nb), dtype=torch.uint8, device=self.device)
+            ws_nb = torch.zeros(int(nb), dtype=torch.uint8, device=self.device)  # fcg.h contract
             _lib.check(L.fcg_nbr_build(v(self.pos), self.R, self.N, self.r_cut, c.cap_e, v(c.ptr),
                                        v(c.nbr), v(c.rev), v(c.own), v(self.status), v(ws_nb),
                                        nb, self.stream()), "fcg_nbr_build")
