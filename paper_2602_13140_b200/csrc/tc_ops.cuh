@@ -144,7 +144,13 @@ __device__ __forceinline__ float ssp_fast(float x) {
 // s * ssp(x) for a power-of-two s > 0 from xs = s * x (exact): the scale rides
 // in the constants, c_ln2 = s ln2 and c_e = -log2(e) / s.
 __device__ __forceinline__ float ssp_scaled(float xs, float c_ln2, float c_e) {
+#ifdef FCG_ACCURATE_EPI  // diagnostic builds: libm transcendentals (precision A/B)
+  const float s = c_ln2 / kLn2;  // the power-of-two scale
+  const float x = xs / s;
+  return s * (fmaxf(x, 0.f) + log1pf(expf(-fabsf(x))) - kLn2);
+#else
   return fmaf(c_ln2, lg2_ftz(fmaf(ex2_ftz(fabsf(xs) * c_e), 0.5f, 0.5f)), fmaxf(xs, 0.f));
+#endif
 }
 __device__ __forceinline__ float sigmoid_fast(float x) {
   return rcp_ftz(1.f + ex2_ftz(x * -kLog2e));

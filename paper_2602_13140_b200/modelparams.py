@@ -209,12 +209,35 @@ def _pow2_exp(bound: float) -> int:
     return 14 - int(np.floor(np.log2(bound))) if bound > 0 else 0
 
 
-def edge_h_exp(w0: np.ndarray, b0: np.ndarray) -> int:
-    """Static scale of h = ssp(W0 b + b0) in the edge kernels: the Gaussian
-    basis times the envelope lies in [0, 1] (model.py:123-133), so |z0[c]| <=
-    sum_k |W0[c,k]| + |b0[c]|, and -ln2 <= ssp(z) <= max(z, 0)."""
-    bz = float(np.max(np.sum(np.abs(w0.astype(np.float64)), axis=1) + np.abs(b0)))
-    return _pow2_exp(max(bz, math.log(2.0)) * 1.001)
+def _dgrid_basis(centers, gamma: float, cutoff: float, n: int = 30001):
+    """Basis rows b(d) (model.py:123-133) and their derivatives on a grid of
+    d over [0, cutoff], 2,000x finer than the basis width."""
+    d = np.linspace(0.0, float(cutoff), n)
+    delta = d[:, None] - np.asarray(centers, np.float64)[None, :]
+    env = 0.5 * (np.cos(np.pi * d / cutoff) + 1.0)
+    denv = -0.5 * np.pi / cutoff * np.sin(np.pi * d / cutoff)
+    g = np.exp(-gamma * delta * delta)
+    return g * env[:, None], g * (-2.0 * gamma * delta * env[:, None] + denv[:, None])
+
+
+def edge_h_exp(w0: np.ndarray, b0: np.ndarray, centers=None, gamma: float = 0.0,
+               cutoff: float = 0.0) -> int:
+    """Static scale of h = ssp(W0 b(d) + b0) in the edge kernels.  z0 depends
+    on the edge only through d, so max |h| over d in [0, cutoff] (a grid
+    2,000x finer than the basis width, 5% margin; the split tolerates 2x
+    more before fp16 overflows) bounds it tightly — about 30x below the
+    algebraic bound sum_k |W0[c,k]| + |b0[c]| (0 <= b <= 1), which the hi/lo
+    split would otherwise spend as 5 bits of precision.  Without the basis
+    parameters the algebraic bound is used."""
+    w0 = np.asarray(w0, np.float64)
+    b0 = np.asarray(b0, np.float64)
+    if centers is None:
+        bz = float(np.max(np.sum(np.abs(w0), axis=1) + np.abs(b0)))
+        return _pow2_exp(max(bz, math.log(2.0)) * 1.001)
+    b, _ = _dgrid_basis(centers, gamma, cutoff)
+    z = b @ w0.T + b0
+    h = np.maximum(z, 0) + np.log1p(np.exp(-np.abs(z))) - math.log(2.0)
+    return _pow2_exp(float(np.max(np.abs(h))) * 1.05)
 
 
 def edge_db_exp(gamma: float, cutoff: float) -> int:
@@ -231,11 +254,7 @@ def edge_v_exp(w0: np.ndarray, centers: np.ndarray, gamma: float, cutoff: float)
     a grid 2,000x finer than the basis width (the function moves < 0.5%
     between points; 5% margin, and the split tolerates 2x before fp16
     overflows)."""
-    d = np.linspace(0.0, float(cutoff), 30001)
-    delta = d[:, None] - np.asarray(centers, np.float64)[None, :]
-    env = 0.5 * (np.cos(np.pi * d / cutoff) + 1.0)
-    denv = -0.5 * np.pi / cutoff * np.sin(np.pi * d / cutoff)
-    db = np.exp(-gamma * delta * delta) * (-2.0 * gamma * delta * env[:, None] + denv[:, None])
+    _, db = _dgrid_basis(centers, gamma, cutoff)
     bound = float(np.max(np.abs(db) @ np.abs(w0.astype(np.float64)).T))
     return _pow2_exp(bound * 1.05)
 
@@ -322,7 +341,8 @@ class DeviceModel:
                 setattr(blk, f"{name}_img", _lib.u16ptr(dev(img.view(np.int16), torch.int16)))
                 setattr(blk, f"{name}_exp", e)
             w0, b0 = dense(f0)
-            blk.f_hexp = edge_h_exp(w0, b0)
+            blk.f_hexp = edge_h_exp(w0, b0, params.rbf.centers, float(params.rbf.gamma),
+                                    float(cfg.cutoff))
             blk.f_dbexp = edge_db_exp(float(np.float32(params.rbf.gamma)), float(cfg.cutoff))
             blk.f1_qmax = 1.0 if isinstance(f1, tuple) else float(np.max(f1.scale))
             blk.f_vexp = edge_v_exp(w0, params.rbf.centers, float(params.rbf.gamma),
