@@ -625,7 +625,9 @@ __device__ __forceinline__ void tile_h(const Wctx &W, float rs0, float b0c, cons
   tc::tmem_ld32w(W.tl + S0, v);
 #pragma unroll
   for (int i = 0; i < TT; ++i) {
-    if (Q) v[i] = __half2float(__float2half_rn(ssp_fast(v[i] * rs0 + b0c)));
+    // W16: fp16(ssp(z)) (quantize.py:80-88) — put8's hi-only pack rounds to
+    // fp16 (RN), so the value goes in unrounded
+    if (Q) v[i] = ssp_fast(v[i] * rs0 + b0c);
     else v[i] = ssp_scaled(v[i] * hk.rs + hk.b, hk.c_ln2, hk.c_e);  // = hs * ssp(z)
   }
 #pragma unroll
@@ -838,7 +840,7 @@ __device__ __forceinline__ void tile_h_bwd(const Wctx &W, float rs0, float b0c, 
       if (Q) {
         const float z = v[i + j] * rs0 + b0c;
         s[j] = sigmoid_fast(z) * kz;
-        v[i + j] = __half2float(__float2half_rn(ssp_fast(z)));
+        v[i + j] = ssp_fast(z);  // rounded to fp16 by put8's hi-only pack
       } else {
         v[i + j] = ssp_scaled(v[i + j] * hk.rs + hk.b, hk.c_ln2, hk.c_e);  // hs * h
         s[j] = fmaf(-0.5f * kz, ex2_ftz(v[i + j] * hk.c_e), kz);        // kz (1 - e^-h / 2)
@@ -1841,7 +1843,7 @@ k_edge_bwd_fm(const EdgeArgs a, const float4 *geo, const float2 *env,
         if (Q) {
           const float zz = z[i] * rs0 + b0c;
           sp = sigmoid_fast(zz) * kv;
-          z[i] = __half2float(__float2half_rn(ssp_fast(zz)));
+          z[i] = ssp_fast(zz);  // rounded to fp16 by put8's hi-only pack (quantize.py:80-88)
         } else {
           z[i] = ssp_scaled(z[i] * hk.rs + hk.b, hk.c_ln2, hk.c_e);  // hs * h
           sp = fmaf(-0.5f * kv, ex2_ftz(z[i] * hk.c_e), kv);         // kv (1 - e^-h / 2)
@@ -2151,7 +2153,7 @@ k_edge_bwd_fmws(const EdgeArgs a, const float4 *geo, const float2 *env,
         if (Q) {
           const float zz = z[i] * rs0 + b0c;
           sp = sigmoid_fast(zz) * kv;
-          z[i] = __half2float(__float2half_rn(ssp_fast(zz)));
+          z[i] = ssp_fast(zz);  // rounded to fp16 by put8's hi-only pack (quantize.py:80-88)
         } else {
           z[i] = ssp_scaled(z[i] * hk.rs + hk.b, hk.c_ln2, hk.c_e);  // hs * h
           sp = fmaf(-0.5f * kv, ex2_ftz(z[i] * hk.c_e), kv);         // kv (1 - e^-h / 2)
