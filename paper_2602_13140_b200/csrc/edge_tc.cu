@@ -596,11 +596,15 @@ __device__ __forceinline__ void tile_basis(const EdgeArgs &a, const Wctx &W, con
       pp[0] = p4.x; pp[1] = p4.y; pp[2] = p4.z; pp[3] = p4.w;
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float dl = dd[i] - mu;
+    for (int i = 0; i < 4; i += 2) {
+      const float2 dl = add2(make_float2(dd[i], dd[i + 1]), f2(-mu));
       // exp(-g dl^2) * 2^log2_scale in one ex2: the operand scale is free
-      const float gs = ex2_ftz(fmaf(ngl * dl, dl, log2_scale));
-      v[4 * j + i] = DERIV ? gs * (g2 * dl * cc[i] + pp[i]) : gs * cc[i];
+      const float2 gs = ex2_2(fma2(mul2(f2(ngl), dl), dl, f2(log2_scale)));
+      const float2 c = make_float2(cc[i], cc[i + 1]);
+      const float2 r = DERIV ? mul2(gs, fma2(mul2(f2(g2), dl), c, make_float2(pp[i], pp[i + 1])))
+                             : mul2(gs, c);
+      v[4 * j + i] = r.x;
+      v[4 * j + i + 1] = r.y;
     }
   }
   constexpr bool LO = DERIV || !Q;
@@ -623,12 +627,15 @@ template <bool Q, uint32_t KS = KSTR>
 __device__ __forceinline__ void tile_h(const Wctx &W, float rs0, float b0c, const HScale &hk) {
   float v[TT];
   tc::tmem_ld32w(W.tl + S0, v);
+  // fp32: hs * ssp(z); W16: ssp(z), rounded to fp16 (quantize.py:80-88) by
+  // put8's hi-only pack (RN).  A pair of edges per instruction.
+  const float rs = Q ? rs0 : hk.rs, bb = Q ? b0c : hk.b;
+  const float cl = Q ? kLn2 : hk.c_ln2, ce = Q ? -kLog2e : hk.c_e;
 #pragma unroll
-  for (int i = 0; i < TT; ++i) {
-    // W16: fp16(ssp(z)) (quantize.py:80-88) — put8's hi-only pack rounds to
-    // fp16 (RN), so the value goes in unrounded
-    if (Q) v[i] = ssp_fast(v[i] * rs0 + b0c);
-    else v[i] = ssp_scaled(v[i] * hk.rs + hk.b, hk.c_ln2, hk.c_e);  // = hs * ssp(z)
+  for (int i = 0; i < TT; i += 2) {
+    const float2 h = ssp_scaled2(fma2(make_float2(v[i], v[i + 1]), f2(rs), f2(bb)), cl, ce);
+    v[i] = h.x;
+    v[i + 1] = h.y;
   }
 #pragma unroll
   for (int j = 0; j < TT / 8; ++j) put8<!Q, KS>(W.hb, D, W.ch, W.eo + 8 * j, &v[8 * j], 1.f);
@@ -1127,7 +1134,12 @@ k_edge_fwd64(const EdgeArgs a, const float4 *geo, const float2 *env,
       const int n_e = min(TT, tr.ee - t0);
       if (n_e > 0) {  // m = (W1 h + b1) * P[src], dst segment sums
 #pragma unroll
-        for (int i = 0; i < TT; ++i) v[i] = (v[i] * s1 + b1c) * pv[i];
+        for (int i = 0; i < TT; i += 2) {
+          const float2 m = mul2(fma2(make_float2(v[i], v[i + 1]), f2(s1), f2(b1c)),
+                                make_float2(pv[i], pv[i + 1]));
+          v[i] = m.x;
+          v[i + 1] = m.y;
+        }
         if (SC) {
           scatter_tile(seg.outc, W.meta(it)->own, v, n_e);
         } else {
@@ -1318,7 +1330,12 @@ k_edge_fwd_ws(const EdgeArgs a, const float4 *geo, const float2 *env,
       const int n_e = min(TT, tr.ee - t0);
       if (n_e > 0) {  // m = (W1 h + b1) * P[src], dst segment sums
 #pragma unroll
-        for (int i = 0; i < TT; ++i) v[i] = (v[i] * s1 + b1c) * pv[i];
+        for (int i = 0; i < TT; i += 2) {
+          const float2 m = mul2(fma2(make_float2(v[i], v[i + 1]), f2(s1), f2(b1c)),
+                                make_float2(pv[i], pv[i + 1]));
+          v[i] = m.x;
+          v[i + 1] = m.y;
+        }
         if (SC) {
           scatter_tile(seg.outc, W.meta(it)->own, v, n_e);
         } else {
@@ -1838,17 +1855,19 @@ k_edge_bwd_fm(const EdgeArgs a, const float4 *geo, const float2 *env,
       tc::tmem_ld16w(W.tl + c0, z);
       tc::tmem_ld16w(W.tl + C::RH + c0, dz);
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        float sp;  // kv * ssp'(z0)
-        if (Q) {
+      for (int i = 0; i < 16; i += Q ? 1 : 2) {
+        if (Q) {  // scalar: pairing the W16 loop costs that kernel a spill
           const float zz = z[i] * rs0 + b0c;
-          sp = sigmoid_fast(zz) * kv;
+          dz[i] *= sigmoid_fast(zz) * kv;  // kv * ssp'(z0)
           z[i] = ssp_fast(zz);  // rounded to fp16 by put8's hi-only pack (quantize.py:80-88)
-        } else {
-          z[i] = ssp_scaled(z[i] * hk.rs + hk.b, hk.c_ln2, hk.c_e);  // hs * h
-          sp = fmaf(-0.5f * kv, ex2_ftz(z[i] * hk.c_e), kv);         // kv (1 - e^-h / 2)
+        } else {  // a pair of edges per instruction
+          const float2 h = ssp_scaled2(fma2(make_float2(z[i], z[i + 1]), f2(hk.rs), f2(hk.b)),
+                                       hk.c_ln2, hk.c_e);                       // hs * h
+          const float2 sp = fma2(f2(-0.5f * kv), ex2_2(mul2(h, f2(hk.c_e))), f2(kv));  // kv ssp'
+          const float2 d = mul2(make_float2(dz[i], dz[i + 1]), sp);
+          z[i] = h.x; z[i + 1] = h.y;
+          dz[i] = d.x; dz[i + 1] = d.y;
         }
-        dz[i] *= sp;
       }
 #pragma unroll
       for (int j = 0; j < 16; j += 8) {
@@ -1913,7 +1932,12 @@ k_edge_bwd_fm(const EdgeArgs a, const float4 *geo, const float2 *env,
         tc::tmem_ld16w(W.tl + h, v);  // w accumulator
         if (n_e > 0) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = h + i < n_e ? gh[h + i] * (v[i] * s1 + b1c) : 0.f;
+          for (int i = 0; i < 16; i += 2) {
+            const float2 m = mul2(make_float2(gh[h + i], gh[h + i + 1]),
+                                  fma2(make_float2(v[i], v[i + 1]), f2(s1), f2(b1c)));
+            v[i] = h + i < n_e ? m.x : 0.f;
+            v[i + 1] = h + i + 1 < n_e ? m.y : 0.f;
+          }
           seg.half(M->own, v, h, st);
         }
       }
@@ -2148,17 +2172,19 @@ k_edge_bwd_fmws(const EdgeArgs a, const float4 *geo, const float2 *env,
       tc::tmem_ld16w(W.tl + c0, z);
       tc::tmem_ld16w(W.tl + C::RH + c0, dz);
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        float sp;  // kv * ssp'(z0)
-        if (Q) {
+      for (int i = 0; i < 16; i += Q ? 1 : 2) {
+        if (Q) {  // scalar: pairing the W16 loop costs that kernel a spill
           const float zz = z[i] * rs0 + b0c;
-          sp = sigmoid_fast(zz) * kv;
+          dz[i] *= sigmoid_fast(zz) * kv;  // kv * ssp'(z0)
           z[i] = ssp_fast(zz);  // rounded to fp16 by put8's hi-only pack (quantize.py:80-88)
-        } else {
-          z[i] = ssp_scaled(z[i] * hk.rs + hk.b, hk.c_ln2, hk.c_e);  // hs * h
-          sp = fmaf(-0.5f * kv, ex2_ftz(z[i] * hk.c_e), kv);         // kv (1 - e^-h / 2)
+        } else {  // a pair of edges per instruction
+          const float2 h = ssp_scaled2(fma2(make_float2(z[i], z[i + 1]), f2(hk.rs), f2(hk.b)),
+                                       hk.c_ln2, hk.c_e);                       // hs * h
+          const float2 sp = fma2(f2(-0.5f * kv), ex2_2(mul2(h, f2(hk.c_e))), f2(kv));  // kv ssp'
+          const float2 d = mul2(make_float2(dz[i], dz[i + 1]), sp);
+          z[i] = h.x; z[i + 1] = h.y;
+          dz[i] = d.x; dz[i + 1] = d.y;
         }
-        dz[i] *= sp;
       }
 #pragma unroll
       for (int j = 0; j < 16; j += 8) {
@@ -2219,7 +2245,12 @@ k_edge_bwd_fmws(const EdgeArgs a, const float4 *geo, const float2 *env,
         tc::tmem_ld16w(W.tl + h, v);  // w accumulator
         if (n_e > 0) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = h + i < n_e ? gh[h + i] * (v[i] * s1 + b1c) : 0.f;
+          for (int i = 0; i < 16; i += 2) {
+            const float2 m = mul2(make_float2(gh[h + i], gh[h + i + 1]),
+                                  fma2(make_float2(v[i], v[i + 1]), f2(s1), f2(b1c)));
+            v[i] = h + i < n_e ? m.x : 0.f;
+            v[i + 1] = h + i + 1 < n_e ? m.y : 0.f;
+          }
           seg.half(M->own, v, h, st);
         }
       }
@@ -2234,8 +2265,14 @@ k_edge_bwd_fmws(const EdgeArgs a, const float4 *geo, const float2 *env,
         const int4 o4 = *(const int4 *)&M->own[j];
         const int oo[4] = {o4.x, o4.y, o4.z, o4.w};
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          q[j + i] *= gh[j + i] * (oo[i] == o_l ? pl : (oo[i] == o_f ? pf : pm));
+        for (int i = 0; i < 4; i += 2) {
+          const float2 pp = make_float2(oo[i] == o_l ? pl : (oo[i] == o_f ? pf : pm),
+                                        oo[i + 1] == o_l ? pl : (oo[i + 1] == o_f ? pf : pm));
+          const float2 r = mul2(mul2(make_float2(q[j + i], q[j + i + 1]),
+                                     make_float2(gh[j + i], gh[j + i + 1])), pp);
+          q[j + i] = r.x;
+          q[j + i + 1] = r.y;
+        }
       }
     } else {  // four or more rows (~5% of coil-269 tiles): per-edge gathers
 #pragma unroll

@@ -156,4 +156,26 @@ __device__ __forceinline__ float sigmoid_fast(float x) {
   return rcp_ftz(1.f + ex2_ftz(x * -kLog2e));
 }
 
+// ---- packed fp32x2 (sm_100 FFMA2 / FMUL2 / FADD2) ----------------------------
+// The edge epilogues are issue-bound; every elementwise step on a pair of
+// values is one instruction.  Round-to-nearest per element, so results are
+// bitwise those of the scalar forms.
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+// c_ln2 * lg2(0.5 t + 0.5) + max(x, 0) with t = 2^(|x| c_e): ssp_scaled on a pair
+__device__ __forceinline__ float2 ssp_scaled2(float2 xs, float c_ln2, float c_e) {
+  const float2 t = make_float2(ex2_ftz(fabsf(xs.x) * c_e), ex2_ftz(fabsf(xs.y) * c_e));
+  const float2 u = fma2(t, f2(0.5f), f2(0.5f));
+  const float2 l = make_float2(lg2_ftz(u.x), lg2_ftz(u.y));
+  return fma2(f2(c_ln2), l, make_float2(fmaxf(xs.x, 0.f), fmaxf(xs.y, 0.f)));
+}
+__device__ __forceinline__ float2 ssp_fast2(float2 x) {
+  return ssp_scaled2(x, kLn2, -kLog2e);
+}
+__device__ __forceinline__ float2 ex2_2(float2 x) {
+  return make_float2(ex2_ftz(x.x), ex2_ftz(x.y));
+}
+
 }  // namespace fcg
