@@ -2238,11 +2238,15 @@ k_edge_bwd_fmws(const EdgeArgs a, const float4 *geo, const float2 *env,
                  count_of(it + 2), W.q, lane);
     float q[TT];
     {
+      tc::tmem_ld32w(W.tl + C::RH, q);  // u accumulator
       const unsigned st = n_e > 0 ? seg.starts_n(M->own, n_e) : 0u;
 #pragma unroll
       for (int h = 0; h < TT; h += 16) {
         float v[16];
         tc::tmem_ld16w(W.tl + h, v);  // w accumulator
+        // the tile's TMEM is read: the next G1 | G1' may write it while the
+        // segment sums run
+        if (h + 16 == TT && more) ws_ready(&wsh->ready[W.g][BAR_G1]);
         if (n_e > 0) {
 #pragma unroll
           for (int i = 0; i < 16; i += 2) {
@@ -2254,10 +2258,8 @@ k_edge_bwd_fmws(const EdgeArgs a, const float4 *geo, const float2 *env,
           seg.half(M->own, v, h, st);
         }
       }
-      tc::tmem_ld32w(W.tl + C::RH, q);  // u accumulator
     }
     STAMP(1, (W.w & 7) == 0, W.g, it, 6);
-    if (more) ws_ready(&wsh->ready[W.g][BAR_G1]);  // TMEM read: next G1 | G1' may write
     if (rows3) {
       pf *= ku; pm *= ku; pl *= ku;
 #pragma unroll
