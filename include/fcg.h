@@ -62,7 +62,9 @@ enum {
   FCG_ST_BLOWUP = 3,      /* sticky: |F| > 1e6 or non-finite (md.py:183)   */
   FCG_ST_BLOWUP_STEP = 4, /* first step index at which BLOWUP was raised   */
   FCG_ST_EDGE_SUM = 5,    /* running sum of EDGES over builds              */
-  FCG_ST_BUILDS = 6       /* number of neighbour builds                    */
+  FCG_ST_BUILDS = 6,      /* number of neighbour builds                    */
+  FCG_ST_ARRIVE = 7       /* internal: arrivals of the MD step's BAOA CTAs
+                             (self-resetting; zero between steps)          */
 };
 
 /* Weight formats of fcg_model.format. */

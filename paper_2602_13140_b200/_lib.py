@@ -18,7 +18,7 @@ FCG_OK, FCG_ERR_CAPACITY, FCG_ERR_ARG, FCG_ERR_CUDA = 0, 1, 2, 3
 FCG_FMT_FP32, FCG_FMT_W16 = 0, 1
 FCG_STATUS_WORDS = 8
 FCG_SCHED_SEGRED, FCG_SCHED_SCATTER = 0, 1   # include/fcg.h
-ST_EDGES, ST_OVERFLOW, ST_MAXDEG, ST_BLOWUP, ST_BLOWUP_STEP, ST_EDGE_SUM, ST_BUILDS = range(7)
+ST_EDGES, ST_OVERFLOW, ST_MAXDEG, ST_BLOWUP, ST_BLOWUP_STEP, ST_EDGE_SUM, ST_BUILDS, ST_ARRIVE = range(8)
 
 _f = C.POINTER(C.c_float)
 _u16 = C.POINTER(C.c_uint16)

@@ -211,10 +211,13 @@ int fcg_md_step(const fcg_model *m, const fcg_prior *pr, const fcg_md_params *p,
 
   int rc;
   // leading B + A + O + A with the forces of the current state (md.py:200-202)
-  if ((rc = langevin_leading(p, mass, R, N, forces, step, pos, vel, ring, s))) return rc;
+  if ((rc = langevin_leading(p, mass, R, N, forces, step, pos, vel, ring, status, s))) return rc;
   // force evaluation at the new positions (md.py:203, _ReplicaForces)
+  // (the fused assembly for N <= 512 is launched by the force evaluation,
+  // together with the edge geometry)
+  NbrDefer defer{};
   if ((rc = nbr_build(pos, R, N, r_cut, cap_e, ptr, nbr, rev, own, status, ws_nbr, nb, s, step,
-                      p->neighbor_stride)))
+                      p->neighbor_stride, &defer)))
     return rc;
   (void)fprior;
   // model forces + prior (evaluated inline by the force assembly, which also
@@ -222,7 +225,7 @@ int fcg_md_step(const fcg_model *m, const fcg_prior *pr, const fcg_md_params *p,
   // (md.py:204-205)
   return energy_forces(m, pos, types, R, N, ptr, nbr, rev, own, cap_e, per_atom, potential,
                        forces, ws_ef, eb, s, nullptr, p, mass, vel, status, step, p->schedule,
-                       pr, prior);
+                       pr, prior, &defer);
 }
 
 }  // extern "C"

@@ -168,11 +168,14 @@ struct ProfScope {
 
 // ---- launchers implemented across the .cu files -----------------------------
 namespace fcg {
+struct NbrDefer;
+struct GeomJob;
 // nbr.cu
 size_t nbr_ws_bytes(int R, int N);
 int nbr_build(const float *pos, int R, int N, double r_cut, int64_t cap_e, int32_t *ptr,
               int32_t *nbr, int32_t *rev, int32_t *own, int64_t *status, void *ws,
-              size_t ws_bytes, cudaStream_t s, const int64_t *gate = nullptr, int stride = 1);
+              size_t ws_bytes, cudaStream_t s, const int64_t *gate = nullptr, int stride = 1,
+              NbrDefer *defer = nullptr);
 int nbr_build_f64(const double *pos, int R, int N, double r_cut, int64_t cap_e, int32_t *ptr,
                   int32_t *nbr, int32_t *rev, int32_t *own, int64_t *status, void *ws,
                   size_t ws_bytes, cudaStream_t s);
@@ -192,7 +195,8 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
                   float *forces, void *ws, size_t ws_bytes, cudaStream_t s,
                   const float *f_extra, const fcg_md_params *kick, const float *mass,
                   float *vel, int64_t *status, const int64_t *step, int schedule = 0,
-                  const fcg_prior *prior = nullptr, float *prior_e = nullptr);
+                  const fcg_prior *prior = nullptr, float *prior_e = nullptr,
+                  const NbrDefer *defer = nullptr);
 // md.cu
 int normal_noise(uint64_t seed, int rep_offset, const int64_t *step, int R, int N, float *out,
                  cudaStream_t s);
@@ -206,7 +210,7 @@ int step_advance(int64_t *step, cudaStream_t s);
 size_t noise_ring_bytes(int R, int N);
 int langevin_leading(const fcg_md_params *p, const float *mass, int R, int N,
                      const float *forces, int64_t *step, float *pos, float *vel, void *ring_ws,
-                     cudaStream_t s);
+                     int64_t *status, cudaStream_t s);
 // node_tc.cu
 void node_tc_configure();
 void launch_node_pre_tc(const float *X, const fcg_block &b, int quant, float *P, int nrows,
@@ -238,6 +242,31 @@ struct EmbedJob {
 void launch_edge_geom(const EdgeArgs &a, float4 *geo, float2 *env, int32_t *unit_rows,
                       int nunits, int32_t *unit_rows_fwd, int nunits_fwd, const EmbedJob &ej,
                       cudaStream_t s);
+// k_edge_geom's work (geometry, work-unit row boundaries, embedding) for a
+// kernel that writes or owns the CSR rows (geo == nullptr: none).
+struct GeomJob {
+  const float *pos;
+  float cutoff;
+  float4 *geo;
+  float2 *env;
+  int32_t *ur[2];
+  int nu[2];
+  EmbedJob ej;
+};
+// The fused neighbour assembly (N <= 512) handed by nbr_build to the force
+// evaluation, which launches it together with the edge geometry (fcg_md_step).
+struct NbrDefer {
+  bool active;
+  const uint32_t *masks;
+  const int32_t *rep_total;
+  int R, N;
+  int64_t cap_e;
+  int32_t *ptr, *nbr, *rev, *own;
+  int64_t *status;
+  const int64_t *gate;
+  int stride;
+};
+void launch_nbr_assemble(const NbrDefer &d, const GeomJob &gj, cudaStream_t s);
 void launch_edge_fwd_tc(const EdgeArgs &a, const float4 *geo, const float2 *env,
                         const int32_t *unit_rows, const float *P, float *H, int grid,
                         cudaStream_t s, bool scatter = false);

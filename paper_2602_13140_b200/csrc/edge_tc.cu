@@ -51,6 +51,7 @@
 #include "common.cuh"
 #include "tc.cuh"
 #include "tc_ops.cuh"
+#include "geom.cuh"
 
 namespace fcg {
 
@@ -217,53 +218,15 @@ k_edge_geom(const float *pos, const int32_t *ptr, const int32_t *nbr, const int3
   __syncthreads();  // keeps ptxas from hoisting loads above the wait
   long long e_tot = ld_dep(&ptr[nrows]);
   if (e_tot > cap_e) e_tot = cap_e;
-  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r <= nrows;
-       r += (long long)gridDim.x * blockDim.x) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x,
+                  nt = (long long)gridDim.x * blockDim.x;
+  for (long long r = t; r <= nrows; r += nt) {
     const long long lo = r == 0 ? -1 : ld_dep(&ptr[r - 1]), hi = ld_dep(&ptr[r]);
-#pragma unroll 1
-    for (int part = 0; part < 2; ++part) {  // backward (4 groups) / forward partitions
-      int32_t *ur = part ? unit_rows2 : unit_rows;
-      const long long G = part ? nunits2 : nunits;
-      if (!ur) continue;
-      if (r == 0) {
-        ur[0] = 0;
-        ur[G] = nrows;
-      }
-      if (hi <= lo) continue;  // empty row: no boundary maps to it
-      long long u = lo < 0 ? 1 : (e_tot > 0 ? ((lo + 1) * G + e_tot - 1) / e_tot : G);
-      if (u < 1) u = 1;
-      for (; u < G && e_tot * u / G <= hi; ++u) ur[u] = (int32_t)r;
-    }
+    unit_rows_at(r, lo, hi, e_tot, unit_rows, nunits, nrows);    // backward (4 groups)
+    unit_rows_at(r, lo, hi, e_tot, unit_rows2, nunits2, nrows);  // forward partition
   }
-  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < e_tot;
-       k += (long long)gridDim.x * blockDim.x) {
-    const float *po = pos + (size_t)own[k] * 3, *pn = pos + (size_t)nbr[k] * 3;
-    float ux = __fsub_rn(po[0], pn[0]), uy = __fsub_rn(po[1], pn[1]), uz = __fsub_rn(po[2], pn[2]);
-    float d = __fsqrt_rn(__fadd_rn(__fadd_rn(__fmul_rn(ux, ux), __fmul_rn(uy, uy)), __fmul_rn(uz, uz)));
-    float c = 0.f, dc = 0.f;
-    if (d < cutoff) {  // cutoff_envelope(_grad), model.py:110-120
-      float sn, cs;
-      sincosf((3.14159265358979f * d) / cutoff, &sn, &cs);
-      c = 0.5f * (cs + 1.f);
-      dc = (float)(-0.5 * 3.141592653589793 / (double)cutoff) * sn;
-    }
-    geo[k] = make_float4(ux, uy, uz, d);
-    env[k] = make_float2(c, dc);
-  }
-  if (ej.X) {  // X = embedding[types] (flash.py:201) and the operand-bound words reset
-    if (blockIdx.x == 0 && (int)threadIdx.x < ej.namax)
-      ej.amax[threadIdx.x] = (threadIdx.x == 0 && ej.P0) ? __float_as_uint(ej.p0_amax) : 0u;
-    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-         q < (long long)nrows * (D / 4); q += (long long)gridDim.x * blockDim.x) {
-      const long long g = q / (D / 4);
-      const int c4 = (int)(q % (D / 4));
-      const int t = ld_dep(&ej.types[g % ej.N]);
-      *(float4 *)&ej.X[g * D + c4 * 4] = ld_dep((const float4 *)&ej.emb[(size_t)t * D + c4 * 4]);
-      if (ej.P0)  // block 0's pre-linear from the per-type table
-        *(float4 *)&ej.P0[g * D + c4 * 4] =
-            ld_dep((const float4 *)&ej.p0_table[(size_t)t * D + c4 * 4]);
-    }
-  }
+  for (long long k = t; k < e_tot; k += nt) edge_geom_one(pos, own[k], nbr[k], cutoff, geo, env, k);
+  embed_rows(ej, nrows, t, nt, blockIdx.x == 0);
 }
 
 // ---- descriptors and MMA chains ------------------------------------------------

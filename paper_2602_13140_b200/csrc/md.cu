@@ -176,9 +176,9 @@ k_normal_noise(uint64_t seed, int rep_offset, const int64_t *__restrict__ stepp,
 // The noise of a step depends only on (seed, replica, step) (md.py:127-131),
 // so the MD step generates it NOISE_RING steps at a time (R x NOISE_RING
 // warps instead of R) into a workspace ring.  A device tag {magic, seed,
-// rep_offset, base step} says which steps the ring holds; the two kernels
-// of the leading half-step (noise + BAOA, step advance) evaluate
-// ring_valid() on the same tag, and only the step advance rewrites it.
+// rep_offset, base step} says which steps the ring holds; every CTA of the
+// leading half-step kernel evaluates ring_valid() on the same tag, and only
+// the step advance (its last CTA to finish) rewrites it.
 struct NoiseTag {
   uint64_t magic, seed;
   int64_t rep_offset, base, layout;  // layout = R * 2^32 + 3N
@@ -232,12 +232,15 @@ int langevin_baoa(const fcg_md_params *p, const float *mass, int R, int N, const
 // step its NOISE_RING warps each generate one step of the replica's noise
 // (the same warps per refill as a separate noise launch would use), then the CTA
 // applies BAOA to the replica's 3N coordinates with this step's slot —
-// only replica r's noise is read, so a CTA barrier orders the two.
+// only replica r's noise is read, so a CTA barrier orders the two.  The
+// last CTA to finish (an arrival counter in the status words, reset by
+// that CTA) then advances the step and, after a refill, the ring tag —
+// every CTA has read both before it arrives.
 static_assert(NOISE_RING * 32 <= 1024, "one warp per ring step");
 __global__ void __launch_bounds__(NOISE_RING * 32)
 k_noise_baoa_ring(fcg_md_params p, const float *mass, int N, int R, const float *F,
-                  const NoiseTag *tag, const int64_t *stepp, float *ring, float *pos,
-                  float *vel) {
+                  NoiseTag *tag, int64_t *stepp, float *ring, float *pos,
+                  float *vel, unsigned long long *arrive) {
   pdl_trigger();
   pdl_wait();
   const int r = blockIdx.x;
@@ -266,21 +269,22 @@ k_noise_baoa_ring(fcg_md_params p, const float *mass, int N, int R, const float 
     vr[k] = v;
     pr[k] = x;
   }
-}
-
-__global__ void k_step_advance_ring(int64_t *step, NoiseTag *tag, uint64_t seed, int rep_offset,
-                                    int64_t layout) {
-  pdl_trigger();
-  pdl_wait();
-  const int64_t s = *step;
-  if (!ring_valid(tag, seed, rep_offset, layout, s)) {
-    tag->magic = kNoiseMagic;
-    tag->seed = seed;
-    tag->rep_offset = rep_offset;
-    tag->layout = layout;
-    tag->base = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(arrive, 1ull) == (unsigned long long)gridDim.x - 1) {
+      __threadfence();
+      if (!valid) {
+        tag->magic = kNoiseMagic;
+        tag->seed = p.seed;
+        tag->rep_offset = p.rep_offset;
+        tag->layout = ((int64_t)R << 32) + n3;
+        tag->base = step;
+      }
+      *stepp = step + 1;
+      *arrive = 0ull;
+    }
   }
-  *step = s + 1;
 }
 
 size_t noise_ring_bytes(int R, int N) {
@@ -291,20 +295,16 @@ size_t noise_ring_bytes(int R, int N) {
 // with the ring noise, then step += 1.
 int langevin_leading(const fcg_md_params *p, const float *mass, int R, int N,
                      const float *forces, int64_t *step, float *pos, float *vel, void *ring_ws,
-                     cudaStream_t s) {
+                     int64_t *status, cudaStream_t s) {
   NoiseTag *tag = (NoiseTag *)ring_ws;
   float *ring = (float *)((char *)ring_ws + 256);
   const long long n = (long long)R * N * 3;
   (void)n;
   {
-    FCG_PROF(P_BAOA, s);  // noise refill (every NOISE_RING steps) + BAOA
+    FCG_PROF(P_BAOA, s);  // noise refill (every NOISE_RING steps) + BAOA + step advance
     launch_pdl(PDL_SMALL, k_noise_baoa_ring, R, NOISE_RING * 32, 0, s, *p, mass, N, R, forces,
-               tag, step, ring, pos, vel);
-  }
-  {
-    FCG_PROF(P_STEP, s);
-    launch_pdl(PDL_SMALL, k_step_advance_ring, 1, 1, 0, s, step, tag, p->seed, p->rep_offset,
-               ((int64_t)R << 32) + 3 * N);
+               tag, step, ring, pos, vel,
+               (unsigned long long *)(status + FCG_ST_ARRIVE));
   }
   return cuda_status("langevin_leading");
 }

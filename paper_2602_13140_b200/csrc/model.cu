@@ -725,7 +725,7 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
                   float *forces, void *ws, size_t ws_bytes, cudaStream_t s,
                   const float *f_extra, const fcg_md_params *kick, const float *mass,
                   float *vel, int64_t *status, const int64_t *step, int schedule,
-                  const fcg_prior *prior, float *prior_e) {
+                  const fcg_prior *prior, float *prior_e, const NbrDefer *defer) {
   if (!m || m->num_blocks < 0 || m->num_blocks > FCG_MAX_BLOCKS) {
     set_error("energy_forces: bad model descriptor");
     return FCG_ERR_ARG;
@@ -764,6 +764,11 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
   const bool p0_tab = m->pre0_table != nullptr && T > 0;
   const EmbedJob ej{m->embedding, types, N, b.X, b.amax, 2 * FCG_MAX_BLOCKS,
                     m->pre0_table, p0_tab ? b.P[0] : nullptr, m->pre0_amax};
+  const bool deferred = defer && defer->active;  // nbr_build left its assembly to us
+  if (deferred && simt) {
+    FCG_PROF(P_NBR_FILL, s);
+    launch_nbr_assemble(*defer, GeomJob{}, s);
+  }
   if (simt) {  // the tcgen05 path does the lookup inside k_edge_geom
     FCG_PROF(P_EMBED, s);
     launch_pdl(PDL_SMALL, k_embed, ceil_div((long long)RN * (D / 4), 256), 256, 0, s, m->embedding,
@@ -772,9 +777,16 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
   if (!simt) {
     edge_tc_configure();
     node_tc_configure();
-    FCG_PROF(P_EDGE_GEOM, s);
-    launch_edge_geom(ea, b.geo, b.env, b.unit_rows, edge_tc_units(eg), b.unit_rows + 2048,
-                     edge_tc_units_fwd(eg), ej, s);
+    if (deferred) {  // one launch: CSR assembly + geometry + unit rows + embedding
+      FCG_PROF(P_NBR_FILL, s);
+      const GeomJob gj{pos, m->cutoff, b.geo, b.env, {b.unit_rows, b.unit_rows + 2048},
+                       {edge_tc_units(eg), edge_tc_units_fwd(eg)}, ej};
+      launch_nbr_assemble(*defer, gj, s);
+    } else {
+      FCG_PROF(P_EDGE_GEOM, s);
+      launch_edge_geom(ea, b.geo, b.env, b.unit_rows, edge_tc_units(eg), b.unit_rows + 2048,
+                       edge_tc_units_fwd(eg), ej, s);
+    }
   }
 
   for (int t = 0; t < T; ++t) {

@@ -15,10 +15,12 @@
 // tests/test_oracle_golden.py against the reference).  We reproduce it with
 // explicit _rn intrinsics so nvcc cannot contract to DFMA.
 #include <stdlib.h>
+#include <type_traits>
 
 #include <cub/cub.cuh>
 
 #include "common.cuh"
+#include "geom.cuh"
 
 namespace fcg {
 
@@ -181,13 +183,24 @@ static size_t nbr_assemble_smem(int N) {
   return (2 * (size_t)N * W + (size_t)N + 1) * 4;
 }
 
+//
+// With a GeomJob (fcg_md_step: nbr_build defers this launch to the force
+// evaluation) the CTA also does k_edge_geom's work for its rows — geometry
+// of the slots it fills, the work-unit boundaries at its rows' CSR
+// boundaries (row i's end, ptr[rN+i+1], is known to the replica's CTAs),
+// and a share of the embedding lookup — which saves that launch.  When the
+// list is kept (neighbor_stride), the same work runs on the live CSR.
 __global__ void __launch_bounds__(512)
 k_nbr_assemble(const uint32_t *masks, const int32_t *rep_total, int R,
                int N, int64_t cap_e, int32_t *ptr, int32_t *nbr,
                int32_t *rev, int32_t *own, int64_t *status,
-               const int64_t *gate, int stride) {
+               const int64_t *gate, int stride, const GeomJob gj) {
   pdl_trigger();
   pdl_wait();
+  const long long cta = (long long)blockIdx.y * gridDim.x + blockIdx.x;
+  if (gj.geo)
+    embed_rows(gj.ej, R * N, cta * blockDim.x + threadIdx.x,
+               (long long)gridDim.x * gridDim.y * blockDim.x, cta == 0);
   // dynamic smem: bit words [N*W] | exclusive popcount per word [N*W] | row offsets [N+1]
   extern __shared__ uint32_t dsm[];
   const int W = (N + 31) / 32;
@@ -198,12 +211,27 @@ k_nbr_assemble(const uint32_t *masks, const int32_t *rep_total, int R,
   const int r = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long long RN = (long long)R * N;
   if (gate && stride > 1 && (*gate % stride) != 0) {  // list kept: only account the step
+    const long long e = ptr[RN];
     if (r == 0 && blockIdx.y == 0 && tid == 0) {
-      const long long e = ptr[RN];
       status[FCG_ST_EDGES] = e;
       if (e > cap_e) status[FCG_ST_OVERFLOW] = 1;
       status[FCG_ST_EDGE_SUM] += e;
       status[FCG_ST_BUILDS] += 1;
+    }
+    if (gj.geo) {  // the geometry of the live list (k_edge_geom's work on this CTA's rows)
+      const long long e_tot = e < cap_e ? e : cap_e;
+      const int rows_per = (N + (int)gridDim.y - 1) / (int)gridDim.y;
+      const int i0 = (int)blockIdx.y * rows_per, i1 = min(N, i0 + rows_per);
+      if (cta == 0 && tid == 0)
+        for (int q = 0; q < 2; ++q) unit_rows_at(0, -1, ptr[0], e_tot, gj.ur[q], gj.nu[q], RN);
+      for (int i = i0 + tid; i < i1; i += blockDim.x) {
+        const long long g = (long long)r * N + i;
+        for (int q = 0; q < 2; ++q) unit_rows_at(g + 1, ptr[g], ptr[g + 1], e_tot, gj.ur[q], gj.nu[q], RN);
+      }
+      const long long k0 = min((long long)ptr[(long long)r * N + i0], e_tot);
+      const long long k1 = min((long long)ptr[(long long)r * N + i1], e_tot);
+      for (long long k = k0 + tid; k < k1; k += blockDim.x)
+        edge_geom_one(gj.pos, own[k], nbr[k], gj.cutoff, gj.geo, gj.env, k);
     }
     return;
   }
@@ -264,6 +292,16 @@ k_nbr_assemble(const uint32_t *masks, const int32_t *rep_total, int R,
   // fill: one warp per row, lane = source candidate of each 32-bit word, so
   // the lanes of a word write consecutive slots
   const bool rev_ok = total <= cap_e;
+  if (gj.geo) {  // work-unit boundaries at this CTA's rows' ends (and at 0)
+    const long long e_tot = total < cap_e ? total : cap_e;
+    if (r == 0 && blockIdx.y == 0 && tid == 0)
+      for (int q = 0; q < 2; ++q) unit_rows_at(0, -1, 0, e_tot, gj.ur[q], gj.nu[q], RN);
+    if (tid >= i0 && tid < i1) {
+      const long long g = (long long)r * N + tid;
+      for (int q = 0; q < 2; ++q)
+        unit_rows_at(g + 1, base + sm_off[tid], base + sm_off[tid + 1], e_tot, gj.ur[q], gj.nu[q], RN);
+    }
+  }
   const uint32_t below = (1u << lane) - 1u;
   for (int i = i0 + warp; i < i1; i += (int)(blockDim.x >> 5)) {
     if (base + sm_off[i + 1] > cap_e) continue;  // row past capacity: CSR invalid
@@ -279,6 +317,8 @@ k_nbr_assemble(const uint32_t *masks, const int32_t *rep_total, int R,
       own[slot] = (int32_t)((long long)r * N + i);
       if (rev_ok)
         rev[slot] = (int32_t)(base + sm_off[j] + sm_pre[j * W + ti] + __popc(sm_mask[j * W + ti] & ibit));
+      if (gj.geo)
+        edge_geom_one(gj.pos, r * N + i, r * N + j, gj.cutoff, gj.geo, gj.env, slot);
     }
   }
 }
@@ -517,7 +557,8 @@ template <typename T>
 int nbr_build_t(const T *pos, int R, int N, double r_cut, int64_t cap_e, int32_t *ptr,
                 int32_t *nbr, int32_t *rev, int32_t *own, int64_t *status, void *ws,
                 size_t ws_bytes, cudaStream_t s, const int64_t *gate = nullptr,
-                int stride = 1) {
+                int stride = 1, NbrDefer *defer = nullptr) {
+  if (defer) defer->active = false;
   if (R < 1 || N < 1) { set_error("nbr_build: need R >= 1 and N >= 1"); return FCG_ERR_ARG; }
 #ifdef FCG_DIAG_NO_NBR  // timing diagnosis only: keep the first list forever
   static int diag_calls = 0;
@@ -565,18 +606,13 @@ int nbr_build_t(const T *pos, int R, int N, double r_cut, int64_t cap_e, int32_t
                  (const int32_t *)ptr, cap_e, (int32_t *)nullptr, (int32_t *)nullptr, status, gate,
                  stride, masks, rep_total);
     }
-    {
+    const NbrDefer d{true, masks, rep_total, R, N, cap_e, ptr, nbr, rev, own, status, gate,
+                     stride};
+    if (defer && std::is_same<T, float>::value) {  // launched by the force evaluation
+      *defer = d;
+    } else {
       FCG_PROF(P_NBR_FILL, s);
-      static bool attr = false;
-      if (!attr) {
-        cudaFuncSetAttribute(k_nbr_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)nbr_assemble_smem(NBR_FUSED_MAX));
-        attr = true;
-      }
-      const dim3 agrid(R, (N + 95) / 96);  // ~96 rows per CTA
-      launch_pdl(PDL_SMALL, k_nbr_assemble, agrid, 512, nbr_assemble_smem(N), s,
-                 (const uint32_t *)masks, (const int32_t *)rep_total, R, N, cap_e, ptr, nbr, rev,
-                 own, status, gate, stride);
+      launch_nbr_assemble(d, GeomJob{}, s);
     }
     return cuda_status("nbr_build");
   }
@@ -649,9 +685,23 @@ int nbr_build_t(const T *pos, int R, int N, double r_cut, int64_t cap_e, int32_t
 
 int nbr_build(const float *pos, int R, int N, double r_cut, int64_t cap_e, int32_t *ptr,
               int32_t *nbr, int32_t *rev, int32_t *own, int64_t *status, void *ws,
-              size_t ws_bytes, cudaStream_t s, const int64_t *gate, int stride) {
+              size_t ws_bytes, cudaStream_t s, const int64_t *gate, int stride,
+              NbrDefer *defer) {
   return nbr_build_t(pos, R, N, r_cut, cap_e, ptr, nbr, rev, own, status, ws, ws_bytes, s, gate,
-                     stride);
+                     stride, defer);
+}
+
+void launch_nbr_assemble(const NbrDefer &d, const GeomJob &gj, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_nbr_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)nbr_assemble_smem(NBR_FUSED_MAX));
+    attr = true;
+  }
+  const dim3 agrid(d.R, (d.N + 95) / 96);  // ~96 rows per CTA
+  launch_pdl(PDL_SMALL, k_nbr_assemble, agrid, 512, nbr_assemble_smem(d.N), s, d.masks,
+             d.rep_total, d.R, d.N, d.cap_e, d.ptr, d.nbr, d.rev, d.own, d.status, d.gate,
+             d.stride, gj);
 }
 int nbr_build_f64(const double *pos, int R, int N, double r_cut, int64_t cap_e, int32_t *ptr,
                   int32_t *nbr, int32_t *rev, int32_t *own, int64_t *status, void *ws,
