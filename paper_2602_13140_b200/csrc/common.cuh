@@ -223,6 +223,18 @@ void launch_node_post_bwd_tc(const float *G, const fcg_block &b, int quant, cons
                              float *GH, int nrows, unsigned int *amax_gh, cudaStream_t s);
 void launch_readout_tc(const float *X, const fcg_model &m, float *per_atom, float *G, int nrows,
                        cudaStream_t s);
+// fused node launches (FCG_NODE_FUSE=0: the separate kernels above)
+void launch_node_post_pre_tc(const float *H, const fcg_block &b, const fcg_block &nxt, int quant,
+                             float *Zp, float *X, float *Pn, int nrows, const int32_t *csr_ptr,
+                             unsigned int *amax_p, cudaStream_t s);
+void launch_node_post_readout_tc(const float *H, const fcg_block &b, const fcg_model &m,
+                                 int quant, float *Zp, float *X, float *per_atom, float *G,
+                                 float *GH, int nrows, const int32_t *csr_ptr,
+                                 unsigned int *amax_gh, cudaStream_t s);
+void launch_node_prebwd_postbwd_tc(const float *GP, const fcg_block &b, const fcg_block &prv,
+                                   int quant, float *G, const float *Zp, float *GH, int nrows,
+                                   const int32_t *csr_ptr, unsigned int *amax_gh,
+                                   cudaStream_t s);
 // edge_tc.cu
 void edge_tc_configure();
 int edge_tc_units(int grid);      // work units of the backward edge kernel

@@ -719,6 +719,15 @@ static void configure_smem() {
   smem_configured = true;
 }
 
+// FCG_NODE_FUSE=0: one launch per node stage (A/B)
+static bool node_fuse_enabled() {
+  static const bool on = [] {
+    const char *v = getenv("FCG_NODE_FUSE");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, int R, int N,
                   const int32_t *ptr, const int32_t *nbr, const int32_t *rev,
                   const int32_t *own, int64_t cap_e, float *per_atom, float *energy,
@@ -789,11 +798,14 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
     }
   }
 
+  // fused node launches (tcgen05 path): post(t) + pre(t+1), post(T-1) +
+  // readout + post_bwd(T-1), pre_bwd(t) + post_bwd(t-1)
+  const bool nfuse = !simt && node_fuse_enabled() && T > 0;
   for (int t = 0; t < T; ++t) {
     const fcg_block &blk = m->blocks[t];
     ea.blk = blk;
     ea.amax_pg = b.amax + 2 * t;
-    if (!(t == 0 && p0_tab && !simt)) {
+    if (!(t == 0 && p0_tab && !simt) && !(nfuse && t > 0)) {
       FCG_PROF(P_NODE_PRE, s);
       if (simt)
         k_node_linear<true, false><<<node_grid, NT, sm1, s>>>(b.X, blk.pre_wt, blk.pre_b, b.P[t],
@@ -811,7 +823,15 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
         launch_edge_fwd_tc(ea, b.geo, b.env, b.unit_rows + 2048, b.P[t], b.H, eg, s, scatter);
       }
     }
-    {
+    if (nfuse && t + 1 < T) {
+      FCG_PROF(P_NODE_POST, s);
+      launch_node_post_pre_tc(b.H, blk, m->blocks[t + 1], quant, b.Zp[t], b.X, b.P[t + 1], RN,
+                              ptr, b.amax + 2 * (t + 1), s);
+    } else if (nfuse) {
+      FCG_PROF(P_NODE_POST, s);
+      launch_node_post_readout_tc(b.H, blk, *m, quant, b.Zp[t], b.X, per_atom, b.G, b.GH, RN,
+                                  ptr, b.amax + 2 * t + 1, s);
+    } else {
       FCG_PROF(P_NODE_POST, s);
       if (simt)
         k_node_post<<<node_grid, NT, sm2, s>>>(b.H, blk, b.Zp[t], b.X, RN, quant);
@@ -819,7 +839,7 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
         launch_node_post_tc(b.H, blk, quant, b.Zp[t], b.X, RN, ptr, s);
     }
   }
-  {
+  if (!nfuse) {
     FCG_PROF(P_READOUT, s);
     if (simt)
       k_readout<<<node_grid, NT, (TE * LDH + TE * LDR) * sizeof(float), s>>>(b.X, *m, per_atom,
@@ -831,7 +851,7 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
     const fcg_block &blk = m->blocks[t];
     ea.blk = blk;
     ea.amax_pg = b.amax + 2 * t;
-    {
+    if (!nfuse) {  // (fused: done by the launch before)
       FCG_PROF(P_NODE_POST_BWD, s);
       if (simt)
         k_node_post_bwd<<<node_grid, NT, sm2, s>>>(b.G, blk, b.Zp[t], b.GH, RN);
@@ -853,7 +873,12 @@ int energy_forces(const fcg_model *m, const float *pos, const int32_t *types, in
     // grad_X of block 0 (flash.py:300) is the gradient with respect to the
     // embedding output, which has no position dependence: forces never read
     // it, so the last pre-linear backward is skipped
-    if (t > 0) {
+    if (t > 0 && nfuse) {
+      FCG_PROF(P_NODE_PRE_BWD, s);
+      const fcg_block &prv = m->blocks[t - 1];
+      launch_node_prebwd_postbwd_tc(b.GP, blk, prv, quant, b.G, b.Zp[t - 1], b.GH, RN, ptr,
+                                    b.amax + 2 * (t - 1) + 1, s);
+    } else if (t > 0) {
       FCG_PROF(P_NODE_PRE_BWD, s);
       if (simt)
         k_node_linear<false, true><<<node_grid, NT, sm1, s>>>(b.GP, blk.pre_w, nullptr, b.G, RN, 0);

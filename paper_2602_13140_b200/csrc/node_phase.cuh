@@ -223,6 +223,25 @@ __device__ __forceinline__ void node_stage_weights(const NodeCtx &c, const uint1
   }
 }
 
+// A weight slot reloaded once the GEMM reading it has completed, so that a
+// chain of stages in one kernel (the fused node launches of node_tc.cu) has
+// its next image in place by the time it needs it.  The copy completes the
+// next phase of the weight barrier; every later node_issue waits for it.
+struct Restage {
+  uint32_t slot;
+  const uint16_t *img;
+  uint32_t bytes;
+};
+__device__ __forceinline__ void node_restage(NodeCtx &c, const Restage *r) {
+  if (!r) return;
+  if (threadIdx.x == 0) {  // thread 0 has seen the GEMM's completion barrier
+    uint8_t *base = (uint8_t *)__cvta_shared_to_generic(c.sbase);
+    tc::mbar_expect_tx(&c.meta->wbar, r->bytes);
+    tc::bulk_g2s(base + r->slot, r->img, r->bytes, &c.meta->wbar);
+  }
+  c.wphase ^= 1u;
+}
+
 // ---------------------------------------------------------------------------
 // Y = X W^T + b (pre-linear, flash.py:207)                      [mode 0]
 // Y += G_in W   (grad_X += grad_P @ W_pre, flash.py:300)        [mode 1]
@@ -231,7 +250,8 @@ template <int kMode, uint32_t KSTR, int NN>
 __device__ __forceinline__ void stage_linear(NodeCtx &c, const float *X, int wexp,
                                              const float *bias, const float *rowscale, int quant,
                                              float *Y, int node0, int rlim,
-                                             unsigned int *amax_out, const int32_t *csr_ptr) {
+                                             unsigned int *amax_out, const int32_t *csr_ptr,
+                                             const Restage *after = nullptr) {
   const size_t r0 = (size_t)(node0 + c.ec) * D + c.ch;  // this thread: rows r0 + i*D
   float *Yr = opaque_ptr(Y + r0);
   const bool fwd = kMode == 0;
@@ -249,6 +269,7 @@ __device__ __forceinline__ void stage_linear(NodeCtx &c, const float *X, int wex
     yv[i] = (!fwd && n < rlim) ? Yr[i * D] : 0.f;
   }
   node_wait(c);
+  node_restage(c, after);
   const float un = pow2f(-((quant ? 0 : wexp) + s)) * ((fwd && quant) ? ld_dep(&rowscale[c.ch]) : 1.f);
   const float b = fwd ? ld_dep(&bias[c.ch]) : 0.f;
   float mx = 0.f;
@@ -275,7 +296,9 @@ __device__ __forceinline__ void stage_linear(NodeCtx &c, const float *X, int wex
 template <uint32_t KSTR, int NN>
 __device__ __forceinline__ void stage_post(NodeCtx &c, const float *H, const fcg_block &blk,
                                            int quant, float *Zp, float *X, int node0, int rlim,
-                                           const int32_t *csr_ptr) {
+                                           const int32_t *csr_ptr,
+                                           const Restage *after1 = nullptr,
+                                           const Restage *after2 = nullptr) {
   const size_t r0 = (size_t)(node0 + c.ec) * D + c.ch;  // this thread: rows r0 + i*D
   float *Zpr = opaque_ptr(Zp + r0), *Xr = opaque_ptr(X + r0);
   const int np = quant ? 1 : 3;
@@ -283,6 +306,7 @@ __device__ __forceinline__ void stage_post(NodeCtx &c, const float *H, const fcg
   const int s0 = rows_to_act<KSTR>(H, node0, rlim, c, 1.f, quant, &c.meta->amax[0], csr_ptr);
   node_issue<KSTR>(c, c.tm + NTM_D0, NSM_WA, IMG128, D, false, D, idesc, np);
   node_wait(c);
+  node_restage(c, after1);
   const float un0 = quant ? ld_dep(&blk.p0_s[c.ch]) : pow2f(-(blk.p0_exp + s0));
   const float b0 = ld_dep(&blk.p0_b[c.ch]);
   float mx = 0.f;
@@ -315,6 +339,7 @@ __device__ __forceinline__ void stage_post(NodeCtx &c, const float *H, const fcg
     xv[i] = n < rlim ? Xr[i * D] : 0.f;
   }
   node_wait(c);
+  node_restage(c, after2);
   const float un1 = quant ? ld_dep(&blk.p1_s[c.ch]) : pow2f(-(blk.p1_exp + s1));
   const float b1 = ld_dep(&blk.p1_b[c.ch]);
 #pragma unroll
@@ -397,7 +422,8 @@ __device__ __forceinline__ void stage_post_bwd(NodeCtx &c, const float *G, const
 // Weights: r0 in slot A.  Scratch [NN][65] floats in the act area.
 template <uint32_t KSTR, int NN>
 __device__ __forceinline__ void stage_readout(NodeCtx &c, const float *X, const ReadoutW &m,
-                                              float *per_atom, float *G, int node0, int rlim) {
+                                              float *per_atom, float *G, int node0, int rlim,
+                                              const Restage *after = nullptr) {
   float *red = (float *)c.act;  // [NN nodes][65] after G1 completes
   const bool quant = m.format == FCG_FMT_W16;
   const size_t r0 = (size_t)(node0 + c.ec) * D + c.ch;  // this thread: rows r0 + i*D
@@ -446,6 +472,7 @@ __device__ __forceinline__ void stage_readout(NodeCtx &c, const float *X, const 
   node_issue<KSTR>(c, c.tm + NTM_D1, NSM_WA, IMG64, D, true, RH, tc::idesc_f16(128, NN, 1, 1),
                    quant ? 2 : 3);
   node_wait(c);
+  node_restage(c, after);
   const float un1 = pow2f(-((quant ? 0 : m.r0_exp) + sz));
 #pragma unroll
   for (int c0 = 0; c0 < NPT; c0 += 16) {

@@ -165,6 +165,67 @@ k_readout_tc(const float *X, const fcg_model m, float *per_atom,
   node_stamp(4, 7);
 }
 
+// ---- fused node launches ---------------------------------------------------
+// Consecutive row-local stages on the same chunk of node rows in one launch
+// (each thread reads back only rows it wrote itself, so no barrier is
+// needed between the stages beyond the ones inside them).  The weight slot
+// a stage no longer reads is reloaded with the next stage's image as soon as
+// its GEMM completes (Restage), overlapping the epilogue.
+
+// post(t) + pre(t+1): X(t+1) = X + post MLP, P(t+1) = X(t+1) W_pre^T + b
+__global__ void __launch_bounds__(CfgPost::NTH, CfgPost::MIN_CTAS)
+k_node_post_pre_tc(const float *H, const fcg_block blk, const fcg_block nxt, int quant,
+                   float *Zp, float *X, float *Pn, int nrows, const int32_t *csr_ptr,
+                   unsigned int *amax_p) {
+  using Cfg = CfgPost;
+  extern __shared__ __align__(1024) uint8_t sm[];
+  NodeCtx c = node_prologue<Cfg>(sm, blk.p0_img, 2 * IMG128, blk.p1_img, 2 * IMG128);
+  const int node0 = blockIdx.x * Cfg::NN;
+  const Restage pre{NSM_WA, nxt.pre_img, 2 * IMG128};
+  stage_post<Cfg::KSTR, Cfg::NN>(c, H, blk, quant, Zp, X, node0, nrows, csr_ptr, &pre);
+  node_chunk_reset(c);
+  stage_linear<0, Cfg::KSTR, Cfg::NN>(c, X, nxt.pre_exp, nxt.pre_b, nxt.pre_s, quant, Pn, node0,
+                                      nrows, amax_p, nullptr);
+  node_epilogue_end(c);
+}
+
+// post(T-1) + readout + post_bwd(T-1): the last block's forward tail and
+// the head of the backward
+__global__ void __launch_bounds__(CfgPost::NTH, CfgPost::MIN_CTAS)
+k_node_post_readout_tc(const float *H, const fcg_block blk, const ReadoutW ro, int quant,
+                       float *Zp, float *X, float *per_atom, float *G, float *GH, int nrows,
+                       const int32_t *csr_ptr, unsigned int *amax_gh) {
+  using Cfg = CfgPost;
+  extern __shared__ __align__(1024) uint8_t sm[];
+  NodeCtx c = node_prologue<Cfg>(sm, blk.p0_img, 2 * IMG128, blk.p1_img, 2 * IMG128);
+  const int node0 = blockIdx.x * Cfg::NN;
+  const Restage r0{NSM_WA, ro.r0_img, 2 * IMG64}, p0{NSM_WB, blk.p0_img, 2 * IMG128};
+  stage_post<Cfg::KSTR, Cfg::NN>(c, H, blk, quant, Zp, X, node0, nrows, csr_ptr, &r0, &p0);
+  node_chunk_reset(c);
+  const Restage p1{NSM_WA, blk.p1_img, 2 * IMG128};
+  stage_readout<Cfg::KSTR, Cfg::NN>(c, X, ro, per_atom, G, node0, nrows, &p1);
+  node_chunk_reset(c);
+  stage_post_bwd<Cfg::KSTR, Cfg::NN>(c, G, blk, quant, Zp, GH, node0, nrows, amax_gh);
+  node_epilogue_end(c);
+}
+
+// pre_bwd(t) + post_bwd(t-1): G += GP(t) W_pre(t), GH(t-1) from G
+__global__ void __launch_bounds__(CfgPost::NTH, CfgPost::MIN_CTAS)
+k_node_prebwd_postbwd_tc(const float *GP, const fcg_block blk, const fcg_block prv, int quant,
+                         float *G, const float *Zp, float *GH, int nrows,
+                         const int32_t *csr_ptr, unsigned int *amax_gh) {
+  using Cfg = CfgPost;
+  extern __shared__ __align__(1024) uint8_t sm[];
+  NodeCtx c = node_prologue<Cfg>(sm, blk.pre_img, 2 * IMG128, prv.p0_img, 2 * IMG128);
+  const int node0 = blockIdx.x * Cfg::NN;
+  const Restage p1{NSM_WA, prv.p1_img, 2 * IMG128};
+  stage_linear<1, Cfg::KSTR, Cfg::NN>(c, GP, blk.pre_exp, nullptr, blk.pre_s, quant, G, node0,
+                                      nrows, nullptr, csr_ptr, &p1);
+  node_chunk_reset(c);
+  stage_post_bwd<Cfg::KSTR, Cfg::NN>(c, G, prv, quant, Zp, GH, node0, nrows, amax_gh);
+  node_epilogue_end(c);
+}
+
 // ---------------------------------------------------------------------------
 void node_tc_configure() {
   static bool done = false;
@@ -174,6 +235,12 @@ void node_tc_configure() {
   cudaFuncSetAttribute(k_node_post_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, CfgPost::SMEM);
   cudaFuncSetAttribute(k_node_post_bwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, CfgPost::SMEM);
   cudaFuncSetAttribute(k_readout_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, CfgRo::SMEM);
+  cudaFuncSetAttribute(k_node_post_pre_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       CfgPost::SMEM);
+  cudaFuncSetAttribute(k_node_post_readout_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       CfgPost::SMEM);
+  cudaFuncSetAttribute(k_node_prebwd_postbwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       CfgPost::SMEM);
   done = true;
 }
 
@@ -202,6 +269,28 @@ void launch_node_post_bwd_tc(const float *G, const fcg_block &b, int quant, cons
                              float *GH, int nrows, unsigned int *amax_gh, cudaStream_t s) {
   launch_pdl(PDL_NODE_POST_BWD, k_node_post_bwd_tc, node_grid<CfgPost>(nrows), CfgPost::NTH,
              CfgPost::SMEM, s, G, b, quant, Zp, GH, nrows, amax_gh);
+}
+void launch_node_post_pre_tc(const float *H, const fcg_block &b, const fcg_block &nxt, int quant,
+                             float *Zp, float *X, float *Pn, int nrows, const int32_t *csr_ptr,
+                             unsigned int *amax_p, cudaStream_t s) {
+  launch_pdl(PDL_NODE_POST, k_node_post_pre_tc, node_grid<CfgPost>(nrows), CfgPost::NTH,
+             CfgPost::SMEM, s, H, b, nxt, quant, Zp, X, Pn, nrows, csr_ptr, amax_p);
+}
+void launch_node_post_readout_tc(const float *H, const fcg_block &b, const fcg_model &m,
+                                 int quant, float *Zp, float *X, float *per_atom, float *G,
+                                 float *GH, int nrows, const int32_t *csr_ptr,
+                                 unsigned int *amax_gh, cudaStream_t s) {
+  launch_pdl(PDL_NODE_POST, k_node_post_readout_tc, node_grid<CfgPost>(nrows), CfgPost::NTH,
+             CfgPost::SMEM, s, H, b, readout_view(m), quant, Zp, X, per_atom, G, GH, nrows,
+             csr_ptr, amax_gh);
+}
+void launch_node_prebwd_postbwd_tc(const float *GP, const fcg_block &b, const fcg_block &prv,
+                                   int quant, float *G, const float *Zp, float *GH, int nrows,
+                                   const int32_t *csr_ptr, unsigned int *amax_gh,
+                                   cudaStream_t s) {
+  launch_pdl(PDL_NODE_POST_BWD, k_node_prebwd_postbwd_tc, node_grid<CfgPost>(nrows),
+             CfgPost::NTH, CfgPost::SMEM, s, GP, b, prv, quant, G, Zp, GH, nrows, csr_ptr,
+             amax_gh);
 }
 void launch_readout_tc(const float *X, const fcg_model &m, float *per_atom, float *G, int nrows,
                        cudaStream_t s) {

@@ -11,6 +11,8 @@ test_gpu_parity.py in a subprocess (settings: space-separated VAR=value):
     reverse-mode 64-edge backward (k_edge_bwd64); with FCG_BWD64=0 too the
     4-group, 32-edge one (k_edge_bwd_tc);
   * FCG_EDGE_IMPL=simt: the SIMT edge kernels (with the separate k_embed);
+  * FCG_NODE_FUSE=0: one launch per node stage instead of the fused
+    post+pre, post+readout+post_bwd and pre_bwd+post_bwd launches;
   * FCG_NBR_FUSED=0 / FCG_NBR_WINDOW=0: the general neighbour builds, run
     through the CSR and large-system tests instead.
 """
@@ -38,7 +40,8 @@ def _run(setting, sel):
 
 @pytest.mark.parametrize("setting", ["FCG_FWD_WS=0", "FCG_FWD_WS=0 FCG_FWD64=0", "FCG_BWD_WS=0",
                                      "FCG_BWD_WS=0 FCG_BWD_UPG=1", "FCG_BWD_FM=0",
-                                     "FCG_BWD_FM=0 FCG_BWD64=0", "FCG_EDGE_IMPL=simt"])
+                                     "FCG_BWD_FM=0 FCG_BWD64=0", "FCG_EDGE_IMPL=simt",
+                                     "FCG_NODE_FUSE=0"])
 def test_alternative_edge_kernels_match_oracle(setting):
     _run(setting, "energy_forces_fp32 or energy_forces_w16 or batched_engine_matches_oracle")
 

@@ -14,7 +14,8 @@ import sys
 
 PDL_KERNELS = ("k_edge_geom", "k_edge_fwd_tc", "k_edge_bwd_tc", "k_edge_bwd64", "k_edge_fwd64",
                "k_edge_bwd_fm", "k_edge_bwd_fmws", "k_edge_fwd_ws", "k_node_linear_tc",
-               "k_node_post_tc", "k_node_post_bwd_tc", "k_readout_tc",
+               "k_node_post_tc", "k_node_post_bwd_tc", "k_readout_tc", "k_node_post_pre_tc",
+               "k_node_post_readout_tc", "k_node_prebwd_postbwd_tc",
                "k_noise_baoa_ring", "k_prior",
                "k_embed", "k_forces_finish", "k_scan_rows", "k_nbr_assemble",
                "k_fill_masks", "k_rev_masks")
