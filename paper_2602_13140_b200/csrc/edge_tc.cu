@@ -1650,16 +1650,20 @@ __device__ __forceinline__ void meta_issue(const EdgeArgs &a, const float4 *geo,
 
 // W1 hi | lo and W0 hi | lo from the staged images into TMEM: warp w moves
 // image (w / 4) % 4 for its lane quarter.
+// Threads from TC_THREADS on (the MMA warpgroup of the WS kernels) only join
+// the closing barrier: every thread reaches the same bar.sync.
 __device__ __forceinline__ void load_fm_weights_tmem(const uint8_t *sm, uint32_t tmem) {
   const int w = threadIdx.x >> 5, q = w & 3, m = 32 * q + (threadIdx.x & 31);
   const int img = (w >> 2) & 3;  // 0: W1 hi, 1: W1 lo, 2: W0 hi, 3: W0 lo
   const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16);
-  if (img < 2)
-    image_row_to_tmem<false>((const uint16_t *)(sm + SM_W1 + (img & 1) * W1_BYTES), D, m,
-                             lane_base + FM_TW1 + (img & 1) * (D / 2));
-  else
-    image_row_to_tmem<false>((const uint16_t *)(sm + SM_W0 + (img & 1) * W0_BYTES), DR, m,
-                             lane_base + FM_TW0 + (img & 1) * (DR / 2));
+  if (threadIdx.x < TC_THREADS) {
+    if (img < 2)
+      image_row_to_tmem<false>((const uint16_t *)(sm + SM_W1 + (img & 1) * W1_BYTES), D, m,
+                               lane_base + FM_TW1 + (img & 1) * (D / 2));
+    else
+      image_row_to_tmem<false>((const uint16_t *)(sm + SM_W0 + (img & 1) * W0_BYTES), DR, m,
+                               lane_base + FM_TW0 + (img & 1) * (DR / 2));
+  }
   prologue_done();
 }
 
@@ -2013,14 +2017,7 @@ k_edge_bwd_fmws(const EdgeArgs a, const float4 *geo, const float2 *env,
   __syncthreads();
   tc::fence_after_sync();
   tc::mbar_wait(&sh->wbar, 0);
-  if (threadIdx.x < TC_THREADS) {
-    load_fm_weights_tmem(sm, sh->tmem);  // ends with the PDL wait + block barrier
-  } else {
-    tc::fence_before_sync();
-    pdl_wait();
-    __syncthreads();
-    tc::fence_after_sync();
-  }
+  load_fm_weights_tmem(sm, sh->tmem);  // ends with the PDL wait + block barrier
   constexpr int NB = Q ? 1 : 3, NDB = Q ? 2 : 3, NH = Q ? 1 : 3, NV = Q ? 2 : 3;
   const uint32_t w0h = sh->tmem + FM_TW0, w0l = w0h + DR / 2;
   const uint32_t w1h = sh->tmem + FM_TW1, w1l = w1h + D / 2;
@@ -2245,12 +2242,15 @@ k_edge_bwd_fmws(const EdgeArgs a, const float4 *geo, const float2 *env,
         q[i] *= gh[i] * ld_gather(Pch + (uint32_t)M->own[i] * D) * ku;
     }
     STAMP(1, (W.w & 7) == 0, W.g, it, 7);
+    // the unit's four partial grad_d rows -> its first warp: a named barrier
+    // per unit (id 2 + u, 128 threads), arrive-only for the producers.  A
+    // producer cannot arrive for tile it+1 before the consumer has synced
+    // for tile it: that needs G2 | G3 of tile it+1, i.e. the consumer's E1.
     float *xg = &sh->xg[u][it & 1][0][0];
     xg[W.q * TT + lane] = warp_edge_sum(q, lane);
-    __syncwarp();
-    if (lane == 0) tc::mbar_arrive(&sh->xbar[u]);
+    if (W.q != 0) asm volatile("bar.arrive %0, 128;" ::"r"(2 + u) : "memory");
     if (W.q == 0) {
-      tc::mbar_wait(&sh->xbar[u], (uint32_t)(it & 1));
+      asm volatile("bar.sync %0, 128;" ::"r"(2 + u) : "memory");
       const int e = lane;
       if (e < n_e) {
         const float gd = ((xg[e] + xg[TT + e]) + xg[2 * TT + e]) + xg[3 * TT + e];

@@ -8,12 +8,12 @@ B="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-gpu-baseline --e2
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
   --log-file gpurun_out/launches_${TAG}.csv $B > gpurun_out/ncu_launch_${TAG}.log 2>&1
 echo "launch list exit $?" >> gpurun_out/ncu_launch_${TAG}.log
-for K in k_edge_bwd64 k_edge_fwd64; do
+for K in k_edge_bwd_fmws k_edge_fwd_ws; do
   timeout 900 ncu --set full --clock-control none --import-source on -k "regex:${K}" -s 3 -c 1 \
     -o gpurun_out/prof_${TAG}_${K} $B > gpurun_out/ncu_full_${TAG}_${K}.log 2>&1
   echo "full $K exit $?" >> gpurun_out/ncu_full_${TAG}_${K}.log
 done
-timeout 900 ncu --set full --clock-control none -k "regex:k_edge_geom|k_scan_rows|k_nbr_assemble|k_noise_ring|k_baoa_ring|k_prior|k_forces_finish|k_step_advance|k_node_linear_tc|k_node_post_tc|k_node_post_bwd_tc|k_readout_tc" -s 20 -c 14 \
+timeout 900 ncu --set full --clock-control none -k "regex:k_scan_rows|k_nbr_assemble|k_noise_baoa_ring|k_forces_finish|k_node_post_pre_tc|k_node_post_readout_tc|k_node_prebwd_postbwd_tc" -s 20 -c 12 \
   -o gpurun_out/prof_${TAG}_small $B > gpurun_out/ncu_full_${TAG}_small.log 2>&1
 echo "full small exit $?" >> gpurun_out/ncu_full_${TAG}_small.log
 for T in memcheck racecheck synccheck; do
