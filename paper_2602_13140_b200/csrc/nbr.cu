@@ -317,9 +317,16 @@ k_nbr_assemble(const uint32_t *masks, const int32_t *rep_total, int R,
       own[slot] = (int32_t)((long long)r * N + i);
       if (rev_ok)
         rev[slot] = (int32_t)(base + sm_off[j] + sm_pre[j * W + ti] + __popc(sm_mask[j * W + ti] & ibit));
-      if (gj.geo)
-        edge_geom_one(gj.pos, r * N + i, r * N + j, gj.cutoff, gj.geo, gj.env, slot);
     }
+  }
+  // geometry of this CTA's slots, all threads over the contiguous slot range
+  // (the fill's lanes are ~10% busy); an overflowing build is discarded by
+  // the host, so it gets none
+  if (gj.geo && rev_ok) {
+    __syncthreads();  // the fill's nbr / own stores are visible to the CTA
+    const long long k0 = base + sm_off[i0], k1 = base + sm_off[i1];
+    for (long long k = k0 + tid; k < k1; k += blockDim.x)
+      edge_geom_one(gj.pos, own[k], nbr[k], gj.cutoff, gj.geo, gj.env, k);
   }
 }
 
