@@ -2162,6 +2162,7 @@ k_edge_bwd_fmws(const EdgeArgs a, const float4 *geo, const float2 *env,
     int o_f = -1, o_l = -1;
     bool rows3 = true;
     float4 ue = make_float4(0.f, 0.f, 0.f, 0.f);
+    float3 acc = make_float3(0.f, 0.f, 0.f);  // the slot's grad from the later blocks
     if (n_e > 0) {
       const int o = M->own[lane];
       o_f = M->own[0];
@@ -2174,7 +2175,13 @@ k_edge_bwd_fmws(const EdgeArgs a, const float4 *geo, const float2 *env,
       pf = ld_gather(Pch + (uint32_t)o_f * D);  // scaled by ku where used
       pm = ld_gather(Pch + (uint32_t)mid * D);
       pl = ld_gather(Pch + (uint32_t)o_l * D);
-      if (W.q == 0 && lane < n_e) ue = ld_dep(&geo[t0 + lane]);
+      if (W.q == 0 && lane < n_e) {
+        ue = ld_dep(&geo[t0 + lane]);
+        if (accumulate) {  // issued a tile ahead of its use: off the iteration's tail
+          const float4 o = gsum[t0 + lane];
+          acc = make_float3(o.x, o.y, o.z);
+        }
+      }
     } else {
 #pragma unroll
       for (int i = 0; i < TT; ++i) gh[i] = 0.f;
@@ -2258,12 +2265,10 @@ k_edge_bwd_fmws(const EdgeArgs a, const float4 *geo, const float2 *env,
         const float inv = ue.w > TINY_DISTANCE ? 1.f / ue.w : 0.f;
         const float sc = -gd * inv;
         float4 g = make_float4(sc * ue.x, sc * ue.y, sc * ue.z, 0.f);
-        float4 *dst = &gsum[t0 + e];
         if (accumulate) {
-          const float4 o = *dst;
-          g.x += o.x; g.y += o.y; g.z += o.z;
+          g.x += acc.x; g.y += acc.y; g.z += acc.z;
         }
-        *dst = g;
+        gsum[t0 + e] = g;
       }
     }
     STAMP(1, (W.w & 7) == 0, W.g, it, 8);
