@@ -265,7 +265,9 @@ __device__ __forceinline__ void mma_chain(uint32_t d, Desc a, Desc b, uint32_t i
 
 // Store 8 consecutive edges e0.. of K-row r of a B operand (hi image, and
 // the lo image K*KSTR/8 bytes further when LO), values times `scale`.
-template <bool LO, uint32_t KS = KSTR>
+// PK: the lo residual of a pair in one packed FADD (the WS kernels; the
+// older kernels keep the scalar form, whose register allocation it upsets).
+template <bool LO, uint32_t KS = KSTR, bool PK = false>
 __device__ __forceinline__ void put8(uint8_t *act, int K, int r, int e0, const float *v,
                                      float scale) {
   const uint32_t off = (uint32_t)(r >> 3) * KS + (uint32_t)(e0 >> 3) * 128u + (uint32_t)(r & 7) * 16u;
@@ -274,7 +276,10 @@ __device__ __forceinline__ void put8(uint8_t *act, int K, int r, int e0, const f
   for (int i = 0; i < 4; ++i) {
     const float a = v[2 * i] * scale, b = v[2 * i + 1] * scale;
     hi[i] = __floats2half2_rn(a, b);
-    if (LO) {
+    if (LO && PK) {  // x - hi is exact: same bits as the scalar form
+      const float2 l = fma2(__half22float2(hi[i]), f2(-1.f), make_float2(a, b));
+      lo[i] = __floats2half2_rn(l.x, l.y);
+    } else if (LO) {
       const float2 hf = __half22float2(hi[i]);
       lo[i] = __floats2half2_rn(a - hf.x, b - hf.y);
     }
@@ -541,7 +546,7 @@ struct MetaRegs {
 // forward basis is scaled 2^14 and split; the W16 forward basis is rounded
 // to fp16 unscaled (quantize.py:68-71); db is always split (fp32 backward).
 // Padding edges carry C = C' = 0, so their columns are zero without a mask.
-template <bool DERIV, bool Q, uint32_t KS = KSTR>
+template <bool DERIV, bool Q, uint32_t KS = KSTR, bool PK = false>
 __device__ __forceinline__ void tile_basis(const EdgeArgs &a, const Wctx &W, const WarpMeta *m,
                                            float log2_scale) {
   const int k = 16 * W.q + (W.lane & 15), e0 = (W.lane >> 4) * 16;  // edges within the tile
@@ -571,8 +576,8 @@ __device__ __forceinline__ void tile_basis(const EdgeArgs &a, const Wctx &W, con
     }
   }
   constexpr bool LO = DERIV || !Q;
-  put8<LO, KS>(W.bb, DR, k, W.eo + e0, &v[0], 1.f);
-  put8<LO, KS>(W.bb, DR, k, W.eo + e0 + 8, &v[8], 1.f);
+  put8<LO, KS, PK>(W.bb, DR, k, W.eo + e0, &v[0], 1.f);
+  put8<LO, KS, PK>(W.bb, DR, k, W.eo + e0 + 8, &v[8], 1.f);
 }
 
 // h = ssp(z0) for this thread's channel over the tile (z0 = TMEM S0 scaled),
@@ -586,7 +591,7 @@ struct HScale {
       : rs(rs0 * hs), b(b0c * hs), c_ln2(kLn2 * hs), c_e(-kLog2e / hs) {}
 };
 
-template <bool Q, uint32_t KS = KSTR>
+template <bool Q, uint32_t KS = KSTR, bool PK = false>
 __device__ __forceinline__ void tile_h(const Wctx &W, float rs0, float b0c, const HScale &hk) {
   float v[TT];
   tc::tmem_ld32w(W.tl + S0, v);
@@ -601,7 +606,7 @@ __device__ __forceinline__ void tile_h(const Wctx &W, float rs0, float b0c, cons
     v[i + 1] = h.y;
   }
 #pragma unroll
-  for (int j = 0; j < TT / 8; ++j) put8<!Q, KS>(W.hb, D, W.ch, W.eo + 8 * j, &v[8 * j], 1.f);
+  for (int j = 0; j < TT / 8; ++j) put8<!Q, KS, PK>(W.hb, D, W.ch, W.eo + 8 * j, &v[8 * j], 1.f);
 }
 
 // Sum of p over the 32 lanes of the warp for every edge: a butterfly
@@ -1270,7 +1275,7 @@ k_edge_fwd_ws(const EdgeArgs a, const float4 *geo, const float2 *env,
       STAMP(0, (W.w & 7) == 0, W.g, it, 0);
       W.wait(BAR_G1, it);
       STAMP(0, (W.w & 7) == 0, W.g, it, 1);
-      tile_h<Q, KSTR64>(W, rs0, b0c, hk);
+      tile_h<Q, KSTR64, true>(W, rs0, b0c, hk);
       STAMP(0, (W.w & 7) == 0, W.g, it, 2);
       ws_ready(&ws->ready[W.g][BAR_G2]);
       STAMP(0, (W.w & 7) == 0, W.g, it, 3);
@@ -1281,7 +1286,7 @@ k_edge_fwd_ws(const EdgeArgs a, const float4 *geo, const float2 *env,
       }
     }
     if (more) {  // basis + G1 of the next tile overlap G2
-      tile_basis<false, Q, KSTR64>(a, W, W.meta(it + 1), bsc);
+      tile_basis<false, Q, KSTR64, true>(a, W, W.meta(it + 1), bsc);
       ws_ready(&ws->ready[W.g][BAR_G1]);
     }
     STAMP(0, (W.w & 7) == 0, W.g, it, 4);
@@ -1685,13 +1690,13 @@ __device__ __forceinline__ void mma_pair_ts(uint32_t d, uint32_t a_hi, uint32_t 
 }
 
 // Basis [b | db] of one tile from a unit buffer into the group's K=64 operand.
-template <bool Q, int UPG>
+template <bool Q, int UPG, bool PK = false>
 __device__ __forceinline__ void tile_basis_pair(const EdgeArgs &a, Wctx &W, const UnitMeta *m,
                                                 float bsc, float dbsc) {
   using C = FmCfg<UPG>;
-  tile_basis<false, Q, C::KS>(a, W, (const WarpMeta *)m, bsc);
+  tile_basis<false, Q, C::KS, PK>(a, W, (const WarpMeta *)m, bsc);
   W.eo += C::RH;
-  tile_basis<true, Q, C::KS>(a, W, (const WarpMeta *)m, dbsc);
+  tile_basis<true, Q, C::KS, PK>(a, W, (const WarpMeta *)m, dbsc);
   W.eo -= C::RH;
 }
 
