@@ -16,7 +16,7 @@ done
 timeout 900 ncu --set full --clock-control none -k "regex:k_scan_rows|k_nbr_assemble|k_noise_baoa_ring|k_forces_finish|k_node_post_pre_tc|k_node_post_readout_tc|k_node_prebwd_postbwd_tc" -s 20 -c 12 \
   -o gpurun_out/prof_${TAG}_small $B > gpurun_out/ncu_full_${TAG}_small.log 2>&1
 echo "full small exit $?" >> gpurun_out/ncu_full_${TAG}_small.log
-for T in memcheck racecheck synccheck; do
+[ -n "$SKIP_SANITIZER" ] || for T in memcheck racecheck synccheck; do
   timeout 900 compute-sanitizer --tool $T --print-limit 50 python __graft_entry__.py smoke > gpurun_out/sanitizer_${T}.log 2>&1
   echo "sanitizer $T exit $?" >> gpurun_out/sanitizer_${T}.log
 done
