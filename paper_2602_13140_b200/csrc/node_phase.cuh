@@ -38,14 +38,15 @@ constexpr uint32_t NSM_WA = 0, NSM_WB = 65536;  // weight image slots (hi|lo, <=
 struct NodeMeta {
   unsigned int amax[4];
   uint64_t bar;   // MMA completion
-  uint64_t wbar;  // weight images landed (bulk copy)
+  uint64_t wbar[2];  // weight slot A / B landed (bulk copy), one barrier per slot
   uint32_t tmem;
 };
 
 struct NodeCtx {
   int warp, lane, quarter, part, ch, ec;
   uint32_t tm, tl, sbase;   // TMEM base, this warp's lane quarter, weight slots' smem base
-  uint32_t phase, wphase;   // MMA and weight-barrier phases
+  uint32_t phase;           // MMA barrier phase
+  uint32_t wph[2];          // weight-slot barrier phases
   int sync_id, sync_n;      // named barrier of the participating threads
   uint8_t *act;             // B operand (K = 128 x NN, hi | lo)
   NodeMeta *meta;
@@ -68,7 +69,7 @@ __device__ __forceinline__ NodeCtx node_ctx(uint8_t *sm_w, uint8_t *act, NodeMet
   c.tl = tmem + ((uint32_t)(32 * c.quarter) << 16);
   c.sbase = tc::smem_u32(sm_w);
   c.phase = 0;
-  c.wphase = 0;
+  c.wph[0] = c.wph[1] = 0;
   c.sync_id = sync_id;
   c.sync_n = sync_n;
   c.act = act;
@@ -186,7 +187,8 @@ __device__ __forceinline__ void node_issue(const NodeCtx &c, uint32_t d, uint32_
   tc::fence_before_sync();
   nsync(c);
   if (threadIdx.x == 0) {
-    tc::mbar_wait(&c.meta->wbar, c.wphase);
+    const int ws = w_slot == NSM_WA ? 0 : 1;  // a GEMM waits for its own slot only
+    tc::mbar_wait(&c.meta->wbar[ws], c.wph[ws]);
     tc::fence_after_sync();
     issue_gemm(d, c.sbase + w_slot, w_lo_off, in_dim, w_mn, tc::smem_u32(c.act), K, idesc, nprod,
                KSTR);
@@ -211,22 +213,27 @@ __host__ __device__ inline ReadoutW readout_view(const fcg_model &m) {
   return ReadoutW{m.format, m.r0_img, m.r0_exp, m.r0_s, m.r0_b, m.r1_w, m.r1_b};
 }
 
-// Stage weight images into the slots (thread 0; barrier phase c.wphase).
+// Stage weight images into the slots (thread 0; one barrier per slot).
 __device__ __forceinline__ void node_stage_weights(const NodeCtx &c, const uint16_t *img_a,
                                                    uint32_t bytes_a, const uint16_t *img_b,
                                                    uint32_t bytes_b) {
   if (threadIdx.x == 0) {
     uint8_t *base = (uint8_t *)__cvta_shared_to_generic(c.sbase);
-    tc::mbar_expect_tx(&c.meta->wbar, bytes_a + bytes_b);
-    tc::bulk_g2s(base + NSM_WA, img_a, bytes_a, &c.meta->wbar);
-    if (img_b) tc::bulk_g2s(base + NSM_WB, img_b, bytes_b, &c.meta->wbar);
+    tc::mbar_expect_tx(&c.meta->wbar[0], bytes_a);
+    tc::bulk_g2s(base + NSM_WA, img_a, bytes_a, &c.meta->wbar[0]);
+    if (img_b) {
+      tc::mbar_expect_tx(&c.meta->wbar[1], bytes_b);
+      tc::bulk_g2s(base + NSM_WB, img_b, bytes_b, &c.meta->wbar[1]);
+    }
   }
 }
 
 // A weight slot reloaded once the GEMM reading it has completed, so that a
 // chain of stages in one kernel (the fused node launches of node_tc.cu) has
 // its next image in place by the time it needs it.  The copy completes the
-// next phase of the weight barrier; every later node_issue waits for it.
+// next phase of that slot's barrier, which the slot's next GEMM waits for
+// (a GEMM on the other slot does not).  The slot must have been staged by
+// the prologue: its phase 0 is that first image.
 struct Restage {
   uint32_t slot;
   const uint16_t *img;
@@ -234,12 +241,13 @@ struct Restage {
 };
 __device__ __forceinline__ void node_restage(NodeCtx &c, const Restage *r) {
   if (!r) return;
+  const int ws = r->slot == NSM_WA ? 0 : 1;
   if (threadIdx.x == 0) {  // thread 0 has seen the GEMM's completion barrier
     uint8_t *base = (uint8_t *)__cvta_shared_to_generic(c.sbase);
-    tc::mbar_expect_tx(&c.meta->wbar, r->bytes);
-    tc::bulk_g2s(base + r->slot, r->img, r->bytes, &c.meta->wbar);
+    tc::mbar_expect_tx(&c.meta->wbar[ws], r->bytes);
+    tc::bulk_g2s(base + r->slot, r->img, r->bytes, &c.meta->wbar[ws]);
   }
-  c.wphase ^= 1u;
+  c.wph[ws] ^= 1u;
 }
 
 // ---------------------------------------------------------------------------

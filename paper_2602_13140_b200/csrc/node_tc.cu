@@ -1,6 +1,5 @@
-// Standalone atom-wise MLP kernels (one chunk of node rows per CTA) over
-// the stages of node_phase.cuh; the fused edge kernels run the same stages
-// in their tails (edge_tc.cu).
+// Atom-wise MLP kernels (one chunk of node rows per CTA) over the stages of
+// node_phase.cuh: one stage per launch, or consecutive stages fused.
 #include "node_phase.cuh"
 
 namespace fcg {
@@ -67,7 +66,8 @@ __device__ __forceinline__ NodeCtx node_prologue(uint8_t *sm, const uint16_t *im
   NodeMeta *meta = (NodeMeta *)(sm + Cfg::META);
   if (threadIdx.x == 0) {
     tc::mbar_init(&meta->bar, 1);
-    tc::mbar_init(&meta->wbar, 1);
+    tc::mbar_init(&meta->wbar[0], 1);
+    tc::mbar_init(&meta->wbar[1], 1);
     tc::fence_mbar_init();
   }
   if (threadIdx.x < 4) meta->amax[threadIdx.x] = 0u;

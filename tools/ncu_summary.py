@@ -124,6 +124,8 @@ def main(tag, config="coil269_rc1.5_fp32_R64"):
                     vals.append(f"{v:.1f}")
             lines.append(f"| {d['kernel']} | " + " | ".join(vals) + " |")
             name = d["kernel"].replace("k_", "", 1)
+            # the default edge kernels carry bench.py's profiler class names
+            name = {"edge_bwd_fmws": "edge_bwd", "edge_fwd_ws": "edge_fwd"}.get(name, name)
             for suf in ("_tc", "64"):  # bench.py's profiler classes drop the suffix
                 if name.endswith(suf):
                     name = name[:-len(suf)]
