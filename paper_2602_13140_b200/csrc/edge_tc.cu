@@ -2165,6 +2165,7 @@ k_edge_bwd_fmws(const EdgeArgs a, const float4 *geo, const float2 *env,
     float gh[TT];
     float pf = 0.f, pm = 0.f, pl = 0.f;  // P[src] of the first, middle and last row
     int o_f = -1, o_l = -1;
+    int ia = TT, ib = TT;  // tile edges [0, ia): first row, [ia, ib): middle, [ib, n_e): last
     bool rows3 = true;
     float4 ue = make_float4(0.f, 0.f, 0.f, 0.f);
     float3 acc = make_float3(0.f, 0.f, 0.f);  // the slot's grad from the later blocks
@@ -2175,6 +2176,10 @@ k_edge_bwd_fmws(const EdgeArgs a, const float4 *geo, const float2 *env,
       const unsigned other = __ballot_sync(0xffffffffu, lane < n_e && o != o_f && o != o_l);
       const int mid = other ? __shfl_sync(0xffffffffu, o, __ffs(other) - 1) : o_f;
       rows3 = __all_sync(0xffffffffu, lane >= n_e || o == o_f || o == o_l || o == mid);
+      if (!Q) {  // the rows are runs (CSR order): edge i's P[src] is a select on i
+        ia = __popc(__ballot_sync(0xffffffffu, lane < n_e && o == o_f));
+        ib = n_e - __popc(__ballot_sync(0xffffffffu, lane < n_e && o == o_l));
+      }
 #pragma unroll
       for (int i = 0; i < TT; ++i) gh[i] = ld_gather(GHch + ((uint32_t)M->nbr[i] << 7));
       pf = ld_gather(Pch + (uint32_t)o_f * D);  // scaled by ku where used
@@ -2232,7 +2237,26 @@ k_edge_bwd_fmws(const EdgeArgs a, const float4 *geo, const float2 *env,
       }
     }
     STAMP(1, (W.w & 7) == 0, W.g, it, 6);
-    if (rows3) {
+    if (!Q && rows3 && ia >= ib) {  // one or two rows (~60% of C2 tiles): a 2-way select
+      pf *= ku; pl *= ku;
+#pragma unroll
+      for (int i = 0; i < TT; i += 2) {
+        const float2 pp = make_float2(i < ia ? pf : pl, i + 1 < ia ? pf : pl);
+        const float2 r = mul2(mul2(make_float2(q[i], q[i + 1]), make_float2(gh[i], gh[i + 1])), pp);
+        q[i] = r.x;
+        q[i + 1] = r.y;
+      }
+    } else if (!Q && rows3) {
+      pf *= ku; pm *= ku; pl *= ku;
+#pragma unroll
+      for (int i = 0; i < TT; i += 2) {
+        const float2 pp = make_float2(i < ia ? pf : (i < ib ? pm : pl),
+                                      i + 1 < ia ? pf : (i + 1 < ib ? pm : pl));
+        const float2 r = mul2(mul2(make_float2(q[i], q[i + 1]), make_float2(gh[i], gh[i + 1])), pp);
+        q[i] = r.x;
+        q[i + 1] = r.y;
+      }
+    } else if (rows3) {  // W16: by row id (the index form costs that kernel a spill)
       pf *= ku; pm *= ku; pl *= ku;
 #pragma unroll
       for (int j = 0; j < TT; j += 4) {
