@@ -2182,6 +2182,11 @@ k_edge_bwd_fmws(const EdgeArgs a, const float4 *geo, const float2 *env,
       }
 #pragma unroll
       for (int i = 0; i < TT; ++i) gh[i] = ld_gather(GHch + ((uint32_t)M->nbr[i] << 7));
+      if (n_e < TT) {  // the unit's last tile (warp-uniform): padding edges carry
+                       // gH = 0, so their messages and q terms vanish unmasked
+#pragma unroll
+        for (int i = 0; i < TT; ++i) gh[i] = i < n_e ? gh[i] : 0.f;
+      }
       pf = ld_gather(Pch + (uint32_t)o_f * D);  // scaled by ku where used
       pm = ld_gather(Pch + (uint32_t)mid * D);
       pl = ld_gather(Pch + (uint32_t)o_l * D);
@@ -2229,8 +2234,8 @@ k_edge_bwd_fmws(const EdgeArgs a, const float4 *geo, const float2 *env,
           for (int i = 0; i < 16; i += 2) {
             const float2 m = mul2(make_float2(gh[h + i], gh[h + i + 1]),
                                   fma2(make_float2(v[i], v[i + 1]), f2(s1), f2(b1c)));
-            v[i] = h + i < n_e ? m.x : 0.f;
-            v[i + 1] = h + i + 1 < n_e ? m.y : 0.f;
+            v[i] = m.x;  // zero past n_e (gH = 0 there)
+            v[i + 1] = m.y;
           }
           seg.half(M->own, v, h, st);
         }
