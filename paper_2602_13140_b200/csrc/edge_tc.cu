@@ -2153,8 +2153,8 @@ k_edge_bwd_fmws(const EdgeArgs a, const float4 *geo, const float2 *env,
       }
 #pragma unroll
       for (int j = 0; j < 16; j += 8) {
-        put8<!Q, C::KS>(W.hb, D, ch, W.eo + c0 + j, &z[j], 1.f);
-        put8<true, C::KS>(W.hb, D, ch, C::RH + W.eo + c0 + j, &dz[j], 1.f);
+        put8<!Q, C::KS, !Q>(W.hb, D, ch, W.eo + c0 + j, &z[j], 1.f);
+        put8<true, C::KS, !Q>(W.hb, D, ch, C::RH + W.eo + c0 + j, &dz[j], 1.f);
       }
     }
     STAMP(1, (W.w & 7) == 0, W.g, it, 2);
