@@ -136,15 +136,25 @@ struct SegSum {
         for (int i = 0; i < 4; ++i) s[i] += s[i + 4];
         acc += (s[0] + s[2]) + (s[1] + s[3]);
       } else {
+        block8(own, &m[h], h, hb & 0xffu);
+        block8(own, &m[h + 8], h + 8, hb >> 8);
+      }
+    }
+  }
+  // Eight edges h0.. with row-start bits b8: a tree sum when no row starts
+  // among them (most 8-edge blocks at ~23 edges per row), else the walk.
+  __device__ __forceinline__ void block8(const int *own, const float *m, int h0, unsigned b8) {
+    if (b8 == 0u) {
+      acc += ((m[0] + m[4]) + (m[2] + m[6])) + ((m[1] + m[5]) + (m[3] + m[7]));
+    } else {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          if ((hb >> i) & 1u) {  // edge h+i starts a row (warp-uniform)
-            if (row >= 0) outc[(uint32_t)row * D] = acc;
-            row = own[h + i];
-            acc = 0.f;
-          }
-          acc += m[h + i];
+      for (int i = 0; i < 8; ++i) {
+        if ((b8 >> i) & 1u) {  // edge h0+i starts a row (warp-uniform)
+          if (row >= 0) outc[(uint32_t)row * D] = acc;
+          row = own[h0 + i];
+          acc = 0.f;
         }
+        acc += m[i];
       }
     }
   }
@@ -174,15 +184,8 @@ struct SegSum {
       for (int i = 0; i < 4; ++i) s[i] += s[i + 4];
       acc += (s[0] + s[2]) + (s[1] + s[3]);
     } else {
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        if ((hb >> i) & 1u) {
-          if (row >= 0) outc[(uint32_t)row * D] = acc;
-          row = own[h + i];
-          acc = 0.f;
-        }
-        acc += m[i];
-      }
+      block8(own, &m[0], h, hb & 0xffu);
+      block8(own, &m[8], h + 8, hb >> 8);
     }
   }
   __device__ __forceinline__ void finish() {
