@@ -35,6 +35,23 @@ constexpr uint32_t IMG64 = 64 * 128 * 2;
 constexpr uint32_t NTM_D0 = 0, NTM_D1 = 128;
 constexpr uint32_t NSM_WA = 0, NSM_WB = 65536;  // weight image slots (hi|lo, <= 64 KB each)
 
+// Diagnostic phase stamps (tools/diag_node_phase.py, -DFCG_NODE_STAMPS): with
+// fcg_debug_phase_buffer set, thread 0 of every CTA records clock64() at
+// phase `ph` of launch kind `kind` (the last launch of a kind wins) and
+// %globaltimer at slots 6 and 7.
+__device__ unsigned long long *d_node_dbg = nullptr;
+__device__ __forceinline__ void node_stamp(int kind, int ph) {
+#ifdef FCG_NODE_STAMPS  // diagnostic builds only: reads d_node_dbg before the PDL wait
+  unsigned long long *b = d_node_dbg;
+  if (b && threadIdx.x == 0) {
+    unsigned long long t;
+    if (ph >= 6) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    else t = clock64();
+    b[4096 + ((size_t)kind * 1024 + blockIdx.x) * 8 + ph] = t;
+  }
+#endif
+}
+
 struct NodeMeta {
   unsigned int amax[4];
   uint64_t bar;   // MMA completion
@@ -259,7 +276,7 @@ __device__ __forceinline__ void stage_linear(NodeCtx &c, const float *X, int wex
                                              const float *bias, const float *rowscale, int quant,
                                              float *Y, int node0, int rlim,
                                              unsigned int *amax_out, const int32_t *csr_ptr,
-                                             const Restage *after = nullptr) {
+                                             const Restage *after = nullptr, int stk = -1) {
   const size_t r0 = (size_t)(node0 + c.ec) * D + c.ch;  // this thread: rows r0 + i*D
   float *Yr = opaque_ptr(Y + r0);
   const bool fwd = kMode == 0;
@@ -267,6 +284,7 @@ __device__ __forceinline__ void stage_linear(NodeCtx &c, const float *X, int wex
   const float fold = (!fwd && quant) ? ld_dep(&rowscale[c.ch]) : 1.f;
   const int s = rows_to_act<KSTR>(X, node0, rlim, c, fold, fwd && quant, &c.meta->amax[0],
                                   csr_ptr);
+  if (stk >= 0) node_stamp(stk, 1);
   node_issue<KSTR>(c, c.tm + NTM_D0, NSM_WA, IMG128, D, !fwd, D,
                    tc::idesc_f16(128, NN, fwd ? 0 : 1, 1), quant ? (fwd ? 1 : 2) : 3);
   // the accumulated operand (backward) is fetched while the GEMM runs
@@ -278,6 +296,7 @@ __device__ __forceinline__ void stage_linear(NodeCtx &c, const float *X, int wex
   }
   node_wait(c);
   node_restage(c, after);
+  if (stk >= 0) node_stamp(stk, 2);
   const float un = pow2f(-((quant ? 0 : wexp) + s)) * ((fwd && quant) ? ld_dep(&rowscale[c.ch]) : 1.f);
   const float b = fwd ? ld_dep(&bias[c.ch]) : 0.f;
   float mx = 0.f;
@@ -306,15 +325,17 @@ __device__ __forceinline__ void stage_post(NodeCtx &c, const float *H, const fcg
                                            int quant, float *Zp, float *X, int node0, int rlim,
                                            const int32_t *csr_ptr,
                                            const Restage *after1 = nullptr,
-                                           const Restage *after2 = nullptr) {
+                                           const Restage *after2 = nullptr, int stk = -1) {
   const size_t r0 = (size_t)(node0 + c.ec) * D + c.ch;  // this thread: rows r0 + i*D
   float *Zpr = opaque_ptr(Zp + r0), *Xr = opaque_ptr(X + r0);
   const int np = quant ? 1 : 3;
   const uint32_t idesc = tc::idesc_f16(128, NN, 0, 1);
   const int s0 = rows_to_act<KSTR>(H, node0, rlim, c, 1.f, quant, &c.meta->amax[0], csr_ptr);
+  if (stk >= 0) node_stamp(stk, 2);
   node_issue<KSTR>(c, c.tm + NTM_D0, NSM_WA, IMG128, D, false, D, idesc, np);
   node_wait(c);
   node_restage(c, after1);
+  if (stk >= 0) node_stamp(stk, 3);
   const float un0 = quant ? ld_dep(&blk.p0_s[c.ch]) : pow2f(-(blk.p0_exp + s0));
   const float b0 = ld_dep(&blk.p0_b[c.ch]);
   float mx = 0.f;
@@ -338,6 +359,7 @@ __device__ __forceinline__ void stage_post(NodeCtx &c, const float *H, const fcg
   int s1 = 0;
   if (!quant) s1 = scale_exp(node_amax(mx, &c.meta->amax[1], c));
   tmem_rows_to_act<KSTR>(c.tl + NTM_D0, c.act, D, c.ch, c.ec, pow2f(s1), !quant);
+  if (stk >= 0) node_stamp(stk, 4);
   node_issue<KSTR>(c, c.tm + NTM_D1, NSM_WB, IMG128, D, false, D, idesc, np);
   // the residual stream is fetched while the GEMM runs
   float xv[NPT];
@@ -348,6 +370,7 @@ __device__ __forceinline__ void stage_post(NodeCtx &c, const float *H, const fcg
   }
   node_wait(c);
   node_restage(c, after2);
+  if (stk >= 0) node_stamp(stk, 5);
   const float un1 = quant ? ld_dep(&blk.p1_s[c.ch]) : pow2f(-(blk.p1_exp + s1));
   const float b1 = ld_dep(&blk.p1_b[c.ch]);
 #pragma unroll

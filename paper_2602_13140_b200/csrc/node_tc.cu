@@ -35,18 +35,6 @@ using CfgPost = NodeCfg<128, 2>;
 // fcg_debug_phase_buffer set, thread 0 of every CTA records clock64() at
 // phase `ph` of launch kind `kind` (the last launch of a kind wins) and
 // %globaltimer at entry (slot 6) and exit (slot 7).
-__device__ unsigned long long *d_node_dbg = nullptr;
-__device__ __forceinline__ void node_stamp(int kind, int ph) {
-#ifdef FCG_NODE_STAMPS  // diagnostic builds only: reads d_node_dbg before the PDL wait
-  unsigned long long *b = d_node_dbg;
-  if (b && threadIdx.x == 0) {
-    unsigned long long t;
-    if (ph >= 6) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    else t = clock64();
-    b[4096 + ((size_t)kind * 1024 + blockIdx.x) * 8 + ph] = t;
-  }
-#endif
-}
 static void node_dbg_sync() {
   static unsigned long long *cur = nullptr;
   if (g_dbg_phase != cur) {
@@ -179,14 +167,22 @@ k_node_post_pre_tc(const float *H, const fcg_block blk, const fcg_block nxt, int
                    unsigned int *amax_p) {
   using Cfg = CfgPost;
   extern __shared__ __align__(1024) uint8_t sm[];
+  node_stamp(2, 0);
   NodeCtx c = node_prologue<Cfg>(sm, blk.p0_img, 2 * IMG128, blk.p1_img, 2 * IMG128);
   const int node0 = blockIdx.x * Cfg::NN;
   const Restage pre{NSM_WA, nxt.pre_img, 2 * IMG128};
-  stage_post<Cfg::KSTR, Cfg::NN>(c, H, blk, quant, Zp, X, node0, nrows, csr_ptr, &pre);
+  node_stamp(2, 6);
+  node_stamp(2, 1);
+  stage_post<Cfg::KSTR, Cfg::NN>(c, H, blk, quant, Zp, X, node0, nrows, csr_ptr, &pre, nullptr, 2);
+  node_stamp(2, 7);
   node_chunk_reset(c);
+  node_stamp(0, 6);
+  node_stamp(0, 0);
   stage_linear<0, Cfg::KSTR, Cfg::NN>(c, X, nxt.pre_exp, nxt.pre_b, nxt.pre_s, quant, Pn, node0,
-                                      nrows, amax_p, nullptr);
+                                      nrows, amax_p, nullptr, nullptr, 0);
+  node_stamp(0, 3);
   node_epilogue_end(c);
+  node_stamp(0, 7);
 }
 
 // post(T-1) + readout + post_bwd(T-1): the last block's forward tail and
@@ -273,6 +269,7 @@ void launch_node_post_bwd_tc(const float *G, const fcg_block &b, int quant, cons
 void launch_node_post_pre_tc(const float *H, const fcg_block &b, const fcg_block &nxt, int quant,
                              float *Zp, float *X, float *Pn, int nrows, const int32_t *csr_ptr,
                              unsigned int *amax_p, cudaStream_t s) {
+  node_dbg_sync();
   launch_pdl(PDL_NODE_POST, k_node_post_pre_tc, node_grid<CfgPost>(nrows), CfgPost::NTH,
              CfgPost::SMEM, s, H, b, nxt, quant, Zp, X, Pn, nrows, csr_ptr, amax_p);
 }

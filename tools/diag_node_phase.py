@@ -27,6 +27,8 @@ eng.evaluate()
 b = buf[4096:].cpu().numpy().reshape(5, 1024, 8)
 names = {0: ("pre", [1, 2, 3, 4]), 1: ("pre_bwd", [1, 2, 3, 4]), 2: ("post", [1, 2, 3, 4, 5]),
          3: ("post_bwd", [1, 2, 3, 5]), 4: ("readout", [1, 2, 3, 5])}
+if os.environ.get("FCG_NODE_FUSE", "1") != "0":  # k_node_post_pre_tc: post part (kind 2), pre part (kind 0)
+    names = {2: ("post_pre:post", [1, 2, 3, 4, 5]), 0: ("post_pre:pre", [1, 2, 3])}
 for k, (name, phs) in names.items():
     t = b[k]
     ok = t[:, 6] > 0
