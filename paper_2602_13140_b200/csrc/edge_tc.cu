@@ -2143,8 +2143,9 @@ k_edge_bwd_fmws(const EdgeArgs a, const float4 *geo, const float2 *env,
       for (int i = 0; i < 16; i += Q ? 1 : 2) {
         if (Q) {  // scalar: pairing the W16 loop costs that kernel a spill
           const float zz = z[i] * rs0 + b0c;
-          dz[i] *= sigmoid_fast(zz) * kv;  // kv * ssp'(z0)
           z[i] = ssp_fast(zz);  // rounded to fp16 by put8's hi-only pack (quantize.py:80-88)
+          // kv * ssp'(z0) = kv (1 - e^-ssp(z0) / 2) from the unrounded ssp, as the fp32 path
+          dz[i] *= fmaf(-0.5f * kv, ex2_ftz(z[i] * -kLog2e), kv);
         } else {  // a pair of edges per instruction
           const float2 h = ssp_scaled2(fma2(make_float2(z[i], z[i + 1]), f2(hk.rs), f2(hk.b)),
                                        hk.c_ln2, hk.c_e);                       // hs * h
