@@ -2180,7 +2180,7 @@ k_edge_bwd_fmws(const EdgeArgs a, const float4 *geo, const float2 *env,
       const unsigned other = __ballot_sync(0xffffffffu, lane < n_e && o != o_f && o != o_l);
       const int mid = other ? __shfl_sync(0xffffffffu, o, __ffs(other) - 1) : o_f;
       rows3 = __all_sync(0xffffffffu, lane >= n_e || o == o_f || o == o_l || o == mid);
-      if (!Q) {  // the rows are runs (CSR order): edge i's P[src] is a select on i
+      {  // the rows are runs (CSR order): edge i's P[src] is a select on i
         ia = __popc(__ballot_sync(0xffffffffu, lane < n_e && o == o_f));
         ib = n_e - __popc(__ballot_sync(0xffffffffu, lane < n_e && o == o_l));
       }
@@ -2246,7 +2246,7 @@ k_edge_bwd_fmws(const EdgeArgs a, const float4 *geo, const float2 *env,
       }
     }
     STAMP(1, (W.w & 7) == 0, W.g, it, 6);
-    if (!Q && rows3 && ia >= ib) {  // one or two rows (~60% of C2 tiles): a 2-way select
+    if (rows3 && ia >= ib) {  // one or two rows (~60% of C2 tiles): a 2-way select
       pf *= ku; pl *= ku;
 #pragma unroll
       for (int i = 0; i < TT; i += 2) {
@@ -2255,7 +2255,7 @@ k_edge_bwd_fmws(const EdgeArgs a, const float4 *geo, const float2 *env,
         q[i] = r.x;
         q[i + 1] = r.y;
       }
-    } else if (!Q && rows3) {
+    } else if (rows3 && !Q) {
       pf *= ku; pm *= ku; pl *= ku;
 #pragma unroll
       for (int i = 0; i < TT; i += 2) {
