@@ -2130,6 +2130,8 @@ k_edge_bwd_fmws(const EdgeArgs a, const float4 *geo, const float2 *env,
     const float rs0 = Q ? ld_dep(&B.f0_s[ch]) : pow2f(-(B.f0_exp + 14));
     const float kv = Q ? rs0 * pow2f(B.f_vexp - B.f_dbexp)
                        : pow2f(B.f_vexp - B.f0_exp - B.f_dbexp);
+    const float e1rs = Q ? rs0 : hk.rs, e1b = Q ? b0c : hk.b;
+    const float e1cl = Q ? kLn2 : hk.c_ln2, e1ce = Q ? -kLog2e : hk.c_e;
     STAMP(1, (W.w & 7) == 0, W.g, it, 0);
     tc::mbar_wait(&sh->bar[W.g][BAR_G1], (uint32_t)(it & 1));
     tc::fence_after_sync();
@@ -2140,20 +2142,16 @@ k_edge_bwd_fmws(const EdgeArgs a, const float4 *geo, const float2 *env,
       tc::tmem_ld16w(W.tl + c0, z);
       tc::tmem_ld16w(W.tl + C::RH + c0, dz);
 #pragma unroll
-      for (int i = 0; i < 16; i += Q ? 1 : 2) {
-        if (Q) {  // scalar: pairing the W16 loop costs that kernel a spill
-          const float zz = z[i] * rs0 + b0c;
-          z[i] = ssp_fast(zz);  // rounded to fp16 by put8's hi-only pack (quantize.py:80-88)
-          // kv * ssp'(z0) = kv (1 - e^-ssp(z0) / 2) from the unrounded ssp, as the fp32 path
-          dz[i] *= fmaf(-0.5f * kv, ex2_ftz(z[i] * -kLog2e), kv);
-        } else {  // a pair of edges per instruction
-          const float2 h = ssp_scaled2(fma2(make_float2(z[i], z[i + 1]), f2(hk.rs), f2(hk.b)),
-                                       hk.c_ln2, hk.c_e);                       // hs * h
-          const float2 sp = fma2(f2(-0.5f * kv), ex2_2(mul2(h, f2(hk.c_e))), f2(kv));  // kv ssp'
-          const float2 d = mul2(make_float2(dz[i], dz[i + 1]), sp);
-          z[i] = h.x; z[i + 1] = h.y;
-          dz[i] = d.x; dz[i + 1] = d.y;
-        }
+      for (int i = 0; i < 16; i += 2) {  // a pair of edges per instruction
+        // fp32: hs * h = hs * ssp(z0); W16: ssp(z0), rounded to fp16 by put8's
+        // hi-only pack (quantize.py:80-88).  kv * ssp'(z0) = kv (1 - e^-ssp / 2)
+        // from the unrounded value.
+        const float2 h = ssp_scaled2(fma2(make_float2(z[i], z[i + 1]), f2(e1rs), f2(e1b)),
+                                     e1cl, e1ce);
+        const float2 sp = fma2(f2(-0.5f * kv), ex2_2(mul2(h, f2(e1ce))), f2(kv));
+        const float2 d = mul2(make_float2(dz[i], dz[i + 1]), sp);
+        z[i] = h.x; z[i + 1] = h.y;
+        dz[i] = d.x; dz[i + 1] = d.y;
       }
 #pragma unroll
       for (int j = 0; j < 16; j += 8) {
