@@ -616,16 +616,20 @@ __device__ __forceinline__ void tile_h(const Wctx &W, float rs0, float b0c, cons
 // reduce-scatter leaves edge `lane`'s sum in lane `lane`.
 __device__ __forceinline__ float warp_edge_sum(float (&p)[TT], int lane) {
 #pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) {
+  for (int o = 16; o >= 2; o >>= 1) {  // the adds a pair per instruction (same sums)
     const bool upper = (lane & o) != 0;
 #pragma unroll
-    for (int i = 0; i < o; ++i) {
-      const float send = upper ? p[i] : p[i + o];
-      const float keep = upper ? p[i + o] : p[i];
-      p[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    for (int i = 0; i < o; i += 2) {
+      const float r0 = __shfl_xor_sync(0xffffffffu, upper ? p[i] : p[i + o], o);
+      const float r1 = __shfl_xor_sync(0xffffffffu, upper ? p[i + 1] : p[i + 1 + o], o);
+      const float2 s = add2(make_float2(upper ? p[i + o] : p[i], upper ? p[i + 1 + o] : p[i + 1]),
+                            make_float2(r0, r1));
+      p[i] = s.x;
+      p[i + 1] = s.y;
     }
   }
-  return p[0];
+  const bool upper = (lane & 1) != 0;
+  return (upper ? p[1] : p[0]) + __shfl_xor_sync(0xffffffffu, upper ? p[0] : p[1], 1);
 }
 
 // phase timestamps for diagnosis: CTA 0, warp 0, first 16 tiles
