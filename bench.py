@@ -19,10 +19,11 @@ Timing: W untimed warm-up steps, then K steps, each a replay of a captured
 one-step CUDA graph bracketed by CUDA events on the replay stream, with a
 256 MiB L2 flush (outside the events) before every step; barrier +
 synchronize around the timed region; max over ranks.  `e2e` repeats the
-step through the engine's public API with host buffers (H2D of
-positions+velocities from pinned memory, MDEngine.run(1) = one graph replay
-of fcg_md_step, D2H of the new state, per-replica energies and status
-words) timed by the host clock.  Multi-GPU: one process per GPU, replicas
+step through the engine's public host-buffer call MDEngine.step_host (H2D
+of positions+velocities from pinned memory, fcg_md_step, D2H of the new
+state, per-replica energies and status words — one graph launch whose
+copies are graph nodes), timed by the host clock around each call's
+synchronisation and status check.  Multi-GPU: one process per GPU, replicas
 sharded with no per-step collective; after the timed region one NCCL
 all_gather of the final positions, velocities and per-replica potential,
 prior and kinetic T.
@@ -416,16 +417,16 @@ def main():
     hst = torch.empty(_lib.FCG_STATUS_WORDS, dtype=torch.int64).pin_memory()
     hstate.copy_(eng.state)
     with torch.cuda.stream(stream):
+        # the public host-buffer stepping call: state in from pinned host
+        # memory, one MD step, state + energies + status back, as one graph
+        # launch (MDEngine.step_host); the first call captures it
+        eng.step_host(hstate, hen, hst)
+        MDEngine.check_status(hst.numpy())
         torch.cuda.synchronize(dev)
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            eng.state.copy_(hstate, non_blocking=True)
-            eng.run(1, graph_steps=1, check=False)  # the public stepping call (graph replay)
-            hstate.copy_(eng.state, non_blocking=True)
-            hen.copy_(eng.energies, non_blocking=True)
-            hst.copy_(eng.status, non_blocking=True)
-            stream.synchronize()
+            eng.step_host(hstate, hen, hst)
             MDEngine.check_status(hst.numpy())
         e2e_s = time.perf_counter() - t0
     e2e_value = ns_per_day(R * world * args.e2e_steps, max_over_ranks(e2e_s))

@@ -300,6 +300,12 @@ int fcg_md_step(const fcg_model *m, const fcg_prior *pr,
                 int32_t *ptr, int32_t *nbr, int32_t *rev, int32_t *own,
                 int64_t *status, void *ws, size_t ws_bytes, void *stream);
 
+/* Asynchronous copy of `bytes` between any two of host (pinned) and device
+ * memory on `stream` (cudaMemcpyDefault): the host I/O of an MD step in the
+ * same stream — and CUDA graph — as fcg_md_step, so a host-buffer step is
+ * one graph launch (paper_2602_13140_b200.MDEngine.step_host). */
+int fcg_memcpy_async(void *dst, const void *src, size_t bytes, void *stream);
+
 /* ---------------------------------------------------------------------
  * (f) output pipeline, md.py:224-228 / :312-326.  HOST pointers.
  * Formats R trajectory frames (replica indices replica0..replica0+R-1) of

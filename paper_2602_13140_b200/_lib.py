@@ -66,6 +66,7 @@ class FcgMdParams(C.Structure):
 _VP = C.c_void_p
 _SIGS = {
     "fcg_abi_version": (C.c_int, []),
+    "fcg_memcpy_async": (C.c_int, [_VP, _VP, C.c_size_t, _VP]),
     "fcg_last_error": (C.c_char_p, []),
     "fcg_profile_enable": (C.c_int, [C.c_int]),
     "fcg_debug_phase_buffer": (C.c_int, [_VP]),

@@ -228,4 +228,14 @@ int fcg_md_step(const fcg_model *m, const fcg_prior *pr, const fcg_md_params *p,
                        pr, prior, &defer);
 }
 
+int fcg_memcpy_async(void *dst, const void *src, size_t bytes, void *stream) {
+  if (bytes == 0) return FCG_OK;
+  if (!dst || !src) {
+    set_error("memcpy_async: null pointer");
+    return FCG_ERR_ARG;
+  }
+  cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, (cudaStream_t)stream);
+  return cuda_status("memcpy_async");
+}
+
 }  // extern "C"

@@ -254,6 +254,50 @@ class MDEngine:
             self._graphs[k] = g
         return g
 
+    def step_host(self, h_state, h_energies=None, h_status=None, n_steps: int = 1):
+        """n_steps MD steps from and to host memory as ONE graph launch: the
+        state [2, R, N, 3] (positions, velocities) is copied in from pinned
+        host memory, the steps run, and the new state, the per-replica
+        energies [2, R] (potential, prior) and the status words are copied
+        back — the copies are nodes of the same captured CUDA graph
+        (fcg_memcpy_async on the capture stream).  Host tensors must be
+        pinned and keep their addresses (the graph is cached per address).
+        Synchronises; the caller checks the copied status words
+        (check_status)."""
+        torch, L, v = self.torch, self.lib, _lib.vp
+        key = ("host", int(n_steps), h_state.data_ptr(),
+               h_energies.data_ptr() if h_energies is not None else 0,
+               h_status.data_ptr() if h_status is not None else 0)
+        g = self._graphs.get(key)
+        if g is None:
+            for t in (h_state, h_energies, h_status):
+                if t is not None and not t.is_pinned():
+                    raise ValueError("step_host needs pinned host tensors")
+            if tuple(h_state.shape) != tuple(self.state.shape) or h_state.dtype != self.state.dtype:
+                raise ValueError(f"h_state must be {tuple(self.state.shape)} float32")
+            s = torch.cuda.Stream(self.device)
+            g = torch.cuda.CUDAGraph()
+            nb = self.state.numel() * 4
+            with torch.cuda.graph(g, stream=s):
+                st = self.stream()
+                _lib.check(L.fcg_memcpy_async(v(self.state), C.c_void_p(h_state.data_ptr()), nb,
+                                              st), "fcg_memcpy_async")
+                for _ in range(int(n_steps)):
+                    self._md_step()
+                _lib.check(L.fcg_memcpy_async(C.c_void_p(h_state.data_ptr()), v(self.state), nb,
+                                              st), "fcg_memcpy_async")
+                if h_energies is not None:
+                    _lib.check(L.fcg_memcpy_async(C.c_void_p(h_energies.data_ptr()),
+                                                  v(self.energies), self.energies.numel() * 4,
+                                                  st), "fcg_memcpy_async")
+                if h_status is not None:
+                    _lib.check(L.fcg_memcpy_async(C.c_void_p(h_status.data_ptr()),
+                                                  v(self.status), self.status.numel() * 8, st),
+                               "fcg_memcpy_async")
+            self._graphs[key] = g
+        g.replay()
+        torch.cuda.current_stream(self.device).synchronize()
+
     # -- flags -----------------------------------------------------------
     def flags(self):
         st = self.status.cpu().numpy()

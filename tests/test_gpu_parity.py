@@ -426,6 +426,27 @@ def test_graph_replay_equals_eager_and_is_deterministic(golden):
         np.testing.assert_array_equal(x, y)
 
 
+def test_step_host_equals_device_steps(golden):
+    """MDEngine.step_host (host state in, one graph launch with its copies as
+    graph nodes, state + energies + status out) is bitwise the device-side
+    step; a second call continues from the state it returned."""
+    import torch
+    a, _, _ = _engine_for("traj_coil269", golden)
+    b, _, _ = _engine_for("traj_coil269", golden)
+    a.run(2)
+    hs = torch.empty(tuple(b.state.shape), dtype=torch.float32).pin_memory()
+    he = torch.empty(tuple(b.energies.shape), dtype=torch.float32).pin_memory()
+    hst = torch.empty(b.status.numel(), dtype=torch.int64).pin_memory()
+    hs.copy_(b.state)
+    b.step_host(hs, he, hst)
+    b.step_host(hs, he, hst)
+    np.testing.assert_array_equal(hs.numpy(), a.state.cpu().numpy())
+    np.testing.assert_array_equal(he.numpy(), a.energies.cpu().numpy())
+    np.testing.assert_array_equal(hst.numpy(), a.status.cpu().numpy())
+    with pytest.raises(ValueError):
+        b.step_host(torch.empty_like(hs, pin_memory=False))
+
+
 def test_replica_sharding_bit_identical(golden):
     full, _, _ = _engine_for("traj_tiny", golden, R=4)
     full.run(6)
